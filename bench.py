@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark: Q_p hex Laplace action GDoF/s (fp64) vs degree p on B200.
+
+BASELINE.json metric "Q_p hex Laplace action GDoF/s (fp64) vs degree p; % of
+roofline", config C2 (configs[1]): 2^18 jittered trilinear hex cells per GPU,
+(p+1)^3 dofs/cell, u ~ U[-1,1], GL (p+1)^3 quadrature, p = 1..8.
+
+A STEP is one application of the action at every degree p = 1..8 over the
+whole batch (8 sfk_eval launches, inputs resident in HBM).  value = total
+local DoFs processed by all ranks / max-over-ranks device time (GDoF/s).
+Weak scaling: each rank owns its own 2^18-cell slab of a (64*N, 64, 64)
+lattice (cell-range sharding, no data-path collective).
+
+Extra keys: per_degree (ms, GDoF/s, cells/s, roofline fraction for every p),
+roofline (dominant kernel, vs the FP64 peak measured live), cpu_baseline
+(the reference's own emitted C over all host cores, rank 0, N=1), e2e (the
+host-buffer C-ABI call sfk_eval_host: H2D + compute + D2H), clocks,
+gpu_launches.  `--impl reference` times the reference CPU path alone.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Q_p hex Laplace action GDoF/s (fp64) vs degree p; % of roofline"
+HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--degrees", default="1-8")
+    ap.add_argument("--lattice", default="64,64,64", help="cells per rank (nx,ny,nz)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-cells", type=int, default=1 << 15,
+                    help="cells per degree in the CPU baseline sample")
+    return ap.parse_args()
+
+
+def degrees_of(s):
+    if "-" in s:
+        a, b = s.split("-")
+        return list(range(int(a), int(b) + 1))
+    return [int(x) for x in s.split(",")]
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.15)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def reference_arm(args):
+    """The reference's own CPU path: its emitted C (oracle/_ref) with an
+    OpenMP cell loop over all host cores; the oracle port if _ref is absent."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import cpu, refc
+    from paper_1711_02473_b200 import compile_kernel, workloads
+
+    degs = degrees_of(args.degrees)
+    nx, ny, nz = (int(x) for x in args.lattice.split(","))
+    sample = min(args.cpu_cells, nx * ny * nz)
+    coords = workloads.lattice_coords(nx, ny, nz)[:sample]
+    plans = [compile_kernel("action_laplace", "hex", p) for p in degs]
+    kind = "reference" if all(refc.available(pl) for pl in plans) else "port"
+    ev = refc.evaluate if kind == "reference" else cpu.evaluate
+    inputs = [{"coords": coords, "w0": workloads.uniform_dofs(sample, (p + 1) ** 3)}
+              for p in degs]
+    for _ in range(args.warmup):
+        for pl, inp in zip(plans, inputs):
+            ev(pl, {"coords": inp["coords"][:256], "w0": inp["w0"][:256]})
+    per = {p: [] for p in degs}
+    for _ in range(args.steps):
+        for p, pl, inp in zip(degs, plans, inputs):
+            t0 = time.perf_counter()
+            ev(pl, inp)
+            per[p].append(time.perf_counter() - t0)
+    total_t = sum(min(v) for v in per.values())
+    dofs = sum(sample * (p + 1) ** 3 for p in degs)
+    value = dofs / total_t / 1e9
+    cores = (refc.threads(plans[0]) if kind == "reference" else cpu.num_threads())
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "GDoF/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_t * 1e3, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 hex Q_p Laplace action, GL (p+1)^3, p=%s" % args.degrees,
+                   "cells_per_degree": sample, "sample_of": nx * ny * nz},
+        "per_degree": [{"p": p, "ms": round(min(per[p]) * 1e3, 4),
+                        "gdofs": round(sample * (p + 1) ** 3 / min(per[p]) / 1e9, 6)}
+                       for p in degs],
+        "cpu_baseline": {"value": round(value, 6), "unit": "GDoF/s", "cores": cores,
+                         "kind": kind,
+                         "sample": "%d of %d cells per degree, p=%s, best of %d"
+                                   % (sample, nx * ny * nz, args.degrees, args.steps)},
+        "e2e": {"value": round(value, 6), "unit": "GDoF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_leg(degs, coords_all, host_inputs, sample_cells):
+    from oracle import cpu, refc
+    from paper_1711_02473_b200 import compile_kernel
+
+    plans = [compile_kernel("action_laplace", "hex", p) for p in degs]
+    kind = "reference" if all(refc.available(pl) for pl in plans) else "port"
+    ev = refc.evaluate if kind == "reference" else cpu.evaluate
+    n = min(sample_cells, coords_all.shape[0])
+    tot_t, tot_d = 0.0, 0
+    for p, pl in zip(degs, plans):
+        inp = {"coords": coords_all[:n], "w0": host_inputs[p][:n]}
+        ev(pl, {"coords": inp["coords"][:64], "w0": inp["w0"][:64]})
+        best = 1e30
+        for _ in range(2):
+            t0 = time.perf_counter()
+            ev(pl, inp)
+            best = min(best, time.perf_counter() - t0)
+        tot_t += best
+        tot_d += n * (p + 1) ** 3
+    cores = refc.threads(plans[0]) if kind == "reference" else cpu.num_threads()
+    return {"value": round(tot_d / tot_t / 1e9, 6), "unit": "GDoF/s", "cores": cores,
+            "kind": kind,
+            "sample": "first %d cells of the C2 batch per degree p=%d..%d, best of 2"
+                      % (n, degs[0], degs[-1])}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1711_02473_b200 import compile_kernel, runtime, workloads
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    degs = degrees_of(args.degrees)
+    nx, ny, nz = (int(x) for x in args.lattice.split(","))
+
+    # rank r owns the slab ix in [nx*r, nx*(r+1)) of a (nx*world, ny, nz) lattice
+    coords_np = workloads.lattice_coords(nx * world, ny, nz, ix_range=(nx * rank, nx * (rank + 1)))
+    ncells = coords_np.shape[0]
+    plans = {p: compile_kernel("action_laplace", "hex", p) for p in degs}
+    host_u = {p: workloads.uniform_dofs(ncells, (p + 1) ** 3, seed=workloads.SEED_U + rank)
+              for p in degs}
+    coords = torch.from_numpy(coords_np).to(dev)
+    u = {p: torch.from_numpy(host_u[p]).to(dev) for p in degs}
+    out = {p: torch.empty_like(u[p]) for p in degs}
+    stream = torch.cuda.current_stream(dev)
+    lib = runtime.load_library()
+    handles = {p: runtime.native_plan(plans[p]) for p in degs}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    # FP64 peak measured live on this GPU (DFMA chains and DMMA), seconds-long
+    dfma, dmma = runtime.fp64_peak(1.0)
+    p64 = max(dfma, dmma)
+
+    def launch(p):
+        runtime._check(lib.sfk_eval(handles[p], ncells, out[p].data_ptr(), coords.data_ptr(),
+                                    u[p].data_ptr(), None, stream.cuda_stream))
+
+    for _ in range(max(args.warmup, 3) if args.warmup > 0 else 0):
+        for p in degs:
+            launch(p)
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev = {p: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(K)] for p in degs}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = runtime.launch_count()
+    with ClockSampler(dev.index if world == 1 else local) as clk:
+        for k in range(K):
+            flush.zero_()  # L2 flush between steps (outside the timed events)
+            for p in degs:
+                e0, e1 = ev[p][k]
+                e0.record(stream)
+                launch(p)
+                e1.record(stream)
+        torch.cuda.synchronize()
+    gpu_launches = runtime.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    ms = {p: sorted(e0.elapsed_time(e1) for e0, e1 in ev[p]) for p in degs}
+    ms_mean = {p: sum(v) / len(v) for p, v in ms.items()}
+    step_ms = sum(ms_mean.values())
+    if world > 1:
+        t = torch.tensor([step_ms] + [ms_mean[p] for p in degs], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = t[0].item()
+        ms_mean = {p: t[1 + i].item() for i, p in enumerate(degs)}
+
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", HBM_FALLBACK)
+    total_dofs = world * sum(ncells * (p + 1) ** 3 for p in degs)
+    value = total_dofs / (step_ms * 1e-3) / 1e9
+    per = []
+    dom = None
+    for p in degs:
+        pl = plans[p]
+        t = ms_mean[p] * 1e-3
+        F = pl.algorithmic_flops
+        Bb = pl.compulsory_bytes
+        t_roof = ncells * max(Bb / (hbm * 1e9), F / (p64 * 1e12))
+        rec = {"p": p, "ms": round(ms_mean[p], 5), "gdofs": round(ncells * (p + 1) ** 3 / t / 1e9, 3),
+               "cells_per_s": round(ncells / t, 1),
+               "fp64_tflops_alg": round(ncells * F / t / 1e12, 3),
+               "hbm_gbs": round(ncells * Bb / t / 1e9, 1),
+               "roofline_frac": round(t_roof / t, 4),
+               "bound": "fp64" if F / (p64 * 1e12) > Bb / (hbm * 1e9) else "hbm"}
+        per.append(rec)
+        if dom is None or ms_mean[p] > ms_mean[dom["p"]]:
+            dom = rec
+    domplan = plans[dom["p"]]
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get("C2_p%d" % dom["p"])
+        except ValueError:
+            traffic = None
+    roofline = {"bound": dom["bound"],
+                "achieved": dom["fp64_tflops_alg"] if dom["bound"] == "fp64" else dom["hbm_gbs"],
+                "peak": round(p64, 3) if dom["bound"] == "fp64" else hbm,
+                "unit": "TFLOP/s" if dom["bound"] == "fp64" else "GB/s",
+                "frac": None, "traffic": traffic,
+                "kernel": "hex_laplace_action_kernel p=%d" % dom["p"],
+                "flops_per_cell": domplan.algorithmic_flops,
+                "bytes_per_cell": domplan.compulsory_bytes,
+                "peak_source": "measured live: max(DFMA %.2f, DMMA %.2f) TFLOP/s; HBM %s GB/s"
+                               % (dfma, dmma, hbm)}
+    roofline["frac"] = round(roofline["achieved"] / roofline["peak"], 4)
+
+    line = {"metric": METRIC, "value": round(value, 4), "unit": "GDoF/s", "n_gpus": world,
+            "steps": K, "warmup": args.warmup, "ms_per_step": round(step_ms, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded jittered lattice, u~U[-1,1])",
+            "config": {"workload": "C2 hex Q_p Laplace action, GL (p+1)^3, p=%s" % args.degrees,
+                       "cells_per_gpu": ncells, "lattice_per_gpu": [nx, ny, nz],
+                       "parallelism": "cell-range shards x%d" % world,
+                       "l2": "flushed between steps (256 MiB write)"},
+            "per_degree": per, "roofline": roofline, "gpu_launches": int(gpu_launches),
+            "clocks": clk.summary()}
+
+    # ---- e2e: host buffers through the C-ABI (H2D + compute + D2H) ----------
+    if not args.no_e2e:
+        pinned = {}
+        for p in degs:
+            pinned[p] = (torch.from_numpy(host_u[p]).pin_memory(),
+                         torch.empty((ncells, (p + 1) ** 3), dtype=torch.float64).pin_memory())
+        pc = torch.from_numpy(coords_np).pin_memory()
+        for p in degs:  # warm-up
+            runtime.evaluate_host_ptrs(plans[p], min(ncells, 4096), pinned[p][1].data_ptr(),
+                                       pc.data_ptr(), pinned[p][0].data_ptr(), None)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(K):
+            for p in degs:
+                runtime.evaluate_host_ptrs(plans[p], ncells, pinned[p][1].data_ptr(),
+                                           pc.data_ptr(), pinned[p][0].data_ptr(), None)
+        e2e_s = (time.perf_counter() - t0) / K
+        if world > 1:
+            tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = tt.item()
+        h2d = sum(ncells * (24 + (p + 1) ** 3) * 8 for p in degs)
+        d2h = sum(ncells * (p + 1) ** 3 * 8 for p in degs)
+        ok = all(np.array_equal(pinned[p][1].numpy(), out[p].cpu().numpy()) for p in degs)
+        line["e2e"] = {"value": round(total_dofs / e2e_s / 1e9, 4), "unit": "GDoF/s",
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                       "ms_per_step": round(e2e_s * 1e3, 3),
+                       "api": "sfk_eval_host (pinned host buffers)", "matches_device_path": ok}
+        del pinned
+
+    # ---- CPU baseline: reference emitted C on the host cores (rank 0, N=1) ---
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_leg(degs, coords_np, host_u, args.cpu_cells)
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

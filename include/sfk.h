@@ -1,0 +1,161 @@
+/*
+ * sfk.h — C ABI of the B200 (sm_100a) sum-factorised cell-kernel library
+ * (libsfk.so, built from paper_1711_02473_b200/csrc).
+ *
+ * What it replaces.  The reference `sumfact` emits one C99 function per
+ * kernel,
+ *
+ *     void NAME(double *restrict A, const double *restrict coords,
+ *               const double *restrict w0 [, const double *restrict w1]);
+ *
+ * (reference pkg/src/sumfact/scheduling.py:731-735) and leaves the loop over
+ * cells to the caller.  `sfk_eval` is that loop, for a whole
+ * batch of cells, on the GPU: same argument order (A first, then coords,
+ * w0, w1), same per-cell layouts, same overwrite
+ * semantics (the emitted kernel zero-fills A first, scheduling.py:372).
+ * `sfk_plan_create` replaces the static const tables T0..Tk the emitted C
+ * embeds (scheduling.py:724-728): the caller passes the reference-bit-exact
+ * 1D tables produced on the host by `compile_kernel` (cli.py:211-217).
+ *
+ * Conventions.
+ *   - Every function returns 0 (SFK_OK) or a non-zero sfk_status; the text of
+ *     the last error on the calling thread is available from sfk_last_error.
+ *   - Batched arrays are C-contiguous row-major [ncells][size] fp64.
+ *   - sfk_eval* take DEVICE pointers, enqueue on `stream` (a cudaStream_t,
+ *     NULL = legacy default stream) and return without synchronising.  They
+ *     do not allocate.  A must not alias the inputs; it is overwritten.
+ *   - sfk_eval_host takes HOST pointers and is synchronous: it is the
+ *     drop-in for the caller's `for c in cells: NAME(A+c*nA, coords+c*nc,
+ *     w0+c*nw)` loop, with host<->device copies pipelined against compute.
+ *   - Plans are immutable after creation and may be used concurrently from
+ *     several threads/streams (the emitted kernels are reentrant).
+ */
+#ifndef SFK_H
+#define SFK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFK_ABI_VERSION 1
+
+typedef struct sfk_plan sfk_plan;
+
+typedef enum sfk_status {
+  SFK_OK = 0,
+  SFK_EINVAL = 1,        /* bad argument (null pointer, negative count, ...)  */
+  SFK_EUNSUPPORTED = 2,  /* no kernel instantiated for this kind/degree/points */
+  SFK_ECUDA = 3,         /* CUDA runtime error                                 */
+  SFK_ENOMEM = 4         /* host or device allocation failed                   */
+} sfk_status;
+
+typedef enum sfk_kind {
+  /* hex or quad Laplace action b = K u (registry `action_laplace`,
+   * reference forms.py:186-189, 235-243, 261-263); GL(m) or collocated GLL */
+  SFK_KIND_ACTION_LAPLACE = 1,
+  /* hex weighted Laplace action b = K_kappa u, kappa = w1 at GLL points
+   * (action_form(REGISTRY['weighted_laplace']), forms.py:192-193)        */
+  SFK_KIND_ACTION_WEIGHTED_LAPLACE = 2,
+  /* mass action b = M u (registry `action_mass`, forms.py:173)            */
+  SFK_KIND_ACTION_MASS = 3,
+  /* local stiffness matrix, test-major A[i*N+j] (registry `laplace`)      */
+  SFK_KIND_LAPLACE_MATRIX = 4,
+  /* vector Q_p^3 neo-Hookean residual (builder FormSpec);
+   * params = {mu, lambda}                                                 */
+  SFK_KIND_NEOHOOKEAN_RESIDUAL = 5
+} sfk_kind;
+
+/* ABI version of the loaded library (== SFK_ABI_VERSION). */
+int sfk_abi_version(void);
+
+/*
+ * Create a plan.  Host pointers, copied into the plan:
+ *   B, D    [n_dof1d * n_q1d]  1D basis / derivative tables, basis-major
+ *           (T[n_q1d*i + q], as the emitted C indexes its tables)
+ *   wq      [n_q1d]            1D quadrature weights on [0,1]
+ *   xq      [n_q1d]            1D quadrature points on [0,1]
+ *   Bc, Dc  [2 * n_q1d]        P1 coordinate-element tables at the points
+ *   params  [nparams]          form parameters (neo-Hookean: mu, lambda)
+ * cell_dim: 2 (quad) or 3 (hex).  collocated: 1 when B is the identity
+ * (GLL element evaluated at its own nodes, reference elements.py:200-220).
+ * Replaces: the static const tables of the emitted kernel
+ * (reference scheduling.py:724-728); built by compile_kernel (cli.py:211).
+ */
+int sfk_plan_create(int kind, int cell_dim, int degree, int n_dof1d,
+                    int n_q1d, int collocated, const double *B,
+                    const double *D, const double *wq, const double *xq,
+                    const double *Bc, const double *Dc, const double *params,
+                    int nparams, sfk_plan **out);
+
+int sfk_plan_destroy(sfk_plan *plan);
+
+/* Per-cell sizes of the plan's arguments, in doubles (for validation). */
+int sfk_plan_sizes(const sfk_plan *plan, int64_t *coords_size,
+                   int64_t *w0_size, int64_t *w1_size, int64_t *a_size);
+
+/*
+ * Batched evaluation on the device (replaces the caller's C cell loop around
+ * the emitted `NAME(A, coords, w0[, w1])`, scheduling.py:731-735).
+ *   A      [ncells][a_size]       output, overwritten
+ *   coords [ncells][2^d * d]      vertex coordinates, v = 4a+2b+c, comp inner
+ *   w0     [ncells][w0_size]      coefficient 0 (trial dofs for actions)
+ *   w1     [ncells][w1_size]      coefficient 1 (kappa) or NULL
+ */
+int sfk_eval(const sfk_plan *plan, int64_t ncells, double *A,
+             const double *coords, const double *w0, const double *w1,
+             void *stream);
+
+/*
+ * Fused evaluation of two plans sharing (coords, w0) in one launch
+ * (BASELINE config C1: quad Q3 action_mass + action_laplace).  Falls back to
+ * two launches when the pair has no fused kernel.
+ */
+int sfk_eval_pair(const sfk_plan *plan0, const sfk_plan *plan1,
+                  int64_t ncells, double *A0, double *A1,
+                  const double *coords, const double *w0, void *stream);
+
+/*
+ * Host-buffer evaluation: synchronous, chunked, copies pipelined with
+ * compute on internal streams.  Same layouts as sfk_eval.  chunk_cells <= 0
+ * picks a default.  Pinned (page-locked) host buffers give full PCIe
+ * bandwidth; pageable buffers work but copy slower.
+ */
+int sfk_eval_host(const sfk_plan *plan, int64_t ncells, double *A,
+                  const double *coords, const double *w0, const double *w1,
+                  int64_t chunk_cells);
+
+/*
+ * Functionals/checksums of a device array x[0..n):
+ *   out[0] = sum x_i^2,  out[1] = sum x_i        (overwritten)
+ * `out` is a DEVICE buffer of at least SFK_SUM_WORKSPACE doubles (the tail is
+ * scratch for per-CTA partials, so the call does not allocate).  The
+ * summation order depends only on n, so the result is bitwise reproducible.
+ * Used for the Frobenius checksum all-reduced over ranks (BASELINE C5).
+ */
+#define SFK_SUM_WORKSPACE 1024
+int sfk_sum_squares(const double *x, int64_t n, double *out, void *stream);
+
+/* Number of sfk kernels launched by this process so far (all threads). */
+int64_t sfk_launch_count(void);
+
+/* Copy the calling thread's last error message (NUL-terminated). */
+int sfk_last_error(char *buf, int64_t size);
+
+/* Device facts for the roofline logs. */
+int sfk_device_info(int device, int *sm_count, int *sm_clock_khz,
+                    int *mem_clock_khz, int *mem_bus_bits, char *name,
+                    int name_size);
+
+/*
+ * FP64 peak micro-benchmark on the current device: DFMA chains and
+ * DMMA (mma.sync m8n8k4 f64).  Runs about `seconds` in total.
+ */
+int sfk_fp64_peak(double seconds, double *tflops_dfma, double *tflops_dmma);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFK_H */

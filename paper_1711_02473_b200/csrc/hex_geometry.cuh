@@ -1,0 +1,92 @@
+// Trilinear hex geometry evaluated on the fly per quadrature point.
+//
+// Reference semantics:
+//   J[a][b] = sum_v coords[3v+a] * dPhi_v/dxhat_b(xi_q)  (geometry.py:42-64)
+//   with Phi_v the P1 tensor basis, v = 4*ix + 2*iy + iz, P1 values
+//   Bc[k][q] = (1-xi_q, xi_q) and derivatives Dc = (-1, +1) (exact);
+//   G = J^-1 by the adjugate, S = |det J|            (geometry.py:71-108).
+//
+// Tensor structure used here: column b of J (dx/dxhat_b) does not depend on
+// xi_b.  A thread that owns the quadrature line (qx, qy, *) therefore keeps
+//   col2            constant along the line, and
+//   col0, col1      affine in the P1 values at qz
+// and forms each J in 12 FMAs instead of the 9 x 8-term sums of the
+// reference loop nest.  The inverse is never formed: with rows
+//   r0 = col1 x col2, r1 = col2 x col0, r2 = col0 x col1  (adj(J) rows),
+// G = [r0; r1; r2] / det, and the Laplace flux is
+//   f = (w/|det|) R R^T g ,  g = reference gradient,
+// evaluated as two 3x3 mat-vecs.
+#pragma once
+
+#include "sfk_internal.cuh"
+
+namespace sfk {
+
+struct HexLineGeom {
+  double al0[2][3];  // col0(qz) = al0[0]*Bc0[qz] + al0[1]*Bc1[qz]
+  double al1[2][3];  // col1(qz) = al1[0]*Bc0[qz] + al1[1]*Bc1[qz]
+  double c2[3];      // col2 (constant along z)
+
+  // X: 24 coords of the cell (v = 4a+2b+c, comp inner); (bx0,bx1), (by0,by1)
+  // the P1 values at the line's qx, qy.
+  __device__ __forceinline__ void setup(const double* X, double bx0, double bx1,
+                                        double by0, double by1) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+      for (int cz = 0; cz < 2; ++cz) {
+        // d/dxhat_x: vertex pairs (1,b,cz) - (0,b,cz)
+        const double e00 = X[3 * (4 + cz) + k] - X[3 * cz + k];
+        const double e01 = X[3 * (6 + cz) + k] - X[3 * (2 + cz) + k];
+        al0[cz][k] = fma(e01, by1, e00 * by0);
+        // d/dxhat_y: (a,1,cz) - (a,0,cz)
+        const double e10 = X[3 * (2 + cz) + k] - X[3 * cz + k];
+        const double e11 = X[3 * (6 + cz) + k] - X[3 * (4 + cz) + k];
+        al1[cz][k] = fma(e11, bx1, e10 * bx0);
+      }
+      // d/dxhat_z: (a,b,1) - (a,b,0)
+      const double f00 = X[3 * 1 + k] - X[3 * 0 + k];
+      const double f01 = X[3 * 3 + k] - X[3 * 2 + k];
+      const double f10 = X[3 * 5 + k] - X[3 * 4 + k];
+      const double f11 = X[3 * 7 + k] - X[3 * 6 + k];
+      c2[k] = fma(fma(f11, by1, f10 * by0), bx1, fma(f01, by1, f00 * by0) * bx0);
+    }
+  }
+
+  // Adjugate rows and determinant at the point with P1 z-values (b0, b1).
+  __device__ __forceinline__ double adj(double b0, double b1, double r0[3],
+                                        double r1[3], double r2[3]) const {
+    double c0[3], c1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      c0[k] = fma(al0[1][k], b1, al0[0][k] * b0);
+      c1[k] = fma(al1[1][k], b1, al1[0][k] * b0);
+    }
+    cross(c1, c2, r0);
+    cross(c2, c0, r1);
+    cross(c0, c1, r2);
+    return fma(c0[2], r0[2], fma(c0[1], r0[1], c0[0] * r0[0]));
+  }
+
+  static __device__ __forceinline__ void cross(const double a[3], const double b[3],
+                                               double o[3]) {
+    o[0] = fma(a[1], b[2], -(a[2] * b[1]));
+    o[1] = fma(a[2], b[0], -(a[0] * b[2]));
+    o[2] = fma(a[0], b[1], -(a[1] * b[0]));
+  }
+};
+
+// f = s * R R^T g  (R rows r0, r1, r2).  In place on (g0, g1, g2).
+__device__ __forceinline__ void laplace_flux(const double r0[3], const double r1[3],
+                                             const double r2[3], double s,
+                                             double& g0, double& g1, double& g2) {
+  const double h0 = g0 * s, h1 = g1 * s, h2 = g2 * s;
+  double v[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) v[k] = fma(h2, r2[k], fma(h1, r1[k], h0 * r0[k]));
+  g0 = fma(r0[2], v[2], fma(r0[1], v[1], r0[0] * v[0]));
+  g1 = fma(r1[2], v[2], fma(r1[1], v[1], r1[0] * v[0]));
+  g2 = fma(r2[2], v[2], fma(r2[1], v[1], r2[0] * v[0]));
+}
+
+}  // namespace sfk

@@ -1,0 +1,282 @@
+// C-ABI entry points of libsfk.so (declared in include/sfk.h).
+//
+// This is the drop-in boundary: the reference hands a per-cell C function to
+// the caller's cell loop (scheduling.py:617-738); these entry
+// points ARE that loop, batched on the device.  Validation and error
+// reporting mirror the reference's: a missing argument is UnboundVariable,
+// a mis-sized one ShapeMismatch (interpreter.py:23-28, 291-299) — on the C
+// side both surface as SFK_EINVAL with the argument name in sfk_last_error,
+// and the Python layer raises the reference exception types before calling.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "sfk_internal.cuh"
+
+namespace sfk {
+
+static thread_local char g_err[512] = "";
+static std::atomic<int64_t> g_launches{0};
+
+int fail(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+int cuda_status(cudaError_t err, const char* what) {
+  if (err == cudaSuccess) return SFK_OK;
+  return fail(err == cudaErrorMemoryAllocation ? SFK_ENOMEM : SFK_ECUDA,
+              "%s: %s (%s)", what, cudaGetErrorName(err), cudaGetErrorString(err));
+}
+
+void note_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+static int dispatch(const sfk_plan* p, int64_t ncells, double* A,
+                    const double* coords, const double* w0, const double* w1,
+                    cudaStream_t s) {
+  switch (p->kind) {
+    case SFK_KIND_ACTION_LAPLACE:
+      if (p->dim == 3)
+        return p->collocated ? launch_hex_colloc_action(p, ncells, A, coords, w0, nullptr, s)
+                             : launch_hex_action(p, ncells, A, coords, w0, nullptr, s);
+      return launch_quad_action(p, nullptr, ncells, A, nullptr, coords, w0, s);
+    case SFK_KIND_ACTION_WEIGHTED_LAPLACE:
+      return launch_hex_colloc_action(p, ncells, A, coords, w0, w1, s);
+    case SFK_KIND_ACTION_MASS:
+      if (p->dim == 2) return launch_quad_action(p, nullptr, ncells, A, nullptr, coords, w0, s);
+      return fail(SFK_EUNSUPPORTED, "action_mass: only the quad kernel is instantiated");
+    case SFK_KIND_LAPLACE_MATRIX:
+      if (p->dim == 3) return launch_hex_matrix(p, ncells, A, coords, s);
+      return fail(SFK_EUNSUPPORTED, "laplace matrix: only the hex kernel is instantiated");
+    case SFK_KIND_NEOHOOKEAN_RESIDUAL:
+      return launch_hex_neohookean(p, ncells, A, coords, w0, s);
+    default:
+      return fail(SFK_EUNSUPPORTED, "unknown kernel kind %d", p->kind);
+  }
+}
+
+static int validate(const sfk_plan* p, int64_t ncells, const double* A,
+                    const double* coords, const double* w0, const double* w1) {
+  if (!p) return fail(SFK_EINVAL, "plan is NULL");
+  if (ncells < 0) return fail(SFK_EINVAL, "ncells < 0");
+  if (ncells == 0) return SFK_OK;
+  if (!A) return fail(SFK_EINVAL, "A is NULL");
+  if (!coords) return fail(SFK_EINVAL, "coords is NULL");
+  if (p->w0_size > 0 && !w0) return fail(SFK_EINVAL, "w0 is NULL");
+  if (p->w1_size > 0 && !w1) return fail(SFK_EINVAL, "w1 is NULL");
+  return SFK_OK;
+}
+
+}  // namespace sfk
+
+using namespace sfk;
+
+extern "C" {
+
+int sfk_abi_version(void) { return SFK_ABI_VERSION; }
+
+int sfk_plan_create(int kind, int cell_dim, int degree, int n, int m, int collocated,
+                    const double* B, const double* D, const double* wq, const double* xq,
+                    const double* Bc, const double* Dc, const double* params, int nparams,
+                    sfk_plan** out) {
+  if (!out) return fail(SFK_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (kind < SFK_KIND_ACTION_LAPLACE || kind > SFK_KIND_NEOHOOKEAN_RESIDUAL)
+    return fail(SFK_EINVAL, "unknown kind %d", kind);
+  if (cell_dim != 2 && cell_dim != 3) return fail(SFK_EINVAL, "cell_dim must be 2 or 3");
+  if (n < 2 || n > SFK_MAXN) return fail(SFK_EUNSUPPORTED, "n_dof1d=%d outside [2,%d]", n, SFK_MAXN);
+  if (m < 1 || m > SFK_MAXM) return fail(SFK_EUNSUPPORTED, "n_q1d=%d outside [1,%d]", m, SFK_MAXM);
+  if (!B || !D || !wq || !xq || !Bc || !Dc) return fail(SFK_EINVAL, "NULL table pointer");
+  if (nparams < 0 || nparams > 8 || (nparams > 0 && !params))
+    return fail(SFK_EINVAL, "bad params (nparams=%d)", nparams);
+  sfk_plan* p = new (std::nothrow) sfk_plan();
+  if (!p) return fail(SFK_ENOMEM, "plan allocation failed");
+  p->kind = kind;
+  p->dim = cell_dim;
+  p->degree = degree;
+  p->n = n;
+  p->m = m;
+  p->collocated = collocated ? 1 : 0;
+  p->nparams = nparams;
+  memcpy(p->B, B, sizeof(double) * n * m);
+  memcpy(p->D, D, sizeof(double) * n * m);
+  memcpy(p->wq, wq, sizeof(double) * m);
+  memcpy(p->xq, xq, sizeof(double) * m);
+  memcpy(p->Bc, Bc, sizeof(double) * 2 * m);
+  memcpy(p->Dc, Dc, sizeof(double) * 2 * m);
+  if (nparams) memcpy(p->params, params, sizeof(double) * nparams);
+  const int64_t nd = cell_dim == 3 ? (int64_t)n * n * n : (int64_t)n * n;
+  p->coords_size = cell_dim == 3 ? 24 : 8;
+  p->w0_size = 0;
+  p->w1_size = 0;
+  switch (kind) {
+    case SFK_KIND_ACTION_LAPLACE:
+    case SFK_KIND_ACTION_MASS:
+      p->w0_size = nd;
+      p->a_size = nd;
+      break;
+    case SFK_KIND_ACTION_WEIGHTED_LAPLACE:
+      p->w0_size = nd;
+      p->w1_size = nd;
+      p->a_size = nd;
+      break;
+    case SFK_KIND_LAPLACE_MATRIX:
+      p->a_size = nd * nd;
+      break;
+    case SFK_KIND_NEOHOOKEAN_RESIDUAL:
+      p->w0_size = 3 * nd;
+      p->a_size = 3 * nd;
+      if (nparams < 2) {
+        delete p;
+        return fail(SFK_EINVAL, "neo-Hookean plan needs params {mu, lambda}");
+      }
+      break;
+  }
+  *out = p;
+  return SFK_OK;
+}
+
+int sfk_plan_destroy(sfk_plan* plan) {
+  delete plan;
+  return SFK_OK;
+}
+
+int sfk_plan_sizes(const sfk_plan* p, int64_t* cs, int64_t* w0s, int64_t* w1s, int64_t* as) {
+  if (!p) return fail(SFK_EINVAL, "plan is NULL");
+  if (cs) *cs = p->coords_size;
+  if (w0s) *w0s = p->w0_size;
+  if (w1s) *w1s = p->w1_size;
+  if (as) *as = p->a_size;
+  return SFK_OK;
+}
+
+int sfk_eval(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+             const double* w0, const double* w1, void* stream) {
+  int st = validate(p, ncells, A, coords, w0, w1);
+  if (st != SFK_OK || ncells == 0) return st;
+  return dispatch(p, ncells, A, coords, w0, w1, (cudaStream_t)stream);
+}
+
+int sfk_eval_pair(const sfk_plan* p0, const sfk_plan* p1, int64_t ncells, double* A0,
+                  double* A1, const double* coords, const double* w0, void* stream) {
+  int st = validate(p0, ncells, A0, coords, w0, nullptr);
+  if (st == SFK_OK) st = validate(p1, ncells, A1, coords, w0, nullptr);
+  if (st != SFK_OK || ncells == 0) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool fusable = p0->dim == 2 && p1->dim == 2 && p0->n == p1->n && p0->m == p1->m &&
+                       !p0->collocated && !p1->collocated &&
+                       (p0->kind == SFK_KIND_ACTION_MASS || p0->kind == SFK_KIND_ACTION_LAPLACE) &&
+                       (p1->kind == SFK_KIND_ACTION_MASS || p1->kind == SFK_KIND_ACTION_LAPLACE) &&
+                       memcmp(p0->wq, p1->wq, sizeof(double) * p0->m) == 0 &&
+                       memcmp(p0->B, p1->B, sizeof(double) * p0->n * p0->m) == 0;
+  if (fusable) return launch_quad_action(p0, p1, ncells, A0, A1, coords, w0, s);
+  st = dispatch(p0, ncells, A0, coords, w0, nullptr, s);
+  if (st != SFK_OK) return st;
+  return dispatch(p1, ncells, A1, coords, w0, nullptr, s);
+}
+
+int sfk_eval_host(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                  const double* w0, const double* w1, int64_t chunk) {
+  int st = validate(p, ncells, A, coords, w0, w1);
+  if (st != SFK_OK || ncells == 0) return st;
+  const int64_t per_cell = p->coords_size + p->w0_size + p->w1_size + p->a_size;
+  if (chunk <= 0) {
+    // ~64 MiB of traffic per chunk: big enough to amortise launch + copy
+    // latency, small enough for 3-deep pipelining.
+    chunk = (int64_t)((64ll << 20) / (8 * per_cell));
+    if (chunk < 1024) chunk = 1024;
+  }
+  if (chunk > ncells) chunk = ncells;
+  constexpr int NS = 3;
+  cudaStream_t st3[NS] = {nullptr, nullptr, nullptr};
+  double* dbuf[NS] = {nullptr, nullptr, nullptr};
+  int rc = SFK_OK;
+  const size_t bytes = (size_t)chunk * per_cell * sizeof(double);
+  for (int i = 0; i < NS && rc == SFK_OK; ++i) {
+    rc = cuda_status(cudaStreamCreateWithFlags(&st3[i], cudaStreamNonBlocking), "cudaStreamCreate");
+    if (rc == SFK_OK) rc = cuda_status(cudaMalloc(&dbuf[i], bytes), "cudaMalloc(eval_host staging)");
+  }
+  int64_t k = 0;
+  for (int64_t c0 = 0; c0 < ncells && rc == SFK_OK; c0 += chunk, ++k) {
+    const int64_t nc = (ncells - c0) < chunk ? (ncells - c0) : chunk;
+    const int i = (int)(k % NS);
+    cudaStream_t s = st3[i];
+    double* dc = dbuf[i];
+    double* dw0 = dc + chunk * p->coords_size;
+    double* dw1 = dw0 + chunk * p->w0_size;
+    double* dA = dw1 + chunk * p->w1_size;
+    rc = cuda_status(cudaMemcpyAsync(dc, coords + c0 * p->coords_size,
+                                     nc * p->coords_size * sizeof(double),
+                                     cudaMemcpyHostToDevice, s), "H2D coords");
+    if (rc == SFK_OK && p->w0_size)
+      rc = cuda_status(cudaMemcpyAsync(dw0, w0 + c0 * p->w0_size, nc * p->w0_size * sizeof(double),
+                                       cudaMemcpyHostToDevice, s), "H2D w0");
+    if (rc == SFK_OK && p->w1_size)
+      rc = cuda_status(cudaMemcpyAsync(dw1, w1 + c0 * p->w1_size, nc * p->w1_size * sizeof(double),
+                                       cudaMemcpyHostToDevice, s), "H2D w1");
+    if (rc == SFK_OK)
+      rc = dispatch(p, nc, dA, dc, p->w0_size ? dw0 : nullptr, p->w1_size ? dw1 : nullptr, s);
+    if (rc == SFK_OK)
+      rc = cuda_status(cudaMemcpyAsync(A + c0 * p->a_size, dA, nc * p->a_size * sizeof(double),
+                                       cudaMemcpyDeviceToHost, s), "D2H A");
+  }
+  for (int i = 0; i < NS; ++i) {
+    if (st3[i]) {
+      cudaError_t e = cudaStreamSynchronize(st3[i]);
+      if (rc == SFK_OK) rc = cuda_status(e, "cudaStreamSynchronize(eval_host)");
+      cudaStreamDestroy(st3[i]);
+    }
+    if (dbuf[i]) cudaFree(dbuf[i]);
+  }
+  return rc;
+}
+
+int sfk_sum_squares(const double* x, int64_t n, double* out, void* stream) {
+  if (n < 0) return fail(SFK_EINVAL, "n < 0");
+  if (!out) return fail(SFK_EINVAL, "out is NULL");
+  if (n == 0) return SFK_OK;
+  if (!x) return fail(SFK_EINVAL, "x is NULL");
+  return launch_sum_squares(x, n, out, (cudaStream_t)stream);
+}
+
+int64_t sfk_launch_count(void) { return g_launches.load(); }
+
+int sfk_last_error(char* buf, int64_t size) {
+  if (!buf || size <= 0) return SFK_EINVAL;
+  snprintf(buf, (size_t)size, "%s", g_err);
+  return SFK_OK;
+}
+
+int sfk_device_info(int device, int* sm_count, int* sm_clock_khz, int* mem_clock_khz,
+                    int* mem_bus_bits, char* name, int name_size) {
+  cudaDeviceProp prop;
+  int rc = cuda_status(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (rc != SFK_OK) return rc;
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  int v = 0;
+  if (sm_clock_khz) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, device);
+    *sm_clock_khz = v;
+  }
+  if (mem_clock_khz) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMemoryClockRate, device);
+    *mem_clock_khz = v;
+  }
+  if (mem_bus_bits) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrGlobalMemoryBusWidth, device);
+    *mem_bus_bits = v;
+  }
+  if (name && name_size > 0) snprintf(name, (size_t)name_size, "%s", prop.name);
+  return SFK_OK;
+}
+
+int sfk_fp64_peak(double seconds, double* dfma, double* dmma) {
+  return run_fp64_peak(seconds, dfma, dmma);
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// Internal declarations shared by the sfk CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sfk.h"
+
+#define SFK_MAXN 17   // dofs per axis (p <= 16)
+#define SFK_MAXM 18   // quadrature points per axis
+
+// The plan behind the opaque sfk_plan* handle.  Tables are HOST copies: they
+// are passed by value (as __grid_constant__ kernel parameters, i.e. constant
+// bank 0) to every launch, so a plan owns no device memory and is usable on
+// any device / stream.
+struct sfk_plan {
+  int kind, dim, degree, n, m, collocated, nparams;
+  double B[SFK_MAXN * SFK_MAXM];   // B[i*m + q]
+  double D[SFK_MAXN * SFK_MAXM];   // D[i*m + q]
+  double wq[SFK_MAXM];
+  double xq[SFK_MAXM];
+  double Bc[2 * SFK_MAXM];         // P1 values  Bc[v*m + q]
+  double Dc[2 * SFK_MAXM];         // P1 derivatives (-1, +1)
+  double params[8];
+  int64_t coords_size, w0_size, w1_size, a_size;
+};
+
+namespace sfk {
+
+// Thread-local error text + status helpers (sfk_api.cu).
+int fail(int status, const char* fmt, ...);
+int cuda_status(cudaError_t err, const char* what);
+void note_launch(int64_t k = 1);
+
+// Tables in the form kernels consume them (kernel parameter => constant bank;
+// compile-time indices become c[0x0][...] operands of DFMA, no loads).
+template <int N, int M>
+struct Tabs {
+  double B[N * M];
+  double D[N * M];
+  double W[M];
+  double Bc[2 * M];
+  double X[M];
+};
+
+template <int N, int M>
+inline Tabs<N, M> make_tabs(const sfk_plan* p) {
+  Tabs<N, M> t;
+  for (int i = 0; i < N; ++i)
+    for (int q = 0; q < M; ++q) {
+      t.B[i * M + q] = p->B[i * p->m + q];
+      t.D[i * M + q] = p->D[i * p->m + q];
+    }
+  for (int q = 0; q < M; ++q) {
+    t.W[q] = p->wq[q];
+    t.X[q] = p->xq[q];
+    t.Bc[q] = p->Bc[q];
+    t.Bc[M + q] = p->Bc[p->m + q];
+  }
+  return t;
+}
+
+// Family launchers (one translation unit each).
+int launch_hex_action(const sfk_plan* p, int64_t ncells, double* A,
+                      const double* coords, const double* w0,
+                      const double* w1, cudaStream_t s);
+int launch_hex_colloc_action(const sfk_plan* p, int64_t ncells, double* A,
+                             const double* coords, const double* w0,
+                             const double* w1, cudaStream_t s);
+int launch_quad_action(const sfk_plan* p0, const sfk_plan* p1, int64_t ncells,
+                       double* A0, double* A1, const double* coords,
+                       const double* w0, cudaStream_t s);
+int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A,
+                      const double* coords, cudaStream_t s);
+int launch_hex_neohookean(const sfk_plan* p, int64_t ncells, double* A,
+                          const double* coords, const double* w0,
+                          cudaStream_t s);
+int launch_sum_squares(const double* x, int64_t n, double* out, cudaStream_t s);
+int run_fp64_peak(double seconds, double* dfma, double* dmma);
+
+}  // namespace sfk
+
+// ---------------------------------------------------------------------------
+// device helpers
+
+namespace sfk {
+
+// 1/x to full double precision: MUFU.RCP64H seed + two Newton steps.
+__device__ __forceinline__ double rcp64(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  return y;
+}
+
+__host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+}  // namespace sfk

@@ -1,0 +1,312 @@
+"""ctypes binding of libsfk.so and the batched evaluation API.
+
+Reference tier 2 of the boundary: per-cell execution is
+the emitted C function driven by the caller's cell loop
+(scheduling.py:731-735), or ``interpreter.run_kernel(program, inputs)``
+(interpreter.py:279-378) in Python.  The drop-in here is
+
+    evaluate_batched(plan, {"coords": (C, 24), "w0": (C, nd), ...}) -> (C, size)
+
+which validates exactly like ``run_kernel`` (missing argument ->
+``UnboundVariable``, wrong per-cell size -> ``ShapeMismatch``,
+interpreter.py:291-299) and then makes ONE ``sfk_eval`` call: device
+tensors run stream-ordered on the current torch stream; numpy (host) arrays
+go through ``sfk_eval_host`` (pipelined H2D / compute / D2H).  There is no
+CPU fallback: without a GPU or without libsfk.so every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import NativeError, ShapeMismatch, UnboundVariable
+
+__all__ = ["load_library", "evaluate_batched", "evaluate_batched_pair",
+           "evaluate_host", "sum_squares", "launch_count", "fp64_peak",
+           "device_info", "native_plan", "EXPORTED_SYMBOLS"]
+
+_LIB = None
+_LOCK = threading.Lock()
+_dp = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+
+EXPORTED_SYMBOLS = (
+    "sfk_abi_version", "sfk_plan_create", "sfk_plan_destroy", "sfk_plan_sizes",
+    "sfk_eval", "sfk_eval_pair", "sfk_eval_host", "sfk_sum_squares",
+    "sfk_launch_count", "sfk_last_error", "sfk_device_info", "sfk_fp64_peak",
+)
+ABI_VERSION = 1
+SUM_WORKSPACE = 1024
+
+
+def library_path():
+    return os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsfk.so")
+
+
+def _declare(lib):
+    i64 = ctypes.c_int64
+    ci = ctypes.c_int
+    lib.sfk_abi_version.restype = ci
+    lib.sfk_plan_create.argtypes = [ci, ci, ci, ci, ci, ci, _dp, _dp, _dp, _dp,
+                                    _dp, _dp, _dp, ci, ctypes.POINTER(_vp)]
+    lib.sfk_plan_create.restype = ci
+    lib.sfk_plan_destroy.argtypes = [_vp]
+    lib.sfk_plan_destroy.restype = ci
+    lib.sfk_plan_sizes.argtypes = [_vp] + [ctypes.POINTER(i64)] * 4
+    lib.sfk_plan_sizes.restype = ci
+    lib.sfk_eval.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, _vp]
+    lib.sfk_eval.restype = ci
+    lib.sfk_eval_pair.argtypes = [_vp, _vp, i64, _vp, _vp, _vp, _vp, _vp]
+    lib.sfk_eval_pair.restype = ci
+    lib.sfk_eval_host.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, i64]
+    lib.sfk_eval_host.restype = ci
+    lib.sfk_sum_squares.argtypes = [_vp, i64, _vp, _vp]
+    lib.sfk_sum_squares.restype = ci
+    lib.sfk_launch_count.restype = i64
+    lib.sfk_last_error.argtypes = [ctypes.c_char_p, i64]
+    lib.sfk_last_error.restype = ci
+    lib.sfk_device_info.argtypes = [ci] + [ctypes.POINTER(ci)] * 4 + [ctypes.c_char_p, ci]
+    lib.sfk_device_info.restype = ci
+    lib.sfk_fp64_peak.argtypes = [ctypes.c_double, _dp, _dp]
+    lib.sfk_fp64_peak.restype = ci
+
+
+def load_library(build_if_missing=True):
+    """Load libsfk.so (building it in-tree with nvcc if it is absent)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    with _LOCK:
+        if _LIB is not None:
+            return _LIB
+        path = library_path()
+        if not os.path.exists(path):
+            if not build_if_missing:
+                raise NativeError(-1, "libsfk.so not built (run __graft_entry__.build())")
+            from ._build import build_native
+            build_native()
+        lib = ctypes.CDLL(path)
+        _declare(lib)
+        if lib.sfk_abi_version() != ABI_VERSION:
+            raise NativeError(-1, "libsfk.so ABI %d != expected %d"
+                              % (lib.sfk_abi_version(), ABI_VERSION))
+        _LIB = lib
+        return lib
+
+
+def _check(status):
+    if status != 0:
+        buf = ctypes.create_string_buffer(512)
+        _LIB.sfk_last_error(buf, 512)
+        raise NativeError(status, buf.value.decode(errors="replace"))
+
+
+def _as_dp(arr):
+    return arr.ctypes.data_as(_dp)
+
+
+class _NativePlan:
+    def __init__(self, plan):
+        lib = load_library()
+        h = _vp()
+        params = np.asarray(plan.params, dtype=np.float64)
+        _check(lib.sfk_plan_create(
+            plan.kind, plan.dim, int(plan.degree), plan.n, plan.m,
+            int(plan.collocated), _as_dp(plan.B), _as_dp(plan.D),
+            _as_dp(plan.wq), _as_dp(plan.xq), _as_dp(plan.Bc), _as_dp(plan.Dc),
+            _as_dp(params) if len(params) else None, len(params),
+            ctypes.byref(h)))
+        self.handle = h
+        self._lib = lib
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self._lib.sfk_plan_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def native_plan(plan):
+    """The C-ABI plan handle of a KernelPlan (created once, cached)."""
+    np_ = plan._native.get("handle")
+    if np_ is None:
+        np_ = _NativePlan(plan)
+        plan._native["handle"] = np_
+    return np_.handle
+
+
+# ---------------------------------------------------------------------------
+# validation (reference interpreter.py:291-299 semantics)
+
+
+def _collect(plan, inputs, is_tensor):
+    """Return ({name: 2D array}, ncells, squeeze) after reference checks."""
+    out = {}
+    ncells = None
+    squeeze = False
+    for name, size in plan.arguments:
+        if name not in inputs:
+            raise UnboundVariable(name)
+        arr = inputs[name]
+        shape = tuple(arr.shape)
+        if len(shape) == 1:
+            if shape[0] != size:
+                raise ShapeMismatch("argument %s has size %d, declared %d"
+                                    % (name, shape[0], size))
+            arr = arr.reshape(1, size)
+            squeeze = True
+        elif len(shape) == 2:
+            if shape[1] != size:
+                raise ShapeMismatch("argument %s has per-cell size %d, declared %d"
+                                    % (name, shape[1], size))
+        else:
+            raise ShapeMismatch("argument %s must be (ncells, %d), got %s"
+                                % (name, size, shape))
+        if ncells is None:
+            ncells = arr.shape[0]
+        elif arr.shape[0] != ncells:
+            raise ShapeMismatch("argument %s has %d cells, expected %d"
+                                % (name, arr.shape[0], ncells))
+        out[name] = arr
+    return out, (ncells or 0), squeeze
+
+
+def evaluate_batched(plan, inputs, out=None, stream=None):
+    """Evaluate ``plan`` on every cell of a batch.
+
+    inputs: mapping argument name -> (ncells, size) float64 array, either
+    torch CUDA tensors (stream-ordered, returns a CUDA tensor) or numpy
+    arrays (synchronous host path, returns numpy).  A 1D array of one cell's
+    size is accepted and a 1D result returned, like ``run_kernel``.
+    """
+    first = next(iter(inputs.values()), None) if inputs else None
+    if first is not None and isinstance(first, np.ndarray):
+        return evaluate_host(plan, inputs, out=out)
+    import torch
+
+    args, ncells, squeeze = _collect(plan, inputs, True)
+    if not torch.cuda.is_available():
+        raise NativeError(-1, "evaluate_batched needs a CUDA device (no CPU fallback)")
+    dev = None
+    for name, t in args.items():
+        if not isinstance(t, torch.Tensor):
+            raise TypeError("argument %s must be a torch.Tensor or numpy array" % name)
+        if t.dtype != torch.float64:
+            raise TypeError("argument %s must be float64, got %s" % (name, t.dtype))
+        if not t.is_cuda:
+            raise TypeError("argument %s must live on a CUDA device" % name)
+        dev = t.device if dev is None else dev
+        if t.device != dev:
+            raise ValueError("all arguments must be on one device")
+        if not t.is_contiguous():
+            args[name] = t.contiguous()
+    rsize = plan.return_size
+    if out is None:
+        out = torch.empty((ncells, rsize), dtype=torch.float64, device=dev)
+    elif tuple(out.shape) != (ncells, rsize) or not out.is_contiguous():
+        raise ShapeMismatch("out must be a contiguous (%d, %d) tensor" % (ncells, rsize))
+    handle = native_plan(plan)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    with torch.cuda.device(dev):
+        _check(_LIB.sfk_eval(handle, ncells, out.data_ptr(),
+                             args["coords"].data_ptr(),
+                             args["w0"].data_ptr() if "w0" in args else None,
+                             args["w1"].data_ptr() if "w1" in args else None,
+                             stream))
+    return out.reshape(rsize) if squeeze else out
+
+
+def evaluate_batched_pair(plan0, plan1, inputs, stream=None):
+    """Two plans over the same (coords, w0) in one fused launch when the pair
+    has a fused kernel (quad mass + Laplace action, BASELINE config C1)."""
+    import torch
+
+    args, ncells, _ = _collect(plan0, inputs, True)
+    _collect(plan1, inputs, True)
+    dev = args["coords"].device
+    a0 = torch.empty((ncells, plan0.return_size), dtype=torch.float64, device=dev)
+    a1 = torch.empty((ncells, plan1.return_size), dtype=torch.float64, device=dev)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    with torch.cuda.device(dev):
+        _check(load_library().sfk_eval_pair(
+            native_plan(plan0), native_plan(plan1), ncells, a0.data_ptr(),
+            a1.data_ptr(), args["coords"].contiguous().data_ptr(),
+            args["w0"].contiguous().data_ptr(), stream))
+    return a0, a1
+
+
+def evaluate_host(plan, inputs, out=None, chunk_cells=0):
+    """Host-buffer evaluation through ``sfk_eval_host`` (synchronous)."""
+    args, ncells, squeeze = _collect(plan, inputs, False)
+    for name in list(args):
+        a = args[name]
+        if a.dtype != np.float64:
+            raise TypeError("argument %s must be float64" % name)
+        if not a.flags.c_contiguous:
+            args[name] = np.ascontiguousarray(a)
+    rsize = plan.return_size
+    if out is None:
+        out = np.empty((ncells, rsize), dtype=np.float64)
+    elif out.shape != (ncells, rsize) or not out.flags.c_contiguous or out.dtype != np.float64:
+        raise ShapeMismatch("out must be a contiguous float64 (%d, %d) array" % (ncells, rsize))
+    lib = load_library()
+
+    def ptr(name):
+        return args[name].ctypes.data if name in args else None
+
+    _check(lib.sfk_eval_host(native_plan(plan), ncells, out.ctypes.data,
+                             ptr("coords"), ptr("w0"), ptr("w1"), int(chunk_cells)))
+    return out.reshape(rsize) if squeeze else out
+
+
+def evaluate_host_ptrs(plan, ncells, a_ptr, coords_ptr, w0_ptr, w1_ptr, chunk_cells=0):
+    """Raw-pointer host evaluation (pinned torch tensors from the bench)."""
+    _check(load_library().sfk_eval_host(native_plan(plan), ncells, a_ptr, coords_ptr,
+                                        w0_ptr, w1_ptr, int(chunk_cells)))
+
+
+def sum_squares(x, workspace=None, stream=None):
+    """(sum x^2, sum x) of a CUDA float64 tensor, as a 2-element CUDA tensor
+    (device-side, stream-ordered; no host sync)."""
+    import torch
+
+    if x.dtype != torch.float64 or not x.is_cuda:
+        raise TypeError("sum_squares needs a CUDA float64 tensor")
+    x = x.contiguous()
+    if workspace is None:
+        workspace = torch.empty(SUM_WORKSPACE, dtype=torch.float64, device=x.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+    with torch.cuda.device(x.device):
+        _check(load_library().sfk_sum_squares(x.data_ptr(), x.numel(),
+                                              workspace.data_ptr(), stream))
+    return workspace[:2]
+
+
+def launch_count():
+    return int(load_library().sfk_launch_count())
+
+
+def fp64_peak(seconds=0.5):
+    lib = load_library()
+    f = ctypes.c_double()
+    m = ctypes.c_double()
+    _check(lib.sfk_fp64_peak(seconds, ctypes.byref(f), ctypes.byref(m)))
+    return f.value, m.value
+
+
+def device_info(device=0):
+    lib = load_library()
+    vals = [ctypes.c_int() for _ in range(4)]
+    name = ctypes.create_string_buffer(256)
+    _check(lib.sfk_device_info(device, *[ctypes.byref(v) for v in vals], name, 256))
+    return {"sm_count": vals[0].value, "sm_clock_khz": vals[1].value,
+            "mem_clock_khz": vals[2].value, "mem_bus_bits": vals[3].value,
+            "name": name.value.decode()}

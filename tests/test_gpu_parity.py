@@ -1,0 +1,131 @@
+"""Parity of the sm_100a kernels (through the C-ABI) with the reference.
+
+Bar (BASELINE.json north_star): relative 1e-12 in fp64 with the SURVEY.md
+§8(c) metric — per cell max|y - y_ref| / max|y_ref|, max over cells.
+Ground truth: the reference's own outputs (tests/golden) and, for larger
+batches, the C oracle (oracle/cpu.py, itself pinned to the golden fixtures in
+tests/test_oracle.py).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, rel_err
+from oracle import cpu
+from paper_1711_02473_b200 import (compile_kernel, evaluate_batched, evaluate_host,
+                                   launch_count, sum_squares, workloads)
+from paper_1711_02473_b200.errors import ShapeMismatch, UnboundVariable
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def _dev(torch, inputs):
+    return {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in inputs.items()}
+
+
+def _run(torch, plan, inputs):
+    out = evaluate_batched(plan, _dev(torch, inputs))
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("p", range(1, 9))
+def test_c2_hex_laplace_action_golden(cuda, p):
+    g = np.load(os.path.join(GOLDEN, "c2.npz"))
+    plan = compile_kernel("action_laplace", "hex", p)
+    inp = {"coords": g["coords"], "w0": g["w0_p%d" % p]}
+    assert rel_err(_run(cuda, plan, inp), g["A_p%d" % p]) < TOL
+
+
+@pytest.mark.parametrize("p", range(1, 9))
+@pytest.mark.parametrize("ncells", [1, 7, 509])
+def test_c2_hex_laplace_action_vs_oracle(cuda, p, ncells):
+    plan = compile_kernel("action_laplace", "hex", p)
+    coords = workloads.lattice_coords(8, 8, 8)[:ncells]
+    inp = {"coords": coords, "w0": workloads.uniform_dofs(ncells, (p + 1) ** 3)}
+    assert rel_err(_run(cuda, plan, inp), cpu.evaluate(plan, inp)) < TOL
+
+
+@pytest.mark.parametrize("p", [1, 3, 8])
+def test_c2_full_size_properties(cuda, p):
+    """2^18 cells (BASELINE config C2): sampled oracle parity, linearity and
+    the patch test (constants are in the kernel of the Laplacian)."""
+    torch = cuda
+    plan = compile_kernel("action_laplace", "hex", p)
+    inp = workloads.c2_inputs(p)
+    dev = _dev(torch, inp)
+    A = evaluate_batched(plan, dev)
+    rng = np.random.default_rng(0)
+    idx = np.sort(rng.choice(inp["coords"].shape[0], 256, replace=False))
+    sample = {k: v[idx] for k, v in inp.items()}
+    assert rel_err(A[torch.from_numpy(idx).cuda()].cpu().numpy(),
+                   cpu.evaluate(plan, sample)) < TOL
+    # linearity: A(u + 2v) = A(u) + 2 A(v)
+    v = torch.roll(dev["w0"], 1, 0)
+    Au = A
+    Av = evaluate_batched(plan, {"coords": dev["coords"], "w0": v})
+    Auv = evaluate_batched(plan, {"coords": dev["coords"], "w0": dev["w0"] + 2 * v})
+    scale = Auv.abs().amax(dim=1)
+    err = ((Auv - Au - 2 * Av).abs().amax(dim=1) / scale).max().item()
+    assert err < 1e-12
+    # patch test: A(1) = 0 relative to A's scale for unit-size data
+    ones = torch.ones_like(dev["w0"])
+    A1 = evaluate_batched(plan, {"coords": dev["coords"], "w0": ones})
+    assert (A1.abs().amax() / Au.abs().amax()).item() < 1e-11
+
+
+def test_host_path_matches_device_path(cuda):
+    torch = cuda
+    plan = compile_kernel("action_laplace", "hex", 4)
+    inp = workloads.c2_inputs(4, dims=(16, 16, 13))
+    dev = _run(torch, plan, inp)
+    host = evaluate_host(plan, inp, chunk_cells=1000)   # several pipelined chunks
+    assert np.array_equal(dev, host)
+    host2 = evaluate_batched(plan, inp)                  # numpy inputs -> host path
+    assert np.array_equal(dev, host2)
+
+
+def test_validation_and_edge_cases(cuda):
+    torch = cuda
+    plan = compile_kernel("action_laplace", "hex", 2)
+    coords = torch.zeros((3, 24), dtype=torch.float64, device="cuda")
+    with pytest.raises(UnboundVariable):
+        evaluate_batched(plan, {"coords": coords})
+    with pytest.raises(ShapeMismatch):
+        evaluate_batched(plan, {"coords": coords,
+                                "w0": torch.zeros((3, 26), dtype=torch.float64, device="cuda")})
+    with pytest.raises(ShapeMismatch):
+        evaluate_batched(plan, {"coords": coords,
+                                "w0": torch.zeros((4, 27), dtype=torch.float64, device="cuda")})
+    # empty batch
+    out = evaluate_batched(plan, {"coords": coords[:0],
+                                  "w0": torch.zeros((0, 27), dtype=torch.float64, device="cuda")})
+    assert out.shape == (0, 27)
+    # a single cell passed as flat arrays, like run_kernel
+    c = workloads.lattice_coords(1, 1, 1)[0]
+    u = workloads.uniform_dofs(1, 27)[0]
+    flat = evaluate_batched(plan, {"coords": torch.from_numpy(c).cuda(),
+                                   "w0": torch.from_numpy(u).cuda()})
+    assert flat.shape == (27,)
+    ref = cpu.evaluate(plan, {"coords": c[None], "w0": u[None]})[0]
+    assert rel_err(flat.cpu().numpy()[None], ref[None]) < TOL
+    # zero dofs -> zero output (SPEC.md action examples)
+    z = evaluate_batched(plan, {"coords": torch.from_numpy(c[None]).cuda(),
+                                "w0": torch.zeros((1, 27), dtype=torch.float64, device="cuda")})
+    assert torch.count_nonzero(z).item() == 0
+
+
+def test_sum_squares_and_launch_counter(cuda):
+    torch = cuda
+    x = torch.from_numpy(np.random.default_rng(1).standard_normal(1_000_003)).cuda()
+    before = launch_count()
+    s = sum_squares(x).cpu().numpy()
+    assert launch_count() > before
+    xn = x.cpu().numpy()
+    assert abs(s[0] - np.dot(xn, xn)) < 1e-12 * np.dot(xn, xn)
+    assert abs(s[1] - xn.sum()) < 1e-9
+    s2 = sum_squares(x).cpu().numpy()
+    assert np.array_equal(s, s2)   # bitwise reproducible
