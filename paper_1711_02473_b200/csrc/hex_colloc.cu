@@ -1,0 +1,235 @@
+// Hex GLL-collocated (weighted) Laplace action — BASELINE config C3
+// (p = 4..16, kappa = w1 at the GLL points) and the collocated variant of
+// registry `action_laplace` (--variant spectral_gll --quadrature
+// collocated-gll).
+//
+// Reference: `action_form(REGISTRY['weighted_laplace'])` lowered with
+// `default_quadrature(..., collocated_gll=True)` (forms.py:192-193, 235-243,
+// 291-306).  The element is evaluated at its own nodes, so its value table
+// is Delta(i, q) (elements.py:200-220) and delta cancellation
+// (passes.py:336-388) leaves, per reference gradient component, ONE 1D
+// D-contraction along that component's axis: 3 forward + 3 transposed
+// contractions of N^4 each, instead of 8 + 8.
+// kappa is a coefficient in the same GLL space: its value at point q is its
+// dof q (the Delta property), so it enters pointwise, no contraction.
+//
+// B200 mapping: one CTA = CPB cells (1 cell for N >= 13: a 17^3 field is
+// 38 KB).  Shared memory holds three N^3 arrays per cell with padded
+// strides (tools/smem_pads.py):  U (u, later A), GX (d_x u, later f_x),
+// GY (d_y u, later f_y).  Phases:
+//   1. coalesced copy u -> U
+//   2. each thread: one x-line (GX = Dx u) and one y-line (GY = Dy u)
+//   3. each thread owns a z-line (x, y): d_z u in registers, then per point
+//      geometry + kappa + flux, writing f_x, f_y in place and accumulating
+//      A_z = Dz^T f_z in registers, stored over its own U line
+//   4. x-lines: U += Dx^T f_x;   5. y-lines: U += Dy^T f_y
+//   6. coalesced copy U -> A
+#include "hex_geometry.cuh"
+
+namespace sfk {
+
+template <int N>
+struct TabsD {
+  double D[N * N];
+  double W[N];
+  double Bc[2 * N];
+};
+
+template <int N, int CPB, int SY, int SX, int CS>
+struct CollocCfg {
+  static constexpr int NN = N * N;
+  static constexpr int N3 = N * N * N;
+  static constexpr int THREADS = round_up(CPB * NN, 32);
+  static constexpr size_t SMEM = (size_t)(3 * CPB * CS + CPB * 24) * sizeof(double);
+};
+
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED>
+__global__ void __launch_bounds__(CollocCfg<N, CPB, SY, SX, CS>::THREADS)
+hex_colloc_action_kernel(const __grid_constant__ TabsD<N> T, int64_t ncells,
+                         const double* __restrict__ coords, const double* __restrict__ u,
+                         const double* __restrict__ kappa, double* __restrict__ A) {
+  using C = CollocCfg<N, CPB, SY, SX, CS>;
+  constexpr int NN = C::NN, N3 = C::N3;
+  extern __shared__ double smem[];
+  double* sU = smem;
+  double* sGX = sU + CPB * CS;
+  double* sGY = sGX + CPB * CS;
+  double* sC = sGY + CPB * CS;
+
+  const int tid = threadIdx.x;
+  const int64_t cell0 = (int64_t)blockIdx.x * CPB;
+  const int64_t rem = ncells - cell0;
+  const int ncb = rem < CPB ? (int)rem : CPB;
+
+  for (int i = tid; i < CPB * 24; i += C::THREADS)
+    sC[i] = i < ncb * 24 ? __ldg(coords + cell0 * 24 + i) : 0.0;
+  {
+    const double* ug = u + cell0 * N3;
+    for (int i = tid; i < CPB * N3; i += C::THREADS) {
+      const int c = i / N3, r = i - c * N3;
+      const int x = r / NN, y = (r / N) % N, z = r % N;
+      sU[c * CS + x * SX + y * SY + z] = c < ncb ? __ldg(ug + i) : 0.0;
+    }
+  }
+  __syncthreads();
+
+  const bool act = tid < CPB * NN;
+  const int c = tid / NN, r = tid - (tid / NN) * NN;
+  const int a = r / N, b = r - (r / N) * N;
+  const int cb = c * CS;
+
+  // ---- phase 2: x-line (y=a, z=b) and y-line (x=a, z=b) ---------------
+  if (act) {
+    double ul[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) ul[i] = sU[cb + i * SX + a * SY + b];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double g = T.D[q] * ul[0];
+#pragma unroll
+      for (int i = 1; i < N; ++i) g = fma(T.D[i * N + q], ul[i], g);
+      sGX[cb + q * SX + a * SY + b] = g;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) ul[i] = sU[cb + a * SX + i * SY + b];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double g = T.D[q] * ul[0];
+#pragma unroll
+      for (int i = 1; i < N; ++i) g = fma(T.D[i * N + q], ul[i], g);
+      sGY[cb + a * SX + q * SY + b] = g;
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 3: z-line (x=a, y=b): d_z u, flux, A_z = Dz^T f_z ---------
+  if (act) {
+    const int base = cb + a * SX + b * SY;
+    double ul[N], az[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      ul[i] = sU[base + i];
+      az[i] = 0.0;
+    }
+    HexLineGeom geo;
+    geo.setup(sC + c * 24, T.Bc[a], T.Bc[N + a], T.Bc[b], T.Bc[N + b]);
+    const double wxy = T.W[a] * T.W[b];
+    const double* kp = WEIGHTED ? kappa + (cell0 + c) * N3 + (a * N + b) * N : nullptr;
+    const bool valid = c < ncb;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double gz = T.D[q] * ul[0];
+#pragma unroll
+      for (int i = 1; i < N; ++i) gz = fma(T.D[i * N + q], ul[i], gz);
+      double gx = sGX[base + q], gy = sGY[base + q];
+      double r0[3], r1[3], r2[3];
+      const double det = geo.adj(T.Bc[q], T.Bc[N + q], r0, r1, r2);
+      double s = (wxy * T.W[q]) * rcp64(fabs(det));
+      if (WEIGHTED) s *= valid ? __ldg(kp + q) : 0.0;
+      laplace_flux(r0, r1, r2, s, gx, gy, gz);
+      sGX[base + q] = gx;
+      sGY[base + q] = gy;
+#pragma unroll
+      for (int i = 0; i < N; ++i) az[i] = fma(T.D[i * N + q], gz, az[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) sU[base + i] = az[i];
+  }
+  __syncthreads();
+
+  // ---- phase 4: x-lines (y=a, z=b): U += Dx^T f_x ----------------------
+  if (act) {
+    double fl[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) fl[q] = sGX[cb + q * SX + a * SY + b];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double s = T.D[i * N] * fl[0];
+#pragma unroll
+      for (int q = 1; q < N; ++q) s = fma(T.D[i * N + q], fl[q], s);
+      sU[cb + i * SX + a * SY + b] += s;
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 5: y-lines (x=a, z=b): U += Dy^T f_y ----------------------
+  if (act) {
+    double fl[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) fl[q] = sGY[cb + a * SX + q * SY + b];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double s = T.D[i * N] * fl[0];
+#pragma unroll
+      for (int q = 1; q < N; ++q) s = fma(T.D[i * N + q], fl[q], s);
+      sU[cb + a * SX + i * SY + b] += s;
+    }
+  }
+  __syncthreads();
+
+  {
+    double* ag = A + cell0 * N3;
+    for (int i = tid; i < ncb * N3; i += C::THREADS) {
+      const int cc = i / N3, rr = i - cc * N3;
+      const int x = rr / NN, y = (rr / N) % N, z = rr % N;
+      ag[i] = sU[cc * CS + x * SX + y * SY + z];
+    }
+  }
+}
+
+template <int N, int CPB, int SY, int SX, int CS>
+static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                    const double* u, const double* kappa, cudaStream_t s) {
+  using C = CollocCfg<N, CPB, SY, SX, CS>;
+  TabsD<N> T;
+  for (int i = 0; i < N * N; ++i) T.D[i] = p->D[i];
+  for (int q = 0; q < N; ++q) {
+    T.W[q] = p->wq[q];
+    T.Bc[q] = p->Bc[q];
+    T.Bc[N + q] = p->Bc[N + q];
+  }
+  const int64_t grid = (ncells + CPB - 1) / CPB;
+  cudaError_t e;
+  if (kappa) {
+    auto k = hex_colloc_action_kernel<N, CPB, SY, SX, CS, true>;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
+    k<<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, u, kappa, A);
+  } else {
+    auto k = hex_colloc_action_kernel<N, CPB, SY, SX, CS, false>;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
+    k<<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, u, nullptr, A);
+  }
+  note_launch();
+  return cuda_status(cudaGetLastError(), "hex_colloc_action_kernel launch");
+}
+
+int launch_hex_colloc_action(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                             const double* w0, const double* w1, cudaStream_t s) {
+  if (p->n != p->m)
+    return fail(SFK_EINVAL, "collocated action needs n_q1d == n_dof1d (got %d, %d)", p->n, p->m);
+  // (N, cells/CTA, SY, SX, CS) from tools/smem_pads.py
+  switch (p->n) {
+    case 2: return launch_n<2, 16, 2, 5, 12>(p, ncells, A, coords, w0, w1, s);
+    case 3: return launch_n<3, 16, 3, 9, 27>(p, ncells, A, coords, w0, w1, s);
+    case 4: return launch_n<4, 8, 4, 19, 76>(p, ncells, A, coords, w0, w1, s);
+    case 5: return launch_n<5, 10, 5, 25, 125>(p, ncells, A, coords, w0, w1, s);
+    case 6: return launch_n<6, 8, 6, 39, 244>(p, ncells, A, coords, w0, w1, s);
+    case 7: return launch_n<7, 5, 7, 52, 369>(p, ncells, A, coords, w0, w1, s);
+    case 8: return launch_n<8, 4, 9, 72, 576>(p, ncells, A, coords, w0, w1, s);
+    case 9: return launch_n<9, 3, 9, 89, 801>(p, ncells, A, coords, w0, w1, s);
+    case 10: return launch_n<10, 3, 11, 110, 1100>(p, ncells, A, coords, w0, w1, s);
+    case 11: return launch_n<11, 2, 11, 123, 1353>(p, ncells, A, coords, w0, w1, s);
+    case 12: return launch_n<12, 2, 13, 156, 1872>(p, ncells, A, coords, w0, w1, s);
+    case 13: return launch_n<13, 1, 13, 169, 2197>(p, ncells, A, coords, w0, w1, s);
+    case 14: return launch_n<14, 1, 17, 238, 3332>(p, ncells, A, coords, w0, w1, s);
+    case 15: return launch_n<15, 1, 15, 225, 3375>(p, ncells, A, coords, w0, w1, s);
+    case 16: return launch_n<16, 1, 17, 272, 4352>(p, ncells, A, coords, w0, w1, s);
+    case 17: return launch_n<17, 1, 17, 289, 4913>(p, ncells, A, coords, w0, w1, s);
+    default:
+      return fail(SFK_EUNSUPPORTED, "collocated hex action: n=%d outside [2,17]", p->n);
+  }
+}
+
+}  // namespace sfk

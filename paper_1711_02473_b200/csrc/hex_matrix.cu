@@ -1,0 +1,212 @@
+// Hex Q_p local stiffness matrices — BASELINE config C5 (p = 1..4).
+//
+// Reference: registry `laplace` on `hex` (forms.py:186-189), rank 2, test
+// index outermost: A[i*N3 + j] (forms.py:402-408); the
+// spectral-mode program is sum-factorised to O(n^7) (SURVEY.md §8(a),
+// reference count 15n^7 + 27n^6 + ...).
+//
+//   A[i][j] = sum_q sum_{l,l'} dphi_i^l(q) K_q[l][l'] dphi_j^l'(q),
+//   K_q = w_q |J| G G^T = (w_q/|det|) R R^T  (R = adjugate rows),
+//   dphi^l = T^l_x (x) T^l_y (x) T^l_z, T^l_d = D if d == l else B.
+//
+// Factorisation used here, for every quadrature plane qx (outer loop):
+//   Z_ll'[qy][iz][jz]      = sum_qz T^l_z[iz][qz] T^l'_z[jz][qz] K_ll'(qx,qy,qz)
+//   Y_g[iy][jy][iz][jz]    = sum_{(l,l') in g} sum_qy T^l_y[iy][qy] T^l'_y[jy][qy] Z_ll'
+//   A[ix,jx][...]         += sum_g T^l_x[ix][qx] T^l'_x[jx][qx] Y_g
+// where g groups the 9 (l,l') pairs by their x-table pattern (BB, BD, DB,
+// DD): 4 x-contractions instead of 9.  Per cell ~ 9 m^3 n^2 + 9 m^2 n^4 +
+// 4 m n^6 FMA (p=4: 0.48 M FMA vs the reference's 1.69 M flops).
+//
+// B200 mapping: one thread per (iy, iz, jy, jz) (n^4 threads per cell) owns
+// the n^2 outputs A[(ix,iy,iz),(jx,jy,jz)] in registers across the qx loop;
+// Y_g never leaves registers.  K and Z for the current plane live in shared
+// memory.  Output rows are written straight from registers: for fixed
+// (ix, jx) a warp stores runs of n^2 contiguous doubles; the 125 KB (p=4)
+// of a cell is complete in L2 before eviction, so DRAM sees full lines.
+#include "hex_geometry.cuh"
+
+namespace sfk {
+
+template <int N, int M>
+struct TabsMat {
+  double B[N * M];
+  double D[N * M];
+  double W[M];
+  double Bc[2 * M];
+};
+
+template <int N, int M, int CPB>
+struct MatCfg {
+  static constexpr int N2 = N * N, N3 = N * N * N, N4 = N * N * N * N;
+  static constexpr int THREADS = round_up(CPB * N4, 32);
+  static constexpr int ZS = 9 * M * N2;     // Z for one cell and one plane
+  static constexpr int KS = 6 * M * M;      // K (6 unique entries) for one plane
+  static constexpr int TS = 2 * N * M;      // B and D copies (runtime-indexed reads)
+};
+
+// pair (l, l') -> symmetric K index: 00 11 22 01 02 12
+__host__ __device__ constexpr int ksym(int l, int r) {
+  return l == r ? l : (l + r == 1 ? 3 : (l + r == 2 ? 4 : 5));
+}
+
+template <int N, int M, int CPB>
+__global__ void __launch_bounds__(MatCfg<N, M, CPB>::THREADS)
+hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncells,
+                          const double* __restrict__ coords, double* __restrict__ A) {
+  using C = MatCfg<N, M, CPB>;
+  constexpr int N2 = C::N2, N3 = C::N3, N4 = C::N4;
+  __shared__ double sZ[CPB * C::ZS];
+  __shared__ double sK[CPB * C::KS];
+  __shared__ double sT[C::TS];
+  __shared__ double sC[CPB * 24];
+  const int tid = threadIdx.x;
+  const int64_t cell0 = (int64_t)blockIdx.x * CPB;
+  const int64_t rem = ncells - cell0;
+  const int ncb = rem < CPB ? (int)rem : CPB;
+  for (int i = tid; i < CPB * 24; i += C::THREADS)
+    sC[i] = i < ncb * 24 ? __ldg(coords + cell0 * 24 + i) : 0.0;
+  for (int i = tid; i < N * M; i += C::THREADS) {
+    sT[i] = T.B[i];
+    sT[N * M + i] = T.D[i];
+  }
+  // thread -> (cell, iy, iz, jy, jz)
+  const bool act = tid < CPB * N4;
+  const int c = tid / N4, r = tid - (tid / N4) * N4;
+  const int iy = r / (N * N2), iz = (r / N2) % N, jy = (r / N) % N, jz = r % N;
+  double acc[N][N];
+#pragma unroll
+  for (int ix = 0; ix < N; ++ix)
+#pragma unroll
+    for (int jx = 0; jx < N; ++jx) acc[ix][jx] = 0.0;
+  __syncthreads();
+  // y products for this thread's (iy, jy): pattern (a, b) in {B,D}^2
+  double py[4][M];
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    const double bi = sT[iy * M + q], di = sT[N * M + iy * M + q];
+    const double bj = sT[jy * M + q], dj = sT[N * M + jy * M + q];
+    py[0][q] = bi * bj;
+    py[1][q] = bi * dj;
+    py[2][q] = di * bj;
+    py[3][q] = di * dj;
+  }
+
+#pragma unroll
+  for (int qx = 0; qx < M; ++qx) {
+    // ---- K at the plane qx: threads over (cell, qy, qz) ------------------
+    for (int t = tid; t < CPB * M * M; t += C::THREADS) {
+      const int cc = t / (M * M), rr = t - cc * (M * M);
+      const int qy = rr / M, qz = rr - qy * M;
+      HexLineGeom geo;  // line (qx, qy, *) evaluated at qz
+      geo.setup(sC + cc * 24, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
+      double r0[3], r1[3], r2[3];
+      const double det = geo.adj(T.Bc[qz], T.Bc[M + qz], r0, r1, r2);
+      const double s = ((T.W[qx] * T.W[qy]) * T.W[qz]) * rcp64(fabs(det));
+      double* k = sK + cc * C::KS + rr;
+      const double* rows[3] = {r0, r1, r2};
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int m2 = l; m2 < 3; ++m2) {
+          const double* a = rows[l];
+          const double* b = rows[m2];
+          k[ksym(l, m2) * M * M] = s * fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0]));
+        }
+    }
+    __syncthreads();
+    // ---- Z_ll'[qy][iz][jz] for the plane: threads over (cell, pair, qy, iz, jz)
+    for (int t = tid; t < CPB * C::ZS; t += C::THREADS) {
+      const int cc = t / C::ZS, rr = t - cc * C::ZS;
+      const int pair = rr / (M * N2), q2 = rr - pair * (M * N2);
+      const int qy = q2 / N2, zz = q2 - qy * N2;
+      const int a = zz / N, b = zz - a * N;
+      const int l = pair / 3, lp = pair - 3 * l;
+      const double* ta = sT + (l == 2 ? N * M : 0) + a * M;
+      const double* tb = sT + (lp == 2 ? N * M : 0) + b * M;
+      const double* k = sK + cc * C::KS + ksym(l, lp) * M * M + qy * M;
+      double z = 0.0;
+#pragma unroll
+      for (int qz = 0; qz < M; ++qz) z = fma(ta[qz] * tb[qz], k[qz], z);
+      sZ[cc * C::ZS + rr] = z;
+    }
+    __syncthreads();
+    // ---- y contraction into the 4 x-pattern groups, then x accumulation --
+    if (act) {
+      const double* z = sZ + c * C::ZS + iz * N + jz;
+      double yg[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int lp = 0; lp < 3; ++lp) {
+          const int pat = (l == 1 ? 2 : 0) + (lp == 1 ? 1 : 0);
+          const int grp = (l == 0 ? 2 : 0) + (lp == 0 ? 1 : 0);
+          const double* zp = z + (l * 3 + lp) * M * N2;
+#pragma unroll
+          for (int qy = 0; qy < M; ++qy) yg[grp] = fma(py[pat][qy], zp[qy * N2], yg[grp]);
+        }
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const double* ta = (g & 2) ? T.D : T.B;  // test  (row) x-table
+        const double* tb = (g & 1) ? T.D : T.B;  // trial (col) x-table
+#pragma unroll
+        for (int jx = 0; jx < N; ++jx) {
+          const double t = tb[jx * M + qx] * yg[g];
+#pragma unroll
+          for (int ix = 0; ix < N; ++ix) acc[ix][jx] = fma(ta[ix * M + qx], t, acc[ix][jx]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  if (act && c < ncb) {
+    double* out = A + (cell0 + c) * (int64_t)(N3 * N3);
+    const int rowoff = iy * N + iz;   // + ix * N2  -> test index
+    const int coloff = jy * N + jz;   // + jx * N2  -> trial index
+#pragma unroll
+    for (int ix = 0; ix < N; ++ix)
+#pragma unroll
+      for (int jx = 0; jx < N; ++jx)
+        out[(int64_t)(ix * N2 + rowoff) * N3 + jx * N2 + coloff] = acc[ix][jx];
+  }
+}
+
+template <int N, int M, int CPB>
+static int launch_mat(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                      cudaStream_t s) {
+  using C = MatCfg<N, M, CPB>;
+  TabsMat<N, M> T;
+  for (int i = 0; i < N; ++i)
+    for (int q = 0; q < M; ++q) {
+      T.B[i * M + q] = p->B[i * p->m + q];
+      T.D[i * M + q] = p->D[i * p->m + q];
+    }
+  for (int q = 0; q < M; ++q) {
+    T.W[q] = p->wq[q];
+    T.Bc[q] = p->Bc[q];
+    T.Bc[M + q] = p->Bc[p->m + q];
+  }
+  const unsigned grid = (unsigned)((ncells + CPB - 1) / CPB);
+  hex_laplace_matrix_kernel<N, M, CPB><<<grid, C::THREADS, 0, s>>>(T, ncells, coords, A);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "hex_laplace_matrix_kernel launch");
+}
+
+int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                      cudaStream_t s) {
+  if (p->collocated)
+    return fail(SFK_EUNSUPPORTED, "hex laplace matrix: collocated variant not instantiated");
+  if (p->n == p->m) {
+    switch (p->n) {
+      case 2: return launch_mat<2, 2, 16>(p, ncells, A, coords, s);
+      case 3: return launch_mat<3, 3, 3>(p, ncells, A, coords, s);
+      case 4: return launch_mat<4, 4, 1>(p, ncells, A, coords, s);
+      case 5: return launch_mat<5, 5, 1>(p, ncells, A, coords, s);
+      default: break;
+    }
+  }
+  return fail(SFK_EUNSUPPORTED,
+              "hex laplace matrix: no kernel for n=%d, m=%d (n==m in 2..5, p<=4)", p->n, p->m);
+}
+
+}  // namespace sfk

@@ -1,0 +1,314 @@
+// Hex Q_p^3 compressible neo-Hookean residual — BASELINE config C4
+// (p = 2..6, GL (p+2)^3, mu = 1, lambda = 10).
+//
+// Reference: not in the reference registry; the
+// builder-supplied FormSpec of SURVEY.md §8(a) row a17, lowered by
+// forms.lower_form with a vector Q_p test space (elements.py:425-452: dof
+// ((ix*n+iy)*n+iz)*3 + comp) and the displacement as coefficient slot 0
+// with first derivatives (forms.py:326-350):
+//   F = I + grad u,  J = det F,  F^-T = cof(F) / J,
+//   P = mu (F - F^-T) + lambda ln(J) F^-T,
+//   r[(i, a)] = sum_q w_q |det Jg| sum_k P[a][k] (grad phi_i)_k .
+// The same 8 + 8 contraction schedule as the scalar Laplace action is run
+// per displacement component (3 x 8 forward, 3 x 8 transposed), with m =
+// n + 1 points per axis.
+//
+// B200 mapping: the scalar line kernel (hex_action.cu) extended to three
+// components.  The forward x/y stages run component by component through a
+// shared X buffer into a 9-array Y buffer whose z-lines are stored with a
+// stride >= m, so that each z-line thread can overwrite, in place, its own
+// 9 lines with (1) the 9 reference-gradient lines, (2) the 9 flux lines and
+// (3) the 9 transposed-z lines — no extra shared memory and no barrier
+// between those three steps.  Transposed y/x stages then run per component.
+#include "hex_geometry.cuh"
+
+namespace sfk {
+
+template <int N, int M, int CPB>
+struct NeoCfg {
+  static constexpr int NN = N * N, MN = M * N, MM = M * M;
+  static constexpr int THREADS = round_up(CPB * MM, 32);
+  static constexpr int PX = NN | 1;
+  static constexpr int LZ = M | 1;             // z-line stride (>= m, odd)
+  static constexpr int XA = M * PX;            // one X/R array per cell
+  static constexpr int XSZ = 2 * XA;
+  static constexpr int YA = MM * LZ;           // one Y array per cell
+  static constexpr int YSZ = 9 * YA;
+  static constexpr size_t SMEM = (size_t)CPB * (XSZ + YSZ + 24) * sizeof(double);
+};
+
+template <int N, int M, int CPB>
+__global__ void __launch_bounds__(NeoCfg<N, M, CPB>::THREADS)
+hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double lam,
+                      int64_t ncells, const double* __restrict__ coords,
+                      const double* __restrict__ u, double* __restrict__ A) {
+  using C = NeoCfg<N, M, CPB>;
+  constexpr int NN = C::NN, MN = C::MN, MM = C::MM, PX = C::PX, LZ = C::LZ;
+  constexpr int XA = C::XA, YA = C::YA;
+  constexpr int N3 = N * NN;
+  extern __shared__ double smem[];
+  double* sX = smem;
+  double* sY = sX + CPB * C::XSZ;
+  double* sC = sY + CPB * C::YSZ;
+  const int tid = threadIdx.x;
+  const int64_t cell0 = (int64_t)blockIdx.x * CPB;
+  const int64_t rem = ncells - cell0;
+  const int ncb = rem < CPB ? (int)rem : CPB;
+  for (int i = tid; i < CPB * 24; i += C::THREADS)
+    sC[i] = i < ncb * 24 ? __ldg(coords + cell0 * 24 + i) : 0.0;
+
+  // ---------------- forward x / y stages, per component -------------------
+#pragma unroll 1
+  for (int a = 0; a < 3; ++a) {
+    if (tid < CPB * NN) {
+      const int c = tid / NN, r = tid - c * NN;
+      double uu[N];
+      const double* up = u + (cell0 + c) * (3 * N3) + 3 * r + a;
+#pragma unroll
+      for (int i = 0; i < N; ++i) uu[i] = c < ncb ? __ldg(up + 3 * i * NN) : 0.0;
+      double* xo = sX + c * C::XSZ + r;
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        double b = T.B[q] * uu[0], d = T.D[q] * uu[0];
+#pragma unroll
+        for (int i = 1; i < N; ++i) {
+          b = fma(T.B[i * M + q], uu[i], b);
+          d = fma(T.D[i * M + q], uu[i], d);
+        }
+        xo[q * PX] = b;
+        xo[XA + q * PX] = d;
+      }
+    }
+    __syncthreads();
+    if (tid < CPB * MN) {
+      const int c = tid / MN, r = tid - c * MN;
+      const int qx = r / N, iz = r - qx * N;
+      const double* xi = sX + c * C::XSZ + qx * PX + iz;
+      double a0[N], a1[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        a0[i] = xi[i * N];
+        a1[i] = xi[XA + i * N];
+      }
+      double* yo = sY + c * C::YSZ + 3 * a * YA + qx * M * LZ + iz;
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        double bb = T.B[q] * a0[0], bd = T.D[q] * a0[0], db = T.B[q] * a1[0];
+#pragma unroll
+        for (int i = 1; i < N; ++i) {
+          bb = fma(T.B[i * M + q], a0[i], bb);
+          bd = fma(T.D[i * M + q], a0[i], bd);
+          db = fma(T.B[i * M + q], a1[i], db);
+        }
+        yo[q * LZ] = bb;         // -> d/dz after z stage
+        yo[YA + q * LZ] = bd;    // -> d/dy
+        yo[2 * YA + q * LZ] = db;  // -> d/dx
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---------------- z-lines: gradients, constitutive flux, transposed z ----
+  if (tid < CPB * MM) {
+    const int c = tid / MM, r = tid - c * MM;
+    const int qx = r / M, qy = r - qx * M;
+    double* line = sY + c * C::YSZ + r * LZ;   // component a, slot k: line[(3a+k)*YA + .]
+    // (1) reference gradients, in place: slots (0,1,2) <- (d_z, d_y, d_x)
+#pragma unroll 1
+    for (int a = 0; a < 3; ++a) {
+      double bb[N], bd[N], db[N];
+      double* l0 = line + 3 * a * YA;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        bb[i] = l0[i];
+        bd[i] = l0[YA + i];
+        db[i] = l0[2 * YA + i];
+      }
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        double gz = T.D[q] * bb[0], gy = T.B[q] * bd[0], gx = T.B[q] * db[0];
+#pragma unroll
+        for (int i = 1; i < N; ++i) {
+          gz = fma(T.D[i * M + q], bb[i], gz);
+          gy = fma(T.B[i * M + q], bd[i], gy);
+          gx = fma(T.B[i * M + q], db[i], gx);
+        }
+        l0[q] = gz;
+        l0[YA + q] = gy;
+        l0[2 * YA + q] = gx;
+      }
+    }
+    // (2) pointwise neo-Hookean flux, in place
+    HexLineGeom geo;
+    geo.setup(sC + c * 24, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
+    const double wxy = T.W[qx] * T.W[qy];
+#pragma unroll 1
+    for (int q = 0; q < M; ++q) {
+      double rr[3][3];
+      const double det = geo.adj(T.Bc[q], T.Bc[M + q], rr[0], rr[1], rr[2]);
+      const double idet = rcp64(det);
+      // grad u_a [k] = (1/det) sum_l r_l[k] d_l u_a ;  F = I + grad u
+      double F[3][3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double g0 = line[(3 * a + 2) * YA + q];  // d_x
+        const double g1 = line[(3 * a + 1) * YA + q];  // d_y
+        const double g2 = line[(3 * a + 0) * YA + q];  // d_z
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          F[a][k] = fma(fma(g2, rr[2][k], fma(g1, rr[1][k], g0 * rr[0][k])), idet,
+                        a == k ? 1.0 : 0.0);
+      }
+      double cof[3][3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int a1 = (a + 1) % 3, a2 = (a + 2) % 3, k1 = (k + 1) % 3, k2 = (k + 2) % 3;
+          cof[a][k] = fma(F[a1][k1], F[a2][k2], -(F[a1][k2] * F[a2][k1]));
+        }
+      const double Jf = fma(F[0][2], cof[0][2], fma(F[0][1], cof[0][1], F[0][0] * cof[0][0]));
+      const double iJ = rcp64(Jf);
+      // P = mu F + (lambda ln J - mu) / J * cof(F)
+      const double beta = (lam * log(Jf) - mu) * iJ;
+      // flux f_a[l] = w sign(det) sum_k r_l[k] P[a][k]
+      const double s = (wxy * T.W[q]) * (det < 0.0 ? -1.0 : 1.0);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double P[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) P[k] = fma(mu, F[a][k], beta * cof[a][k]);
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+          const double f = s * fma(rr[l][2], P[2], fma(rr[l][1], P[1], rr[l][0] * P[0]));
+          line[(3 * a + 2 - l) * YA + q] = f;   // slot 2 = x, 1 = y, 0 = z
+        }
+      }
+    }
+    // (3) transposed z, in place: slot 2 <- Bz^T f_x, 1 <- Bz^T f_y, 0 <- Dz^T f_z
+#pragma unroll 1
+    for (int a = 0; a < 3; ++a) {
+      double fz[M], fy[M], fx[M];
+      double* l0 = line + 3 * a * YA;
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        fz[q] = l0[q];
+        fy[q] = l0[YA + q];
+        fx[q] = l0[2 * YA + q];
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double sz = T.D[i * M] * fz[0], sy = T.B[i * M] * fy[0], sx = T.B[i * M] * fx[0];
+#pragma unroll
+        for (int q = 1; q < M; ++q) {
+          sz = fma(T.D[i * M + q], fz[q], sz);
+          sy = fma(T.B[i * M + q], fy[q], sy);
+          sx = fma(T.B[i * M + q], fx[q], sx);
+        }
+        l0[i] = sz;
+        l0[YA + i] = sy;
+        l0[2 * YA + i] = sx;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---------------- transposed y / x stages, per component ---------------
+#pragma unroll 1
+  for (int a = 0; a < 3; ++a) {
+    if (tid < CPB * MN) {
+      const int c = tid / MN, r = tid - c * MN;
+      const int qx = r / N, iz = r - qx * N;
+      const double* yi = sY + c * C::YSZ + 3 * a * YA + qx * M * LZ + iz;
+      double pz[M], py[M], px[M];
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        pz[q] = yi[q * LZ];
+        py[q] = yi[YA + q * LZ];
+        px[q] = yi[2 * YA + q * LZ];
+      }
+      double* xo = sX + c * C::XSZ + qx * PX + iz;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double r1 = T.B[i * M] * px[0];
+        double r2 = fma(T.D[i * M], py[0], T.B[i * M] * pz[0]);
+#pragma unroll
+        for (int q = 1; q < M; ++q) {
+          r1 = fma(T.B[i * M + q], px[q], r1);
+          r2 = fma(T.D[i * M + q], py[q], r2);
+          r2 = fma(T.B[i * M + q], pz[q], r2);
+        }
+        xo[i * N] = r1;
+        xo[XA + i * N] = r2;
+      }
+    }
+    __syncthreads();
+    if (tid < CPB * NN) {
+      const int c = tid / NN, r = tid - c * NN;
+      if (c < ncb) {
+        const double* xi = sX + c * C::XSZ + r;
+        double p1[M], p2[M];
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+          p1[q] = xi[q * PX];
+          p2[q] = xi[XA + q * PX];
+        }
+        double* ap = A + (cell0 + c) * (3 * N3) + 3 * r + a;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double v = fma(T.D[i * M], p1[0], T.B[i * M] * p2[0]);
+#pragma unroll
+          for (int q = 1; q < M; ++q) {
+            v = fma(T.D[i * M + q], p1[q], v);
+            v = fma(T.B[i * M + q], p2[q], v);
+          }
+          ap[3 * i * NN] = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int N, int M, int CPB>
+static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                      const double* u, cudaStream_t s) {
+  using C = NeoCfg<N, M, CPB>;
+  auto k = hex_neohookean_kernel<N, M, CPB>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)C::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(neohookean)");
+  const Tabs<N, M> T = make_tabs<N, M>(p);
+  const unsigned grid = (unsigned)((ncells + CPB - 1) / CPB);
+  k<<<grid, C::THREADS, C::SMEM, s>>>(T, p->params[0], p->params[1], ncells, coords, u, A);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "hex_neohookean_kernel launch");
+}
+
+int launch_hex_neohookean(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                          const double* w0, cudaStream_t s) {
+  const int n = p->n, m = p->m;
+  if (m == n + 1) {
+    switch (n) {
+      case 2: return launch_neo<2, 3, 16>(p, ncells, A, coords, w0, s);
+      case 3: return launch_neo<3, 4, 16>(p, ncells, A, coords, w0, s);
+      case 4: return launch_neo<4, 5, 8>(p, ncells, A, coords, w0, s);
+      case 5: return launch_neo<5, 6, 4>(p, ncells, A, coords, w0, s);
+      case 6: return launch_neo<6, 7, 4>(p, ncells, A, coords, w0, s);
+      case 7: return launch_neo<7, 8, 2>(p, ncells, A, coords, w0, s);
+      default: break;
+    }
+  } else if (m == n) {
+    switch (n) {
+      case 2: return launch_neo<2, 2, 16>(p, ncells, A, coords, w0, s);
+      case 3: return launch_neo<3, 3, 16>(p, ncells, A, coords, w0, s);
+      case 4: return launch_neo<4, 4, 8>(p, ncells, A, coords, w0, s);
+      default: break;
+    }
+  }
+  return fail(SFK_EUNSUPPORTED,
+              "neo-Hookean residual: no kernel for n=%d, m=%d (m==n+1 in 2..7 or m==n in 2..4)",
+              n, m);
+}
+
+}  // namespace sfk

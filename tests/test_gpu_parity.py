@@ -129,3 +129,130 @@ def test_sum_squares_and_launch_counter(cuda):
     assert abs(s[1] - xn.sum()) < 1e-9
     s2 = sum_squares(x).cpu().numpy()
     assert np.array_equal(s, s2)   # bitwise reproducible
+
+
+# ---------------------------------------------------------------------------
+# C3: GLL-collocated (weighted) Laplace action
+
+from paper_1711_02473_b200 import (REGISTRY, action_form, compile_form,  # noqa: E402
+                                   evaluate_batched_pair, neohookean_residual_form)
+
+
+def _c3_plan(p, weighted=True):
+    if weighted:
+        return compile_form(action_form(REGISTRY["weighted_laplace"]), "hex", p, "spectral",
+                            "spectral_gll", "collocated-gll")
+    return compile_kernel("action_laplace", "hex", p, "spectral", "spectral_gll",
+                          "collocated-gll")
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 6, 8, 12, 16])
+def test_c3_golden(cuda, p):
+    g = np.load(os.path.join(GOLDEN, "c3.npz"))
+    inp = {"coords": g["coords"], "w0": g["w0_p%d" % p], "w1": g["w1_p%d" % p]}
+    assert rel_err(_run(cuda, _c3_plan(p), inp), g["A_p%d" % p]) < TOL
+    lap = {"coords": g["coords"], "w0": g["w0_p%d" % p]}
+    assert rel_err(_run(cuda, _c3_plan(p, False), lap), g["Alap_p%d" % p]) < TOL
+
+
+@pytest.mark.parametrize("p", range(1, 17))
+def test_c3_vs_oracle(cuda, p):
+    plan = _c3_plan(p)
+    n = p + 1
+    nc = 37
+    inp = {"coords": workloads.lattice_coords(4, 4, 4)[:nc],
+           "w0": workloads.uniform_dofs(nc, n ** 3),
+           "w1": workloads.uniform_dofs(nc, n ** 3, 0.5, 2.0, seed=workloads.SEED_KAPPA)}
+    assert rel_err(_run(cuda, plan, inp), cpu.evaluate(plan, inp)) < TOL
+
+
+# ---------------------------------------------------------------------------
+# C1: quad Q3 mass + Laplace action (fused pair)
+
+
+def test_c1_golden_and_fused_pair(cuda):
+    torch = cuda
+    g = np.load(os.path.join(GOLDEN, "c1.npz"))
+    pm = compile_kernel("action_mass", "quad", 3)
+    pl = compile_kernel("action_laplace", "quad", 3)
+    inp = {"coords": g["coords"], "w0": g["w0"]}
+    assert rel_err(_run(torch, pm, inp), g["A_action_mass"]) < TOL
+    assert rel_err(_run(torch, pl, inp), g["A_action_laplace"]) < TOL
+    full = workloads.c1_inputs()
+    am, al = evaluate_batched_pair(pm, pl, _dev(torch, full))
+    assert rel_err(am.cpu().numpy(), cpu.evaluate(pm, full)) < TOL
+    assert rel_err(al.cpu().numpy(), cpu.evaluate(pl, full)) < TOL
+    # fused == separate, bit for bit is not required; parity is
+    assert rel_err(am.cpu().numpy(), _run(torch, pm, full)) < 1e-14
+
+
+@pytest.mark.parametrize("p", range(1, 9))
+def test_quad_actions_vs_oracle(cuda, p):
+    nc = 45
+    inp = {"coords": workloads.quad_coords(nc), "w0": workloads.uniform_dofs(nc, (p + 1) ** 2)}
+    for form in ("action_mass", "action_laplace"):
+        plan = compile_kernel(form, "quad", p)
+        assert rel_err(_run(cuda, plan, inp), cpu.evaluate(plan, inp)) < TOL
+
+
+# ---------------------------------------------------------------------------
+# C5: hex Laplace local matrices
+
+
+@pytest.mark.parametrize("p", range(1, 5))
+def test_c5_golden_and_properties(cuda, p):
+    g = np.load(os.path.join(GOLDEN, "c5.npz"))
+    plan = compile_kernel("laplace", "hex", p)
+    assert rel_err(_run(cuda, plan, {"coords": g["coords"]}), g["A_p%d" % p]) < TOL
+    coords = workloads.lattice_coords(4, 4, 3)[:41]
+    A = _run(cuda, plan, {"coords": coords})
+    assert rel_err(A, cpu.evaluate(plan, {"coords": coords})) < TOL
+    nd = (p + 1) ** 3
+    M = A.reshape(-1, nd, nd)
+    scale = np.abs(M).max()
+    assert np.abs(M.sum(axis=2)).max() < 1e-12 * scale           # patch test
+    assert np.abs(M - M.transpose(0, 2, 1)).max() < 1e-13 * scale  # symmetry
+    # matrix/action consistency
+    u = workloads.uniform_dofs(coords.shape[0], nd)
+    act = _run(cuda, compile_kernel("action_laplace", "hex", p), {"coords": coords, "w0": u})
+    assert rel_err(np.einsum("cij,cj->ci", M, u), act) < 1e-12
+
+
+def test_c5_reference_cell_analytic(cuda):
+    g = np.load(os.path.join(GOLDEN, "c5.npz"))
+    M1 = np.array([[1 / 3, 1 / 6], [1 / 6, 1 / 3]])
+    K1 = np.array([[1.0, -1.0], [-1.0, 1.0]])
+    expect = (np.kron(np.kron(K1, M1), M1) + np.kron(np.kron(M1, K1), M1)
+              + np.kron(np.kron(M1, M1), K1))
+    A = _run(cuda, compile_kernel("laplace", "hex", 1), {"coords": g["ref_coords"]})
+    assert np.abs(A.reshape(8, 8) - expect).max() < 1e-14
+
+
+# ---------------------------------------------------------------------------
+# C4: neo-Hookean residual
+
+
+@pytest.mark.parametrize("p", range(1, 7))
+def test_c4_golden(cuda, p):
+    g = np.load(os.path.join(GOLDEN, "c4.npz"))
+    plan = compile_form(neohookean_residual_form(), "hex", p, quadrature=p + 2)
+    for s in ("", "b"):
+        inp = {"coords": g["coords"], "w0": g["w0%s_p%d" % (s, p)]}
+        ref = g["A%s_p%d" % (s, p)]
+        out = _run(cuda, plan, inp)
+        assert np.array_equal(np.isnan(out), np.isnan(ref))
+        ok = ~np.isnan(ref).any(axis=1)
+        if ok.any():
+            assert rel_err(out[ok], ref[ok]) < TOL
+
+
+@pytest.mark.parametrize("p", range(2, 7))
+def test_c4_vs_oracle(cuda, p):
+    plan = compile_form(neohookean_residual_form(), "hex", p, quadrature=p + 2)
+    inp = workloads.c4_inputs(p, dims=(2, 4, 5))
+    with np.errstate(invalid="ignore"):
+        ref = cpu.evaluate(plan, inp)
+    out = _run(cuda, plan, inp)
+    assert np.array_equal(np.isnan(out), np.isnan(ref))
+    ok = ~np.isnan(ref).any(axis=1)
+    assert rel_err(out[ok], ref[ok]) < TOL

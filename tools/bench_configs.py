@@ -1,0 +1,181 @@
+#!/usr/bin/env python
+"""Per-config measurements of every BASELINE config (C1..C5) on one B200.
+
+    python tools/bench_configs.py [C1 C2 C3 C4 C5] [--reps 5] [--cpu-cells 4096]
+
+For each config and degree: device time of one sfk_eval over the full
+BASELINE batch (CUDA events on the launching stream, L2 flushed between
+repetitions, median of --reps), GDoF/s, cells/s, the roofline fraction
+(max(bytes/HBM, F_alg/P64) / t, P64 measured live), and the CPU baseline
+(the reference's emitted C from oracle/_ref over all host cores, or the
+oracle port) on a bounded sample of the same batch.  One JSON line per
+(config, degree); the headline C2 line with the full contract is bench.py.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="*", default=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--cpu-cells", type=int, default=4096)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    import torch
+
+    from oracle import cpu, refc
+    from paper_1711_02473_b200 import (REGISTRY, action_form, compile_form, compile_kernel,
+                                       neohookean_residual_form, runtime, workloads)
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    lib = runtime.load_library()
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    dfma, dmma = runtime.fp64_peak(0.5)
+    p64 = max(dfma, dmma)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    hbm = peaks.get("hbm_gbs", 6650.0)
+
+    def time_launch(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(args.reps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        return statistics.median(ts)
+
+    def cpu_time(plan, inputs, n):
+        if args.no_cpu:
+            return None
+        sample = {k: v[:n] for k, v in inputs.items()}
+        kind = "reference" if refc.available(plan) else "port"
+        ev = refc.evaluate if kind == "reference" else cpu.evaluate
+        ev(plan, {k: v[:16] for k, v in sample.items()})
+        best = 1e30
+        with np.errstate(invalid="ignore"):
+            for _ in range(2):
+                t0 = time.perf_counter()
+                ev(plan, sample)
+                best = min(best, time.perf_counter() - t0)
+        cores = refc.threads(plan) if kind == "reference" else cpu.num_threads()
+        return {"s_per_cell": best / n, "kind": kind, "cores": cores, "sample_cells": n}
+
+    def report(cfg, plan, inputs, dofs_per_cell, fn, extra=None, cpu_plan=None):
+        ncells = inputs["coords"].shape[0]
+        t = time_launch(fn)
+        F = plan.algorithmic_flops
+        Bb = plan.compulsory_bytes if extra is None else extra
+        t_roof = ncells * max(Bb / (hbm * 1e9), (F or 0) / (p64 * 1e12))
+        rec = {"config": cfg, "form": plan.name, "p": plan.degree, "cells": ncells,
+               "ms": round(t * 1e3, 5), "gdofs": round(ncells * dofs_per_cell / t / 1e9, 3),
+               "cells_per_s": round(ncells / t, 1), "flops_per_cell_alg": F,
+               "bytes_per_cell": Bb,
+               "fp64_tflops_alg": round(ncells * F / t / 1e12, 3) if F else None,
+               "hbm_gbs": round(ncells * Bb / t / 1e9, 1),
+               "roofline_frac": round(t_roof / t, 4) if F else None,
+               "bound": ("fp64" if F and F / (p64 * 1e12) > Bb / (hbm * 1e9) else "hbm"),
+               "p64_tflops": round(p64, 2), "hbm_peak_gbs": hbm}
+        c = cpu_time(cpu_plan or plan, inputs, min(args.cpu_cells, ncells))
+        if c:
+            rec["cpu_baseline"] = {"gdofs": round(dofs_per_cell / c["s_per_cell"] / 1e9, 5),
+                                   "cells_per_s": round(1 / c["s_per_cell"], 1),
+                                   "cores": c["cores"], "kind": c["kind"],
+                                   "sample_cells": c["sample_cells"]}
+            rec["speedup_vs_cpu"] = round(c["s_per_cell"] * ncells / t, 1)
+        print(json.dumps(rec), flush=True)
+
+    def dev_inputs(inputs):
+        return {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in inputs.items()}
+
+    def sfk(plan, d, out):
+        h = runtime.native_plan(plan)
+        return lambda: runtime._check(lib.sfk_eval(
+            h, d["coords"].shape[0], out.data_ptr(), d["coords"].data_ptr(),
+            d["w0"].data_ptr() if "w0" in d else None,
+            d["w1"].data_ptr() if "w1" in d else None, stream.cuda_stream))
+
+    for cfg in args.configs:
+        if cfg == "C1":
+            pm = compile_kernel("action_mass", "quad", 3)
+            pl = compile_kernel("action_laplace", "quad", 3)
+            inp = workloads.c1_inputs()
+            d = dev_inputs(inp)
+            am = torch.empty((1024, 16), dtype=torch.float64, device=dev)
+            al = torch.empty_like(am)
+            hm, hl = runtime.native_plan(pm), runtime.native_plan(pl)
+            fn = lambda: runtime._check(lib.sfk_eval_pair(  # noqa: E731
+                hm, hl, 1024, am.data_ptr(), al.data_ptr(), d["coords"].data_ptr(),
+                d["w0"].data_ptr(), stream.cuda_stream))
+
+            class Pair:
+                name = "action_mass+action_laplace"
+                degree = 3
+                algorithmic_flops = 944 + 1872
+                compulsory_bytes = 8 * (8 + 16 + 32)
+            report("C1", Pair, inp, 16, fn, cpu_plan=pl)
+        elif cfg == "C2":
+            for p in range(1, 9):
+                plan = compile_kernel("action_laplace", "hex", p)
+                inp = workloads.c2_inputs(p)
+                d = dev_inputs(inp)
+                out = torch.empty_like(d["w0"])
+                report("C2", plan, inp, (p + 1) ** 3, sfk(plan, d, out))
+                del d, out
+        elif cfg == "C3":
+            spec = action_form(REGISTRY["weighted_laplace"])
+            for p in range(4, 17):
+                plan = compile_form(spec, "hex", p, "spectral", "spectral_gll", "collocated-gll")
+                inp = workloads.c3_inputs(p)
+                d = dev_inputs(inp)
+                out = torch.empty_like(d["w0"])
+                report("C3", plan, inp, (p + 1) ** 3, sfk(plan, d, out))
+                del d, out
+        elif cfg == "C4":
+            for p in range(2, 7):
+                plan = compile_form(neohookean_residual_form(), "hex", p, quadrature=p + 2)
+                inp = workloads.c4_inputs(p)
+                d = dev_inputs(inp)
+                out = torch.empty_like(d["w0"])
+                report("C4", plan, inp, 3 * (p + 1) ** 3, sfk(plan, d, out))
+                del d, out
+        elif cfg == "C5":
+            for p in range(1, 5):
+                plan = compile_kernel("laplace", "hex", p)
+                inp = workloads.c5_inputs()
+                d = dev_inputs(inp)
+                nd = (p + 1) ** 3
+                out = torch.empty((d["coords"].shape[0], nd * nd), dtype=torch.float64,
+                                  device=dev)
+                report("C5", plan, inp, nd, sfk(plan, d, out))
+                del d, out
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
