@@ -255,4 +255,14 @@ def test_c4_vs_oracle(cuda, p):
     out = _run(cuda, plan, inp)
     assert np.array_equal(np.isnan(out), np.isnan(ref))
     ok = ~np.isnan(ref).any(axis=1)
-    assert rel_err(out[ok], ref[ok]) < TOL
+    if ok.any():
+        assert rel_err(out[ok], ref[ok]) < TOL
+    # the config's draw inverts elements at p >= 5 (ln J of J <= 0 -> NaN, as
+    # in the reference); a smaller displacement keeps every cell finite
+    amp = 0.03 / p ** 2
+    small = {"coords": inp["coords"],
+             "w0": workloads.uniform_dofs(inp["coords"].shape[0], inp["w0"].shape[1],
+                                          -amp, amp, seed=7, scale=workloads.H)}
+    ref = cpu.evaluate(plan, small)
+    assert not np.isnan(ref).any()
+    assert rel_err(_run(cuda, plan, small), ref) < TOL
