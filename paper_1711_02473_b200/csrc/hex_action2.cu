@@ -1,0 +1,495 @@
+// Hex Q_p Laplace action, line kernel v2 — BASELINE config C2 (headline).
+//
+// Same math and reference mapping as hex_action.cu (v1; see its header:
+// forms.py:186-189, 235-243; passes.py:672-743 schedule; scheduling.py:617-738
+// emitted kernel).  What changes is the B200 mapping, driven by the r01 ncu
+// capture of v1 at p=8 (profiles/r01a_prof_p8.md): FP64 pipe 53% busy, one
+// 8-warp CTA per SM (254 registers), 14% of stalls on the HBM loads of u,
+// 7% on barriers, and one LDCU (constant -> uniform register) per DFMA in
+// the contractions.
+//
+//  * R lines per thread and stage: every table entry fetched into a uniform
+//    register feeds R DFMAs (R independent accumulator sets = R-fold ILP).
+//  * Persistent CTAs, double-buffered: u and coords of the NEXT cell batch
+//    are copied HBM -> shared memory with cp.async (LDGSTS) while the
+//    current batch computes; the x stage reads u from shared memory.
+//  * z stage in three register-light passes over thread-private shared
+//    lines: (1) reference gradient lines written in place, (2) pointwise
+//    geometry + flux in place, (3) transposed z in place — no barrier
+//    between them and no 6N-wide register working set.
+//  * Small CTAs (2+ per SM) so barrier waits of one CTA overlap with the
+//    other's work.
+#include <cstdlib>
+
+#include "hex_geometry.cuh"
+
+namespace sfk {
+
+template <int N, int M, int CPB, int R>
+struct HexAction2Cfg {
+  static constexpr int NN = N * N, MN = M * N, MM = M * M, N3 = N * N * N;
+  static constexpr int LINES = (MM > NN ? MM : NN) * CPB;   // max lines of a stage
+  static constexpr int THREADS = round_up((LINES + R - 1) / R, 32);
+  static constexpr int PX = (N >= 4) ? NN + (((N - NN) % 16) + 16) % 16 : NN;
+  static constexpr int LZ = (M > N ? M : N) | 1;   // z-line stride, >= m (in-place z)
+  static constexpr int XA = M * PX;                // one X/R array per cell
+  static constexpr int XSZ = 2 * XA;
+  static constexpr int YA = MM * LZ;               // one Y/S array per cell
+  static constexpr int YSZ = 3 * YA;
+  static constexpr int USZ = round_up(CPB * N3, 2); // u buffer (16B multiple)
+  static constexpr int CSZ = CPB * 24;
+  static constexpr size_t SMEM =
+      (size_t)(CPB * XSZ + CPB * YSZ + USZ + 2 * CSZ) * sizeof(double);
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(K));
+}
+
+// Copy `n` doubles global -> shared (both arrays 8B aligned; 16B chunks when
+// the source allows it).  Called by every thread of the CTA.
+template <int THREADS>
+__device__ __forceinline__ void async_copy(double* dst, const double* src, int n, int tid) {
+  const bool al16 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  if (al16) {
+    const int n2 = n >> 1;
+    for (int i = tid; i < n2; i += THREADS) cp_async16(dst + 2 * i, src + 2 * i);
+    if ((n & 1) && tid == 0) cp_async8(dst + n - 1, src + n - 1);
+  } else {
+    for (int i = tid; i < n; i += THREADS) cp_async8(dst + i, src + i);
+  }
+}
+
+// ROLL: 0 = everything unrolled; 1 = pointwise loop rolled; 2 = also the
+// outer (output-index) loop of every contraction rolled (table entries then
+// come from warp-uniform constant loads; code size drops ~M-fold).
+template <int N, int M, int CPB, int R, int MINB, int ROLL>
+__global__ void __launch_bounds__(HexAction2Cfg<N, M, CPB, R>::THREADS, MINB)
+hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
+                      const double* __restrict__ coords, const double* __restrict__ u,
+                      double* __restrict__ A) {
+  using C = HexAction2Cfg<N, M, CPB, R>;
+  constexpr int NN = C::NN, MN = C::MN, MM = C::MM, N3 = C::N3, PX = C::PX, LZ = C::LZ;
+  constexpr int XA = C::XA, YA = C::YA, TH = C::THREADS;
+  constexpr int UQ = ROLL >= 2 ? 1 : M, UI = ROLL >= 2 ? 1 : N, UP = ROLL >= 1 ? 1 : M;
+  extern __shared__ __align__(16) double smem[];
+  double* sX = smem;                        // [CPB][2][M][PX]
+  double* sY = sX + CPB * C::XSZ;           // [CPB][3][M*M][LZ]
+  double* sU = sY + CPB * C::YSZ;           // [CPB*N3]   (single buffer)
+  double* sCo = sU + C::USZ;                // [2][CPB*24] (double buffer)
+  const int tid = threadIdx.x;
+  const int64_t nbatch = (ncells + CPB - 1) / CPB;
+
+  // u of the next batch streams into the single u buffer as soon as the
+  // current x stage has consumed it (overlapping the y, z, y^T, x^T stages);
+  // coords are double-buffered because the z stage still needs them.
+  auto prefetch = [&](int64_t b, int buf) {
+    const int64_t c0 = b * CPB;
+    const int nc = (int)((ncells - c0) < CPB ? (ncells - c0) : CPB);
+    async_copy<TH>(sU, u + c0 * N3, nc * N3, tid);
+    async_copy<TH>(sCo + buf * C::CSZ, coords + c0 * 24, nc * 24, tid);
+    cp_async_commit();
+  };
+
+  int64_t b = blockIdx.x;
+  if (b < nbatch) prefetch(b, 0);
+  for (int k = 0; b < nbatch; b += gridDim.x, ++k) {
+    const int cur = k & 1;
+    const int64_t cell0 = b * CPB;
+    const int ncb = (int)((ncells - cell0) < CPB ? (ncells - cell0) : CPB);
+    cp_async_wait<0>();
+    __syncthreads();
+    const double* su = sU;
+    const double* sC = sCo + cur * C::CSZ;
+
+    // ---- x stage: lines (c, iy, iz): X0 = Bx u, X1 = Dx u -------------
+    {
+      constexpr int L = CPB * NN;
+      int ln[R];
+      bool on[R];
+      double uu[R][N];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        ln[j] = tid + j * TH;
+        on[j] = ln[j] < L;
+        const int lc = on[j] ? ln[j] : 0;
+        const int c = lc / NN, r = lc - c * NN;
+        const bool live = on[j] && c < ncb;
+#pragma unroll
+        for (int i = 0; i < N; ++i) uu[j][i] = su[c * N3 + i * NN + r];
+        if (!live) {
+#pragma unroll
+          for (int i = 0; i < N; ++i) uu[j][i] = 0.0;
+        }
+      }
+#pragma unroll (UQ)
+      for (int q = 0; q < M; ++q) {
+        double bq[R], dq[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          bq[j] = T.B[q] * uu[j][0];
+          dq[j] = T.D[q] * uu[j][0];
+        }
+#pragma unroll
+        for (int i = 1; i < N; ++i)
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            bq[j] = fma(T.B[i * M + q], uu[j][i], bq[j]);
+            dq[j] = fma(T.D[i * M + q], uu[j][i], dq[j]);
+          }
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          if (on[j]) {
+            const int c = ln[j] / NN, r = ln[j] - c * NN;
+            double* xo = sX + c * C::XSZ + r;
+            xo[q * PX] = bq[j];
+            xo[XA + q * PX] = dq[j];
+          }
+      }
+    }
+    __syncthreads();
+    if (b + gridDim.x < nbatch) prefetch(b + gridDim.x, cur ^ 1);
+
+    // ---- y stage: lines (c, qx, iz): BB = By X0, BD = Dy X0, DB = By X1 --
+    {
+      constexpr int L = CPB * MN;
+      double a0[R][N], a1[R][N];
+      int ln[R];
+      bool on[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        ln[j] = tid + j * TH;
+        on[j] = ln[j] < L;
+        const int lc = on[j] ? ln[j] : 0;
+        const int c = lc / MN, r = lc - c * MN;
+        const int qx = r / N, iz = r - qx * N;
+        const double* xi = sX + c * C::XSZ + qx * PX + iz;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          a0[j][i] = xi[i * N];
+          a1[j][i] = xi[XA + i * N];
+        }
+      }
+#pragma unroll (UQ)
+      for (int q = 0; q < M; ++q) {
+        double bb[R], bd[R], db[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          bb[j] = T.B[q] * a0[j][0];
+          bd[j] = T.D[q] * a0[j][0];
+          db[j] = T.B[q] * a1[j][0];
+        }
+#pragma unroll
+        for (int i = 1; i < N; ++i)
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            bb[j] = fma(T.B[i * M + q], a0[j][i], bb[j]);
+            bd[j] = fma(T.D[i * M + q], a0[j][i], bd[j]);
+            db[j] = fma(T.B[i * M + q], a1[j][i], db[j]);
+          }
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          if (on[j]) {
+            const int c = ln[j] / MN, r = ln[j] - c * MN;
+            const int qx = r / N, iz = r - qx * N;
+            double* yo = sY + c * C::YSZ + (qx * M + q) * LZ + iz;
+            yo[0] = bb[j];
+            yo[YA] = bd[j];
+            yo[2 * YA] = db[j];
+          }
+      }
+    }
+    __syncthreads();
+
+    // ---- z stage: lines (c, qx, qy), three in-place passes ---------------
+    {
+      constexpr int L = CPB * MM;
+      int ln[R];
+      bool on[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        ln[j] = tid + j * TH;
+        on[j] = ln[j] < L;
+      }
+      // (1) reference gradient lines: slot 0 <- Dz BB (d_z), 1 <- Bz BD (d_y),
+      //     2 <- Bz DB (d_x)
+      {
+        double bb[R][N], bd[R][N], db[R][N];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const int c = on[j] ? ln[j] / MM : 0, r = on[j] ? ln[j] - c * MM : 0;
+          const double* yi = sY + c * C::YSZ + r * LZ;
+#pragma unroll (UQ)
+          for (int i = 0; i < N; ++i) {
+            bb[j][i] = yi[i];
+            bd[j][i] = yi[YA + i];
+            db[j][i] = yi[2 * YA + i];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+          double gz[R], gy[R], gx[R];
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            gz[j] = T.D[q] * bb[j][0];
+            gy[j] = T.B[q] * bd[j][0];
+            gx[j] = T.B[q] * db[j][0];
+          }
+#pragma unroll
+          for (int i = 1; i < N; ++i)
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+              gz[j] = fma(T.D[i * M + q], bb[j][i], gz[j]);
+              gy[j] = fma(T.B[i * M + q], bd[j][i], gy[j]);
+              gx[j] = fma(T.B[i * M + q], db[j][i], gx[j]);
+            }
+          if (M > N) {
+            // in place is only safe once every input entry was read: for
+            // M > N the outputs q >= N go beyond the inputs, q < N overwrite
+            // inputs already consumed (all inputs are in registers)
+          }
+#pragma unroll
+          for (int j = 0; j < R; ++j)
+            if (on[j]) {
+              const int c = ln[j] / MM, r = ln[j] - c * MM;
+              double* yo = sY + c * C::YSZ + r * LZ + q;
+              yo[0] = gz[j];
+              yo[YA] = gy[j];
+              yo[2 * YA] = gx[j];
+            }
+        }
+      }
+      // (2) pointwise: geometry per point + Laplace flux, in place
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int lc = on[j] ? ln[j] : 0;
+        const int c = lc / MM, r = lc - c * MM;
+        const int qx = r / M, qy = r - qx * M;
+        double* yl = sY + c * C::YSZ + r * LZ;
+        HexLineGeom geo;
+        geo.setup(sC + c * 24, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
+        const double wxy = T.W[qx] * T.W[qy];
+#pragma unroll (UP)
+        for (int q = 0; q < M; ++q) {
+          double gz = yl[q], gy = yl[YA + q], gx = yl[2 * YA + q];
+          double r0[3], r1[3], r2[3];
+          const double det = geo.adj(T.Bc[q], T.Bc[M + q], r0, r1, r2);
+          const double s = (wxy * T.W[q]) * rcp64(fabs(det));
+          laplace_flux(r0, r1, r2, s, gx, gy, gz);
+          if (on[j]) {
+            yl[q] = gz;
+            yl[YA + q] = gy;
+            yl[2 * YA + q] = gx;
+          }
+        }
+      }
+      // (3) transposed z, in place: slot 0 <- Dz^T f_z, 1 <- Bz^T f_y,
+      //     2 <- Bz^T f_x
+      {
+        double fz[R][M], fy[R][M], fx[R][M];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const int c = on[j] ? ln[j] / MM : 0, r = on[j] ? ln[j] - c * MM : 0;
+          const double* yi = sY + c * C::YSZ + r * LZ;
+#pragma unroll
+          for (int q = 0; q < M; ++q) {
+            fz[j][q] = yi[q];
+            fy[j][q] = yi[YA + q];
+            fx[j][q] = yi[2 * YA + q];
+          }
+        }
+#pragma unroll (UI)
+        for (int i = 0; i < N; ++i) {
+          double sz[R], sy[R], sx[R];
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            sz[j] = T.D[i * M] * fz[j][0];
+            sy[j] = T.B[i * M] * fy[j][0];
+            sx[j] = T.B[i * M] * fx[j][0];
+          }
+#pragma unroll
+          for (int q = 1; q < M; ++q)
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+              sz[j] = fma(T.D[i * M + q], fz[j][q], sz[j]);
+              sy[j] = fma(T.B[i * M + q], fy[j][q], sy[j]);
+              sx[j] = fma(T.B[i * M + q], fx[j][q], sx[j]);
+            }
+#pragma unroll
+          for (int j = 0; j < R; ++j)
+            if (on[j]) {
+              const int c = ln[j] / MM, r = ln[j] - c * MM;
+              double* yo = sY + c * C::YSZ + r * LZ + i;
+              yo[0] = sz[j];
+              yo[YA] = sy[j];
+              yo[2 * YA] = sx[j];
+            }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- transposed y stage: lines (c, qx, iz) ----------------------------
+    {
+      constexpr int L = CPB * MN;
+      double pz[R][M], py[R][M], px[R][M];
+      int ln[R];
+      bool on[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        ln[j] = tid + j * TH;
+        on[j] = ln[j] < L;
+        const int lc = on[j] ? ln[j] : 0;
+        const int c = lc / MN, r = lc - c * MN;
+        const int qx = r / N, iz = r - qx * N;
+        const double* yi = sY + c * C::YSZ + qx * M * LZ + iz;
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+          pz[j][q] = yi[q * LZ];
+          py[j][q] = yi[YA + q * LZ];
+          px[j][q] = yi[2 * YA + q * LZ];
+        }
+      }
+#pragma unroll (UI)
+      for (int i = 0; i < N; ++i) {
+        double r1[R], r2[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          r1[j] = T.B[i * M] * px[j][0];
+          r2[j] = fma(T.D[i * M], py[j][0], T.B[i * M] * pz[j][0]);
+        }
+#pragma unroll
+        for (int q = 1; q < M; ++q)
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            r1[j] = fma(T.B[i * M + q], px[j][q], r1[j]);
+            r2[j] = fma(T.D[i * M + q], py[j][q], r2[j]);
+            r2[j] = fma(T.B[i * M + q], pz[j][q], r2[j]);
+          }
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          if (on[j]) {
+            const int c = ln[j] / MN, r = ln[j] - c * MN;
+            const int qx = r / N, iz = r - qx * N;
+            double* xo = sX + c * C::XSZ + qx * PX + iz;
+            xo[i * N] = r1[j];
+            xo[XA + i * N] = r2[j];
+          }
+      }
+    }
+    __syncthreads();
+
+    // ---- transposed x stage: lines (c, iy, iz) -> A ------------------------
+    {
+      constexpr int L = CPB * NN;
+      double p1[R][M], p2[R][M];
+      int ln[R];
+      bool on[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        ln[j] = tid + j * TH;
+        on[j] = ln[j] < L && (ln[j] / NN) < ncb;
+        const int c = on[j] ? ln[j] / NN : 0, r = on[j] ? ln[j] - c * NN : 0;
+        const double* xi = sX + c * C::XSZ + r;
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+          p1[j][q] = xi[q * PX];
+          p2[j][q] = xi[XA + q * PX];
+        }
+      }
+#pragma unroll (UI)
+      for (int i = 0; i < N; ++i) {
+        double a[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) a[j] = fma(T.D[i * M], p1[j][0], T.B[i * M] * p2[j][0]);
+#pragma unroll
+        for (int q = 1; q < M; ++q)
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            a[j] = fma(T.D[i * M + q], p1[j][q], a[j]);
+            a[j] = fma(T.B[i * M + q], p2[j][q], a[j]);
+          }
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          if (on[j]) {
+            const int c = ln[j] / NN, r = ln[j] - c * NN;
+            A[(cell0 + c) * N3 + i * NN + r] = a[j];
+          }
+      }
+    }
+    __syncthreads();   // X/R region is rewritten by the next batch's x stage
+  }
+}
+
+template <int N, int M, int CPB, int R, int MINB, int ROLL = 1>
+static int launch_v2(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                     const double* u, cudaStream_t s) {
+  using C = HexAction2Cfg<N, M, CPB, R>;
+  auto kern = hex_laplace_action_v2<N, M, CPB, R, MINB, ROLL>;
+  static int sms = 0, per_sm = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_action_v2)");
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    if (per_sm < 1) return fail(SFK_ECUDA, "hex_action_v2<%d>: kernel does not fit on an SM", N);
+  }
+  const Tabs<N, M> T = make_tabs<N, M>(p);
+  const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  const int64_t resident = (int64_t)sms * per_sm;
+  const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
+  kern<<<grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, u, A);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "hex_laplace_action_v2 launch");
+}
+
+// Per-degree configuration (cells per CTA, lines per thread, min CTAs/SM,
+// loop rolling).  SFK_C2_R=1|2 and SFK_C2_ROLL=1|2 override the defaults
+// (tuning runs only).
+static int env_int(const char* name) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : 0;
+}
+
+template <int N, int CPB, int MINB1, int MINB2>
+static int pick(int r, int roll, const sfk_plan* p, int64_t ncells, double* A,
+                const double* coords, const double* w0, cudaStream_t s) {
+  if (r == 2) return launch_v2<N, N, CPB, 2, MINB2, 1>(p, ncells, A, coords, w0, s);
+  if (roll == 2) return launch_v2<N, N, CPB, 1, MINB1, 2>(p, ncells, A, coords, w0, s);
+  return launch_v2<N, N, CPB, 1, MINB1, 1>(p, ncells, A, coords, w0, s);
+}
+
+int launch_hex_action_v2(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                         const double* w0, cudaStream_t s) {
+  if (p->n != p->m) return SFK_EUNSUPPORTED;   // caller falls back to v1
+  static const int r_env = env_int("SFK_C2_R"), roll_env = env_int("SFK_C2_ROLL");
+  const int r = r_env ? r_env : 1, roll = roll_env ? roll_env : 1;
+  switch (p->n) {
+    case 2: return pick<2, 64, 2, 2>(r, roll, p, ncells, A, coords, w0, s);
+    case 3: return pick<3, 32, 2, 2>(r, roll, p, ncells, A, coords, w0, s);
+    case 4: return pick<4, 16, 2, 2>(r, roll, p, ncells, A, coords, w0, s);
+    case 5: return pick<5, 10, 2, 2>(r, roll, p, ncells, A, coords, w0, s);
+    case 6: return pick<6, 8, 2, 2>(r, roll, p, ncells, A, coords, w0, s);
+    case 7: return pick<7, 5, 2, 2>(r, roll, p, ncells, A, coords, w0, s);
+    case 8: return pick<8, 4, 2, 2>(r, roll, p, ncells, A, coords, w0, s);
+    case 9: return pick<9, 3, 2, 2>(r, roll, p, ncells, A, coords, w0, s);
+    default: return SFK_EUNSUPPORTED;
+  }
+}
+
+}  // namespace sfk

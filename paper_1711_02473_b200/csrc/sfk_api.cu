@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -36,14 +37,29 @@ int cuda_status(cudaError_t err, const char* what) {
 
 void note_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
+// SFK_C2_KERNEL=v1 selects the first-generation hex action kernel (A/B runs).
+static int c2_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SFK_C2_KERNEL");
+    v = (e && strcmp(e, "v1") == 0) ? 1 : 2;
+  }
+  return v;
+}
+
 static int dispatch(const sfk_plan* p, int64_t ncells, double* A,
                     const double* coords, const double* w0, const double* w1,
                     cudaStream_t s) {
   switch (p->kind) {
     case SFK_KIND_ACTION_LAPLACE:
-      if (p->dim == 3)
-        return p->collocated ? launch_hex_colloc_action(p, ncells, A, coords, w0, nullptr, s)
-                             : launch_hex_action(p, ncells, A, coords, w0, nullptr, s);
+      if (p->dim == 3) {
+        if (p->collocated) return launch_hex_colloc_action(p, ncells, A, coords, w0, nullptr, s);
+        if (c2_variant() != 1) {
+          const int rc = launch_hex_action_v2(p, ncells, A, coords, w0, s);
+          if (rc != SFK_EUNSUPPORTED) return rc;
+        }
+        return launch_hex_action(p, ncells, A, coords, w0, nullptr, s);
+      }
       return launch_quad_action(p, nullptr, ncells, A, nullptr, coords, w0, s);
     case SFK_KIND_ACTION_WEIGHTED_LAPLACE:
       return launch_hex_colloc_action(p, ncells, A, coords, w0, w1, s);
