@@ -21,6 +21,7 @@
 //    other's work.
 #include <cstdlib>
 
+#include "async_copy.cuh"
 #include "hex_geometry.cuh"
 
 namespace sfk {
@@ -41,34 +42,6 @@ struct HexAction2Cfg {
   static constexpr size_t SMEM =
       (size_t)(CPB * XSZ + CPB * YSZ + USZ + 2 * CSZ) * sizeof(double);
 };
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int K>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(K));
-}
-
-// Copy `n` doubles global -> shared (both arrays 8B aligned; 16B chunks when
-// the source allows it).  Called by every thread of the CTA.
-template <int THREADS>
-__device__ __forceinline__ void async_copy(double* dst, const double* src, int n, int tid) {
-  const bool al16 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
-  if (al16) {
-    const int n2 = n >> 1;
-    for (int i = tid; i < n2; i += THREADS) cp_async16(dst + 2 * i, src + 2 * i);
-    if ((n & 1) && tid == 0) cp_async8(dst + n - 1, src + n - 1);
-  } else {
-    for (int i = tid; i < n; i += THREADS) cp_async8(dst + i, src + i);
-  }
-}
 
 // ROLL: 0 = everything unrolled; 1 = pointwise loop rolled; 2 = also the
 // outer (output-index) loop of every contraction rolled (table entries then

@@ -37,14 +37,49 @@ int cuda_status(cudaError_t err, const char* what) {
 
 void note_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
-// SFK_C2_KERNEL=v1 selects the first-generation hex action kernel (A/B runs).
+// Hex Laplace action (BASELINE C2) kernel generation per degree.  The
+// default ("auto") is the fastest measured generation for each n = p+1
+// (profiles/r01*_*.json A/B runs); SFK_C2_KERNEL=v1|v2|v3|tc forces one
+// (tuning / A-B runs; a generation that has no instance for n falls back).
+//   v1: line kernel, thread per line, non-persistent       (hex_action.cu)
+//   v2: persistent, cp.async prefetch, in-place z passes    (hex_action2.cu)
+//   v3: v2 + input-streaming contractions, searched pads    (hex_action3.cu)
+//   tc: FP64 tensor-core (DMMA) stages, n = 8               (hex_action_tc.cu)
 static int c2_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SFK_C2_KERNEL");
-    v = (e && strcmp(e, "v1") == 0) ? 1 : 2;
+    v = 0;
+    if (e && e[0] == 'v' && e[1] >= '1' && e[1] <= '3') v = e[1] - '0';
+    if (e && strcmp(e, "tc") == 0) v = 4;
   }
   return v;
+}
+
+static int c2_auto(int n) {
+  switch (n) {
+    case 2: return 3;
+    case 3: return 3;
+    case 4: return 2;
+    case 5: return 3;
+    case 6: return 2;
+    case 7: return 3;
+    case 8: return 4;
+    case 9: return 2;
+    default: return 1;
+  }
+}
+
+static int launch_c2(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                     const double* w0, cudaStream_t s) {
+  int v = c2_variant();
+  if (v == 0) v = c2_auto(p->n);
+  int rc = SFK_EUNSUPPORTED;
+  if (v == 4) rc = launch_hex_action_tc(p, ncells, A, coords, w0, s);
+  if (rc == SFK_EUNSUPPORTED && v >= 3) rc = launch_hex_action_v3(p, ncells, A, coords, w0, s);
+  if (rc == SFK_EUNSUPPORTED && v >= 2) rc = launch_hex_action_v2(p, ncells, A, coords, w0, s);
+  if (rc == SFK_EUNSUPPORTED) rc = launch_hex_action(p, ncells, A, coords, w0, nullptr, s);
+  return rc;
 }
 
 static int dispatch(const sfk_plan* p, int64_t ncells, double* A,
@@ -54,11 +89,7 @@ static int dispatch(const sfk_plan* p, int64_t ncells, double* A,
     case SFK_KIND_ACTION_LAPLACE:
       if (p->dim == 3) {
         if (p->collocated) return launch_hex_colloc_action(p, ncells, A, coords, w0, nullptr, s);
-        if (c2_variant() != 1) {
-          const int rc = launch_hex_action_v2(p, ncells, A, coords, w0, s);
-          if (rc != SFK_EUNSUPPORTED) return rc;
-        }
-        return launch_hex_action(p, ncells, A, coords, w0, nullptr, s);
+        return launch_c2(p, ncells, A, coords, w0, s);
       }
       return launch_quad_action(p, nullptr, ncells, A, nullptr, coords, w0, s);
     case SFK_KIND_ACTION_WEIGHTED_LAPLACE:
