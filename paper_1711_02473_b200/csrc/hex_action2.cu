@@ -37,10 +37,10 @@ struct HexAction2Cfg {
   static constexpr int XSZ = 2 * XA;
   static constexpr int YA = MM * LZ;               // one Y/S array per cell
   static constexpr int YSZ = 3 * YA;
-  static constexpr int USZ = round_up(CPB * N3, 2); // u buffer (16B multiple)
+  static constexpr int USZ = round_up(CPB * N3 + 1, 2); // u buffer (16B multiple)
   static constexpr int CSZ = CPB * 24;
   static constexpr size_t SMEM =
-      (size_t)(CPB * XSZ + CPB * YSZ + USZ + 2 * CSZ) * sizeof(double);
+      (size_t)(round_up(CPB * XSZ + CPB * YSZ, 2) + USZ + 2 * CSZ) * sizeof(double);
 };
 
 // ROLL: 0 = everything unrolled; 1 = pointwise loop rolled; 2 = also the
@@ -58,7 +58,7 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
   extern __shared__ __align__(16) double smem[];
   double* sX = smem;                        // [CPB][2][M][PX]
   double* sY = sX + CPB * C::XSZ;           // [CPB][3][M*M][LZ]
-  double* sU = sY + CPB * C::YSZ;           // [CPB*N3]   (single buffer)
+  double* sU = smem + round_up(CPB * C::XSZ + CPB * C::YSZ, 2);  // [CPB*N3+1]
   double* sCo = sU + C::USZ;                // [2][CPB*24] (double buffer)
   const int tid = threadIdx.x;
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
@@ -69,7 +69,7 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
   auto prefetch = [&](int64_t b, int buf) {
     const int64_t c0 = b * CPB;
     const int nc = (int)((ncells - c0) < CPB ? (ncells - c0) : CPB);
-    async_copy<TH>(sU, u + c0 * N3, nc * N3, tid);
+    async_copy_phase<TH>(sU + dst_shift(u + c0 * N3), u + c0 * N3, nc * N3, tid);
     async_copy<TH>(sCo + buf * C::CSZ, coords + c0 * 24, nc * 24, tid);
     cp_async_commit();
   };
@@ -82,7 +82,7 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
     const int ncb = (int)((ncells - cell0) < CPB ? (ncells - cell0) : CPB);
     cp_async_wait<0>();
     __syncthreads();
-    const double* su = sU;
+    const double* su = sU + dst_shift(u + cell0 * N3);
     const double* sC = sCo + cur * C::CSZ;
 
     // ---- x stage: lines (c, iy, iz): X0 = Bx u, X1 = Dx u -------------

@@ -35,9 +35,9 @@ struct Act3Layout {
   static constexpr int NN = N * N, MN = M * N, MM = M * M, N3 = N * N * N;
   static constexpr int XA = M * PX, YA = M * YX;
   static constexpr int THREADS = round_up(CPB * (MM > NN ? MM : NN), 32);
-  static constexpr int USZ = round_up(CPB * N3, 2);
+  static constexpr int USZ = round_up(CPB * N3 + 1, 2);
   static constexpr int CSZ = CPB * 24;
-  static constexpr size_t SMEM = (size_t)(CPB * XC + CPB * YC + USZ + 2 * CSZ) * sizeof(double);
+  static constexpr size_t SMEM = (size_t)(round_up(CPB * XC + CPB * YC, 2) + USZ + 2 * CSZ) * sizeof(double);
   static_assert(XC >= 2 * XA && YC >= 3 * YA && LZ >= M && LZ >= N, "layout too small");
 };
 
@@ -52,7 +52,7 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
   extern __shared__ __align__(16) double smem[];
   double* sX = smem;
   double* sY = sX + CPB * XC;
-  double* sU = sY + CPB * YC;
+  double* sU = smem + round_up(CPB * XC + CPB * YC, 2);
   double* sCo = sU + L::USZ;
   const int tid = threadIdx.x;
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
@@ -60,7 +60,7 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
   auto prefetch = [&](int64_t bb, int buf) {
     const int64_t c0 = bb * CPB;
     const int nc = (int)((ncells - c0) < CPB ? (ncells - c0) : CPB);
-    async_copy<TH>(sU, u + c0 * N3, nc * N3, tid);
+    async_copy_phase<TH>(sU + dst_shift(u + c0 * N3), u + c0 * N3, nc * N3, tid);
     async_copy<TH>(sCo + buf * L::CSZ, coords + c0 * 24, nc * 24, tid);
     cp_async_commit();
   };
@@ -79,7 +79,7 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
     if (tid < CPB * NN) {
       const int c = tid / NN, r = tid - c * NN;
       const int iy = r / N, iz = r - iy * N;
-      const double* ui = sU + c * N3 + r;
+      const double* ui = sU + dst_shift(u + cell0 * N3) + c * N3 + r;
       const bool live = c < ncb;
       double xb[M], xd[M];
       {
