@@ -16,14 +16,15 @@
 // B200 mapping: one CTA = CPB cells (1 cell for N >= 13: a 17^3 field is
 // 38 KB).  Shared memory holds three N^3 arrays per cell with padded
 // strides (tools/smem_pads.py):  U (u, later A), GX (d_x u, later f_x),
-// GY (d_y u, later f_y).  Phases:
-//   1. coalesced copy u -> U
+// GY (d_y u, later f_y), plus K (kappa) for the weighted form.  Phases:
+//   1. cp.async u -> U and kappa -> K (kappa lands during phase 2)
 //   2. each thread: one x-line (GX = Dx u) and one y-line (GY = Dy u)
 //   3. each thread owns a z-line (x, y): d_z u in registers, then per point
 //      geometry + kappa + flux, writing f_x, f_y in place and accumulating
 //      A_z = Dz^T f_z in registers, stored over its own U line
 //   4. x-lines: U += Dx^T f_x;   5. y-lines: U += Dy^T f_y
 //   6. coalesced copy U -> A
+#include "async_copy.cuh"
 #include "hex_geometry.cuh"
 
 namespace sfk {
@@ -40,7 +41,9 @@ struct CollocCfg {
   static constexpr int NN = N * N;
   static constexpr int N3 = N * N * N;
   static constexpr int THREADS = round_up(CPB * NN, 32);
-  static constexpr size_t SMEM = (size_t)(3 * CPB * CS + CPB * 24) * sizeof(double);
+  static constexpr size_t smem(bool weighted) {
+    return (size_t)((weighted ? 4 : 3) * CPB * CS + CPB * 24) * sizeof(double);
+  }
 };
 
 template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED>
@@ -55,20 +58,37 @@ hex_colloc_action_kernel(const __grid_constant__ TabsD<N> T, int64_t ncells,
   double* sGX = sU + CPB * CS;
   double* sGY = sGX + CPB * CS;
   double* sC = sGY + CPB * CS;
+  double* sK = sC + CPB * 24;   // kappa (WEIGHTED), same padded layout as U
 
   const int tid = threadIdx.x;
   const int64_t cell0 = (int64_t)blockIdx.x * CPB;
   const int64_t rem = ncells - cell0;
   const int ncb = rem < CPB ? (int)rem : CPB;
 
+  // u (group 0) and kappa (group 1) stream into the padded shared layouts
+  // with cp.async; kappa is only needed by the pointwise phase, so its
+  // latency hides behind phase 2.
   for (int i = tid; i < CPB * 24; i += C::THREADS)
     sC[i] = i < ncb * 24 ? __ldg(coords + cell0 * 24 + i) : 0.0;
   {
     const double* ug = u + cell0 * N3;
-    for (int i = tid; i < CPB * N3; i += C::THREADS) {
+    for (int i = tid; i < ncb * N3; i += C::THREADS) {
       const int c = i / N3, r = i - c * N3;
       const int x = r / NN, y = (r / N) % N, z = r % N;
-      sU[c * CS + x * SX + y * SY + z] = c < ncb ? __ldg(ug + i) : 0.0;
+      cp_async8(sU + c * CS + x * SX + y * SY + z, ug + i);
+    }
+    cp_async_commit();
+    if (WEIGHTED) {
+      const double* kg = kappa + cell0 * N3;
+      for (int i = tid; i < ncb * N3; i += C::THREADS) {
+        const int c = i / N3, r = i - c * N3;
+        const int x = r / NN, y = (r / N) % N, z = r % N;
+        cp_async8(sK + c * CS + x * SX + y * SY + z, kg + i);
+      }
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
   }
   __syncthreads();
@@ -100,7 +120,8 @@ hex_colloc_action_kernel(const __grid_constant__ TabsD<N> T, int64_t ncells,
       sGY[cb + a * SX + q * SY + b] = g;
     }
   }
-  __syncthreads();
+  if (WEIGHTED) cp_async_wait<0>();   // kappa copies of this thread landed
+  __syncthreads();                     // ... and everybody's are visible
 
   // ---- phase 3: z-line (x=a, y=b): d_z u, flux, A_z = Dz^T f_z ---------
   if (act) {
@@ -114,8 +135,7 @@ hex_colloc_action_kernel(const __grid_constant__ TabsD<N> T, int64_t ncells,
     HexLineGeom geo;
     geo.setup(sC + c * 24, T.Bc[a], T.Bc[N + a], T.Bc[b], T.Bc[N + b]);
     const double wxy = T.W[a] * T.W[b];
-    const double* kp = WEIGHTED ? kappa + (cell0 + c) * N3 + (a * N + b) * N : nullptr;
-    const bool valid = c < ncb;
+    const double* kp = sK + base;
 #pragma unroll
     for (int q = 0; q < N; ++q) {
       double gz = T.D[q] * ul[0];
@@ -125,7 +145,7 @@ hex_colloc_action_kernel(const __grid_constant__ TabsD<N> T, int64_t ncells,
       double r0[3], r1[3], r2[3];
       const double det = geo.adj(T.Bc[q], T.Bc[N + q], r0, r1, r2);
       double s = (wxy * T.W[q]) * rcp64(fabs(det));
-      if (WEIGHTED) s *= valid ? __ldg(kp + q) : 0.0;
+      if (WEIGHTED) s *= kp[q];
       laplace_flux(r0, r1, r2, s, gx, gy, gz);
       sGX[base + q] = gx;
       sGY[base + q] = gy;
@@ -192,14 +212,14 @@ static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* 
   cudaError_t e;
   if (kappa) {
     auto k = hex_colloc_action_kernel<N, CPB, SY, SX, CS, true>;
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem(true));
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
-    k<<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, u, kappa, A);
+    k<<<(unsigned)grid, C::THREADS, C::smem(true), s>>>(T, ncells, coords, u, kappa, A);
   } else {
     auto k = hex_colloc_action_kernel<N, CPB, SY, SX, CS, false>;
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem(false));
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
-    k<<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, u, nullptr, A);
+    k<<<(unsigned)grid, C::THREADS, C::smem(false), s>>>(T, ncells, coords, u, nullptr, A);
   }
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_colloc_action_kernel launch");

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cpu-cells", type=int, default=4096)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--p", type=int, nargs="*", default=None, help="only these degrees")
     args = ap.parse_args()
 
     import torch
@@ -141,6 +142,8 @@ def main():
             report("C1", Pair, inp, 16, fn, cpu_plan=pl)
         elif cfg == "C2":
             for p in range(1, 9):
+                if args.p and p not in args.p:
+                    continue
                 plan = compile_kernel("action_laplace", "hex", p)
                 inp = workloads.c2_inputs(p)
                 d = dev_inputs(inp)
@@ -150,6 +153,8 @@ def main():
         elif cfg == "C3":
             spec = action_form(REGISTRY["weighted_laplace"])
             for p in range(4, 17):
+                if args.p and p not in args.p:
+                    continue
                 plan = compile_form(spec, "hex", p, "spectral", "spectral_gll", "collocated-gll")
                 inp = workloads.c3_inputs(p)
                 d = dev_inputs(inp)
@@ -158,6 +163,8 @@ def main():
                 del d, out
         elif cfg == "C4":
             for p in range(2, 7):
+                if args.p and p not in args.p:
+                    continue
                 plan = compile_form(neohookean_residual_form(), "hex", p, quadrature=p + 2)
                 inp = workloads.c4_inputs(p)
                 d = dev_inputs(inp)
@@ -166,6 +173,8 @@ def main():
                 del d, out
         elif cfg == "C5":
             for p in range(1, 5):
+                if args.p and p not in args.p:
+                    continue
                 plan = compile_kernel("laplace", "hex", p)
                 inp = workloads.c5_inputs()
                 d = dev_inputs(inp)

@@ -1,5 +1,5 @@
 #!/bin/bash
-# gpu tests + per-config measurements
+# gpu tests + per-config measurements: bash tools/gpu_tests.sh TAG [configs...] [--p ...]
 TAG=${1:-r01}
 mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/${TAG}_pytest_gpu.log 2>&1
