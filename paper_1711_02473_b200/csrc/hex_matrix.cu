@@ -17,12 +17,15 @@
 // DD): 4 x-contractions instead of 9.  Per cell ~ 9 m^3 n^2 + 9 m^2 n^4 +
 // 4 m n^6 FMA (p=4: 0.48 M FMA vs the reference's 1.69 M flops).
 //
-// B200 mapping: one thread per (iy, iz, jy, jz) (n^4 threads per cell) owns
-// the n^2 outputs A[(ix,iy,iz),(jx,jy,jz)] in registers across the qx loop;
-// Y_g never leaves registers.  K and Z for the current plane live in shared
-// memory.  Output rows are written straight from registers: for fixed
-// (ix, jx) a warp stores runs of n^2 contiguous doubles; the 125 KB (p=4)
-// of a cell is complete in L2 before eviction, so DRAM sees full lines.
+// B200 mapping: one CTA per cell (n^4 threads; several cells for n <= 3).
+// K at all points, Z for all planes and Y_g for all planes live in shared
+// memory (150 KB at p=4), each produced by one CTA-wide phase; every thread
+// r = (iy, iz, jy, jz) contracts Z over qy into its 4 Y_g values per plane.  A final pass gives each
+// thread its n^2 outputs A[(ix,iy,iz),(jx,jy,jz)] from 4m shared loads and
+// 4 m n^2 register FMAs — no register array lives across the plane loop (the
+// r01 version spilled it).  Output rows are written straight from registers:
+// for fixed (ix, jx) a warp stores runs of n^2 contiguous doubles; the 125 KB
+// (p=4) of a cell is complete in L2 before eviction, so DRAM sees full lines.
 #include "hex_geometry.cuh"
 
 namespace sfk {
@@ -37,11 +40,14 @@ struct TabsMat {
 
 template <int N, int M, int CPB>
 struct MatCfg {
-  static constexpr int N2 = N * N, N3 = N * N * N, N4 = N * N * N * N;
+  static constexpr int N2 = N * N, N3 = N * N * N, N4 = N * N * N * N, M3 = M * M * M;
   static constexpr int THREADS = round_up(CPB * N4, 32);
-  static constexpr int ZS = 9 * M * N2;     // Z for one cell and one plane
-  static constexpr int KS = 6 * M * M;      // K (6 unique entries) for one plane
-  static constexpr int TS = 2 * N * M;      // B and D copies (runtime-indexed reads)
+  static constexpr int ZS = 9 * M * M * N2;  // Z[pair][qx][qy][iz][jz] for one cell
+  static constexpr int KS = 6 * M3;          // K (6 unique entries) at every point
+  static constexpr int TS = 2 * N * M;       // B and D copies (runtime-indexed reads)
+  static constexpr int YS = 4 * M * N4;      // Y_g[qx][r] for one cell, all planes
+  static constexpr size_t SMEM =
+      (size_t)(CPB * (ZS + KS + YS + 24) + TS) * sizeof(double);
 };
 
 // pair (l, l') -> symmetric K index: 00 11 22 01 02 12
@@ -49,16 +55,23 @@ __host__ __device__ constexpr int ksym(int l, int r) {
   return l == r ? l : (l + r == 1 ? 3 : (l + r == 2 ? 4 : 5));
 }
 
+// Four phases per CTA, each over all quadrature planes at once (3 barriers):
+//  K  at every point (threads over points),
+//  Z_ll'[qx][qy][iz][jz] = sum_qz Tz Tz' K_ll'   (threads over (pair, qx, qy, iz, jz)),
+//  Y_g[qx][r]            = sum over pairs in g, qy (thread r = (iy, iz, jy, jz)),
+//  A[(ix,..),(jx,..)]    = sum_{g,qx} Tx Tx' Y_g[qx][r]   (thread r, then stores).
 template <int N, int M, int CPB>
 __global__ void __launch_bounds__(MatCfg<N, M, CPB>::THREADS)
 hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncells,
                           const double* __restrict__ coords, double* __restrict__ A) {
   using C = MatCfg<N, M, CPB>;
-  constexpr int N2 = C::N2, N3 = C::N3, N4 = C::N4;
-  __shared__ double sZ[CPB * C::ZS];
-  __shared__ double sK[CPB * C::KS];
-  __shared__ double sT[C::TS];
-  __shared__ double sC[CPB * 24];
+  constexpr int N2 = C::N2, N3 = C::N3, N4 = C::N4, M3 = C::M3;
+  extern __shared__ double smem[];
+  double* sZ = smem;                       // [CPB][9][M][M][N2]
+  double* sK = sZ + CPB * C::ZS;           // [CPB][6][M3]
+  double* sY = sK + CPB * C::KS;           // [CPB][4][M][N4]
+  double* sC = sY + CPB * C::YS;           // [CPB][24]
+  double* sT = sC + CPB * 24;              // B, D
   const int tid = threadIdx.x;
   const int64_t cell0 = (int64_t)blockIdx.x * CPB;
   const int64_t rem = ncells - cell0;
@@ -71,68 +84,62 @@ hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncell
   }
   // thread -> (cell, iy, iz, jy, jz)
   const bool act = tid < CPB * N4;
-  const int c = tid / N4, r = tid - (tid / N4) * N4;
+  const int c = act ? tid / N4 : 0, r = tid - c * N4;
   const int iy = r / (N * N2), iz = (r / N2) % N, jy = (r / N) % N, jz = r % N;
-  double acc[N][N];
-#pragma unroll
-  for (int ix = 0; ix < N; ++ix)
-#pragma unroll
-    for (int jx = 0; jx < N; ++jx) acc[ix][jx] = 0.0;
   __syncthreads();
-  // y products for this thread's (iy, jy): pattern (a, b) in {B,D}^2
-  double py[4][M];
-#pragma unroll
-  for (int q = 0; q < M; ++q) {
-    const double bi = sT[iy * M + q], di = sT[N * M + iy * M + q];
-    const double bj = sT[jy * M + q], dj = sT[N * M + jy * M + q];
-    py[0][q] = bi * bj;
-    py[1][q] = bi * dj;
-    py[2][q] = di * bj;
-    py[3][q] = di * dj;
-  }
 
+  // ---- K at every point: threads over (cell, qx, qy, qz) -------------------
+  for (int t = tid; t < CPB * M3; t += C::THREADS) {
+    const int cc = t / M3, rr = t - cc * M3;
+    const int qx = rr / (M * M), qy = (rr / M) % M, qz = rr % M;
+    HexLineGeom geo;
+    geo.setup(sC + cc * 24, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
+    double r0[3], r1[3], r2[3];
+    const double det = geo.adj(T.Bc[qz], T.Bc[M + qz], r0, r1, r2);
+    const double s = ((T.W[qx] * T.W[qy]) * T.W[qz]) * rcp64(fabs(det));
+    double* k = sK + cc * C::KS + rr;
+    const double* rows[3] = {r0, r1, r2};
 #pragma unroll
-  for (int qx = 0; qx < M; ++qx) {
-    // ---- K at the plane qx: threads over (cell, qy, qz) ------------------
-    for (int t = tid; t < CPB * M * M; t += C::THREADS) {
-      const int cc = t / (M * M), rr = t - cc * (M * M);
-      const int qy = rr / M, qz = rr - qy * M;
-      HexLineGeom geo;  // line (qx, qy, *) evaluated at qz
-      geo.setup(sC + cc * 24, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
-      double r0[3], r1[3], r2[3];
-      const double det = geo.adj(T.Bc[qz], T.Bc[M + qz], r0, r1, r2);
-      const double s = ((T.W[qx] * T.W[qy]) * T.W[qz]) * rcp64(fabs(det));
-      double* k = sK + cc * C::KS + rr;
-      const double* rows[3] = {r0, r1, r2};
+    for (int l = 0; l < 3; ++l)
 #pragma unroll
-      for (int l = 0; l < 3; ++l)
+      for (int m2 = l; m2 < 3; ++m2) {
+        const double* a = rows[l];
+        const double* b = rows[m2];
+        k[ksym(l, m2) * M3] = s * fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0]));
+      }
+  }
+  __syncthreads();
+  // ---- Z_ll'[qx][qy][iz][jz]: threads over (cell, pair, qx, qy, iz, jz) -----
+  for (int t = tid; t < CPB * C::ZS; t += C::THREADS) {
+    const int cc = t / C::ZS, rr = t - cc * C::ZS;
+    const int pair = rr / (M * M * N2), q2 = rr - pair * (M * M * N2);
+    const int qxy = q2 / N2, zz = q2 - qxy * N2;
+    const int a = zz / N, b = zz - a * N;
+    const int l = pair / 3, lp = pair - 3 * l;
+    const double* ta = sT + (l == 2 ? N * M : 0) + a * M;
+    const double* tb = sT + (lp == 2 ? N * M : 0) + b * M;
+    const double* k = sK + cc * C::KS + ksym(l, lp) * M3 + qxy * M;
+    double z = 0.0;
 #pragma unroll
-        for (int m2 = l; m2 < 3; ++m2) {
-          const double* a = rows[l];
-          const double* b = rows[m2];
-          k[ksym(l, m2) * M * M] = s * fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0]));
-        }
+    for (int qz = 0; qz < M; ++qz) z = fma(ta[qz] * tb[qz], k[qz], z);
+    sZ[cc * C::ZS + rr] = z;
+  }
+  __syncthreads();
+  // ---- y contraction into the 4 x-pattern groups, every plane ---------------
+  if (act) {
+    double py[4][M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) {
+      const double bi = sT[iy * M + q], di = sT[N * M + iy * M + q];
+      const double bj = sT[jy * M + q], dj = sT[N * M + jy * M + q];
+      py[0][q] = bi * bj;
+      py[1][q] = bi * dj;
+      py[2][q] = di * bj;
+      py[3][q] = di * dj;
     }
-    __syncthreads();
-    // ---- Z_ll'[qy][iz][jz] for the plane: threads over (cell, pair, qy, iz, jz)
-    for (int t = tid; t < CPB * C::ZS; t += C::THREADS) {
-      const int cc = t / C::ZS, rr = t - cc * C::ZS;
-      const int pair = rr / (M * N2), q2 = rr - pair * (M * N2);
-      const int qy = q2 / N2, zz = q2 - qy * N2;
-      const int a = zz / N, b = zz - a * N;
-      const int l = pair / 3, lp = pair - 3 * l;
-      const double* ta = sT + (l == 2 ? N * M : 0) + a * M;
-      const double* tb = sT + (lp == 2 ? N * M : 0) + b * M;
-      const double* k = sK + cc * C::KS + ksym(l, lp) * M * M + qy * M;
-      double z = 0.0;
-#pragma unroll
-      for (int qz = 0; qz < M; ++qz) z = fma(ta[qz] * tb[qz], k[qz], z);
-      sZ[cc * C::ZS + rr] = z;
-    }
-    __syncthreads();
-    // ---- y contraction into the 4 x-pattern groups, then x accumulation --
-    if (act) {
-      const double* z = sZ + c * C::ZS + iz * N + jz;
+#pragma unroll 1
+    for (int qx = 0; qx < M; ++qx) {
+      const double* z = sZ + c * C::ZS + qx * M * N2 + iz * N + jz;
       double yg[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int l = 0; l < 3; ++l)
@@ -140,26 +147,40 @@ hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncell
         for (int lp = 0; lp < 3; ++lp) {
           const int pat = (l == 1 ? 2 : 0) + (lp == 1 ? 1 : 0);
           const int grp = (l == 0 ? 2 : 0) + (lp == 0 ? 1 : 0);
-          const double* zp = z + (l * 3 + lp) * M * N2;
+          const double* zp = z + (l * 3 + lp) * M * M * N2;
 #pragma unroll
           for (int qy = 0; qy < M; ++qy) yg[grp] = fma(py[pat][qy], zp[qy * N2], yg[grp]);
         }
+      double* y = sY + c * C::YS + qx * N4 + r;
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const double* ta = (g & 2) ? T.D : T.B;  // test  (row) x-table
-        const double* tb = (g & 1) ? T.D : T.B;  // trial (col) x-table
+      for (int g = 0; g < 4; ++g) y[g * M * N4] = yg[g];
+    }
+  }
+  __syncthreads();
+
+  // ---- phase B: x contraction and store --------------------------------------
+  if (act && c < ncb) {
+    double acc[N][N];
+#pragma unroll
+    for (int ix = 0; ix < N; ++ix)
+#pragma unroll
+      for (int jx = 0; jx < N; ++jx) acc[ix][jx] = 0.0;
+    const double* y = sY + c * C::YS + r;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const double* ta = (g & 2) ? T.D : T.B;  // test  (row) x-table
+      const double* tb = (g & 1) ? T.D : T.B;  // trial (col) x-table
+#pragma unroll
+      for (int qx = 0; qx < M; ++qx) {
+        const double v = y[(g * M + qx) * N4];
 #pragma unroll
         for (int jx = 0; jx < N; ++jx) {
-          const double t = tb[jx * M + qx] * yg[g];
+          const double t = tb[jx * M + qx] * v;
 #pragma unroll
           for (int ix = 0; ix < N; ++ix) acc[ix][jx] = fma(ta[ix * M + qx], t, acc[ix][jx]);
         }
       }
     }
-    __syncthreads();
-  }
-
-  if (act && c < ncb) {
     double* out = A + (cell0 + c) * (int64_t)(N3 * N3);
     const int rowoff = iy * N + iz;   // + ix * N2  -> test index
     const int coloff = jy * N + jz;   // + jx * N2  -> trial index
@@ -187,7 +208,11 @@ static int launch_mat(const sfk_plan* p, int64_t ncells, double* A, const double
     T.Bc[M + q] = p->Bc[p->m + q];
   }
   const unsigned grid = (unsigned)((ncells + CPB - 1) / CPB);
-  hex_laplace_matrix_kernel<N, M, CPB><<<grid, C::THREADS, 0, s>>>(T, ncells, coords, A);
+  auto kern = hex_laplace_matrix_kernel<N, M, CPB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)C::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_matrix)");
+  kern<<<grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, A);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_matrix_kernel launch");
 }
