@@ -13,13 +13,14 @@
 // per displacement component (3 x 8 forward, 3 x 8 transposed), with m =
 // n + 1 points per axis.
 //
-// B200 mapping: the scalar line kernel (hex_action.cu) extended to three
-// components.  The forward x/y stages run component by component through a
-// shared X buffer into a 9-array Y buffer whose z-lines are stored with a
+// B200 mapping: the scalar line kernel (hex_action2.cu) extended to three
+// components; persistent CTAs with cp.async prefetch of the next batch.
+// The forward x/y stages run component by component through a shared X buffer into a 9-array Y buffer whose z-lines are stored with a
 // stride >= m, so that each z-line thread can overwrite, in place, its own
 // 9 lines with (1) the 9 reference-gradient lines, (2) the 9 flux lines and
 // (3) the 9 transposed-z lines — no extra shared memory and no barrier
 // between those three steps.  Transposed y/x stages then run per component.
+#include "async_copy.cuh"
 #include "hex_geometry.cuh"
 
 namespace sfk {
@@ -34,7 +35,10 @@ struct NeoCfg {
   static constexpr int XSZ = 2 * XA;
   static constexpr int YA = MM * LZ;           // one Y array per cell
   static constexpr int YSZ = 9 * YA;
-  static constexpr size_t SMEM = (size_t)CPB * (XSZ + YSZ + 24) * sizeof(double);
+  static constexpr int USZ = round_up(CPB * 3 * N * N * N + 1, 2);   // u of one batch
+  static constexpr int CSZ = CPB * 24;
+  static constexpr size_t SMEM =
+      (size_t)(round_up(CPB * (XSZ + YSZ), 2) + USZ + 2 * CSZ) * sizeof(double);
 };
 
 template <int N, int M, int CPB>
@@ -46,16 +50,34 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
   constexpr int NN = C::NN, MN = C::MN, MM = C::MM, PX = C::PX, LZ = C::LZ;
   constexpr int XA = C::XA, YA = C::YA;
   constexpr int N3 = N * NN;
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   double* sX = smem;
   double* sY = sX + CPB * C::XSZ;
-  double* sC = sY + CPB * C::YSZ;
+  double* sU = smem + round_up(CPB * (C::XSZ + C::YSZ), 2);
+  double* sCo = sU + C::USZ;
   const int tid = threadIdx.x;
-  const int64_t cell0 = (int64_t)blockIdx.x * CPB;
-  const int64_t rem = ncells - cell0;
-  const int ncb = rem < CPB ? (int)rem : CPB;
-  for (int i = tid; i < CPB * 24; i += C::THREADS)
-    sC[i] = i < ncb * 24 ? __ldg(coords + cell0 * 24 + i) : 0.0;
+  const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  // persistent CTAs: u (3 components interleaved, as stored) and coords of
+  // the next batch stream into shared memory with cp.async while the current
+  // batch computes (u once the last x stage consumed it, coords
+  // double-buffered because the z stage needs them)
+  auto prefetch = [&](int64_t bt, int buf) {
+    const int64_t c0 = bt * CPB;
+    const int nc = (int)((ncells - c0) < CPB ? (ncells - c0) : CPB);
+    const double* src = u + c0 * (3 * N3);
+    async_copy_phase<C::THREADS>(sU + dst_shift(src), src, nc * 3 * N3, tid);
+    async_copy<C::THREADS>(sCo + buf * C::CSZ, coords + c0 * 24, nc * 24, tid);
+    cp_async_commit();
+  };
+  int64_t batch = blockIdx.x;
+  if (batch < nbatch) prefetch(batch, 0);
+  for (int it = 0; batch < nbatch; batch += gridDim.x, ++it) {
+  const int64_t cell0 = batch * CPB;
+  const int ncb = (int)((ncells - cell0) < CPB ? (ncells - cell0) : CPB);
+  cp_async_wait<0>();
+  __syncthreads();
+  const double* sC = sCo + (it & 1) * C::CSZ;
+  const double* su = sU + dst_shift(u + cell0 * (3 * N3));
 
   // ---------------- forward x / y stages, per component -------------------
 #pragma unroll 1
@@ -63,9 +85,9 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
     if (tid < CPB * NN) {
       const int c = tid / NN, r = tid - c * NN;
       double uu[N];
-      const double* up = u + (cell0 + c) * (3 * N3) + 3 * r + a;
+      const double* up = su + c * (3 * N3) + 3 * r + a;
 #pragma unroll
-      for (int i = 0; i < N; ++i) uu[i] = c < ncb ? __ldg(up + 3 * i * NN) : 0.0;
+      for (int i = 0; i < N; ++i) uu[i] = c < ncb ? up[3 * i * NN] : 0.0;
       double* xo = sX + c * C::XSZ + r;
 #pragma unroll
       for (int q = 0; q < M; ++q) {
@@ -80,6 +102,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
       }
     }
     __syncthreads();
+    if (a == 2 && batch + gridDim.x < nbatch) prefetch(batch + gridDim.x, (it & 1) ^ 1);
     if (tid < CPB * MN) {
       const int c = tid / MN, r = tid - c * MN;
       const int qx = r / N, iz = r - qx * N;
@@ -268,6 +291,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
     }
     __syncthreads();
   }
+  }  // persistent batch loop
 }
 
 template <int N, int M, int CPB>
@@ -278,8 +302,17 @@ static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)C::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(neohookean)");
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C::THREADS, C::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "occupancy(neohookean)");
+  if (per_sm < 1) return fail(SFK_ECUDA, "neo-Hookean kernel does not fit on an SM");
   const Tabs<N, M> T = make_tabs<N, M>(p);
-  const unsigned grid = (unsigned)((ncells + CPB - 1) / CPB);
+  const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  const int64_t resident = (int64_t)sms * per_sm;
+  const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
   k<<<grid, C::THREADS, C::SMEM, s>>>(T, p->params[0], p->params[1], ncells, coords, u, A);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_neohookean_kernel launch");
@@ -293,8 +326,8 @@ int launch_hex_neohookean(const sfk_plan* p, int64_t ncells, double* A, const do
       case 2: return launch_neo<2, 3, 16>(p, ncells, A, coords, w0, s);
       case 3: return launch_neo<3, 4, 16>(p, ncells, A, coords, w0, s);
       case 4: return launch_neo<4, 5, 8>(p, ncells, A, coords, w0, s);
-      case 5: return launch_neo<5, 6, 4>(p, ncells, A, coords, w0, s);
-      case 6: return launch_neo<6, 7, 4>(p, ncells, A, coords, w0, s);
+      case 5: return launch_neo<5, 6, 3>(p, ncells, A, coords, w0, s);
+      case 6: return launch_neo<6, 7, 3>(p, ncells, A, coords, w0, s);
       case 7: return launch_neo<7, 8, 2>(p, ncells, A, coords, w0, s);
       default: break;
     }
