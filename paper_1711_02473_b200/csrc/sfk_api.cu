@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 
 #include "sfk_internal.cuh"
@@ -105,6 +106,47 @@ static int dispatch(const sfk_plan* p, int64_t ncells, double* A,
     default:
       return fail(SFK_EUNSUPPORTED, "unknown kernel kind %d", p->kind);
   }
+}
+
+
+// Per-device staging for sfk_eval_host: streams and device buffers are
+// created once and reused (the r01 version allocated them per call, which
+// cost milliseconds on small batches).  Calls on one device serialise on the
+// context mutex.
+struct HostCtx {
+  static constexpr int NS = 4;
+  std::mutex mu;
+  bool init = false;
+  cudaStream_t stream[NS] = {};
+  double* buf[NS] = {};
+  size_t cap = 0;
+  int reserve(size_t bytes) {
+    if (!init) {
+      for (int i = 0; i < NS; ++i) {
+        int rc = cuda_status(cudaStreamCreateWithFlags(&stream[i], cudaStreamNonBlocking),
+                             "cudaStreamCreate(eval_host)");
+        if (rc != SFK_OK) return rc;
+      }
+      init = true;
+    }
+    if (bytes <= cap) return SFK_OK;
+    for (int i = 0; i < NS; ++i) {
+      if (buf[i]) cudaFree(buf[i]);
+      buf[i] = nullptr;
+    }
+    cap = 0;
+    for (int i = 0; i < NS; ++i) {
+      int rc = cuda_status(cudaMalloc(&buf[i], bytes), "cudaMalloc(eval_host staging)");
+      if (rc != SFK_OK) return rc;
+    }
+    cap = bytes;
+    return SFK_OK;
+  }
+};
+
+static HostCtx* host_ctx(int dev) {
+  static HostCtx ctx[64];
+  return (dev >= 0 && dev < 64) ? &ctx[dev] : nullptr;
 }
 
 static int validate(const sfk_plan* p, int64_t ncells, const double* A,
@@ -233,27 +275,28 @@ int sfk_eval_host(const sfk_plan* p, int64_t ncells, double* A, const double* co
   if (st != SFK_OK || ncells == 0) return st;
   const int64_t per_cell = p->coords_size + p->w0_size + p->w1_size + p->a_size;
   if (chunk <= 0) {
-    // ~64 MiB of traffic per chunk: big enough to amortise launch + copy
-    // latency, small enough for 3-deep pipelining.
+    // ~64 MiB of traffic per chunk: H2D of chunk k+1, the kernel of chunk k
+    // and the D2H of chunk k-1 overlap (separate copy engines per direction;
+    // tools/pcie_probe.py: 55 GB/s H2D, 57 GB/s D2H, 100 GB/s concurrent)
     chunk = (int64_t)((64ll << 20) / (8 * per_cell));
     if (chunk < 1024) chunk = 1024;
   }
   if (chunk > ncells) chunk = ncells;
-  constexpr int NS = 3;
-  cudaStream_t st3[NS] = {nullptr, nullptr, nullptr};
-  double* dbuf[NS] = {nullptr, nullptr, nullptr};
-  int rc = SFK_OK;
+  int dev = 0;
+  int rc = cuda_status(cudaGetDevice(&dev), "cudaGetDevice");
+  if (rc != SFK_OK) return rc;
+  HostCtx* ctx = host_ctx(dev);
+  if (!ctx) return fail(SFK_EINVAL, "device %d out of range for sfk_eval_host", dev);
+  std::lock_guard<std::mutex> lock(ctx->mu);
   const size_t bytes = (size_t)chunk * per_cell * sizeof(double);
-  for (int i = 0; i < NS && rc == SFK_OK; ++i) {
-    rc = cuda_status(cudaStreamCreateWithFlags(&st3[i], cudaStreamNonBlocking), "cudaStreamCreate");
-    if (rc == SFK_OK) rc = cuda_status(cudaMalloc(&dbuf[i], bytes), "cudaMalloc(eval_host staging)");
-  }
+  rc = ctx->reserve(bytes);
+  if (rc != SFK_OK) return rc;
   int64_t k = 0;
   for (int64_t c0 = 0; c0 < ncells && rc == SFK_OK; c0 += chunk, ++k) {
     const int64_t nc = (ncells - c0) < chunk ? (ncells - c0) : chunk;
-    const int i = (int)(k % NS);
-    cudaStream_t s = st3[i];
-    double* dc = dbuf[i];
+    const int i = (int)(k % HostCtx::NS);
+    cudaStream_t s = ctx->stream[i];
+    double* dc = ctx->buf[i];
     double* dw0 = dc + chunk * p->coords_size;
     double* dw1 = dw0 + chunk * p->w0_size;
     double* dA = dw1 + chunk * p->w1_size;
@@ -272,13 +315,9 @@ int sfk_eval_host(const sfk_plan* p, int64_t ncells, double* A, const double* co
       rc = cuda_status(cudaMemcpyAsync(A + c0 * p->a_size, dA, nc * p->a_size * sizeof(double),
                                        cudaMemcpyDeviceToHost, s), "D2H A");
   }
-  for (int i = 0; i < NS; ++i) {
-    if (st3[i]) {
-      cudaError_t e = cudaStreamSynchronize(st3[i]);
-      if (rc == SFK_OK) rc = cuda_status(e, "cudaStreamSynchronize(eval_host)");
-      cudaStreamDestroy(st3[i]);
-    }
-    if (dbuf[i]) cudaFree(dbuf[i]);
+  for (int i = 0; i < HostCtx::NS; ++i) {
+    cudaError_t e = cudaStreamSynchronize(ctx->stream[i]);
+    if (rc == SFK_OK) rc = cuda_status(e, "cudaStreamSynchronize(eval_host)");
   }
   return rc;
 }
