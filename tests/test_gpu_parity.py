@@ -266,3 +266,82 @@ def test_c4_vs_oracle(cuda, p):
     ref = cpu.evaluate(plan, small)
     assert not np.isnan(ref).any()
     assert rel_err(_run(cuda, plan, small), ref) < TOL
+
+
+# ---------------------------------------------------------------------------
+# determinism, streams, threads, layouts
+
+
+def test_bitwise_reproducible_and_stream_concurrency(cuda):
+    torch = cuda
+    plans = [compile_kernel("action_laplace", "hex", p) for p in (2, 5, 7, 8)]
+    ins = [_dev(torch, workloads.c2_inputs(p.degree, dims=(8, 8, 9))) for p in plans]
+    ref = [evaluate_batched(p, i) for p, i in zip(plans, ins)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in plans]
+    outs = []
+    for p, i, s in zip(plans, ins, streams):
+        with torch.cuda.stream(s):
+            outs.append(evaluate_batched(p, i))
+    torch.cuda.synchronize()
+    for a, b in zip(ref, outs):
+        assert torch.equal(a, b)      # no atomics anywhere: bitwise identical
+
+
+def test_host_path_thread_safe(cuda):
+    import threading
+
+    plan = compile_kernel("action_laplace", "hex", 3)
+    inp = workloads.c2_inputs(3, dims=(8, 8, 8))
+    expect = evaluate_host(plan, inp)
+    res = [None] * 4
+
+    def work(k):
+        res[k] = evaluate_host(plan, inp, chunk_cells=97 + k)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for r in res:
+        assert np.array_equal(r, expect)
+
+
+def test_non_contiguous_and_offset_inputs(cuda):
+    torch = cuda
+    plan = compile_kernel("action_laplace", "hex", 4)
+    inp = workloads.c2_inputs(4, dims=(4, 4, 5))
+    dev = _dev(torch, inp)
+    # column-sliced (non-contiguous) coords and an odd cell offset (8-byte
+    # aligned only, exercising the cp.async 16-byte phase fix-up)
+    wide = torch.zeros((dev["coords"].shape[0], 30), dtype=torch.float64, device="cuda")
+    wide[:, 3:27] = dev["coords"]
+    off = {"coords": wide[1:, 3:27], "w0": dev["w0"][1:]}
+    got = evaluate_batched(plan, off).cpu().numpy()
+    ref = cpu.evaluate(plan, {k: v[1:] for k, v in inp.items()})
+    assert rel_err(got, ref) < TOL
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_c2_every_kernel_generation(cuda, p):
+    """Each C2 kernel generation that has an instance for n = p+1 agrees with
+    the oracle (the auto selection only changes speed, never results)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, torch, sys; sys.path.insert(0, %r);"
+        "from paper_1711_02473_b200 import compile_kernel, evaluate_batched, workloads;"
+        "from oracle import cpu;"
+        "plan = compile_kernel('action_laplace', 'hex', %d);"
+        "inp = workloads.c2_inputs(%d, dims=(5, 5, 7));"
+        "out = evaluate_batched(plan, {k: torch.from_numpy(v).cuda() for k, v in inp.items()}).cpu().numpy();"
+        "ref = cpu.evaluate(plan, inp);"
+        "err = (np.abs(out-ref).max(axis=1)/np.abs(ref).max(axis=1)).max();"
+        "print(err); assert err < 1e-12"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), p, p)
+    for gen in ("v1", "v2", "v3", "tc", "cell"):
+        env = dict(os.environ, SFK_C2_KERNEL=gen)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+        assert r.returncode == 0, (gen, r.stdout, r.stderr[-2000:])
