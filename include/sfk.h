@@ -127,6 +127,23 @@ int sfk_eval_host(const sfk_plan *plan, int64_t ncells, double *A,
                   int64_t chunk_cells);
 
 /*
+ * Global (assembled) operator application, matrix-free:
+ *     y += sum_c P_c^T A_c P_c x
+ * P_c gathers the cell's local dofs from the global vector x through
+ * cell_dofs[c][i] (global index of local dof i of cell c, reference local
+ * order (ix*n+iy)*n+iz); A_c is the plan's cell kernel; the scatter-add into
+ * y is fused (fp64 atomics, so the summation order of shared dofs is not
+ * fixed).  DEVICE pointers, stream-ordered; y is accumulated into (zero it
+ * first for y = K x).  Supported: hex action_laplace, GL (m == n).
+ * Replaces: the caller's assembly loop around the emitted kernel — the
+ * "global gather/scatter" next step of SURVEY.md §8(f) (the reference
+ * scopes global assembly out).
+ */
+int sfk_eval_gather_scatter(const sfk_plan *plan, int64_t ncells,
+                            const int32_t *cell_dofs, const double *x,
+                            double *y, const double *coords, void *stream);
+
+/*
  * Functionals/checksums of a device array x[0..n):
  *   out[0] = sum x_i^2,  out[1] = sum x_i        (overwritten)
  * `out` is a DEVICE buffer of at least SFK_SUM_WORKSPACE doubles (the tail is

@@ -41,11 +41,19 @@ struct Act3Layout {
   static_assert(XC >= 2 * XA && YC >= 3 * YA && LZ >= M && LZ >= N, "layout too small");
 };
 
-template <class L, int MINB>
+// GS = false: batched E-vector action, A[c] = A_c u[c] (BASELINE C2).
+// GS = true : global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
+//             item 1): `u` is the global vector x, `A` the global vector y,
+//             cmap[c][i] the global dof of local dof i of cell c.  The gather
+//             is fused into the x stage (x[cmap] read through L1/L2, the map
+//             block itself streamed with cp.async), the scatter into the
+//             transposed x stage (fp64 atomicAdd; neighbouring cells share
+//             face/edge/vertex dofs).
+template <class L, int MINB, bool GS = false>
 __global__ void __launch_bounds__(L::THREADS, MINB)
 hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
-                      double* __restrict__ A) {
+                      double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
   constexpr int N = L::N, M = L::M, CPB = L::CPB, NN = L::NN, MN = L::MN, MM = L::MM;
   constexpr int N3 = L::N3, XY = L::XY, PX = L::PX, XC = L::XC, LZ = L::LZ, YX = L::YX;
   constexpr int YC = L::YC, XA = L::XA, YA = L::YA, TH = L::THREADS;
@@ -57,10 +65,15 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
   const int tid = threadIdx.x;
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
 
+  int* sMap = reinterpret_cast<int*>(sU);   // GS: [2][CPB*N3] in the u buffer
   auto prefetch = [&](int64_t bb, int buf) {
     const int64_t c0 = bb * CPB;
     const int nc = (int)((ncells - c0) < CPB ? (ncells - c0) : CPB);
-    async_copy_phase<TH>(sU + dst_shift(u + c0 * N3), u + c0 * N3, nc * N3, tid);
+    if (GS) {
+      for (int i = tid; i < nc * N3; i += TH) cp_async4(sMap + buf * CPB * N3 + i, cmap + c0 * N3 + i);
+    } else {
+      async_copy_phase<TH>(sU + dst_shift(u + c0 * N3), u + c0 * N3, nc * N3, tid);
+    }
     async_copy<TH>(sCo + buf * L::CSZ, coords + c0 * 24, nc * 24, tid);
     cp_async_commit();
   };
@@ -79,11 +92,13 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
     if (tid < CPB * NN) {
       const int c = tid / NN, r = tid - c * NN;
       const int iy = r / N, iz = r - iy * N;
-      const double* ui = sU + dst_shift(u + cell0 * N3) + c * N3 + r;
+      const double* ui = sU + (GS ? 0 : dst_shift(u + cell0 * N3)) + c * N3 + r;
+      const int* mi = sMap + cur * CPB * N3 + c * N3 + r;
       const bool live = c < ncb;
+      auto uval = [&](int i) { return GS ? __ldg(u + mi[i * NN]) : ui[i * NN]; };
       double xb[M], xd[M];
       {
-        const double v = live ? ui[0] : 0.0;
+        const double v = live ? uval(0) : 0.0;
 #pragma unroll
         for (int q = 0; q < M; ++q) {
           xb[q] = T.B[q] * v;
@@ -92,7 +107,7 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
       }
 #pragma unroll
       for (int i = 1; i < N; ++i) {
-        const double v = live ? ui[i * NN] : 0.0;
+        const double v = live ? uval(i) : 0.0;
 #pragma unroll
         for (int q = 0; q < M; ++q) {
           xb[q] = fma(T.B[i * M + q], v, xb[q]);
@@ -282,19 +297,25 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
             a[i] = fma(T.B[i * M + q], p2, a[i]);
           }
         }
-        double* ap = A + (cell0 + c) * N3 + r;
+        if (GS) {
+          const int* mi = sMap + cur * CPB * N3 + c * N3 + r;
 #pragma unroll
-        for (int i = 0; i < N; ++i) ap[i * NN] = a[i];
+          for (int i = 0; i < N; ++i) atomicAdd(A + mi[i * NN], a[i]);
+        } else {
+          double* ap = A + (cell0 + c) * N3 + r;
+#pragma unroll
+          for (int i = 0; i < N; ++i) ap[i * NN] = a[i];
+        }
       }
     }
     __syncthreads();   // X/R is rewritten by the next batch's x stage
   }
 }
 
-template <class L, int MINB>
+template <class L, int MINB, bool GS = false>
 static int launch_v3(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                     const double* u, cudaStream_t s) {
-  auto kern = hex_laplace_action_v3<L, MINB>;
+                     const double* u, cudaStream_t s, const int* cmap = nullptr) {
+  auto kern = hex_laplace_action_v3<L, MINB, GS>;
   static int sms = 0, per_sm = 0;
   if (!sms) {
     int dev = 0;
@@ -312,26 +333,37 @@ static int launch_v3(const sfk_plan* p, int64_t ncells, double* A, const double*
   const int64_t nbatch = (ncells + L::CPB - 1) / L::CPB;
   const int64_t resident = (int64_t)sms * per_sm;
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
-  kern<<<grid, L::THREADS, L::SMEM, s>>>(T, ncells, coords, u, A);
+  kern<<<grid, L::THREADS, L::SMEM, s>>>(T, ncells, coords, u, A, cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_v3 launch");
 }
 
 // (N, M, CPB, XY, PX, XC, LZ, YX, YC) from tools/smem_pads_action.py
-int launch_hex_action_v3(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                         const double* w0, cudaStream_t s) {
+template <bool GS>
+static int dispatch_v3(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                       const double* w0, cudaStream_t s, const int* cmap) {
   if (p->n != p->m) return SFK_EUNSUPPORTED;
   switch (p->n) {
-    case 2: return launch_v3<Act3Layout<2, 2, 64, 2, 6, 28, 3, 6, 36>, 2>(p, ncells, A, coords, w0, s);
-    case 3: return launch_v3<Act3Layout<3, 3, 32, 3, 19, 121, 3, 9, 91>, 2>(p, ncells, A, coords, w0, s);
-    case 4: return launch_v3<Act3Layout<4, 4, 16, 4, 20, 160, 5, 20, 240>, 2>(p, ncells, A, coords, w0, s);
-    case 5: return launch_v3<Act3Layout<5, 5, 10, 5, 37, 377, 5, 25, 381>, 2>(p, ncells, A, coords, w0, s);
-    case 6: return launch_v3<Act3Layout<6, 6, 8, 6, 38, 468, 9, 54, 980>, 2>(p, ncells, A, coords, w0, s);
-    case 7: return launch_v3<Act3Layout<7, 7, 5, 7, 55, 785, 9, 63, 1337>, 2>(p, ncells, A, coords, w0, s);
-    case 8: return launch_v3<Act3Layout<8, 8, 4, 8, 72, 1152, 9, 72, 1728>, 2>(p, ncells, A, coords, w0, s);
-    case 9: return launch_v3<Act3Layout<9, 9, 3, 9, 89, 1617, 9, 81, 2201>, 2>(p, ncells, A, coords, w0, s);
+    case 2: return launch_v3<Act3Layout<2, 2, 64, 2, 6, 28, 3, 6, 36>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
+    case 3: return launch_v3<Act3Layout<3, 3, 32, 3, 19, 121, 3, 9, 91>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
+    case 4: return launch_v3<Act3Layout<4, 4, 16, 4, 20, 160, 5, 20, 240>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
+    case 5: return launch_v3<Act3Layout<5, 5, 10, 5, 37, 377, 5, 25, 381>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
+    case 6: return launch_v3<Act3Layout<6, 6, 8, 6, 38, 468, 9, 54, 980>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
+    case 7: return launch_v3<Act3Layout<7, 7, 5, 7, 55, 785, 9, 63, 1337>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
+    case 8: return launch_v3<Act3Layout<8, 8, 4, 8, 72, 1152, 9, 72, 1728>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
+    case 9: return launch_v3<Act3Layout<9, 9, 3, 9, 89, 1617, 9, 81, 2201>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
     default: return SFK_EUNSUPPORTED;
   }
+}
+
+int launch_hex_action_v3(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                         const double* w0, cudaStream_t s) {
+  return dispatch_v3<false>(p, ncells, A, coords, w0, s, nullptr);
+}
+
+int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                         double* y, const double* coords, cudaStream_t s) {
+  return dispatch_v3<true>(p, ncells, y, coords, x, s, cmap);
 }
 
 }  // namespace sfk

@@ -326,6 +326,18 @@ int sfk_eval_host(const sfk_plan* p, int64_t ncells, double* A, const double* co
   return rc;
 }
 
+int sfk_eval_gather_scatter(const sfk_plan* p, int64_t ncells, const int32_t* cell_dofs,
+                            const double* x, double* y, const double* coords, void* stream) {
+  if (!p) return fail(SFK_EINVAL, "plan is NULL");
+  if (ncells < 0) return fail(SFK_EINVAL, "ncells < 0");
+  if (ncells == 0) return SFK_OK;
+  if (!cell_dofs || !x || !y || !coords) return fail(SFK_EINVAL, "NULL pointer argument");
+  if (p->kind != SFK_KIND_ACTION_LAPLACE || p->dim != 3 || p->collocated || p->n != p->m)
+    return fail(SFK_EUNSUPPORTED,
+                "gather/scatter operator: hex action_laplace with m == n only");
+  return launch_hex_action_gs(p, ncells, cell_dofs, x, y, coords, (cudaStream_t)stream);
+}
+
 int sfk_sum_squares(const double* x, int64_t n, double* out, void* stream) {
   if (n < 0) return fail(SFK_EINVAL, "n < 0");
   if (!out) return fail(SFK_EINVAL, "out is NULL");

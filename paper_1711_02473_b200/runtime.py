@@ -38,6 +38,7 @@ EXPORTED_SYMBOLS = (
     "sfk_abi_version", "sfk_plan_create", "sfk_plan_destroy", "sfk_plan_sizes",
     "sfk_eval", "sfk_eval_pair", "sfk_eval_host", "sfk_sum_squares",
     "sfk_launch_count", "sfk_last_error", "sfk_device_info", "sfk_fp64_peak",
+    "sfk_eval_gather_scatter",
 )
 ABI_VERSION = 1
 SUM_WORKSPACE = 1024
@@ -73,6 +74,8 @@ def _declare(lib):
     lib.sfk_device_info.restype = ci
     lib.sfk_fp64_peak.argtypes = [ctypes.c_double, _dp, _dp]
     lib.sfk_fp64_peak.restype = ci
+    lib.sfk_eval_gather_scatter.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, _vp]
+    lib.sfk_eval_gather_scatter.restype = ci
 
 
 def load_library(build_if_missing=True):

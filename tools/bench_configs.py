@@ -150,6 +150,34 @@ def main():
                 out = torch.empty_like(d["w0"])
                 report("C2", plan, inp, (p + 1) ** 3, sfk(plan, d, out))
                 del d, out
+        elif cfg == "C2G":
+            # global matrix-free operator: fused gather +
+            # action + atomic scatter on the (64,64,64) lattice's continuous Q_p
+            from paper_1711_02473_b200.assembly import (GlobalOperator, lattice_dof_map,
+                                                        lattice_ndofs)
+            for p in range(1, 9):
+                if args.p and p not in args.p:
+                    continue
+                plan = compile_kernel("action_laplace", "hex", p)
+                dims = (64, 64, 64)
+                coords = torch.from_numpy(workloads.lattice_coords(*dims)).to(dev)
+                gmap = torch.from_numpy(lattice_dof_map(*dims, p)).to(dev)
+                nd = lattice_ndofs(*dims, p)
+                op = GlobalOperator(plan, gmap, coords, nd)
+                x = torch.rand(nd, dtype=torch.float64, device=dev)
+                y = torch.zeros_like(x)
+                t = time_launch(lambda: op.apply(x, out=y, accumulate=True))
+                C = coords.shape[0]
+                # compulsory bytes: coords + map (int32) + x, y (read+write) once
+                byt = C * (24 * 8 + 4 * (p + 1) ** 3) + 3 * 8 * nd
+                rec = {"config": "C2G", "form": "global action_laplace (gather-scatter)", "p": p,
+                       "cells": C, "global_dofs": nd, "ms": round(t * 1e3, 5),
+                       "gdofs_local": round(C * (p + 1) ** 3 / t / 1e9, 3),
+                       "gdofs_global": round(nd / t / 1e9, 3),
+                       "roofline_frac": round(C * max(byt / C / (hbm * 1e9),
+                                                      plan.algorithmic_flops / (p64 * 1e12)) / t, 4)}
+                print(json.dumps(rec), flush=True)
+                del coords, gmap, x, y
         elif cfg == "C3":
             spec = action_form(REGISTRY["weighted_laplace"])
             for p in range(4, 17):
