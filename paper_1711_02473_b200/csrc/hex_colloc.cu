@@ -46,11 +46,20 @@ struct CollocCfg {
   }
 };
 
+// Register policy per n, from same-box A/B runs (profiles/r01ae_*): 2 =
+// __launch_bounds__(T, 2) (two CTAs per SM, no spills at that cap), 1 =
+// (T, 1), 0 = (T) only — ptxas picks different (and here faster) register
+// budgets for the last two (e.g. n = 16: 132 vs 254 registers).
+__host__ __device__ constexpr int colloc_minb(int n) {
+  return (n <= 5 || n == 7 || n == 9 || n == 11 || n == 16) ? 2 : (n == 8 || n == 15) ? 0 : 1;
+}
+
 template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED>
-__global__ void __launch_bounds__(CollocCfg<N, CPB, SY, SX, CS>::THREADS)
-hex_colloc_action_kernel(const __grid_constant__ TabsD<N> T, int64_t ncells,
-                         const double* __restrict__ coords, const double* __restrict__ u,
-                         const double* __restrict__ kappa, double* __restrict__ A) {
+__device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
+                                            const double* __restrict__ coords,
+                                            const double* __restrict__ u,
+                                            const double* __restrict__ kappa,
+                                            double* __restrict__ A) {
   using C = CollocCfg<N, CPB, SY, SX, CS>;
   constexpr int NN = C::NN, N3 = C::N3;
   extern __shared__ double smem[];
@@ -71,10 +80,11 @@ hex_colloc_action_kernel(const __grid_constant__ TabsD<N> T, int64_t ncells,
   for (int i = tid; i < CPB * 24; i += C::THREADS)
     sC[i] = i < ncb * 24 ? __ldg(coords + cell0 * 24 + i) : 0.0;
   {
+    // consecutive threads copy consecutive doubles (coalesced global reads)
     const double* ug = u + cell0 * N3;
     for (int i = tid; i < ncb * N3; i += C::THREADS) {
       const int c = i / N3, r = i - c * N3;
-      const int x = r / NN, y = (r / N) % N, z = r % N;
+      const int x = r / NN, yz = r - x * NN, y = yz / N, z = yz - y * N;
       cp_async8(sU + c * CS + x * SX + y * SY + z, ug + i);
     }
     cp_async_commit();
@@ -82,7 +92,7 @@ hex_colloc_action_kernel(const __grid_constant__ TabsD<N> T, int64_t ncells,
       const double* kg = kappa + cell0 * N3;
       for (int i = tid; i < ncb * N3; i += C::THREADS) {
         const int c = i / N3, r = i - c * N3;
-        const int x = r / NN, y = (r / N) % N, z = r % N;
+        const int x = r / NN, yz = r - x * NN, y = yz / N, z = yz - y * N;
         cp_async8(sK + c * CS + x * SX + y * SY + z, kg + i);
       }
       cp_async_commit();
@@ -188,13 +198,38 @@ hex_colloc_action_kernel(const __grid_constant__ TabsD<N> T, int64_t ncells,
   __syncthreads();
 
   {
+    // coalesced write-back: consecutive threads take consecutive elements of
+    // the batch; the (c, x, y, z) decomposition is incremental per thread
     double* ag = A + cell0 * N3;
     for (int i = tid; i < ncb * N3; i += C::THREADS) {
       const int cc = i / N3, rr = i - cc * N3;
-      const int x = rr / NN, y = (rr / N) % N, z = rr % N;
+      const int x = rr / NN, yz = rr - x * NN, y = yz / N, z = yz - y * N;
       ag[i] = sU[cc * CS + x * SX + y * SY + z];
     }
   }
+}
+
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, int MINB>
+__global__ void __launch_bounds__(CollocCfg<N, CPB, SY, SX, CS>::THREADS, MINB)
+hex_colloc_action_kernel(const __grid_constant__ TabsD<N> T, int64_t ncells,
+                         const double* __restrict__ coords, const double* __restrict__ u,
+                         const double* __restrict__ kappa, double* __restrict__ A) {
+  colloc_body<N, CPB, SY, SX, CS, WEIGHTED>(T, ncells, coords, u, kappa, A);
+}
+
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED>
+__global__ void __launch_bounds__(CollocCfg<N, CPB, SY, SX, CS>::THREADS)
+hex_colloc_action_kernel_free(const __grid_constant__ TabsD<N> T, int64_t ncells,
+                              const double* __restrict__ coords, const double* __restrict__ u,
+                              const double* __restrict__ kappa, double* __restrict__ A) {
+  colloc_body<N, CPB, SY, SX, CS, WEIGHTED>(T, ncells, coords, u, kappa, A);
+}
+
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED>
+static auto colloc_kernel() {
+  constexpr int mb = colloc_minb(N);
+  if constexpr (mb == 0) return hex_colloc_action_kernel_free<N, CPB, SY, SX, CS, WEIGHTED>;
+  else return hex_colloc_action_kernel<N, CPB, SY, SX, CS, WEIGHTED, mb>;
 }
 
 template <int N, int CPB, int SY, int SX, int CS>
@@ -211,12 +246,12 @@ static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* 
   const int64_t grid = (ncells + CPB - 1) / CPB;
   cudaError_t e;
   if (kappa) {
-    auto k = hex_colloc_action_kernel<N, CPB, SY, SX, CS, true>;
+    auto k = colloc_kernel<N, CPB, SY, SX, CS, true>();
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem(true));
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
     k<<<(unsigned)grid, C::THREADS, C::smem(true), s>>>(T, ncells, coords, u, kappa, A);
   } else {
-    auto k = hex_colloc_action_kernel<N, CPB, SY, SX, CS, false>;
+    auto k = colloc_kernel<N, CPB, SY, SX, CS, false>();
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem(false));
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
     k<<<(unsigned)grid, C::THREADS, C::smem(false), s>>>(T, ncells, coords, u, nullptr, A);

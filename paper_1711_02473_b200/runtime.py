@@ -45,7 +45,10 @@ SUM_WORKSPACE = 1024
 
 
 def library_path():
-    return os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsfk.so")
+    """In-tree libsfk.so; SFK_LIBRARY overrides the path (A/B runs of two
+    builds of the same ABI)."""
+    return os.environ.get("SFK_LIBRARY") or os.path.join(
+        os.path.dirname(os.path.abspath(__file__)), "libsfk.so")
 
 
 def _declare(lib):
@@ -74,8 +77,9 @@ def _declare(lib):
     lib.sfk_device_info.restype = ci
     lib.sfk_fp64_peak.argtypes = [ctypes.c_double, _dp, _dp]
     lib.sfk_fp64_peak.restype = ci
-    lib.sfk_eval_gather_scatter.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, _vp]
-    lib.sfk_eval_gather_scatter.restype = ci
+    if hasattr(lib, "sfk_eval_gather_scatter"):   # absent from pre-(f) A/B builds
+        lib.sfk_eval_gather_scatter.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, _vp]
+        lib.sfk_eval_gather_scatter.restype = ci
 
 
 def load_library(build_if_missing=True):
