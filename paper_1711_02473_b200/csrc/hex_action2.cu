@@ -249,14 +249,14 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
         const int c = lc / MM, r = lc - c * MM;
         const int qx = r / M, qy = r - qx * M;
         double* yl = sY + c * C::YSZ + r * LZ;
-        HexLineGeom geo;
+        HexLineAdj geo;
         geo.setup(sC + c * 24, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
         const double wxy = T.W[qx] * T.W[qy];
 #pragma unroll (UP)
         for (int q = 0; q < M; ++q) {
           double gz = yl[q], gy = yl[YA + q], gx = yl[2 * YA + q];
           double r0[3], r1[3], r2[3];
-          const double det = geo.adj(T.Bc[q], T.Bc[M + q], r0, r1, r2);
+          const double det = geo.adj(T.Bc[M + q], r0, r1, r2);
           const double s = (wxy * T.W[q]) * rcp64(fabs(det));
           laplace_flux(r0, r1, r2, s, gx, gy, gz);
           if (on[j]) {
