@@ -24,6 +24,8 @@
 //      A_z = Dz^T f_z in registers, stored over its own U line
 //   4. x-lines: U += Dx^T f_x;   5. y-lines: U += Dy^T f_y
 //   6. coalesced copy U -> A
+#include <type_traits>
+
 #include "async_copy.cuh"
 #include "hex_geometry.cuh"
 
@@ -142,7 +144,11 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
       ul[i] = sU[base + i];
       az[i] = 0.0;
     }
-    HexLineGeom geo;
+    // precomputed adjugate polynomials (hex_geometry.cuh) except at n = 15, 16,
+    // where their 9 extra registers per thread cost more than they save
+    // (same-box A/B, profiles/r01ai_*)
+    using Geo = typename std::conditional<(N == 15 || N == 16), HexLineGeom, HexLineAdj>::type;
+    Geo geo;
     geo.setup(sC + c * 24, T.Bc[a], T.Bc[N + a], T.Bc[b], T.Bc[N + b]);
     const double wxy = T.W[a] * T.W[b];
     const double* kp = sK + base;
@@ -153,7 +159,9 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
       for (int i = 1; i < N; ++i) gz = fma(T.D[i * N + q], ul[i], gz);
       double gx = sGX[base + q], gy = sGY[base + q];
       double r0[3], r1[3], r2[3];
-      const double det = geo.adj(T.Bc[q], T.Bc[N + q], r0, r1, r2);
+      double det;
+      if constexpr (N == 15 || N == 16) det = geo.adj(T.Bc[q], T.Bc[N + q], r0, r1, r2);
+      else det = geo.adj(T.Bc[N + q], r0, r1, r2);
       double s = (wxy * T.W[q]) * rcp64(fabs(det));
       if (WEIGHTED) s *= kp[q];
       laplace_flux(r0, r1, r2, s, gx, gy, gz);

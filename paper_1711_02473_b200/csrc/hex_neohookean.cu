@@ -162,13 +162,13 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
       }
     }
     // (2) pointwise neo-Hookean flux, in place
-    HexLineGeom geo;
+    HexLineAdj geo;
     geo.setup(sC + c * 24, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
     const double wxy = T.W[qx] * T.W[qy];
 #pragma unroll 1
     for (int q = 0; q < M; ++q) {
       double rr[3][3];
-      const double det = geo.adj(T.Bc[q], T.Bc[M + q], rr[0], rr[1], rr[2]);
+      const double det = geo.adj(T.Bc[M + q], rr[0], rr[1], rr[2]);
       const double idet = rcp64(det);
       // grad u_a [k] = (1/det) sum_l r_l[k] d_l u_a ;  F = I + grad u
       double F[3][3];
