@@ -154,6 +154,53 @@ int sfk_eval_gather_scatter(const sfk_plan *plan, int64_t ncells,
 #define SFK_SUM_WORKSPACE 1024
 int sfk_sum_squares(const double *x, int64_t n, double *out, void *stream);
 
+/* ------------------------------------------------------------------------
+ * LoopProgram path: any kernel the reference can
+ * compile, given as its loss-free JSON serialization
+ *     sumfact.scheduling.serialize_program(program)   (scheduling.py:465-532)
+ * of the LoopProgram returned by cli.compile_kernel (cli.py:211-217) or
+ * scheduling.schedule (scheduling.py:341).  libsfk generates a batched
+ * sm_100a kernel from the statement list (one CTA-wide phase per loop nest,
+ * buffers in shared memory, cells across threads) and compiles it with
+ * NVRTC.  Replaces: emit_c + the host C compiler + the caller's per-cell
+ * loop (scheduling.py:617-738).  Without SFK_PROGRAM_FMA every
+ * target element is summed in the reference's loop order with separately
+ * rounded multiplies and adds, i.e. bit-identical to the reference's C
+ * compiled with -ffp-contract=off (IEEE division and sqrt on both sides).
+ * ---------------------------------------------------------------------- */
+typedef struct sfk_program sfk_program;
+
+#define SFK_PROGRAM_FMA 1     /* allow FMA contraction (not bit-exact)       */
+#define SFK_PROGRAM_NO_JIT 2  /* parse + generate only (inspect the source)  */
+
+/* json: the serialize_program text (len < 0: NUL-terminated).  Parses,
+ * generates and JIT-compiles (NVRTC, no GPU needed); the module is loaded on
+ * a device at its first sfk_program_eval there.  Malformed programs ->
+ * SFK_EINVAL (the reference's UnloweredNode / parse errors); NVRTC missing
+ * -> SFK_EUNSUPPORTED. */
+int sfk_program_create(const char *json, int64_t len, int flags,
+                       sfk_program **out);
+int sfk_program_destroy(sfk_program *program);
+
+/* program.return_buffer[1] and the sizes of program.arguments, in order. */
+int sfk_program_sizes(const sfk_program *program, int64_t *return_size,
+                      int *nargs, int64_t *arg_sizes, int max_args);
+
+/* Launch geometry: out[0..8] = cells per CTA, threads, slots per cell,
+ * dynamic smem bytes, global-scratch flag, phases, serial phases, barriers,
+ * cubin bytes. */
+int sfk_program_config(const sfk_program *program, int64_t *out, int n);
+
+/* what = 0: generated CUDA source, 1: kernel entry name, 2: program name. */
+int sfk_program_text(const sfk_program *program, int what, char *buf,
+                     int64_t size, int64_t *length);
+
+/* A[ncells][return_size] = NAME(coords, w0, ...) per cell.  DEVICE pointers
+ * (args[k] is [ncells][arg_sizes[k]], in program.arguments order), enqueued
+ * on `stream`; A is overwritten (the emitted kernel zero-fills it). */
+int sfk_program_eval(const sfk_program *program, int64_t ncells, double *A,
+                     const double *const *args, int nargs, void *stream);
+
 /* Number of sfk kernels launched by this process so far (all threads). */
 int64_t sfk_launch_count(void);
 

@@ -1,6 +1,6 @@
 """In-tree build of libsfk.so (sm_100a) with nvcc.
 
-Every ``csrc/*.cu`` is compiled to an object under ``build/`` (in parallel,
+Every ``csrc/*.cu`` (and host-only ``csrc/*.cpp``) is compiled to an object under ``build/`` (in parallel,
 only when stale) and linked into ``paper_1711_02473_b200/libsfk.so`` with the
 static CUDA runtime, so the library carries no dependency on a particular
 libcudart and travels with the repo snapshot to the GPU box.
@@ -36,6 +36,7 @@ def nvcc():
 
 def _headers():
     return (glob.glob(os.path.join(CSRC, "*.cuh"))
+            + glob.glob(os.path.join(CSRC, "*.h"))
             + glob.glob(os.path.join(INCLUDE, "*.h")))
 
 
@@ -60,12 +61,12 @@ def _compile(src, obj, verbose):
 def build_native(force=False, verbose=False, jobs=None):
     """Build (if stale) and return the path of libsfk.so."""
     os.makedirs(BUILD, exist_ok=True)
-    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     hdrs = _headers()
     objs = []
     todo = []
     for s in srcs:
-        o = os.path.join(BUILD, os.path.basename(s)[:-3] + ".o")
+        o = os.path.join(BUILD, os.path.splitext(os.path.basename(s))[0] + ".o")
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
             todo.append((s, o))
@@ -80,7 +81,7 @@ def build_native(force=False, verbose=False, jobs=None):
             os.remove(o)
     if force or todo or _stale(LIB, objs):
         tmp = LIB + ".tmp"
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart", "static"]
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart", "static", "-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError("link of libsfk.so failed:\n%s\n%s" % (res.stdout, res.stderr))

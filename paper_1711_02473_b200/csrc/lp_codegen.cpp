@@ -1,0 +1,670 @@
+// LoopProgram JSON -> batched sm_100a CUDA kernel.  See lp_program.h for the
+// execution model; the reference semantics followed here are those of
+// emit_c (reference scheduling.py:617-738):
+//   ZeroFill  -> buffer[z] = 0.0                       (:707-709)
+//   Assign    -> target[addr] = expr                   (:710-713)
+//   Accumulate-> target[addr] += expr                  (:714-717)
+//   Delta     -> ((i == j) ? 1.0 : 0.0)                (:666-667)
+//   Comparison-> ((a op b) ? 1.0 : 0.0)                (:685-686)
+//   MathFunction via _C_FUNCTIONS (ln -> log, abs -> fabs)  (:601-602)
+// with row-major strides for Indexed tables / variables (:654-661) and the
+// explicit (offset, terms) address of FlexiblyIndexed (:662-663).
+#include <algorithm>
+#include <cinttypes>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <set>
+#include <sstream>
+#include <stdexcept>
+
+#include "lp_program.h"
+
+namespace sfk {
+namespace lp {
+
+// ---------------------------------------------------------------------------
+// parsing (mirror of parse_program, reference scheduling.py:535-596)
+
+namespace {
+
+struct Reader {
+  Program& P;
+  std::map<std::string, int> table_ids;
+
+  Entry entry(const json::Value& v) {
+    Entry e;
+    if (v.is_arr()) {
+      e.idx = idx(v);
+    } else {
+      e.val = v.i();
+    }
+    return e;
+  }
+  int idx(const json::Value& v) {
+    if (!v.is_arr() || v.size() != 3 || v.at(0).s() != "idx")
+      throw std::runtime_error("LoopProgram: bad index spec");
+    const int id = (int)v.at(1).i();
+    const int ext = (int)v.at(2).i();
+    auto it = P.extents.find(id);
+    if (it != P.extents.end() && it->second != ext)
+      throw std::runtime_error("LoopProgram: index extent mismatch");
+    P.extents[id] = ext;
+    return id;
+  }
+  static std::vector<long long> row_major(const std::vector<long long>& shape) {
+    std::vector<long long> s(shape.size());
+    long long acc = 1;
+    for (size_t k = shape.size(); k-- > 0;) {
+      s[k] = acc;
+      acc *= shape[k];
+    }
+    return s;
+  }
+  int table(const json::Value& t) {
+    Table tb;
+    for (const auto& d : t.at(1).arr) tb.shape.push_back(d.i());
+    for (const auto& x : t.at(2).arr) tb.values.push_back(x.d());
+    long long n = 1;
+    for (auto d : tb.shape) n *= d;
+    if ((long long)tb.values.size() != n) throw std::runtime_error("LoopProgram: table size");
+    std::string key((const char*)tb.shape.data(), tb.shape.size() * sizeof(long long));
+    key.append((const char*)tb.values.data(), tb.values.size() * sizeof(double));
+    auto it = table_ids.find(key);
+    if (it != table_ids.end()) return it->second;
+    const int id = (int)P.tables.size();
+    P.tables.push_back(std::move(tb));
+    table_ids.emplace(std::move(key), id);
+    return id;
+  }
+  ExprP expr(const json::Value& v) {
+    const std::string& tag = v.at(0).s();
+    auto e = std::make_shared<Expr>();
+    if (tag == "lit") {
+      e->k = Expr::LIT;
+      e->lit = v.at(1).d();
+    } else if (tag == "indexed") {
+      const json::Value& base = v.at(1);
+      const json::Value& mi = v.at(2);
+      std::vector<long long> shape;
+      const std::string& btag = base.at(0).s();
+      if (btag == "table") {
+        e->k = Expr::TABLE;
+        e->table = table(base);
+        shape = P.tables[e->table].shape;
+      } else if (btag == "var") {
+        e->k = Expr::LOAD;
+        e->name = base.at(1).s();
+        for (const auto& d : base.at(2).arr) shape.push_back(d.i());
+      } else {
+        throw std::runtime_error("LoopProgram: indexed base '" + btag + "'");
+      }
+      if (shape.size() != mi.size()) throw std::runtime_error("LoopProgram: rank mismatch");
+      const auto strides = row_major(shape);
+      for (size_t k = 0; k < mi.size(); ++k) e->terms.push_back({entry(mi.at(k)), strides[k]});
+    } else if (tag == "flex") {
+      const json::Value& base = v.at(1);
+      if (base.at(0).s() != "var") throw std::runtime_error("LoopProgram: flex base");
+      e->k = Expr::LOAD;
+      e->name = base.at(1).s();
+      e->offset = v.at(2).i();
+      for (const auto& t : v.at(3).arr) e->terms.push_back({entry(t.at(0)), t.at(1).i()});
+    } else if (tag == "delta") {
+      e->k = Expr::DELTA;
+      e->d0 = entry(v.at(1));
+      e->d1 = entry(v.at(2));
+    } else if (tag == "+" || tag == "*" || tag == "/" || tag == "pow" || tag == "min" ||
+               tag == "max") {
+      e->k = tag == "+" ? Expr::ADD : tag == "*" ? Expr::MUL : tag == "/" ? Expr::DIV
+           : tag == "pow" ? Expr::POW : tag == "min" ? Expr::MIN : Expr::MAX;
+      e->a = expr(v.at(1));
+      e->b = expr(v.at(2));
+    } else if (tag == "call") {
+      e->k = Expr::CALL;
+      e->name = v.at(1).s();
+      e->a = expr(v.at(2));
+    } else if (tag == "cmp") {
+      e->k = Expr::CMP;
+      e->name = v.at(1).s();
+      e->a = expr(v.at(2));
+      e->b = expr(v.at(3));
+    } else if (tag == "var" || tag == "table") {
+      throw std::runtime_error("LoopProgram: bare " + tag);
+    } else {
+      throw std::runtime_error("LoopProgram: cannot parse '" + tag + "'");
+    }
+    return e;
+  }
+  void ref(const json::Value& r, Stmt& s) {
+    s.name = r.at(0).s();
+    s.offset = r.at(1).i();
+    for (const auto& t : r.at(2).arr) s.terms.push_back({entry(t.at(0)), t.at(1).i()});
+  }
+  Stmt stmt(const json::Value& v) {
+    const std::string& tag = v.at(0).s();
+    Stmt s;
+    if (tag == "loop") {
+      s.k = Stmt::LOOP;
+      s.idx = idx(v.at(1));
+      s.extent = P.extents[s.idx];
+      for (const auto& b : v.at(2).arr) s.body.push_back(stmt(b));
+    } else if (tag == "assign" || tag == "accumulate") {
+      s.k = tag == "assign" ? Stmt::ASSIGN : Stmt::ACCUM;
+      ref(v.at(1), s);
+      s.e = expr(v.at(2));
+    } else if (tag == "zero") {
+      s.k = Stmt::ZERO;
+      s.name = v.at(1).s();
+      s.size = v.at(2).i();
+    } else {
+      throw std::runtime_error("LoopProgram: unknown statement '" + tag + "'");
+    }
+    return s;
+  }
+};
+
+}  // namespace
+
+Program parse_program(const char* text, size_t n) {
+  const json::Value doc = json::parse(text, n);
+  Program P;
+  Reader r{P, {}};
+  P.name = doc.at("name").s();
+  P.ret_name = doc.at("return").at(0).s();
+  P.ret_size = doc.at("return").at(1).i();
+  for (const auto& a : doc.at("arguments").arr) P.args.emplace_back(a.at(0).s(), a.at(1).i());
+  for (const auto& t : doc.at("temporaries").arr) P.temps.emplace_back(t.at(0).s(), t.at(1).i());
+  for (const auto& s : doc.at("body").arr) P.body.push_back(r.stmt(s));
+  return P;
+}
+
+// ---------------------------------------------------------------------------
+// analysis
+
+namespace {
+
+struct Phase {
+  enum K { ZERO, NEST, SERIAL } k = ZERO;
+  const Stmt* top = nullptr;
+  const Stmt* leaf = nullptr;
+  std::vector<std::pair<int, int>> par, red;   // (index id, extent), nest order
+  long long npar = 1;
+  bool zero_init = false;                      // folded ZeroFill (ACCUM starts at 0)
+  std::string zname;
+  long long zsize = 0;
+  std::set<std::string> reads, writes;
+};
+
+void expr_reads(const Expr& e, std::set<std::string>& out) {
+  if (e.k == Expr::LOAD) out.insert(e.name);
+  if (e.a) expr_reads(*e.a, out);
+  if (e.b) expr_reads(*e.b, out);
+}
+
+void stmt_rw(const Stmt& s, std::set<std::string>& r, std::set<std::string>& w) {
+  switch (s.k) {
+    case Stmt::LOOP:
+      for (const auto& b : s.body) stmt_rw(b, r, w);
+      break;
+    case Stmt::ZERO:
+      w.insert(s.name);
+      break;
+    case Stmt::ASSIGN:
+      w.insert(s.name);
+      expr_reads(*s.e, r);
+      break;
+    case Stmt::ACCUM:
+      w.insert(s.name);
+      r.insert(s.name);
+      expr_reads(*s.e, r);
+      break;
+  }
+}
+
+// Target addresses of a perfect nest over its parallel box: injective?  Does
+// the set equal {0..size-1}?
+void target_map(const Stmt& leaf, const std::vector<std::pair<int, int>>& par,
+                long long cover_size, bool& injective, bool& covers) {
+  long long base = leaf.offset;
+  std::map<int, long long> stride;
+  for (const auto& t : leaf.terms) {
+    if (t.e.idx < 0) base += t.e.val * t.stride;
+    else stride[t.e.idx] += t.stride;
+  }
+  long long total = 1;
+  for (const auto& pr : par) total *= pr.second;
+  injective = false;
+  covers = false;
+  if (total > (1LL << 24)) return;
+  long long lo = base, hi = base;
+  for (const auto& pr : par) {
+    const long long s = stride[pr.first] * (pr.second - 1);
+    if (s < 0) lo += s; else hi += s;
+  }
+  if (lo < 0) return;
+  std::vector<char> seen((size_t)(hi - lo + 1), 0);
+  std::vector<int> it(par.size(), 0);
+  for (long long n = 0; n < total; ++n) {
+    long long a = base;
+    for (size_t k = 0; k < par.size(); ++k) a += stride[par[k].first] * it[k];
+    if (seen[a - lo]) return;
+    seen[a - lo] = 1;
+    for (size_t k = par.size(); k-- > 0;) {
+      if (++it[k] < par[k].second) break;
+      it[k] = 0;
+    }
+  }
+  injective = true;
+  covers = (lo == 0 && hi == cover_size - 1 && total == cover_size);
+}
+
+Phase classify(const Stmt& s) {
+  Phase ph;
+  ph.top = &s;
+  stmt_rw(s, ph.reads, ph.writes);
+  // descend the perfect nest
+  std::vector<std::pair<int, int>> loops;
+  const Stmt* cur = &s;
+  while (cur->k == Stmt::LOOP && cur->body.size() == 1) {
+    loops.emplace_back(cur->idx, cur->extent);
+    cur = &cur->body[0];
+  }
+  if (cur->k == Stmt::LOOP || cur->k == Stmt::ZERO) {  // imperfect nest
+    ph.k = Phase::SERIAL;
+    return ph;
+  }
+  ph.leaf = cur;
+  std::set<int> tgt;
+  for (const auto& t : cur->terms)
+    if (t.e.idx >= 0 && t.stride != 0) tgt.insert(t.e.idx);
+  std::set<int> loop_ids;
+  for (const auto& l : loops) loop_ids.insert(l.first);
+  for (int id : tgt)
+    if (!loop_ids.count(id)) { ph.k = Phase::SERIAL; return ph; }
+  for (const auto& l : loops) (tgt.count(l.first) ? ph.par : ph.red).push_back(l);
+  std::set<std::string> er;
+  expr_reads(*cur->e, er);
+  bool inj = false, cov = false;
+  target_map(*cur, ph.par, -1, inj, cov);
+  if (!inj || er.count(cur->name)) {
+    ph.k = Phase::SERIAL;
+    ph.par.clear();
+    ph.red.clear();
+    return ph;
+  }
+  ph.k = Phase::NEST;
+  for (const auto& pr : ph.par) ph.npar *= pr.second;
+  return ph;
+}
+
+bool nest_covers(const Phase& ph, long long size) {
+  bool inj = false, cov = false;
+  target_map(*ph.leaf, ph.par, size, inj, cov);
+  return inj && cov;
+}
+
+std::string fmt_double(double x) {
+  if (std::isnan(x) || std::isinf(x)) {
+    long long bits;
+    std::memcpy(&bits, &x, 8);
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "__longlong_as_double(0x%016llxLL)", (unsigned long long)bits);
+    return buf;
+  }
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%a", x);  // exact (hex float literal)
+  return buf;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// generation
+
+Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
+  (void)allow_fma;
+  std::map<std::string, long long> bufsize;
+  bufsize[P.ret_name] = P.ret_size;
+  for (const auto& a : P.args) bufsize[a.first] = a.second;
+  for (const auto& t : P.temps) bufsize[t.first] = t.second;
+
+  // 1. phases with ZeroFill folding
+  std::vector<Phase> phases;
+  std::map<std::string, long long> pending;  // name -> zero size
+  auto flush_zero = [&](const std::string& nm) {
+    Phase z;
+    z.k = Phase::ZERO;
+    z.zname = nm;
+    z.zsize = pending[nm];
+    z.writes.insert(nm);
+    phases.push_back(z);
+    pending.erase(nm);
+  };
+  for (const auto& s : P.body) {
+    if (s.k == Stmt::ZERO) {
+      if (!bufsize.count(s.name)) throw std::runtime_error("LoopProgram: unknown buffer " + s.name);
+      if (pending.count(s.name)) flush_zero(s.name);
+      pending[s.name] = s.size;
+      continue;
+    }
+    Phase ph = classify(s);
+    std::set<std::string> touched = ph.reads;
+    touched.insert(ph.writes.begin(), ph.writes.end());
+    for (const auto& nm : touched) {
+      if (!bufsize.count(nm)) throw std::runtime_error("LoopProgram: unknown buffer " + nm);
+      if (!pending.count(nm)) continue;
+      std::set<std::string> er;
+      if (ph.k == Phase::NEST) expr_reads(*ph.leaf->e, er);
+      const bool fold = ph.k == Phase::NEST && ph.leaf->name == nm && !er.count(nm) &&
+                        pending[nm] == bufsize[nm] && nest_covers(ph, pending[nm]);
+      if (fold) {
+        if (ph.leaf->k == Stmt::ACCUM) ph.zero_init = true;
+        pending.erase(nm);
+      } else {
+        flush_zero(nm);
+      }
+    }
+    phases.push_back(std::move(ph));
+  }
+  if (pending.count(P.ret_name)) flush_zero(P.ret_name);
+
+  // 2. storage: args, A fixed; temporaries packed by liveness
+  std::map<std::string, long long> base;
+  long long fixed = 0;
+  for (const auto& a : P.args) { base[a.first] = fixed; fixed += a.second; }
+  base[P.ret_name] = fixed;
+  fixed += P.ret_size;
+  std::map<std::string, int> first, last;
+  for (int k = 0; k < (int)phases.size(); ++k) {
+    std::set<std::string> t = phases[k].reads;
+    t.insert(phases[k].writes.begin(), phases[k].writes.end());
+    for (const auto& nm : t) {
+      if (!first.count(nm)) first[nm] = k;
+      last[nm] = k;
+    }
+  }
+  long long peak = fixed;
+  {
+    std::vector<std::pair<long long, long long>> used;  // [start, end) of live temps
+    std::vector<std::pair<int, std::string>> live;      // (last, name)
+    for (int k = 0; k < (int)phases.size(); ++k) {
+      for (size_t j = 0; j < live.size();) {
+        if (live[j].first < k) {
+          const long long s = base[live[j].second];
+          used.erase(std::find_if(used.begin(), used.end(),
+                                  [&](const std::pair<long long, long long>& u) { return u.first == s; }));
+          live.erase(live.begin() + j);
+        } else {
+          ++j;
+        }
+      }
+      for (const auto& t : P.temps) {
+        if (!first.count(t.first) || first[t.first] != k) continue;
+        std::sort(used.begin(), used.end());
+        long long at = fixed;
+        for (const auto& u : used) {
+          if (at + t.second <= u.first) break;
+          at = std::max(at, u.second);
+        }
+        base[t.first] = at;
+        used.emplace_back(at, at + t.second);
+        live.emplace_back(last[t.first], t.first);
+        peak = std::max(peak, at + t.second);
+      }
+    }
+  }
+  for (const auto& t : P.temps)
+    if (!base.count(t.first)) base[t.first] = 0;  // never touched
+
+  // 3. launch geometry
+  Generated G;
+  Config& C = G.cfg;
+  C.slots = peak;
+  long long tbl_doubles = 0;
+  std::vector<long long> toff;
+  for (const auto& t : P.tables) { toff.push_back(tbl_doubles); tbl_doubles += (long long)t.values.size(); }
+  const long long tbl_bytes_smem = ((tbl_doubles * 8 + 15) / 16) * 16;
+  C.tables_in_smem = tbl_bytes_smem <= 64 * 1024;
+  const long long tb = C.tables_in_smem ? tbl_bytes_smem : 0;
+  auto ncp_of = [](int nc) { return nc >= 4 ? nc + 1 : nc; };
+  auto bytes_of = [&](int nc) { return tb + peak * ncp_of(nc) * 8; };
+  int nc = 0;
+  for (int cand = 32; cand >= 1; cand /= 2)
+    if (bytes_of(cand) <= 112 * 1024) { nc = cand; break; }
+  if (!nc && bytes_of(1) <= smem_limit) nc = 1;
+  if (nc) {
+    C.cells_per_block = nc;
+    C.ncp = ncp_of(nc);
+    C.smem_bytes = bytes_of(nc);
+  } else {
+    C.global_scratch = true;
+    C.cells_per_block = 1;
+    C.ncp = 1;
+    C.smem_bytes = tb;
+    C.arena_doubles_per_block = ((peak + 31) / 32) * 32;
+  }
+  long long maxitems = 1;
+  for (const auto& ph : phases)
+    if (ph.k == Phase::NEST) maxitems = std::max(maxitems, ph.npar * C.cells_per_block);
+  for (const auto& a : P.args) maxitems = std::max(maxitems, a.second * C.cells_per_block);
+  C.threads = (int)std::min<long long>(256, std::max<long long>(64, ((maxitems + 31) / 32) * 32));
+
+  // 4. emission
+  const int NC = C.cells_per_block, NCP = C.ncp, T = C.threads;
+  std::ostringstream o;
+  auto slot = [&](const std::string& nm, const std::string& addr) {
+    std::ostringstream s;
+    const long long b = base.at(nm);
+    if (NCP == 1) s << "S[" << b << " + (" << addr << ")]";
+    else s << "S[(" << b << " + (" << addr << ")) * " << NCP << " + c]";
+    return s.str();
+  };
+  auto ent = [](const Entry& e) { return e.idx >= 0 ? "i" + std::to_string(e.idx) : std::to_string(e.val); };
+  auto addr = [&](long long off, const std::vector<Term>& terms) {
+    std::ostringstream s;
+    long long c0 = off;
+    bool any = false;
+    for (const auto& t : terms) {
+      if (t.e.idx < 0) { c0 += t.e.val * t.stride; continue; }
+      if (t.stride == 0) continue;
+      if (any) s << " + ";
+      if (t.stride == 1) s << "i" << t.e.idx;
+      else s << t.stride << " * i" << t.e.idx;
+      any = true;
+    }
+    if (c0 || !any) { if (any) s << " + "; s << c0; }
+    return s.str();
+  };
+  std::function<std::string(const Expr&)> ex = [&](const Expr& e) -> std::string {
+    switch (e.k) {
+      case Expr::LIT: return fmt_double(e.lit);
+      case Expr::LOAD: return slot(e.name, addr(e.offset, e.terms));
+      case Expr::TABLE: {
+        std::ostringstream s;
+        s << (C.tables_in_smem ? "Tb[" : "sfk_tables[") << toff[e.table] << " + ("
+          << addr(0, e.terms) << ")]";
+        return s.str();
+      }
+      case Expr::DELTA: return "((" + ent(e.d0) + " == " + ent(e.d1) + ") ? 1.0 : 0.0)";
+      case Expr::ADD: return "(" + ex(*e.a) + " + " + ex(*e.b) + ")";
+      case Expr::MUL: return "(" + ex(*e.a) + " * " + ex(*e.b) + ")";
+      case Expr::DIV: return "(" + ex(*e.a) + " / " + ex(*e.b) + ")";
+      case Expr::POW: return "pow(" + ex(*e.a) + ", " + ex(*e.b) + ")";
+      case Expr::MIN: return "fmin(" + ex(*e.a) + ", " + ex(*e.b) + ")";
+      case Expr::MAX: return "fmax(" + ex(*e.a) + ", " + ex(*e.b) + ")";
+      case Expr::CALL: {
+        static const std::map<std::string, std::string> fn = {
+            {"sqrt", "sqrt"}, {"sin", "sin"}, {"cos", "cos"}, {"tan", "tan"},
+            {"exp", "exp"},   {"ln", "log"},  {"abs", "fabs"}};
+        auto it = fn.find(e.name);
+        if (it == fn.end()) throw std::runtime_error("LoopProgram: unsupported function " + e.name);
+        return it->second + "(" + ex(*e.a) + ")";
+      }
+      case Expr::CMP: {
+        static const std::set<std::string> ops = {"<", ">", "<=", ">=", "==", "!="};
+        if (!ops.count(e.name)) throw std::runtime_error("LoopProgram: comparison " + e.name);
+        return "((" + ex(*e.a) + " " + e.name + " " + ex(*e.b) + ") ? 1.0 : 0.0)";
+      }
+    }
+    return "0.0";
+  };
+  std::function<void(const Stmt&, int)> serial = [&](const Stmt& s, int ind) {
+    const std::string pad(ind * 2, ' ');
+    switch (s.k) {
+      case Stmt::LOOP:
+        o << pad << "for (int i" << s.idx << " = 0; i" << s.idx << " < " << s.extent << "; ++i"
+          << s.idx << ") {\n";
+        for (const auto& b : s.body) serial(b, ind + 1);
+        o << pad << "}\n";
+        break;
+      case Stmt::ZERO:
+        o << pad << "for (int z = 0; z < " << s.size << "; ++z) " << slot(s.name, "z") << " = 0.0;\n";
+        break;
+      case Stmt::ASSIGN:
+        o << pad << slot(s.name, addr(s.offset, s.terms)) << " = " << ex(*s.e) << ";\n";
+        break;
+      case Stmt::ACCUM: {
+        const std::string t = slot(s.name, addr(s.offset, s.terms));
+        o << pad << t << " = " << t << " + " << ex(*s.e) << ";\n";
+        break;
+      }
+    }
+  };
+
+  G.entry = "sfk_lp_" + P.name;
+  for (auto& ch : G.entry)
+    if (!std::isalnum((unsigned char)ch) && ch != '_') ch = '_';
+  o << "// generated by libsfk from the LoopProgram '" << P.name << "'\n"
+    << "// NC=" << NC << " cells/CTA, " << T << " threads, " << C.slots << " slots/cell, "
+    << (C.global_scratch ? "global arena" : "shared memory") << "\n";
+  if (tbl_doubles) {
+    o << "__device__ const double sfk_tables[" << tbl_doubles << "] = {";
+    long long n = 0;
+    for (const auto& t : P.tables)
+      for (double v : t.values) o << (n++ ? ", " : "") << fmt_double(v);
+    o << "};\n";
+  }
+  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ") " << G.entry
+    << "(double* __restrict__ gA";
+  for (size_t a = 0; a < P.args.size(); ++a) o << ", const double* __restrict__ g" << a;
+  o << ", long long ncells, double* __restrict__ arena) {\n"
+    << "  extern __shared__ __align__(16) double smem[];\n";
+  if (C.tables_in_smem && tbl_doubles) {
+    o << "  double* Tb = smem;\n"
+      << "  for (int k = threadIdx.x; k < " << tbl_doubles << "; k += " << T
+      << ") Tb[k] = sfk_tables[k];\n"
+      << "  __syncthreads();\n";
+  }
+  if (C.global_scratch)
+    o << "  double* __restrict__ S = arena + (long long)blockIdx.x * " << C.arena_doubles_per_block
+      << ";\n";
+  else
+    o << "  double* S = smem + " << tb / 8 << ";\n";
+  o << "  const long long nchunks = (ncells + " << NC - 1 << ") / " << NC << ";\n"
+    << "  for (long long chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {\n"
+    << "    const long long c0 = chunk * " << NC << ";\n"
+    << "    const int nvalid = (int)((ncells - c0) < " << NC << " ? (ncells - c0) : " << NC << ");\n";
+  if (NC == 1) o << "    const int c = 0; (void)c;\n";
+  // loads
+  for (size_t a = 0; a < P.args.size(); ++a) {
+    const long long sz = P.args[a].second;
+    o << "    for (int e = threadIdx.x; e < " << NC * sz << "; e += " << T << ") {\n";
+    if (NC > 1) o << "      const int c = e / " << sz << ", k = e - c * " << sz << ";\n";
+    else o << "      const int k = e;\n";
+    o << "      " << slot(P.args[a].first, "k") << " = (c < nvalid) ? g" << a << "[c0 * " << sz
+      << " + e] : 0.0;\n    }\n";
+  }
+  // barrier tracking by storage interval
+  typedef std::pair<long long, long long> Iv;
+  std::vector<Iv> W, R;
+  auto iv = [&](const std::string& nm) { return Iv(base.at(nm), base.at(nm) + bufsize.at(nm)); };
+  auto hit = [](const std::vector<Iv>& a, const Iv& b) {
+    for (const auto& x : a)
+      if (x.first < b.second && b.first < x.second) return true;
+    return false;
+  };
+  auto sync_if = [&](const std::set<std::string>& rd, const std::set<std::string>& wr) {
+    bool need = false;
+    for (const auto& nm : rd) need = need || hit(W, iv(nm));
+    for (const auto& nm : wr) need = need || hit(W, iv(nm)) || hit(R, iv(nm));
+    if (need) {
+      o << "    __syncthreads();\n";
+      ++C.barriers;
+      W.clear();
+      R.clear();
+    }
+    for (const auto& nm : rd) R.push_back(iv(nm));
+    for (const auto& nm : wr) W.push_back(iv(nm));
+  };
+  {
+    std::set<std::string> wr;
+    for (const auto& a : P.args) wr.insert(a.first);
+    for (const auto& nm : wr) W.push_back(iv(nm));
+  }
+  C.phases = (int)phases.size();
+  for (size_t k = 0; k < phases.size(); ++k) {
+    const Phase& ph = phases[k];
+    std::set<std::string> rd = ph.reads;
+    if (ph.k == Phase::NEST && ph.zero_init) rd.erase(ph.leaf->name);
+    sync_if(rd, ph.writes);
+    if (ph.k == Phase::ZERO) {
+      o << "    // phase " << k << ": zero " << ph.zname << "\n"
+        << "    for (int e = threadIdx.x; e < " << NC * ph.zsize << "; e += " << T << ") {\n";
+      if (NC > 1) o << "      const int c = e % " << NC << ", z = e / " << NC << ";\n";
+      else o << "      const int z = e;\n";
+      o << "      " << slot(ph.zname, "z") << " = 0.0;\n    }\n";
+    } else if (ph.k == Phase::SERIAL) {
+      ++C.serial_phases;
+      o << "    // phase " << k << ": serial nest (thread per cell)\n";
+      if (NC > 1) o << "    for (int c = threadIdx.x; c < " << NC << "; c += " << T << ") {\n";
+      else o << "    if (threadIdx.x == 0) {\n";
+      serial(*ph.top, 3);
+      o << "    }\n";
+    } else {
+      const Stmt& L = *ph.leaf;
+      o << "    // phase " << k << ": " << (L.k == Stmt::ACCUM ? "accumulate " : "assign ") << L.name
+        << " (" << ph.npar << " parallel x " << ph.red.size() << " reduction loops)\n"
+        << "    for (int w = threadIdx.x; w < " << NC * ph.npar << "; w += " << T << ") {\n";
+      if (NC > 1) o << "      const int c = w % " << NC << ";\n      int q = w / " << NC << ";\n";
+      else o << "      int q = w;\n";
+      for (size_t j = ph.par.size(); j-- > 0;) {
+        const auto& pr = ph.par[j];
+        if (j == 0) o << "      const int i" << pr.first << " = q;\n";
+        else o << "      const int i" << pr.first << " = q % " << pr.second << "; q /= " << pr.second << ";\n";
+      }
+      if (ph.par.empty()) o << "      (void)q;\n";
+      const std::string tgt = slot(L.name, addr(L.offset, L.terms));
+      std::string pad = "      ";
+      if (L.k == Stmt::ACCUM) o << pad << "double acc = " << (ph.zero_init ? "0.0" : tgt) << ";\n";
+      for (const auto& r : ph.red) {
+        o << pad << "for (int i" << r.first << " = 0; i" << r.first << " < " << r.second << "; ++i"
+          << r.first << ") {\n";
+        pad += "  ";
+      }
+      if (L.k == Stmt::ACCUM) o << pad << "acc = acc + " << ex(*L.e) << ";\n";
+      else o << pad << tgt << " = " << ex(*L.e) << ";\n";
+      for (size_t r = 0; r < ph.red.size(); ++r) {
+        pad.resize(pad.size() - 2);
+        o << pad << "}\n";
+      }
+      if (L.k == Stmt::ACCUM) o << "      " << tgt << " = acc;\n";
+      o << "    }\n";
+    }
+  }
+  // store A
+  sync_if({P.ret_name}, {});
+  {
+    const long long sz = P.ret_size;
+    o << "    for (int e = threadIdx.x; e < " << NC * sz << "; e += " << T << ") {\n";
+    if (NC > 1) o << "      const int c = e / " << sz << ", k = e - c * " << sz << ";\n";
+    else o << "      const int c = 0, k = e;\n";
+    o << "      if (c < nvalid) gA[c0 * " << sz << " + e] = " << slot(P.ret_name, "k") << ";\n"
+      << "    }\n";
+  }
+  o << "    __syncthreads();\n  }\n}\n";
+  G.source = o.str();
+  return G;
+}
+
+}  // namespace lp
+}  // namespace sfk

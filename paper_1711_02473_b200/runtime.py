@@ -38,7 +38,8 @@ EXPORTED_SYMBOLS = (
     "sfk_abi_version", "sfk_plan_create", "sfk_plan_destroy", "sfk_plan_sizes",
     "sfk_eval", "sfk_eval_pair", "sfk_eval_host", "sfk_sum_squares",
     "sfk_launch_count", "sfk_last_error", "sfk_device_info", "sfk_fp64_peak",
-    "sfk_eval_gather_scatter",
+    "sfk_eval_gather_scatter", "sfk_program_create", "sfk_program_destroy",
+    "sfk_program_sizes", "sfk_program_config", "sfk_program_text", "sfk_program_eval",
 )
 ABI_VERSION = 1
 SUM_WORKSPACE = 1024
@@ -191,6 +192,8 @@ def evaluate_batched(plan, inputs, out=None, stream=None):
     arrays (synchronous host path, returns numpy).  A 1D array of one cell's
     size is accepted and a 1D result returned, like ``run_kernel``.
     """
+    if getattr(plan, "meta", {}).get("backend") == "loopprogram":
+        return plan.evaluate(inputs, out=out, stream=stream)
     first = next(iter(inputs.values()), None) if inputs else None
     if first is not None and isinstance(first, np.ndarray):
         return evaluate_host(plan, inputs, out=out)
