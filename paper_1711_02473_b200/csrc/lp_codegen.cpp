@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cinttypes>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <set>
@@ -316,6 +317,129 @@ std::string fmt_double(double x) {
   return buf;
 }
 
+
+// Exact barrier placement.  Phase k needs a __syncthreads() before it iff
+// some shared-memory element it touches was touched since the last barrier
+// by a DIFFERENT thread, with at least one of the two accesses a write
+// (thread of item w = w % T, as the generated loops deal items).  Same-thread
+// chains (pointwise statements reading what the same item wrote) need none.
+// Phases too large to enumerate fall back to "barrier before and after".
+struct Access {
+  long long elem;
+  int thread;
+  bool write;
+};
+
+void collect_loads(const Expr& e, std::vector<const Expr*>& out) {
+  if (e.k == Expr::LOAD) out.push_back(&e);
+  if (e.a) collect_loads(*e.a, out);
+  if (e.b) collect_loads(*e.b, out);
+}
+
+long long eval_addr(long long off, const std::vector<Term>& terms, const std::vector<long long>& val) {
+  long long a = off;
+  for (const auto& t : terms) a += t.stride * (t.e.idx >= 0 ? val[t.e.idx] : t.e.val);
+  return a;
+}
+
+// Returns false if the phase is too large to enumerate.
+bool phase_accesses(const Phase& ph, const std::map<std::string, long long>& base,
+                    const std::map<std::string, long long>& bufsize, int NC, int T, int max_idx,
+                    std::vector<Access>& out) {
+  const long long kBudget = 1LL << 23;
+  out.clear();
+  auto elem = [&](long long slot, int c) { return slot * NC + c; };
+  if (ph.k == Phase::ZERO) {
+    const long long b = base.at(ph.zname);
+    for (long long e = 0; e < NC * ph.zsize; ++e)
+      out.push_back({elem(b + e / NC, (int)(e % NC)), (int)(e % T), true});
+    return true;
+  }
+  if (ph.k == Phase::SERIAL) {
+    long long n = 0;
+    for (const auto& nm : ph.reads) n += bufsize.at(nm);
+    for (const auto& nm : ph.writes) n += bufsize.at(nm);
+    if (n * NC > kBudget) return false;
+    for (int c = 0; c < NC; ++c) {
+      for (const auto& nm : ph.reads)
+        for (long long z = 0; z < bufsize.at(nm); ++z)
+          out.push_back({elem(base.at(nm) + z, c), c % T, false});
+      for (const auto& nm : ph.writes)
+        for (long long z = 0; z < bufsize.at(nm); ++z)
+          out.push_back({elem(base.at(nm) + z, c), c % T, true});
+    }
+    return true;
+  }
+  const Stmt& L = *ph.leaf;
+  std::vector<const Expr*> loads;
+  collect_loads(*L.e, loads);
+  long long nred = 1;
+  for (const auto& r : ph.red) nred *= r.second;
+  if ((long long)NC * ph.npar * (1 + nred * (long long)loads.size()) > kBudget) return false;
+  std::vector<long long> val(max_idx + 1, 0);
+  const long long tb = base.at(L.name);
+  for (long long w = 0; w < NC * ph.npar; ++w) {
+    const int c = (int)(w % NC);
+    long long q = w / NC;
+    for (size_t j = ph.par.size(); j-- > 0;) {
+      if (j == 0) { val[ph.par[j].first] = q; break; }
+      val[ph.par[j].first] = q % ph.par[j].second;
+      q /= ph.par[j].second;
+    }
+    const int t = (int)(w % T);
+    out.push_back({elem(tb + eval_addr(L.offset, L.terms, val), c), t, true});
+    if (loads.empty()) continue;
+    std::vector<int> it(ph.red.size(), 0);
+    for (long long r = 0; r < nred; ++r) {
+      for (size_t j = 0; j < ph.red.size(); ++j) val[ph.red[j].first] = it[j];
+      for (const Expr* ld : loads)
+        out.push_back({elem(base.at(ld->name) + eval_addr(ld->offset, ld->terms, val), c), t, false});
+      for (size_t j = ph.red.size(); j-- > 0;) {
+        if (++it[j] < ph.red[j].second) break;
+        it[j] = 0;
+      }
+    }
+  }
+  return true;
+}
+
+struct Window {
+  std::vector<int> writer, reader;
+  std::vector<char> multi;
+  std::vector<long long> touched;
+  bool poisoned = false;
+  explicit Window(long long n) : writer(n, -1), reader(n, -1), multi(n, 0) {}
+  bool conflicts(const std::vector<Access>& acc) const {
+    if (poisoned) return true;
+    for (const auto& a : acc) {
+      const int w = writer[a.elem];
+      if (w >= 0 && w != a.thread) return true;
+      if (a.write) {
+        const int r = reader[a.elem];
+        if (r >= 0 && (r != a.thread || multi[a.elem])) return true;
+      }
+    }
+    return false;
+  }
+  void add(const std::vector<Access>& acc) {
+    for (const auto& a : acc) {
+      if (writer[a.elem] < 0 && reader[a.elem] < 0) touched.push_back(a.elem);
+      if (a.write) {
+        writer[a.elem] = a.thread;
+      } else if (reader[a.elem] < 0) {
+        reader[a.elem] = a.thread;
+      } else if (reader[a.elem] != a.thread) {
+        multi[a.elem] = 1;
+      }
+    }
+  }
+  void clear() {
+    for (long long e : touched) { writer[e] = -1; reader[e] = -1; multi[e] = 0; }
+    touched.clear();
+    poisoned = false;
+  }
+};
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -426,11 +550,15 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
   const long long tbl_bytes_smem = ((tbl_doubles * 8 + 15) / 16) * 16;
   C.tables_in_smem = tbl_bytes_smem <= 64 * 1024;
   const long long tb = C.tables_in_smem ? tbl_bytes_smem : 0;
-  auto ncp_of = [](int nc) { return nc >= 4 ? nc + 1 : nc; };
+  // cell stride of a slot: NC (cell-fastest, so a warp touching consecutive
+  // items of one phase reads consecutive doubles: conflict-free)
+  auto ncp_of = [](int nc) { return nc; };
   auto bytes_of = [&](int nc) { return tb + peak * ncp_of(nc) * 8; };
   int nc = 0;
+  long long cta_budget = 56 * 1024;  // ~4 CTAs per SM (measured best, tools/lp_sweep.sh)
+  if (const char* e = std::getenv("SFK_LP_SMEM_KB")) cta_budget = std::atoll(e) * 1024;
   for (int cand = 32; cand >= 1; cand /= 2)
-    if (bytes_of(cand) <= 112 * 1024) { nc = cand; break; }
+    if (bytes_of(cand) <= cta_budget) { nc = cand; break; }
   if (!nc && bytes_of(1) <= smem_limit) nc = 1;
   if (nc) {
     C.cells_per_block = nc;
@@ -443,11 +571,34 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
     C.smem_bytes = tb;
     C.arena_doubles_per_block = ((peak + 31) / 32) * 32;
   }
+  // CTA size (tools/lp_sweep.sh): 256 threads, one item each in the widest
+  // phase if fewer suffice -- unless the work-weighted median phase needs two
+  // rounds of 256 but fits one round of <= 512 (then one round).  The launch
+  // bound keeps <= 128 registers so the ~4 CTAs the 56 KB smem budget allows
+  // are not register-limited.
   long long maxitems = 1;
-  for (const auto& ph : phases)
-    if (ph.k == Phase::NEST) maxitems = std::max(maxitems, ph.npar * C.cells_per_block);
-  for (const auto& a : P.args) maxitems = std::max(maxitems, a.second * C.cells_per_block);
-  C.threads = (int)std::min<long long>(256, std::max<long long>(64, ((maxitems + 31) / 32) * 32));
+  std::vector<std::pair<long long, double>> items;  // (items, work)
+  double work_total = 0;
+  for (const auto& ph : phases) {
+    if (ph.k != Phase::NEST) continue;
+    long long nred = 1;
+    for (const auto& r : ph.red) nred *= r.second;
+    const long long it = ph.npar * C.cells_per_block;
+    maxitems = std::max(maxitems, it);
+    items.emplace_back(it, (double)it * nred);
+    work_total += (double)it * nred;
+  }
+  std::sort(items.begin(), items.end());
+  long long median = 0;
+  double acc_w = 0;
+  for (const auto& it : items) {
+    acc_w += it.second;
+    if (acc_w >= 0.5 * work_total) { median = it.first; break; }
+  }
+  long long tmax = 256;
+  if (median > 256 && median <= 512) maxitems = median, tmax = 512;
+  if (const char* e = std::getenv("SFK_LP_MAX_THREADS")) tmax = std::atoll(e);
+  C.threads = (int)std::min<long long>(tmax, std::max<long long>(64, ((maxitems + 31) / 32) * 32));
 
   // 4. emission
   const int NC = C.cells_per_block, NCP = C.ncp, T = C.threads;
@@ -544,7 +695,12 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
       for (double v : t.values) o << (n++ ? ", " : "") << fmt_double(v);
     o << "};\n";
   }
-  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ") " << G.entry
+  // registers: enough CTAs for the smem budget, at most 1024 threads per SM
+  const long long smem_ctas = std::max<long long>(1, (228 * 1024) / (C.smem_bytes + 1024));
+  long long minb = std::max<long long>(1, std::min<long long>(smem_ctas, 1024 / T));
+  if (const char* e = std::getenv("SFK_LP_MINB")) minb = std::atoll(e);
+  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << minb << ") "
+    << G.entry
     << "(double* __restrict__ gA";
   for (size_t a = 0; a < P.args.size(); ++a) o << ", const double* __restrict__ g" << a;
   o << ", long long ncells, double* __restrict__ arena) {\n"
@@ -565,48 +721,61 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
     << "    const long long c0 = chunk * " << NC << ";\n"
     << "    const int nvalid = (int)((ncells - c0) < " << NC << " ? (ncells - c0) : " << NC << ");\n";
   if (NC == 1) o << "    const int c = 0; (void)c;\n";
-  // loads
+  // global <-> shared transfers: each warp moves G consecutive elements of
+  // 32/G cells (G*NC = 32 when NC <= 32): G-double runs per cell in HBM,
+  // 32 consecutive doubles in shared memory (element k of cell c at k*NC + c)
+  std::vector<Access> acc;
+  auto xfer_g = [&](long long sz) { return std::min<long long>(sz, std::max(1, 32 / NC)); };
+  auto xfer_items = [&](long long sz) {
+    const long long g = xfer_g(sz);
+    return NC * g * ((sz + g - 1) / g);
+  };
+  auto xfer_open = [&](long long sz) {
+    const long long g = xfer_g(sz);
+    o << "    for (int e = threadIdx.x; e < " << xfer_items(sz) << "; e += " << T << ") {\n";
+    if (NC > 1)
+      o << "      const int c = (e / " << g << ") % " << NC << ", k = (e / " << g * NC << ") * " << g
+        << " + e % " << g << ";\n";
+    else
+      o << "      const int k = e;\n";
+  };
+  auto xfer_access = [&](long long sz, long long b, bool write) {
+    const long long g = xfer_g(sz);
+    acc.clear();
+    for (long long e = 0; e < xfer_items(sz); ++e) {
+      const long long c = NC > 1 ? (e / g) % NC : 0;
+      const long long k = NC > 1 ? (e / (g * NC)) * g + e % g : e;
+      if (k < sz) acc.push_back({(b + k) * NC + c, (int)(e % T), write});
+    }
+  };
   for (size_t a = 0; a < P.args.size(); ++a) {
     const long long sz = P.args[a].second;
-    o << "    for (int e = threadIdx.x; e < " << NC * sz << "; e += " << T << ") {\n";
-    if (NC > 1) o << "      const int c = e / " << sz << ", k = e - c * " << sz << ";\n";
-    else o << "      const int k = e;\n";
-    o << "      " << slot(P.args[a].first, "k") << " = (c < nvalid) ? g" << a << "[c0 * " << sz
-      << " + e] : 0.0;\n    }\n";
+    xfer_open(sz);
+    o << "      if (k < " << sz << ") " << slot(P.args[a].first, "k") << " = (c < nvalid) ? g" << a
+      << "[(c0 + c) * " << sz << " + k] : 0.0;\n    }\n";
   }
-  // barrier tracking by storage interval
-  typedef std::pair<long long, long long> Iv;
-  std::vector<Iv> W, R;
-  auto iv = [&](const std::string& nm) { return Iv(base.at(nm), base.at(nm) + bufsize.at(nm)); };
-  auto hit = [](const std::vector<Iv>& a, const Iv& b) {
-    for (const auto& x : a)
-      if (x.first < b.second && b.first < x.second) return true;
-    return false;
-  };
-  auto sync_if = [&](const std::set<std::string>& rd, const std::set<std::string>& wr) {
-    bool need = false;
-    for (const auto& nm : rd) need = need || hit(W, iv(nm));
-    for (const auto& nm : wr) need = need || hit(W, iv(nm)) || hit(R, iv(nm));
+  // barrier plan (see Window): the argument loads open the window
+  int max_idx = 0;
+  for (const auto& kv : P.extents) max_idx = std::max(max_idx, kv.first);
+  Window win(C.slots * NC);
+  for (size_t a = 0; a < P.args.size(); ++a) {
+    xfer_access(P.args[a].second, base.at(P.args[a].first), true);
+    win.add(acc);
+  }
+  auto barrier_for = [&](bool known) {
+    const bool need = !known || win.conflicts(acc);
     if (need) {
       o << "    __syncthreads();\n";
       ++C.barriers;
-      W.clear();
-      R.clear();
+      win.clear();
     }
-    for (const auto& nm : rd) R.push_back(iv(nm));
-    for (const auto& nm : wr) W.push_back(iv(nm));
+    if (known) win.add(acc);
+    else win.poisoned = true;
   };
-  {
-    std::set<std::string> wr;
-    for (const auto& a : P.args) wr.insert(a.first);
-    for (const auto& nm : wr) W.push_back(iv(nm));
-  }
   C.phases = (int)phases.size();
   for (size_t k = 0; k < phases.size(); ++k) {
     const Phase& ph = phases[k];
-    std::set<std::string> rd = ph.reads;
-    if (ph.k == Phase::NEST && ph.zero_init) rd.erase(ph.leaf->name);
-    sync_if(rd, ph.writes);
+    barrier_for(phase_accesses(ph, base, bufsize, NC, T, max_idx, acc));
     if (ph.k == Phase::ZERO) {
       o << "    // phase " << k << ": zero " << ph.zname << "\n"
         << "    for (int e = threadIdx.x; e < " << NC * ph.zsize << "; e += " << T << ") {\n";
@@ -636,7 +805,9 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
       const std::string tgt = slot(L.name, addr(L.offset, L.terms));
       std::string pad = "      ";
       if (L.k == Stmt::ACCUM) o << pad << "double acc = " << (ph.zero_init ? "0.0" : tgt) << ";\n";
-      for (const auto& r : ph.red) {
+      for (size_t j = 0; j < ph.red.size(); ++j) {
+        const auto& r = ph.red[j];
+        if (j + 1 == ph.red.size() && r.second <= 32) o << pad << "#pragma unroll\n";
         o << pad << "for (int i" << r.first << " = 0; i" << r.first << " < " << r.second << "; ++i"
           << r.first << ") {\n";
         pad += "  ";
@@ -652,15 +823,11 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
     }
   }
   // store A
-  sync_if({P.ret_name}, {});
-  {
-    const long long sz = P.ret_size;
-    o << "    for (int e = threadIdx.x; e < " << NC * sz << "; e += " << T << ") {\n";
-    if (NC > 1) o << "      const int c = e / " << sz << ", k = e - c * " << sz << ";\n";
-    else o << "      const int c = 0, k = e;\n";
-    o << "      if (c < nvalid) gA[c0 * " << sz << " + e] = " << slot(P.ret_name, "k") << ";\n"
-      << "    }\n";
-  }
+  xfer_access(P.ret_size, base.at(P.ret_name), false);
+  barrier_for(true);
+  xfer_open(P.ret_size);
+  o << "      if (k < " << P.ret_size << " && c < nvalid) gA[(c0 + c) * " << P.ret_size << " + k] = "
+    << slot(P.ret_name, "k") << ";\n    }\n";
   o << "    __syncthreads();\n  }\n}\n";
   G.source = o.str();
   return G;

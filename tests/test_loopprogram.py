@@ -69,7 +69,7 @@ def test_generate_every_fixture_without_jit():
         assert [list(a) for a in plan.arguments] == m["arguments"]
         cfg = plan.config
         assert cfg["cells_per_block"] in (1, 2, 4, 8, 16, 32)
-        assert cfg["threads"] % 32 == 0 and cfg["threads"] <= 256
+        assert cfg["threads"] % 32 == 0 and cfg["threads"] <= 512
         assert cfg["cubin_bytes"] == 0
         if cfg["global_scratch"]:
             assert cfg["smem_bytes"] <= 64 * 1024 + 16
