@@ -19,7 +19,7 @@ from .elements import (coordinate_element, lagrange_interval, lagrange_tables,
 from .forms import (REGISTRY, FormSpec, action_form, default_quadrature,
                     form_element, neohookean_residual_form)
 from .plan import KernelPlan, compile_form, compile_kernel
-from .loopprogram import LoopProgramPlan, load_program
+from .loopprogram import LoopProgramPlan, load_program, program_flops
 from .runtime import (evaluate_batched, evaluate_batched_pair, evaluate_host,
                       launch_count, load_library, sum_squares)
 

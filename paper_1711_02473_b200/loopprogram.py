@@ -37,7 +37,7 @@ import numpy as np
 from .errors import NativeError, ShapeMismatch, UsageError
 from . import runtime as _rt
 
-__all__ = ["LoopProgramPlan", "load_program"]
+__all__ = ["LoopProgramPlan", "load_program", "program_flops"]
 
 FMA = 1
 NO_JIT = 2
@@ -196,6 +196,40 @@ class LoopProgramPlan:
             _rt._check(self._libref.sfk_program_eval(self._handle, ncells, out.data_ptr(), ptrs,
                                                      len(self.arguments), stream))
         return out.reshape(rsize) if squeeze else out
+
+
+_OPS = frozenset(("+", "*", "/", "pow", "min", "max", "call", "cmp"))
+
+
+def _expr_ops(e):
+    if not isinstance(e, list) or not e or not isinstance(e[0], str):
+        return 0
+    tag = e[0]
+    if tag in ("lit", "indexed", "flex", "delta", "var", "table", "idx"):
+        return 0
+    n = 1 if tag in _OPS else 0
+    return n + sum(_expr_ops(x) for x in e[1:] if isinstance(x, list))
+
+
+def program_flops(program):
+    """The reference's static flop count of a LoopProgram
+    (``scheduling.count_flops``, scheduling.py:416-437, with the operation
+    model of ``scalar_ops``, :123-131): arithmetic, function and comparison
+    nodes count 1, an accumulation adds 1, loops multiply, ZeroFill, Delta and
+    table loads are free.  Used as F_alg for the program path's roofline."""
+    doc = json.loads(_text_of(program))
+
+    def walk(stmts, mult):
+        total = 0
+        for st in stmts:
+            if st[0] == "loop":
+                total += walk(st[2], mult * st[1][2])
+            elif st[0] == "assign":
+                total += _expr_ops(st[2]) * mult
+            elif st[0] == "accumulate":
+                total += (_expr_ops(st[2]) + 1) * mult
+        return total
+    return walk(doc["body"], 1)
 
 
 def load_program(program, fma=False, jit=True):

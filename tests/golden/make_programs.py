@@ -152,7 +152,7 @@ def _one(case):
     meta = {"key": key, "form": form, "cell": cell, "degree": degree, "mode": mode,
             "variant": variant, "quadrature": quad, "ncells": ncells, "name": prog.name,
             "return": list(prog.return_buffer), "arguments": [list(a) for a in prog.arguments],
-            **flags}
+            "flops": scheduling.count_flops(prog).total_flops, **flags}
     return key, text, inputs, A, meta
 
 

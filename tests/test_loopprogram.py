@@ -19,7 +19,8 @@ import pytest
 
 from conftest import GOLDEN, rel_err
 from oracle.loopprog import program_iterations, run_program
-from paper_1711_02473_b200 import compile_kernel, evaluate_batched, load_program, runtime
+from paper_1711_02473_b200 import (compile_kernel, evaluate_batched, load_program,
+                                   program_flops, runtime)
 from paper_1711_02473_b200 import workloads
 from paper_1711_02473_b200.errors import NativeError
 
@@ -79,6 +80,12 @@ def test_generate_every_fixture_without_jit():
         assert plan.entry in src and "__global__" in src
         # deterministic generation
         assert load_program(text, jit=False).cuda_source == src
+
+
+def test_program_flops_equal_reference_count_flops():
+    for key in KEYS:
+        text, _, _ = fixture(key)
+        assert program_flops(text) == META[key]["flops"], key
 
 
 def test_imperfect_nests_run_thread_per_cell():
