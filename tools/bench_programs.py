@@ -19,9 +19,11 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from paper_1711_02473_b200 import compile_kernel, evaluate_batched, load_program  # noqa: E402
+from paper_1711_02473_b200 import (compile_kernel, evaluate_batched, load_program,  # noqa: E402
+                                   program_flops, runtime)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
+HBM_GBS = 6549.8   # MEASURED_PEAKS.json hbm_gbs
 DEFAULT = ["action_laplace_hex_p1", "action_laplace_hex_p2", "action_laplace_hex_p3",
            "action_laplace_hex_p4", "action_laplace_hex_p6", "laplace_hex_p2", "laplace_hex_p3",
            "stokes_momentum_hex_p2", "vector_mass_hex_p2", "weighted_laplace_prism_p2",
@@ -56,6 +58,7 @@ def main():
     idx = {m["key"]: m for m in json.load(open(os.path.join(GOLDEN, "programs.json")))}
     z = np.load(os.path.join(GOLDEN, "programs.npz"))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    p64 = max(runtime.fp64_peak(0.5))
     for key in a.keys or DEFAULT:
         m = idx[key]
         text = bytes(z[key + "__json"]).decode()
@@ -68,8 +71,16 @@ def main():
             ins[name] = torch.from_numpy(np.tile(v, (reps, 1))[:cells].copy()).cuda()
         out = torch.empty((cells, m["return"][1]), dtype=torch.float64, device="cuda")
         ms = timeit(lambda: evaluate_batched(plan, ins, out=out), a.reps, flush)
+        fl = program_flops(text)
+        nbytes = 8 * (m["return"][1] + sum(sz for _, sz in m["arguments"]))
+        tf = fl * cells / ms * 1e-9
+        t_roof = cells * max(fl / (p64 * 1e12), nbytes / (HBM_GBS * 1e9)) * 1e3
         rec = {"key": key, "cells": cells, "ms": round(ms, 5),
-               "cells_per_s": round(cells / ms * 1e3, 1), "config": plan.config}
+               "cells_per_s": round(cells / ms * 1e3, 1), "flops_per_cell_ref": fl,
+               "bytes_per_cell": nbytes, "fp64_tflops_ref": round(tf, 3),
+               "hbm_gbs": round(nbytes * cells / ms * 1e-6, 1), "p64_tflops": round(p64, 2),
+               "bound": "fp64" if fl / (p64 * 1e12) >= nbytes / (HBM_GBS * 1e9) else "hbm",
+               "roofline_frac": round(t_roof / ms, 4), "config": plan.config}
         if key in HAND and not key.endswith("colloc"):
             hp = compile_kernel(*HAND[key])
             hms = timeit(lambda: evaluate_batched(hp, ins, out=out), a.reps, flush)
