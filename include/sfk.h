@@ -144,6 +144,48 @@ int sfk_eval_gather_scatter(const sfk_plan *plan, int64_t ncells,
                             double *y, const double *coords, void *stream);
 
 /*
+ * Assembled sparse matrices (local-matrix assembly +
+ * sparse insertion; the paper's "global assembly" step, PAPER.md:166-167,
+ * scoped out by the reference).
+ *
+ * sfk_csr_create: the CSR sparsity pattern of sum_c P_c^T A_c P_c for the
+ * cell -> dof map cell_dofs[ncells][ndofs_per_cell] (DEVICE, int32 global
+ * dof numbers < ndofs): rows 0..ndofs-1, row_ptr int64, col_idx int32
+ * sorted ascending within each row.  Built on the device (radix sort +
+ * unique of the (row, col) pairs), synchronous on `stream`; the pattern
+ * owns its device arrays (sfk_csr_info exposes them, sfk_csr_destroy frees
+ * them).  Requires ndofs^2 < 2^64.
+ */
+typedef struct sfk_csr sfk_csr;
+int sfk_csr_create(int64_t ncells, int ndofs_per_cell, const int32_t *cell_dofs,
+                   int64_t ndofs, void *stream, sfk_csr **out);
+int sfk_csr_info(const sfk_csr *pattern, int64_t *nrows, int64_t *nnz,
+                 int64_t **row_ptr, int32_t **col_idx);
+/* Entry map of a pattern: map[c][i][j] (DEVICE, int32, caller-allocated,
+ * ncells * ndofs_per_cell^2) = position of the cell entry (i, j) in
+ * col_idx/values.  Computed once per pattern (binary search per entry);
+ * passed to sfk_assemble_csr it turns every insertion into one load and one
+ * atomic.  Requires nnz < 2^31. */
+int sfk_csr_entry_map(const sfk_csr *pattern, int64_t ncells, int ndofs_per_cell,
+                      const int32_t *cell_dofs, int32_t *map, void *stream);
+int sfk_csr_destroy(sfk_csr *pattern);
+
+/*
+ * values[nnz] += the assembled hex Laplace stiffness matrix: the C5 kernel
+ * (plan kind SFK_KIND_LAPLACE_MATRIX, p <= 4) computes each cell matrix in
+ * shared memory/registers and scatter-adds it straight into the CSR values
+ * (fp64 atomics) — the (p+1)^6 local matrix never reaches HBM.  Positions
+ * come from entry_map (sfk_csr_entry_map) when it is non-NULL, else from a
+ * binary search of the column in its row.  DEVICE pointers, stream-ordered;
+ * zero `values` first.  Replaces: the caller's insertion loop around the
+ * emitted `laplace` kernel.
+ */
+int sfk_assemble_csr(const sfk_plan *plan, int64_t ncells,
+                     const int32_t *cell_dofs, const double *coords,
+                     const int64_t *row_ptr, const int32_t *col_idx,
+                     const int32_t *entry_map, double *values, void *stream);
+
+/*
  * Functionals/checksums of a device array x[0..n):
  *   out[0] = sum x_i^2,  out[1] = sum x_i        (overwritten)
  * `out` is a DEVICE buffer of at least SFK_SUM_WORKSPACE doubles (the tail is

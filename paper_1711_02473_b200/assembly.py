@@ -1,4 +1,4 @@
-"""Global (assembled) matrix-free operators — SURVEY.md §8(f) item 1.
+"""Global (assembled) operators — SURVEY.md §8(f) items 1 and 3.
 
 The reference stops at the per-cell kernel; global assembly is the caller's
 job.  The immediate caller of the hot path is the E-vector <->
@@ -8,6 +8,14 @@ vector, apply the cell kernel, scatter-add back (PAPER.md:176-189,
 C2 line kernel (``sfk_eval_gather_scatter``: gather fused into the x stage,
 fp64 atomic scatter fused into the transposed x stage), so the E-vector
 never exists in HBM.
+
+``CsrPattern`` + ``assemble_csr`` (§8(f) item 3) assemble the global
+stiffness matrix itself: the CSR pattern is built on the device from the
+cell -> dof map (``sfk_csr_create``: radix sort + unique of the (row, col)
+pairs) and the C5 local-matrix kernel scatter-adds every cell matrix
+straight into the CSR values (``sfk_assemble_csr``), so the (p+1)^6 local
+matrices never reach HBM.  ``CsrPattern.matrix`` wraps the result as a
+``torch.sparse_csr_tensor`` (cuSPARSE SpMV for the solver).
 
 ``lattice_dof_map`` numbers the continuous Q_p space of the structured
 jittered lattice used by the BASELINE configs: cell (cx, cy, cz), local dof
@@ -21,7 +29,8 @@ import numpy as np
 
 from .errors import NativeError, ShapeMismatch
 
-__all__ = ["lattice_dof_map", "lattice_boundary_mask", "GlobalOperator", "cg"]
+__all__ = ["lattice_dof_map", "lattice_boundary_mask", "GlobalOperator", "cg",
+           "CsrPattern", "assemble_csr"]
 
 
 def lattice_dof_map(nx, ny, nz, degree, ix_range=None):
@@ -136,3 +145,125 @@ def cg(op, b, fixed=None, tol=1e-10, maxiter=1000):
         p = r + (rr_new / rr) * p
         rr = rr_new
     return x, it, (rr.sqrt() / b2).item()
+
+
+class _DevArray:
+    """__cuda_array_interface__ view of a libsfk-owned device array."""
+
+    def __init__(self, ptr, n, typestr, owner):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
+                                         "data": (int(ptr or 0), False), "version": 3}
+        self._owner = owner
+
+
+class CsrPattern:
+    """Sparsity pattern of K = sum_c P_c^T A_c P_c on the device.
+
+    ``row_ptr`` (ndofs + 1, int64) and ``col_idx`` (nnz, int32, sorted per
+    row) are torch views of arrays owned by libsfk (freed with the pattern).
+    """
+
+    def __init__(self, cell_dofs, ndofs, stream=None):
+        import ctypes
+
+        import torch
+
+        from .runtime import _check, load_library
+
+        if cell_dofs.dtype != torch.int32 or not cell_dofs.is_cuda or cell_dofs.dim() != 2:
+            raise TypeError("cell_dofs must be a 2D int32 CUDA tensor")
+        cell_dofs = cell_dofs.contiguous()
+        self._lib = load_library()
+        self._h = ctypes.c_void_p()
+        if stream is None:
+            stream = torch.cuda.current_stream(cell_dofs.device).cuda_stream
+        with torch.cuda.device(cell_dofs.device):
+            _check(self._lib.sfk_csr_create(cell_dofs.shape[0], cell_dofs.shape[1],
+                                            cell_dofs.data_ptr(), int(ndofs), stream,
+                                            ctypes.byref(self._h)))
+        nrows, nnz = ctypes.c_int64(), ctypes.c_int64()
+        rp, ci = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(self._lib.sfk_csr_info(self._h, ctypes.byref(nrows), ctypes.byref(nnz),
+                                      ctypes.byref(rp), ctypes.byref(ci)))
+        self.nrows, self.nnz = nrows.value, nnz.value
+        self.device = cell_dofs.device
+        with torch.cuda.device(self.device):
+            self.row_ptr = torch.as_tensor(_DevArray(rp.value, self.nrows + 1, "<i8", self),
+                                           device=self.device)
+            self.col_idx = torch.as_tensor(_DevArray(ci.value, self.nnz, "<i4", self),
+                                           device=self.device)
+
+    def __del__(self):
+        try:
+            if self._h:
+                self._lib.sfk_csr_destroy(self._h)
+        except Exception:
+            pass
+
+    def entry_map(self, cell_dofs, stream=None):
+        """(C, nd^2) int32 CUDA tensor: position of every cell entry A_c[i][j]
+        in ``values`` (``sfk_csr_entry_map``; once per pattern, then every
+        ``assemble_csr(..., entry_map=m)`` inserts with one load + one atomic
+        per entry instead of a binary search)."""
+        import torch
+
+        from .runtime import _check
+
+        cell_dofs = cell_dofs.contiguous()
+        nc, nd = cell_dofs.shape
+        m = torch.empty((nc, nd * nd), dtype=torch.int32, device=cell_dofs.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(cell_dofs.device).cuda_stream
+        with torch.cuda.device(cell_dofs.device):
+            _check(self._lib.sfk_csr_entry_map(self._h, nc, nd, cell_dofs.data_ptr(),
+                                               m.data_ptr(), stream))
+        return m
+
+    def matrix(self, values):
+        """torch.sparse_csr_tensor over this pattern (values length nnz)."""
+        import torch
+
+        # torch wants one index dtype for both arrays
+        if self.nnz < 2 ** 31:
+            crow, col = self.row_ptr.to(torch.int32), self.col_idx
+        else:
+            crow, col = self.row_ptr, self.col_idx.to(torch.int64)
+        return torch.sparse_csr_tensor(crow, col, values, size=(self.nrows, self.nrows),
+                                       check_invariants=False)
+
+
+def assemble_csr(plan, cell_dofs, coords, pattern, values=None, entry_map=None, stream=None):
+    """Assembled stiffness matrix values (length pattern.nnz, float64 CUDA):
+    values += sum_c P_c^T A_c P_c with A_c the hex ``laplace`` cell matrix of
+    ``plan`` (C5 kernel, p <= 4).  ``values`` is zeroed unless given."""
+    import torch
+
+    from .runtime import _check, load_library, native_plan
+
+    if cell_dofs.dtype != torch.int32 or not cell_dofs.is_cuda:
+        raise TypeError("cell_dofs must be an int32 CUDA tensor")
+    if coords.dtype != torch.float64 or not coords.is_cuda:
+        raise TypeError("coords must be a float64 CUDA tensor")
+    nd = plan.return_size
+    n3 = int(round(nd ** 0.5))
+    if tuple(cell_dofs.shape) != (coords.shape[0], n3):
+        raise ShapeMismatch("cell_dofs must be (%d, %d)" % (coords.shape[0], n3))
+    cell_dofs = cell_dofs.contiguous()
+    coords = coords.contiguous()
+    if entry_map is not None and (entry_map.dtype != torch.int32 or not entry_map.is_contiguous()
+                                  or tuple(entry_map.shape) != (coords.shape[0], n3 * n3)):
+        raise ShapeMismatch("entry_map must be a contiguous int32 (%d, %d) tensor"
+                            % (coords.shape[0], n3 * n3))
+    if values is None:
+        values = torch.zeros(pattern.nnz, dtype=torch.float64, device=coords.device)
+    elif values.numel() != pattern.nnz:
+        raise ShapeMismatch("values must have nnz = %d entries" % pattern.nnz)
+    if stream is None:
+        stream = torch.cuda.current_stream(coords.device).cuda_stream
+    with torch.cuda.device(coords.device):
+        _check(load_library().sfk_assemble_csr(
+            native_plan(plan), coords.shape[0], cell_dofs.data_ptr(), coords.data_ptr(),
+            pattern.row_ptr.data_ptr(), pattern.col_idx.data_ptr(),
+            entry_map.data_ptr() if entry_map is not None else None, values.data_ptr(), stream))
+    return values
+

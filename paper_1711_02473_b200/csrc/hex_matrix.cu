@@ -46,8 +46,9 @@ struct MatCfg {
   static constexpr int KS = 6 * M3;          // K (6 unique entries) at every point
   static constexpr int TS = 2 * N * M;       // B and D copies (runtime-indexed reads)
   static constexpr int YS = 4 * M * N4;      // Y_g[qx][r] for one cell, all planes
+  static constexpr int DS = (CPB * N3 + 1) / 2;  // the cells' dof lists (int32, CSR mode)
   static constexpr size_t SMEM =
-      (size_t)(CPB * (ZS + KS + YS + 24) + TS) * sizeof(double);
+      (size_t)(CPB * (ZS + KS + YS + 24) + TS + DS) * sizeof(double);
 };
 
 // pair (l, l') -> symmetric K index: 00 11 22 01 02 12
@@ -60,10 +61,26 @@ __host__ __device__ constexpr int ksym(int l, int r) {
 //  Z_ll'[qx][qy][iz][jz] = sum_qz Tz Tz' K_ll'   (threads over (pair, qx, qy, iz, jz)),
 //  Y_g[qx][r]            = sum over pairs in g, qy (thread r = (iy, iz, jy, jz)),
 //  A[(ix,..),(jx,..)]    = sum_{g,qx} Tx Tx' Y_g[qx][r]   (thread r, then stores).
-template <int N, int M, int CPB>
+// Position of column `col` in the sorted CSR row [lo, hi) (lower bound).
+__device__ __forceinline__ int64_t csr_find(const int32_t* __restrict__ col_idx, int64_t lo,
+                                            int64_t hi, int32_t col) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(col_idx + mid) < col) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// CSR = false: A[cell][N3*N3] is written (the reference's per-cell output).
+// CSR = true : the cell matrices are scatter-added into the assembled CSR
+//              matrix (values A, pattern row_ptr / col_idx from sfk_csr_create)
+//              through cell_dofs — the local matrix never reaches HBM.
+template <int N, int M, int CPB, bool CSR>
 __global__ void __launch_bounds__(MatCfg<N, M, CPB>::THREADS)
 hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncells,
-                          const double* __restrict__ coords, double* __restrict__ A) {
+                          const double* __restrict__ coords, double* __restrict__ A,
+                          const int32_t* __restrict__ dofs, const int64_t* __restrict__ row_ptr,
+                          const int32_t* __restrict__ col_idx, const int32_t* __restrict__ emap) {
   using C = MatCfg<N, M, CPB>;
   constexpr int N2 = C::N2, N3 = C::N3, N4 = C::N4, M3 = C::M3;
   extern __shared__ double smem[];
@@ -72,12 +89,15 @@ hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncell
   double* sY = sK + CPB * C::KS;           // [CPB][4][M][N4]
   double* sC = sY + CPB * C::YS;           // [CPB][24]
   double* sT = sC + CPB * 24;              // B, D
+  int32_t* sD = reinterpret_cast<int32_t*>(sT + C::TS);  // [CPB][N3] (CSR)
   const int tid = threadIdx.x;
   const int64_t cell0 = (int64_t)blockIdx.x * CPB;
   const int64_t rem = ncells - cell0;
   const int ncb = rem < CPB ? (int)rem : CPB;
   for (int i = tid; i < CPB * 24; i += C::THREADS)
     sC[i] = i < ncb * 24 ? __ldg(coords + cell0 * 24 + i) : 0.0;
+  if (CSR)
+    for (int i = tid; i < ncb * N3; i += C::THREADS) sD[i] = __ldg(dofs + cell0 * N3 + i);
   for (int i = tid; i < N * M; i += C::THREADS) {
     sT[i] = T.B[i];
     sT[N * M + i] = T.D[i];
@@ -181,20 +201,45 @@ hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncell
         }
       }
     }
-    double* out = A + (cell0 + c) * (int64_t)(N3 * N3);
     const int rowoff = iy * N + iz;   // + ix * N2  -> test index
     const int coloff = jy * N + jz;   // + jx * N2  -> trial index
+    if (CSR && emap) {
+      // positions precomputed per pattern (sfk_csr_entry_map): one load each
+      const int32_t* mp = emap + (cell0 + c) * (int64_t)(N3 * N3);
 #pragma unroll
-    for (int ix = 0; ix < N; ++ix)
+      for (int ix = 0; ix < N; ++ix)
 #pragma unroll
-      for (int jx = 0; jx < N; ++jx)
-        out[(int64_t)(ix * N2 + rowoff) * N3 + jx * N2 + coloff] = acc[ix][jx];
+        for (int jx = 0; jx < N; ++jx)
+          atomicAdd(A + __ldg(mp + (ix * N2 + rowoff) * N3 + jx * N2 + coloff), acc[ix][jx]);
+    } else if (CSR) {
+      const int32_t* cd = sD + c * N3;
+      int32_t cols[N];
+#pragma unroll
+      for (int jx = 0; jx < N; ++jx) cols[jx] = cd[jx * N2 + coloff];
+#pragma unroll
+      for (int ix = 0; ix < N; ++ix) {
+        const int32_t row = cd[ix * N2 + rowoff];
+        const int64_t lo = __ldg(row_ptr + row), hi = __ldg(row_ptr + row + 1);
+#pragma unroll
+        for (int jx = 0; jx < N; ++jx)
+          atomicAdd(A + csr_find(col_idx, lo, hi, cols[jx]), acc[ix][jx]);
+      }
+    } else {
+      double* out = A + (cell0 + c) * (int64_t)(N3 * N3);
+#pragma unroll
+      for (int ix = 0; ix < N; ++ix)
+#pragma unroll
+        for (int jx = 0; jx < N; ++jx)
+          out[(int64_t)(ix * N2 + rowoff) * N3 + jx * N2 + coloff] = acc[ix][jx];
+    }
   }
 }
 
-template <int N, int M, int CPB>
+template <int N, int M, int CPB, bool CSR = false>
 static int launch_mat(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                      cudaStream_t s) {
+                      cudaStream_t s, const int32_t* dofs = nullptr,
+                      const int64_t* row_ptr = nullptr, const int32_t* col_idx = nullptr,
+                      const int32_t* emap = nullptr) {
   using C = MatCfg<N, M, CPB>;
   TabsMat<N, M> T;
   for (int i = 0; i < N; ++i)
@@ -208,11 +253,11 @@ static int launch_mat(const sfk_plan* p, int64_t ncells, double* A, const double
     T.Bc[M + q] = p->Bc[p->m + q];
   }
   const unsigned grid = (unsigned)((ncells + CPB - 1) / CPB);
-  auto kern = hex_laplace_matrix_kernel<N, M, CPB>;
+  auto kern = hex_laplace_matrix_kernel<N, M, CPB, CSR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)C::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_matrix)");
-  kern<<<grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, A);
+  kern<<<grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, A, dofs, row_ptr, col_idx, emap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_matrix_kernel launch");
 }
@@ -232,6 +277,29 @@ int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double
   }
   return fail(SFK_EUNSUPPORTED,
               "hex laplace matrix: no kernel for n=%d, m=%d (n==m in 2..5, p<=4)", p->n, p->m);
+}
+
+int launch_hex_matrix_csr(const sfk_plan* p, int64_t ncells, const int32_t* dofs,
+                          const double* coords, const int64_t* row_ptr, const int32_t* col_idx,
+                          const int32_t* emap, double* values, cudaStream_t s) {
+  if (p->collocated || p->n != p->m)
+    return fail(SFK_EUNSUPPORTED, "CSR assembly: hex laplace with m == n only");
+  switch (p->n) {
+    case 2:
+      return launch_mat<2, 2, 16, true>(p, ncells, values, coords, s, dofs, row_ptr, col_idx,
+                                        emap);
+    case 3:
+      return launch_mat<3, 3, 3, true>(p, ncells, values, coords, s, dofs, row_ptr, col_idx,
+                                        emap);
+    case 4:
+      return launch_mat<4, 4, 1, true>(p, ncells, values, coords, s, dofs, row_ptr, col_idx,
+                                        emap);
+    case 5:
+      return launch_mat<5, 5, 1, true>(p, ncells, values, coords, s, dofs, row_ptr, col_idx,
+                                        emap);
+    default: break;
+  }
+  return fail(SFK_EUNSUPPORTED, "CSR assembly: no kernel for n=%d (p<=4)", p->n);
 }
 
 }  // namespace sfk

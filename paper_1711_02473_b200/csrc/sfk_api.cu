@@ -338,6 +338,20 @@ int sfk_eval_gather_scatter(const sfk_plan* p, int64_t ncells, const int32_t* ce
   return launch_hex_action_gs(p, ncells, cell_dofs, x, y, coords, (cudaStream_t)stream);
 }
 
+int sfk_assemble_csr(const sfk_plan* p, int64_t ncells, const int32_t* cell_dofs,
+                     const double* coords, const int64_t* row_ptr, const int32_t* col_idx,
+                     const int32_t* entry_map, double* values, void* stream) {
+  if (!p) return fail(SFK_EINVAL, "plan is NULL");
+  if (ncells < 0) return fail(SFK_EINVAL, "ncells < 0");
+  if (ncells == 0) return SFK_OK;
+  if (!cell_dofs || !coords || !row_ptr || !col_idx || !values)
+    return fail(SFK_EINVAL, "NULL pointer argument");
+  if (p->kind != SFK_KIND_LAPLACE_MATRIX || p->dim != 3)
+    return fail(SFK_EUNSUPPORTED, "CSR assembly: hex laplace (matrix) plans only");
+  return launch_hex_matrix_csr(p, ncells, cell_dofs, coords, row_ptr, col_idx, entry_map, values,
+                               (cudaStream_t)stream);
+}
+
 int sfk_sum_squares(const double* x, int64_t n, double* out, void* stream) {
   if (n < 0) return fail(SFK_EINVAL, "n < 0");
   if (!out) return fail(SFK_EINVAL, "out is NULL");

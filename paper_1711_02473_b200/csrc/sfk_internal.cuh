@@ -82,6 +82,9 @@ int launch_quad_action(const sfk_plan* p0, const sfk_plan* p1, int64_t ncells,
                        const double* w0, cudaStream_t s);
 int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A,
                       const double* coords, cudaStream_t s);
+int launch_hex_matrix_csr(const sfk_plan* p, int64_t ncells, const int32_t* dofs,
+                          const double* coords, const int64_t* row_ptr, const int32_t* col_idx,
+                          const int32_t* emap, double* values, cudaStream_t s);
 int launch_hex_neohookean(const sfk_plan* p, int64_t ncells, double* A,
                           const double* coords, const double* w0,
                           cudaStream_t s);

@@ -40,6 +40,8 @@ EXPORTED_SYMBOLS = (
     "sfk_launch_count", "sfk_last_error", "sfk_device_info", "sfk_fp64_peak",
     "sfk_eval_gather_scatter", "sfk_program_create", "sfk_program_destroy",
     "sfk_program_sizes", "sfk_program_config", "sfk_program_text", "sfk_program_eval",
+    "sfk_csr_create", "sfk_csr_info", "sfk_csr_destroy", "sfk_assemble_csr",
+    "sfk_csr_entry_map",
 )
 ABI_VERSION = 1
 SUM_WORKSPACE = 1024
@@ -81,6 +83,18 @@ def _declare(lib):
     if hasattr(lib, "sfk_eval_gather_scatter"):   # absent from pre-(f) A/B builds
         lib.sfk_eval_gather_scatter.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, _vp]
         lib.sfk_eval_gather_scatter.restype = ci
+    if hasattr(lib, "sfk_csr_create"):
+        lib.sfk_csr_create.argtypes = [i64, ci, _vp, i64, _vp, ctypes.POINTER(_vp)]
+        lib.sfk_csr_create.restype = ci
+        lib.sfk_csr_info.argtypes = [_vp, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                     ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
+        lib.sfk_csr_info.restype = ci
+        lib.sfk_csr_destroy.argtypes = [_vp]
+        lib.sfk_csr_destroy.restype = ci
+        lib.sfk_csr_entry_map.argtypes = [_vp, i64, ci, _vp, _vp, _vp]
+        lib.sfk_csr_entry_map.restype = ci
+        lib.sfk_assemble_csr.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+        lib.sfk_assemble_csr.restype = ci
 
 
 def load_library(build_if_missing=True):

@@ -76,3 +76,101 @@ def test_cg_poisson_manufactured(cuda):
     x, it, res = cg(op, b, fixed=fixed, tol=1e-11, maxiter=2000)
     assert res < 1e-11
     assert (x - xs).abs().max().item() < 1e-8
+
+
+# ---------------------------------------------------------------------------
+# assembled CSR matrices
+
+
+def _scipy_csr(coords, cell_dofs, nd, p):
+    """Oracle: dense cell matrices from the CPU oracle, summed by scipy."""
+    import scipy.sparse as sp
+
+    plan = compile_kernel("laplace", "hex", p)
+    A = cpu.evaluate(plan, {"coords": coords}).reshape(len(cell_dofs), -1)
+    n3 = cell_dofs.shape[1]
+    rows = np.repeat(cell_dofs, n3, axis=1).reshape(-1)
+    cols = np.tile(cell_dofs, (1, n3)).reshape(-1)
+    K = sp.coo_matrix((A.reshape(-1), (rows, cols)), shape=(nd, nd)).tocsr()
+    K.sum_duplicates()
+    K.sort_indices()
+    return K
+
+
+def _permuted_dofs(dims, p, seed=3):
+    """Lattice numbering scrambled by a random permutation (rows whose
+    columns are not monotone in the local order)."""
+    g = lattice_dof_map(*dims, p)
+    nd = lattice_ndofs(*dims, p)
+    perm = np.random.default_rng(seed).permutation(nd).astype(np.int32)
+    return np.ascontiguousarray(perm[g]), nd
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+@pytest.mark.parametrize("numbering", ["lattice", "permuted"])
+def test_csr_assembly_matches_oracle(cuda, p, numbering):
+    torch = cuda
+    from paper_1711_02473_b200.assembly import CsrPattern, assemble_csr
+
+    dims = (3, 2, 3)
+    coords = workloads.lattice_coords(*dims)
+    if numbering == "lattice":
+        g, nd = lattice_dof_map(*dims, p), lattice_ndofs(*dims, p)
+    else:
+        g, nd = _permuted_dofs(dims, p)
+    K = _scipy_csr(coords, g, nd, p)
+    gd = torch.from_numpy(g).cuda()
+    pat = CsrPattern(gd, nd)
+    assert pat.nnz == K.nnz and pat.nrows == nd
+    assert np.array_equal(pat.row_ptr.cpu().numpy(), K.indptr.astype(np.int64))
+    assert np.array_equal(pat.col_idx.cpu().numpy(), K.indices.astype(np.int32))
+    vals = assemble_csr(compile_kernel("laplace", "hex", p), gd,
+                        torch.from_numpy(coords).cuda(), pat).cpu().numpy()
+    assert np.abs(vals - K.data).max() <= 1e-12 * np.abs(K.data).max()
+    # the entry-map insertion path: positions, then the same values
+    emap = pat.entry_map(gd)
+    kk = np.asarray(K[np.repeat(g, g.shape[1], axis=1).reshape(-1),
+                      np.tile(g, (1, g.shape[1])).reshape(-1)]).reshape(-1)
+    pos = emap.cpu().numpy().reshape(-1)
+    assert np.array_equal(K.indices[pos], np.tile(g, (1, g.shape[1])).reshape(-1))
+    assert np.array_equal(K.data[pos], kk)
+    vm = assemble_csr(compile_kernel("laplace", "hex", p), gd, torch.from_numpy(coords).cuda(),
+                      pat, entry_map=emap).cpu().numpy()
+    assert np.abs(vm - K.data).max() <= 1e-12 * np.abs(K.data).max()
+    # assembling twice into the same values doubles them (accumulate semantics)
+    v2 = assemble_csr(compile_kernel("laplace", "hex", p), gd, torch.from_numpy(coords).cuda(),
+                      pat, values=torch.from_numpy(vals).cuda()).cpu().numpy()
+    assert np.abs(v2 - 2 * K.data).max() <= 2e-12 * np.abs(K.data).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_csr_matvec_equals_matrix_free_operator(cuda, p):
+    """The assembled matrix and the fused matrix-free operator are the same K."""
+    torch = cuda
+    from paper_1711_02473_b200.assembly import CsrPattern, GlobalOperator, assemble_csr
+
+    dims = (4, 4, 3)
+    coords = torch.from_numpy(workloads.lattice_coords(*dims)).cuda()
+    g = torch.from_numpy(lattice_dof_map(*dims, p)).cuda()
+    nd = lattice_ndofs(*dims, p)
+    pat = CsrPattern(g, nd)
+    K = pat.matrix(assemble_csr(compile_kernel("laplace", "hex", p), g, coords, pat))
+    x = torch.from_numpy(np.random.default_rng(7).uniform(-1, 1, nd)).cuda()
+    y_csr = (K @ x.unsqueeze(1)).squeeze(1)
+    y_mf = GlobalOperator(compile_kernel("action_laplace", "hex", p), g, coords, nd).apply(x)
+    assert (y_csr - y_mf).abs().max().item() <= 1e-12 * y_mf.abs().max().item()
+
+
+@pytest.mark.gpu
+def test_csr_pattern_edge_cases(cuda):
+    torch = cuda
+    from paper_1711_02473_b200.assembly import CsrPattern
+
+    empty = CsrPattern(torch.zeros((0, 8), dtype=torch.int32, device="cuda"), 5)
+    assert empty.nnz == 0 and empty.row_ptr.cpu().tolist() == [0] * 6
+    # one cell, a dof unused by every cell -> empty row
+    one = CsrPattern(torch.tensor([[0, 2]], dtype=torch.int32, device="cuda"), 3)
+    assert one.row_ptr.cpu().tolist() == [0, 2, 2, 4]
+    assert one.col_idx.cpu().tolist() == [0, 2, 0, 2]
