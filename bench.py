@@ -8,8 +8,10 @@ roofline", config C2 (configs[1]): 2^18 jittered trilinear hex cells per GPU,
 A STEP is one application of the action at every degree p = 1..8 over the
 whole batch (8 sfk_eval launches, inputs resident in HBM).  value = total
 local DoFs processed by all ranks / max-over-ranks device time (GDoF/s).
-Weak scaling: each rank owns its own 2^18-cell slab of a (64*N, 64, 64)
-lattice (cell-range sharding, no data-path collective).
+Weak scaling (default): each rank owns its own 2^18-cell slab of a
+(64*N, 64, 64) lattice (cell-range sharding, no data-path collective;
+SURVEY.md §8(e)).  `--scaling strong`: the (64, 64, 64) lattice is fixed and
+split into ix-slabs over the ranks (SURVEY.md §8(e) asks for both).
 
 Extra keys: per_degree (ms, GDoF/s, cells/s, roofline fraction for every p),
 roofline (dominant kernel, vs the FP64 peak measured live), cpu_baseline
@@ -45,7 +47,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--degrees", default="1-8")
-    ap.add_argument("--lattice", default="64,64,64", help="cells per rank (nx,ny,nz)")
+    ap.add_argument("--lattice", default="64,64,64",
+                    help="cells per rank (weak) or in total (strong), nx,ny,nz")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-cells", type=int, default=1 << 15,
@@ -235,12 +239,26 @@ def main():
     degs = degrees_of(args.degrees)
     nx, ny, nz = (int(x) for x in args.lattice.split(","))
 
-    # rank r owns the slab ix in [nx*r, nx*(r+1)) of a (nx*world, ny, nz) lattice
-    coords_np = workloads.lattice_coords(nx * world, ny, nz, ix_range=(nx * rank, nx * (rank + 1)))
-    ncells = coords_np.shape[0]
+    if args.scaling == "weak":
+        # rank r owns the slab ix in [nx*r, nx*(r+1)) of a (nx*world, ny, nz) lattice
+        coords_np = workloads.lattice_coords(nx * world, ny, nz,
+                                             ix_range=(nx * rank, nx * (rank + 1)))
+        ncells = coords_np.shape[0]
+        total_cells = world * ncells
+        host_u = {p: workloads.uniform_dofs(ncells, (p + 1) ** 3, seed=workloads.SEED_U + rank)
+                  for p in degs}
+    else:
+        # the (nx, ny, nz) lattice is fixed; rank r owns a balanced ix-slab of it
+        from paper_1711_02473_b200.parallel import shard_range
+        lo, hi = shard_range(nx, rank, world)
+        coords_np = workloads.lattice_coords(nx, ny, nz, ix_range=(lo, hi))
+        ncells = coords_np.shape[0]
+        total_cells = nx * ny * nz
+        c0 = lo * ny * nz
+        host_u = {p: np.ascontiguousarray(
+                      workloads.uniform_dofs(total_cells, (p + 1) ** 3)[c0:c0 + ncells])
+                  for p in degs}
     plans = {p: compile_kernel("action_laplace", "hex", p) for p in degs}
-    host_u = {p: workloads.uniform_dofs(ncells, (p + 1) ** 3, seed=workloads.SEED_U + rank)
-              for p in degs}
     coords = torch.from_numpy(coords_np).to(dev)
     u = {p: torch.from_numpy(host_u[p]).to(dev) for p in degs}
     out = {p: torch.empty_like(u[p]) for p in degs}
@@ -292,7 +310,7 @@ def main():
 
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", HBM_FALLBACK)
-    total_dofs = world * sum(ncells * (p + 1) ** 3 for p in degs)
+    total_dofs = sum(total_cells * (p + 1) ** 3 for p in degs)
     value = total_dofs / (step_ms * 1e-3) / 1e9
     per = []
     dom = None
@@ -333,10 +351,13 @@ def main():
 
     line = {"metric": METRIC, "value": round(value, 4), "unit": "GDoF/s", "n_gpus": world,
             "steps": K, "warmup": args.warmup, "ms_per_step": round(step_ms, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "f64",
             "data": "synthetic (seeded jittered lattice, u~U[-1,1])",
             "config": {"workload": "C2 hex Q_p Laplace action, GL (p+1)^3, p=%s" % args.degrees,
-                       "cells_per_gpu": ncells, "lattice_per_gpu": [nx, ny, nz],
+                       "cells_per_gpu": ncells, "cells_total": total_cells,
+                       ("lattice_per_gpu" if args.scaling == "weak" else "lattice_total"):
+                           [nx, ny, nz],
                        "parallelism": "cell-range shards x%d" % world,
                        "l2": "flushed between steps (256 MiB write)"},
             "per_degree": per, "roofline": roofline, "gpu_launches": int(gpu_launches),
