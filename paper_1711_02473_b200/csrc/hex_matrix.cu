@@ -26,6 +26,8 @@
 // r01 version spilled it).  Output rows are written straight from registers:
 // for fixed (ix, jx) a warp stores runs of n^2 contiguous doubles; the 125 KB
 // (p=4) of a cell is complete in L2 before eviction, so DRAM sees full lines.
+#include <cstdlib>
+
 #include "hex_geometry.cuh"
 
 namespace sfk {
@@ -268,7 +270,16 @@ int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double
     return fail(SFK_EUNSUPPORTED, "hex laplace matrix: collocated variant not instantiated");
   if (p->n == p->m) {
     switch (p->n) {
-      case 2: return launch_mat<2, 2, 16>(p, ncells, A, coords, s);
+      case 2: {
+        // thread-per-cell kernel (hex_matrix_p1.cu); SFK_C5_P1=phase selects
+        // the CTA-phase kernel below for A/B runs
+        static const bool phase = [] {
+          const char* e = std::getenv("SFK_C5_P1");
+          return e && e[0] == 'p';
+        }();
+        if (!phase) return launch_hex_matrix_p1(p, ncells, A, coords, s);
+        return launch_mat<2, 2, 16>(p, ncells, A, coords, s);
+      }
       case 3: return launch_mat<3, 3, 3>(p, ncells, A, coords, s);
       case 4: return launch_mat<4, 4, 1>(p, ncells, A, coords, s);
       case 5: return launch_mat<5, 5, 1>(p, ncells, A, coords, s);
