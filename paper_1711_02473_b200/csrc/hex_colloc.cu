@@ -48,12 +48,17 @@ struct CollocCfg {
   }
 };
 
-// Register policy per n, from same-box A/B runs (profiles/r01ae_*): 2 =
+// Register policy per n, from same-box A/B runs (profiles/r01ae_*,
+// r01an_c3_minb.jsonl: n = 6 and 13 moved to 2 after the kappa/adjugate
+// changes, 0.29 -> 0.20 ms and 3.06 -> 2.11 ms): 2 =
 // __launch_bounds__(T, 2) (two CTAs per SM, no spills at that cap), 1 =
 // (T, 1), 0 = (T) only — ptxas picks different (and here faster) register
 // budgets for the last two (e.g. n = 16: 132 vs 254 registers).
 __host__ __device__ constexpr int colloc_minb(int n) {
-  return (n <= 5 || n == 7 || n == 9 || n == 11 || n == 16) ? 2 : (n == 8 || n == 15) ? 0 : 1;
+#ifdef SFK_COLLOC_MINB
+  if (SFK_COLLOC_MINB >= 0) return SFK_COLLOC_MINB;   // A/B builds (tools/build_variant.py)
+#endif
+  return (n <= 7 || n == 9 || n == 11 || n == 13 || n == 16) ? 2 : (n == 8 || n == 15) ? 0 : 1;
 }
 
 template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED>
