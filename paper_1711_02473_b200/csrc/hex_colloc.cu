@@ -49,8 +49,10 @@ struct CollocCfg {
 };
 
 // Register policy per n, from same-box A/B runs (profiles/r01ae_*,
-// r01an_c3_minb.jsonl: n = 6 and 13 moved to 2 after the kappa/adjugate
-// changes, 0.29 -> 0.20 ms and 3.06 -> 2.11 ms): 2 =
+// r01an_c3_minb.jsonl, r01ao_c3_cpb.jsonl: n = 6, 10, 12, 13 moved to 2
+// after the kappa/adjugate changes, with 2 / 1 cells per CTA at n = 10 / 12;
+// p = 5: 0.29 -> 0.20 ms, p = 9: 1.21 -> 0.93, p = 11: 2.11 -> 1.96,
+// p = 12: 3.06 -> 2.11): 2 =
 // __launch_bounds__(T, 2) (two CTAs per SM, no spills at that cap), 1 =
 // (T, 1), 0 = (T) only — ptxas picks different (and here faster) register
 // budgets for the last two (e.g. n = 16: 132 vs 254 registers).
@@ -58,7 +60,7 @@ __host__ __device__ constexpr int colloc_minb(int n) {
 #ifdef SFK_COLLOC_MINB
   if (SFK_COLLOC_MINB >= 0) return SFK_COLLOC_MINB;   // A/B builds (tools/build_variant.py)
 #endif
-  return (n <= 7 || n == 9 || n == 11 || n == 13 || n == 16) ? 2 : (n == 8 || n == 15) ? 0 : 1;
+  return (n <= 7 || (n >= 9 && n <= 13) || n == 16) ? 2 : (n == 8 || n == 15) ? 0 : 1;
 }
 
 template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED>
@@ -273,6 +275,14 @@ static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* 
   return cuda_status(cudaGetLastError(), "hex_colloc_action_kernel launch");
 }
 
+// cells per CTA at n = 10, 12 (overridable for A/B builds)
+#ifndef SFK_COLLOC_CPB10
+#define SFK_COLLOC_CPB10 2
+#endif
+#ifndef SFK_COLLOC_CPB12
+#define SFK_COLLOC_CPB12 1
+#endif
+
 int launch_hex_colloc_action(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                              const double* w0, const double* w1, cudaStream_t s) {
   if (p->n != p->m)
@@ -287,9 +297,9 @@ int launch_hex_colloc_action(const sfk_plan* p, int64_t ncells, double* A, const
     case 7: return launch_n<7, 5, 7, 52, 369>(p, ncells, A, coords, w0, w1, s);
     case 8: return launch_n<8, 4, 9, 72, 576>(p, ncells, A, coords, w0, w1, s);
     case 9: return launch_n<9, 3, 9, 89, 801>(p, ncells, A, coords, w0, w1, s);
-    case 10: return launch_n<10, 3, 11, 110, 1100>(p, ncells, A, coords, w0, w1, s);
+    case 10: return launch_n<10, SFK_COLLOC_CPB10, 11, 110, 1100>(p, ncells, A, coords, w0, w1, s);
     case 11: return launch_n<11, 2, 11, 123, 1353>(p, ncells, A, coords, w0, w1, s);
-    case 12: return launch_n<12, 2, 13, 156, 1872>(p, ncells, A, coords, w0, w1, s);
+    case 12: return launch_n<12, SFK_COLLOC_CPB12, 13, 156, 1872>(p, ncells, A, coords, w0, w1, s);
     case 13: return launch_n<13, 1, 13, 169, 2197>(p, ncells, A, coords, w0, w1, s);
     case 14: return launch_n<14, 1, 17, 238, 3332>(p, ncells, A, coords, w0, w1, s);
     case 15: return launch_n<15, 1, 15, 225, 3375>(p, ncells, A, coords, w0, w1, s);
