@@ -46,11 +46,16 @@ struct HexAction2Cfg {
 // ROLL: 0 = everything unrolled; 1 = pointwise loop rolled; 2 = also the
 // outer (output-index) loop of every contraction rolled (table entries then
 // come from warp-uniform constant loads; code size drops ~M-fold).
-template <int N, int M, int CPB, int R, int MINB, int ROLL>
+// GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
+// item 1), as in hex_action3.cu: `u` is x, `A` is y, cmap[c][i] the global
+// dof of local dof i; the map (int32) is double-buffered in the u buffer, x
+// is gathered through it in the x stage and y scattered with fp64 atomics
+// in the transposed x stage.
+template <int N, int M, int CPB, int R, int MINB, int ROLL, bool GS = false>
 __global__ void __launch_bounds__(HexAction2Cfg<N, M, CPB, R>::THREADS, MINB)
 hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
-                      double* __restrict__ A) {
+                      double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
   using C = HexAction2Cfg<N, M, CPB, R>;
   constexpr int NN = C::NN, MN = C::MN, MM = C::MM, N3 = C::N3, PX = C::PX, LZ = C::LZ;
   constexpr int XA = C::XA, YA = C::YA, TH = C::THREADS;
@@ -62,6 +67,8 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
   double* sCo = sU + C::USZ;                // [2][CPB*24] (double buffer)
   const int tid = threadIdx.x;
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  int* sMap = reinterpret_cast<int*>(sU);   // GS: [2][CPB*N3] int32 in the u buffer
+  static_assert(!GS || 2 * CPB * N3 <= 2 * C::USZ, "map double buffer does not fit");
 
   // u of the next batch streams into the single u buffer as soon as the
   // current x stage has consumed it (overlapping the y, z, y^T, x^T stages);
@@ -69,7 +76,12 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
   auto prefetch = [&](int64_t b, int buf) {
     const int64_t c0 = b * CPB;
     const int nc = (int)((ncells - c0) < CPB ? (ncells - c0) : CPB);
-    async_copy_phase<TH>(sU + dst_shift(u + c0 * N3), u + c0 * N3, nc * N3, tid);
+    if (GS) {
+      for (int i = tid; i < nc * N3; i += TH)
+        cp_async4(sMap + buf * CPB * N3 + i, cmap + c0 * N3 + i);
+    } else {
+      async_copy_phase<TH>(sU + dst_shift(u + c0 * N3), u + c0 * N3, nc * N3, tid);
+    }
     async_copy<TH>(sCo + buf * C::CSZ, coords + c0 * 24, nc * 24, tid);
     cp_async_commit();
   };
@@ -82,7 +94,8 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
     const int ncb = (int)((ncells - cell0) < CPB ? (ncells - cell0) : CPB);
     cp_async_wait<0>();
     __syncthreads();
-    const double* su = sU + dst_shift(u + cell0 * N3);
+    const double* su = sU + (GS ? 0 : dst_shift(u + cell0 * N3));
+    const int* smap = sMap + cur * CPB * N3;
     const double* sC = sCo + cur * C::CSZ;
 
     // ---- x stage: lines (c, iy, iz): X0 = Bx u, X1 = Dx u -------------
@@ -99,7 +112,9 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
         const int c = lc / NN, r = lc - c * NN;
         const bool live = on[j] && c < ncb;
 #pragma unroll
-        for (int i = 0; i < N; ++i) uu[j][i] = su[c * N3 + i * NN + r];
+        for (int i = 0; i < N; ++i)
+          uu[j][i] = GS ? (live ? __ldg(u + smap[c * N3 + i * NN + r]) : 0.0)
+                        : su[c * N3 + i * NN + r];
         if (!live) {
 #pragma unroll
           for (int i = 0; i < N; ++i) uu[j][i] = 0.0;
@@ -396,7 +411,8 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
         for (int j = 0; j < R; ++j)
           if (on[j]) {
             const int c = ln[j] / NN, r = ln[j] - c * NN;
-            A[(cell0 + c) * N3 + i * NN + r] = a[j];
+            if (GS) atomicAdd(A + smap[c * N3 + i * NN + r], a[j]);
+            else A[(cell0 + c) * N3 + i * NN + r] = a[j];
           }
       }
     }
@@ -404,11 +420,11 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
   }
 }
 
-template <int N, int M, int CPB, int R, int MINB, int ROLL = 1>
+template <int N, int M, int CPB, int R, int MINB, int ROLL = 1, bool GS = false>
 static int launch_v2(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                     const double* u, cudaStream_t s) {
+                     const double* u, cudaStream_t s, const int* cmap = nullptr) {
   using C = HexAction2Cfg<N, M, CPB, R>;
-  auto kern = hex_laplace_action_v2<N, M, CPB, R, MINB, ROLL>;
+  auto kern = hex_laplace_action_v2<N, M, CPB, R, MINB, ROLL, GS>;
   static int sms = 0, per_sm = 0;
   if (!sms) {
     int dev = 0;
@@ -426,7 +442,7 @@ static int launch_v2(const sfk_plan* p, int64_t ncells, double* A, const double*
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
   const int64_t resident = (int64_t)sms * per_sm;
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
-  kern<<<grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, u, A);
+  kern<<<grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, u, A, cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_v2 launch");
 }
@@ -461,6 +477,17 @@ int launch_hex_action_v2(const sfk_plan* p, int64_t ncells, double* A, const dou
     case 7: return pick<7, 5, 2, 2>(r, roll, p, ncells, A, coords, w0, s);
     case 8: return pick<8, 4, 2, 2>(r, roll, p, ncells, A, coords, w0, s);
     case 9: return pick<9, 3, 2, 2>(r, roll, p, ncells, A, coords, w0, s);
+    default: return SFK_EUNSUPPORTED;
+  }
+}
+
+int launch_hex_action_v2_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                            double* y, const double* coords, cudaStream_t s) {
+  if (p->n != p->m) return SFK_EUNSUPPORTED;
+  switch (p->n) {
+    case 4: return launch_v2<4, 4, 16, 1, 2, 1, true>(p, ncells, y, coords, x, s, cmap);
+    case 6: return launch_v2<6, 6, 8, 1, 2, 1, true>(p, ncells, y, coords, x, s, cmap);
+    case 9: return launch_v2<9, 9, 3, 1, 2, 1, true>(p, ncells, y, coords, x, s, cmap);
     default: return SFK_EUNSUPPORTED;
   }
 }

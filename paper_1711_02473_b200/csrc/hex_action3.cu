@@ -20,6 +20,7 @@
 //    per-point geometry being identical code for every point — then the
 //    transposed z contraction in place);
 //  * shared strides from tools/smem_pads_action.py (bank-conflict search).
+#include <cstdlib>
 #include "async_copy.cuh"
 #include "hex_geometry.cuh"
 
@@ -361,8 +362,21 @@ int launch_hex_action_v3(const sfk_plan* p, int64_t ncells, double* A, const dou
   return dispatch_v3<false>(p, ncells, A, coords, w0, s, nullptr);
 }
 
+// Same generation as the E-vector action per degree (sfk_api.cu c2_auto):
+// p = 1 cell kernel, p = 3, 5, 8 v2, the rest v3 (p = 7's DMMA kernel has
+// no gather/scatter mode; v3 serves it).  SFK_C2G_KERNEL=v3 forces v3.
 int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                          double* y, const double* coords, cudaStream_t s) {
+  static const bool force_v3 = [] {
+    const char* e = std::getenv("SFK_C2G_KERNEL");
+    return e && e[0] == 'v' && e[1] == '3';
+  }();
+  if (!force_v3 && p->n == p->m) {
+    if (p->n == 2 && (reinterpret_cast<uintptr_t>(cmap) & 15) == 0)   // int4 map loads
+      return launch_hex_action_p1_gs(p, ncells, cmap, x, y, coords, s);
+    if (p->n == 4 || p->n == 6 || p->n == 9)
+      return launch_hex_action_v2_gs(p, ncells, cmap, x, y, coords, s);
+  }
   return dispatch_v3<true>(p, ncells, y, coords, x, s, cmap);
 }
 

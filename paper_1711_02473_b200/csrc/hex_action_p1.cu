@@ -23,10 +23,14 @@ constexpr int US = 10;               // padded u stride (8 used)
 constexpr size_t SMEM = (size_t)CPB * (CS + US) * sizeof(double);
 }  // namespace p1
 
+// GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
+// item 1): u = x gathered through cmap[c][0..7], A = y scatter-added with
+// fp64 atomics.
+template <bool GS>
 __global__ void __launch_bounds__(p1::CPB, 3)
 hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
-                      double* __restrict__ A) {
+                      double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
   using namespace p1;
   extern __shared__ __align__(16) double smem[];
   double* sC = smem;
@@ -39,19 +43,22 @@ hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
     // per cell when the bases are; otherwise fall back to 8-byte copies)
     const double* cg = coords + cell0 * 24;
     const double* ug = u + cell0 * 8;
-    const bool al = ((reinterpret_cast<uintptr_t>(cg) | reinterpret_cast<uintptr_t>(ug)) & 15) == 0;
+    const bool al = ((reinterpret_cast<uintptr_t>(cg) |
+                      (GS ? 0 : reinterpret_cast<uintptr_t>(ug))) & 15) == 0;
     if (al) {
       for (int ch = tid; ch < ncb * 12; ch += CPB) {
         const int c = ch / 12, k = ch - c * 12;
         cp_async16(sC + c * CS + 2 * k, cg + 2 * ch);
       }
-      for (int ch = tid; ch < ncb * 4; ch += CPB) {
-        const int c = ch >> 2, k = ch & 3;
-        cp_async16(sU + c * US + 2 * k, ug + 2 * ch);
-      }
+      if (!GS)
+        for (int ch = tid; ch < ncb * 4; ch += CPB) {
+          const int c = ch >> 2, k = ch & 3;
+          cp_async16(sU + c * US + 2 * k, ug + 2 * ch);
+        }
     } else {
       for (int e = tid; e < ncb * 24; e += CPB) cp_async8(sC + (e / 24) * CS + e % 24, cg + e);
-      for (int e = tid; e < ncb * 8; e += CPB) cp_async8(sU + (e >> 3) * US + (e & 7), ug + e);
+      if (!GS)
+        for (int e = tid; e < ncb * 8; e += CPB) cp_async8(sU + (e >> 3) * US + (e & 7), ug + e);
     }
     cp_async_commit();
     cp_async_wait<0>();
@@ -60,17 +67,27 @@ hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
   if (tid >= ncb) return;
 
   double X[24], uu[8];
+  int gm[8];
 #pragma unroll
   for (int k = 0; k < 12; ++k) {
     const double2 v = *reinterpret_cast<const double2*>(sC + tid * CS + 2 * k);
     X[2 * k] = v.x;
     X[2 * k + 1] = v.y;
   }
+  if (GS) {
+    const int4* mp = reinterpret_cast<const int4*>(cmap + (cell0 + tid) * 8);
+    const int4 m0 = __ldg(mp), m1 = __ldg(mp + 1);
+    gm[0] = m0.x; gm[1] = m0.y; gm[2] = m0.z; gm[3] = m0.w;
+    gm[4] = m1.x; gm[5] = m1.y; gm[6] = m1.z; gm[7] = m1.w;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const double2 v = *reinterpret_cast<const double2*>(sU + tid * US + 2 * k);
-    uu[2 * k] = v.x;
-    uu[2 * k + 1] = v.y;
+    for (int k = 0; k < 8; ++k) uu[k] = __ldg(u + gm[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double2 v = *reinterpret_cast<const double2*>(sU + tid * US + 2 * k);
+      uu[2 * k] = v.x;
+      uu[2 * k + 1] = v.y;
+    }
   }
   // dof / point index (x, y, z) -> 4x + 2y + z;  tables T.B[i*2+q], T.D[i*2+q]
   // forward: g_x = Dx By Bz u, g_y = Bx Dy Bz u, g_z = Bx By Dz u at 8 points
@@ -152,6 +169,11 @@ hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
       v = fma(T.B[2 * ix + 1], r2[4 + r], v);
       a[4 * ix + r] = v;
     }
+  if (GS) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) atomicAdd(A + gm[k], a[k]);
+    return;
+  }
   double* ap = A + (cell0 + tid) * 8;
   if ((reinterpret_cast<uintptr_t>(ap) & 15) == 0) {
 #pragma unroll
@@ -162,12 +184,13 @@ hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
   }
 }
 
-int launch_hex_action_p1(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                         const double* w0, cudaStream_t s) {
+template <bool GS>
+static int launch_p1(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                     const double* w0, cudaStream_t s, const int* cmap) {
   if (p->n != 2 || p->m != 2) return SFK_EUNSUPPORTED;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(hex_laplace_action_p1,
+    cudaError_t e = cudaFuncSetAttribute(hex_laplace_action_p1<GS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)p1::SMEM);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_action_p1)");
@@ -175,9 +198,19 @@ int launch_hex_action_p1(const sfk_plan* p, int64_t ncells, double* A, const dou
   }
   const Tabs<2, 2> T = make_tabs<2, 2>(p);
   const unsigned grid = (unsigned)((ncells + p1::CPB - 1) / p1::CPB);
-  hex_laplace_action_p1<<<grid, p1::CPB, p1::SMEM, s>>>(T, ncells, coords, w0, A);
+  hex_laplace_action_p1<GS><<<grid, p1::CPB, p1::SMEM, s>>>(T, ncells, coords, w0, A, cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_p1 launch");
+}
+
+int launch_hex_action_p1(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                         const double* w0, cudaStream_t s) {
+  return launch_p1<false>(p, ncells, A, coords, w0, s, nullptr);
+}
+
+int launch_hex_action_p1_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                            double* y, const double* coords, cudaStream_t s) {
+  return launch_p1<true>(p, ncells, y, coords, x, s, cmap);
 }
 
 }  // namespace sfk
