@@ -363,8 +363,8 @@ int launch_hex_action_v3(const sfk_plan* p, int64_t ncells, double* A, const dou
 }
 
 // Same generation as the E-vector action per degree (sfk_api.cu c2_auto):
-// p = 1 cell kernel, p = 3, 5, 8 v2, the rest v3 (p = 7's DMMA kernel has
-// no gather/scatter mode; v3 serves it).  SFK_C2G_KERNEL=v3 forces v3.
+// p = 1 cell kernel, p = 3, 5, 8 v2, p = 7 DMMA, the rest v3.
+// SFK_C2G_KERNEL=v3 forces v3 (A/B runs).
 int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                          double* y, const double* coords, cudaStream_t s) {
   static const bool force_v3 = [] {
@@ -376,6 +376,7 @@ int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, con
       return launch_hex_action_p1_gs(p, ncells, cmap, x, y, coords, s);
     if (p->n == 4 || p->n == 6 || p->n == 9)
       return launch_hex_action_v2_gs(p, ncells, cmap, x, y, coords, s);
+    if (p->n == 8) return launch_hex_action_tc_gs(p, ncells, cmap, x, y, coords, s);
   }
   return dispatch_v3<true>(p, ncells, y, coords, x, s, cmap);
 }

@@ -60,10 +60,15 @@ __device__ __forceinline__ int xaddr(int q, int iy, int iz) {
 __device__ __forceinline__ int yaddr(int qx, int qy, int z) { return qx * YX + qy * 8 + (z ^ sw(qy)); }
 }  // namespace tc8
 
+// GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
+// item 1): the map cmap[c][0..511] (int32) is double-buffered in the u area,
+// x is gathered through it by the x stage, y scattered with fp64 atomics by
+// the transposed x stage.
+template <bool GS>
 __global__ void __launch_bounds__(tc8::THREADS, 2)
 hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
                        const double* __restrict__ coords, const double* __restrict__ u,
-                       double* __restrict__ A) {
+                       double* __restrict__ A, const int* __restrict__ cmap) {
   using namespace tc8;
   extern __shared__ __align__(16) double smem[];
   double* sX = smem;
@@ -73,6 +78,8 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kq = lane & 3, gq = lane >> 2;   // fragment coordinates
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  int* sMap = reinterpret_cast<int*>(sU);   // GS: [2][CPB*512] int32
+  static_assert(2 * CPB * N3 <= 2 * CPB * UC, "map double buffer does not fit");
 
   // table fragments
   //  D-form fwd  A[m=q][k=i]  : T[4ks+kq][gq]      (bf, df)
@@ -97,7 +104,10 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
     const int64_t c0 = bt * CPB;
     const int nc = (int)((ncells - c0) < CPB ? (ncells - c0) : CPB);
     const double* src = u + c0 * N3;
-    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    if (GS) {
+      for (int e = tid; e < nc * N3; e += THREADS)
+        cp_async4(sMap + buf * CPB * N3 + e, cmap + c0 * N3 + e);
+    } else if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
       for (int ch = tid; ch < nc * (N3 / 2); ch += THREADS) {
         const int c = ch >> 8, r = ch & 255;
         cp_async16(sU + c * UC + (r >> 5) * UPL + 2 * (r & 31), src + 2 * ch);
@@ -121,6 +131,7 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
     cp_async_wait<0>();
     __syncthreads();
     const double* sC = sCo + cur * CSZ;
+    const int* smap = sMap + cur * CPB * N3;
 
     // Each warp owns tiles t = warp + WARPS*j (the same in-cell tile index for
     // TPW cells): all fragment loads first, then the DMMAs (TPW independent
@@ -132,9 +143,15 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
-        const double* in = sU + c * UC + iy * 8 + gq;
-        f[j][0] = in[kq * UPL];
-        f[j][1] = in[(4 + kq) * UPL];
+        if (GS) {
+          const int* mp = smap + c * N3 + iy * 8 + gq;   // (ix, iy, iz = gq)
+          f[j][0] = c < ncb ? __ldg(u + mp[kq * NN]) : 0.0;
+          f[j][1] = c < ncb ? __ldg(u + mp[(4 + kq) * NN]) : 0.0;
+        } else {
+          const double* in = sU + c * UC + iy * 8 + gq;
+          f[j][0] = in[kq * UPL];
+          f[j][1] = in[(4 + kq) * UPL];
+        }
       }
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks)
@@ -355,7 +372,11 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
-        if (c < ncb) {
+        if (GS && c < ncb) {
+          const int* mp = smap + c * N3 + gq * NN + iy * 8 + 2 * kq;
+          atomicAdd(A + mp[0], o[j][0]);
+          atomicAdd(A + mp[1], o[j][1]);
+        } else if (c < ncb) {
           // D: ix = gq, iz = 2kq + h -> A[cell][ix*64 + iy*8 + iz]
           double* ap = A + (cell0 + c) * N3 + gq * NN + iy * 8 + 2 * kq;
           if ((reinterpret_cast<uintptr_t>(ap) & 15) == 0) {
@@ -371,22 +392,22 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
   }
 }
 
-int launch_hex_action_tc(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                         const double* w0, cudaStream_t s) {
+template <bool GS>
+static int launch_tc8(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                      const double* w0, cudaStream_t s, const int* cmap) {
   if (p->n != 8 || p->m != 8) return SFK_EUNSUPPORTED;
   using namespace tc8;
+  auto kern = hex_laplace_action_tc8<GS>;
   static int sms = 0, per_sm = 0;
   if (!sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(hex_laplace_action_tc8,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SMEM);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_action_tc8)");
-    cudaFuncSetAttribute(hex_laplace_action_tc8, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         100);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hex_laplace_action_tc8, THREADS,
-                                                      SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, SMEM);
     if (e != cudaSuccess) return cuda_status(e, "occupancy(hex_action_tc8)");
     if (per_sm < 1) return fail(SFK_ECUDA, "hex_action_tc8 does not fit on an SM");
   }
@@ -394,9 +415,19 @@ int launch_hex_action_tc(const sfk_plan* p, int64_t ncells, double* A, const dou
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
   const int64_t resident = (int64_t)sms * per_sm;
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
-  hex_laplace_action_tc8<<<grid, THREADS, SMEM, s>>>(T, ncells, coords, w0, A);
+  kern<<<grid, THREADS, SMEM, s>>>(T, ncells, coords, w0, A, cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_tc8 launch");
+}
+
+int launch_hex_action_tc(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                         const double* w0, cudaStream_t s) {
+  return launch_tc8<false>(p, ncells, A, coords, w0, s, nullptr);
+}
+
+int launch_hex_action_tc_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                            double* y, const double* coords, cudaStream_t s) {
+  return launch_tc8<true>(p, ncells, y, coords, x, s, cmap);
 }
 
 }  // namespace sfk
