@@ -9,6 +9,9 @@ echo "smoke rc=$?" >> gpurun_out/${TAG}_smoke.log
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 echo "bench rc=$?" >> gpurun_out/${TAG}_bench.err
 timeout 1500 python tools/bench_configs.py C1 C3 C4 C5 C2G > gpurun_out/${TAG}_configs.jsonl 2> gpurun_out/${TAG}_configs.err
+timeout 600 python tools/bench_programs.py > gpurun_out/${TAG}_lp.jsonl 2> gpurun_out/${TAG}_lp.err
+timeout 900 python tools/bench_csr.py > gpurun_out/${TAG}_csr.jsonl 2> gpurun_out/${TAG}_csr.err
+bash tools/dist_check.sh
 PCMD="python bench.py --steps 1 --warmup 1 --degrees 1-8 --no-e2e --no-cpu"
 timeout 600 $PCMD > gpurun_out/${TAG}_plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
