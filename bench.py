@@ -141,6 +141,30 @@ def dist_env():
     return world, rank, local
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _time_ref(ev, plans, inputs, reps):
+    """Best-of-reps seconds per degree of evaluator ev over inputs."""
+    best = []
+    for pl, inp in zip(plans, inputs):
+        ev(pl, {"coords": inp["coords"][:64], "w0": inp["w0"][:64]})
+        t = 1e30
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            ev(pl, inp)
+            t = min(t, time.perf_counter() - t0)
+        best.append(t)
+    return best
+
+
 def reference_arm(args):
     """The reference's own CPU path: its emitted C (oracle/_ref) with an
     OpenMP cell loop over all host cores; the oracle port if _ref is absent."""
@@ -159,17 +183,34 @@ def reference_arm(args):
     ev = refc.evaluate if kind == "reference" else cpu.evaluate
     inputs = [{"coords": coords, "w0": workloads.uniform_dofs(sample, (p + 1) ** 3)}
               for p in degs]
+    # both builds of the reference C: the parity build and
+    # the paper's -ffast-math build; the faster one is the reference value
+    builds = ["parity"]
+    if kind == "reference" and all(refc.available(pl, "fast") for pl in plans):
+        builds.append("fast")
+
+    def ev_for(build):
+        if kind != "reference":
+            return ev
+        return lambda pl, inp: refc.evaluate(pl, inp, build=build)
     for _ in range(args.warmup):
-        for pl, inp in zip(plans, inputs):
-            ev(pl, {"coords": inp["coords"][:256], "w0": inp["w0"][:256]})
-    per = {p: [] for p in degs}
-    for _ in range(args.steps):
-        for p, pl, inp in zip(degs, plans, inputs):
-            t0 = time.perf_counter()
-            ev(pl, inp)
-            per[p].append(time.perf_counter() - t0)
-    total_t = sum(min(v) for v in per.values())
+        for b in builds:
+            for pl, inp in zip(plans, inputs):
+                ev_for(b)(pl, {"coords": inp["coords"][:256], "w0": inp["w0"][:256]})
+    per_build = {}
+    for b in builds:
+        per = {p: [] for p in degs}
+        for _ in range(args.steps):
+            for p, pl, inp in zip(degs, plans, inputs):
+                t0 = time.perf_counter()
+                ev_for(b)(pl, inp)
+                per[p].append(time.perf_counter() - t0)
+        per_build[b] = per
     dofs = sum(sample * (p + 1) ** 3 for p in degs)
+    totals = {b: sum(min(v) for v in per.values()) for b, per in per_build.items()}
+    best_build = min(totals, key=totals.get)
+    per = per_build[best_build]
+    total_t = totals[best_build]
     value = dofs / total_t / 1e9
     cores = (refc.threads(plans[0]) if kind == "reference" else cpu.num_threads())
     line = {
@@ -183,7 +224,8 @@ def reference_arm(args):
                         "gdofs": round(sample * (p + 1) ** 3 / min(per[p]) / 1e9, 6)}
                        for p in degs],
         "cpu_baseline": {"value": round(value, 6), "unit": "GDoF/s", "cores": cores,
-                         "kind": kind,
+                         "kind": kind, "build": best_build, "cpu_model": cpu_model(),
+                         "by_build": {b: round(dofs / t / 1e9, 6) for b, t in totals.items()},
                          "sample": "%d of %d cells per degree, p=%s, best of %d"
                                    % (sample, nx * ny * nz, args.degrees, args.steps)},
         "e2e": {"value": round(value, 6), "unit": "GDoF/s", "h2d_bytes_per_step": 0,
@@ -194,29 +236,47 @@ def reference_arm(args):
 
 
 def cpu_baseline_leg(degs, coords_all, host_inputs, sample_cells):
+    """The reference's emitted C on this host: parity build
+    and -ffast-math build over all cores on the first `sample_cells` cells per
+    degree, plus the parity build on 1 thread (smaller sample)."""
     from oracle import cpu, refc
     from paper_1711_02473_b200 import compile_kernel
 
     plans = [compile_kernel("action_laplace", "hex", p) for p in degs]
     kind = "reference" if all(refc.available(pl) for pl in plans) else "port"
-    ev = refc.evaluate if kind == "reference" else cpu.evaluate
     n = min(sample_cells, coords_all.shape[0])
-    tot_t, tot_d = 0.0, 0
-    for p, pl in zip(degs, plans):
-        inp = {"coords": coords_all[:n], "w0": host_inputs[p][:n]}
-        ev(pl, {"coords": inp["coords"][:64], "w0": inp["w0"][:64]})
-        best = 1e30
-        for _ in range(2):
-            t0 = time.perf_counter()
-            ev(pl, inp)
-            best = min(best, time.perf_counter() - t0)
-        tot_t += best
-        tot_d += n * (p + 1) ** 3
-    cores = refc.threads(plans[0]) if kind == "reference" else cpu.num_threads()
-    return {"value": round(tot_d / tot_t / 1e9, 6), "unit": "GDoF/s", "cores": cores,
-            "kind": kind,
-            "sample": "first %d cells of the C2 batch per degree p=%d..%d, best of 2"
-                      % (n, degs[0], degs[-1])}
+    inputs = [{"coords": coords_all[:n], "w0": host_inputs[p][:n]} for p in degs]
+    dofs = sum(n * (p + 1) ** 3 for p in degs)
+    out = {"unit": "GDoF/s", "kind": kind, "cpu_model": cpu_model()}
+    if kind != "reference":
+        t = sum(_time_ref(cpu.evaluate, plans, inputs, 2))
+        out.update(value=round(dofs / t / 1e9, 6), cores=cpu.num_threads(),
+                   sample="first %d cells of the C2 batch per degree p=%d..%d, best of 2"
+                          % (n, degs[0], degs[-1]))
+        return out
+    by = {}
+    for b in ("parity", "fast"):
+        if all(refc.available(pl, b) for pl in plans):
+            t = sum(_time_ref(lambda pl, inp, b=b: refc.evaluate(pl, inp, build=b),
+                              plans, inputs, 2))
+            by[b] = round(dofs / t / 1e9, 6)
+    best = max(by, key=by.get)
+    out.update(value=by[best], build=best, by_build=by, cores=refc.threads(plans[0]),
+               sample="first %d cells of the C2 batch per degree p=%d..%d, best of 2"
+                      % (n, degs[0], degs[-1]))
+    # 1-thread run of the parity build on a smaller sample
+    n1 = min(n, 2048)
+    in1 = [{"coords": i["coords"][:n1], "w0": i["w0"][:n1]} for i in inputs]
+    for pl in plans:
+        refc.set_threads(pl, 1)
+    try:
+        t1 = sum(_time_ref(refc.evaluate, plans, in1, 1))
+    finally:
+        for pl in plans:
+            refc.set_threads(pl, 0)
+    out["single_thread"] = {"value": round(sum(n1 * (p + 1) ** 3 for p in degs) / t1 / 1e9, 6),
+                            "build": "parity", "sample": "first %d cells per degree" % n1}
+    return out
 
 
 def main():

@@ -32,30 +32,43 @@ def key_for(plan):
     return None
 
 
-def available(plan):
+def available(plan, build="parity"):
     k = key_for(plan)
-    return k is not None and os.path.exists(os.path.join(OUT, "libref_%s.so" % k))
+    sfx = "_fast" if build == "fast" else ""
+    return k is not None and os.path.exists(os.path.join(OUT, "libref_%s%s.so" % (k, sfx)))
 
 
-def _lib(key):
-    if key not in _libs:
-        path = os.path.join(OUT, "libref_%s.so" % key)
+def _lib(key, build="parity"):
+    """build: "parity" (-O3 -march=native -ffp-contract=off) or "fast"
+    (-ffast-math, the paper's flags)."""
+    if (key, build) not in _libs:
+        path = os.path.join(OUT, "libref_%s%s.so" % (key, "_fast" if build == "fast" else ""))
         L = ctypes.CDLL(path)
         L.sumfact_ref_run.argtypes = [ctypes.c_int64] + [ctypes.c_void_p] * 4
         L.sumfact_ref_threads.restype = ctypes.c_int
+        if hasattr(L, "sumfact_ref_set_threads"):
+            L.sumfact_ref_set_threads.argtypes = [ctypes.c_int]
         meta = json.load(open(os.path.join(OUT, "src", key + ".json")))
-        _libs[key] = (L, meta)
-    return _libs[key]
+        _libs[(key, build)] = (L, meta)
+    return _libs[(key, build)]
 
 
-def threads(plan):
-    return _lib(key_for(plan))[0].sumfact_ref_threads()
+def threads(plan, build="parity"):
+    return _lib(key_for(plan), build)[0].sumfact_ref_threads()
 
 
-def evaluate(plan, inputs, out=None):
+def set_threads(plan, n, build="parity"):
+    """OpenMP threads of the cell loop (0 = all host cores)."""
+    L = _lib(key_for(plan), build)[0]
+    if not hasattr(L, "sumfact_ref_set_threads"):
+        raise RuntimeError("oracle/_ref predates the thread control; rerun build()")
+    L.sumfact_ref_set_threads(int(n))
+
+
+def evaluate(plan, inputs, out=None, build="parity"):
     """Run the reference's emitted kernel over every cell (OpenMP)."""
     key = key_for(plan)
-    L, meta = _lib(key)
+    L, meta = _lib(key, build)
     assert [tuple(a) for a in meta["arguments"]] == [tuple(a) for a in plan.arguments], \
         (meta["arguments"], plan.arguments)
     arrs = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in inputs.items()}
