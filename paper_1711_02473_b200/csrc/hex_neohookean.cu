@@ -318,17 +318,39 @@ static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double
   return cuda_status(cudaGetLastError(), "hex_neohookean_kernel launch");
 }
 
+// cells per CTA for m = n + 1 (C4) per degree p (overridable for A/B builds;
+// profiles/r01au_c4_cpb.jsonl: p = 2 16 -> 8 cells 0.199 -> 0.164 ms, p = 3
+// 8 -> 4, p = 6 2 -> 1; smaller CTAs interleave the barrier-heavy phases)
+#ifndef SFK_NEO_CPB_P1
+#define SFK_NEO_CPB_P1 16
+#endif
+#ifndef SFK_NEO_CPB_P2
+#define SFK_NEO_CPB_P2 8
+#endif
+#ifndef SFK_NEO_CPB_P3
+#define SFK_NEO_CPB_P3 4
+#endif
+#ifndef SFK_NEO_CPB_P4
+#define SFK_NEO_CPB_P4 3
+#endif
+#ifndef SFK_NEO_CPB_P5
+#define SFK_NEO_CPB_P5 3
+#endif
+#ifndef SFK_NEO_CPB_P6
+#define SFK_NEO_CPB_P6 1
+#endif
+
 int launch_hex_neohookean(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                           const double* w0, cudaStream_t s) {
   const int n = p->n, m = p->m;
   if (m == n + 1) {
     switch (n) {
-      case 2: return launch_neo<2, 3, 16>(p, ncells, A, coords, w0, s);
-      case 3: return launch_neo<3, 4, 16>(p, ncells, A, coords, w0, s);
-      case 4: return launch_neo<4, 5, 8>(p, ncells, A, coords, w0, s);
-      case 5: return launch_neo<5, 6, 3>(p, ncells, A, coords, w0, s);
-      case 6: return launch_neo<6, 7, 3>(p, ncells, A, coords, w0, s);
-      case 7: return launch_neo<7, 8, 2>(p, ncells, A, coords, w0, s);
+      case 2: return launch_neo<2, 3, SFK_NEO_CPB_P1>(p, ncells, A, coords, w0, s);
+      case 3: return launch_neo<3, 4, SFK_NEO_CPB_P2>(p, ncells, A, coords, w0, s);
+      case 4: return launch_neo<4, 5, SFK_NEO_CPB_P3>(p, ncells, A, coords, w0, s);
+      case 5: return launch_neo<5, 6, SFK_NEO_CPB_P4>(p, ncells, A, coords, w0, s);
+      case 6: return launch_neo<6, 7, SFK_NEO_CPB_P5>(p, ncells, A, coords, w0, s);
+      case 7: return launch_neo<7, 8, SFK_NEO_CPB_P6>(p, ncells, A, coords, w0, s);
       default: break;
     }
   } else if (m == n) {
