@@ -190,6 +190,12 @@ struct Phase {
   const Stmt* leaf = nullptr;
   std::vector<std::pair<int, int>> par, red;   // (index id, extent), nest order
   long long npar = 1;
+  // output blocking: the parallel index `blk` (extent blk_ext) is handled
+  // inside one thread, so loads that do not depend on it are shared by the
+  // blk_ext outputs (accumulators in registers); opar = par without blk
+  int blk = -1, blk_ext = 1;
+  std::vector<std::pair<int, int>> opar;
+  long long nitem = 1;                          // items per cell = npar / blk_ext
   bool zero_init = false;                      // folded ZeroFill (ACCUM starts at 0)
   std::string zname;
   long long zsize = 0;
@@ -295,6 +301,37 @@ Phase classify(const Stmt& s) {
   }
   ph.k = Phase::NEST;
   for (const auto& pr : ph.par) ph.npar *= pr.second;
+  // output blocking: pick the parallel index most loads do not depend on
+  {
+    std::vector<const Expr*> lds;
+    std::function<void(const Expr&)> col = [&](const Expr& e) {
+      if (e.k == Expr::LOAD || e.k == Expr::TABLE) lds.push_back(&e);
+      if (e.a) col(*e.a);
+      if (e.b) col(*e.b);
+    };
+    col(*cur->e);
+    // (a variant restricted to reductions reusing a temporary lost most of the
+    // gain: profiles/r01av_lp_block.jsonl)
+    int best = 0;
+    for (const auto& pr : ph.par) {
+      if (pr.second < 2 || pr.second > 16) continue;
+      int score = 0;
+      for (const Expr* ld : lds) {
+        bool dep = false;
+        for (const auto& t : ld->terms) dep = dep || (t.e.idx == pr.first && t.stride != 0);
+        score += dep ? 0 : 1;
+      }
+      if (score > best || (score == best && score > 0 && pr.second > ph.blk_ext)) {
+        best = score;
+        ph.blk = pr.first;
+        ph.blk_ext = pr.second;
+      }
+    }
+    if (best == 0) ph.blk = -1, ph.blk_ext = 1;
+    for (const auto& pr : ph.par)
+      if (pr.first != ph.blk) ph.opar.push_back(pr);
+    ph.nitem = ph.npar / ph.blk_ext;
+  }
   return ph;
 }
 
@@ -378,25 +415,29 @@ bool phase_accesses(const Phase& ph, const std::map<std::string, long long>& bas
   if ((long long)NC * ph.npar * (1 + nred * (long long)loads.size()) > kBudget) return false;
   std::vector<long long> val(max_idx + 1, 0);
   const long long tb = base.at(L.name);
-  for (long long w = 0; w < NC * ph.npar; ++w) {
+  for (long long w = 0; w < NC * ph.nitem; ++w) {
     const int c = (int)(w % NC);
     long long q = w / NC;
-    for (size_t j = ph.par.size(); j-- > 0;) {
-      if (j == 0) { val[ph.par[j].first] = q; break; }
-      val[ph.par[j].first] = q % ph.par[j].second;
-      q /= ph.par[j].second;
+    for (size_t j = ph.opar.size(); j-- > 0;) {
+      if (j == 0) { val[ph.opar[j].first] = q; break; }
+      val[ph.opar[j].first] = q % ph.opar[j].second;
+      q /= ph.opar[j].second;
     }
     const int t = (int)(w % T);
-    out.push_back({elem(tb + eval_addr(L.offset, L.terms, val), c), t, true});
-    if (loads.empty()) continue;
-    std::vector<int> it(ph.red.size(), 0);
-    for (long long r = 0; r < nred; ++r) {
-      for (size_t j = 0; j < ph.red.size(); ++j) val[ph.red[j].first] = it[j];
-      for (const Expr* ld : loads)
-        out.push_back({elem(base.at(ld->name) + eval_addr(ld->offset, ld->terms, val), c), t, false});
-      for (size_t j = ph.red.size(); j-- > 0;) {
-        if (++it[j] < ph.red[j].second) break;
-        it[j] = 0;
+    for (int bv = 0; bv < ph.blk_ext; ++bv) {
+      if (ph.blk >= 0) val[ph.blk] = bv;
+      out.push_back({elem(tb + eval_addr(L.offset, L.terms, val), c), t, true});
+      if (loads.empty()) continue;
+      std::vector<int> it(ph.red.size(), 0);
+      for (long long r = 0; r < nred; ++r) {
+        for (size_t j = 0; j < ph.red.size(); ++j) val[ph.red[j].first] = it[j];
+        for (const Expr* ld : loads)
+          out.push_back({elem(base.at(ld->name) + eval_addr(ld->offset, ld->terms, val), c), t,
+                         false});
+        for (size_t j = ph.red.size(); j-- > 0;) {
+          if (++it[j] < ph.red[j].second) break;
+          it[j] = 0;
+        }
       }
     }
   }
@@ -583,7 +624,7 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
     if (ph.k != Phase::NEST) continue;
     long long nred = 1;
     for (const auto& r : ph.red) nred *= r.second;
-    const long long it = ph.npar * C.cells_per_block;
+    const long long it = ph.nitem * C.cells_per_block;
     maxitems = std::max(maxitems, it);
     items.emplace_back(it, (double)it * nred);
     work_total += (double)it * nred;
@@ -791,34 +832,56 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
       o << "    }\n";
     } else {
       const Stmt& L = *ph.leaf;
+      const int E = ph.blk_ext;
+      const std::string bv = ph.blk >= 0 ? "i" + std::to_string(ph.blk) : std::string();
       o << "    // phase " << k << ": " << (L.k == Stmt::ACCUM ? "accumulate " : "assign ") << L.name
-        << " (" << ph.npar << " parallel x " << ph.red.size() << " reduction loops)\n"
-        << "    for (int w = threadIdx.x; w < " << NC * ph.npar << "; w += " << T << ") {\n";
+        << " (" << ph.npar << " parallel";
+      if (E > 1) o << ", " << E << " per thread along " << bv;
+      o << " x " << ph.red.size() << " reduction loops)\n"
+        << "    for (int w = threadIdx.x; w < " << NC * ph.nitem << "; w += " << T << ") {\n";
       if (NC > 1) o << "      const int c = w % " << NC << ";\n      int q = w / " << NC << ";\n";
       else o << "      int q = w;\n";
-      for (size_t j = ph.par.size(); j-- > 0;) {
-        const auto& pr = ph.par[j];
+      for (size_t j = ph.opar.size(); j-- > 0;) {
+        const auto& pr = ph.opar[j];
         if (j == 0) o << "      const int i" << pr.first << " = q;\n";
         else o << "      const int i" << pr.first << " = q % " << pr.second << "; q /= " << pr.second << ";\n";
       }
-      if (ph.par.empty()) o << "      (void)q;\n";
+      if (ph.opar.empty()) o << "      (void)q;\n";
       const std::string tgt = slot(L.name, addr(L.offset, L.terms));
+      const std::string av = E > 1 ? "acc[" + bv + "]" : std::string("acc");
+      // the E outputs of the block accumulate in registers and are stored at
+      // the end, so loads independent of the block index are loaded once
+      auto bopen = [&](const std::string& pad) {
+        if (E > 1)
+          o << pad << "#pragma unroll\n" << pad << "for (int " << bv << " = 0; " << bv << " < " << E
+            << "; ++" << bv << ") ";
+      };
+      o << "      double acc" << (E > 1 ? "[" + std::to_string(E) + "]" : std::string()) << ";\n";
+      if (L.k == Stmt::ACCUM) {
+        bopen("      ");
+        o << (E > 1 ? "" : "      ") << av << " = " << (ph.zero_init ? "0.0" : tgt) << ";\n";
+      }
       std::string pad = "      ";
-      if (L.k == Stmt::ACCUM) o << pad << "double acc = " << (ph.zero_init ? "0.0" : tgt) << ";\n";
       for (size_t j = 0; j < ph.red.size(); ++j) {
         const auto& r = ph.red[j];
-        if (j + 1 == ph.red.size() && r.second <= 32) o << pad << "#pragma unroll\n";
+        if (j + 1 == ph.red.size() && r.second <= 32 && r.second * E <= 64)
+          o << pad << "#pragma unroll\n";
         o << pad << "for (int i" << r.first << " = 0; i" << r.first << " < " << r.second << "; ++i"
           << r.first << ") {\n";
         pad += "  ";
       }
-      if (L.k == Stmt::ACCUM) o << pad << "acc = acc + " << ex(*L.e) << ";\n";
-      else o << pad << tgt << " = " << ex(*L.e) << ";\n";
+      if (E > 1) {
+        o << pad << "#pragma unroll\n"
+          << pad << "for (int " << bv << " = 0; " << bv << " < " << E << "; ++" << bv << ")\n  ";
+      }
+      o << pad << av << " = " << (L.k == Stmt::ACCUM ? av + " + " : std::string()) << ex(*L.e)
+        << ";\n";
       for (size_t r = 0; r < ph.red.size(); ++r) {
         pad.resize(pad.size() - 2);
         o << pad << "}\n";
       }
-      if (L.k == Stmt::ACCUM) o << "      " << tgt << " = acc;\n";
+      bopen("      ");
+      o << (E > 1 ? "" : "      ") << tgt << " = " << av << ";\n";
       o << "    }\n";
     }
   }
