@@ -144,6 +144,19 @@ int sfk_eval_gather_scatter(const sfk_plan *plan, int64_t ncells,
                             double *y, const double *coords, void *stream);
 
 /*
+ * The same for every action kernel with a fused gather/scatter mode:
+ *     y += sum_c P_c^T K_c(P_c x)
+ * hex action_laplace (GL or collocated GLL), action_weighted_laplace (w1 =
+ * kappa per cell, [ncells][n^3], NOT gathered) and the neo-Hookean residual
+ * (cell_dofs[c][3*node + comp], the reference's vector dof order; y is the
+ * assembled nonlinear residual r(x)).  Same conventions as
+ * sfk_eval_gather_scatter, which is this call with w1 = NULL.
+ */
+int sfk_eval_global(const sfk_plan *plan, int64_t ncells,
+                    const int32_t *cell_dofs, const double *x, double *y,
+                    const double *coords, const double *w1, void *stream);
+
+/*
  * Assembled sparse matrices (local-matrix assembly +
  * sparse insertion; the paper's "global assembly" step, PAPER.md:166-167,
  * scoped out by the reference).

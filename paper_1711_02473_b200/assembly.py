@@ -29,7 +29,8 @@ import numpy as np
 
 from .errors import NativeError, ShapeMismatch
 
-__all__ = ["lattice_dof_map", "lattice_boundary_mask", "GlobalOperator", "cg",
+__all__ = ["lattice_dof_map", "lattice_vector_dof_map", "lattice_boundary_mask",
+           "GlobalOperator", "cg",
            "CsrPattern", "assemble_csr"]
 
 
@@ -51,6 +52,17 @@ def lattice_dof_map(nx, ny, nz, degree, ix_range=None):
     return np.ascontiguousarray(g, dtype=np.int32)
 
 
+def lattice_vector_dof_map(nx, ny, nz, degree, ix_range=None):
+    """(C, 3 (p+1)^3) int32 global dofs of a vector Q_p field in the
+    reference's vector layout (local dof = 3*node + comp, global dof =
+    3*node + comp of the node lattice)."""
+    g = lattice_dof_map(nx, ny, nz, degree, ix_range).astype(np.int64)
+    v = 3 * g[:, :, None] + np.arange(3)[None, None, :]
+    if v.max() >= 2 ** 31:
+        raise ValueError("global dof count exceeds int32")
+    return np.ascontiguousarray(v.reshape(g.shape[0], -1), dtype=np.int32)
+
+
 def lattice_ndofs(nx, ny, nz, degree):
     p = degree
     return (nx * p + 1) * (ny * p + 1) * (nz * p + 1)
@@ -66,15 +78,22 @@ def lattice_boundary_mask(nx, ny, nz, degree):
 
 
 class GlobalOperator:
-    """y = K x with K = sum_c P_c^T A_c P_c, applied matrix-free on the GPU.
+    """y = sum_c P_c^T K_c(P_c x), applied matrix-free on the GPU in ONE
+    fused gather -> cell kernel -> scatter launch (``sfk_eval_global``).
 
-    plan       a hex ``action_laplace`` KernelPlan (GL, m == n)
-    cell_dofs  (C, nd) int32 CUDA tensor (``lattice_dof_map``)
+    plan       a hex KernelPlan: ``action_laplace`` (GL or collocated GLL),
+               ``action_weighted_laplace`` (collocated GLL; pass ``w1``) or
+               ``neohookean_residual`` (then y is the assembled nonlinear
+               residual r(x) and cell_dofs the vector map)
+    cell_dofs  (C, nd) int32 CUDA tensor (``lattice_dof_map`` /
+               ``lattice_vector_dof_map``)
     coords     (C, 24) float64 CUDA tensor
     ndofs      length of the global vectors
+    w1         (C, n^3) float64 CUDA tensor of per-cell coefficient values
+               (kappa) for the weighted Laplacian, not gathered
     """
 
-    def __init__(self, plan, cell_dofs, coords, ndofs):
+    def __init__(self, plan, cell_dofs, coords, ndofs, w1=None):
         import torch
 
         if cell_dofs.dtype != torch.int32 or not cell_dofs.is_cuda:
@@ -84,10 +103,21 @@ class GlobalOperator:
         nd = plan.argument_size("w0")
         if tuple(cell_dofs.shape) != (coords.shape[0], nd):
             raise ShapeMismatch("cell_dofs must be (%d, %d)" % (coords.shape[0], nd))
+        if "w1" in dict(plan.arguments):
+            if w1 is None:
+                raise ShapeMismatch("plan %s needs w1 (per-cell coefficient)" % plan.name)
+            if (w1.dtype != torch.float64 or not w1.is_cuda
+                    or tuple(w1.shape) != (coords.shape[0], plan.argument_size("w1"))):
+                raise ShapeMismatch("w1 must be a float64 CUDA (%d, %d) tensor"
+                                    % (coords.shape[0], plan.argument_size("w1")))
+            w1 = w1.contiguous()
+        elif w1 is not None:
+            raise ShapeMismatch("plan %s takes no w1" % plan.name)
         self.plan = plan
         self.cell_dofs = cell_dofs.contiguous()
         self.coords = coords.contiguous()
         self.ndofs = int(ndofs)
+        self.w1 = w1
 
     def apply(self, x, out=None, accumulate=False, stream=None):
         import torch
@@ -104,9 +134,10 @@ class GlobalOperator:
         if stream is None:
             stream = torch.cuda.current_stream(x.device).cuda_stream
         with torch.cuda.device(x.device):
-            _check(load_library().sfk_eval_gather_scatter(
+            _check(load_library().sfk_eval_global(
                 native_plan(self.plan), self.coords.shape[0], self.cell_dofs.data_ptr(),
-                x.data_ptr(), out.data_ptr(), self.coords.data_ptr(), stream))
+                x.data_ptr(), out.data_ptr(), self.coords.data_ptr(),
+                self.w1.data_ptr() if self.w1 is not None else None, stream))
         return out
 
     __call__ = apply

@@ -63,12 +63,16 @@ __host__ __device__ constexpr int colloc_minb(int n) {
   return (n <= 7 || (n >= 9 && n <= 13) || n == 16) ? 2 : (n == 8 || n == 15) ? 0 : 1;
 }
 
-template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED>
+// GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
+// item 1): u = x gathered through cmap[c][i] by per-element cp.async into the
+// padded u layout, A = y scatter-added with fp64 atomics at the write-back.
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS = false>
 __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
                                             const double* __restrict__ coords,
                                             const double* __restrict__ u,
                                             const double* __restrict__ kappa,
-                                            double* __restrict__ A) {
+                                            double* __restrict__ A,
+                                            const int* __restrict__ cmap) {
   using C = CollocCfg<N, CPB, SY, SX, CS>;
   constexpr int NN = C::NN, N3 = C::N3;
   extern __shared__ double smem[];
@@ -94,7 +98,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
     for (int i = tid; i < ncb * N3; i += C::THREADS) {
       const int c = i / N3, r = i - c * N3;
       const int x = r / NN, yz = r - x * NN, y = yz / N, z = yz - y * N;
-      cp_async8(sU + c * CS + x * SX + y * SY + z, ug + i);
+      cp_async8(sU + c * CS + x * SX + y * SY + z, GS ? u + __ldg(cmap + cell0 * N3 + i) : ug + i);
     }
     cp_async_commit();
     if (WEIGHTED) {
@@ -219,37 +223,41 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
     for (int i = tid; i < ncb * N3; i += C::THREADS) {
       const int cc = i / N3, rr = i - cc * N3;
       const int x = rr / NN, yz = rr - x * NN, y = yz / N, z = yz - y * N;
-      ag[i] = sU[cc * CS + x * SX + y * SY + z];
+      if (GS) atomicAdd(A + __ldg(cmap + cell0 * N3 + i), sU[cc * CS + x * SX + y * SY + z]);
+      else ag[i] = sU[cc * CS + x * SX + y * SY + z];
     }
   }
 }
 
-template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, int MINB>
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, int MINB, bool GS>
 __global__ void __launch_bounds__(CollocCfg<N, CPB, SY, SX, CS>::THREADS, MINB)
 hex_colloc_action_kernel(const __grid_constant__ TabsD<N> T, int64_t ncells,
                          const double* __restrict__ coords, const double* __restrict__ u,
-                         const double* __restrict__ kappa, double* __restrict__ A) {
-  colloc_body<N, CPB, SY, SX, CS, WEIGHTED>(T, ncells, coords, u, kappa, A);
+                         const double* __restrict__ kappa, double* __restrict__ A,
+                         const int* __restrict__ cmap) {
+  colloc_body<N, CPB, SY, SX, CS, WEIGHTED, GS>(T, ncells, coords, u, kappa, A, cmap);
 }
 
-template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED>
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS>
 __global__ void __launch_bounds__(CollocCfg<N, CPB, SY, SX, CS>::THREADS)
 hex_colloc_action_kernel_free(const __grid_constant__ TabsD<N> T, int64_t ncells,
                               const double* __restrict__ coords, const double* __restrict__ u,
-                              const double* __restrict__ kappa, double* __restrict__ A) {
-  colloc_body<N, CPB, SY, SX, CS, WEIGHTED>(T, ncells, coords, u, kappa, A);
+                              const double* __restrict__ kappa, double* __restrict__ A,
+                              const int* __restrict__ cmap) {
+  colloc_body<N, CPB, SY, SX, CS, WEIGHTED, GS>(T, ncells, coords, u, kappa, A, cmap);
 }
 
-template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED>
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS>
 static auto colloc_kernel() {
   constexpr int mb = colloc_minb(N);
-  if constexpr (mb == 0) return hex_colloc_action_kernel_free<N, CPB, SY, SX, CS, WEIGHTED>;
-  else return hex_colloc_action_kernel<N, CPB, SY, SX, CS, WEIGHTED, mb>;
+  if constexpr (mb == 0) return hex_colloc_action_kernel_free<N, CPB, SY, SX, CS, WEIGHTED, GS>;
+  else return hex_colloc_action_kernel<N, CPB, SY, SX, CS, WEIGHTED, mb, GS>;
 }
 
-template <int N, int CPB, int SY, int SX, int CS>
+template <int N, int CPB, int SY, int SX, int CS, bool GS = false>
 static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                    const double* u, const double* kappa, cudaStream_t s) {
+                    const double* u, const double* kappa, cudaStream_t s,
+                    const int* cmap = nullptr) {
   using C = CollocCfg<N, CPB, SY, SX, CS>;
   TabsD<N> T;
   for (int i = 0; i < N * N; ++i) T.D[i] = p->D[i];
@@ -261,15 +269,15 @@ static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* 
   const int64_t grid = (ncells + CPB - 1) / CPB;
   cudaError_t e;
   if (kappa) {
-    auto k = colloc_kernel<N, CPB, SY, SX, CS, true>();
+    auto k = colloc_kernel<N, CPB, SY, SX, CS, true, GS>();
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem(true));
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
-    k<<<(unsigned)grid, C::THREADS, C::smem(true), s>>>(T, ncells, coords, u, kappa, A);
+    k<<<(unsigned)grid, C::THREADS, C::smem(true), s>>>(T, ncells, coords, u, kappa, A, cmap);
   } else {
-    auto k = colloc_kernel<N, CPB, SY, SX, CS, false>();
+    auto k = colloc_kernel<N, CPB, SY, SX, CS, false, GS>();
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem(false));
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
-    k<<<(unsigned)grid, C::THREADS, C::smem(false), s>>>(T, ncells, coords, u, nullptr, A);
+    k<<<(unsigned)grid, C::THREADS, C::smem(false), s>>>(T, ncells, coords, u, nullptr, A, cmap);
   }
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_colloc_action_kernel launch");
@@ -283,31 +291,43 @@ static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* 
 #define SFK_COLLOC_CPB12 1
 #endif
 
-int launch_hex_colloc_action(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                             const double* w0, const double* w1, cudaStream_t s) {
+template <bool GS>
+static int dispatch_colloc(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                           const double* w0, const double* w1, cudaStream_t s,
+                           const int* cmap) {
   if (p->n != p->m)
     return fail(SFK_EINVAL, "collocated action needs n_q1d == n_dof1d (got %d, %d)", p->n, p->m);
   // (N, cells/CTA, SY, SX, CS) from tools/smem_pads.py
   switch (p->n) {
-    case 2: return launch_n<2, 16, 2, 5, 12>(p, ncells, A, coords, w0, w1, s);
-    case 3: return launch_n<3, 16, 3, 9, 27>(p, ncells, A, coords, w0, w1, s);
-    case 4: return launch_n<4, 8, 4, 19, 76>(p, ncells, A, coords, w0, w1, s);
-    case 5: return launch_n<5, 10, 5, 25, 125>(p, ncells, A, coords, w0, w1, s);
-    case 6: return launch_n<6, 8, 6, 39, 244>(p, ncells, A, coords, w0, w1, s);
-    case 7: return launch_n<7, 5, 7, 52, 369>(p, ncells, A, coords, w0, w1, s);
-    case 8: return launch_n<8, 4, 9, 72, 576>(p, ncells, A, coords, w0, w1, s);
-    case 9: return launch_n<9, 3, 9, 89, 801>(p, ncells, A, coords, w0, w1, s);
-    case 10: return launch_n<10, SFK_COLLOC_CPB10, 11, 110, 1100>(p, ncells, A, coords, w0, w1, s);
-    case 11: return launch_n<11, 2, 11, 123, 1353>(p, ncells, A, coords, w0, w1, s);
-    case 12: return launch_n<12, SFK_COLLOC_CPB12, 13, 156, 1872>(p, ncells, A, coords, w0, w1, s);
-    case 13: return launch_n<13, 1, 13, 169, 2197>(p, ncells, A, coords, w0, w1, s);
-    case 14: return launch_n<14, 1, 17, 238, 3332>(p, ncells, A, coords, w0, w1, s);
-    case 15: return launch_n<15, 1, 15, 225, 3375>(p, ncells, A, coords, w0, w1, s);
-    case 16: return launch_n<16, 1, 17, 272, 4352>(p, ncells, A, coords, w0, w1, s);
-    case 17: return launch_n<17, 1, 17, 289, 4913>(p, ncells, A, coords, w0, w1, s);
+    case 2: return launch_n<2, 16, 2, 5, 12, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 3: return launch_n<3, 16, 3, 9, 27, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 4: return launch_n<4, 8, 4, 19, 76, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 5: return launch_n<5, 10, 5, 25, 125, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 6: return launch_n<6, 8, 6, 39, 244, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 7: return launch_n<7, 5, 7, 52, 369, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 8: return launch_n<8, 4, 9, 72, 576, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 9: return launch_n<9, 3, 9, 89, 801, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 10: return launch_n<10, SFK_COLLOC_CPB10, 11, 110, 1100, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 11: return launch_n<11, 2, 11, 123, 1353, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 12: return launch_n<12, SFK_COLLOC_CPB12, 13, 156, 1872, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 13: return launch_n<13, 1, 13, 169, 2197, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 14: return launch_n<14, 1, 17, 238, 3332, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 15: return launch_n<15, 1, 15, 225, 3375, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 16: return launch_n<16, 1, 17, 272, 4352, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 17: return launch_n<17, 1, 17, 289, 4913, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     default:
       return fail(SFK_EUNSUPPORTED, "collocated hex action: n=%d outside [2,17]", p->n);
   }
+}
+
+int launch_hex_colloc_action(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                             const double* w0, const double* w1, cudaStream_t s) {
+  return dispatch_colloc<false>(p, ncells, A, coords, w0, w1, s, nullptr);
+}
+
+int launch_hex_colloc_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                         double* y, const double* coords, const double* kappa, cudaStream_t s) {
+  return dispatch_colloc<true>(p, ncells, y, coords, x, kappa, s, cmap);
 }
 
 }  // namespace sfk

@@ -41,11 +41,16 @@ struct NeoCfg {
       (size_t)(round_up(CPB * (XSZ + YSZ), 2) + USZ + 2 * CSZ) * sizeof(double);
 };
 
-template <int N, int M, int CPB>
+// GS = true: global residual y += sum_c P_c^T r_c(P_c x) (SURVEY.md §8(f)
+// item 1): cmap[c][3*node + comp] is the global dof of local dof
+// (node, comp); x is gathered into the shared u buffer by per-element
+// cp.async through the map, the residual scattered with fp64 atomics.
+template <int N, int M, int CPB, bool GS = false>
 __global__ void __launch_bounds__(NeoCfg<N, M, CPB>::THREADS)
 hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double lam,
                       int64_t ncells, const double* __restrict__ coords,
-                      const double* __restrict__ u, double* __restrict__ A) {
+                      const double* __restrict__ u, double* __restrict__ A,
+                      const int* __restrict__ cmap = nullptr) {
   using C = NeoCfg<N, M, CPB>;
   constexpr int NN = C::NN, MN = C::MN, MM = C::MM, PX = C::PX, LZ = C::LZ;
   constexpr int XA = C::XA, YA = C::YA;
@@ -65,7 +70,12 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
     const int64_t c0 = bt * CPB;
     const int nc = (int)((ncells - c0) < CPB ? (ncells - c0) : CPB);
     const double* src = u + c0 * (3 * N3);
-    async_copy_phase<C::THREADS>(sU + dst_shift(src), src, nc * 3 * N3, tid);
+    if (GS) {
+      const int* mp = cmap + c0 * (3 * N3);
+      for (int e = tid; e < nc * 3 * N3; e += C::THREADS) cp_async8(sU + e, u + __ldg(mp + e));
+    } else {
+      async_copy_phase<C::THREADS>(sU + dst_shift(src), src, nc * 3 * N3, tid);
+    }
     async_copy<C::THREADS>(sCo + buf * C::CSZ, coords + c0 * 24, nc * 24, tid);
     cp_async_commit();
   };
@@ -77,7 +87,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
   cp_async_wait<0>();
   __syncthreads();
   const double* sC = sCo + (it & 1) * C::CSZ;
-  const double* su = sU + dst_shift(u + cell0 * (3 * N3));
+  const double* su = sU + (GS ? 0 : dst_shift(u + cell0 * (3 * N3)));
 
   // ---------------- forward x / y stages, per component -------------------
 #pragma unroll 1
@@ -285,7 +295,8 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
             v = fma(T.D[i * M + q], p1[q], v);
             v = fma(T.B[i * M + q], p2[q], v);
           }
-          ap[3 * i * NN] = v;
+          if (GS) atomicAdd(A + __ldg(cmap + (cell0 + c) * (3 * N3) + 3 * (i * NN + r) + a), v);
+          else ap[3 * i * NN] = v;
         }
       }
     }
@@ -294,11 +305,11 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
   }  // persistent batch loop
 }
 
-template <int N, int M, int CPB>
+template <int N, int M, int CPB, bool GS = false>
 static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                      const double* u, cudaStream_t s) {
+                      const double* u, cudaStream_t s, const int* cmap = nullptr) {
   using C = NeoCfg<N, M, CPB>;
-  auto k = hex_neohookean_kernel<N, M, CPB>;
+  auto k = hex_neohookean_kernel<N, M, CPB, GS>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)C::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(neohookean)");
@@ -313,7 +324,8 @@ static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
   const int64_t resident = (int64_t)sms * per_sm;
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
-  k<<<grid, C::THREADS, C::SMEM, s>>>(T, p->params[0], p->params[1], ncells, coords, u, A);
+  k<<<grid, C::THREADS, C::SMEM, s>>>(T, p->params[0], p->params[1], ncells, coords, u, A,
+                                      cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_neohookean_kernel launch");
 }
@@ -340,30 +352,41 @@ static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double
 #define SFK_NEO_CPB_P6 1
 #endif
 
-int launch_hex_neohookean(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                          const double* w0, cudaStream_t s) {
+template <bool GS>
+static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                        const double* w0, cudaStream_t s, const int* cmap) {
   const int n = p->n, m = p->m;
   if (m == n + 1) {
     switch (n) {
-      case 2: return launch_neo<2, 3, SFK_NEO_CPB_P1>(p, ncells, A, coords, w0, s);
-      case 3: return launch_neo<3, 4, SFK_NEO_CPB_P2>(p, ncells, A, coords, w0, s);
-      case 4: return launch_neo<4, 5, SFK_NEO_CPB_P3>(p, ncells, A, coords, w0, s);
-      case 5: return launch_neo<5, 6, SFK_NEO_CPB_P4>(p, ncells, A, coords, w0, s);
-      case 6: return launch_neo<6, 7, SFK_NEO_CPB_P5>(p, ncells, A, coords, w0, s);
-      case 7: return launch_neo<7, 8, SFK_NEO_CPB_P6>(p, ncells, A, coords, w0, s);
+      case 2: return launch_neo<2, 3, SFK_NEO_CPB_P1, GS>(p, ncells, A, coords, w0, s, cmap);
+      case 3: return launch_neo<3, 4, SFK_NEO_CPB_P2, GS>(p, ncells, A, coords, w0, s, cmap);
+      case 4: return launch_neo<4, 5, SFK_NEO_CPB_P3, GS>(p, ncells, A, coords, w0, s, cmap);
+      case 5: return launch_neo<5, 6, SFK_NEO_CPB_P4, GS>(p, ncells, A, coords, w0, s, cmap);
+      case 6: return launch_neo<6, 7, SFK_NEO_CPB_P5, GS>(p, ncells, A, coords, w0, s, cmap);
+      case 7: return launch_neo<7, 8, SFK_NEO_CPB_P6, GS>(p, ncells, A, coords, w0, s, cmap);
       default: break;
     }
   } else if (m == n) {
     switch (n) {
-      case 2: return launch_neo<2, 2, 16>(p, ncells, A, coords, w0, s);
-      case 3: return launch_neo<3, 3, 16>(p, ncells, A, coords, w0, s);
-      case 4: return launch_neo<4, 4, 8>(p, ncells, A, coords, w0, s);
+      case 2: return launch_neo<2, 2, 16, GS>(p, ncells, A, coords, w0, s, cmap);
+      case 3: return launch_neo<3, 3, 16, GS>(p, ncells, A, coords, w0, s, cmap);
+      case 4: return launch_neo<4, 4, 8, GS>(p, ncells, A, coords, w0, s, cmap);
       default: break;
     }
   }
   return fail(SFK_EUNSUPPORTED,
               "neo-Hookean residual: no kernel for n=%d, m=%d (m==n+1 in 2..7 or m==n in 2..4)",
               n, m);
+}
+
+int launch_hex_neohookean(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                          const double* w0, cudaStream_t s) {
+  return dispatch_neo<false>(p, ncells, A, coords, w0, s, nullptr);
+}
+
+int launch_hex_neohookean_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                             double* y, const double* coords, cudaStream_t s) {
+  return dispatch_neo<true>(p, ncells, y, coords, x, s, cmap);
 }
 
 }  // namespace sfk

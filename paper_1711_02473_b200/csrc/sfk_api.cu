@@ -338,6 +338,34 @@ int sfk_eval_gather_scatter(const sfk_plan* p, int64_t ncells, const int32_t* ce
   return launch_hex_action_gs(p, ncells, cell_dofs, x, y, coords, (cudaStream_t)stream);
 }
 
+int sfk_eval_global(const sfk_plan* p, int64_t ncells, const int32_t* cell_dofs,
+                    const double* x, double* y, const double* coords, const double* w1,
+                    void* stream) {
+  if (!p) return fail(SFK_EINVAL, "plan is NULL");
+  if (ncells < 0) return fail(SFK_EINVAL, "ncells < 0");
+  if (ncells == 0) return SFK_OK;
+  if (!cell_dofs || !x || !y || !coords) return fail(SFK_EINVAL, "NULL pointer argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->dim != 3) return fail(SFK_EUNSUPPORTED, "global operator: hex plans only");
+  switch (p->kind) {
+    case SFK_KIND_ACTION_LAPLACE:
+      if (w1) return fail(SFK_EINVAL, "action_laplace takes no w1");
+      if (p->collocated) return launch_hex_colloc_gs(p, ncells, cell_dofs, x, y, coords, nullptr, s);
+      if (p->n != p->m)
+        return fail(SFK_EUNSUPPORTED, "global operator: action_laplace with m == n only");
+      return launch_hex_action_gs(p, ncells, cell_dofs, x, y, coords, s);
+    case SFK_KIND_ACTION_WEIGHTED_LAPLACE:
+      if (!w1) return fail(SFK_EINVAL, "w1 (kappa per cell) is NULL");
+      return launch_hex_colloc_gs(p, ncells, cell_dofs, x, y, coords, w1, s);
+    case SFK_KIND_NEOHOOKEAN_RESIDUAL:
+      if (w1) return fail(SFK_EINVAL, "neohookean_residual takes no w1");
+      return launch_hex_neohookean_gs(p, ncells, cell_dofs, x, y, coords, s);
+    default:
+      return fail(SFK_EUNSUPPORTED, "global operator: kind %d has no fused gather/scatter",
+                  p->kind);
+  }
+}
+
 int sfk_assemble_csr(const sfk_plan* p, int64_t ncells, const int32_t* cell_dofs,
                      const double* coords, const int64_t* row_ptr, const int32_t* col_idx,
                      const int32_t* entry_map, double* values, void* stream) {

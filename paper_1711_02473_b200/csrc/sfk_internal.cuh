@@ -78,6 +78,10 @@ int launch_hex_action_v2_gs(const sfk_plan* p, int64_t ncells, const int* cmap, 
                             double* y, const double* coords, cudaStream_t s);
 int launch_hex_action_tc_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                             double* y, const double* coords, cudaStream_t s);
+int launch_hex_neohookean_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                             double* y, const double* coords, cudaStream_t s);
+int launch_hex_colloc_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                         double* y, const double* coords, const double* kappa, cudaStream_t s);
 int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                          double* y, const double* coords, cudaStream_t s);
 int launch_hex_colloc_action(const sfk_plan* p, int64_t ncells, double* A,

@@ -41,7 +41,7 @@ EXPORTED_SYMBOLS = (
     "sfk_eval_gather_scatter", "sfk_program_create", "sfk_program_destroy",
     "sfk_program_sizes", "sfk_program_config", "sfk_program_text", "sfk_program_eval",
     "sfk_csr_create", "sfk_csr_info", "sfk_csr_destroy", "sfk_assemble_csr",
-    "sfk_csr_entry_map",
+    "sfk_csr_entry_map", "sfk_eval_global",
 )
 ABI_VERSION = 1
 SUM_WORKSPACE = 1024
@@ -83,6 +83,9 @@ def _declare(lib):
     if hasattr(lib, "sfk_eval_gather_scatter"):   # absent from pre-(f) A/B builds
         lib.sfk_eval_gather_scatter.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, _vp]
         lib.sfk_eval_gather_scatter.restype = ci
+    if hasattr(lib, "sfk_eval_global"):
+        lib.sfk_eval_global.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, _vp, _vp]
+        lib.sfk_eval_global.restype = ci
     if hasattr(lib, "sfk_csr_create"):
         lib.sfk_csr_create.argtypes = [i64, ci, _vp, i64, _vp, ctypes.POINTER(_vp)]
         lib.sfk_csr_create.restype = ci

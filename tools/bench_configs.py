@@ -178,6 +178,47 @@ def main():
                                                       plan.algorithmic_flops / (p64 * 1e12)) / t, 4)}
                 print(json.dumps(rec), flush=True)
                 del coords, gmap, x, y
+        elif cfg in ("C3G", "C4G"):
+            # the other fused global operators: C3's weighted collocated Laplace
+            # and C4's assembled neo-Hookean residual, on their BASELINE
+            # lattices (16, 64, 64)
+            from paper_1711_02473_b200.assembly import (GlobalOperator, lattice_dof_map,
+                                                        lattice_ndofs, lattice_vector_dof_map)
+            dims = (16, 64, 64)
+            coords = torch.from_numpy(workloads.lattice_coords(*dims)).to(dev)
+            C = coords.shape[0]
+            degs = range(4, 17) if cfg == "C3G" else range(2, 7)
+            for p in degs:
+                if args.p and p not in args.p:
+                    continue
+                n3 = (p + 1) ** 3
+                if cfg == "C3G":
+                    plan = compile_form(action_form(REGISTRY["weighted_laplace"]), "hex", p,
+                                        "spectral", "spectral_gll", "collocated-gll")
+                    gmap = torch.from_numpy(lattice_dof_map(*dims, p)).to(dev)
+                    nd = lattice_ndofs(*dims, p)
+                    w1 = torch.from_numpy(workloads.c3_inputs(p, dims)["w1"]).to(dev)
+                    ndl = n3
+                else:
+                    plan = compile_form(neohookean_residual_form(), "hex", p, quadrature=p + 2)
+                    gmap = torch.from_numpy(lattice_vector_dof_map(*dims, p)).to(dev)
+                    nd = 3 * lattice_ndofs(*dims, p)
+                    w1 = None
+                    ndl = 3 * n3
+                op = GlobalOperator(plan, gmap, coords, nd, w1=w1)
+                x = (torch.rand(nd, dtype=torch.float64, device=dev) - 0.5) * (0.02 * workloads.H)
+                y = torch.zeros_like(x)
+                t = time_launch(lambda: op.apply(x, out=y, accumulate=True))
+                byt = C * (24 * 8 + 4 * ndl + (8 * n3 if w1 is not None else 0)) + 3 * 8 * nd
+                rec = {"config": cfg, "form": "global %s (gather-scatter)" % plan.name, "p": p,
+                       "cells": C, "global_dofs": nd, "ms": round(t * 1e3, 5),
+                       "gdofs_local": round(C * ndl / t / 1e9, 3),
+                       "gdofs_global": round(nd / t / 1e9, 3),
+                       "roofline_frac": round(C * max(byt / C / (hbm * 1e9),
+                                                      plan.algorithmic_flops / (p64 * 1e12)) / t, 4)}
+                print(json.dumps(rec), flush=True)
+                del gmap, x, y
+            del coords
         elif cfg == "C3":
             spec = action_form(REGISTRY["weighted_laplace"])
             for p in range(4, 17):
