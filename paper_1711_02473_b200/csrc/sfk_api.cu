@@ -47,6 +47,7 @@ void note_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed)
 //   v3: v2 + input-streaming contractions, searched pads    (hex_action3.cu)
 //   tc: FP64 tensor-core (DMMA) stages, n = 8               (hex_action_tc.cu)
 //   cell: one thread per cell, everything in registers, n = 2 (hex_action_p1.cu)
+//   v4: v3 with whole cells per warp, no CTA barriers, n = 3..5 (hex_action4.cu)
 static int c2_variant() {
   static int v = -1;
   if (v < 0) {
@@ -55,6 +56,7 @@ static int c2_variant() {
     if (e && e[0] == 'v' && e[1] >= '1' && e[1] <= '3') v = e[1] - '0';
     if (e && strcmp(e, "tc") == 0) v = 4;
     if (e && strcmp(e, "cell") == 0) v = 5;
+    if (e && strcmp(e, "v4") == 0) v = 6;
   }
   return v;
 }
@@ -62,8 +64,8 @@ static int c2_variant() {
 static int c2_auto(int n) {
   switch (n) {
     case 2: return 5;
-    case 3: return 3;
-    case 4: return 2;
+    case 3: return 6;
+    case 4: return 6;
     case 5: return 3;
     case 6: return 2;
     case 7: return 3;
@@ -78,6 +80,10 @@ static int launch_c2(const sfk_plan* p, int64_t ncells, double* A, const double*
   int v = c2_variant();
   if (v == 0) v = c2_auto(p->n);
   int rc = SFK_EUNSUPPORTED;
+  if (v == 6) {
+    rc = launch_hex_action_v4(p, ncells, A, coords, w0, s);
+    if (rc == SFK_EUNSUPPORTED) v = 3;
+  }
   if (v == 5) rc = launch_hex_action_p1(p, ncells, A, coords, w0, s);
   if (v == 4) rc = launch_hex_action_tc(p, ncells, A, coords, w0, s);
   if (v >= 4 && rc == SFK_EUNSUPPORTED) v = 3;
