@@ -20,6 +20,8 @@
 // 9 lines with (1) the 9 reference-gradient lines, (2) the 9 flux lines and
 // (3) the 9 transposed-z lines — no extra shared memory and no barrier
 // between those three steps.  Transposed y/x stages then run per component.
+#include <cstdlib>
+
 #include "async_copy.cuh"
 #include "hex_geometry.cuh"
 
@@ -45,8 +47,12 @@ struct NeoCfg {
 // item 1): cmap[c][3*node + comp] is the global dof of local dof
 // (node, comp); x is gathered into the shared u buffer by per-element
 // cp.async through the map, the residual scattered with fp64 atomics.
-template <int N, int M, int CPB, bool GS = false>
-__global__ void __launch_bounds__(NeoCfg<N, M, CPB>::THREADS)
+// WARPS > 0: warp-synchronous mode for small p — each warp owns CPB whole
+// cells (every stage has <= 32 lines for them) with its own shared-memory
+// slice and prefetch, and the stages sync with __syncwarp instead of CTA
+// barriers (the CTA version runs ~13 barriers per batch).
+template <int N, int M, int CPB, bool GS = false, int WARPS = 0>
+__global__ void __launch_bounds__(WARPS ? 32 * WARPS : NeoCfg<N, M, CPB>::THREADS)
 hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double lam,
                       int64_t ncells, const double* __restrict__ coords,
                       const double* __restrict__ u, double* __restrict__ A,
@@ -55,37 +61,48 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
   constexpr int NN = C::NN, MN = C::MN, MM = C::MM, PX = C::PX, LZ = C::LZ;
   constexpr int XA = C::XA, YA = C::YA;
   constexpr int N3 = N * NN;
+  constexpr int TH = WARPS ? 32 : C::THREADS;       // threads sharing one cell group
+  constexpr int GROUPS = WARPS ? WARPS : 1;         // independent cell groups per CTA
+  static_assert(!WARPS || CPB * MM <= 32, "warp-synchronous mode needs CPB*m^2 <= 32");
   extern __shared__ __align__(16) double smem[];
-  double* sX = smem;
+  const int grp = WARPS ? (int)(threadIdx.x >> 5) : 0;
+  double* gbase = smem + (size_t)grp * (C::SMEM / sizeof(double));
+  double* sX = gbase;
   double* sY = sX + CPB * C::XSZ;
-  double* sU = smem + round_up(CPB * (C::XSZ + C::YSZ), 2);
+  double* sU = gbase + round_up(CPB * (C::XSZ + C::YSZ), 2);
   double* sCo = sU + C::USZ;
-  const int tid = threadIdx.x;
-  const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  const int tid = WARPS ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+  auto sync = [] { if (WARPS) __syncwarp(); else __syncthreads(); };
+  const int64_t nbatch = (ncells + CPB * GROUPS - 1) / (CPB * GROUPS);
   // persistent CTAs: u (3 components interleaved, as stored) and coords of
   // the next batch stream into shared memory with cp.async while the current
   // batch computes (u once the last x stage consumed it, coords
   // double-buffered because the z stage needs them)
   auto prefetch = [&](int64_t bt, int buf) {
-    const int64_t c0 = bt * CPB;
+    const int64_t c0 = bt * (CPB * GROUPS) + grp * CPB;
     const int nc = (int)((ncells - c0) < CPB ? (ncells - c0) : CPB);
+    if (nc <= 0) {
+      cp_async_commit();
+      return;
+    }
     const double* src = u + c0 * (3 * N3);
     if (GS) {
       const int* mp = cmap + c0 * (3 * N3);
-      for (int e = tid; e < nc * 3 * N3; e += C::THREADS) cp_async8(sU + e, u + __ldg(mp + e));
+      for (int e = tid; e < nc * 3 * N3; e += TH) cp_async8(sU + e, u + __ldg(mp + e));
     } else {
-      async_copy_phase<C::THREADS>(sU + dst_shift(src), src, nc * 3 * N3, tid);
+      async_copy_phase<TH>(sU + dst_shift(src), src, nc * 3 * N3, tid);
     }
-    async_copy<C::THREADS>(sCo + buf * C::CSZ, coords + c0 * 24, nc * 24, tid);
+    async_copy<TH>(sCo + buf * C::CSZ, coords + c0 * 24, nc * 24, tid);
     cp_async_commit();
   };
   int64_t batch = blockIdx.x;
   if (batch < nbatch) prefetch(batch, 0);
   for (int it = 0; batch < nbatch; batch += gridDim.x, ++it) {
-  const int64_t cell0 = batch * CPB;
-  const int ncb = (int)((ncells - cell0) < CPB ? (ncells - cell0) : CPB);
+  const int64_t cell0 = batch * (CPB * GROUPS) + grp * CPB;
+  const int ncb = (int)((ncells - cell0) < CPB ? ((ncells - cell0) > 0 ? ncells - cell0 : 0)
+                                                : CPB);
   cp_async_wait<0>();
-  __syncthreads();
+  sync();
   const double* sC = sCo + (it & 1) * C::CSZ;
   const double* su = sU + (GS ? 0 : dst_shift(u + cell0 * (3 * N3)));
 
@@ -111,7 +128,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
         xo[XA + q * PX] = d;
       }
     }
-    __syncthreads();
+    sync();
     if (a == 2 && batch + gridDim.x < nbatch) prefetch(batch + gridDim.x, (it & 1) ^ 1);
     if (tid < CPB * MN) {
       const int c = tid / MN, r = tid - c * MN;
@@ -138,7 +155,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
         yo[2 * YA + q * LZ] = db;  // -> d/dx
       }
     }
-    __syncthreads();
+    sync();
   }
 
   // ---------------- z-lines: gradients, constitutive flux, transposed z ----
@@ -244,7 +261,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
       }
     }
   }
-  __syncthreads();
+  sync();
 
   // ---------------- transposed y / x stages, per component ---------------
 #pragma unroll 1
@@ -275,7 +292,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
         xo[XA + i * N] = r2;
       }
     }
-    __syncthreads();
+    sync();
     if (tid < CPB * NN) {
       const int c = tid / NN, r = tid - c * NN;
       if (c < ncb) {
@@ -300,32 +317,34 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
         }
       }
     }
-    __syncthreads();
+    sync();
   }
   }  // persistent batch loop
 }
 
-template <int N, int M, int CPB, bool GS = false>
+template <int N, int M, int CPB, bool GS = false, int WARPS = 0>
 static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                       const double* u, cudaStream_t s, const int* cmap = nullptr) {
   using C = NeoCfg<N, M, CPB>;
-  auto k = hex_neohookean_kernel<N, M, CPB, GS>;
+  constexpr int THREADS = WARPS ? 32 * WARPS : C::THREADS;
+  constexpr size_t SMEM = WARPS ? WARPS * C::SMEM : C::SMEM;
+  constexpr int CPBT = WARPS ? WARPS * CPB : CPB;
+  auto k = hex_neohookean_kernel<N, M, CPB, GS, WARPS>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)C::SMEM);
+                                       (int)SMEM);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(neohookean)");
   cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C::THREADS, C::SMEM);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, SMEM);
   if (e != cudaSuccess) return cuda_status(e, "occupancy(neohookean)");
   if (per_sm < 1) return fail(SFK_ECUDA, "neo-Hookean kernel does not fit on an SM");
   const Tabs<N, M> T = make_tabs<N, M>(p);
-  const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  const int64_t nbatch = (ncells + CPBT - 1) / CPBT;
   const int64_t resident = (int64_t)sms * per_sm;
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
-  k<<<grid, C::THREADS, C::SMEM, s>>>(T, p->params[0], p->params[1], ncells, coords, u, A,
-                                      cmap);
+  k<<<grid, THREADS, SMEM, s>>>(T, p->params[0], p->params[1], ncells, coords, u, A, cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_neohookean_kernel launch");
 }
@@ -333,6 +352,10 @@ static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double
 // cells per CTA for m = n + 1 (C4) per degree p (overridable for A/B builds;
 // profiles/r01au_c4_cpb.jsonl: p = 2 16 -> 8 cells 0.199 -> 0.164 ms, p = 3
 // 8 -> 4, p = 6 2 -> 1; smaller CTAs interleave the barrier-heavy phases)
+#ifndef SFK_NEO_WARPS_DEFAULT
+#define SFK_NEO_WARPS_DEFAULT 4   // warp-synchronous kernels at p <= 3 (A/B: SFK_NEO_WARPS;
+                                  // profiles/r01bb_c4_warps.jsonl: ~3% at p = 2, 3)
+#endif
 #ifndef SFK_NEO_CPB_P1
 #define SFK_NEO_CPB_P1 16
 #endif
@@ -356,6 +379,22 @@ template <bool GS>
 static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                         const double* w0, cudaStream_t s, const int* cmap) {
   const int n = p->n, m = p->m;
+  static const int warps = [] {
+    const char* e = std::getenv("SFK_NEO_WARPS");
+    return e ? std::atoi(e) : SFK_NEO_WARPS_DEFAULT;
+  }();
+  if (m == n + 1 && warps > 0 && n <= 4) {
+    // warp-synchronous: 3 / 2 / 1 cells per warp at p = 1 / 2 / 3
+    if (warps == 8) {
+      if (n == 2) return launch_neo<2, 3, 3, GS, 8>(p, ncells, A, coords, w0, s, cmap);
+      if (n == 3) return launch_neo<3, 4, 2, GS, 8>(p, ncells, A, coords, w0, s, cmap);
+      if (n == 4) return launch_neo<4, 5, 1, GS, 8>(p, ncells, A, coords, w0, s, cmap);
+    } else {
+      if (n == 2) return launch_neo<2, 3, 3, GS, 4>(p, ncells, A, coords, w0, s, cmap);
+      if (n == 3) return launch_neo<3, 4, 2, GS, 4>(p, ncells, A, coords, w0, s, cmap);
+      if (n == 4) return launch_neo<4, 5, 1, GS, 4>(p, ncells, A, coords, w0, s, cmap);
+    }
+  }
   if (m == n + 1) {
     switch (n) {
       case 2: return launch_neo<2, 3, SFK_NEO_CPB_P1, GS>(p, ncells, A, coords, w0, s, cmap);
