@@ -362,8 +362,16 @@ int launch_hex_action_v3(const sfk_plan* p, int64_t ncells, double* A, const dou
   return dispatch_v3<false>(p, ncells, A, coords, w0, s, nullptr);
 }
 
+static bool force_v3_small() {
+  static const bool v = [] {
+    const char* e = std::getenv("SFK_C2G_SMALL");   // "v3": A/B of the p = 2, 3 path
+    return e && e[0] == 'v' && e[1] == '3';
+  }();
+  return v;
+}
+
 // Same generation as the E-vector action per degree (sfk_api.cu c2_auto):
-// p = 1 cell kernel, p = 3, 5, 8 v2, p = 7 DMMA, the rest v3.
+// p = 1 cell kernel, p = 2, 3 v4, p = 5, 8 v2, p = 7 DMMA, the rest v3.
 // SFK_C2G_KERNEL=v3 forces v3 (A/B runs).
 int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                          double* y, const double* coords, cudaStream_t s) {
@@ -374,7 +382,9 @@ int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, con
   if (!force_v3 && p->n == p->m) {
     if (p->n == 2 && (reinterpret_cast<uintptr_t>(cmap) & 15) == 0)   // int4 map loads
       return launch_hex_action_p1_gs(p, ncells, cmap, x, y, coords, s);
-    if (p->n == 4 || p->n == 6 || p->n == 9)
+    if ((p->n == 3 || p->n == 4) && !force_v3_small())
+      return launch_hex_action_v4_gs(p, ncells, cmap, x, y, coords, s);
+    if (p->n == 6 || p->n == 9 || (p->n == 4 && force_v3_small()))
       return launch_hex_action_v2_gs(p, ncells, cmap, x, y, coords, s);
     if (p->n == 8) return launch_hex_action_tc_gs(p, ncells, cmap, x, y, coords, s);
   }

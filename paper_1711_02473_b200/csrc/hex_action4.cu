@@ -35,11 +35,15 @@ struct Act4Layout {
   static_assert(CPW >= 1, "n^2 > 32");
 };
 
-template <class L, int MINB>
+// GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
+// item 1), as in v3: each warp double-buffers its cells' map (int32) in its
+// u slot, gathers x through it in the x stage and scatter-adds y with fp64
+// atomics in the transposed x stage.
+template <class L, int MINB, bool GS = false>
 __global__ void __launch_bounds__(L::THREADS, MINB)
 hex_laplace_action_v4(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
-                      double* __restrict__ A) {
+                      double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
   constexpr int N = L::N, M = L::M, NN = L::NN, N3 = L::N3, CPW = L::CPW, CPB = L::CPB;
   constexpr int XY = L::XY, PX = L::PX, XC = L::XC, LZ = L::LZ, YX = L::YX, YC = L::YC;
   constexpr int XA = L::XA, YA = L::YA, MN = M * N, MM = M * M;
@@ -51,12 +55,18 @@ hex_laplace_action_v4(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
   double* sU = base + round_up(L::CELLS, 2);       // [CPW*N3 + 1]
   double* sCo = sU + L::UW;                        // [2][CPW*24]
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  int* sMap = reinterpret_cast<int*>(sU);            // GS: [2][CPW*N3] int32
+  static_assert(!GS || CPW * N3 <= L::UW, "map double buffer does not fit");
 
   auto prefetch = [&](int64_t bb, int buf) {
     const int64_t c0 = bb * CPB + warp * CPW;
     const int nc = (int)((ncells - c0) < CPW ? (ncells - c0) : CPW);
     if (nc > 0) {
-      async_copy_phase<32>(sU + dst_shift(u + c0 * N3), u + c0 * N3, nc * N3, lane);
+      if (GS) {
+        for (int e = lane; e < nc * N3; e += 32) cp_async4(sMap + buf * CPW * N3 + e, cmap + c0 * N3 + e);
+      } else {
+        async_copy_phase<32>(sU + dst_shift(u + c0 * N3), u + c0 * N3, nc * N3, lane);
+      }
       async_copy<32>(sCo + buf * L::CW, coords + c0 * 24, nc * 24, lane);
     }
     cp_async_commit();
@@ -74,14 +84,17 @@ hex_laplace_action_v4(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
     const bool act = lane < CPW * NN;              // n = m: every stage has NN lines/cell
     const int c = act ? lane / NN : 0, r = act ? lane - (lane / NN) * NN : 0;
     const bool live = act && c < ncw;
+    const int* smap = sMap + cur * CPW * N3;
 
     // ---- x stage: line (c, iy, iz) -> X0 = Bx u, X1 = Dx u ---------------
     if (act) {
       const int iy = r / N, iz = r - iy * N;
-      const double* ui = sU + dst_shift(u + cell0 * N3) + c * N3 + r;
+      const double* ui = sU + (GS ? 0 : dst_shift(u + cell0 * N3)) + c * N3 + r;
+      const int* mi = smap + c * N3 + r;
+      auto uval = [&](int i) { return GS ? __ldg(u + mi[i * NN]) : ui[i * NN]; };
       double xb[M], xd[M];
       {
-        const double v = live ? ui[0] : 0.0;
+        const double v = live ? uval(0) : 0.0;
 #pragma unroll
         for (int q = 0; q < M; ++q) {
           xb[q] = T.B[q] * v;
@@ -90,7 +103,7 @@ hex_laplace_action_v4(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
       }
 #pragma unroll
       for (int i = 1; i < N; ++i) {
-        const double v = live ? ui[i * NN] : 0.0;
+        const double v = live ? uval(i) : 0.0;
 #pragma unroll
         for (int q = 0; q < M; ++q) {
           xb[q] = fma(T.B[i * M + q], v, xb[q]);
@@ -271,18 +284,24 @@ hex_laplace_action_v4(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
           a[i] = fma(T.B[i * M + q], p2, a[i]);
         }
       }
-      double* ap = A + (cell0 + c) * N3 + r;
+      if (GS) {
+        const int* mi = smap + c * N3 + r;
 #pragma unroll
-      for (int i = 0; i < N; ++i) ap[i * NN] = a[i];
+        for (int i = 0; i < N; ++i) atomicAdd(A + mi[i * NN], a[i]);
+      } else {
+        double* ap = A + (cell0 + c) * N3 + r;
+#pragma unroll
+        for (int i = 0; i < N; ++i) ap[i * NN] = a[i];
+      }
     }
     __syncwarp();   // X/R is rewritten by this warp's next x stage
   }
 }
 
-template <class L, int MINB>
+template <class L, int MINB, bool GS = false>
 static int launch_v4(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                     const double* u, cudaStream_t s) {
-  auto kern = hex_laplace_action_v4<L, MINB>;
+                     const double* u, cudaStream_t s, const int* cmap = nullptr) {
+  auto kern = hex_laplace_action_v4<L, MINB, GS>;
   static int sms = 0, per_sm = 0;
   if (!sms) {
     int dev = 0;
@@ -300,7 +319,7 @@ static int launch_v4(const sfk_plan* p, int64_t ncells, double* A, const double*
   const int64_t nbatch = (ncells + L::CPB - 1) / L::CPB;
   const int64_t resident = (int64_t)sms * per_sm;
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
-  kern<<<grid, L::THREADS, L::SMEM, s>>>(T, ncells, coords, u, A);
+  kern<<<grid, L::THREADS, L::SMEM, s>>>(T, ncells, coords, u, A, cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_v4 launch");
 }
@@ -323,6 +342,17 @@ int launch_hex_action_v4(const sfk_plan* p, int64_t ncells, double* A, const dou
     case 3: return launch_v4<Act4Layout<3, W, 3, 19, 121, 3, 9, 91>, MB>(p, ncells, A, coords, w0, s);
     case 4: return launch_v4<Act4Layout<4, W, 4, 20, 160, 5, 20, 240>, MB>(p, ncells, A, coords, w0, s);
     case 5: return launch_v4<Act4Layout<5, W, 5, 37, 377, 5, 25, 381>, MB>(p, ncells, A, coords, w0, s);
+    default: return SFK_EUNSUPPORTED;
+  }
+}
+
+int launch_hex_action_v4_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                            double* y, const double* coords, cudaStream_t s) {
+  if (p->n != p->m) return SFK_EUNSUPPORTED;
+  constexpr int W = SFK_V4_WARPS, MB = SFK_V4_MINB;
+  switch (p->n) {
+    case 3: return launch_v4<Act4Layout<3, W, 3, 19, 121, 3, 9, 91>, MB, true>(p, ncells, y, coords, x, s, cmap);
+    case 4: return launch_v4<Act4Layout<4, W, 4, 20, 160, 5, 20, 240>, MB, true>(p, ncells, y, coords, x, s, cmap);
     default: return SFK_EUNSUPPORTED;
   }
 }
