@@ -641,14 +641,45 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
   if (const char* e = std::getenv("SFK_LP_MAX_THREADS")) tmax = std::atoll(e);
   C.threads = (int)std::min<long long>(tmax, std::max<long long>(64, ((maxitems + 31) / 32) * 32));
 
+  // warp mode: with at least one cell per warp, every warp owns whole cells
+  // through all phases, so all dependencies stay inside a warp and the
+  // barriers become __syncwarp (the CTA-wide version spent 18% of its stalls
+  // at barriers, profiles/r01av_lp_p3.md).  SFK_LP_WARP=0 disables it.
+  {
+    // measured (profiles/r01bc_lp_warp.jsonl): a win for matrix-shaped
+    // programs (laplace hex p=2 1.04 -> 0.72 ms, curl_curl, prism matrices),
+    // a loss for the actions, whose large phases want many threads per cell
+    bool wm = C.cells_per_block >= 2 && !C.global_scratch && P.ret_size >= 128;
+    if (const char* e = std::getenv("SFK_LP_WARP")) wm = wm && std::atoi(e) != 0;
+    if (wm) {
+      // largest power of two <= min(threads / 32, NC) (NC is a power of two)
+      const int cap = std::max(1, std::min(C.threads / 32, C.cells_per_block));
+      int warps = 1;
+      while (warps * 2 <= cap) warps *= 2;
+      C.threads = 32 * warps;
+      C.warp_mode = 1;
+      C.cells_per_warp = C.cells_per_block / warps;
+    }
+  }
+
   // 4. emission
   const int NC = C.cells_per_block, NCP = C.ncp, T = C.threads;
+  const bool WM = C.warp_mode != 0;
+  const int LN = WM ? C.cells_per_warp : NC;   // cells of one loop group (warp or CTA)
+  const int LT = WM ? 32 : T;                  // threads of one loop group
+  const std::string TID = WM ? "lane" : "threadIdx.x";
+  // warp mode: each warp has its own [slot][LN] region (Sw), c is the
+  // warp-local cell and wbase + c the CTA cell (global addressing, nvalid)
+  const std::string CB = WM ? "wbase + " : "";
+  const std::string SYNC = WM ? "__syncwarp()" : "__syncthreads()";
   std::ostringstream o;
   auto slot = [&](const std::string& nm, const std::string& addr) {
     std::ostringstream s;
     const long long b = base.at(nm);
-    if (NCP == 1) s << "S[" << b << " + (" << addr << ")]";
-    else s << "S[(" << b << " + (" << addr << ")) * " << NCP << " + c]";
+    const int stride = WM ? LN : NCP;
+    const char* arr = WM ? "Sw" : "S";
+    if (stride == 1) s << arr << "[" << b << " + (" << addr << ")]";
+    else s << arr << "[(" << b << " + (" << addr << ")) * " << stride << " + c]";
     return s.str();
   };
   auto ent = [](const Entry& e) { return e.idx >= 0 ? "i" + std::to_string(e.idx) : std::to_string(e.val); };
@@ -762,43 +793,47 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
     << "    const long long c0 = chunk * " << NC << ";\n"
     << "    const int nvalid = (int)((ncells - c0) < " << NC << " ? (ncells - c0) : " << NC << ");\n";
   if (NC == 1) o << "    const int c = 0; (void)c;\n";
+  if (WM)
+    o << "    const int lane = threadIdx.x & 31, wbase = (threadIdx.x >> 5) * " << LN << ";\n"
+      << "    double* Sw = S + (threadIdx.x >> 5) * " << C.slots * LN << ";\n";
   // global <-> shared transfers: each warp moves G consecutive elements of
   // 32/G cells (G*NC = 32 when NC <= 32): G-double runs per cell in HBM,
   // 32 consecutive doubles in shared memory (element k of cell c at k*NC + c)
   std::vector<Access> acc;
-  auto xfer_g = [&](long long sz) { return std::min<long long>(sz, std::max(1, 32 / NC)); };
+  auto xfer_g = [&](long long sz) { return std::min<long long>(sz, std::max(1, 32 / LN)); };
   auto xfer_items = [&](long long sz) {
     const long long g = xfer_g(sz);
-    return NC * g * ((sz + g - 1) / g);
+    return LN * g * ((sz + g - 1) / g);
   };
   auto xfer_open = [&](long long sz) {
     const long long g = xfer_g(sz);
-    o << "    for (int e = threadIdx.x; e < " << xfer_items(sz) << "; e += " << T << ") {\n";
+    o << "    for (int e = " << TID << "; e < " << xfer_items(sz) << "; e += " << LT << ") {\n";
     if (NC > 1)
-      o << "      const int c = (e / " << g << ") % " << NC << ", k = (e / " << g * NC << ") * " << g
-        << " + e % " << g << ";\n";
+      o << "      const int c = (e / " << g << ") % " << LN << ", k = (e / " << g * LN
+        << ") * " << g << " + e % " << g << ";\n";
     else
       o << "      const int k = e;\n";
   };
+  // accesses of one loop group (element = slot * LN + group-local cell)
   auto xfer_access = [&](long long sz, long long b, bool write) {
     const long long g = xfer_g(sz);
     acc.clear();
     for (long long e = 0; e < xfer_items(sz); ++e) {
-      const long long c = NC > 1 ? (e / g) % NC : 0;
-      const long long k = NC > 1 ? (e / (g * NC)) * g + e % g : e;
-      if (k < sz) acc.push_back({(b + k) * NC + c, (int)(e % T), write});
+      const long long c = NC > 1 ? (e / g) % LN : 0;
+      const long long k = NC > 1 ? (e / (g * LN)) * g + e % g : e;
+      if (k < sz) acc.push_back({(b + k) * LN + c, (int)(e % LT), write});
     }
   };
   for (size_t a = 0; a < P.args.size(); ++a) {
     const long long sz = P.args[a].second;
     xfer_open(sz);
-    o << "      if (k < " << sz << ") " << slot(P.args[a].first, "k") << " = (c < nvalid) ? g" << a
-      << "[(c0 + c) * " << sz << " + k] : 0.0;\n    }\n";
+    o << "      if (k < " << sz << ") " << slot(P.args[a].first, "k") << " = (" << CB
+      << "c < nvalid) ? g" << a << "[(c0 + " << CB << "c) * " << sz << " + k] : 0.0;\n    }\n";
   }
   // barrier plan (see Window): the argument loads open the window
   int max_idx = 0;
   for (const auto& kv : P.extents) max_idx = std::max(max_idx, kv.first);
-  Window win(C.slots * NC);
+  Window win(C.slots * LN);
   for (size_t a = 0; a < P.args.size(); ++a) {
     xfer_access(P.args[a].second, base.at(P.args[a].first), true);
     win.add(acc);
@@ -806,7 +841,7 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
   auto barrier_for = [&](bool known) {
     const bool need = !known || win.conflicts(acc);
     if (need) {
-      o << "    __syncthreads();\n";
+      o << "    " << SYNC << ";\n";
       ++C.barriers;
       win.clear();
     }
@@ -816,17 +851,18 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
   C.phases = (int)phases.size();
   for (size_t k = 0; k < phases.size(); ++k) {
     const Phase& ph = phases[k];
-    barrier_for(phase_accesses(ph, base, bufsize, NC, T, max_idx, acc));
+    barrier_for(phase_accesses(ph, base, bufsize, LN, LT, max_idx, acc));
     if (ph.k == Phase::ZERO) {
       o << "    // phase " << k << ": zero " << ph.zname << "\n"
-        << "    for (int e = threadIdx.x; e < " << NC * ph.zsize << "; e += " << T << ") {\n";
-      if (NC > 1) o << "      const int c = e % " << NC << ", z = e / " << NC << ";\n";
+        << "    for (int e = " << TID << "; e < " << LN * ph.zsize << "; e += " << LT << ") {\n";
+      if (NC > 1) o << "      const int c = e % " << LN << ", z = e / " << LN << ";\n";
       else o << "      const int z = e;\n";
       o << "      " << slot(ph.zname, "z") << " = 0.0;\n    }\n";
     } else if (ph.k == Phase::SERIAL) {
       ++C.serial_phases;
       o << "    // phase " << k << ": serial nest (thread per cell)\n";
-      if (NC > 1) o << "    for (int c = threadIdx.x; c < " << NC << "; c += " << T << ") {\n";
+      if (NC > 1)
+        o << "    for (int c = " << TID << "; c < " << LN << "; c += " << LT << ") {\n";
       else o << "    if (threadIdx.x == 0) {\n";
       serial(*ph.top, 3);
       o << "    }\n";
@@ -838,8 +874,8 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
         << " (" << ph.npar << " parallel";
       if (E > 1) o << ", " << E << " per thread along " << bv;
       o << " x " << ph.red.size() << " reduction loops)\n"
-        << "    for (int w = threadIdx.x; w < " << NC * ph.nitem << "; w += " << T << ") {\n";
-      if (NC > 1) o << "      const int c = w % " << NC << ";\n      int q = w / " << NC << ";\n";
+        << "    for (int w = " << TID << "; w < " << LN * ph.nitem << "; w += " << LT << ") {\n";
+      if (NC > 1) o << "      const int c = w % " << LN << ";\n      int q = w / " << LN << ";\n";
       else o << "      int q = w;\n";
       for (size_t j = ph.opar.size(); j-- > 0;) {
         const auto& pr = ph.opar[j];
@@ -889,9 +925,9 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
   xfer_access(P.ret_size, base.at(P.ret_name), false);
   barrier_for(true);
   xfer_open(P.ret_size);
-  o << "      if (k < " << P.ret_size << " && c < nvalid) gA[(c0 + c) * " << P.ret_size << " + k] = "
-    << slot(P.ret_name, "k") << ";\n    }\n";
-  o << "    __syncthreads();\n  }\n}\n";
+  o << "      if (k < " << P.ret_size << " && " << CB << "c < nvalid) gA[(c0 + " << CB << "c) * "
+    << P.ret_size << " + k] = " << slot(P.ret_name, "k") << ";\n    }\n";
+  o << "    " << SYNC << ";\n  }\n}\n";
   G.source = o.str();
   return G;
 }

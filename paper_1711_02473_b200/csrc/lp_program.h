@@ -102,7 +102,9 @@ struct Config {
   int tables_in_smem = 1;
   int phases = 0;            // CTA-wide phases (after zero folding)
   int serial_phases = 0;     // phases executed thread-per-cell
-  int barriers = 0;
+  int barriers = 0;          // __syncthreads, or __syncwarp in warp mode
+  int warp_mode = 0;         // 1: every warp owns cells_per_warp whole cells
+  int cells_per_warp = 0;
 };
 
 struct Generated {

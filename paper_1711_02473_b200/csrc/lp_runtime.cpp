@@ -240,7 +240,8 @@ int sfk_program_config(const sfk_program* P, int64_t* out, int n) {
   if (!P || !out) return sfk::fail(SFK_EINVAL, "sfk_program_config: null argument");
   const auto& C = P->gen.cfg;
   const int64_t v[] = {C.cells_per_block, C.threads, C.slots, C.smem_bytes, C.global_scratch,
-                       C.phases, C.serial_phases, C.barriers, (int64_t)P->cubin.size()};
+                       C.phases, C.serial_phases, C.barriers, (int64_t)P->cubin.size(),
+                       C.warp_mode};
   for (int k = 0; k < n && k < (int)(sizeof v / sizeof v[0]); ++k) out[k] = v[k];
   return SFK_OK;
 }
