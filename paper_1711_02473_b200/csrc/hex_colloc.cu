@@ -66,7 +66,10 @@ __host__ __device__ constexpr int colloc_minb(int n) {
 // GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
 // item 1): u = x gathered through cmap[c][i] by per-element cp.async into the
 // padded u layout, A = y scatter-added with fp64 atomics at the write-back.
-template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS = false>
+// WARPS > 0: warp-synchronous mode for n <= 5 — each warp owns CPB whole
+// cells (CPB * n^2 <= 32 lines) in its own shared-memory slice and the
+// phases sync with __syncwarp instead of CTA barriers.
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS = false, int WARPS = 0>
 __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
                                             const double* __restrict__ coords,
                                             const double* __restrict__ u,
@@ -76,26 +79,30 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
   using C = CollocCfg<N, CPB, SY, SX, CS>;
   constexpr int NN = C::NN, N3 = C::N3;
   extern __shared__ double smem[];
-  double* sU = smem;
+  constexpr int TH = WARPS ? 32 : C::THREADS;
+  static_assert(!WARPS || CPB * NN <= 32, "warp mode needs CPB * n^2 <= 32");
+  const int grp = WARPS ? (int)(threadIdx.x >> 5) : 0;
+  double* sU = smem + (size_t)grp * (C::smem(WEIGHTED) / sizeof(double));
   double* sGX = sU + CPB * CS;
   double* sGY = sGX + CPB * CS;
   double* sC = sGY + CPB * CS;
   double* sK = sC + CPB * 24;   // kappa (WEIGHTED), same padded layout as U
 
-  const int tid = threadIdx.x;
-  const int64_t cell0 = (int64_t)blockIdx.x * CPB;
+  const int tid = WARPS ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+  auto sync = [] { if (WARPS) __syncwarp(); else __syncthreads(); };
+  const int64_t cell0 = ((int64_t)blockIdx.x * (WARPS ? WARPS : 1) + grp) * CPB;
   const int64_t rem = ncells - cell0;
   const int ncb = rem < CPB ? (int)rem : CPB;
 
   // u (group 0) and kappa (group 1) stream into the padded shared layouts
   // with cp.async; kappa is only needed by the pointwise phase, so its
   // latency hides behind phase 2.
-  for (int i = tid; i < CPB * 24; i += C::THREADS)
+  for (int i = tid; i < CPB * 24; i += TH)
     sC[i] = i < ncb * 24 ? __ldg(coords + cell0 * 24 + i) : 0.0;
   {
     // consecutive threads copy consecutive doubles (coalesced global reads)
     const double* ug = u + cell0 * N3;
-    for (int i = tid; i < ncb * N3; i += C::THREADS) {
+    for (int i = tid; i < ncb * N3; i += TH) {
       const int c = i / N3, r = i - c * N3;
       const int x = r / NN, yz = r - x * NN, y = yz / N, z = yz - y * N;
       cp_async8(sU + c * CS + x * SX + y * SY + z, GS ? u + __ldg(cmap + cell0 * N3 + i) : ug + i);
@@ -103,7 +110,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
     cp_async_commit();
     if (WEIGHTED) {
       const double* kg = kappa + cell0 * N3;
-      for (int i = tid; i < ncb * N3; i += C::THREADS) {
+      for (int i = tid; i < ncb * N3; i += TH) {
         const int c = i / N3, r = i - c * N3;
         const int x = r / NN, yz = r - x * NN, y = yz / N, z = yz - y * N;
         cp_async8(sK + c * CS + x * SX + y * SY + z, kg + i);
@@ -114,7 +121,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
       cp_async_wait<0>();
     }
   }
-  __syncthreads();
+  sync();
 
   const bool act = tid < CPB * NN;
   const int c = tid / NN, r = tid - (tid / NN) * NN;
@@ -144,7 +151,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
     }
   }
   if (WEIGHTED) cp_async_wait<0>();   // kappa copies of this thread landed
-  __syncthreads();                     // ... and everybody's are visible
+  sync();                     // ... and everybody's are visible
 
   // ---- phase 3: z-line (x=a, y=b): d_z u, flux, A_z = Dz^T f_z ---------
   if (act) {
@@ -184,7 +191,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
 #pragma unroll
     for (int i = 0; i < N; ++i) sU[base + i] = az[i];
   }
-  __syncthreads();
+  sync();
 
   // ---- phase 4: x-lines (y=a, z=b): U += Dx^T f_x ----------------------
   if (act) {
@@ -199,7 +206,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
       sU[cb + i * SX + a * SY + b] += s;
     }
   }
-  __syncthreads();
+  sync();
 
   // ---- phase 5: y-lines (x=a, z=b): U += Dy^T f_y ----------------------
   if (act) {
@@ -214,13 +221,13 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
       sU[cb + a * SX + i * SY + b] += s;
     }
   }
-  __syncthreads();
+  sync();
 
   {
     // coalesced write-back: consecutive threads take consecutive elements of
     // the batch; the (c, x, y, z) decomposition is incremental per thread
     double* ag = A + cell0 * N3;
-    for (int i = tid; i < ncb * N3; i += C::THREADS) {
+    for (int i = tid; i < ncb * N3; i += TH) {
       const int cc = i / N3, rr = i - cc * N3;
       const int x = rr / NN, yz = rr - x * NN, y = yz / N, z = yz - y * N;
       if (GS) atomicAdd(A + __ldg(cmap + cell0 * N3 + i), sU[cc * CS + x * SX + y * SY + z]);
@@ -229,36 +236,39 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
   }
 }
 
-template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, int MINB, bool GS>
-__global__ void __launch_bounds__(CollocCfg<N, CPB, SY, SX, CS>::THREADS, MINB)
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, int MINB, bool GS, int WARPS>
+__global__ void __launch_bounds__(WARPS ? 32 * WARPS : CollocCfg<N, CPB, SY, SX, CS>::THREADS, MINB)
 hex_colloc_action_kernel(const __grid_constant__ TabsD<N> T, int64_t ncells,
                          const double* __restrict__ coords, const double* __restrict__ u,
                          const double* __restrict__ kappa, double* __restrict__ A,
                          const int* __restrict__ cmap) {
-  colloc_body<N, CPB, SY, SX, CS, WEIGHTED, GS>(T, ncells, coords, u, kappa, A, cmap);
+  colloc_body<N, CPB, SY, SX, CS, WEIGHTED, GS, WARPS>(T, ncells, coords, u, kappa, A, cmap);
 }
 
-template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS>
-__global__ void __launch_bounds__(CollocCfg<N, CPB, SY, SX, CS>::THREADS)
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS, int WARPS>
+__global__ void __launch_bounds__(WARPS ? 32 * WARPS : CollocCfg<N, CPB, SY, SX, CS>::THREADS)
 hex_colloc_action_kernel_free(const __grid_constant__ TabsD<N> T, int64_t ncells,
                               const double* __restrict__ coords, const double* __restrict__ u,
                               const double* __restrict__ kappa, double* __restrict__ A,
                               const int* __restrict__ cmap) {
-  colloc_body<N, CPB, SY, SX, CS, WEIGHTED, GS>(T, ncells, coords, u, kappa, A, cmap);
+  colloc_body<N, CPB, SY, SX, CS, WEIGHTED, GS, WARPS>(T, ncells, coords, u, kappa, A, cmap);
 }
 
-template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS>
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS, int WARPS = 0>
 static auto colloc_kernel() {
   constexpr int mb = colloc_minb(N);
-  if constexpr (mb == 0) return hex_colloc_action_kernel_free<N, CPB, SY, SX, CS, WEIGHTED, GS>;
-  else return hex_colloc_action_kernel<N, CPB, SY, SX, CS, WEIGHTED, mb, GS>;
+  if constexpr (mb == 0)
+    return hex_colloc_action_kernel_free<N, CPB, SY, SX, CS, WEIGHTED, GS, WARPS>;
+  else return hex_colloc_action_kernel<N, CPB, SY, SX, CS, WEIGHTED, mb, GS, WARPS>;
 }
 
-template <int N, int CPB, int SY, int SX, int CS, bool GS = false>
+template <int N, int CPB, int SY, int SX, int CS, bool GS = false, int WARPS = 0>
 static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                     const double* u, const double* kappa, cudaStream_t s,
                     const int* cmap = nullptr) {
   using C = CollocCfg<N, CPB, SY, SX, CS>;
+  constexpr int G = WARPS ? WARPS : 1;                 // cell groups per CTA
+  constexpr int THREADS = WARPS ? 32 * WARPS : C::THREADS;
   TabsD<N> T;
   for (int i = 0; i < N * N; ++i) T.D[i] = p->D[i];
   for (int q = 0; q < N; ++q) {
@@ -266,22 +276,28 @@ static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* 
     T.Bc[q] = p->Bc[q];
     T.Bc[N + q] = p->Bc[N + q];
   }
-  const int64_t grid = (ncells + CPB - 1) / CPB;
+  const int64_t grid = (ncells + CPB * G - 1) / (CPB * G);
   cudaError_t e;
   if (kappa) {
-    auto k = colloc_kernel<N, CPB, SY, SX, CS, true, GS>();
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem(true));
+    auto k = colloc_kernel<N, CPB, SY, SX, CS, true, GS, WARPS>();
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(G * C::smem(true)));
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
-    k<<<(unsigned)grid, C::THREADS, C::smem(true), s>>>(T, ncells, coords, u, kappa, A, cmap);
+    k<<<(unsigned)grid, THREADS, G * C::smem(true), s>>>(T, ncells, coords, u, kappa, A, cmap);
   } else {
-    auto k = colloc_kernel<N, CPB, SY, SX, CS, false, GS>();
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem(false));
+    auto k = colloc_kernel<N, CPB, SY, SX, CS, false, GS, WARPS>();
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(G * C::smem(false)));
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
-    k<<<(unsigned)grid, C::THREADS, C::smem(false), s>>>(T, ncells, coords, u, nullptr, A, cmap);
+    k<<<(unsigned)grid, THREADS, G * C::smem(false), s>>>(T, ncells, coords, u, nullptr, A, cmap);
   }
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_colloc_action_kernel launch");
 }
+
+#ifndef SFK_COLLOC_WARPS_DEFAULT
+#define SFK_COLLOC_WARPS_DEFAULT 0   // warp mode measured slower at p = 4 (profiles/r01bd_c3_warps.jsonl)
+#endif
 
 // cells per CTA at n = 10, 12 (overridable for A/B builds)
 #ifndef SFK_COLLOC_CPB10
@@ -297,6 +313,20 @@ static int dispatch_colloc(const sfk_plan* p, int64_t ncells, double* A, const d
                            const int* cmap) {
   if (p->n != p->m)
     return fail(SFK_EINVAL, "collocated action needs n_q1d == n_dof1d (got %d, %d)", p->n, p->m);
+  // warp-synchronous variants for n <= 5 (SFK_COLLOC_WARPS = warps per CTA)
+  static const int cw = [] {
+    const char* e = std::getenv("SFK_COLLOC_WARPS");
+    return e ? std::atoi(e) : SFK_COLLOC_WARPS_DEFAULT;
+  }();
+  if (cw > 0) {
+    switch (p->n) {
+      case 2: return launch_n<2, 8, 2, 5, 12, GS, 8>(p, ncells, A, coords, w0, w1, s, cmap);
+      case 3: return launch_n<3, 3, 3, 9, 27, GS, 8>(p, ncells, A, coords, w0, w1, s, cmap);
+      case 4: return launch_n<4, 2, 4, 19, 76, GS, 8>(p, ncells, A, coords, w0, w1, s, cmap);
+      case 5: return launch_n<5, 1, 5, 25, 125, GS, 8>(p, ncells, A, coords, w0, w1, s, cmap);
+      default: break;
+    }
+  }
   // (N, cells/CTA, SY, SX, CS) from tools/smem_pads.py
   switch (p->n) {
     case 2: return launch_n<2, 16, 2, 5, 12, GS>(p, ncells, A, coords, w0, w1, s, cmap);
