@@ -345,3 +345,38 @@ def test_c2_every_kernel_generation(cuda, p):
         env = dict(os.environ, SFK_C2_KERNEL=gen)
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
         assert r.returncode == 0, (gen, r.stdout, r.stderr[-2000:])
+
+
+@pytest.mark.parametrize("mode", ["colloc_warps", "neo_cta"])
+def test_alternative_kernel_modes(cuda, mode):
+    """Kernel modes that are off by default for speed (C3's warp-synchronous
+    variant, SFK_COLLOC_WARPS) or on by default (C4's, SFK_NEO_WARPS=0 turns
+    it off) agree with the oracle too."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if mode == "colloc_warps":
+        env_var, degrees = {"SFK_COLLOC_WARPS": "8"}, (1, 2, 3, 4)
+        build = ("compile_form(action_form(REGISTRY['weighted_laplace']), 'hex', p, 'spectral',"
+                 " 'spectral_gll', 'collocated-gll')")
+        inputs = "workloads.c3_inputs(p, dims=(3, 5, 7))"
+    else:
+        env_var, degrees = {"SFK_NEO_WARPS": "0"}, (1, 2, 3)
+        build = "compile_form(neohookean_residual_form(), 'hex', p, quadrature=p + 2)"
+        inputs = "workloads.c4_inputs(p, dims=(3, 5, 7))"
+    code = (
+        "import numpy as np, torch, sys; sys.path.insert(0, %r);"
+        "from paper_1711_02473_b200 import *; from paper_1711_02473_b200 import workloads;"
+        "from oracle import cpu;"
+        "errs = []\n"
+        "for p in %r:\n"
+        "    plan = %s; inp = %s\n"
+        "    out = evaluate_batched(plan, {k: torch.from_numpy(v).cuda() for k, v in inp.items()}).cpu().numpy()\n"
+        "    ref = cpu.evaluate(plan, inp)\n"
+        "    errs.append((np.abs(out-ref).max(axis=1)/np.abs(ref).max(axis=1)).max())\n"
+        "print(errs); assert max(errs) < 1e-12"
+    ) % (root, degrees, build, inputs)
+    env = dict(os.environ, **env_var)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    assert r.returncode == 0, (mode, r.stdout, r.stderr[-2000:])
