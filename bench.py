@@ -435,11 +435,16 @@ def main():
                                        pc.data_ptr(), pinned[p][0].data_ptr(), None)
         if world > 1:
             dist.barrier()
+        # every degree's batch is enqueued on the library's staging streams
+        # (sfk_eval_host_async) so the 8 copy pipelines overlap; one wait per
+        # step, after which every result is in host memory
         t0 = time.perf_counter()
         for _ in range(K):
             for p in degs:
                 runtime.evaluate_host_ptrs(plans[p], ncells, pinned[p][1].data_ptr(),
-                                           pc.data_ptr(), pinned[p][0].data_ptr(), None)
+                                           pc.data_ptr(), pinned[p][0].data_ptr(), None,
+                                           wait=False)
+            runtime.host_wait()
         e2e_s = (time.perf_counter() - t0) / K
         if world > 1:
             tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -451,7 +456,8 @@ def main():
         line["e2e"] = {"value": round(total_dofs / e2e_s / 1e9, 4), "unit": "GDoF/s",
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                        "ms_per_step": round(e2e_s * 1e3, 3),
-                       "api": "sfk_eval_host (pinned host buffers)", "matches_device_path": ok}
+                       "api": "sfk_eval_host_async per degree + sfk_host_wait per step "
+                              "(pinned host buffers)", "matches_device_path": ok}
         del pinned
 
     # ---- CPU baseline: reference emitted C on the host cores (rank 0, N=1) ---

@@ -127,6 +127,19 @@ int sfk_eval_host(const sfk_plan *plan, int64_t ncells, double *A,
                   int64_t chunk_cells);
 
 /*
+ * The same, enqueued only: returns once every copy and kernel of the batch is
+ * queued on the library's per-device staging streams, so consecutive calls
+ * (e.g. one per degree) overlap their copy pipelines.  The host buffers must
+ * stay valid and untouched until sfk_host_wait() returns; results are in A
+ * only then.
+ */
+int sfk_eval_host_async(const sfk_plan *plan, int64_t ncells, double *A,
+                        const double *coords, const double *w0,
+                        const double *w1, int64_t chunk_cells);
+/* Wait for every sfk_eval_host_async call on the current device. */
+int sfk_host_wait(void);
+
+/*
  * Global (assembled) operator application, matrix-free:
  *     y += sum_c P_c^T A_c P_c x
  * P_c gathers the cell's local dofs from the global vector x through

@@ -123,8 +123,11 @@ static int dispatch(const sfk_plan* p, int64_t ncells, double* A,
 // created once and reused (the r01 version allocated them per call, which
 // cost milliseconds on small batches).  Calls on one device serialise on the
 // context mutex.
+#ifndef SFK_HOST_STREAMS
+#define SFK_HOST_STREAMS 8   // 8 > 4 > 2 streams for e2e (profiles/r01bf_e2e_streams.jsonl)
+#endif
 struct HostCtx {
-  static constexpr int NS = 4;
+  static constexpr int NS = SFK_HOST_STREAMS;
   std::mutex mu;
   bool init = false;
   cudaStream_t stream[NS] = {};
@@ -140,6 +143,11 @@ struct HostCtx {
       init = true;
     }
     if (bytes <= cap) return SFK_OK;
+    // growing: earlier (possibly asynchronous) calls may still use the buffers
+    for (int i = 0; i < NS; ++i) {
+      int rc = cuda_status(cudaStreamSynchronize(stream[i]), "cudaStreamSynchronize(eval_host)");
+      if (rc != SFK_OK) return rc;
+    }
     for (int i = 0; i < NS; ++i) {
       if (buf[i]) cudaFree(buf[i]);
       buf[i] = nullptr;
@@ -279,8 +287,8 @@ int sfk_eval_pair(const sfk_plan* p0, const sfk_plan* p1, int64_t ncells, double
   return dispatch(p1, ncells, A1, coords, w0, nullptr, s);
 }
 
-int sfk_eval_host(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                  const double* w0, const double* w1, int64_t chunk) {
+static int eval_host_impl(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                          const double* w0, const double* w1, int64_t chunk, bool wait) {
   int st = validate(p, ncells, A, coords, w0, w1);
   if (st != SFK_OK || ncells == 0) return st;
   const int64_t per_cell = p->coords_size + p->w0_size + p->w1_size + p->a_size;
@@ -325,9 +333,35 @@ int sfk_eval_host(const sfk_plan* p, int64_t ncells, double* A, const double* co
       rc = cuda_status(cudaMemcpyAsync(A + c0 * p->a_size, dA, nc * p->a_size * sizeof(double),
                                        cudaMemcpyDeviceToHost, s), "D2H A");
   }
+  if (!wait && rc == SFK_OK) return SFK_OK;
   for (int i = 0; i < HostCtx::NS; ++i) {
     cudaError_t e = cudaStreamSynchronize(ctx->stream[i]);
     if (rc == SFK_OK) rc = cuda_status(e, "cudaStreamSynchronize(eval_host)");
+  }
+  return rc;
+}
+
+int sfk_eval_host(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                  const double* w0, const double* w1, int64_t chunk) {
+  return eval_host_impl(p, ncells, A, coords, w0, w1, chunk, true);
+}
+
+int sfk_eval_host_async(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                        const double* w0, const double* w1, int64_t chunk) {
+  return eval_host_impl(p, ncells, A, coords, w0, w1, chunk, false);
+}
+
+int sfk_host_wait(void) {
+  int dev = 0;
+  int rc = cuda_status(cudaGetDevice(&dev), "cudaGetDevice");
+  if (rc != SFK_OK) return rc;
+  HostCtx* ctx = host_ctx(dev);
+  if (!ctx) return fail(SFK_EINVAL, "device %d out of range", dev);
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  if (!ctx->init) return SFK_OK;
+  for (int i = 0; i < HostCtx::NS; ++i) {
+    cudaError_t e = cudaStreamSynchronize(ctx->stream[i]);
+    if (rc == SFK_OK) rc = cuda_status(e, "cudaStreamSynchronize(host_wait)");
   }
   return rc;
 }

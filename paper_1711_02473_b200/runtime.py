@@ -41,7 +41,7 @@ EXPORTED_SYMBOLS = (
     "sfk_eval_gather_scatter", "sfk_program_create", "sfk_program_destroy",
     "sfk_program_sizes", "sfk_program_config", "sfk_program_text", "sfk_program_eval",
     "sfk_csr_create", "sfk_csr_info", "sfk_csr_destroy", "sfk_assemble_csr",
-    "sfk_csr_entry_map", "sfk_eval_global",
+    "sfk_csr_entry_map", "sfk_eval_global", "sfk_eval_host_async", "sfk_host_wait",
 )
 ABI_VERSION = 1
 SUM_WORKSPACE = 1024
@@ -83,6 +83,10 @@ def _declare(lib):
     if hasattr(lib, "sfk_eval_gather_scatter"):   # absent from pre-(f) A/B builds
         lib.sfk_eval_gather_scatter.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, _vp]
         lib.sfk_eval_gather_scatter.restype = ci
+    if hasattr(lib, "sfk_eval_host_async"):
+        lib.sfk_eval_host_async.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, i64]
+        lib.sfk_eval_host_async.restype = ci
+        lib.sfk_host_wait.restype = ci
     if hasattr(lib, "sfk_eval_global"):
         lib.sfk_eval_global.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, _vp, _vp]
         lib.sfk_eval_global.restype = ci
@@ -293,10 +297,18 @@ def evaluate_host(plan, inputs, out=None, chunk_cells=0):
     return out.reshape(rsize) if squeeze else out
 
 
-def evaluate_host_ptrs(plan, ncells, a_ptr, coords_ptr, w0_ptr, w1_ptr, chunk_cells=0):
-    """Raw-pointer host evaluation (pinned torch tensors from the bench)."""
-    _check(load_library().sfk_eval_host(native_plan(plan), ncells, a_ptr, coords_ptr,
-                                        w0_ptr, w1_ptr, int(chunk_cells)))
+def evaluate_host_ptrs(plan, ncells, a_ptr, coords_ptr, w0_ptr, w1_ptr, chunk_cells=0,
+                       wait=True):
+    """Raw-pointer host evaluation (pinned torch tensors from the bench).
+    wait=False only enqueues (sfk_eval_host_async): call host_wait() before
+    touching the buffers."""
+    fn = load_library().sfk_eval_host if wait else load_library().sfk_eval_host_async
+    _check(fn(native_plan(plan), ncells, a_ptr, coords_ptr, w0_ptr, w1_ptr, int(chunk_cells)))
+
+
+def host_wait():
+    """Wait for every evaluate_host_ptrs(..., wait=False) on the current device."""
+    _check(load_library().sfk_host_wait())
 
 
 def sum_squares(x, workspace=None, stream=None):

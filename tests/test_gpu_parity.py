@@ -15,7 +15,7 @@ import pytest
 from conftest import GOLDEN, rel_err
 from oracle import cpu
 from paper_1711_02473_b200 import (compile_kernel, evaluate_batched, evaluate_host,
-                                   launch_count, sum_squares, workloads)
+                                   launch_count, runtime, sum_squares, workloads)
 from paper_1711_02473_b200.errors import ShapeMismatch, UnboundVariable
 
 pytestmark = pytest.mark.gpu
@@ -380,3 +380,24 @@ def test_alternative_kernel_modes(cuda, mode):
     env = dict(os.environ, **env_var)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     assert r.returncode == 0, (mode, r.stdout, r.stderr[-2000:])
+
+
+def test_host_async_overlapping_calls(cuda):
+    """sfk_eval_host_async for several degrees back to back (staging buffers
+    grow mid-sequence), one sfk_host_wait: every result equals the device
+    path bit for bit."""
+    torch = cuda
+    degs = (1, 3, 2, 5, 4)
+    coords = torch.from_numpy(workloads.lattice_coords(9, 10, 11)).pin_memory()
+    res = {}
+    for p in degs:
+        plan = compile_kernel("action_laplace", "hex", p)
+        u = torch.from_numpy(workloads.uniform_dofs(coords.shape[0], (p + 1) ** 3)).pin_memory()
+        a = torch.empty_like(u).pin_memory()
+        runtime.evaluate_host_ptrs(plan, coords.shape[0], a.data_ptr(), coords.data_ptr(),
+                                   u.data_ptr(), None, chunk_cells=97, wait=False)
+        res[p] = (plan, u, a)
+    runtime.host_wait()
+    for p, (plan, u, a) in res.items():
+        dev = evaluate_batched(plan, {"coords": coords.cuda(), "w0": u.cuda()}).cpu()
+        assert torch.equal(a, dev), p
