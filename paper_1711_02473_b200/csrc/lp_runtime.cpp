@@ -32,7 +32,10 @@ struct sfk_program {
     CUfunction fn = nullptr;
     int blocks = 0;  // persistent grid size
   };
-  std::vector<PerDevice> dev;
+  // fixed storage: pointers handed out by module_for stay valid while other
+  // threads load the module on further devices
+  static constexpr int kMaxDevices = 64;
+  PerDevice dev[kMaxDevices];
 };
 
 namespace {
@@ -156,8 +159,9 @@ int compile(sfk_program* P) {
 }
 
 int module_for(sfk_program* P, int dev, sfk_program::PerDevice** out) {
+  if (dev < 0 || dev >= sfk_program::kMaxDevices)
+    return sfk::fail(SFK_EINVAL, "device %d out of range", dev);
   std::lock_guard<std::mutex> lk(P->mu);
-  if ((int)P->dev.size() <= dev) P->dev.resize(dev + 1);
   sfk_program::PerDevice& d = P->dev[dev];
   if (!d.fn) {
     if (P->cubin.empty()) return sfk::fail(SFK_EUNSUPPORTED, "program was created without JIT");
