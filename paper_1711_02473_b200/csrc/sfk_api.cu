@@ -68,7 +68,7 @@ static int c2_auto(int n) {
     case 4: return 6;
     case 5: return 3;
     case 6: return 2;
-    case 7: return 3;
+    case 7: return 2;   // v2 1.705 vs v3 1.751 ms (profiles/r01bg_c2_generations.jsonl)
     case 8: return 4;
     case 9: return 2;
     default: return 1;
