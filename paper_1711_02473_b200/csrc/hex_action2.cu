@@ -487,6 +487,7 @@ int launch_hex_action_v2_gs(const sfk_plan* p, int64_t ncells, const int* cmap, 
   switch (p->n) {
     case 4: return launch_v2<4, 4, 16, 1, 2, 1, true>(p, ncells, y, coords, x, s, cmap);
     case 6: return launch_v2<6, 6, 8, 1, 2, 1, true>(p, ncells, y, coords, x, s, cmap);
+    case 7: return launch_v2<7, 7, 5, 1, 2, 1, true>(p, ncells, y, coords, x, s, cmap);
     case 9: return launch_v2<9, 9, 3, 1, 2, 1, true>(p, ncells, y, coords, x, s, cmap);
     default: return SFK_EUNSUPPORTED;
   }

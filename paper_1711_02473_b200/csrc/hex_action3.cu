@@ -371,7 +371,7 @@ static bool force_v3_small() {
 }
 
 // Same generation as the E-vector action per degree (sfk_api.cu c2_auto):
-// p = 1 cell kernel, p = 2, 3 v4, p = 5, 8 v2, p = 7 DMMA, the rest v3.
+// p = 1 cell kernel, p = 2, 3 v4, p = 5, 6, 8 v2, p = 7 DMMA, p = 4 v3.
 // SFK_C2G_KERNEL=v3 forces v3 (A/B runs).
 int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                          double* y, const double* coords, cudaStream_t s) {
@@ -384,7 +384,7 @@ int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, con
       return launch_hex_action_p1_gs(p, ncells, cmap, x, y, coords, s);
     if ((p->n == 3 || p->n == 4) && !force_v3_small())
       return launch_hex_action_v4_gs(p, ncells, cmap, x, y, coords, s);
-    if (p->n == 6 || p->n == 9 || (p->n == 4 && force_v3_small()))
+    if (p->n == 6 || p->n == 7 || p->n == 9 || (p->n == 4 && force_v3_small()))
       return launch_hex_action_v2_gs(p, ncells, cmap, x, y, coords, s);
     if (p->n == 8) return launch_hex_action_tc_gs(p, ncells, cmap, x, y, coords, s);
   }
