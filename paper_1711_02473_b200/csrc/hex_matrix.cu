@@ -77,7 +77,7 @@ __device__ __forceinline__ int64_t csr_find(const int32_t* __restrict__ col_idx,
 // CSR = true : the cell matrices are scatter-added into the assembled CSR
 //              matrix (values A, pattern row_ptr / col_idx from sfk_csr_create)
 //              through cell_dofs — the local matrix never reaches HBM.
-template <int N, int M, int CPB, bool CSR>
+template <int N, int M, int CPB, bool CSR, bool YMAP = false>
 __global__ void __launch_bounds__(MatCfg<N, M, CPB>::THREADS)
 hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncells,
                           const double* __restrict__ coords, double* __restrict__ A,
@@ -107,7 +107,14 @@ hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncell
   // thread -> (cell, iy, iz, jy, jz)
   const bool act = tid < CPB * N4;
   const int c = act ? tid / N4 : 0, r = tid - c * N4;
-  const int iy = r / (N * N2), iz = (r / N2) % N, jy = (r / N) % N, jz = r % N;
+  // YMAP: (jy, iy) fastest, so the lanes of a warp share (iz, jz) and the
+  // Y-stage Z loads are broadcasts — faster at n = 4, slower at n = 3, 5
+  // where the less contiguous output stores cost more (A/B:
+  // profiles/r01bh_c5_ymap.jsonl)
+  const int iy = YMAP ? (r / N) % N : r / (N * N2);
+  const int iz = YMAP ? r / (N * N2) : (r / N2) % N;
+  const int jy = YMAP ? r % N : (r / N) % N;
+  const int jz = YMAP ? (r / N2) % N : r % N;
   __syncthreads();
 
   // ---- K at every point: threads over (cell, qx, qy, qz) -------------------
@@ -237,7 +244,7 @@ hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncell
   }
 }
 
-template <int N, int M, int CPB, bool CSR = false>
+template <int N, int M, int CPB, bool CSR = false, bool YMAP = false>
 static int launch_mat(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                       cudaStream_t s, const int32_t* dofs = nullptr,
                       const int64_t* row_ptr = nullptr, const int32_t* col_idx = nullptr,
@@ -255,7 +262,7 @@ static int launch_mat(const sfk_plan* p, int64_t ncells, double* A, const double
     T.Bc[M + q] = p->Bc[p->m + q];
   }
   const unsigned grid = (unsigned)((ncells + CPB - 1) / CPB);
-  auto kern = hex_laplace_matrix_kernel<N, M, CPB, CSR>;
+  auto kern = hex_laplace_matrix_kernel<N, M, CPB, CSR, YMAP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)C::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_matrix)");
@@ -281,7 +288,7 @@ int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double
         return launch_mat<2, 2, 16>(p, ncells, A, coords, s);
       }
       case 3: return launch_mat<3, 3, 3>(p, ncells, A, coords, s);
-      case 4: return launch_mat<4, 4, 1>(p, ncells, A, coords, s);
+      case 4: return launch_mat<4, 4, 1, false, true>(p, ncells, A, coords, s);
       case 5: return launch_mat<5, 5, 1>(p, ncells, A, coords, s);
       default: break;
     }
