@@ -1,0 +1,227 @@
+// Hex Q_3 local stiffness matrices on the FP64 tensor cores — BASELINE C5
+// at p = 3 (n = m = 4).
+//
+// Same math and reference mapping as hex_matrix.cu (registry `laplace` on
+// `hex`, forms.py:186-189; test index outermost A[i*64 + j], forms.py:402-408),
+// same K and Z phases.  The two phases that carry the work are recast as
+// small GEMMs with a CONSTANT left operand, so they run as DMMA
+// (mma.sync.m8n8k4.f64) with the A fragments held in registers for the whole
+// kernel:
+//   Y stage  Y_g[qx][(iy,jy),(iz,jz)] = sum_{(l,l') in g, qy}
+//              P_g[(iy,jy)][(l,l'),qy] * Z_ll'[qx][qy][(iz,jz)],
+//            P_g[(iy,jy)][(l,l'),qy] = T^l_y[iy][qy] T^l'_y[jy][qy]
+//            (16 x K_g with K_g = 4 |g| in {4, 8, 8, 16}: one k-step per pair);
+//   x stage  A[(ix,jx)][r] = sum_{g,qx} W[(ix,jx)][(g,qx)] * Y_g[qx][r],
+//            W[(ix,jx)][(g,qx)] = T^g_x,test[ix][qx] T^g_x,trial[jx][qx]
+//            (16 x 16 constant, 256 columns r = (iy,iz,jy,jz) per cell).
+// At n = 4 every tile dimension is a multiple of the m8n8k4 shape: no
+// padding.  The FMA version of this kernel was shared-memory-issue bound in
+// its Y stage (profiles/r01al_C5_p4.md: MIO throttle 25%).
+#include "hex_geometry.cuh"
+
+namespace sfk {
+
+struct TabsMat4 {
+  double B[16], D[16], W[4], Bc[8];
+};
+
+namespace m4 {
+constexpr int N = 4, M = 4, N2 = 16, N3 = 64, N4 = 256, M3 = 64;
+constexpr int THREADS = 256, WARPS = 8;
+constexpr int KS = 6 * M3;              // K (6 unique entries) at every point
+constexpr int ZR = 20;                  // Z row stride (16 used; = 4 mod 16: conflict-free B loads)
+constexpr int ZS = 9 * M * M * ZR;      // Z[pair][qx*M + qy][ZR]
+constexpr int YR = 260;                 // Y row stride (256 used; = 4 mod 16)
+constexpr int YS = 4 * M * YR;          // Y[(g*M + qx)][YR]
+constexpr size_t SMEM = (size_t)(KS + ZS + YS + 24) * sizeof(double);
+}  // namespace m4
+
+__device__ __forceinline__ void dmma4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// pairs (l, l') (index 3l + l') of x-pattern group g = (l == 0) * 2 + (l' == 0)
+__device__ __forceinline__ int group_pair(int g, int s) {
+  // g = 0: (1,1) (1,2) (2,1) (2,2); g = 1: (1,0) (2,0); g = 2: (0,1) (0,2); g = 3: (0,0)
+  return g == 0 ? (s == 0 ? 4 : s == 1 ? 5 : s == 2 ? 7 : 8)
+       : g == 1 ? (s == 0 ? 3 : 6) : g == 2 ? (s == 0 ? 1 : 2) : 0;
+}
+__device__ __forceinline__ int group_size(int g) { return g == 0 ? 4 : g == 3 ? 1 : 2; }
+
+__host__ __device__ constexpr int ksym4(int l, int r) {
+  return l == r ? l : (l + r == 1 ? 3 : (l + r == 2 ? 4 : 5));
+}
+
+// Persistent CTAs, one cell per iteration; the constant A fragments of the
+// three DMMA stages are built once per CTA.
+__global__ void __launch_bounds__(m4::THREADS, 3)
+hex_laplace_matrix_tc4(const __grid_constant__ TabsMat4 T, int64_t ncells,
+                       const double* __restrict__ coords, double* __restrict__ A) {
+  using namespace m4;
+  extern __shared__ __align__(16) double smem[];
+  double* sY = smem;                 // [16][YR]   (16-byte aligned rows)
+  double* sZ = sY + YS;              // [9][M*M][ZR]
+  double* sK = sZ + ZS;              // [6][M3]  (point index (qx*M + qy)*M + qz)
+  double* sC = sK + KS;              // [24]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, kq = lane & 3;
+
+  // --- constant A fragments -------------------------------------------------
+  // Y stage: warp = (group g, row tile rt); P_g[(iy,jy)][(pair s, qy = kq)]
+  const int yg = warp >> 1, yrt = warp & 1, ynp = group_size(yg);
+  double pa[4];
+  {
+    const int row = yrt * 8 + gq, iy = row / N, jy = row % N;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int pr = group_pair(yg, s < ynp ? s : 0), l = pr / 3, lp = pr % 3;
+      pa[s] = (l == 1 ? T.D : T.B)[iy * M + kq] * (lp == 1 ? T.D : T.B)[jy * M + kq];
+    }
+  }
+  // x stage: W[(ix,jx)][(g = s, qx = kq)], row tile = warp & 1
+  double wa[4];
+  {
+    const int row = (warp & 1) * 8 + gq, ix = row / N, jx = row % N;
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      wa[s] = ((s & 2) ? T.D : T.B)[ix * M + kq] * ((s & 1) ? T.D : T.B)[jx * M + kq];
+  }
+
+  // K at every point of `cell` (threads < M3): reads sC, writes sK
+  auto k_phase = [&](int64_t cell) {
+    if (tid < M3 && cell < ncells) {
+      const int qx = tid / (M * M), qy = (tid / M) % M, qz = tid % M;
+      HexLineGeom geo;
+      geo.setup(sC, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
+      double r0[3], r1[3], r2[3];
+      const double det = geo.adj(T.Bc[qz], T.Bc[M + qz], r0, r1, r2);
+      const double s = ((T.W[qx] * T.W[qy]) * T.W[qz]) * rcp64(fabs(det));
+      const double* rows[3] = {r0, r1, r2};
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int m2 = l; m2 < 3; ++m2) {
+          const double* a = rows[l];
+          const double* b = rows[m2];
+          sK[ksym4(l, m2) * M3 + tid] = s * fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0]));
+        }
+    }
+  };
+
+  // Software pipeline, 3 barriers per cell: the next cell's coords load during
+  // this cell's Y stage and its K phase runs beside this cell's x stage (they
+  // touch disjoint shared arrays).
+  int64_t cell = blockIdx.x;
+  if (cell < ncells && tid < 24) sC[tid] = __ldg(coords + cell * 24 + tid);
+  __syncthreads();
+  k_phase(cell);
+  __syncthreads();
+  for (; cell < ncells; cell += gridDim.x) {
+    const int64_t next = cell + gridDim.x;
+
+    // ---- Z stage (DMMA): Z_pair[(iz,jz)][(qx,qy)] = TT_pair (16 x 4) * K (4 x 16)
+    //      tiles (pair, rt, ct): 36 over 8 warps
+    for (int t = warp; t < 36; t += WARPS) {
+      const int pair = t >> 2, rt = (t >> 1) & 1, ct = t & 1;
+      const int l = pair / 3, lp = pair % 3;
+      const int zz = rt * 8 + gq, iz = zz / N, jz = zz % N;
+      const double a = (l == 2 ? T.D : T.B)[iz * M + kq] * (lp == 2 ? T.D : T.B)[jz * M + kq];
+      const double b = sK[ksym4(l, lp) * M3 + (ct * 8 + gq) * M + kq];
+      double d0 = 0.0, d1 = 0.0;
+      dmma4(d0, d1, a, b);
+      // D: row zz = rt*8 + gq, cols qxy = ct*8 + 2kq, +1
+      const int qxy = ct * 8 + 2 * kq;
+      sZ[(pair * M * M + qxy) * ZR + zz] = d0;
+      sZ[(pair * M * M + qxy + 1) * ZR + zz] = d1;
+    }
+    __syncthreads();
+
+    // ---- Y stage (DMMA); the next cell's coords land meanwhile ----------------
+    if (next < ncells && tid >= THREADS - 24) sC[tid - (THREADS - 24)] =
+        __ldg(coords + next * 24 + (tid - (THREADS - 24)));
+#pragma unroll 1
+    for (int qx = 0; qx < M; ++qx) {
+#pragma unroll
+      for (int ct = 0; ct < 2; ++ct) {
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          if (s < ynp) {
+            const int pr = group_pair(yg, s);
+            dmma4(d0, d1, pa[s], sZ[(pr * M * M + qx * M + kq) * ZR + ct * 8 + gq]);
+          }
+        }
+        // D: rows (iy, jy) = rt*8 + gq, cols (iz, jz) = ct*8 + 2kq, +1
+        const int oiy = (yrt * 8 + gq) / N, ojy = (yrt * 8 + gq) % N;
+        const int col = ct * 8 + 2 * kq, iz = col / N, jz = col % N;
+        const int r = ((oiy * N + iz) * N + ojy) * N + jz;
+        *reinterpret_cast<double2*>(sY + (yg * M + qx) * YR + r) = make_double2(d0, d1);
+      }
+    }
+    __syncthreads();
+
+    // ---- x stage (DMMA): A[(ix,jx)][r] = W (16 x 16) * Y (16 x 256); then the
+    //      next cell's K (disjoint arrays) ------------------------------------
+    {
+      const int rt = warp & 1;
+      double* out = A + cell * (int64_t)(N3 * N3);
+#pragma unroll 2
+      for (int j = 0; j < 8; ++j) {
+        const int ct = (warp >> 1) + 4 * j;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) dmma4(d0, d1, wa[s], sY[(s * M + kq) * YR + ct * 8 + gq]);
+        const int oix = (rt * 8 + gq) / N, ojx = (rt * 8 + gq) % N;
+        const int r = ct * 8 + 2 * kq;
+        const int iy = r / (N * N2), iz = (r / N2) % N, jy = (r / N) % N, jz = r % N;
+        double* ap = out + (int64_t)(oix * N2 + iy * N + iz) * N3 + ojx * N2 + jy * N + jz;
+        *reinterpret_cast<double2*>(ap) = make_double2(d0, d1);
+      }
+    }
+    k_phase(next);
+    __syncthreads();
+  }
+}
+
+int launch_hex_matrix_tc4(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                          cudaStream_t s) {
+  if (p->n != 4 || p->m != 4 || p->collocated) return SFK_EUNSUPPORTED;
+  if ((reinterpret_cast<uintptr_t>(A) & 15) != 0) return SFK_EUNSUPPORTED;   // double2 stores
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(hex_laplace_matrix_tc4,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)m4::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_matrix_tc4)");
+    configured = true;
+  }
+  TabsMat4 T;
+  for (int i = 0; i < 16; ++i) {
+    T.B[i] = p->B[i];
+    T.D[i] = p->D[i];
+  }
+  for (int q = 0; q < 4; ++q) {
+    T.W[q] = p->wq[q];
+    T.Bc[q] = p->Bc[q];
+    T.Bc[4 + q] = p->Bc[4 + q];
+  }
+  static int sms = 0, per_sm = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, hex_laplace_matrix_tc4, m4::THREADS, m4::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "occupancy(hex_matrix_tc4)");
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t resident = (int64_t)sms * per_sm;
+  const unsigned grid = (unsigned)(ncells < resident ? ncells : resident);
+  hex_laplace_matrix_tc4<<<grid, m4::THREADS, m4::SMEM, s>>>(T, ncells, coords, A);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "hex_laplace_matrix_tc4 launch");
+}
+
+}  // namespace sfk

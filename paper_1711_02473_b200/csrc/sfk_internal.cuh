@@ -96,6 +96,8 @@ int launch_quad_action(const sfk_plan* p0, const sfk_plan* p1, int64_t ncells,
                        const double* w0, cudaStream_t s);
 int launch_hex_matrix_p1(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          cudaStream_t s);
+int launch_hex_matrix_tc4(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                          cudaStream_t s);
 int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A,
                       const double* coords, cudaStream_t s);
 int launch_hex_matrix_csr(const sfk_plan* p, int64_t ncells, const int32_t* dofs,
