@@ -300,7 +300,18 @@ int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double
         }
         return launch_mat<4, 4, 1, false, true>(p, ncells, A, coords, s);
       }
-      case 5: return launch_mat<5, 5, 1>(p, ncells, A, coords, s);
+      case 5: {
+        // DMMA kernel (hex_matrix_tc.cu); SFK_C5_P4=phase selects the FMA one
+        static const bool phase = [] {
+          const char* e = std::getenv("SFK_C5_P4");
+          return e && e[0] == 'p';
+        }();
+        if (!phase) {
+          const int rc = launch_hex_matrix_tc5(p, ncells, A, coords, s);
+          if (rc != SFK_EUNSUPPORTED) return rc;
+        }
+        return launch_mat<5, 5, 1>(p, ncells, A, coords, s);
+      }
       default: break;
     }
   }

@@ -225,3 +225,237 @@ int launch_hex_matrix_tc4(const sfk_plan* p, int64_t ncells, double* A, const do
 }
 
 }  // namespace sfk
+
+// ===========================================================================
+// p = 4 (n = m = 5): the same three DMMA stages with zero padding
+// (rows / columns 25 -> 32, K = 5|g| -> multiples of 4; the x stage's K =
+// 4 groups x 5 planes = 20 is exact).  Padded A entries are 0; padded B
+// entries read zero-initialised shared memory, so no NaN can leak in.
+namespace sfk {
+
+namespace m5 {
+constexpr int N = 5, M = 5, N2 = 25, N3 = 125, N4 = 625, M3 = 125;
+constexpr int THREADS = 512, WARPS = 16;
+constexpr int KS = 6 * M3;
+constexpr int ZR = 36;                  // Z row stride (32 read, 25 written; = 4 mod 16)
+constexpr int ZS = 9 * M * M * ZR;      // Z[pair][qx*M + qy][ZR]
+constexpr int YR = 644;                 // Y row stride (632 read, 625 written; = 4 mod 16)
+constexpr int YS = 4 * M * YR;          // Y[(g*M + qx)][YR]
+constexpr size_t SMEM = (size_t)(YS + ZS + KS + 24) * sizeof(double);
+}  // namespace m5
+
+struct TabsMat5 {
+  double B[25], D[25], W[5], Bc[10];
+};
+
+__global__ void __launch_bounds__(m5::THREADS, 1)
+hex_laplace_matrix_tc5(const __grid_constant__ TabsMat5 T, int64_t ncells,
+                       const double* __restrict__ coords, double* __restrict__ A) {
+  using namespace m5;
+  extern __shared__ __align__(16) double smem[];
+  double* sY = smem;                 // [20][YR]
+  double* sZ = sY + YS;              // [9][M*M][ZR]
+  double* sK = sZ + ZS;              // [6][M3]
+  double* sC = sK + KS;              // [24]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, kq = lane & 3;
+
+  // padding of Y and Z stays zero: clear everything once
+  for (int i = tid; i < YS + ZS; i += THREADS) smem[i] = 0.0;
+
+  auto k_phase = [&](int64_t cell) {
+    if (tid < M3 && cell < ncells) {
+      const int qx = tid / (M * M), qy = (tid / M) % M, qz = tid % M;
+      HexLineGeom geo;
+      geo.setup(sC, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
+      double r0[3], r1[3], r2[3];
+      const double det = geo.adj(T.Bc[qz], T.Bc[M + qz], r0, r1, r2);
+      const double s = ((T.W[qx] * T.W[qy]) * T.W[qz]) * rcp64(fabs(det));
+      const double* rows[3] = {r0, r1, r2};
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int m2 = l; m2 < 3; ++m2) {
+          const double* a = rows[l];
+          const double* b = rows[m2];
+          sK[ksym4(l, m2) * M3 + tid] = s * fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0]));
+        }
+    }
+  };
+
+  // x-stage A fragments: row tile xrt = warp & 3, W[(ix,jx)][k = (g, qx)] (k = 4s + kq)
+  const int xrt = warp & 3;
+  double wa[5];
+  {
+    const int row = xrt * 8 + gq, ix = row / N, jx = row % N;
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const int k = 4 * s + kq, g = k / M, qx = k % M;
+      wa[s] = row < N2 ? ((g & 2) ? T.D : T.B)[ix * M + qx] * ((g & 1) ? T.D : T.B)[jx * M + qx]
+                       : 0.0;
+    }
+  }
+
+  // Z-stage tiles of this warp: (pair = j, rt = (warp >> 2) & 3, ct = warp & 3)
+  const int zrt = (warp >> 2) & 3, zct = warp & 3;
+  double za[9][2];
+  {
+    const int zz = zrt * 8 + gq, iz = zz / N, jz = zz % N;
+#pragma unroll
+    for (int pair = 0; pair < 9; ++pair)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int qz = 4 * s + kq, l = pair / 3, lp = pair % 3;
+        za[pair][s] = (zz < N2 && qz < M)
+            ? (l == 2 ? T.D : T.B)[iz * M + qz] * (lp == 2 ? T.D : T.B)[jz * M + qz] : 0.0;
+      }
+  }
+  // Y-stage unit of this warp: (g = warp >> 2, rt = warp & 3)
+  const int yg = warp >> 2, yrt = warp & 3, ynp = group_size(yg), ykg = 5 * ynp;
+  const int ynks = (ykg + 3) / 4;
+  double pa[5];
+  int prow[5];   // sZ row offset (pair * 25 + qy) of each k-step's B fragment
+  {
+    const int row = yrt * 8 + gq, iy = row / N, jy = row % N;
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const int k = 4 * s + kq, sp = k / M, qy = k % M;
+      const int pr = group_pair(yg, sp < ynp ? sp : 0);
+      double v = 0.0;
+      if (row < N2 && k < ykg) {
+        const int l = pr / 3, lp = pr % 3;
+        v = (l == 1 ? T.D : T.B)[iy * M + qy] * (lp == 1 ? T.D : T.B)[jy * M + qy];
+      }
+      pa[s] = v;
+      prow[s] = pr * M * M + qy;
+    }
+  }
+
+  int64_t cell = blockIdx.x;
+  if (cell < ncells && tid < 24) sC[tid] = __ldg(coords + cell * 24 + tid);
+  __syncthreads();
+  k_phase(cell);
+  __syncthreads();
+  for (; cell < ncells; cell += gridDim.x) {
+    const int64_t next = cell + gridDim.x;
+
+    // ---- Z stage: Z_pair[(iz,jz)][(qx,qy)] = TT (32 x 8) * K (8 x 32) ----------
+    //      this warp: tiles (pair 0..8, zrt, zct), 2 k-steps each (unrolled:
+    //      the za fragments stay in registers)
+#pragma unroll
+    for (int pair = 0; pair < 9; ++pair) {
+      const int l = pair / 3, lp = pair % 3;
+      const int zz = zrt * 8 + gq, rt = zrt, ct = zct;
+      const int qxy = ct * 8 + gq;                       // B column
+      const double* kp = sK + ksym4(l, lp) * M3 + qxy * M;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int qz = 4 * s + kq;
+        const double b = (qxy < N2 && qz < M) ? kp[qz] : 0.0;
+        dmma4(d0, d1, za[pair][s], b);
+      }
+      (void)rt;
+      if (zz < N2) {
+        const int c0 = ct * 8 + 2 * kq;                  // D columns c0, c0 + 1 = (qx,qy)
+        if (c0 < N2) sZ[(pair * M * M + c0) * ZR + zz] = d0;
+        if (c0 + 1 < N2) sZ[(pair * M * M + c0 + 1) * ZR + zz] = d1;
+      }
+    }
+    __syncthreads();
+
+    // ---- Y stage: per (g, qx), Y = P_g (32 x K_g) * Zcat (K_g x 32) ----------
+    //      units (g, rt 0..3): 16 over 16 warps; loops qx x ct
+    if (next < ncells && tid >= THREADS - 24) sC[tid - (THREADS - 24)] =
+        __ldg(coords + next * 24 + (tid - (THREADS - 24)));
+    {
+      const int g = yg, row = yrt * 8 + gq, iy = row / N, jy = row % N;
+#pragma unroll 1
+      for (int qx = 0; qx < M; ++qx) {
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct) {
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int s = 0; s < 5; ++s) {
+            // padded k rows: A is 0 there and prow points at a valid (finite) row
+            if (s < ynks) dmma4(d0, d1, pa[s], sZ[(prow[s] + qx * M) * ZR + ct * 8 + gq]);
+          }
+          if (row < N2) {
+            const int c0 = ct * 8 + 2 * kq;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int col = c0 + h;
+              if (col < N2) {
+                const int iz = col / N, jz = col - iz * N;
+                sY[(g * M + qx) * YR + ((iy * N + iz) * N + jy) * N + jz] = h ? d1 : d0;
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- x stage: A[(ix,jx)][r] = W (32 x 20) * Y (20 x 632) ------------------
+    {
+      double* out = A + cell * (int64_t)(N3 * N3);
+      const int row = xrt * 8 + gq, ix = row / N, jx = row % N;
+#pragma unroll 2
+      for (int ct = warp >> 2; ct < 79; ct += 4) {
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int s = 0; s < 5; ++s) dmma4(d0, d1, wa[s], sY[(4 * s + kq) * YR + ct * 8 + gq]);
+        if (row < N2) {
+          // r = (iy*N + iz) * N2 + (jy*N + jz): address = rowpart + (r / 25) * 125 + r % 25
+          const int r0 = ct * 8 + 2 * kq;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = r0 + h;
+            if (r < N4) {
+              const int a = r / N2, b = r - a * N2;
+              out[(int64_t)(ix * N2 + a) * N3 + jx * N2 + b] = h ? d1 : d0;
+            }
+          }
+        }
+      }
+    }
+    k_phase(next);
+    __syncthreads();
+  }
+}
+
+int launch_hex_matrix_tc5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                          cudaStream_t s) {
+  if (p->n != 5 || p->m != 5 || p->collocated) return SFK_EUNSUPPORTED;
+  static int sms = 0, per_sm = 0;
+  if (!sms) {
+    cudaError_t e = cudaFuncSetAttribute(hex_laplace_matrix_tc5,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)m5::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_matrix_tc5)");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hex_laplace_matrix_tc5,
+                                                      m5::THREADS, m5::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "occupancy(hex_matrix_tc5)");
+    if (per_sm < 1) return fail(SFK_ECUDA, "hex_matrix_tc5 does not fit on an SM");
+  }
+  TabsMat5 T;
+  for (int i = 0; i < 25; ++i) {
+    T.B[i] = p->B[i];
+    T.D[i] = p->D[i];
+  }
+  for (int q = 0; q < 5; ++q) {
+    T.W[q] = p->wq[q];
+    T.Bc[q] = p->Bc[q];
+    T.Bc[5 + q] = p->Bc[5 + q];
+  }
+  const int64_t resident = (int64_t)sms * per_sm;
+  const unsigned grid = (unsigned)(ncells < resident ? ncells : resident);
+  hex_laplace_matrix_tc5<<<grid, m5::THREADS, m5::SMEM, s>>>(T, ncells, coords, A);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "hex_laplace_matrix_tc5 launch");
+}
+
+}  // namespace sfk

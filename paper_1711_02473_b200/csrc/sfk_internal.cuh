@@ -98,6 +98,8 @@ int launch_hex_matrix_p1(const sfk_plan* p, int64_t ncells, double* A, const dou
                          cudaStream_t s);
 int launch_hex_matrix_tc4(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                           cudaStream_t s);
+int launch_hex_matrix_tc5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                          cudaStream_t s);
 int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A,
                       const double* coords, cudaStream_t s);
 int launch_hex_matrix_csr(const sfk_plan* p, int64_t ncells, const int32_t* dofs,
