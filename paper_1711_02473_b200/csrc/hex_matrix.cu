@@ -324,6 +324,18 @@ int launch_hex_matrix_csr(const sfk_plan* p, int64_t ncells, const int32_t* dofs
                           const int32_t* emap, double* values, cudaStream_t s) {
   if (p->collocated || p->n != p->m)
     return fail(SFK_EUNSUPPORTED, "CSR assembly: hex laplace with m == n only");
+  // (the DMMA kernels of hex_matrix_tc.cu have an entry-map epilogue too, but
+  // their fragment-order map loads and atomics scatter: p = 3 1.74 -> 1.88 ms,
+  // p = 4 8.7 -> 10.9 ms, profiles/r01bk_csr_dmma.jsonl; SFK_CSR_DMMA=1 uses them)
+  static const bool csr_dmma = [] {
+    const char* e = std::getenv("SFK_CSR_DMMA");
+    return e && e[0] == '1';
+  }();
+  if (csr_dmma && emap && (p->n == 4 || p->n == 5)) {
+    const int rc = p->n == 4 ? launch_hex_matrix_tc4(p, ncells, values, coords, s, emap)
+                             : launch_hex_matrix_tc5(p, ncells, values, coords, s, emap);
+    if (rc != SFK_EUNSUPPORTED) return rc;
+  }
   switch (p->n) {
     case 2:
       return launch_mat<2, 2, 16, true>(p, ncells, values, coords, s, dofs, row_ptr, col_idx,

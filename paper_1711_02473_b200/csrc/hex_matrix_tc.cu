@@ -56,9 +56,13 @@ __host__ __device__ constexpr int ksym4(int l, int r) {
 
 // Persistent CTAs, one cell per iteration; the constant A fragments of the
 // three DMMA stages are built once per CTA.
+// emap != nullptr: CSR mode — A is the CSR values array and every cell entry
+// (i, j) is atomically added at values[emap[cell][i * 64 + j]]
+// (sfk_csr_entry_map); the dense offset of the entry indexes the map.
 __global__ void __launch_bounds__(m4::THREADS, 3)
 hex_laplace_matrix_tc4(const __grid_constant__ TabsMat4 T, int64_t ncells,
-                       const double* __restrict__ coords, double* __restrict__ A) {
+                       const double* __restrict__ coords, double* __restrict__ A,
+                       const int32_t* __restrict__ emap) {
   using namespace m4;
   extern __shared__ __align__(16) double smem[];
   double* sY = smem;                 // [16][YR]   (16-byte aligned rows)
@@ -176,8 +180,14 @@ hex_laplace_matrix_tc4(const __grid_constant__ TabsMat4 T, int64_t ncells,
         const int oix = (rt * 8 + gq) / N, ojx = (rt * 8 + gq) % N;
         const int r = ct * 8 + 2 * kq;
         const int iy = r / (N * N2), iz = (r / N2) % N, jy = (r / N) % N, jz = r % N;
-        double* ap = out + (int64_t)(oix * N2 + iy * N + iz) * N3 + ojx * N2 + jy * N + jz;
-        *reinterpret_cast<double2*>(ap) = make_double2(d0, d1);
+        const int64_t off = (int64_t)(oix * N2 + iy * N + iz) * N3 + ojx * N2 + jy * N + jz;
+        if (emap) {
+          const int32_t* mp = emap + cell * (int64_t)(N3 * N3) + off;
+          atomicAdd(A + __ldg(mp), d0);
+          atomicAdd(A + __ldg(mp + 1), d1);
+        } else {
+          *reinterpret_cast<double2*>(out + off) = make_double2(d0, d1);
+        }
       }
     }
     k_phase(next);
@@ -186,9 +196,9 @@ hex_laplace_matrix_tc4(const __grid_constant__ TabsMat4 T, int64_t ncells,
 }
 
 int launch_hex_matrix_tc4(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                          cudaStream_t s) {
+                          cudaStream_t s, const int32_t* emap) {
   if (p->n != 4 || p->m != 4 || p->collocated) return SFK_EUNSUPPORTED;
-  if ((reinterpret_cast<uintptr_t>(A) & 15) != 0) return SFK_EUNSUPPORTED;   // double2 stores
+  if (!emap && (reinterpret_cast<uintptr_t>(A) & 15) != 0) return SFK_EUNSUPPORTED;   // double2 stores
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(hex_laplace_matrix_tc4,
@@ -219,7 +229,7 @@ int launch_hex_matrix_tc4(const sfk_plan* p, int64_t ncells, double* A, const do
   }
   const int64_t resident = (int64_t)sms * per_sm;
   const unsigned grid = (unsigned)(ncells < resident ? ncells : resident);
-  hex_laplace_matrix_tc4<<<grid, m4::THREADS, m4::SMEM, s>>>(T, ncells, coords, A);
+  hex_laplace_matrix_tc4<<<grid, m4::THREADS, m4::SMEM, s>>>(T, ncells, coords, A, emap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_matrix_tc4 launch");
 }
@@ -250,7 +260,8 @@ struct TabsMat5 {
 
 __global__ void __launch_bounds__(m5::THREADS, 1)
 hex_laplace_matrix_tc5(const __grid_constant__ TabsMat5 T, int64_t ncells,
-                       const double* __restrict__ coords, double* __restrict__ A) {
+                       const double* __restrict__ coords, double* __restrict__ A,
+                       const int32_t* __restrict__ emap) {
   using namespace m5;
   extern __shared__ __align__(16) double smem[];
   double* sY = smem;                 // [20][YR]
@@ -413,7 +424,9 @@ hex_laplace_matrix_tc5(const __grid_constant__ TabsMat5 T, int64_t ncells,
             const int r = r0 + h;
             if (r < N4) {
               const int a = r / N2, b = r - a * N2;
-              out[(int64_t)(ix * N2 + a) * N3 + jx * N2 + b] = h ? d1 : d0;
+              const int64_t off = (int64_t)(ix * N2 + a) * N3 + jx * N2 + b;
+              if (emap) atomicAdd(A + __ldg(emap + cell * (int64_t)(N3 * N3) + off), h ? d1 : d0);
+              else out[off] = h ? d1 : d0;
             }
           }
         }
@@ -425,7 +438,7 @@ hex_laplace_matrix_tc5(const __grid_constant__ TabsMat5 T, int64_t ncells,
 }
 
 int launch_hex_matrix_tc5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                          cudaStream_t s) {
+                          cudaStream_t s, const int32_t* emap) {
   if (p->n != 5 || p->m != 5 || p->collocated) return SFK_EUNSUPPORTED;
   static int sms = 0, per_sm = 0;
   if (!sms) {
@@ -453,7 +466,7 @@ int launch_hex_matrix_tc5(const sfk_plan* p, int64_t ncells, double* A, const do
   }
   const int64_t resident = (int64_t)sms * per_sm;
   const unsigned grid = (unsigned)(ncells < resident ? ncells : resident);
-  hex_laplace_matrix_tc5<<<grid, m5::THREADS, m5::SMEM, s>>>(T, ncells, coords, A);
+  hex_laplace_matrix_tc5<<<grid, m5::THREADS, m5::SMEM, s>>>(T, ncells, coords, A, emap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_matrix_tc5 launch");
 }

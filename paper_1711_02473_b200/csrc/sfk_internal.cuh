@@ -97,9 +97,9 @@ int launch_quad_action(const sfk_plan* p0, const sfk_plan* p1, int64_t ncells,
 int launch_hex_matrix_p1(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          cudaStream_t s);
 int launch_hex_matrix_tc4(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                          cudaStream_t s);
+                          cudaStream_t s, const int32_t* emap = nullptr);
 int launch_hex_matrix_tc5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                          cudaStream_t s);
+                          cudaStream_t s, const int32_t* emap = nullptr);
 int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A,
                       const double* coords, cudaStream_t s);
 int launch_hex_matrix_csr(const sfk_plan* p, int64_t ncells, const int32_t* dofs,
