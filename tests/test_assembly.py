@@ -250,3 +250,18 @@ def test_vector_dof_map_layout():
     v = lattice_vector_dof_map(2, 2, 1, 2)
     assert v.shape == (4, 3 * 27) and v.dtype == np.int32
     assert np.array_equal(v[:, 0::3], 3 * g) and np.array_equal(v[:, 2::3], 3 * g + 2)
+
+
+@pytest.mark.gpu
+def test_csr_dmma_epilogue_opt_in(cuda):
+    """The DMMA kernels' entry-map CSR epilogue (opt-in, SFK_CSR_DMMA=1) gives
+    the same assembled matrices."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SFK_CSR_DMMA="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m",
+                        "gpu", "-k", "csr_assembly_matches_oracle"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:]
