@@ -287,6 +287,8 @@ int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double
         if (!phase) return launch_hex_matrix_p1(p, ncells, A, coords, s);
         return launch_mat<2, 2, 16>(p, ncells, A, coords, s);
       }
+      // (a DMMA version at n = 3 measured slower, 0.54 vs 0.37 ms: too little
+      // work per cell for the padded tiles, profiles/r01bl_c5_p2_dmma.jsonl)
       case 3: return launch_mat<3, 3, 3>(p, ncells, A, coords, s);
       case 4: {
         // DMMA kernel (hex_matrix_tc.cu); SFK_C5_P3=phase selects the FMA one
