@@ -352,6 +352,9 @@ static int dispatch_colloc(const sfk_plan* p, int64_t ncells, double* A, const d
 
 int launch_hex_colloc_action(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                              const double* w0, const double* w1, cudaStream_t s) {
+  // n = 8, 12, 16: DMMA kernel (hex_colloc_tc.cu)
+  const int rc = launch_hex_colloc_tc(p, ncells, A, coords, w0, w1, s);
+  if (rc != SFK_EUNSUPPORTED) return rc;
   return dispatch_colloc<false>(p, ncells, A, coords, w0, w1, s, nullptr);
 }
 

@@ -86,6 +86,8 @@ int launch_hex_action_v4(const sfk_plan* p, int64_t ncells, double* A, const dou
                          const double* w0, cudaStream_t s);
 int launch_hex_action_v4_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                             double* y, const double* coords, cudaStream_t s);
+int launch_hex_colloc_tc(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                         const double* w0, const double* w1, cudaStream_t s);
 int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                          double* y, const double* coords, cudaStream_t s);
 int launch_hex_colloc_action(const sfk_plan* p, int64_t ncells, double* A,

@@ -347,7 +347,7 @@ def test_c2_every_kernel_generation(cuda, p):
         assert r.returncode == 0, (gen, r.stdout, r.stderr[-2000:])
 
 
-@pytest.mark.parametrize("mode", ["colloc_warps", "neo_cta"])
+@pytest.mark.parametrize("mode", ["colloc_warps", "neo_cta", "colloc_tc"])
 def test_alternative_kernel_modes(cuda, mode):
     """Kernel modes that are off by default for speed (C3's warp-synchronous
     variant, SFK_COLLOC_WARPS) or on by default (C4's, SFK_NEO_WARPS=0 turns
@@ -356,8 +356,9 @@ def test_alternative_kernel_modes(cuda, mode):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    if mode == "colloc_warps":
-        env_var, degrees = {"SFK_COLLOC_WARPS": "8"}, (1, 2, 3, 4)
+    if mode in ("colloc_warps", "colloc_tc"):
+        env_var, degrees = (({"SFK_COLLOC_WARPS": "8"}, (1, 2, 3, 4)) if mode == "colloc_warps"
+                            else ({"SFK_C3_TC": "1"}, (7, 11, 15)))
         build = ("compile_form(action_form(REGISTRY['weighted_laplace']), 'hex', p, 'spectral',"
                  " 'spectral_gll', 'collocated-gll')")
         inputs = "workloads.c3_inputs(p, dims=(3, 5, 7))"
