@@ -254,10 +254,10 @@ int sfk_program_destroy(sfk_program *program);
 int sfk_program_sizes(const sfk_program *program, int64_t *return_size,
                       int *nargs, int64_t *arg_sizes, int max_args);
 
-/* Launch geometry: out[0..9] = cells per CTA, threads, slots per cell,
+/* Launch geometry: out[0..10] = cells per CTA, threads, slots per cell,
  * dynamic smem bytes, global-scratch flag, phases, serial phases, barriers,
  * cubin bytes, warp mode (1: each warp owns whole cells, barriers are
- * __syncwarp). */
+ * __syncwarp), phases fused into the previous phase's loop. */
 int sfk_program_config(const sfk_program *program, int64_t *out, int n);
 
 /* what = 0: generated CUDA source, 1: kernel entry name, 2: program name. */

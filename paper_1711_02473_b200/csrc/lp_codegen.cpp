@@ -365,6 +365,7 @@ struct Access {
   long long elem;
   int thread;
   bool write;
+  int item = -1;   // loop item (w) of a NEST phase; -1 elsewhere (never fusable)
 };
 
 void collect_loads(const Expr& e, std::vector<const Expr*>& out) {
@@ -426,14 +427,14 @@ bool phase_accesses(const Phase& ph, const std::map<std::string, long long>& bas
     const int t = (int)(w % T);
     for (int bv = 0; bv < ph.blk_ext; ++bv) {
       if (ph.blk >= 0) val[ph.blk] = bv;
-      out.push_back({elem(tb + eval_addr(L.offset, L.terms, val), c), t, true});
+      out.push_back({elem(tb + eval_addr(L.offset, L.terms, val), c), t, true, (int)w});
       if (loads.empty()) continue;
       std::vector<int> it(ph.red.size(), 0);
       for (long long r = 0; r < nred; ++r) {
         for (size_t j = 0; j < ph.red.size(); ++j) val[ph.red[j].first] = it[j];
         for (const Expr* ld : loads)
           out.push_back({elem(base.at(ld->name) + eval_addr(ld->offset, ld->terms, val), c), t,
-                         false});
+                         false, (int)w});
         for (size_t j = ph.red.size(); j-- > 0;) {
           if (++it[j] < ph.red[j].second) break;
           it[j] = 0;
@@ -478,6 +479,39 @@ struct Window {
     for (long long e : touched) { writer[e] = -1; reader[e] = -1; multi[e] = 0; }
     touched.clear();
     poisoned = false;
+  }
+};
+
+// Item-level dependence inside a fused loop group: every element touched by
+// two phases of the group (at least one write) must be touched by the SAME
+// item w, so running the phases' bodies back to back per item preserves
+// every dependence.
+struct ItemWindow {
+  std::vector<int> writer, reader;   // -1 none, -2 several items
+  std::vector<long long> touched;
+  explicit ItemWindow(long long n) : writer(n, -1), reader(n, -1) {}
+  bool compatible(const std::vector<Access>& acc) const {
+    for (const auto& a : acc) {
+      if (a.item < 0) return false;
+      const int w = writer[a.elem], r = reader[a.elem];
+      if (w != -1 && w != a.item) return false;
+      if (a.write && r != -1 && r != a.item) return false;
+    }
+    return true;
+  }
+  void add(const std::vector<Access>& acc) {
+    for (const auto& a : acc) {
+      if (writer[a.elem] == -1 && reader[a.elem] == -1) touched.push_back(a.elem);
+      if (a.write) {
+        writer[a.elem] = (writer[a.elem] == -1 || writer[a.elem] == a.item) ? a.item : -2;
+      } else {
+        reader[a.elem] = (reader[a.elem] == -1 || reader[a.elem] == a.item) ? a.item : -2;
+      }
+    }
+  }
+  void clear() {
+    for (long long e : touched) { writer[e] = -1; reader[e] = -1; }
+    touched.clear();
   }
 };
 
@@ -838,20 +872,35 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
     xfer_access(P.args[a].second, base.at(P.args[a].first), true);
     win.add(acc);
   }
+  // fused loop groups: consecutive NEST phases with the same trip count, no
+  // barrier between them and only same-item dependences share one loop over w
+  bool fusion = true;
+  if (const char* e = std::getenv("SFK_LP_FUSE")) fusion = std::atoi(e) != 0;
+  ItemWindow iwin(C.slots * LN);
+  long long group_trips = -1;   // trip count of the open loop group (-1: none open)
+  auto close_group = [&]() {
+    if (group_trips >= 0) o << "    }\n";
+    group_trips = -1;
+    iwin.clear();
+  };
   auto barrier_for = [&](bool known) {
     const bool need = !known || win.conflicts(acc);
     if (need) {
+      close_group();
       o << "    " << SYNC << ";\n";
       ++C.barriers;
       win.clear();
     }
     if (known) win.add(acc);
     else win.poisoned = true;
+    return need;
   };
   C.phases = (int)phases.size();
   for (size_t k = 0; k < phases.size(); ++k) {
     const Phase& ph = phases[k];
-    barrier_for(phase_accesses(ph, base, bufsize, LN, LT, max_idx, acc));
+    const bool known = phase_accesses(ph, base, bufsize, LN, LT, max_idx, acc);
+    barrier_for(known);
+    if (ph.k != Phase::NEST) close_group();
     if (ph.k == Phase::ZERO) {
       o << "    // phase " << k << ": zero " << ph.zname << "\n"
         << "    for (int e = " << TID << "; e < " << LN * ph.zsize << "; e += " << LT << ") {\n";
@@ -873,9 +922,20 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
       o << "    // phase " << k << ": " << (L.k == Stmt::ACCUM ? "accumulate " : "assign ") << L.name
         << " (" << ph.npar << " parallel";
       if (E > 1) o << ", " << E << " per thread along " << bv;
-      o << " x " << ph.red.size() << " reduction loops)\n"
-        << "    for (int w = " << TID << "; w < " << LN * ph.nitem << "; w += " << LT << ") {\n";
-      if (NC > 1) o << "      const int c = w % " << LN << ";\n      int q = w / " << LN << ";\n";
+      o << " x " << ph.red.size() << " reduction loops)\n";
+      const long long trips = LN * ph.nitem;
+      const bool join = fusion && known && group_trips == trips && iwin.compatible(acc);
+      if (!join) {
+        close_group();
+        o << "    for (int w = " << TID << "; w < " << trips << "; w += " << LT << ") {\n";
+        if (NC > 1) o << "      const int c = w % " << LN << ";\n";
+        group_trips = trips;
+      } else {
+        ++C.fused_phases;
+      }
+      iwin.add(acc);
+      o << "     {\n";
+      if (NC > 1) o << "      int q = w / " << LN << ";\n";
       else o << "      int q = w;\n";
       for (size_t j = ph.opar.size(); j-- > 0;) {
         const auto& pr = ph.opar[j];
@@ -918,9 +978,10 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
       }
       bopen("      ");
       o << (E > 1 ? "" : "      ") << tgt << " = " << av << ";\n";
-      o << "    }\n";
+      o << "     }\n";
     }
   }
+  close_group();
   // store A
   xfer_access(P.ret_size, base.at(P.ret_name), false);
   barrier_for(true);

@@ -104,6 +104,7 @@ struct Config {
   int serial_phases = 0;     // phases executed thread-per-cell
   int barriers = 0;          // __syncthreads, or __syncwarp in warp mode
   int warp_mode = 0;         // 1: every warp owns cells_per_warp whole cells
+  int fused_phases = 0;      // phases running inside the previous phase's loop
   int cells_per_warp = 0;
 };
 

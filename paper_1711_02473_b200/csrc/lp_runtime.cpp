@@ -245,7 +245,7 @@ int sfk_program_config(const sfk_program* P, int64_t* out, int n) {
   const auto& C = P->gen.cfg;
   const int64_t v[] = {C.cells_per_block, C.threads, C.slots, C.smem_bytes, C.global_scratch,
                        C.phases, C.serial_phases, C.barriers, (int64_t)P->cubin.size(),
-                       C.warp_mode};
+                       C.warp_mode, C.fused_phases};
   for (int k = 0; k < n && k < (int)(sizeof v / sizeof v[0]); ++k) out[k] = v[k];
   return SFK_OK;
 }

@@ -43,7 +43,7 @@ FMA = 1
 NO_JIT = 2
 _CONFIG_KEYS = ("cells_per_block", "threads", "slots_per_cell", "smem_bytes",
                 "global_scratch", "phases", "serial_phases", "barriers",
-                "cubin_bytes", "warp_mode")
+                "cubin_bytes", "warp_mode", "fused_phases")
 
 
 def _declare(lib):
