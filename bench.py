@@ -58,10 +58,14 @@ def parse():
 
 
 def degrees_of(s):
-    if "-" in s:
-        a, b = s.split("-")
-        return list(range(int(a), int(b) + 1))
-    return [int(x) for x in s.split(",")]
+    out = []
+    for part in s.split(","):
+        if "-" in part:
+            a, b = part.split("-")
+            out.extend(range(int(a), int(b) + 1))
+        else:
+            out.append(int(part))
+    return out
 
 
 def measured_peaks():

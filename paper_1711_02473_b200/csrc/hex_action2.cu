@@ -24,7 +24,29 @@
 #include "async_copy.cuh"
 #include "hex_geometry.cuh"
 
+// SFK_V2_CLAMP=1: threads past a stage's last line redo that line instead of
+// skipping it, so every store is unconditional (no branch between the
+// unrolled output iterations: the compiler can interleave the accumulator
+// chains of different outputs; with the branches the transposed stages ran
+// as one 2M-deep DFMA chain at a time).
+#ifndef SFK_V2_CLAMP
+#define SFK_V2_CLAMP 0
+#endif
+
 namespace sfk {
+
+constexpr bool CLAMP = SFK_V2_CLAMP;
+// SFK_V2_SPLIT=1: the transposed y/x stages accumulate each table's sum in
+// its own chain (2-3 independent M-deep DFMA chains per output instead of one
+// 2M/3M-deep chain); summation order changes, within the 1e-12 gate.
+#ifndef SFK_V2_SPLIT
+#define SFK_V2_SPLIT 1
+#endif
+constexpr bool SPLIT = SFK_V2_SPLIT;
+
+__device__ __forceinline__ int clamp_line(int ln, int L) {
+  return CLAMP ? (ln < L ? ln : L - 1) : ln;
+}
 
 template <int N, int M, int CPB, int R>
 struct HexAction2Cfg {
@@ -106,8 +128,8 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
       double uu[R][N];
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        ln[j] = tid + j * TH;
-        on[j] = ln[j] < L;
+        ln[j] = clamp_line(tid + j * TH, L);
+        on[j] = CLAMP || tid + j * TH < L;
         const int lc = on[j] ? ln[j] : 0;
         const int c = lc / NN, r = lc - c * NN;
         const bool live = on[j] && c < ncb;
@@ -125,19 +147,19 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
         double bq[R], dq[R];
 #pragma unroll
         for (int j = 0; j < R; ++j) {
-          bq[j] = T.B[q] * uu[j][0];
-          dq[j] = T.D[q] * uu[j][0];
+          bq[j] = TB(q) * uu[j][0];
+          dq[j] = TD(q) * uu[j][0];
         }
 #pragma unroll
         for (int i = 1; i < N; ++i)
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            bq[j] = fma(T.B[i * M + q], uu[j][i], bq[j]);
-            dq[j] = fma(T.D[i * M + q], uu[j][i], dq[j]);
+            bq[j] = fma(TB(i * M + q), uu[j][i], bq[j]);
+            dq[j] = fma(TD(i * M + q), uu[j][i], dq[j]);
           }
 #pragma unroll
         for (int j = 0; j < R; ++j)
-          if (on[j]) {
+          if (CLAMP || on[j]) {
             const int c = ln[j] / NN, r = ln[j] - c * NN;
             double* xo = sX + c * C::XSZ + r;
             xo[q * PX] = bq[j];
@@ -156,8 +178,8 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
       bool on[R];
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        ln[j] = tid + j * TH;
-        on[j] = ln[j] < L;
+        ln[j] = clamp_line(tid + j * TH, L);
+        on[j] = CLAMP || tid + j * TH < L;
         const int lc = on[j] ? ln[j] : 0;
         const int c = lc / MN, r = lc - c * MN;
         const int qx = r / N, iz = r - qx * N;
@@ -173,21 +195,21 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
         double bb[R], bd[R], db[R];
 #pragma unroll
         for (int j = 0; j < R; ++j) {
-          bb[j] = T.B[q] * a0[j][0];
-          bd[j] = T.D[q] * a0[j][0];
-          db[j] = T.B[q] * a1[j][0];
+          bb[j] = TB(q) * a0[j][0];
+          bd[j] = TD(q) * a0[j][0];
+          db[j] = TB(q) * a1[j][0];
         }
 #pragma unroll
         for (int i = 1; i < N; ++i)
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            bb[j] = fma(T.B[i * M + q], a0[j][i], bb[j]);
-            bd[j] = fma(T.D[i * M + q], a0[j][i], bd[j]);
-            db[j] = fma(T.B[i * M + q], a1[j][i], db[j]);
+            bb[j] = fma(TB(i * M + q), a0[j][i], bb[j]);
+            bd[j] = fma(TD(i * M + q), a0[j][i], bd[j]);
+            db[j] = fma(TB(i * M + q), a1[j][i], db[j]);
           }
 #pragma unroll
         for (int j = 0; j < R; ++j)
-          if (on[j]) {
+          if (CLAMP || on[j]) {
             const int c = ln[j] / MN, r = ln[j] - c * MN;
             const int qx = r / N, iz = r - qx * N;
             double* yo = sY + c * C::YSZ + (qx * M + q) * LZ + iz;
@@ -206,8 +228,8 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
       bool on[R];
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        ln[j] = tid + j * TH;
-        on[j] = ln[j] < L;
+        ln[j] = clamp_line(tid + j * TH, L);
+        on[j] = CLAMP || tid + j * TH < L;
       }
       // (1) reference gradient lines: slot 0 <- Dz BB (d_z), 1 <- Bz BD (d_y),
       //     2 <- Bz DB (d_x)
@@ -229,17 +251,17 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
           double gz[R], gy[R], gx[R];
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            gz[j] = T.D[q] * bb[j][0];
-            gy[j] = T.B[q] * bd[j][0];
-            gx[j] = T.B[q] * db[j][0];
+            gz[j] = TD(q) * bb[j][0];
+            gy[j] = TB(q) * bd[j][0];
+            gx[j] = TB(q) * db[j][0];
           }
 #pragma unroll
           for (int i = 1; i < N; ++i)
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-              gz[j] = fma(T.D[i * M + q], bb[j][i], gz[j]);
-              gy[j] = fma(T.B[i * M + q], bd[j][i], gy[j]);
-              gx[j] = fma(T.B[i * M + q], db[j][i], gx[j]);
+              gz[j] = fma(TD(i * M + q), bb[j][i], gz[j]);
+              gy[j] = fma(TB(i * M + q), bd[j][i], gy[j]);
+              gx[j] = fma(TB(i * M + q), db[j][i], gx[j]);
             }
           if (M > N) {
             // in place is only safe once every input entry was read: for
@@ -248,7 +270,7 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
           }
 #pragma unroll
           for (int j = 0; j < R; ++j)
-            if (on[j]) {
+            if (CLAMP || on[j]) {
               const int c = ln[j] / MM, r = ln[j] - c * MM;
               double* yo = sY + c * C::YSZ + r * LZ + q;
               yo[0] = gz[j];
@@ -274,7 +296,7 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
           const double det = geo.adj(T.Bc[M + q], r0, r1, r2);
           const double s = (wxy * T.W[q]) * rcp64(fabs(det));
           laplace_flux(r0, r1, r2, s, gx, gy, gz);
-          if (on[j]) {
+          if (CLAMP || on[j]) {
             yl[q] = gz;
             yl[YA + q] = gy;
             yl[2 * YA + q] = gx;
@@ -301,21 +323,21 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
           double sz[R], sy[R], sx[R];
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            sz[j] = T.D[i * M] * fz[j][0];
-            sy[j] = T.B[i * M] * fy[j][0];
-            sx[j] = T.B[i * M] * fx[j][0];
+            sz[j] = TD(i * M) * fz[j][0];
+            sy[j] = TB(i * M) * fy[j][0];
+            sx[j] = TB(i * M) * fx[j][0];
           }
 #pragma unroll
           for (int q = 1; q < M; ++q)
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-              sz[j] = fma(T.D[i * M + q], fz[j][q], sz[j]);
-              sy[j] = fma(T.B[i * M + q], fy[j][q], sy[j]);
-              sx[j] = fma(T.B[i * M + q], fx[j][q], sx[j]);
+              sz[j] = fma(TD(i * M + q), fz[j][q], sz[j]);
+              sy[j] = fma(TB(i * M + q), fy[j][q], sy[j]);
+              sx[j] = fma(TB(i * M + q), fx[j][q], sx[j]);
             }
 #pragma unroll
           for (int j = 0; j < R; ++j)
-            if (on[j]) {
+            if (CLAMP || on[j]) {
               const int c = ln[j] / MM, r = ln[j] - c * MM;
               double* yo = sY + c * C::YSZ + r * LZ + i;
               yo[0] = sz[j];
@@ -335,8 +357,8 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
       bool on[R];
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        ln[j] = tid + j * TH;
-        on[j] = ln[j] < L;
+        ln[j] = clamp_line(tid + j * TH, L);
+        on[j] = CLAMP || tid + j * TH < L;
         const int lc = on[j] ? ln[j] : 0;
         const int c = lc / MN, r = lc - c * MN;
         const int qx = r / N, iz = r - qx * N;
@@ -351,22 +373,43 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
 #pragma unroll (UI)
       for (int i = 0; i < N; ++i) {
         double r1[R], r2[R];
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-          r1[j] = T.B[i * M] * px[j][0];
-          r2[j] = fma(T.D[i * M], py[j][0], T.B[i * M] * pz[j][0]);
-        }
-#pragma unroll
-        for (int q = 1; q < M; ++q)
+        if (SPLIT) {
+          // three independent M-deep chains (Dy^T Sy and By^T Sz summed last)
+          double r3[R];
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            r1[j] = fma(T.B[i * M + q], px[j][q], r1[j]);
-            r2[j] = fma(T.D[i * M + q], py[j][q], r2[j]);
-            r2[j] = fma(T.B[i * M + q], pz[j][q], r2[j]);
+            r1[j] = TB(i * M) * px[j][0];
+            r2[j] = TD(i * M) * py[j][0];
+            r3[j] = TB(i * M) * pz[j][0];
           }
 #pragma unroll
+          for (int q = 1; q < M; ++q)
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+              r1[j] = fma(TB(i * M + q), px[j][q], r1[j]);
+              r2[j] = fma(TD(i * M + q), py[j][q], r2[j]);
+              r3[j] = fma(TB(i * M + q), pz[j][q], r3[j]);
+            }
+#pragma unroll
+          for (int j = 0; j < R; ++j) r2[j] += r3[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            r1[j] = TB(i * M) * px[j][0];
+            r2[j] = fma(TD(i * M), py[j][0], TB(i * M) * pz[j][0]);
+          }
+#pragma unroll
+          for (int q = 1; q < M; ++q)
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+              r1[j] = fma(TB(i * M + q), px[j][q], r1[j]);
+              r2[j] = fma(TD(i * M + q), py[j][q], r2[j]);
+              r2[j] = fma(TB(i * M + q), pz[j][q], r2[j]);
+            }
+        }
+#pragma unroll
         for (int j = 0; j < R; ++j)
-          if (on[j]) {
+          if (CLAMP || on[j]) {
             const int c = ln[j] / MN, r = ln[j] - c * MN;
             const int qx = r / N, iz = r - qx * N;
             double* xo = sX + c * C::XSZ + qx * PX + iz;
@@ -385,9 +428,11 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
       bool on[R];
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        ln[j] = tid + j * TH;
-        on[j] = ln[j] < L && (ln[j] / NN) < ncb;
-        const int c = on[j] ? ln[j] / NN : 0, r = on[j] ? ln[j] - c * NN : 0;
+        // CLAMP: lines past the live cells redo the last live line (same
+        // inputs, same instructions: bit-identical duplicate stores)
+        ln[j] = CLAMP ? clamp_line(tid + j * TH, ncb * NN) : tid + j * TH;
+        on[j] = tid + j * TH < L && ((tid + j * TH) / NN) < ncb;
+        const int c = (CLAMP || on[j]) ? ln[j] / NN : 0, r = (CLAMP || on[j]) ? ln[j] - c * NN : 0;
         const double* xi = sX + c * C::XSZ + r;
 #pragma unroll
         for (int q = 0; q < M; ++q) {
@@ -398,20 +443,39 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
 #pragma unroll (UI)
       for (int i = 0; i < N; ++i) {
         double a[R];
-#pragma unroll
-        for (int j = 0; j < R; ++j) a[j] = fma(T.D[i * M], p1[j][0], T.B[i * M] * p2[j][0]);
-#pragma unroll
-        for (int q = 1; q < M; ++q)
+        if (SPLIT) {
+          // two independent M-deep chains (Dx^T R1 and Bx^T R2 summed last)
+          double a2[R];
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            a[j] = fma(T.D[i * M + q], p1[j][q], a[j]);
-            a[j] = fma(T.B[i * M + q], p2[j][q], a[j]);
+            a[j] = TD(i * M) * p1[j][0];
+            a2[j] = TB(i * M) * p2[j][0];
           }
 #pragma unroll
+          for (int q = 1; q < M; ++q)
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+              a[j] = fma(TD(i * M + q), p1[j][q], a[j]);
+              a2[j] = fma(TB(i * M + q), p2[j][q], a2[j]);
+            }
+#pragma unroll
+          for (int j = 0; j < R; ++j) a[j] += a2[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < R; ++j) a[j] = fma(TD(i * M), p1[j][0], TB(i * M) * p2[j][0]);
+#pragma unroll
+          for (int q = 1; q < M; ++q)
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+              a[j] = fma(TD(i * M + q), p1[j][q], a[j]);
+              a[j] = fma(TB(i * M + q), p2[j][q], a[j]);
+            }
+        }
+#pragma unroll
         for (int j = 0; j < R; ++j)
-          if (on[j]) {
+          if (CLAMP || on[j]) {
             const int c = ln[j] / NN, r = ln[j] - c * NN;
-            if (GS) atomicAdd(A + smap[c * N3 + i * NN + r], a[j]);
+            if (GS) atomicAdd(A + smap[c * N3 + i * NN + r], on[j] ? a[j] : 0.0);
             else A[(cell0 + c) * N3 + i * NN + r] = a[j];
           }
       }

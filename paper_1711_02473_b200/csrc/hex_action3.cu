@@ -21,6 +21,9 @@
 //    transposed z contraction in place);
 //  * shared strides from tools/smem_pads_action.py (bank-conflict search).
 #include <cstdlib>
+// 128-bit (B, D) table pairs measured slower here (p=5 1.03 -> 1.6 ms):
+// separate B / D tables
+#define SFK_TAB_PAIRS 0
 #include "async_copy.cuh"
 #include "hex_geometry.cuh"
 
@@ -102,8 +105,8 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
         const double v = live ? uval(0) : 0.0;
 #pragma unroll
         for (int q = 0; q < M; ++q) {
-          xb[q] = T.B[q] * v;
-          xd[q] = T.D[q] * v;
+          xb[q] = TB(q) * v;
+          xd[q] = TD(q) * v;
         }
       }
 #pragma unroll
@@ -111,8 +114,8 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
         const double v = live ? uval(i) : 0.0;
 #pragma unroll
         for (int q = 0; q < M; ++q) {
-          xb[q] = fma(T.B[i * M + q], v, xb[q]);
-          xd[q] = fma(T.D[i * M + q], v, xd[q]);
+          xb[q] = fma(TB(i * M + q), v, xb[q]);
+          xd[q] = fma(TD(i * M + q), v, xd[q]);
         }
       }
       double* xo = sX + c * XC + iy * XY + iz;
@@ -135,9 +138,9 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
         const double v0 = xi[0], v1 = xi[XA];
 #pragma unroll
         for (int q = 0; q < M; ++q) {
-          bb[q] = T.B[q] * v0;
-          bd[q] = T.D[q] * v0;
-          db[q] = T.B[q] * v1;
+          bb[q] = TB(q) * v0;
+          bd[q] = TD(q) * v0;
+          db[q] = TB(q) * v1;
         }
       }
 #pragma unroll
@@ -145,9 +148,9 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
         const double v0 = xi[i * XY], v1 = xi[XA + i * XY];
 #pragma unroll
         for (int q = 0; q < M; ++q) {
-          bb[q] = fma(T.B[i * M + q], v0, bb[q]);
-          bd[q] = fma(T.D[i * M + q], v0, bd[q]);
-          db[q] = fma(T.B[i * M + q], v1, db[q]);
+          bb[q] = fma(TB(i * M + q), v0, bb[q]);
+          bd[q] = fma(TD(i * M + q), v0, bd[q]);
+          db[q] = fma(TB(i * M + q), v1, db[q]);
         }
       }
       double* yo = sY + c * YC + qx * YX + iz;
@@ -173,9 +176,9 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
           const double v0 = yl[0], v1 = yl[YA], v2 = yl[2 * YA];
 #pragma unroll
           for (int q = 0; q < M; ++q) {
-            gz[q] = T.D[q] * v0;
-            gy[q] = T.B[q] * v1;
-            gx[q] = T.B[q] * v2;
+            gz[q] = TD(q) * v0;
+            gy[q] = TB(q) * v1;
+            gx[q] = TB(q) * v2;
           }
         }
 #pragma unroll
@@ -183,9 +186,9 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
           const double v0 = yl[i], v1 = yl[YA + i], v2 = yl[2 * YA + i];
 #pragma unroll
           for (int q = 0; q < M; ++q) {
-            gz[q] = fma(T.D[i * M + q], v0, gz[q]);
-            gy[q] = fma(T.B[i * M + q], v1, gy[q]);
-            gx[q] = fma(T.B[i * M + q], v2, gx[q]);
+            gz[q] = fma(TD(i * M + q), v0, gz[q]);
+            gy[q] = fma(TB(i * M + q), v1, gy[q]);
+            gx[q] = fma(TB(i * M + q), v2, gx[q]);
           }
         }
 #pragma unroll
@@ -219,9 +222,9 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
           const double f0 = yl[0], f1 = yl[YA], f2 = yl[2 * YA];
 #pragma unroll
           for (int i = 0; i < N; ++i) {
-            sz[i] = T.D[i * M] * f0;
-            sy[i] = T.B[i * M] * f1;
-            sx[i] = T.B[i * M] * f2;
+            sz[i] = TD(i * M) * f0;
+            sy[i] = TB(i * M) * f1;
+            sx[i] = TB(i * M) * f2;
           }
         }
 #pragma unroll
@@ -229,9 +232,9 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
           const double f0 = yl[q], f1 = yl[YA + q], f2 = yl[2 * YA + q];
 #pragma unroll
           for (int i = 0; i < N; ++i) {
-            sz[i] = fma(T.D[i * M + q], f0, sz[i]);
-            sy[i] = fma(T.B[i * M + q], f1, sy[i]);
-            sx[i] = fma(T.B[i * M + q], f2, sx[i]);
+            sz[i] = fma(TD(i * M + q), f0, sz[i]);
+            sy[i] = fma(TB(i * M + q), f1, sy[i]);
+            sx[i] = fma(TB(i * M + q), f2, sx[i]);
           }
         }
 #pragma unroll
@@ -254,8 +257,8 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
         const double pz = yi[0], py = yi[YA], px = yi[2 * YA];
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-          r1[i] = T.B[i * M] * px;
-          r2[i] = fma(T.D[i * M], py, T.B[i * M] * pz);
+          r1[i] = TB(i * M) * px;
+          r2[i] = fma(TD(i * M), py, TB(i * M) * pz);
         }
       }
 #pragma unroll
@@ -263,9 +266,9 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
         const double pz = yi[q * LZ], py = yi[YA + q * LZ], px = yi[2 * YA + q * LZ];
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-          r1[i] = fma(T.B[i * M + q], px, r1[i]);
-          r2[i] = fma(T.D[i * M + q], py, r2[i]);
-          r2[i] = fma(T.B[i * M + q], pz, r2[i]);
+          r1[i] = fma(TB(i * M + q), px, r1[i]);
+          r2[i] = fma(TD(i * M + q), py, r2[i]);
+          r2[i] = fma(TB(i * M + q), pz, r2[i]);
         }
       }
       double* xo = sX + c * XC + qx * PX + iz;
@@ -287,15 +290,15 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
         {
           const double p1 = xi[0], p2 = xi[XA];
 #pragma unroll
-          for (int i = 0; i < N; ++i) a[i] = fma(T.D[i * M], p1, T.B[i * M] * p2);
+          for (int i = 0; i < N; ++i) a[i] = fma(TD(i * M), p1, TB(i * M) * p2);
         }
 #pragma unroll
         for (int q = 1; q < M; ++q) {
           const double p1 = xi[q * PX], p2 = xi[XA + q * PX];
 #pragma unroll
           for (int i = 0; i < N; ++i) {
-            a[i] = fma(T.D[i * M + q], p1, a[i]);
-            a[i] = fma(T.B[i * M + q], p2, a[i]);
+            a[i] = fma(TD(i * M + q), p1, a[i]);
+            a[i] = fma(TB(i * M + q), p2, a[i]);
           }
         }
         if (GS) {

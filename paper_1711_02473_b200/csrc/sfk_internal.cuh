@@ -36,6 +36,9 @@ void note_launch(int64_t k = 1);
 // compile-time indices become c[0x0][...] operands of DFMA, no loads).
 template <int N, int M>
 struct Tabs {
+  // (B, D) pairs interleaved: the line kernels use B[i][q] and D[i][q]
+  // together, so one 128-bit constant load (LDCU.128) feeds both.
+  alignas(16) double BD[2 * N * M];
   double B[N * M];
   double D[N * M];
   double W[M];
@@ -50,6 +53,8 @@ inline Tabs<N, M> make_tabs(const sfk_plan* p) {
     for (int q = 0; q < M; ++q) {
       t.B[i * M + q] = p->B[i * p->m + q];
       t.D[i * M + q] = p->D[i * p->m + q];
+      t.BD[2 * (i * M + q)] = t.B[i * M + q];
+      t.BD[2 * (i * M + q) + 1] = t.D[i * M + q];
     }
   for (int q = 0; q < M; ++q) {
     t.W[q] = p->wq[q];
@@ -114,6 +119,19 @@ int launch_sum_squares(const double* x, int64_t n, double* out, cudaStream_t s);
 int run_fp64_peak(double seconds, double* dfma, double* dmma);
 
 }  // namespace sfk
+
+// Table entry accessors of the line kernels: TB(k) = B[k], TD(k) = D[k]
+// (k = i*M + q), read from the interleaved pairs unless SFK_TAB_PAIRS=0.
+#ifndef SFK_TAB_PAIRS
+#define SFK_TAB_PAIRS 1
+#endif
+#if SFK_TAB_PAIRS
+#define TB(k) T.BD[2 * (k)]
+#define TD(k) T.BD[2 * (k) + 1]
+#else
+#define TB(k) T.B[k]
+#define TD(k) T.D[k]
+#endif
 
 // ---------------------------------------------------------------------------
 // device helpers
