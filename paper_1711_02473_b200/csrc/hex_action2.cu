@@ -23,6 +23,7 @@
 
 #include "async_copy.cuh"
 #include "hex_geometry.cuh"
+#include "hex_line_cfg.cuh"
 
 // SFK_V2_CLAMP=1: threads past a stage's last line redo that line instead of
 // skipping it, so every store is unconditional (no branch between the
@@ -48,22 +49,6 @@ __device__ __forceinline__ int clamp_line(int ln, int L) {
   return CLAMP ? (ln < L ? ln : L - 1) : ln;
 }
 
-template <int N, int M, int CPB, int R>
-struct HexAction2Cfg {
-  static constexpr int NN = N * N, MN = M * N, MM = M * M, N3 = N * N * N;
-  static constexpr int LINES = (MM > NN ? MM : NN) * CPB;   // max lines of a stage
-  static constexpr int THREADS = round_up((LINES + R - 1) / R, 32);
-  static constexpr int PX = (N >= 4) ? NN + (((N - NN) % 16) + 16) % 16 : NN;
-  static constexpr int LZ = (M > N ? M : N) | 1;   // z-line stride, >= m (in-place z)
-  static constexpr int XA = M * PX;                // one X/R array per cell
-  static constexpr int XSZ = 2 * XA;
-  static constexpr int YA = MM * LZ;               // one Y/S array per cell
-  static constexpr int YSZ = 3 * YA;
-  static constexpr int USZ = round_up(CPB * N3 + 1, 2); // u buffer (16B multiple)
-  static constexpr int CSZ = CPB * 24;
-  static constexpr size_t SMEM =
-      (size_t)(round_up(CPB * XSZ + CPB * YSZ, 2) + USZ + 2 * CSZ) * sizeof(double);
-};
 
 // ROLL: 0 = everything unrolled; 1 = pointwise loop rolled; 2 = also the
 // outer (output-index) loop of every contraction rolled (table entries then
@@ -79,6 +64,8 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
                       double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
   using C = HexAction2Cfg<N, M, CPB, R>;
+  // (B, D) pairs spill at n = 6 (96-register cap at CPB 8): separate tables there
+  constexpr bool PAIRS = SFK_TAB_PAIRS && N != 6;
   constexpr int NN = C::NN, MN = C::MN, MM = C::MM, N3 = C::N3, PX = C::PX, LZ = C::LZ;
   constexpr int XA = C::XA, YA = C::YA, TH = C::THREADS;
   constexpr int UQ = ROLL >= 2 ? 1 : M, UI = ROLL >= 2 ? 1 : N, UP = ROLL >= 1 ? 1 : M;
@@ -147,15 +134,15 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
         double bq[R], dq[R];
 #pragma unroll
         for (int j = 0; j < R; ++j) {
-          bq[j] = TB(q) * uu[j][0];
-          dq[j] = TD(q) * uu[j][0];
+          bq[j] = TBP(q) * uu[j][0];
+          dq[j] = TDP(q) * uu[j][0];
         }
 #pragma unroll
         for (int i = 1; i < N; ++i)
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            bq[j] = fma(TB(i * M + q), uu[j][i], bq[j]);
-            dq[j] = fma(TD(i * M + q), uu[j][i], dq[j]);
+            bq[j] = fma(TBP(i * M + q), uu[j][i], bq[j]);
+            dq[j] = fma(TDP(i * M + q), uu[j][i], dq[j]);
           }
 #pragma unroll
         for (int j = 0; j < R; ++j)
@@ -195,17 +182,17 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
         double bb[R], bd[R], db[R];
 #pragma unroll
         for (int j = 0; j < R; ++j) {
-          bb[j] = TB(q) * a0[j][0];
-          bd[j] = TD(q) * a0[j][0];
-          db[j] = TB(q) * a1[j][0];
+          bb[j] = TBP(q) * a0[j][0];
+          bd[j] = TDP(q) * a0[j][0];
+          db[j] = TBP(q) * a1[j][0];
         }
 #pragma unroll
         for (int i = 1; i < N; ++i)
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            bb[j] = fma(TB(i * M + q), a0[j][i], bb[j]);
-            bd[j] = fma(TD(i * M + q), a0[j][i], bd[j]);
-            db[j] = fma(TB(i * M + q), a1[j][i], db[j]);
+            bb[j] = fma(TBP(i * M + q), a0[j][i], bb[j]);
+            bd[j] = fma(TDP(i * M + q), a0[j][i], bd[j]);
+            db[j] = fma(TBP(i * M + q), a1[j][i], db[j]);
           }
 #pragma unroll
         for (int j = 0; j < R; ++j)
@@ -251,17 +238,17 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
           double gz[R], gy[R], gx[R];
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            gz[j] = TD(q) * bb[j][0];
-            gy[j] = TB(q) * bd[j][0];
-            gx[j] = TB(q) * db[j][0];
+            gz[j] = TDP(q) * bb[j][0];
+            gy[j] = TBP(q) * bd[j][0];
+            gx[j] = TBP(q) * db[j][0];
           }
 #pragma unroll
           for (int i = 1; i < N; ++i)
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-              gz[j] = fma(TD(i * M + q), bb[j][i], gz[j]);
-              gy[j] = fma(TB(i * M + q), bd[j][i], gy[j]);
-              gx[j] = fma(TB(i * M + q), db[j][i], gx[j]);
+              gz[j] = fma(TDP(i * M + q), bb[j][i], gz[j]);
+              gy[j] = fma(TBP(i * M + q), bd[j][i], gy[j]);
+              gx[j] = fma(TBP(i * M + q), db[j][i], gx[j]);
             }
           if (M > N) {
             // in place is only safe once every input entry was read: for
@@ -323,17 +310,17 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
           double sz[R], sy[R], sx[R];
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            sz[j] = TD(i * M) * fz[j][0];
-            sy[j] = TB(i * M) * fy[j][0];
-            sx[j] = TB(i * M) * fx[j][0];
+            sz[j] = TDP(i * M) * fz[j][0];
+            sy[j] = TBP(i * M) * fy[j][0];
+            sx[j] = TBP(i * M) * fx[j][0];
           }
 #pragma unroll
           for (int q = 1; q < M; ++q)
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-              sz[j] = fma(TD(i * M + q), fz[j][q], sz[j]);
-              sy[j] = fma(TB(i * M + q), fy[j][q], sy[j]);
-              sx[j] = fma(TB(i * M + q), fx[j][q], sx[j]);
+              sz[j] = fma(TDP(i * M + q), fz[j][q], sz[j]);
+              sy[j] = fma(TBP(i * M + q), fy[j][q], sy[j]);
+              sx[j] = fma(TBP(i * M + q), fx[j][q], sx[j]);
             }
 #pragma unroll
           for (int j = 0; j < R; ++j)
@@ -378,33 +365,33 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
           double r3[R];
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            r1[j] = TB(i * M) * px[j][0];
-            r2[j] = TD(i * M) * py[j][0];
-            r3[j] = TB(i * M) * pz[j][0];
+            r1[j] = TBP(i * M) * px[j][0];
+            r2[j] = TDP(i * M) * py[j][0];
+            r3[j] = TBP(i * M) * pz[j][0];
           }
 #pragma unroll
           for (int q = 1; q < M; ++q)
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-              r1[j] = fma(TB(i * M + q), px[j][q], r1[j]);
-              r2[j] = fma(TD(i * M + q), py[j][q], r2[j]);
-              r3[j] = fma(TB(i * M + q), pz[j][q], r3[j]);
+              r1[j] = fma(TBP(i * M + q), px[j][q], r1[j]);
+              r2[j] = fma(TDP(i * M + q), py[j][q], r2[j]);
+              r3[j] = fma(TBP(i * M + q), pz[j][q], r3[j]);
             }
 #pragma unroll
           for (int j = 0; j < R; ++j) r2[j] += r3[j];
         } else {
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            r1[j] = TB(i * M) * px[j][0];
-            r2[j] = fma(TD(i * M), py[j][0], TB(i * M) * pz[j][0]);
+            r1[j] = TBP(i * M) * px[j][0];
+            r2[j] = fma(TDP(i * M), py[j][0], TBP(i * M) * pz[j][0]);
           }
 #pragma unroll
           for (int q = 1; q < M; ++q)
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-              r1[j] = fma(TB(i * M + q), px[j][q], r1[j]);
-              r2[j] = fma(TD(i * M + q), py[j][q], r2[j]);
-              r2[j] = fma(TB(i * M + q), pz[j][q], r2[j]);
+              r1[j] = fma(TBP(i * M + q), px[j][q], r1[j]);
+              r2[j] = fma(TDP(i * M + q), py[j][q], r2[j]);
+              r2[j] = fma(TBP(i * M + q), pz[j][q], r2[j]);
             }
         }
 #pragma unroll
@@ -448,27 +435,27 @@ hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
           double a2[R];
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            a[j] = TD(i * M) * p1[j][0];
-            a2[j] = TB(i * M) * p2[j][0];
+            a[j] = TDP(i * M) * p1[j][0];
+            a2[j] = TBP(i * M) * p2[j][0];
           }
 #pragma unroll
           for (int q = 1; q < M; ++q)
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-              a[j] = fma(TD(i * M + q), p1[j][q], a[j]);
-              a2[j] = fma(TB(i * M + q), p2[j][q], a2[j]);
+              a[j] = fma(TDP(i * M + q), p1[j][q], a[j]);
+              a2[j] = fma(TBP(i * M + q), p2[j][q], a2[j]);
             }
 #pragma unroll
           for (int j = 0; j < R; ++j) a[j] += a2[j];
         } else {
 #pragma unroll
-          for (int j = 0; j < R; ++j) a[j] = fma(TD(i * M), p1[j][0], TB(i * M) * p2[j][0]);
+          for (int j = 0; j < R; ++j) a[j] = fma(TDP(i * M), p1[j][0], TBP(i * M) * p2[j][0]);
 #pragma unroll
           for (int q = 1; q < M; ++q)
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-              a[j] = fma(TD(i * M + q), p1[j][q], a[j]);
-              a[j] = fma(TB(i * M + q), p2[j][q], a[j]);
+              a[j] = fma(TDP(i * M + q), p1[j][q], a[j]);
+              a[j] = fma(TBP(i * M + q), p2[j][q], a[j]);
             }
         }
 #pragma unroll

@@ -57,6 +57,7 @@ static int c2_variant() {
     if (e && strcmp(e, "tc") == 0) v = 4;
     if (e && strcmp(e, "cell") == 0) v = 5;
     if (e && strcmp(e, "v4") == 0) v = 6;
+    if (e && strcmp(e, "v5") == 0) v = 7;
   }
   return v;
 }
@@ -67,10 +68,12 @@ static int c2_auto(int n) {
     case 3: return 6;
     case 4: return 6;
     case 5: return 3;
-    case 6: return 2;
-    case 7: return 2;   // v2 1.705 vs v3 1.751 ms (profiles/r01bg_c2_generations.jsonl)
+    // v5 (grouped outputs) over v2: p = 5 1.043 -> 0.985, p = 6 1.685 -> 1.621,
+    // p = 8 3.639 -> 3.513 ms (profiles/r01bu_*.jsonl)
+    case 6: return 7;
+    case 7: return 7;
     case 8: return 4;
-    case 9: return 2;
+    case 9: return 7;
     default: return 1;
   }
 }
@@ -80,6 +83,10 @@ static int launch_c2(const sfk_plan* p, int64_t ncells, double* A, const double*
   int v = c2_variant();
   if (v == 0) v = c2_auto(p->n);
   int rc = SFK_EUNSUPPORTED;
+  if (v == 7) {
+    rc = launch_hex_action_v5(p, ncells, A, coords, w0, s);
+    if (rc == SFK_EUNSUPPORTED) v = 2;
+  }
   if (v == 6) {
     rc = launch_hex_action_v4(p, ncells, A, coords, w0, s);
     if (rc == SFK_EUNSUPPORTED) v = 3;

@@ -87,6 +87,8 @@ int launch_hex_neohookean_gs(const sfk_plan* p, int64_t ncells, const int* cmap,
                              double* y, const double* coords, cudaStream_t s);
 int launch_hex_colloc_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                          double* y, const double* coords, const double* kappa, cudaStream_t s);
+int launch_hex_action_v5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                         const double* w0, cudaStream_t s);
 int launch_hex_action_v4(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, cudaStream_t s);
 int launch_hex_action_v4_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
@@ -132,6 +134,9 @@ int run_fp64_peak(double seconds, double* dfma, double* dmma);
 #define TB(k) T.B[k]
 #define TD(k) T.D[k]
 #endif
+// Per-instantiation choice (a kernel defines `constexpr bool PAIRS`).
+#define TBP(k) (PAIRS ? T.BD[2 * (k)] : T.B[k])
+#define TDP(k) (PAIRS ? T.BD[2 * (k) + 1] : T.D[k])
 
 // ---------------------------------------------------------------------------
 // device helpers

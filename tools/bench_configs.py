@@ -62,6 +62,7 @@ def main():
         ts = []
         for _ in range(args.reps):
             flush.zero_()
+            torch.cuda._sleep(2_000_000)   # host launch latency off the timed events
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)

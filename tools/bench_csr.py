@@ -37,6 +37,7 @@ def timed(fn, reps, flush):
     ts = []
     for _ in range(reps):
         flush.zero_()
+        torch.cuda._sleep(2_000_000)   # host launch latency off the timed events
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         fn()

@@ -39,6 +39,7 @@ def timeit(fn, reps, flush):
     ts = []
     for _ in range(reps):
         flush.zero_()
+        torch.cuda._sleep(2_000_000)   # host launch latency off the timed events
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         fn()
