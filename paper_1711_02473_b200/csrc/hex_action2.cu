@@ -60,7 +60,7 @@ __device__ __forceinline__ int clamp_line(int ln, int L) {
 // in the transposed x stage.
 template <int N, int M, int CPB, int R, int MINB, int ROLL, bool GS = false>
 __global__ void __launch_bounds__(HexAction2Cfg<N, M, CPB, R>::THREADS, MINB)
-hex_laplace_action_v2(const __grid_constant__ Tabs<N, M> T, int64_t ncells,
+hex_laplace_action_v2(const __grid_constant__ TabsBD<N, M> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
                       double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
   using C = HexAction2Cfg<N, M, CPB, R>;
@@ -489,7 +489,7 @@ static int launch_v2(const sfk_plan* p, int64_t ncells, double* A, const double*
     if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) return fail(SFK_ECUDA, "hex_action_v2<%d>: kernel does not fit on an SM", N);
   }
-  const Tabs<N, M> T = make_tabs<N, M>(p);
+  const TabsBD<N, M> T = make_tabs_bd<N, M>(p);
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
   const int64_t resident = (int64_t)sms * per_sm;
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);

@@ -41,7 +41,7 @@ struct Act4Layout {
 // atomics in the transposed x stage.
 template <class L, int MINB, bool GS = false>
 __global__ void __launch_bounds__(L::THREADS, MINB)
-hex_laplace_action_v4(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells,
+hex_laplace_action_v4(const __grid_constant__ TabsBD<L::N, L::M> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
                       double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
   constexpr int N = L::N, M = L::M, NN = L::NN, N3 = L::N3, CPW = L::CPW, CPB = L::CPB;
@@ -315,7 +315,7 @@ static int launch_v4(const sfk_plan* p, int64_t ncells, double* A, const double*
     if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) return fail(SFK_ECUDA, "hex_action_v4<%d>: does not fit on an SM", L::N);
   }
-  const Tabs<L::N, L::M> T = make_tabs<L::N, L::M>(p);
+  const TabsBD<L::N, L::M> T = make_tabs_bd<L::N, L::M>(p);
   const int64_t nbatch = (ncells + L::CPB - 1) / L::CPB;
   const int64_t resident = (int64_t)sms * per_sm;
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);

@@ -20,15 +20,22 @@
 // from measurements (launch_hex_action_v5).
 #include <cstdlib>
 
+// pointwise loop unroll factor (1 = rolled; A/B builds)
+#ifndef SFK_V5_UP
+#define SFK_V5_UP 1
+#endif
+
 #include "async_copy.cuh"
 #include "hex_geometry.cuh"
 #include "hex_line_cfg.cuh"
 
 namespace sfk {
 
+constexpr int V5_UP = SFK_V5_UP;
+
 template <int N, int CPB, int G, int MINB, bool PAIRS>
 __global__ void __launch_bounds__(HexAction2Cfg<N, N, CPB, 1>::THREADS, MINB)
-hex_laplace_action_v5(const __grid_constant__ Tabs<N, N> T, int64_t ncells,
+hex_laplace_action_v5(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
                       double* __restrict__ A) {
   using C = HexAction2Cfg<N, N, CPB, 1>;
@@ -202,7 +209,7 @@ hex_laplace_action_v5(const __grid_constant__ Tabs<N, N> T, int64_t ncells,
         HexLineAdj geo;
         geo.setup(sC + c * 24, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
         const double wxy = T.W[qx] * T.W[qy];
-#pragma unroll 1
+#pragma unroll (V5_UP)
         for (int q = 0; q < M; ++q) {
           double gz = yl[q], gy = yl[YA + q], gx = yl[2 * YA + q];
           double r0[3], r1[3], r2[3];
@@ -367,7 +374,7 @@ static int launch_v5(const sfk_plan* p, int64_t ncells, double* A, const double*
     if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) return fail(SFK_ECUDA, "hex_action_v5<%d>: kernel does not fit on an SM", N);
   }
-  const Tabs<N, N> T = make_tabs<N, N>(p);
+  const TabsBD<N, N> T = make_tabs_bd<N, N>(p);
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
   const int64_t resident = (int64_t)sms * per_sm;
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);

@@ -36,9 +36,6 @@ void note_launch(int64_t k = 1);
 // compile-time indices become c[0x0][...] operands of DFMA, no loads).
 template <int N, int M>
 struct Tabs {
-  // (B, D) pairs interleaved: the line kernels use B[i][q] and D[i][q]
-  // together, so one 128-bit constant load (LDCU.128) feeds both.
-  alignas(16) double BD[2 * N * M];
   double B[N * M];
   double D[N * M];
   double W[M];
@@ -53,8 +50,6 @@ inline Tabs<N, M> make_tabs(const sfk_plan* p) {
     for (int q = 0; q < M; ++q) {
       t.B[i * M + q] = p->B[i * p->m + q];
       t.D[i * M + q] = p->D[i * p->m + q];
-      t.BD[2 * (i * M + q)] = t.B[i * M + q];
-      t.BD[2 * (i * M + q) + 1] = t.D[i * M + q];
     }
   for (int q = 0; q < M; ++q) {
     t.W[q] = p->wq[q];
@@ -63,6 +58,40 @@ inline Tabs<N, M> make_tabs(const sfk_plan* p) {
     t.Bc[M + q] = p->Bc[p->m + q];
   }
   return t;
+}
+
+// Tables plus (B, D) pairs interleaved, for the line kernels (v2, v4, v5):
+// they use B[i][q] and D[i][q] together, so one 128-bit constant load
+// (LDCU.128) feeds both.  A separate type so the other kernels keep the
+// compact parameter block (the tc8 kernel measured 10% slower with the
+// pairs in its parameters: profiles/r01bw_*.jsonl).
+template <int N, int M>
+struct TabsBD {
+  alignas(16) double BD[2 * N * M];
+  double B[N * M];
+  double D[N * M];
+  double W[M];
+  double Bc[2 * M];
+  double X[M];
+};
+
+template <int N, int M>
+inline TabsBD<N, M> make_tabs_bd(const sfk_plan* p) {
+  const Tabs<N, M> t = make_tabs<N, M>(p);
+  TabsBD<N, M> o;
+  for (int k = 0; k < N * M; ++k) {
+    o.B[k] = t.B[k];
+    o.D[k] = t.D[k];
+    o.BD[2 * k] = t.B[k];
+    o.BD[2 * k + 1] = t.D[k];
+  }
+  for (int q = 0; q < M; ++q) {
+    o.W[q] = t.W[q];
+    o.X[q] = t.X[q];
+    o.Bc[q] = t.Bc[q];
+    o.Bc[M + q] = t.Bc[M + q];
+  }
+  return o;
 }
 
 // Family launchers (one translation unit each).
