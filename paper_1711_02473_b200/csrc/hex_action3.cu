@@ -24,6 +24,9 @@
 // 128-bit (B, D) table pairs measured slower here (p=5 1.03 -> 1.6 ms):
 // separate B / D tables
 #define SFK_TAB_PAIRS 0
+#ifndef SFK_V3_YT
+#define SFK_V3_YT 1
+#endif
 #include "async_copy.cuh"
 #include "hex_geometry.cuh"
 
@@ -61,6 +64,14 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
   constexpr int N = L::N, M = L::M, CPB = L::CPB, NN = L::NN, MN = L::MN, MM = L::MM;
   constexpr int N3 = L::N3, XY = L::XY, PX = L::PX, XC = L::XC, LZ = L::LZ, YX = L::YX;
   constexpr int YC = L::YC, XA = L::XA, YA = L::YA, TH = L::THREADS;
+  // YT: Y/S lines qy-major (element (qx, qy, z) at qy*YX + qx*LZ + z), so
+  // the y / y^T stages (thread (qx, iz), iz fastest) touch consecutive
+  // addresses; the z stage sees the same line slots in another order.  On at
+  // n = 5 only (tools/smem_pads_yt.py: y-stage wavefronts 31 -> 25 per
+  // access at the z-optimal cell stride 381; the other n keep their
+  // searched qx-major strides).
+  constexpr bool YT = SFK_V3_YT && N == 5 && YX == M * LZ;
+  constexpr int QS = YT ? YX : LZ;
   extern __shared__ __align__(16) double smem[];
   double* sX = smem;
   double* sY = sX + CPB * XC;
@@ -153,12 +164,12 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
           db[q] = fma(TB(i * M + q), v1, db[q]);
         }
       }
-      double* yo = sY + c * YC + qx * YX + iz;
+      double* yo = sY + c * YC + (YT ? qx * LZ : qx * YX) + iz;
 #pragma unroll
       for (int q = 0; q < M; ++q) {
-        yo[q * LZ] = bb[q];
-        yo[YA + q * LZ] = bd[q];
-        yo[2 * YA + q * LZ] = db[q];
+        yo[q * QS] = bb[q];
+        yo[YA + q * QS] = bd[q];
+        yo[2 * YA + q * QS] = db[q];
       }
     }
     __syncthreads();
@@ -166,8 +177,9 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
     // ---- z stage: line (c, qx, qy), three in-place passes ------------------
     if (tid < CPB * MM) {
       const int c = tid / MM, r = tid - c * MM;
-      const int qx = r / M, qy = r - qx * M;
-      double* yl = sY + c * YC + qx * YX + qy * LZ;
+      const int r0 = r / M, r1 = r - r0 * M;
+      const int qx = YT ? r1 : r0, qy = YT ? r0 : r1;
+      double* yl = sY + c * YC + r0 * YX + r1 * LZ;
       // (1) reference gradient: slot0 <- Dz BB (d_z), slot1 <- Bz BD (d_y),
       //     slot2 <- Bz DB (d_x)
       {
@@ -251,7 +263,7 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
     if (tid < CPB * MN) {
       const int c = tid / MN, r = tid - c * MN;
       const int qx = r / N, iz = r - qx * N;
-      const double* yi = sY + c * YC + qx * YX + iz;
+      const double* yi = sY + c * YC + (YT ? qx * LZ : qx * YX) + iz;
       double r1[N], r2[N];
       {
         const double pz = yi[0], py = yi[YA], px = yi[2 * YA];
@@ -263,7 +275,7 @@ hex_laplace_action_v3(const __grid_constant__ Tabs<L::N, L::M> T, int64_t ncells
       }
 #pragma unroll
       for (int q = 1; q < M; ++q) {
-        const double pz = yi[q * LZ], py = yi[YA + q * LZ], px = yi[2 * YA + q * LZ];
+        const double pz = yi[q * QS], py = yi[YA + q * QS], px = yi[2 * YA + q * QS];
 #pragma unroll
         for (int i = 0; i < N; ++i) {
           r1[i] = fma(TB(i * M + q), px, r1[i]);

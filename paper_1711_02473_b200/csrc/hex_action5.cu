@@ -20,9 +20,13 @@
 // from measurements (launch_hex_action_v5).
 #include <cstdlib>
 
-// pointwise loop unroll factor (1 = rolled; A/B builds)
+// pointwise loop unroll factor (0 = per degree; A/B builds)
 #ifndef SFK_V5_UP
-#define SFK_V5_UP 1
+#define SFK_V5_UP 0
+#endif
+// Y/S line order (1 = qy-major; A/B builds)
+#ifndef SFK_V5_YT
+#define SFK_V5_YT 1
 #endif
 
 #include "async_copy.cuh"
@@ -33,15 +37,36 @@ namespace sfk {
 
 constexpr int V5_UP = SFK_V5_UP;
 
+// Per-cell Y/S stride padding for the qy-major layout (tools/smem_pads_yt.py:
+// modelled wavefronts of the y-stage and z-stage accesses, cell boundaries
+// included, z weighted 3x as it is accessed 3x as often; n = 9: 2201,
+// n = 7: 1031, n = 6: 764 doubles per cell).
+__host__ __device__ constexpr int v5_ypad(int n) {
+#ifdef SFK_V5_YPAD
+  if (SFK_V5_YPAD >= 0) return SFK_V5_YPAD;
+#endif
+  return SFK_V5_YT ? (n == 9 ? 14 : n == 7 ? 2 : n == 6 ? 8 : 0) : 0;
+}
+
 template <int N, int CPB, int G, int MINB, bool PAIRS>
-__global__ void __launch_bounds__(HexAction2Cfg<N, N, CPB, 1>::THREADS, MINB)
+__global__ void __launch_bounds__(HexAction2Cfg<N, N, CPB, 1, v5_ypad(N)>::THREADS, MINB)
 hex_laplace_action_v5(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
                       double* __restrict__ A) {
-  using C = HexAction2Cfg<N, N, CPB, 1>;
+  using C = HexAction2Cfg<N, N, CPB, 1, v5_ypad(N)>;
   constexpr int M = N;
   constexpr int NN = C::NN, MN = C::MN, MM = C::MM, N3 = C::N3, PX = C::PX, LZ = C::LZ;
   constexpr int XA = C::XA, YA = C::YA, TH = C::THREADS;
+  // YT: Y/S lines stored qy-major ([qy][qx][z]) instead of qx-major: the y
+  // and y^T stages (thread (qx, iz), iz fastest) then touch consecutive
+  // addresses LZ*qx + iz — conflict-free — while the z stage (thread = line
+  // slot, stride LZ odd) stays conflict-free; qx-major cost 2-3-way
+  // conflicts there (profiles/r01bv_p6.md: 34% excess wavefronts).
+  constexpr bool YT = SFK_V5_YT;
+  constexpr int QS = YT ? M * LZ : LZ;      // stride of q (= qy) in the y stages
+  // pointwise loop: 3-way unrolled at n = 9 (126 registers, p = 8 3.51 ->
+  // 3.46 ms, profiles/r01by_*.jsonl), rolled elsewhere (no gain / spills)
+  constexpr int UPN = V5_UP > 0 ? V5_UP : (N == 9 ? 3 : 1);
   extern __shared__ __align__(16) double smem[];
   double* sX = smem;                        // [CPB][2][M][PX]
   double* sY = sX + CPB * C::XSZ;           // [CPB][3][M*M][LZ]
@@ -124,7 +149,7 @@ hex_laplace_action_v5(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
         a0[i] = xi[i * N];
         a1[i] = xi[XA + i * N];
       }
-      double* yo = sY + c * C::YSZ + qx * M * LZ + iz;
+      double* yo = sY + c * C::YSZ + (YT ? qx * LZ : qx * M * LZ) + iz;
 #pragma unroll
       for (int q0 = 0; q0 < M; q0 += G) {
         double bb[G], bd[G], db[G];
@@ -148,9 +173,9 @@ hex_laplace_action_v5(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
 #pragma unroll
           for (int g = 0; g < G; ++g)
             if (q0 + g < M) {
-              yo[(q0 + g) * LZ] = bb[g];
-              yo[YA + (q0 + g) * LZ] = bd[g];
-              yo[2 * YA + (q0 + g) * LZ] = db[g];
+              yo[(q0 + g) * QS] = bb[g];
+              yo[YA + (q0 + g) * QS] = bd[g];
+              yo[2 * YA + (q0 + g) * QS] = db[g];
             }
         }
       }
@@ -205,11 +230,12 @@ hex_laplace_action_v5(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
       }
       // (2) pointwise: geometry per point + Laplace flux, in place
       {
-        const int qx = r / M, qy = r - qx * M;
+        const int r0 = r / M, r1 = r - r0 * M;
+        const int qx = YT ? r1 : r0, qy = YT ? r0 : r1;
         HexLineAdj geo;
         geo.setup(sC + c * 24, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
         const double wxy = T.W[qx] * T.W[qy];
-#pragma unroll (V5_UP)
+#pragma unroll (UPN)
         for (int q = 0; q < M; ++q) {
           double gz = yl[q], gy = yl[YA + q], gx = yl[2 * YA + q];
           double r0[3], r1[3], r2[3];
@@ -274,13 +300,13 @@ hex_laplace_action_v5(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
       const int lc = on ? tid : 0;
       const int c = lc / MN, r = lc - c * MN;
       const int qx = r / N, iz = r - qx * N;
-      const double* yi = sY + c * C::YSZ + qx * M * LZ + iz;
+      const double* yi = sY + c * C::YSZ + (YT ? qx * LZ : qx * M * LZ) + iz;
       double pz[M], py[M], px[M];
 #pragma unroll
       for (int q = 0; q < M; ++q) {
-        pz[q] = yi[q * LZ];
-        py[q] = yi[YA + q * LZ];
-        px[q] = yi[2 * YA + q * LZ];
+        pz[q] = yi[q * QS];
+        py[q] = yi[YA + q * QS];
+        px[q] = yi[2 * YA + q * QS];
       }
       double* xo = sX + c * C::XSZ + qx * PX + iz;
 #pragma unroll
@@ -359,7 +385,7 @@ hex_laplace_action_v5(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
 template <int N, int CPB, int G, int MINB, bool PAIRS>
 static int launch_v5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                      const double* u, cudaStream_t s) {
-  using C = HexAction2Cfg<N, N, CPB, 1>;
+  using C = HexAction2Cfg<N, N, CPB, 1, v5_ypad(N)>;
   auto kern = hex_laplace_action_v5<N, CPB, G, MINB, PAIRS>;
   static int sms = 0, per_sm = 0;
   if (!sms) {

@@ -7,7 +7,9 @@
 
 namespace sfk {
 
-template <int N, int M, int CPB, int R>
+// YPAD: extra doubles per cell after the Y/S triple (cell-stride tuning,
+// tools/smem_pads_yt.py).
+template <int N, int M, int CPB, int R, int YPAD = 0>
 struct HexAction2Cfg {
   static constexpr int NN = N * N, MN = M * N, MM = M * M, N3 = N * N * N;
   static constexpr int LINES = (MM > NN ? MM : NN) * CPB;   // max lines of a stage
@@ -17,7 +19,7 @@ struct HexAction2Cfg {
   static constexpr int XA = M * PX;                // one X/R array per cell
   static constexpr int XSZ = 2 * XA;
   static constexpr int YA = MM * LZ;               // one Y/S array per cell
-  static constexpr int YSZ = 3 * YA;
+  static constexpr int YSZ = 3 * YA + YPAD;
   static constexpr int USZ = round_up(CPB * N3 + 1, 2); // u buffer (16B multiple)
   static constexpr int CSZ = CPB * 24;
   static constexpr size_t SMEM =
