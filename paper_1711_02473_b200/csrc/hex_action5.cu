@@ -410,13 +410,13 @@ static int launch_v5(const sfk_plan* p, int64_t ncells, double* A, const double*
 }
 
 // Output group size per degree: SFK_C2_G overrides (tuning runs only).
-template <int N, int CPB, int G0>
+template <int N, int CPB, int G0, bool PAIRS = true>
 static int pick_v5(int g, const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                    const double* w0, cudaStream_t s) {
   switch (g ? g : G0) {
-    case 1: return launch_v5<N, CPB, 1, 2, N != 6>(p, ncells, A, coords, w0, s);
-    case 2: return launch_v5<N, CPB, 2, 2, N != 6>(p, ncells, A, coords, w0, s);
-    default: return launch_v5<N, CPB, 3, 2, N != 6>(p, ncells, A, coords, w0, s);
+    case 1: return launch_v5<N, CPB, 1, 2, PAIRS>(p, ncells, A, coords, w0, s);
+    case 2: return launch_v5<N, CPB, 2, 2, PAIRS>(p, ncells, A, coords, w0, s);
+    default: return launch_v5<N, CPB, 3, 2, PAIRS>(p, ncells, A, coords, w0, s);
   }
 }
 
@@ -427,12 +427,20 @@ int launch_hex_action_v5(const sfk_plan* p, int64_t ncells, double* A, const dou
     const char* e = getenv("SFK_C2_G");
     return e ? atoi(e) : 0;
   }();
+  static const int cpb6_env = [] {
+    const char* e = getenv("SFK_V5_CPB6");
+    return e ? atoi(e) : 0;
+  }();
   switch (p->n) {
     // profiles/r01bu_*.jsonl (same box, ms at 2^18 cells; G = 1 / 2 / 3):
     //   n = 5: 0.592 / 0.590 / 0.588 (v3 0.531 stays)   n = 6: 0.985 / 1.87 (spills) / 1.10
     //   n = 7: 1.676 / 1.621 / 1.667                     n = 9: 3.642 / 3.513 / 4.33 (spills)
     case 5: return pick_v5<5, 10, 2>(g_env, p, ncells, A, coords, w0, s);
-    case 6: return pick_v5<6, 8, 1>(g_env, p, ncells, A, coords, w0, s);
+    case 6:
+      // CPB 8 = 288 threads (register cap 96: no (B, D) pairs, G = 1);
+      // CPB 7 = 256 threads (cap 128) measured as an alternative
+      if (cpb6_env == 7) return pick_v5<6, 7, 2>(g_env, p, ncells, A, coords, w0, s);
+      return pick_v5<6, 8, 1, false>(g_env, p, ncells, A, coords, w0, s);
     case 7: return pick_v5<7, 5, 2>(g_env, p, ncells, A, coords, w0, s);
     case 9: return pick_v5<9, 3, 2>(g_env, p, ncells, A, coords, w0, s);
     default: return SFK_EUNSUPPORTED;
