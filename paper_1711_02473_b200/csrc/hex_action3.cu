@@ -394,11 +394,17 @@ int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, con
     const char* e = std::getenv("SFK_C2G_KERNEL");
     return e && e[0] == 'v' && e[1] == '3';
   }();
+  static const bool force_v2 = [] {
+    const char* e = std::getenv("SFK_C2G_KERNEL");
+    return e && e[0] == 'v' && e[1] == '2';
+  }();
   if (!force_v3 && p->n == p->m) {
     if (p->n == 2 && (reinterpret_cast<uintptr_t>(cmap) & 15) == 0)   // int4 map loads
       return launch_hex_action_p1_gs(p, ncells, cmap, x, y, coords, s);
     if ((p->n == 3 || p->n == 4) && !force_v3_small())
       return launch_hex_action_v4_gs(p, ncells, cmap, x, y, coords, s);
+    if ((p->n == 6 || p->n == 7 || p->n == 9) && !force_v2)
+      return launch_hex_action_v5_gs(p, ncells, cmap, x, y, coords, s);
     if (p->n == 6 || p->n == 7 || p->n == 9 || (p->n == 4 && force_v3_small()))
       return launch_hex_action_v2_gs(p, ncells, cmap, x, y, coords, s);
     if (p->n == 8) return launch_hex_action_tc_gs(p, ncells, cmap, x, y, coords, s);

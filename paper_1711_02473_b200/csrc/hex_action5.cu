@@ -48,11 +48,15 @@ __host__ __device__ constexpr int v5_ypad(int n) {
   return SFK_V5_YT ? (n == 9 ? 14 : n == 7 ? 2 : n == 6 ? 8 : 0) : 0;
 }
 
-template <int N, int CPB, int G, int MINB, bool PAIRS>
+// GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
+// item 1), as in v2: `u` is x, `A` is y, cmap[c][i] the global dof of local
+// dof i; the map (int32) is double-buffered in the u buffer, x is gathered
+// through it in the x stage and y scattered with fp64 atomics in x^T.
+template <int N, int CPB, int G, int MINB, bool PAIRS, bool GS = false>
 __global__ void __launch_bounds__(HexAction2Cfg<N, N, CPB, 1, v5_ypad(N)>::THREADS, MINB)
 hex_laplace_action_v5(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
-                      double* __restrict__ A) {
+                      double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
   using C = HexAction2Cfg<N, N, CPB, 1, v5_ypad(N)>;
   constexpr int M = N;
   constexpr int NN = C::NN, MN = C::MN, MM = C::MM, N3 = C::N3, PX = C::PX, LZ = C::LZ;
@@ -74,11 +78,18 @@ hex_laplace_action_v5(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
   double* sCo = sU + C::USZ;                // [2][CPB*24]
   const int tid = threadIdx.x;
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  int* sMap = reinterpret_cast<int*>(sU);   // GS: [2][CPB*N3] int32 in the u buffer
+  static_assert(!GS || 2 * CPB * N3 <= 2 * C::USZ, "map double buffer does not fit");
 
   auto prefetch = [&](int64_t b, int buf) {
     const int64_t c0 = b * CPB;
     const int nc = (int)((ncells - c0) < CPB ? (ncells - c0) : CPB);
-    async_copy_phase<TH>(sU + dst_shift(u + c0 * N3), u + c0 * N3, nc * N3, tid);
+    if (GS) {
+      for (int i = tid; i < nc * N3; i += TH)
+        cp_async4(sMap + buf * CPB * N3 + i, cmap + c0 * N3 + i);
+    } else {
+      async_copy_phase<TH>(sU + dst_shift(u + c0 * N3), u + c0 * N3, nc * N3, tid);
+    }
     async_copy<TH>(sCo + buf * C::CSZ, coords + c0 * 24, nc * 24, tid);
     cp_async_commit();
   };
@@ -91,7 +102,8 @@ hex_laplace_action_v5(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
     const int ncb = (int)((ncells - cell0) < CPB ? (ncells - cell0) : CPB);
     cp_async_wait<0>();
     __syncthreads();
-    const double* su = sU + dst_shift(u + cell0 * N3);
+    const double* su = sU + (GS ? 0 : dst_shift(u + cell0 * N3));
+    const int* smap = sMap + cur * CPB * N3;
     const double* sC = sCo + cur * C::CSZ;
 
     // ---- x stage: line (c, iy, iz): X0 = Bx u, X1 = Dx u ----------------
@@ -103,7 +115,8 @@ hex_laplace_action_v5(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
       const bool live = on && c < ncb;
       double uu[N];
 #pragma unroll
-      for (int i = 0; i < N; ++i) uu[i] = live ? su[c * N3 + i * NN + r] : 0.0;
+      for (int i = 0; i < N; ++i)
+        uu[i] = live ? (GS ? __ldg(u + smap[c * N3 + i * NN + r]) : su[c * N3 + i * NN + r]) : 0.0;
       double* xo = sX + c * C::XSZ + r;
 #pragma unroll
       for (int q0 = 0; q0 < M; q0 += G) {
@@ -374,7 +387,10 @@ hex_laplace_action_v5(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
         if (on) {
 #pragma unroll
           for (int g = 0; g < G; ++g)
-            if (i0 + g < N) ap[(i0 + g) * NN] = a1[g] + a2[g];
+            if (i0 + g < N) {
+              if (GS) atomicAdd(A + smap[c * N3 + (i0 + g) * NN + r], a1[g] + a2[g]);
+              else ap[(i0 + g) * NN] = a1[g] + a2[g];
+            }
         }
       }
     }
@@ -382,11 +398,11 @@ hex_laplace_action_v5(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
   }
 }
 
-template <int N, int CPB, int G, int MINB, bool PAIRS>
+template <int N, int CPB, int G, int MINB, bool PAIRS, bool GS = false>
 static int launch_v5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                     const double* u, cudaStream_t s) {
+                     const double* u, cudaStream_t s, const int* cmap = nullptr) {
   using C = HexAction2Cfg<N, N, CPB, 1, v5_ypad(N)>;
-  auto kern = hex_laplace_action_v5<N, CPB, G, MINB, PAIRS>;
+  auto kern = hex_laplace_action_v5<N, CPB, G, MINB, PAIRS, GS>;
   static int sms = 0, per_sm = 0;
   if (!sms) {
     int dev = 0;
@@ -404,7 +420,7 @@ static int launch_v5(const sfk_plan* p, int64_t ncells, double* A, const double*
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
   const int64_t resident = (int64_t)sms * per_sm;
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
-  kern<<<grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, u, A);
+  kern<<<grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, u, A, cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_v5 launch");
 }
@@ -437,12 +453,25 @@ int launch_hex_action_v5(const sfk_plan* p, int64_t ncells, double* A, const dou
     //   n = 7: 1.676 / 1.621 / 1.667                     n = 9: 3.642 / 3.513 / 4.33 (spills)
     case 5: return pick_v5<5, 10, 2>(g_env, p, ncells, A, coords, w0, s);
     case 6:
-      // CPB 8 = 288 threads (register cap 96: no (B, D) pairs, G = 1);
-      // CPB 7 = 256 threads (cap 128) measured as an alternative
-      if (cpb6_env == 7) return pick_v5<6, 7, 2>(g_env, p, ncells, A, coords, w0, s);
-      return pick_v5<6, 8, 1, false>(g_env, p, ncells, A, coords, w0, s);
+      // CPB 7 = 256 threads (register cap 128: (B, D) pairs fit) over CPB 8
+      // = 288 threads (cap 96: no pairs): 0.995 -> 0.947 ms with G = 1
+      // (profiles/r01cb_*.jsonl); SFK_V5_CPB6=8 selects the latter
+      if (cpb6_env == 8) return pick_v5<6, 8, 1, false>(g_env, p, ncells, A, coords, w0, s);
+      return pick_v5<6, 7, 1>(g_env, p, ncells, A, coords, w0, s);
     case 7: return pick_v5<7, 5, 2>(g_env, p, ncells, A, coords, w0, s);
     case 9: return pick_v5<9, 3, 2>(g_env, p, ncells, A, coords, w0, s);
+    default: return SFK_EUNSUPPORTED;
+  }
+}
+
+// Global operator (fused gather / scatter) through v5 at n = 6, 7, 9.
+int launch_hex_action_v5_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                            double* y, const double* coords, cudaStream_t s) {
+  if (p->n != p->m) return SFK_EUNSUPPORTED;
+  switch (p->n) {
+    case 6: return launch_v5<6, 7, 1, 2, true, true>(p, ncells, y, coords, x, s, cmap);
+    case 7: return launch_v5<7, 5, 2, 2, true, true>(p, ncells, y, coords, x, s, cmap);
+    case 9: return launch_v5<9, 3, 2, 2, true, true>(p, ncells, y, coords, x, s, cmap);
     default: return SFK_EUNSUPPORTED;
   }
 }

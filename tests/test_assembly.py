@@ -265,3 +265,20 @@ def test_csr_dmma_epilogue_opt_in(cuda):
                         "gpu", "-k", "csr_assembly_matches_oracle"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("gen", ["v2", "v3"])
+def test_gather_scatter_alternative_generations(cuda, gen):
+    """The global operator through the older kernel generations
+    (SFK_C2G_KERNEL=v2 / v3; the default is v5 at p = 5, 6, 8) agrees with
+    the assembled oracle too."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SFK_C2G_KERNEL=gen)
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m",
+                        "gpu", "-k", "gather_scatter_matches_oracle"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:]
