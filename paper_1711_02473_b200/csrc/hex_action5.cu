@@ -45,7 +45,7 @@ __host__ __device__ constexpr int v5_ypad(int n) {
 #ifdef SFK_V5_YPAD
   if (SFK_V5_YPAD >= 0) return SFK_V5_YPAD;
 #endif
-  return SFK_V5_YT ? (n == 9 ? 14 : n == 7 ? 2 : n == 6 ? 8 : 0) : 0;
+  return SFK_V5_YT ? (n == 9 ? 14 : n == 7 ? 2 : n == 6 ? 8 : n == 5 ? 6 : 0) : 0;
 }
 
 // GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)

@@ -56,10 +56,24 @@ struct CollocCfg {
 // __launch_bounds__(T, 2) (two CTAs per SM, no spills at that cap), 1 =
 // (T, 1), 0 = (T) only — ptxas picks different (and here faster) register
 // budgets for the last two (e.g. n = 16: 132 vs 254 registers).
+// Phase 3 as three register-light passes (SPLITZ) at n = 12..15, with its
+// own register policy (same-box A/B over fused/split x min-blocks 0-3,
+// profiles/r01cf_*.jsonl: p = 11 1.969 -> 1.664 ms, p = 12 2.118 -> 1.918,
+// p = 13 3.803 -> 3.085, p = 14 3.652 -> 3.355; the other n keep the fused
+// loop).  SFK_COLLOC_SPLITZ=n0 (A/B builds) splits every n >= n0.
+__host__ __device__ constexpr bool colloc_splitz(int n) {
+#ifdef SFK_COLLOC_SPLITZ
+  return n >= SFK_COLLOC_SPLITZ;
+#else
+  return n >= 12 && n <= 15;
+#endif
+}
+
 __host__ __device__ constexpr int colloc_minb(int n) {
 #ifdef SFK_COLLOC_MINB
   if (SFK_COLLOC_MINB >= 0) return SFK_COLLOC_MINB;   // A/B builds (tools/build_variant.py)
 #endif
+  if (colloc_splitz(n)) return n <= 13 ? 3 : n == 14 ? 0 : 2;
   return (n <= 7 || (n >= 9 && n <= 13) || n == 16) ? 2 : (n == 8 || n == 15) ? 0 : 1;
 }
 
@@ -78,6 +92,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
                                             const int* __restrict__ cmap) {
   using C = CollocCfg<N, CPB, SY, SX, CS>;
   constexpr int NN = C::NN, N3 = C::N3;
+  constexpr bool SPLITZ = colloc_splitz(N);
   extern __shared__ double smem[];
   constexpr int TH = WARPS ? 32 : C::THREADS;
   static_assert(!WARPS || CPB * NN <= 32, "warp mode needs CPB * n^2 <= 32");
@@ -154,7 +169,58 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
   sync();                     // ... and everybody's are visible
 
   // ---- phase 3: z-line (x=a, y=b): d_z u, flux, A_z = Dz^T f_z ---------
-  if (act) {
+  // SPLITZ (large n): three register-light passes over the thread's own
+  // lines instead of one fused loop (whose d_z input line + A_z accumulators
+  // + geometry needed 2n + 24 live doubles: 254 registers at n = 14, one CTA
+  // per SM): (a) d_z u written over the U line, (b) pointwise flux in place
+  // on the GX / GY / U lines, (c) Dz^T f_z over the U line.  Same operations
+  // in the same order per output (bit-identical to the fused loop).
+  if (SPLITZ && act) {
+    const int base = cb + a * SX + b * SY;
+    {
+      double ul[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) ul[i] = sU[base + i];
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        double gz = T.D[q] * ul[0];
+#pragma unroll
+        for (int i = 1; i < N; ++i) gz = fma(T.D[i * N + q], ul[i], gz);
+        sU[base + q] = gz;
+      }
+    }
+    {
+      HexLineAdj geo;
+      geo.setup(sC + c * 24, T.Bc[a], T.Bc[N + a], T.Bc[b], T.Bc[N + b]);
+      const double wxy = T.W[a] * T.W[b];
+      const double* kp = sK + base;
+#pragma unroll 1
+      for (int q = 0; q < N; ++q) {
+        double gx = sGX[base + q], gy = sGY[base + q], gz = sU[base + q];
+        double r0[3], r1[3], r2[3];
+        const double det = geo.adj(T.Bc[N + q], r0, r1, r2);
+        double s = (wxy * T.W[q]) * rcp64(fabs(det));
+        if (WEIGHTED) s *= kp[q];
+        laplace_flux(r0, r1, r2, s, gx, gy, gz);
+        sGX[base + q] = gx;
+        sGY[base + q] = gy;
+        sU[base + q] = gz;
+      }
+    }
+    {
+      double fz[N];
+#pragma unroll
+      for (int q = 0; q < N; ++q) fz[q] = sU[base + q];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double az = T.D[i * N] * fz[0];
+#pragma unroll
+        for (int q = 1; q < N; ++q) az = fma(T.D[i * N + q], fz[q], az);
+        sU[base + i] = az;
+      }
+    }
+  }
+  if (!SPLITZ && act) {
     const int base = cb + a * SX + b * SY;
     double ul[N], az[N];
 #pragma unroll
