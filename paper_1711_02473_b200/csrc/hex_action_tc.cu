@@ -25,10 +25,31 @@
 // bit 1 of the slower indices) instead of padding, which makes every
 // fragment load/store and the pointwise pass bank-conflict free with ~2%
 // padding.
+#include <type_traits>
+
 #include "async_copy.cuh"
 #include "hex_geometry.cuh"
 
 namespace sfk {
+
+// Pointwise geometry of the tc8 kernel: the direct HexLineGeom form (33
+// FP64 ops per point).  SFK_TC8_GEOM=0 selects HexLineAdj (adjugate rows as
+// polynomials in xi_z, 15 ops per point), which the line kernels use but
+// which measured slower here: p = 7 2.10 -> 2.35 ms (profiles/r01ch_*.jsonl).
+#ifndef SFK_TC8_GEOM
+#define SFK_TC8_GEOM 1
+#endif
+using TC8Geo = std::conditional<SFK_TC8_GEOM == 1, HexLineGeom, HexLineAdj>::type;
+template <class TT>
+__device__ __forceinline__ double tc8_adj(const HexLineGeom& g, const TT& T, int q, double r0[3],
+                                          double r1[3], double r2[3]) {
+  return g.adj(T.Bc[q], T.Bc[8 + q], r0, r1, r2);
+}
+template <class TT>
+__device__ __forceinline__ double tc8_adj(const HexLineAdj& g, const TT& T, int q, double r0[3],
+                                          double r1[3], double r2[3]) {
+  return g.adj(T.Bc[8 + q], r0, r1, r2);
+}
 
 __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -248,7 +269,7 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
       const int c = tid >> 6, r = tid & 63;
       const int qx = r & 7, qy = r >> 3;
       double* yl = sY + c * YC;
-      HexLineGeom geo;
+      TC8Geo geo;
       geo.setup(sC + c * 24, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
       const double wxy = T.W[qx] * T.W[qy];
 #pragma unroll 1
@@ -259,13 +280,13 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
         double2 gx = *reinterpret_cast<double2*>(p + 2 * YA);
         {
           double r0[3], r1[3], r2[3];
-          const double det = geo.adj(T.Bc[q], T.Bc[M + q], r0, r1, r2);
+          const double det = tc8_adj(geo, T, q, r0, r1, r2);
           const double s = (wxy * T.W[q]) * rcp64(fabs(det));
           laplace_flux(r0, r1, r2, s, gx.x, gy.x, gz.x);
         }
         {
           double r0[3], r1[3], r2[3];
-          const double det = geo.adj(T.Bc[q + 1], T.Bc[M + q + 1], r0, r1, r2);
+          const double det = tc8_adj(geo, T, q + 1, r0, r1, r2);
           const double s = (wxy * T.W[q + 1]) * rcp64(fabs(det));
           laplace_flux(r0, r1, r2, s, gx.y, gy.y, gz.y);
         }

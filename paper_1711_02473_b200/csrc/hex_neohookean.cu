@@ -25,7 +25,13 @@
 #include "async_copy.cuh"
 #include "hex_geometry.cuh"
 
+#ifndef SFK_NEO_YT
+#define SFK_NEO_YT 1
+#endif
+
 namespace sfk {
+
+constexpr bool NEO_YT = SFK_NEO_YT;
 
 template <int N, int M, int CPB>
 struct NeoCfg {
@@ -59,6 +65,10 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
                       const int* __restrict__ cmap = nullptr) {
   using C = NeoCfg<N, M, CPB>;
   constexpr int NN = C::NN, MN = C::MN, MM = C::MM, PX = C::PX, LZ = C::LZ;
+  // Y lines qy-major (as hex_action5.cu): the y / y^T stages' accesses
+  // (thread (qx, iz), iz fastest) become near-consecutive; the z-line
+  // threads keep their odd line stride.  SFK_NEO_YT=0 restores qx-major.
+  constexpr int QS = NEO_YT ? M * LZ : LZ;
   constexpr int XA = C::XA, YA = C::YA;
   constexpr int N3 = N * NN;
   constexpr int TH = WARPS ? 32 : C::THREADS;       // threads sharing one cell group
@@ -140,7 +150,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
         a0[i] = xi[i * N];
         a1[i] = xi[XA + i * N];
       }
-      double* yo = sY + c * C::YSZ + 3 * a * YA + qx * M * LZ + iz;
+      double* yo = sY + c * C::YSZ + 3 * a * YA + (NEO_YT ? qx * LZ : qx * M * LZ) + iz;
 #pragma unroll
       for (int q = 0; q < M; ++q) {
         double bb = T.B[q] * a0[0], bd = T.D[q] * a0[0], db = T.B[q] * a1[0];
@@ -150,9 +160,9 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
           bd = fma(T.D[i * M + q], a0[i], bd);
           db = fma(T.B[i * M + q], a1[i], db);
         }
-        yo[q * LZ] = bb;         // -> d/dz after z stage
-        yo[YA + q * LZ] = bd;    // -> d/dy
-        yo[2 * YA + q * LZ] = db;  // -> d/dx
+        yo[q * QS] = bb;         // -> d/dz after z stage
+        yo[YA + q * QS] = bd;    // -> d/dy
+        yo[2 * YA + q * QS] = db;  // -> d/dx
       }
     }
     sync();
@@ -161,7 +171,8 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
   // ---------------- z-lines: gradients, constitutive flux, transposed z ----
   if (tid < CPB * MM) {
     const int c = tid / MM, r = tid - c * MM;
-    const int qx = r / M, qy = r - qx * M;
+    const int r0 = r / M, r1 = r - r0 * M;
+    const int qx = NEO_YT ? r1 : r0, qy = NEO_YT ? r0 : r1;
     double* line = sY + c * C::YSZ + r * LZ;   // component a, slot k: line[(3a+k)*YA + .]
     // (1) reference gradients, in place: slots (0,1,2) <- (d_z, d_y, d_x)
 #pragma unroll 1
@@ -269,13 +280,13 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
     if (tid < CPB * MN) {
       const int c = tid / MN, r = tid - c * MN;
       const int qx = r / N, iz = r - qx * N;
-      const double* yi = sY + c * C::YSZ + 3 * a * YA + qx * M * LZ + iz;
+      const double* yi = sY + c * C::YSZ + 3 * a * YA + (NEO_YT ? qx * LZ : qx * M * LZ) + iz;
       double pz[M], py[M], px[M];
 #pragma unroll
       for (int q = 0; q < M; ++q) {
-        pz[q] = yi[q * LZ];
-        py[q] = yi[YA + q * LZ];
-        px[q] = yi[2 * YA + q * LZ];
+        pz[q] = yi[q * QS];
+        py[q] = yi[YA + q * QS];
+        px[q] = yi[2 * YA + q * QS];
       }
       double* xo = sX + c * C::XSZ + qx * PX + iz;
 #pragma unroll
