@@ -67,8 +67,11 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
   constexpr int NN = C::NN, MN = C::MN, MM = C::MM, PX = C::PX, LZ = C::LZ;
   // Y lines qy-major (as hex_action5.cu): the y / y^T stages' accesses
   // (thread (qx, iz), iz fastest) become near-consecutive; the z-line
-  // threads keep their odd line stride.  SFK_NEO_YT=0 restores qx-major.
-  constexpr int QS = NEO_YT ? M * LZ : LZ;
+  // threads keep their odd line stride.  On at n = 6 (p = 5: 1.311 -> 1.243
+  // ms; neutral at p = 3, 4, 6, slightly slower at p = 2 —
+  // profiles/r01ci_*.jsonl).  SFK_NEO_YT=0 restores qx-major everywhere.
+  constexpr bool NYT = NEO_YT && N == 6;
+  constexpr int QS = NYT ? M * LZ : LZ;
   constexpr int XA = C::XA, YA = C::YA;
   constexpr int N3 = N * NN;
   constexpr int TH = WARPS ? 32 : C::THREADS;       // threads sharing one cell group
@@ -150,7 +153,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
         a0[i] = xi[i * N];
         a1[i] = xi[XA + i * N];
       }
-      double* yo = sY + c * C::YSZ + 3 * a * YA + (NEO_YT ? qx * LZ : qx * M * LZ) + iz;
+      double* yo = sY + c * C::YSZ + 3 * a * YA + (NYT ? qx * LZ : qx * M * LZ) + iz;
 #pragma unroll
       for (int q = 0; q < M; ++q) {
         double bb = T.B[q] * a0[0], bd = T.D[q] * a0[0], db = T.B[q] * a1[0];
@@ -172,7 +175,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
   if (tid < CPB * MM) {
     const int c = tid / MM, r = tid - c * MM;
     const int r0 = r / M, r1 = r - r0 * M;
-    const int qx = NEO_YT ? r1 : r0, qy = NEO_YT ? r0 : r1;
+    const int qx = NYT ? r1 : r0, qy = NYT ? r0 : r1;
     double* line = sY + c * C::YSZ + r * LZ;   // component a, slot k: line[(3a+k)*YA + .]
     // (1) reference gradients, in place: slots (0,1,2) <- (d_z, d_y, d_x)
 #pragma unroll 1
@@ -280,7 +283,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
     if (tid < CPB * MN) {
       const int c = tid / MN, r = tid - c * MN;
       const int qx = r / N, iz = r - qx * N;
-      const double* yi = sY + c * C::YSZ + 3 * a * YA + (NEO_YT ? qx * LZ : qx * M * LZ) + iz;
+      const double* yi = sY + c * C::YSZ + 3 * a * YA + (NYT ? qx * LZ : qx * M * LZ) + iz;
       double pz[M], py[M], px[M];
 #pragma unroll
       for (int q = 0; q < M; ++q) {
