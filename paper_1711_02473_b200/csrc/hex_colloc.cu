@@ -24,6 +24,7 @@
 //      A_z = Dz^T f_z in registers, stored over its own U line
 //   4. x-lines: U += Dx^T f_x;   5. y-lines: U += Dy^T f_y
 //   6. coalesced copy U -> A
+#include <algorithm>
 #include <type_traits>
 
 #include "async_copy.cuh"
@@ -38,13 +39,29 @@ struct TabsD {
   double Bc[2 * N];
 };
 
+// Persistent CTAs with the next batch's u / kappa / coords prefetched by
+// cp.async while the current batch computes (one-shot CTAs load, then
+// compute: their load latency showed as 16% long-scoreboard stalls at p = 4,
+// profiles/r01cj_C3_p4.md).  Measured per n (profiles/r01ck_*.jsonl): only
+// n = 5 gains (p = 4 0.1167 -> 0.1127 ms); at n = 6..11 the doubled u /
+// kappa buffers cost occupancy and registers (p = 6..10 up to 44% slower).
+// SFK_COLLOC_PERSIST=n0 (A/B builds) makes every n <= n0 persistent.
+#ifdef SFK_COLLOC_PERSIST
+__host__ __device__ constexpr bool colloc_persist(int n) { return n <= SFK_COLLOC_PERSIST; }
+#else
+__host__ __device__ constexpr bool colloc_persist(int n) { return n == 5; }
+#endif
+
 template <int N, int CPB, int SY, int SX, int CS>
 struct CollocCfg {
   static constexpr int NN = N * N;
   static constexpr int N3 = N * N * N;
   static constexpr int THREADS = round_up(CPB * NN, 32);
-  static constexpr size_t smem(bool weighted) {
-    return (size_t)((weighted ? 4 : 3) * CPB * CS + CPB * 24) * sizeof(double);
+  static constexpr bool persist(int warps) { return warps == 0 && colloc_persist(N); }
+  static constexpr size_t smem(bool weighted, int warps = 0) {
+    return persist(warps)
+               ? (size_t)((weighted ? 6 : 4) * CPB * CS + 2 * CPB * 24) * sizeof(double)
+               : (size_t)((weighted ? 4 : 3) * CPB * CS + CPB * 24) * sizeof(double);
   }
 };
 
@@ -93,28 +110,36 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
   using C = CollocCfg<N, CPB, SY, SX, CS>;
   constexpr int NN = C::NN, N3 = C::N3;
   constexpr bool SPLITZ = colloc_splitz(N);
+  constexpr bool PERSIST = C::persist(WARPS);
   extern __shared__ double smem[];
   constexpr int TH = WARPS ? 32 : C::THREADS;
   static_assert(!WARPS || CPB * NN <= 32, "warp mode needs CPB * n^2 <= 32");
   const int grp = WARPS ? (int)(threadIdx.x >> 5) : 0;
-  double* sU = smem + (size_t)grp * (C::smem(WEIGHTED) / sizeof(double));
-  double* sGX = sU + CPB * CS;
+  // one-shot:   [U][GX][GY][coords][K]
+  // persistent: [U0][U1][GX][GY][coords0][coords1][K0][K1] (u, coords, kappa
+  //             of the next batch stream in while the current one computes)
+  double* base = smem + (size_t)grp * (C::smem(WEIGHTED, WARPS) / sizeof(double));
+  double* sGX = base + (PERSIST ? 2 : 1) * CPB * CS;
   double* sGY = sGX + CPB * CS;
-  double* sC = sGY + CPB * CS;
-  double* sK = sC + CPB * 24;   // kappa (WEIGHTED), same padded layout as U
+  double* sC0 = sGY + CPB * CS;
+  double* sK0 = sC0 + (PERSIST ? 2 : 1) * CPB * 24;
 
   const int tid = WARPS ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
   auto sync = [] { if (WARPS) __syncwarp(); else __syncthreads(); };
-  const int64_t cell0 = ((int64_t)blockIdx.x * (WARPS ? WARPS : 1) + grp) * CPB;
-  const int64_t rem = ncells - cell0;
-  const int ncb = rem < CPB ? (int)rem : CPB;
 
   // u (group 0) and kappa (group 1) stream into the padded shared layouts
-  // with cp.async; kappa is only needed by the pointwise phase, so its
-  // latency hides behind phase 2.
-  for (int i = tid; i < CPB * 24; i += TH)
-    sC[i] = i < ncb * 24 ? __ldg(coords + cell0 * 24 + i) : 0.0;
-  {
+  // with cp.async (one-shot mode: kappa is only needed by the pointwise
+  // phase, so its latency hides behind phase 2).
+  auto load = [&](int64_t cell0, int ncb, int buf) {
+    double* sU = base + buf * (CPB * CS);
+    double* sK = sK0 + buf * (CPB * CS);
+    double* sC = sC0 + buf * (CPB * 24);
+    if (PERSIST) {
+      for (int i = tid; i < ncb * 24; i += TH) cp_async8(sC + i, coords + cell0 * 24 + i);
+    } else {
+      for (int i = tid; i < CPB * 24; i += TH)
+        sC[i] = i < ncb * 24 ? __ldg(coords + cell0 * 24 + i) : 0.0;
+    }
     // consecutive threads copy consecutive doubles (coalesced global reads)
     const double* ug = u + cell0 * N3;
     for (int i = tid; i < ncb * N3; i += TH) {
@@ -131,175 +156,203 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
         cp_async8(sK + c * CS + x * SX + y * SY + z, kg + i);
       }
       cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
     }
-  }
-  sync();
+  };
 
-  const bool act = tid < CPB * NN;
-  const int c = tid / NN, r = tid - (tid / NN) * NN;
-  const int a = r / N, b = r - (r / N) * N;
-  const int cb = c * CS;
+  auto compute = [&](int64_t cell0, int ncb, int buf) {
+    double* sU = base + buf * (CPB * CS);
+    const double* sK = sK0 + buf * (CPB * CS);
+    const double* sC = sC0 + buf * (CPB * 24);
+    const bool act = tid < CPB * NN;
+    const int c = tid / NN, r = tid - (tid / NN) * NN;
+    const int a = r / N, b = r - (r / N) * N;
+    const int cb = c * CS;
 
-  // ---- phase 2: x-line (y=a, z=b) and y-line (x=a, z=b) ---------------
-  if (act) {
-    double ul[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) ul[i] = sU[cb + i * SX + a * SY + b];
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-      double g = T.D[q] * ul[0];
-#pragma unroll
-      for (int i = 1; i < N; ++i) g = fma(T.D[i * N + q], ul[i], g);
-      sGX[cb + q * SX + a * SY + b] = g;
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) ul[i] = sU[cb + a * SX + i * SY + b];
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-      double g = T.D[q] * ul[0];
-#pragma unroll
-      for (int i = 1; i < N; ++i) g = fma(T.D[i * N + q], ul[i], g);
-      sGY[cb + a * SX + q * SY + b] = g;
-    }
-  }
-  if (WEIGHTED) cp_async_wait<0>();   // kappa copies of this thread landed
-  sync();                     // ... and everybody's are visible
-
-  // ---- phase 3: z-line (x=a, y=b): d_z u, flux, A_z = Dz^T f_z ---------
-  // SPLITZ (large n): three register-light passes over the thread's own
-  // lines instead of one fused loop (whose d_z input line + A_z accumulators
-  // + geometry needed 2n + 24 live doubles: 254 registers at n = 14, one CTA
-  // per SM): (a) d_z u written over the U line, (b) pointwise flux in place
-  // on the GX / GY / U lines, (c) Dz^T f_z over the U line.  Same operations
-  // in the same order per output (bit-identical to the fused loop).
-  if (SPLITZ && act) {
-    const int base = cb + a * SX + b * SY;
-    {
+    // ---- phase 2: x-line (y=a, z=b) and y-line (x=a, z=b) ---------------
+    if (act) {
       double ul[N];
-#pragma unroll
-      for (int i = 0; i < N; ++i) ul[i] = sU[base + i];
-#pragma unroll
+  #pragma unroll
+      for (int i = 0; i < N; ++i) ul[i] = sU[cb + i * SX + a * SY + b];
+  #pragma unroll
       for (int q = 0; q < N; ++q) {
-        double gz = T.D[q] * ul[0];
-#pragma unroll
-        for (int i = 1; i < N; ++i) gz = fma(T.D[i * N + q], ul[i], gz);
-        sU[base + q] = gz;
+        double g = T.D[q] * ul[0];
+  #pragma unroll
+        for (int i = 1; i < N; ++i) g = fma(T.D[i * N + q], ul[i], g);
+        sGX[cb + q * SX + a * SY + b] = g;
+      }
+  #pragma unroll
+      for (int i = 0; i < N; ++i) ul[i] = sU[cb + a * SX + i * SY + b];
+  #pragma unroll
+      for (int q = 0; q < N; ++q) {
+        double g = T.D[q] * ul[0];
+  #pragma unroll
+        for (int i = 1; i < N; ++i) g = fma(T.D[i * N + q], ul[i], g);
+        sGY[cb + a * SX + q * SY + b] = g;
       }
     }
-    {
-      HexLineAdj geo;
+    if (WEIGHTED && !PERSIST) cp_async_wait<0>();   // kappa copies of this thread landed
+    sync();                     // ... and everybody's are visible
+
+    // ---- phase 3: z-line (x=a, y=b): d_z u, flux, A_z = Dz^T f_z ---------
+    // SPLITZ (large n): three register-light passes over the thread's own
+    // lines instead of one fused loop (whose d_z input line + A_z accumulators
+    // + geometry needed 2n + 24 live doubles: 254 registers at n = 14, one CTA
+    // per SM): (a) d_z u written over the U line, (b) pointwise flux in place
+    // on the GX / GY / U lines, (c) Dz^T f_z over the U line.  Same operations
+    // in the same order per output (bit-identical to the fused loop).
+    if (SPLITZ && act) {
+      const int base = cb + a * SX + b * SY;
+      {
+        double ul[N];
+  #pragma unroll
+        for (int i = 0; i < N; ++i) ul[i] = sU[base + i];
+  #pragma unroll
+        for (int q = 0; q < N; ++q) {
+          double gz = T.D[q] * ul[0];
+  #pragma unroll
+          for (int i = 1; i < N; ++i) gz = fma(T.D[i * N + q], ul[i], gz);
+          sU[base + q] = gz;
+        }
+      }
+      {
+        HexLineAdj geo;
+        geo.setup(sC + c * 24, T.Bc[a], T.Bc[N + a], T.Bc[b], T.Bc[N + b]);
+        const double wxy = T.W[a] * T.W[b];
+        const double* kp = sK + base;
+  #pragma unroll 1
+        for (int q = 0; q < N; ++q) {
+          double gx = sGX[base + q], gy = sGY[base + q], gz = sU[base + q];
+          double r0[3], r1[3], r2[3];
+          const double det = geo.adj(T.Bc[N + q], r0, r1, r2);
+          double s = (wxy * T.W[q]) * rcp64(fabs(det));
+          if (WEIGHTED) s *= kp[q];
+          laplace_flux(r0, r1, r2, s, gx, gy, gz);
+          sGX[base + q] = gx;
+          sGY[base + q] = gy;
+          sU[base + q] = gz;
+        }
+      }
+      {
+        double fz[N];
+  #pragma unroll
+        for (int q = 0; q < N; ++q) fz[q] = sU[base + q];
+  #pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double az = T.D[i * N] * fz[0];
+  #pragma unroll
+          for (int q = 1; q < N; ++q) az = fma(T.D[i * N + q], fz[q], az);
+          sU[base + i] = az;
+        }
+      }
+    }
+    if (!SPLITZ && act) {
+      const int base = cb + a * SX + b * SY;
+      double ul[N], az[N];
+  #pragma unroll
+      for (int i = 0; i < N; ++i) {
+        ul[i] = sU[base + i];
+        az[i] = 0.0;
+      }
+      // precomputed adjugate polynomials (hex_geometry.cuh) except at n = 15, 16,
+      // where their 9 extra registers per thread cost more than they save
+      // (same-box A/B, profiles/r01ai_*)
+      using Geo = typename std::conditional<(N == 15 || N == 16), HexLineGeom, HexLineAdj>::type;
+      Geo geo;
       geo.setup(sC + c * 24, T.Bc[a], T.Bc[N + a], T.Bc[b], T.Bc[N + b]);
       const double wxy = T.W[a] * T.W[b];
       const double* kp = sK + base;
-#pragma unroll 1
+  #pragma unroll
       for (int q = 0; q < N; ++q) {
-        double gx = sGX[base + q], gy = sGY[base + q], gz = sU[base + q];
+        double gz = T.D[q] * ul[0];
+  #pragma unroll
+        for (int i = 1; i < N; ++i) gz = fma(T.D[i * N + q], ul[i], gz);
+        double gx = sGX[base + q], gy = sGY[base + q];
         double r0[3], r1[3], r2[3];
-        const double det = geo.adj(T.Bc[N + q], r0, r1, r2);
+        double det;
+        if constexpr (N == 15 || N == 16) det = geo.adj(T.Bc[q], T.Bc[N + q], r0, r1, r2);
+        else det = geo.adj(T.Bc[N + q], r0, r1, r2);
         double s = (wxy * T.W[q]) * rcp64(fabs(det));
         if (WEIGHTED) s *= kp[q];
         laplace_flux(r0, r1, r2, s, gx, gy, gz);
         sGX[base + q] = gx;
         sGY[base + q] = gy;
-        sU[base + q] = gz;
+  #pragma unroll
+        for (int i = 0; i < N; ++i) az[i] = fma(T.D[i * N + q], gz, az[i]);
       }
+  #pragma unroll
+      for (int i = 0; i < N; ++i) sU[base + i] = az[i];
     }
-    {
-      double fz[N];
-#pragma unroll
-      for (int q = 0; q < N; ++q) fz[q] = sU[base + q];
-#pragma unroll
+    sync();
+
+    // ---- phase 4: x-lines (y=a, z=b): U += Dx^T f_x ----------------------
+    if (act) {
+      double fl[N];
+  #pragma unroll
+      for (int q = 0; q < N; ++q) fl[q] = sGX[cb + q * SX + a * SY + b];
+  #pragma unroll
       for (int i = 0; i < N; ++i) {
-        double az = T.D[i * N] * fz[0];
-#pragma unroll
-        for (int q = 1; q < N; ++q) az = fma(T.D[i * N + q], fz[q], az);
-        sU[base + i] = az;
+        double s = T.D[i * N] * fl[0];
+  #pragma unroll
+        for (int q = 1; q < N; ++q) s = fma(T.D[i * N + q], fl[q], s);
+        sU[cb + i * SX + a * SY + b] += s;
       }
     }
-  }
-  if (!SPLITZ && act) {
-    const int base = cb + a * SX + b * SY;
-    double ul[N], az[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      ul[i] = sU[base + i];
-      az[i] = 0.0;
-    }
-    // precomputed adjugate polynomials (hex_geometry.cuh) except at n = 15, 16,
-    // where their 9 extra registers per thread cost more than they save
-    // (same-box A/B, profiles/r01ai_*)
-    using Geo = typename std::conditional<(N == 15 || N == 16), HexLineGeom, HexLineAdj>::type;
-    Geo geo;
-    geo.setup(sC + c * 24, T.Bc[a], T.Bc[N + a], T.Bc[b], T.Bc[N + b]);
-    const double wxy = T.W[a] * T.W[b];
-    const double* kp = sK + base;
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-      double gz = T.D[q] * ul[0];
-#pragma unroll
-      for (int i = 1; i < N; ++i) gz = fma(T.D[i * N + q], ul[i], gz);
-      double gx = sGX[base + q], gy = sGY[base + q];
-      double r0[3], r1[3], r2[3];
-      double det;
-      if constexpr (N == 15 || N == 16) det = geo.adj(T.Bc[q], T.Bc[N + q], r0, r1, r2);
-      else det = geo.adj(T.Bc[N + q], r0, r1, r2);
-      double s = (wxy * T.W[q]) * rcp64(fabs(det));
-      if (WEIGHTED) s *= kp[q];
-      laplace_flux(r0, r1, r2, s, gx, gy, gz);
-      sGX[base + q] = gx;
-      sGY[base + q] = gy;
-#pragma unroll
-      for (int i = 0; i < N; ++i) az[i] = fma(T.D[i * N + q], gz, az[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) sU[base + i] = az[i];
-  }
-  sync();
+    sync();
 
-  // ---- phase 4: x-lines (y=a, z=b): U += Dx^T f_x ----------------------
-  if (act) {
-    double fl[N];
-#pragma unroll
-    for (int q = 0; q < N; ++q) fl[q] = sGX[cb + q * SX + a * SY + b];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double s = T.D[i * N] * fl[0];
-#pragma unroll
-      for (int q = 1; q < N; ++q) s = fma(T.D[i * N + q], fl[q], s);
-      sU[cb + i * SX + a * SY + b] += s;
+    // ---- phase 5: y-lines (x=a, z=b): U += Dy^T f_y ----------------------
+    if (act) {
+      double fl[N];
+  #pragma unroll
+      for (int q = 0; q < N; ++q) fl[q] = sGY[cb + a * SX + q * SY + b];
+  #pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double s = T.D[i * N] * fl[0];
+  #pragma unroll
+        for (int q = 1; q < N; ++q) s = fma(T.D[i * N + q], fl[q], s);
+        sU[cb + a * SX + i * SY + b] += s;
+      }
     }
-  }
-  sync();
+    sync();
 
-  // ---- phase 5: y-lines (x=a, z=b): U += Dy^T f_y ----------------------
-  if (act) {
-    double fl[N];
-#pragma unroll
-    for (int q = 0; q < N; ++q) fl[q] = sGY[cb + a * SX + q * SY + b];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double s = T.D[i * N] * fl[0];
-#pragma unroll
-      for (int q = 1; q < N; ++q) s = fma(T.D[i * N + q], fl[q], s);
-      sU[cb + a * SX + i * SY + b] += s;
+    {
+      // coalesced write-back: consecutive threads take consecutive elements of
+      // the batch; the (c, x, y, z) decomposition is incremental per thread
+      double* ag = A + cell0 * N3;
+      for (int i = tid; i < ncb * N3; i += TH) {
+        const int cc = i / N3, rr = i - cc * N3;
+        const int x = rr / NN, yz = rr - x * NN, y = yz / N, z = yz - y * N;
+        if (GS) atomicAdd(A + __ldg(cmap + cell0 * N3 + i), sU[cc * CS + x * SX + y * SY + z]);
+        else ag[i] = sU[cc * CS + x * SX + y * SY + z];
+      }
     }
-  }
-  sync();
+  };
 
-  {
-    // coalesced write-back: consecutive threads take consecutive elements of
-    // the batch; the (c, x, y, z) decomposition is incremental per thread
-    double* ag = A + cell0 * N3;
-    for (int i = tid; i < ncb * N3; i += TH) {
-      const int cc = i / N3, rr = i - cc * N3;
-      const int x = rr / NN, yz = rr - x * NN, y = yz / N, z = yz - y * N;
-      if (GS) atomicAdd(A + __ldg(cmap + cell0 * N3 + i), sU[cc * CS + x * SX + y * SY + z]);
-      else ag[i] = sU[cc * CS + x * SX + y * SY + z];
+  const int64_t ngroups = (ncells + CPB - 1) / CPB;   // cell batches
+  if (PERSIST) {
+    int64_t bt = blockIdx.x;
+    auto nb_of = [&](int64_t bb) {
+      const int64_t rem = ncells - bb * CPB;
+      return rem < CPB ? (int)rem : CPB;
+    };
+    if (bt < ngroups) load(bt * CPB, nb_of(bt), 0);
+    for (int k = 0; bt < ngroups; bt += gridDim.x, ++k) {
+      const int cur = k & 1;
+      cp_async_wait<0>();
+      sync();   // this batch landed; the previous batch's write-back is done
+      if (bt + gridDim.x < ngroups) load((bt + gridDim.x) * CPB, nb_of(bt + gridDim.x), cur ^ 1);
+      compute(bt * CPB, nb_of(bt), cur);
     }
+  } else {
+    const int64_t cell0 = ((int64_t)blockIdx.x * (WARPS ? WARPS : 1) + grp) * CPB;
+    const int64_t rem = ncells - cell0;
+    const int ncb = rem < CPB ? (int)rem : CPB;
+    load(cell0, ncb, 0);
+    if (WEIGHTED) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    sync();
+    compute(cell0, ncb, 0);
   }
+  (void)ngroups;
 }
 
 template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, int MINB, bool GS, int WARPS>
@@ -342,20 +395,30 @@ static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* 
     T.Bc[q] = p->Bc[q];
     T.Bc[N + q] = p->Bc[N + q];
   }
-  const int64_t grid = (ncells + CPB * G - 1) / (CPB * G);
+  int64_t grid = (ncells + CPB * G - 1) / (CPB * G);
   cudaError_t e;
+  // persistent mode: one resident wave of CTAs looping over the batches
+  auto resident = [&](auto k, size_t smem_bytes) -> int64_t {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem_bytes);
+    return (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  };
   if (kappa) {
     auto k = colloc_kernel<N, CPB, SY, SX, CS, true, GS, WARPS>();
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(G * C::smem(true)));
+    const size_t sm = G * C::smem(true, WARPS);
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
-    k<<<(unsigned)grid, THREADS, G * C::smem(true), s>>>(T, ncells, coords, u, kappa, A, cmap);
+    if (C::persist(WARPS)) grid = std::min(grid, resident(k, sm));
+    if (grid > 0) k<<<(unsigned)grid, THREADS, sm, s>>>(T, ncells, coords, u, kappa, A, cmap);
   } else {
     auto k = colloc_kernel<N, CPB, SY, SX, CS, false, GS, WARPS>();
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(G * C::smem(false)));
+    const size_t sm = G * C::smem(false, WARPS);
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
-    k<<<(unsigned)grid, THREADS, G * C::smem(false), s>>>(T, ncells, coords, u, nullptr, A, cmap);
+    if (C::persist(WARPS)) grid = std::min(grid, resident(k, sm));
+    if (grid > 0) k<<<(unsigned)grid, THREADS, sm, s>>>(T, ncells, coords, u, nullptr, A, cmap);
   }
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_colloc_action_kernel launch");

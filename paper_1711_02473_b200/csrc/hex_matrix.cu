@@ -30,6 +30,10 @@
 
 #include "hex_geometry.cuh"
 
+#ifndef SFK_MAT_ZB
+#define SFK_MAT_ZB 1   // batched-pair Z phase at n <= 3 (A/B builds: 0)
+#endif
+
 namespace sfk {
 
 template <int N, int M>
@@ -85,6 +89,7 @@ hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncell
                           const int32_t* __restrict__ col_idx, const int32_t* __restrict__ emap) {
   using C = MatCfg<N, M, CPB>;
   constexpr int N2 = C::N2, N3 = C::N3, N4 = C::N4, M3 = C::M3;
+  constexpr bool ZB = SFK_MAT_ZB && N <= 3;
   extern __shared__ double smem[];
   double* sZ = smem;                       // [CPB][9][M][M][N2]
   double* sK = sZ + CPB * C::ZS;           // [CPB][6][M3]
@@ -139,7 +144,42 @@ hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncell
   }
   __syncthreads();
   // ---- Z_ll'[qx][qy][iz][jz]: threads over (cell, pair, qx, qy, iz, jz) -----
-  for (int t = tid; t < CPB * C::ZS; t += C::THREADS) {
+  // ZB (small n): threads over (cell, qx, qy, iz, jz), all 9 pairs per
+  // thread — the index arithmetic and the K / table loads are shared by the
+  // pairs (at n = 3 the per-entry form was issue-bound on integer work:
+  // FP64 pipe 29%, profiles/r01cj_C5_p2.md).  Same products, same order.
+  if (ZB) {
+    constexpr int PL = M * M * N2;   // one pair's plane block
+    for (int t = tid; t < CPB * PL; t += C::THREADS) {
+      const int cc = t / PL, q2 = t - cc * PL;
+      const int qxy = q2 / N2, zz = q2 - qxy * N2;
+      const int a = zz / N, b = zz - a * N;
+      double ta[2][M], tb[2][M], kk[6][M];
+#pragma unroll
+      for (int qz = 0; qz < M; ++qz) {
+        ta[0][qz] = sT[a * M + qz];
+        ta[1][qz] = sT[N * M + a * M + qz];
+        tb[0][qz] = sT[b * M + qz];
+        tb[1][qz] = sT[N * M + b * M + qz];
+      }
+      const double* k = sK + cc * C::KS + qxy * M;
+#pragma unroll
+      for (int e = 0; e < 6; ++e)
+#pragma unroll
+        for (int qz = 0; qz < M; ++qz) kk[e][qz] = k[e * M3 + qz];
+      double* zo = sZ + cc * C::ZS + q2;
+#pragma unroll
+      for (int pair = 0; pair < 9; ++pair) {
+        const int l = pair / 3, lp = pair - 3 * l;
+        double z = 0.0;
+#pragma unroll
+        for (int qz = 0; qz < M; ++qz)
+          z = fma(ta[l == 2][qz] * tb[lp == 2][qz], kk[ksym(l, lp)][qz], z);
+        zo[pair * PL] = z;
+      }
+    }
+  }
+  for (int t = tid; !ZB && t < CPB * C::ZS; t += C::THREADS) {
     const int cc = t / C::ZS, rr = t - cc * C::ZS;
     const int pair = rr / (M * M * N2), q2 = rr - pair * (M * M * N2);
     const int qxy = q2 / N2, zz = q2 - qxy * N2;
