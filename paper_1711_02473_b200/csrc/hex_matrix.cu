@@ -33,6 +33,12 @@
 #ifndef SFK_MAT_ZB
 #define SFK_MAT_ZB 1   // batched-pair Z phase at n <= 3 (A/B builds: 0)
 #endif
+#ifndef SFK_MAT_YB
+#define SFK_MAT_YB 1   // all-jy Y phase at n <= 3 (A/B builds: 0)
+#endif
+#ifndef SFK_MAT_MINB3
+#define SFK_MAT_MINB3 0   // min CTAs/SM of the n = 3 kernel (A/B builds)
+#endif
 
 namespace sfk {
 
@@ -82,7 +88,7 @@ __device__ __forceinline__ int64_t csr_find(const int32_t* __restrict__ col_idx,
 //              matrix (values A, pattern row_ptr / col_idx from sfk_csr_create)
 //              through cell_dofs — the local matrix never reaches HBM.
 template <int N, int M, int CPB, bool CSR, bool YMAP = false>
-__global__ void __launch_bounds__(MatCfg<N, M, CPB>::THREADS)
+__global__ void __launch_bounds__(MatCfg<N, M, CPB>::THREADS, N == 3 ? SFK_MAT_MINB3 : 0)
 hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncells,
                           const double* __restrict__ coords, double* __restrict__ A,
                           const int32_t* __restrict__ dofs, const int64_t* __restrict__ row_ptr,
@@ -90,6 +96,7 @@ hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncell
   using C = MatCfg<N, M, CPB>;
   constexpr int N2 = C::N2, N3 = C::N3, N4 = C::N4, M3 = C::M3;
   constexpr bool ZB = SFK_MAT_ZB && N <= 3;
+  constexpr bool YB = SFK_MAT_YB && N <= 3 && !YMAP;
   extern __shared__ double smem[];
   double* sZ = smem;                       // [CPB][9][M][M][N2]
   double* sK = sZ + CPB * C::ZS;           // [CPB][6][M3]
@@ -195,7 +202,59 @@ hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncell
   }
   __syncthreads();
   // ---- y contraction into the 4 x-pattern groups, every plane ---------------
-  if (act) {
+  // ZB (small n): threads over (cell, qx, iy, iz, jz), every jy per thread:
+  // the 9 M z-values of (qx, iz, jz) are loaded once for the N jy outputs
+  // (the per-(iy,iz,jy,jz) form issued one shared load per FMA).  Same
+  // accumulation order per output.
+  if (YB) {
+    constexpr int YT = M * N3;   // work items per cell
+    for (int t = tid; t < CPB * YT; t += C::THREADS) {
+      const int cc = t / YT, w = t - cc * YT;
+      const int qx = w / N3, w2 = w - qx * N3;
+      const int yi = w2 / N2, w3 = w2 - yi * N2;
+      const int zi = w3 / N, zj = w3 - zi * N;
+      const double* z = sZ + cc * C::ZS + qx * M * N2 + zi * N + zj;
+      double zv[9][M];
+#pragma unroll
+      for (int pr = 0; pr < 9; ++pr)
+#pragma unroll
+        for (int qy = 0; qy < M; ++qy) zv[pr][qy] = z[pr * M * M * N2 + qy * N2];
+      double bi[M], di[M];
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        bi[q] = sT[yi * M + q];
+        di[q] = sT[N * M + yi * M + q];
+      }
+#pragma unroll
+      for (int yj = 0; yj < N; ++yj) {
+        double pyj[4][M];
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+          const double bj = sT[yj * M + q], dj = sT[N * M + yj * M + q];
+          pyj[0][q] = bi[q] * bj;
+          pyj[1][q] = bi[q] * dj;
+          pyj[2][q] = di[q] * bj;
+          pyj[3][q] = di[q] * dj;
+        }
+        double yg[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int l = 0; l < 3; ++l)
+#pragma unroll
+          for (int lp = 0; lp < 3; ++lp) {
+            const int pat = (l == 1 ? 2 : 0) + (lp == 1 ? 1 : 0);
+            const int grp = (l == 0 ? 2 : 0) + (lp == 0 ? 1 : 0);
+#pragma unroll
+            for (int qy = 0; qy < M; ++qy)
+              yg[grp] = fma(pyj[pat][qy], zv[l * 3 + lp][qy], yg[grp]);
+          }
+        // r = (iy, iz, jy, jz) in the non-YMAP thread order of phase B
+        double* y = sY + cc * C::YS + qx * N4 + ((yi * N + zi) * N + yj) * N + zj;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) y[g * M * N4] = yg[g];
+      }
+    }
+  }
+  if (!YB && act) {
     double py[4][M];
 #pragma unroll
     for (int q = 0; q < M; ++q) {
