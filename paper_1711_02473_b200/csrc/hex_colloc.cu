@@ -52,6 +52,15 @@ __host__ __device__ constexpr bool colloc_persist(int n) { return n <= SFK_COLLO
 __host__ __device__ constexpr bool colloc_persist(int n) { return n == 5; }
 #endif
 
+// KG: kappa read from global memory (through L1/L2) in the pointwise phase
+// instead of being staged in shared memory — drops one of the four N^3
+// arrays, so n = 16 (139 -> 104 KB per CTA) fits two CTAs per SM.
+#ifdef SFK_COLLOC_KG
+__host__ __device__ constexpr bool colloc_kg(int n) { return n >= SFK_COLLOC_KG; }
+#else
+__host__ __device__ constexpr bool colloc_kg(int n) { return n == 16; }
+#endif
+
 template <int N, int CPB, int SY, int SX, int CS>
 struct CollocCfg {
   static constexpr int NN = N * N;
@@ -61,7 +70,7 @@ struct CollocCfg {
   static constexpr size_t smem(bool weighted, int warps = 0) {
     return persist(warps)
                ? (size_t)((weighted ? 6 : 4) * CPB * CS + 2 * CPB * 24) * sizeof(double)
-               : (size_t)((weighted ? 4 : 3) * CPB * CS + CPB * 24) * sizeof(double);
+               : (size_t)((weighted && !colloc_kg(N) ? 4 : 3) * CPB * CS + CPB * 24) * sizeof(double);
   }
 };
 
@@ -111,6 +120,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
   constexpr int NN = C::NN, N3 = C::N3;
   constexpr bool SPLITZ = colloc_splitz(N);
   constexpr bool PERSIST = C::persist(WARPS);
+  constexpr bool KG = WEIGHTED && colloc_kg(N) && !PERSIST;
   extern __shared__ double smem[];
   constexpr int TH = WARPS ? 32 : C::THREADS;
   static_assert(!WARPS || CPB * NN <= 32, "warp mode needs CPB * n^2 <= 32");
@@ -148,7 +158,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
       cp_async8(sU + c * CS + x * SX + y * SY + z, GS ? u + __ldg(cmap + cell0 * N3 + i) : ug + i);
     }
     cp_async_commit();
-    if (WEIGHTED) {
+    if (WEIGHTED && !KG) {
       const double* kg = kappa + cell0 * N3;
       for (int i = tid; i < ncb * N3; i += TH) {
         const int c = i / N3, r = i - c * N3;
@@ -218,14 +228,14 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
         HexLineAdj geo;
         geo.setup(sC + c * 24, T.Bc[a], T.Bc[N + a], T.Bc[b], T.Bc[N + b]);
         const double wxy = T.W[a] * T.W[b];
-        const double* kp = sK + base;
+        const double* kp = KG ? kappa + (cell0 + c) * N3 + a * NN + b * N : sK + base;
   #pragma unroll 1
         for (int q = 0; q < N; ++q) {
           double gx = sGX[base + q], gy = sGY[base + q], gz = sU[base + q];
           double r0[3], r1[3], r2[3];
           const double det = geo.adj(T.Bc[N + q], r0, r1, r2);
           double s = (wxy * T.W[q]) * rcp64(fabs(det));
-          if (WEIGHTED) s *= kp[q];
+          if (WEIGHTED) s *= KG ? __ldg(kp + q) : kp[q];
           laplace_flux(r0, r1, r2, s, gx, gy, gz);
           sGX[base + q] = gx;
           sGY[base + q] = gy;
@@ -260,7 +270,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
       Geo geo;
       geo.setup(sC + c * 24, T.Bc[a], T.Bc[N + a], T.Bc[b], T.Bc[N + b]);
       const double wxy = T.W[a] * T.W[b];
-      const double* kp = sK + base;
+      const double* kp = KG ? kappa + (cell0 + c) * N3 + a * NN + b * N : sK + base;
   #pragma unroll
       for (int q = 0; q < N; ++q) {
         double gz = T.D[q] * ul[0];
@@ -272,7 +282,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
         if constexpr (N == 15 || N == 16) det = geo.adj(T.Bc[q], T.Bc[N + q], r0, r1, r2);
         else det = geo.adj(T.Bc[N + q], r0, r1, r2);
         double s = (wxy * T.W[q]) * rcp64(fabs(det));
-        if (WEIGHTED) s *= kp[q];
+        if (WEIGHTED) s *= KG ? __ldg(kp + q) : kp[q];
         laplace_flux(r0, r1, r2, s, gx, gy, gz);
         sGX[base + q] = gx;
         sGY[base + q] = gy;
@@ -347,7 +357,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
     const int64_t rem = ncells - cell0;
     const int ncb = rem < CPB ? (int)rem : CPB;
     load(cell0, ncb, 0);
-    if (WEIGHTED) cp_async_wait<1>();
+    if (WEIGHTED && !KG) cp_async_wait<1>();
     else cp_async_wait<0>();
     sync();
     compute(cell0, ncb, 0);
