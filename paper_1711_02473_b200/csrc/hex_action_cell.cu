@@ -1,0 +1,236 @@
+// Hex Q_p Laplace action, one thread per cell at small n — BASELINE C2 at
+// p = 2 (n = m = 3) and, measured, p = 3.
+//
+// Same math and reference mapping as the other C2 kernels (forms.py:186-189,
+// 235-243; passes.py:672-743 schedule; scheduling.py:617-738 emitted
+// kernel).  The line kernels (v4 at p = 2) give each lane one 1D line per
+// stage: 3 cells x 9 lines = 27 of 32 lanes busy, lines re-dealt through
+// shared memory between stages.  Here a thread owns a whole cell and runs the
+// pipeline in slices, so nothing is exchanged between threads (no barrier,
+// every lane busy, u / coords / A straight from / to HBM):
+//   (A) per iz-slice: the x contraction of the n x n (ix, iy) dofs (in
+//       registers) feeds the y contraction at once; the 3 y-outputs
+//       (BB, BD, DB) of the slice go to this thread's private shared-memory
+//       block Y[3][qx][qy][iz] (stride n^3*3 + 1 doubles per thread: odd, so
+//       the per-thread 64-bit accesses of a warp are conflict-free);
+//   (B) per z-line (qx, qy): z contraction, per-point geometry + Laplace
+//       flux (HexLineAdj), transposed z — written back in place;
+//   (C) per iz-slice: transposed y (registers) feeding transposed x, and the
+//       n^2 results of the slice stored to A.
+// Occupancy is bounded by the private Y block (3 n^3 doubles per thread).
+#include <cstdint>
+#include <cstdlib>
+
+#include "hex_geometry.cuh"
+
+namespace sfk {
+
+template <int N>
+struct CellCfg {
+  static constexpr int N3 = N * N * N;
+  static constexpr int YS = 3 * N3 + 1;          // per-thread Y block (odd stride)
+};
+
+template <int N, int TH, int MINB>
+__global__ void __launch_bounds__(TH, MINB)
+hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
+                        const double* __restrict__ coords, const double* __restrict__ u,
+                        double* __restrict__ A) {
+  constexpr bool PAIRS = true;
+  constexpr int M = N, NN = N * N, N3 = CellCfg<N>::N3, YS = CellCfg<N>::YS;
+  constexpr int S1 = N3;                           // slot stride in Y
+  extern __shared__ double smem[];
+  double* Y = smem + threadIdx.x * YS;             // [3][qx][qy][iz] at ((qx*M+qy)*N+iz)
+  const int64_t cell = (int64_t)blockIdx.x * TH + threadIdx.x;
+  if (cell >= ncells) return;
+  double X[24];   // this cell's coords, in registers (the geometry setup runs per z-line)
+  {
+    const double* cg = coords + cell * 24;
+    if ((reinterpret_cast<uintptr_t>(cg) & 15) == 0) {
+#pragma unroll
+      for (int k = 0; k < 12; ++k) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(cg) + k);
+        X[2 * k] = v.x;
+        X[2 * k + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 24; ++k) X[k] = __ldg(cg + k);
+    }
+  }
+  const double* uc = u + cell * N3;
+
+  // (A) forward x + y, one iz-slice at a time
+#pragma unroll 1
+  for (int iz = 0; iz < N; ++iz) {
+    double ux[N][N];   // [ix][iy]
+#pragma unroll
+    for (int ix = 0; ix < N; ++ix)
+#pragma unroll
+      for (int iy = 0; iy < N; ++iy) ux[ix][iy] = __ldg(uc + (ix * N + iy) * N + iz);
+    double x0[M][N], x1[M][N];   // [qx][iy]: Bx u, Dx u
+#pragma unroll
+    for (int qx = 0; qx < M; ++qx)
+#pragma unroll
+      for (int iy = 0; iy < N; ++iy) {
+        double b = TBP(qx) * ux[0][iy], d = TDP(qx) * ux[0][iy];
+#pragma unroll
+        for (int ix = 1; ix < N; ++ix) {
+          b = fma(TBP(ix * M + qx), ux[ix][iy], b);
+          d = fma(TDP(ix * M + qx), ux[ix][iy], d);
+        }
+        x0[qx][iy] = b;
+        x1[qx][iy] = d;
+      }
+#pragma unroll
+    for (int qx = 0; qx < M; ++qx)
+#pragma unroll
+      for (int qy = 0; qy < M; ++qy) {
+        double bb = TBP(qy) * x0[qx][0], bd = TDP(qy) * x0[qx][0], db = TBP(qy) * x1[qx][0];
+#pragma unroll
+        for (int iy = 1; iy < N; ++iy) {
+          bb = fma(TBP(iy * M + qy), x0[qx][iy], bb);
+          bd = fma(TDP(iy * M + qy), x0[qx][iy], bd);
+          db = fma(TBP(iy * M + qy), x1[qx][iy], db);
+        }
+        const int o = (qx * M + qy) * N + iz;
+        Y[o] = bb;
+        Y[S1 + o] = bd;
+        Y[2 * S1 + o] = db;
+      }
+  }
+
+  // (B) z-lines: gradients, pointwise flux, transposed z, in place
+#pragma unroll 1
+  for (int l = 0; l < M * M; ++l) {
+    const int qx = l / M, qy = l - qx * M;
+    double* yl = Y + l * N;
+    double bb[N], bd[N], db[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      bb[i] = yl[i];
+      bd[i] = yl[S1 + i];
+      db[i] = yl[2 * S1 + i];
+    }
+    double gz[M], gy[M], gx[M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) {
+      gz[q] = TDP(q) * bb[0];
+      gy[q] = TBP(q) * bd[0];
+      gx[q] = TBP(q) * db[0];
+#pragma unroll
+      for (int i = 1; i < N; ++i) {
+        gz[q] = fma(TDP(i * M + q), bb[i], gz[q]);
+        gy[q] = fma(TBP(i * M + q), bd[i], gy[q]);
+        gx[q] = fma(TBP(i * M + q), db[i], gx[q]);
+      }
+    }
+    HexLineAdj geo;
+    geo.setup(X, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
+    const double wxy = T.W[qx] * T.W[qy];
+#pragma unroll
+    for (int q = 0; q < M; ++q) {
+      double r0[3], r1[3], r2[3];
+      const double det = geo.adj(T.Bc[M + q], r0, r1, r2);
+      const double s = (wxy * T.W[q]) * rcp64(fabs(det));
+      laplace_flux(r0, r1, r2, s, gx[q], gy[q], gz[q]);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double sz = TDP(i * M) * gz[0], sy = TBP(i * M) * gy[0], sx = TBP(i * M) * gx[0];
+#pragma unroll
+      for (int q = 1; q < M; ++q) {
+        sz = fma(TDP(i * M + q), gz[q], sz);
+        sy = fma(TBP(i * M + q), gy[q], sy);
+        sx = fma(TBP(i * M + q), gx[q], sx);
+      }
+      yl[i] = sz;
+      yl[S1 + i] = sy;
+      yl[2 * S1 + i] = sx;
+    }
+  }
+
+  // (C) transposed y + x, one iz-slice at a time
+  double* ac = A + cell * N3;
+#pragma unroll 1
+  for (int iz = 0; iz < N; ++iz) {
+    double r1[M][N], r2[M][N];   // [qx][iy]: By^T Sx, Dy^T Sy + By^T Sz
+#pragma unroll
+    for (int qx = 0; qx < M; ++qx) {
+      double pz[M], py[M], px[M];
+#pragma unroll
+      for (int qy = 0; qy < M; ++qy) {
+        const int o = (qx * M + qy) * N + iz;
+        pz[qy] = Y[o];
+        py[qy] = Y[S1 + o];
+        px[qy] = Y[2 * S1 + o];
+      }
+#pragma unroll
+      for (int iy = 0; iy < N; ++iy) {
+        double a = TBP(iy * M) * px[0], b = TDP(iy * M) * py[0], c = TBP(iy * M) * pz[0];
+#pragma unroll
+        for (int qy = 1; qy < M; ++qy) {
+          a = fma(TBP(iy * M + qy), px[qy], a);
+          b = fma(TDP(iy * M + qy), py[qy], b);
+          c = fma(TBP(iy * M + qy), pz[qy], c);
+        }
+        r1[qx][iy] = a;
+        r2[qx][iy] = b + c;
+      }
+    }
+#pragma unroll
+    for (int ix = 0; ix < N; ++ix)
+#pragma unroll
+      for (int iy = 0; iy < N; ++iy) {
+        double a = TDP(ix * M) * r1[0][iy], b = TBP(ix * M) * r2[0][iy];
+#pragma unroll
+        for (int qx = 1; qx < M; ++qx) {
+          a = fma(TDP(ix * M + qx), r1[qx][iy], a);
+          b = fma(TBP(ix * M + qx), r2[qx][iy], b);
+        }
+        ac[(ix * N + iy) * N + iz] = a + b;
+      }
+  }
+}
+
+template <int N, int TH, int MINB>
+static int launch_cell(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                       const double* u, cudaStream_t s) {
+  constexpr size_t SMEM = (size_t)TH * CellCfg<N>::YS * sizeof(double);
+  auto kern = hex_laplace_action_cell<N, TH, MINB>;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_action_cell)");
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    init = true;
+  }
+  const TabsBD<N, N> T = make_tabs_bd<N, N>(p);
+  const int64_t grid = (ncells + TH - 1) / TH;
+  if (grid > 0) kern<<<(unsigned)grid, TH, SMEM, s>>>(T, ncells, coords, u, A);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "hex_laplace_action_cell launch");
+}
+
+// Threads per CTA: SFK_CELL_TH overrides (tuning runs only).
+int launch_hex_action_cell(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                           const double* w0, cudaStream_t s) {
+  if (p->n != p->m) return SFK_EUNSUPPORTED;
+  static const int th = [] {
+    const char* e = getenv("SFK_CELL_TH");
+    return e ? atoi(e) : 0;
+  }();
+  switch (p->n) {
+    case 3:
+      if (th == 128) return launch_cell<3, 128, 1>(p, ncells, A, coords, w0, s);
+      if (th == 96) return launch_cell<3, 96, 1>(p, ncells, A, coords, w0, s);
+      return launch_cell<3, 64, 1>(p, ncells, A, coords, w0, s);
+    case 4:
+      if (th == 64) return launch_cell<4, 64, 1>(p, ncells, A, coords, w0, s);
+      return launch_cell<4, 32, 1>(p, ncells, A, coords, w0, s);
+    default: return SFK_EUNSUPPORTED;
+  }
+}
+
+}  // namespace sfk

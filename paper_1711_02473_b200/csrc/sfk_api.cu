@@ -58,6 +58,7 @@ static int c2_variant() {
     if (e && strcmp(e, "cell") == 0) v = 5;
     if (e && strcmp(e, "v4") == 0) v = 6;
     if (e && strcmp(e, "v5") == 0) v = 7;
+    if (e && strcmp(e, "cellv") == 0) v = 8;
   }
   return v;
 }
@@ -83,6 +84,10 @@ static int launch_c2(const sfk_plan* p, int64_t ncells, double* A, const double*
   int v = c2_variant();
   if (v == 0) v = c2_auto(p->n);
   int rc = SFK_EUNSUPPORTED;
+  if (v == 8) {
+    rc = launch_hex_action_cell(p, ncells, A, coords, w0, s);
+    if (rc == SFK_EUNSUPPORTED) v = 3;
+  }
   if (v == 7) {
     rc = launch_hex_action_v5(p, ncells, A, coords, w0, s);
     if (rc == SFK_EUNSUPPORTED) v = 2;

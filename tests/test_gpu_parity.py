@@ -341,7 +341,7 @@ def test_c2_every_kernel_generation(cuda, p):
         "err = (np.abs(out-ref).max(axis=1)/np.abs(ref).max(axis=1)).max();"
         "print(err); assert err < 1e-12"
     ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), p, p)
-    gens = [(g, {}) for g in ("v1", "v2", "v3", "v4", "tc", "cell", "v5")]
+    gens = [(g, {}) for g in ("v1", "v2", "v3", "v4", "tc", "cell", "v5", "cellv")]
     gens += [("v5", {"SFK_C2_G": g}) for g in ("1", "2", "3")]
     for gen, extra in gens:
         env = dict(os.environ, SFK_C2_KERNEL=gen, **extra)
