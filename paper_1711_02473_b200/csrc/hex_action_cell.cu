@@ -28,7 +28,7 @@ namespace sfk {
 template <int N>
 struct CellCfg {
   static constexpr int N3 = N * N * N;
-  static constexpr int YS = 3 * N3 + 1;          // per-thread Y block (odd stride)
+  static constexpr int YS = (3 * N3) | 1;        // per-thread Y block (odd stride)
 };
 
 template <int N, int TH, int MINB>
@@ -59,15 +59,20 @@ hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
     }
   }
   const double* uc = u + cell * N3;
+  // the whole cell's dofs in flight at once (the slice order would touch
+  // every sector of the cell's 8 N^3 bytes N times)
+  double ua[N3];
+#pragma unroll
+  for (int k = 0; k < N3; ++k) ua[k] = __ldg(uc + k);
 
   // (A) forward x + y, one iz-slice at a time
-#pragma unroll 1
+#pragma unroll
   for (int iz = 0; iz < N; ++iz) {
     double ux[N][N];   // [ix][iy]
 #pragma unroll
     for (int ix = 0; ix < N; ++ix)
 #pragma unroll
-      for (int iy = 0; iy < N; ++iy) ux[ix][iy] = __ldg(uc + (ix * N + iy) * N + iz);
+      for (int iy = 0; iy < N; ++iy) ux[ix][iy] = ua[(ix * N + iy) * N + iz];
     double x0[M][N], x1[M][N];   // [qx][iy]: Bx u, Dx u
 #pragma unroll
     for (int qx = 0; qx < M; ++qx)
@@ -221,10 +226,17 @@ int launch_hex_action_cell(const sfk_plan* p, int64_t ncells, double* A, const d
     const char* e = getenv("SFK_CELL_TH");
     return e ? atoi(e) : 0;
   }();
+  static const int minb = [] {
+    const char* e = getenv("SFK_CELL_MINB");
+    return e ? atoi(e) : 0;
+  }();
   switch (p->n) {
     case 3:
+      // 64 threads per CTA (profiles/r01cs_*.jsonl: 0.1008 ms vs 0.1071 / 0.1032
+      // at 96 / 128); SFK_CELL_MINB=5 caps registers for a 5th CTA per SM
       if (th == 128) return launch_cell<3, 128, 1>(p, ncells, A, coords, w0, s);
       if (th == 96) return launch_cell<3, 96, 1>(p, ncells, A, coords, w0, s);
+      if (minb == 5) return launch_cell<3, 64, 5>(p, ncells, A, coords, w0, s);
       return launch_cell<3, 64, 1>(p, ncells, A, coords, w0, s);
     case 4:
       if (th == 64) return launch_cell<4, 64, 1>(p, ncells, A, coords, w0, s);

@@ -66,7 +66,7 @@ static int c2_variant() {
 static int c2_auto(int n) {
   switch (n) {
     case 2: return 5;
-    case 3: return 6;
+    case 3: return 8;   // thread-per-cell over v4: 0.1245 -> 0.1115 ms (profiles/r01cq_*.jsonl)
     case 4: return 6;
     case 5: return 3;
     // v5 (grouped outputs) over v2: p = 5 1.043 -> 0.985, p = 6 1.685 -> 1.621,
