@@ -21,7 +21,12 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "async_copy.cuh"
 #include "hex_geometry.cuh"
+
+#ifndef SFK_CELL_STAGE
+#define SFK_CELL_STAGE 1
+#endif
 
 namespace sfk {
 
@@ -37,14 +42,176 @@ hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
                         const double* __restrict__ coords, const double* __restrict__ u,
                         double* __restrict__ A) {
   constexpr bool PAIRS = true;
-  constexpr int M = N, NN = N * N, N3 = CellCfg<N>::N3, YS = CellCfg<N>::YS;
+  constexpr bool STAGE = SFK_CELL_STAGE;
+  constexpr int M = N, N3 = CellCfg<N>::N3, YS = CellCfg<N>::YS;
   constexpr int S1 = N3;                           // slot stride in Y
   extern __shared__ double smem[];
   double* Y = smem + threadIdx.x * YS;             // [3][qx][qy][iz] at ((qx*M+qy)*N+iz)
-  const int64_t cell = (int64_t)blockIdx.x * TH + threadIdx.x;
-  if (cell >= ncells) return;
+  // STAGE: the CTA's u block (TH cells x N^3, contiguous in HBM) is copied
+  // to shared memory with coalesced 16-byte cp.async, and A leaves the same
+  // way; per-thread rows of N^3 doubles (odd for n = 3: conflict-free reads)
+  double* sU = smem + TH * YS;
+  const int64_t cell0 = (int64_t)blockIdx.x * TH;
+  const int64_t cell = cell0 + threadIdx.x;
+  const int ncb = (int)((ncells - cell0) < TH ? (ncells - cell0) : TH);
+  if (STAGE) {
+    async_copy<TH>(sU, u + cell0 * N3, ncb * N3, threadIdx.x);
+    cp_async_commit();
+  }
   double X[24];   // this cell's coords, in registers (the geometry setup runs per z-line)
-  {
+  auto cell_pipeline = [&]() {
+    const double* uc = u + cell * N3;
+    // the whole cell's dofs in flight at once (the slice order would touch
+    // every sector of the cell's 8 N^3 bytes N times)
+    double ua[N3];
+    if (STAGE) {
+#pragma unroll
+      for (int k = 0; k < N3; ++k) ua[k] = sU[threadIdx.x * N3 + k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < N3; ++k) ua[k] = __ldg(uc + k);
+    }
+
+    // (A) forward x + y, one iz-slice at a time
+#pragma unroll
+    for (int iz = 0; iz < N; ++iz) {
+      double ux[N][N];   // [ix][iy]
+#pragma unroll
+      for (int ix = 0; ix < N; ++ix)
+#pragma unroll
+        for (int iy = 0; iy < N; ++iy) ux[ix][iy] = ua[(ix * N + iy) * N + iz];
+      double x0[M][N], x1[M][N];   // [qx][iy]: Bx u, Dx u
+#pragma unroll
+      for (int qx = 0; qx < M; ++qx)
+#pragma unroll
+        for (int iy = 0; iy < N; ++iy) {
+          double b = TBP(qx) * ux[0][iy], d = TDP(qx) * ux[0][iy];
+#pragma unroll
+          for (int ix = 1; ix < N; ++ix) {
+            b = fma(TBP(ix * M + qx), ux[ix][iy], b);
+            d = fma(TDP(ix * M + qx), ux[ix][iy], d);
+          }
+          x0[qx][iy] = b;
+          x1[qx][iy] = d;
+        }
+#pragma unroll
+      for (int qx = 0; qx < M; ++qx)
+#pragma unroll
+        for (int qy = 0; qy < M; ++qy) {
+          double bb = TBP(qy) * x0[qx][0], bd = TDP(qy) * x0[qx][0], db = TBP(qy) * x1[qx][0];
+#pragma unroll
+          for (int iy = 1; iy < N; ++iy) {
+            bb = fma(TBP(iy * M + qy), x0[qx][iy], bb);
+            bd = fma(TDP(iy * M + qy), x0[qx][iy], bd);
+            db = fma(TBP(iy * M + qy), x1[qx][iy], db);
+          }
+          const int o = (qx * M + qy) * N + iz;
+          Y[o] = bb;
+          Y[S1 + o] = bd;
+          Y[2 * S1 + o] = db;
+        }
+    }
+
+    // (B) z-lines: gradients, pointwise flux, transposed z, in place
+#pragma unroll 1
+    for (int l = 0; l < M * M; ++l) {
+      const int qx = l / M, qy = l - qx * M;
+      double* yl = Y + l * N;
+      double bb[N], bd[N], db[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        bb[i] = yl[i];
+        bd[i] = yl[S1 + i];
+        db[i] = yl[2 * S1 + i];
+      }
+      double gz[M], gy[M], gx[M];
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        gz[q] = TDP(q) * bb[0];
+        gy[q] = TBP(q) * bd[0];
+        gx[q] = TBP(q) * db[0];
+#pragma unroll
+        for (int i = 1; i < N; ++i) {
+          gz[q] = fma(TDP(i * M + q), bb[i], gz[q]);
+          gy[q] = fma(TBP(i * M + q), bd[i], gy[q]);
+          gx[q] = fma(TBP(i * M + q), db[i], gx[q]);
+        }
+      }
+      HexLineAdj geo;
+      geo.setup(X, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
+      const double wxy = T.W[qx] * T.W[qy];
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        double r0[3], r1[3], r2[3];
+        const double det = geo.adj(T.Bc[M + q], r0, r1, r2);
+        const double s = (wxy * T.W[q]) * rcp64(fabs(det));
+        laplace_flux(r0, r1, r2, s, gx[q], gy[q], gz[q]);
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double sz = TDP(i * M) * gz[0], sy = TBP(i * M) * gy[0], sx = TBP(i * M) * gx[0];
+#pragma unroll
+        for (int q = 1; q < M; ++q) {
+          sz = fma(TDP(i * M + q), gz[q], sz);
+          sy = fma(TBP(i * M + q), gy[q], sy);
+          sx = fma(TBP(i * M + q), gx[q], sx);
+        }
+        yl[i] = sz;
+        yl[S1 + i] = sy;
+        yl[2 * S1 + i] = sx;
+      }
+    }
+
+    // (C) transposed y + x, one iz-slice at a time
+    double* ac = A + cell * N3;
+#pragma unroll 1
+    for (int iz = 0; iz < N; ++iz) {
+      double r1[M][N], r2[M][N];   // [qx][iy]: By^T Sx, Dy^T Sy + By^T Sz
+#pragma unroll
+      for (int qx = 0; qx < M; ++qx) {
+        double pz[M], py[M], px[M];
+#pragma unroll
+        for (int qy = 0; qy < M; ++qy) {
+          const int o = (qx * M + qy) * N + iz;
+          pz[qy] = Y[o];
+          py[qy] = Y[S1 + o];
+          px[qy] = Y[2 * S1 + o];
+        }
+#pragma unroll
+        for (int iy = 0; iy < N; ++iy) {
+          double a = TBP(iy * M) * px[0], b = TDP(iy * M) * py[0], c = TBP(iy * M) * pz[0];
+#pragma unroll
+          for (int qy = 1; qy < M; ++qy) {
+            a = fma(TBP(iy * M + qy), px[qy], a);
+            b = fma(TDP(iy * M + qy), py[qy], b);
+            c = fma(TBP(iy * M + qy), pz[qy], c);
+          }
+          r1[qx][iy] = a;
+          r2[qx][iy] = b + c;
+        }
+      }
+#pragma unroll
+      for (int ix = 0; ix < N; ++ix)
+#pragma unroll
+        for (int iy = 0; iy < N; ++iy) {
+          double a = TDP(ix * M) * r1[0][iy], b = TBP(ix * M) * r2[0][iy];
+#pragma unroll
+          for (int qx = 1; qx < M; ++qx) {
+            a = fma(TDP(ix * M + qx), r1[qx][iy], a);
+            b = fma(TBP(ix * M + qx), r2[qx][iy], b);
+          }
+          if (STAGE) sU[threadIdx.x * N3 + (ix * N + iy) * N + iz] = a + b;
+          else ac[(ix * N + iy) * N + iz] = a + b;
+        }
+    }
+  };
+  // (coords staged like u through the Y region measured slower: 0.081 ->
+  // 0.090 ms, profiles/r01cv_*.jsonl — they are read as 16-byte vectors)
+  if (STAGE) {
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  if (cell < ncells) {
     const double* cg = coords + cell * 24;
     if ((reinterpret_cast<uintptr_t>(cg) & 15) == 0) {
 #pragma unroll
@@ -58,150 +225,27 @@ hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
       for (int k = 0; k < 24; ++k) X[k] = __ldg(cg + k);
     }
   }
-  const double* uc = u + cell * N3;
-  // the whole cell's dofs in flight at once (the slice order would touch
-  // every sector of the cell's 8 N^3 bytes N times)
-  double ua[N3];
-#pragma unroll
-  for (int k = 0; k < N3; ++k) ua[k] = __ldg(uc + k);
-
-  // (A) forward x + y, one iz-slice at a time
-#pragma unroll
-  for (int iz = 0; iz < N; ++iz) {
-    double ux[N][N];   // [ix][iy]
-#pragma unroll
-    for (int ix = 0; ix < N; ++ix)
-#pragma unroll
-      for (int iy = 0; iy < N; ++iy) ux[ix][iy] = ua[(ix * N + iy) * N + iz];
-    double x0[M][N], x1[M][N];   // [qx][iy]: Bx u, Dx u
-#pragma unroll
-    for (int qx = 0; qx < M; ++qx)
-#pragma unroll
-      for (int iy = 0; iy < N; ++iy) {
-        double b = TBP(qx) * ux[0][iy], d = TDP(qx) * ux[0][iy];
-#pragma unroll
-        for (int ix = 1; ix < N; ++ix) {
-          b = fma(TBP(ix * M + qx), ux[ix][iy], b);
-          d = fma(TDP(ix * M + qx), ux[ix][iy], d);
-        }
-        x0[qx][iy] = b;
-        x1[qx][iy] = d;
-      }
-#pragma unroll
-    for (int qx = 0; qx < M; ++qx)
-#pragma unroll
-      for (int qy = 0; qy < M; ++qy) {
-        double bb = TBP(qy) * x0[qx][0], bd = TDP(qy) * x0[qx][0], db = TBP(qy) * x1[qx][0];
-#pragma unroll
-        for (int iy = 1; iy < N; ++iy) {
-          bb = fma(TBP(iy * M + qy), x0[qx][iy], bb);
-          bd = fma(TDP(iy * M + qy), x0[qx][iy], bd);
-          db = fma(TBP(iy * M + qy), x1[qx][iy], db);
-        }
-        const int o = (qx * M + qy) * N + iz;
-        Y[o] = bb;
-        Y[S1 + o] = bd;
-        Y[2 * S1 + o] = db;
-      }
-  }
-
-  // (B) z-lines: gradients, pointwise flux, transposed z, in place
-#pragma unroll 1
-  for (int l = 0; l < M * M; ++l) {
-    const int qx = l / M, qy = l - qx * M;
-    double* yl = Y + l * N;
-    double bb[N], bd[N], db[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      bb[i] = yl[i];
-      bd[i] = yl[S1 + i];
-      db[i] = yl[2 * S1 + i];
+  if (cell < ncells) cell_pipeline();
+  if (STAGE) {
+    __syncthreads();   // every live thread's row is in sU
+    double* ag = A + cell0 * N3;
+    const bool al = ((reinterpret_cast<uintptr_t>(ag)) & 15) == 0;
+    const int n = ncb * N3;
+    if (al) {
+      for (int i = threadIdx.x; i < n / 2; i += TH)
+        reinterpret_cast<double2*>(ag)[i] = reinterpret_cast<const double2*>(sU)[i];
+      if ((n & 1) && threadIdx.x == 0) ag[n - 1] = sU[n - 1];
+    } else {
+      for (int i = threadIdx.x; i < n; i += TH) ag[i] = sU[i];
     }
-    double gz[M], gy[M], gx[M];
-#pragma unroll
-    for (int q = 0; q < M; ++q) {
-      gz[q] = TDP(q) * bb[0];
-      gy[q] = TBP(q) * bd[0];
-      gx[q] = TBP(q) * db[0];
-#pragma unroll
-      for (int i = 1; i < N; ++i) {
-        gz[q] = fma(TDP(i * M + q), bb[i], gz[q]);
-        gy[q] = fma(TBP(i * M + q), bd[i], gy[q]);
-        gx[q] = fma(TBP(i * M + q), db[i], gx[q]);
-      }
-    }
-    HexLineAdj geo;
-    geo.setup(X, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
-    const double wxy = T.W[qx] * T.W[qy];
-#pragma unroll
-    for (int q = 0; q < M; ++q) {
-      double r0[3], r1[3], r2[3];
-      const double det = geo.adj(T.Bc[M + q], r0, r1, r2);
-      const double s = (wxy * T.W[q]) * rcp64(fabs(det));
-      laplace_flux(r0, r1, r2, s, gx[q], gy[q], gz[q]);
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double sz = TDP(i * M) * gz[0], sy = TBP(i * M) * gy[0], sx = TBP(i * M) * gx[0];
-#pragma unroll
-      for (int q = 1; q < M; ++q) {
-        sz = fma(TDP(i * M + q), gz[q], sz);
-        sy = fma(TBP(i * M + q), gy[q], sy);
-        sx = fma(TBP(i * M + q), gx[q], sx);
-      }
-      yl[i] = sz;
-      yl[S1 + i] = sy;
-      yl[2 * S1 + i] = sx;
-    }
-  }
-
-  // (C) transposed y + x, one iz-slice at a time
-  double* ac = A + cell * N3;
-#pragma unroll 1
-  for (int iz = 0; iz < N; ++iz) {
-    double r1[M][N], r2[M][N];   // [qx][iy]: By^T Sx, Dy^T Sy + By^T Sz
-#pragma unroll
-    for (int qx = 0; qx < M; ++qx) {
-      double pz[M], py[M], px[M];
-#pragma unroll
-      for (int qy = 0; qy < M; ++qy) {
-        const int o = (qx * M + qy) * N + iz;
-        pz[qy] = Y[o];
-        py[qy] = Y[S1 + o];
-        px[qy] = Y[2 * S1 + o];
-      }
-#pragma unroll
-      for (int iy = 0; iy < N; ++iy) {
-        double a = TBP(iy * M) * px[0], b = TDP(iy * M) * py[0], c = TBP(iy * M) * pz[0];
-#pragma unroll
-        for (int qy = 1; qy < M; ++qy) {
-          a = fma(TBP(iy * M + qy), px[qy], a);
-          b = fma(TDP(iy * M + qy), py[qy], b);
-          c = fma(TBP(iy * M + qy), pz[qy], c);
-        }
-        r1[qx][iy] = a;
-        r2[qx][iy] = b + c;
-      }
-    }
-#pragma unroll
-    for (int ix = 0; ix < N; ++ix)
-#pragma unroll
-      for (int iy = 0; iy < N; ++iy) {
-        double a = TDP(ix * M) * r1[0][iy], b = TBP(ix * M) * r2[0][iy];
-#pragma unroll
-        for (int qx = 1; qx < M; ++qx) {
-          a = fma(TDP(ix * M + qx), r1[qx][iy], a);
-          b = fma(TBP(ix * M + qx), r2[qx][iy], b);
-        }
-        ac[(ix * N + iy) * N + iz] = a + b;
-      }
   }
 }
 
 template <int N, int TH, int MINB>
 static int launch_cell(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                        const double* u, cudaStream_t s) {
-  constexpr size_t SMEM = (size_t)TH * CellCfg<N>::YS * sizeof(double);
+  constexpr size_t SMEM =
+      (size_t)TH * (CellCfg<N>::YS + (SFK_CELL_STAGE ? CellCfg<N>::N3 : 0)) * sizeof(double);
   auto kern = hex_laplace_action_cell<N, TH, MINB>;
   static bool init = false;
   if (!init) {

@@ -14,6 +14,10 @@
 #include "async_copy.cuh"
 #include "hex_geometry.cuh"
 
+#ifndef SFK_P1_MINB
+#define SFK_P1_MINB 3   // CTAs per SM the register budget allows (A/B builds)
+#endif
+
 namespace sfk {
 
 namespace p1 {
@@ -27,7 +31,7 @@ constexpr size_t SMEM = (size_t)CPB * (CS + US) * sizeof(double);
 // item 1): u = x gathered through cmap[c][0..7], A = y scatter-added with
 // fp64 atomics.
 template <bool GS>
-__global__ void __launch_bounds__(p1::CPB, 3)
+__global__ void __launch_bounds__(p1::CPB, SFK_P1_MINB)
 hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
                       double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
