@@ -24,6 +24,9 @@
 // 128-bit (B, D) table pairs measured slower here (p=5 1.03 -> 1.6 ms):
 // separate B / D tables
 #define SFK_TAB_PAIRS 0
+#ifndef SFK_V3_MINB5
+#define SFK_V3_MINB5 2   // min CTAs/SM at n = 5 (A/B builds; 3 spills: 0.508 -> 0.615 ms, r01da_*)
+#endif
 #ifndef SFK_V3_YT
 #define SFK_V3_YT 1
 #endif
@@ -363,7 +366,7 @@ static int dispatch_v3(const sfk_plan* p, int64_t ncells, double* A, const doubl
     case 2: return launch_v3<Act3Layout<2, 2, 64, 2, 6, 28, 3, 6, 36>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
     case 3: return launch_v3<Act3Layout<3, 3, 32, 3, 19, 121, 3, 9, 91>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
     case 4: return launch_v3<Act3Layout<4, 4, 16, 4, 20, 160, 5, 20, 240>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
-    case 5: return launch_v3<Act3Layout<5, 5, 10, 5, 37, 377, 5, 25, 381>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
+    case 5: return launch_v3<Act3Layout<5, 5, 10, 5, 37, 377, 5, 25, 381>, SFK_V3_MINB5, GS>(p, ncells, A, coords, w0, s, cmap);
     case 6: return launch_v3<Act3Layout<6, 6, 8, 6, 38, 468, 9, 54, 980>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
     case 7: return launch_v3<Act3Layout<7, 7, 5, 7, 55, 785, 9, 63, 1337>, 2, GS>(p, ncells, A, coords, w0, s, cmap);
     case 8: return launch_v3<Act3Layout<8, 8, 4, 8, 72, 1152, 9, 72, 1728>, 2, GS>(p, ncells, A, coords, w0, s, cmap);

@@ -455,7 +455,8 @@ int launch_hex_action_v5(const sfk_plan* p, int64_t ncells, double* A, const dou
     case 6:
       // CPB 7 = 256 threads (register cap 128: (B, D) pairs fit) over CPB 8
       // = 288 threads (cap 96: no pairs): 0.995 -> 0.947 ms with G = 1
-      // (profiles/r01cb_*.jsonl); SFK_V5_CPB6=8 selects the latter
+      // (profiles/r01cb_*.jsonl); SFK_V5_CPB6=8 selects the latter.  6 cells
+      // per CTA at 3 CTAs/SM spill (80-register cap): 1.07 ms (r01cz_*)
       if (cpb6_env == 8) return pick_v5<6, 8, 1, false>(g_env, p, ncells, A, coords, w0, s);
       return pick_v5<6, 7, 1>(g_env, p, ncells, A, coords, w0, s);
     case 7: return pick_v5<7, 5, 2>(g_env, p, ncells, A, coords, w0, s);
