@@ -404,6 +404,8 @@ int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, con
   if (!force_v3 && p->n == p->m) {
     if (p->n == 2 && (reinterpret_cast<uintptr_t>(cmap) & 15) == 0)   // int4 map loads
       return launch_hex_action_p1_gs(p, ncells, cmap, x, y, coords, s);
+    if (p->n == 3 && !force_v3_small() && !force_v2)
+      return launch_hex_action_cell_gs(p, ncells, cmap, x, y, coords, s);
     if ((p->n == 3 || p->n == 4) && !force_v3_small())
       return launch_hex_action_v4_gs(p, ncells, cmap, x, y, coords, s);
     if ((p->n == 6 || p->n == 7 || p->n == 9) && !force_v2)

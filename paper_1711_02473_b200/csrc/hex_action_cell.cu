@@ -36,13 +36,17 @@ struct CellCfg {
   static constexpr int YS = (3 * N3) | 1;        // per-thread Y block (odd stride)
 };
 
-template <int N, int TH, int MINB>
+// GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
+// item 1): `u` is x, `A` is y; the CTA's block of the cell -> dof map
+// (int32, contiguous) is staged in the u area, each thread gathers its
+// cell's x values through it and scatter-adds its results with fp64 atomics.
+template <int N, int TH, int MINB, bool GS = false>
 __global__ void __launch_bounds__(TH, MINB)
 hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
                         const double* __restrict__ coords, const double* __restrict__ u,
-                        double* __restrict__ A) {
+                        double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
   constexpr bool PAIRS = true;
-  constexpr bool STAGE = SFK_CELL_STAGE;
+  constexpr bool STAGE = SFK_CELL_STAGE || GS;
   constexpr int M = N, N3 = CellCfg<N>::N3, YS = CellCfg<N>::YS;
   constexpr int S1 = N3;                           // slot stride in Y
   extern __shared__ double smem[];
@@ -54,7 +58,11 @@ hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
   const int64_t cell0 = (int64_t)blockIdx.x * TH;
   const int64_t cell = cell0 + threadIdx.x;
   const int ncb = (int)((ncells - cell0) < TH ? (ncells - cell0) : TH);
-  if (STAGE) {
+  int* sMap = reinterpret_cast<int*>(sU);          // GS: [thread][N3] int32
+  if (GS) {
+    for (int i = threadIdx.x; i < ncb * N3; i += TH) cp_async4(sMap + i, cmap + cell0 * N3 + i);
+    cp_async_commit();
+  } else if (STAGE) {
     async_copy<TH>(sU, u + cell0 * N3, ncb * N3, threadIdx.x);
     cp_async_commit();
   }
@@ -64,7 +72,10 @@ hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
     // the whole cell's dofs in flight at once (the slice order would touch
     // every sector of the cell's 8 N^3 bytes N times)
     double ua[N3];
-    if (STAGE) {
+    if (GS) {
+#pragma unroll
+      for (int k = 0; k < N3; ++k) ua[k] = __ldg(u + sMap[threadIdx.x * N3 + k]);
+    } else if (STAGE) {
 #pragma unroll
       for (int k = 0; k < N3; ++k) ua[k] = sU[threadIdx.x * N3 + k];
     } else {
@@ -200,7 +211,8 @@ hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
             a = fma(TDP(ix * M + qx), r1[qx][iy], a);
             b = fma(TBP(ix * M + qx), r2[qx][iy], b);
           }
-          if (STAGE) sU[threadIdx.x * N3 + (ix * N + iy) * N + iz] = a + b;
+          if (GS) atomicAdd(A + sMap[threadIdx.x * N3 + (ix * N + iy) * N + iz], a + b);
+          else if (STAGE) sU[threadIdx.x * N3 + (ix * N + iy) * N + iz] = a + b;
           else ac[(ix * N + iy) * N + iz] = a + b;
         }
     }
@@ -226,7 +238,7 @@ hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
     }
   }
   if (cell < ncells) cell_pipeline();
-  if (STAGE) {
+  if (STAGE && !GS) {
     __syncthreads();   // every live thread's row is in sU
     double* ag = A + cell0 * N3;
     const bool al = ((reinterpret_cast<uintptr_t>(ag)) & 15) == 0;
@@ -241,12 +253,12 @@ hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
   }
 }
 
-template <int N, int TH, int MINB>
+template <int N, int TH, int MINB, bool GS = false>
 static int launch_cell(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                       const double* u, cudaStream_t s) {
+                       const double* u, cudaStream_t s, const int* cmap = nullptr) {
   constexpr size_t SMEM =
-      (size_t)TH * (CellCfg<N>::YS + (SFK_CELL_STAGE ? CellCfg<N>::N3 : 0)) * sizeof(double);
-  auto kern = hex_laplace_action_cell<N, TH, MINB>;
+      (size_t)TH * (CellCfg<N>::YS + (SFK_CELL_STAGE || GS ? CellCfg<N>::N3 : 0)) * sizeof(double);
+  auto kern = hex_laplace_action_cell<N, TH, MINB, GS>;
   static bool init = false;
   if (!init) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -257,7 +269,7 @@ static int launch_cell(const sfk_plan* p, int64_t ncells, double* A, const doubl
   }
   const TabsBD<N, N> T = make_tabs_bd<N, N>(p);
   const int64_t grid = (ncells + TH - 1) / TH;
-  if (grid > 0) kern<<<(unsigned)grid, TH, SMEM, s>>>(T, ncells, coords, u, A);
+  if (grid > 0) kern<<<(unsigned)grid, TH, SMEM, s>>>(T, ncells, coords, u, A, cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_cell launch");
 }
@@ -287,6 +299,13 @@ int launch_hex_action_cell(const sfk_plan* p, int64_t ncells, double* A, const d
       return launch_cell<4, 32, 1>(p, ncells, A, coords, w0, s);
     default: return SFK_EUNSUPPORTED;
   }
+}
+
+// Global operator through the thread-per-cell kernel at n = 3.
+int launch_hex_action_cell_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                              double* y, const double* coords, cudaStream_t s) {
+  if (p->n != 3 || p->m != 3) return SFK_EUNSUPPORTED;
+  return launch_cell<3, 64, 1, true>(p, ncells, y, coords, x, s, cmap);
 }
 
 }  // namespace sfk

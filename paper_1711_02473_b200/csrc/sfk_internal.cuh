@@ -118,6 +118,8 @@ int launch_hex_colloc_gs(const sfk_plan* p, int64_t ncells, const int* cmap, con
                          double* y, const double* coords, const double* kappa, cudaStream_t s);
 int launch_hex_action_v5_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                             double* y, const double* coords, cudaStream_t s);
+int launch_hex_action_cell_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                              double* y, const double* coords, cudaStream_t s);
 int launch_hex_action_cell(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                            const double* w0, cudaStream_t s);
 int launch_hex_action_v5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
