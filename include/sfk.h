@@ -197,6 +197,20 @@ int sfk_csr_entry_map(const sfk_csr *pattern, int64_t ncells, int ndofs_per_cell
 int sfk_csr_destroy(sfk_csr *pattern);
 
 /*
+ * values[nnz] += sum_c P_c^T A_c P_c for DENSE per-cell matrices
+ * cell_matrices[ncells][nd][nd] (test index outer — the reference's return
+ * layout, forms.py:402-408) produced by ANY kernel: a hand-written family or
+ * a generated LoopProgram (every registry matrix form, any cell / degree /
+ * vector layout).  Positions from entry_map (sfk_csr_entry_map) when
+ * non-NULL, else a binary search per entry in row_ptr / col_idx.  DEVICE
+ * pointers, stream-ordered, fp64 atomics.  Replaces: the caller's insertion
+ * loop around any emitted matrix kernel.
+ */
+int sfk_csr_insert(int64_t ncells, int ndofs_per_cell, const double *cell_matrices,
+                   const int32_t *cell_dofs, const int64_t *row_ptr, const int32_t *col_idx,
+                   const int32_t *entry_map, double *values, void *stream);
+
+/*
  * values[nnz] += the assembled hex Laplace stiffness matrix: the C5 kernel
  * (plan kind SFK_KIND_LAPLACE_MATRIX, p <= 4) computes each cell matrix in
  * shared memory/registers and scatter-adds it straight into the CSR values

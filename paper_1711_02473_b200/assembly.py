@@ -31,7 +31,7 @@ from .errors import NativeError, ShapeMismatch
 
 __all__ = ["lattice_dof_map", "lattice_vector_dof_map", "lattice_boundary_mask",
            "GlobalOperator", "cg",
-           "CsrPattern", "assemble_csr"]
+           "CsrPattern", "assemble_csr", "insert_csr", "assemble_csr_from"]
 
 
 def lattice_dof_map(nx, ny, nz, degree, ix_range=None):
@@ -298,3 +298,53 @@ def assemble_csr(plan, cell_dofs, coords, pattern, values=None, entry_map=None, 
             entry_map.data_ptr() if entry_map is not None else None, values.data_ptr(), stream))
     return values
 
+
+def insert_csr(cell_matrices, cell_dofs, pattern, values=None, entry_map=None, stream=None):
+    """values += sum_c P_c^T A_c P_c for dense cell matrices (C, nd*nd) or
+    (C, nd, nd) float64 CUDA, test index outer — what any matrix kernel
+    returns (a hand-written family or a generated LoopProgram), so every
+    registry matrix form on every cell can be assembled (``sfk_csr_insert``:
+    one fp64 atomic per entry, positions from ``entry_map`` or a binary
+    search).  ``values`` is zeroed unless given."""
+    import torch
+
+    from .runtime import _check, load_library
+
+    if cell_dofs.dtype != torch.int32 or not cell_dofs.is_cuda:
+        raise TypeError("cell_dofs must be an int32 CUDA tensor")
+    if cell_matrices.dtype != torch.float64 or not cell_matrices.is_cuda:
+        raise TypeError("cell_matrices must be a float64 CUDA tensor")
+    ncells, nd = cell_dofs.shape
+    if cell_matrices.numel() != ncells * nd * nd:
+        raise ShapeMismatch("cell_matrices must hold (%d, %d x %d) entries" % (ncells, nd, nd))
+    cell_dofs = cell_dofs.contiguous()
+    cell_matrices = cell_matrices.contiguous()
+    if entry_map is not None and (entry_map.dtype != torch.int32 or not entry_map.is_contiguous()
+                                  or entry_map.numel() != ncells * nd * nd):
+        raise ShapeMismatch("entry_map must be a contiguous int32 (%d, %d) tensor"
+                            % (ncells, nd * nd))
+    if values is None:
+        values = torch.zeros(pattern.nnz, dtype=torch.float64, device=cell_dofs.device)
+    elif values.numel() != pattern.nnz:
+        raise ShapeMismatch("values must have nnz = %d entries" % pattern.nnz)
+    if stream is None:
+        stream = torch.cuda.current_stream(cell_dofs.device).cuda_stream
+    with torch.cuda.device(cell_dofs.device):
+        _check(load_library().sfk_csr_insert(
+            ncells, nd, cell_matrices.data_ptr(), cell_dofs.data_ptr(),
+            pattern.row_ptr.data_ptr(), pattern.col_idx.data_ptr(),
+            entry_map.data_ptr() if entry_map is not None else None, values.data_ptr(), stream))
+    return values
+
+
+def assemble_csr_from(plan, inputs, cell_dofs, pattern, values=None, entry_map=None):
+    """Assemble any matrix kernel: evaluate the per-cell matrices of ``plan``
+    (a ``compile_kernel`` plan or a ``load_program`` LoopProgram plan) on
+    ``inputs`` with ``evaluate_batched`` and insert them (``insert_csr``).
+    For the hex Laplace matrix at p <= 4 ``assemble_csr`` is the fused path
+    (no cell matrices in HBM); this one covers every other form, cell and
+    degree."""
+    from .runtime import evaluate_batched
+
+    A = evaluate_batched(plan, inputs)
+    return insert_csr(A, cell_dofs, pattern, values=values, entry_map=entry_map)

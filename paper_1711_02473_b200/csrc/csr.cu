@@ -74,6 +74,39 @@ __global__ void csr_map_kernel(int64_t ncells, int ndpc, const int32_t* __restri
   }
 }
 
+// values[pos(c, i, j)] += Ac[c][i][j] for dense per-cell matrices (test
+// index outer, as every reference kernel returns them): the insertion half of
+// sfk_assemble_csr for matrices produced by any kernel (hand-written or a
+// generated LoopProgram).  pos from the entry map, else a binary search of
+// the column within its row.
+__global__ void csr_insert_kernel(int64_t ncells, int ndpc, const double* __restrict__ Ac,
+                                  const int32_t* __restrict__ dofs,
+                                  const int64_t* __restrict__ row_ptr,
+                                  const int32_t* __restrict__ col_idx,
+                                  const int32_t* __restrict__ map, double* __restrict__ values) {
+  const int64_t per = (int64_t)ndpc * ndpc;
+  const int64_t total = ncells * per;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t pos;
+    if (map) {
+      pos = __ldg(map + k);
+    } else {
+      const int64_t c = k / per;
+      const int r = (int)(k - c * per);
+      const int i = r / ndpc, j = r - i * ndpc;
+      const int32_t row = __ldg(dofs + c * ndpc + i), col = __ldg(dofs + c * ndpc + j);
+      int64_t lo = __ldg(row_ptr + row), hi = __ldg(row_ptr + row + 1);
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(col_idx + mid) < col) lo = mid + 1; else hi = mid;
+      }
+      pos = lo;
+    }
+    atomicAdd(values + pos, __ldg(Ac + k));
+  }
+}
+
 }  // namespace sfk
 
 using namespace sfk;
@@ -168,6 +201,22 @@ int sfk_csr_entry_map(const sfk_csr* P, int64_t ncells, int ndofs_per_cell,
       ncells, ndofs_per_cell, cell_dofs, P->row_ptr, P->col_idx, map);
   note_launch();
   return cuda_status(cudaGetLastError(), "csr_map_kernel");
+}
+
+int sfk_csr_insert(int64_t ncells, int ndofs_per_cell, const double* cell_matrices,
+                   const int32_t* cell_dofs, const int64_t* row_ptr, const int32_t* col_idx,
+                   const int32_t* entry_map, double* values, void* stream) {
+  if (ncells < 0 || ndofs_per_cell <= 0) return fail(SFK_EINVAL, "sfk_csr_insert: bad sizes");
+  if (ncells == 0) return SFK_OK;
+  if (!cell_matrices || !values || (!entry_map && (!cell_dofs || !row_ptr || !col_idx)))
+    return fail(SFK_EINVAL, "sfk_csr_insert: NULL pointer argument");
+  const int64_t total = ncells * (int64_t)ndofs_per_cell * ndofs_per_cell;
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>((total + threads - 1) / threads, 148 * 32);
+  csr_insert_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
+      ncells, ndofs_per_cell, cell_matrices, cell_dofs, row_ptr, col_idx, entry_map, values);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "csr_insert_kernel");
 }
 
 int sfk_csr_info(const sfk_csr* P, int64_t* nrows, int64_t* nnz, int64_t** row_ptr,

@@ -305,10 +305,16 @@ static int eval_host_impl(const sfk_plan* p, int64_t ncells, double* A, const do
   if (st != SFK_OK || ncells == 0) return st;
   const int64_t per_cell = p->coords_size + p->w0_size + p->w1_size + p->a_size;
   if (chunk <= 0) {
-    // ~64 MiB of traffic per chunk: H2D of chunk k+1, the kernel of chunk k
+    // ~128 MiB of traffic per chunk: H2D of chunk k+1, the kernel of chunk k
     // and the D2H of chunk k-1 overlap (separate copy engines per direction;
-    // tools/pcie_probe.py: 55 GB/s H2D, 57 GB/s D2H, 100 GB/s concurrent)
-    chunk = (int64_t)((64ll << 20) / (8 * per_cell));
+    // tools/pcie_probe.py: 55 GB/s H2D, 57 GB/s D2H, 100 GB/s concurrent).
+    // e2e GDoF/s by chunk size 16 / 32 / 64 / 128 / 256 MiB: 4.34 / 4.74 /
+    // 4.94 / 5.09 / 4.79 (profiles/r01df_*.jsonl)
+    static const long long mb = [] {
+      const char* e = getenv("SFK_HOST_CHUNK_MB");   // A/B runs only
+      return e ? atoll(e) : 128ll;
+    }();
+    chunk = (int64_t)((mb << 20) / (8 * per_cell));
     if (chunk < 1024) chunk = 1024;
   }
   if (chunk > ncells) chunk = ncells;

@@ -42,6 +42,7 @@ EXPORTED_SYMBOLS = (
     "sfk_program_sizes", "sfk_program_config", "sfk_program_text", "sfk_program_eval",
     "sfk_csr_create", "sfk_csr_info", "sfk_csr_destroy", "sfk_assemble_csr",
     "sfk_csr_entry_map", "sfk_eval_global", "sfk_eval_host_async", "sfk_host_wait",
+    "sfk_csr_insert",
 )
 ABI_VERSION = 1
 SUM_WORKSPACE = 1024
@@ -102,6 +103,9 @@ def _declare(lib):
         lib.sfk_csr_entry_map.restype = ci
         lib.sfk_assemble_csr.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         lib.sfk_assemble_csr.restype = ci
+    if hasattr(lib, "sfk_csr_insert"):
+        lib.sfk_csr_insert.argtypes = [i64, ci, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+        lib.sfk_csr_insert.restype = ci
 
 
 def load_library(build_if_missing=True):

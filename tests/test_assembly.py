@@ -282,3 +282,84 @@ def test_gather_scatter_alternative_generations(cuda, gen):
                         "gpu", "-k", "gather_scatter_matches_oracle"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:]
+
+
+# ---------------------------------------------------------------------------
+# CSR insertion of ANY kernel's cell matrices (§8(f) item 3 beyond the fused
+# hex-Laplace path): reference LoopProgram fixtures (every cell type, vector
+# and mixed forms), a random cell -> dof map with shared and repeated dofs,
+# oracle = the reference's own cell matrices summed with np.add.at.
+
+ANY_FORMS = ["mass_triangle_p2", "laplace_prism_p2", "vector_mass_hex_p1",
+             "stokes_momentum_quad_p2", "curl_curl_quad_p2", "weighted_laplace_hex_p2",
+             "laplace_interval_p2"]
+
+
+def _program_fixture(key):
+    import json
+    import os
+
+    from conftest import GOLDEN
+
+    meta = {m["key"]: m for m in json.load(open(os.path.join(GOLDEN, "programs.json")))}[key]
+    z = np.load(os.path.join(GOLDEN, "programs.npz"))
+    text = bytes(z[key + "__json"]).decode()
+    inputs = {a: z["%s__%s" % (key, a)] for a, _ in meta["arguments"]}
+    return text, inputs, z[key + "__A"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", ANY_FORMS)
+@pytest.mark.parametrize("use_map", [False, True])
+def test_insert_csr_any_matrix_form(cuda, key, use_map):
+    torch = cuda
+    from paper_1711_02473_b200 import load_program
+    from paper_1711_02473_b200.assembly import CsrPattern, assemble_csr_from
+
+    text, inputs, ref = _program_fixture(key)
+    nc, nd2 = ref.shape
+    nd = int(round(nd2 ** 0.5))
+    ndofs = max(2 * nd, nc * nd // 3)
+    dofs = np.random.default_rng(7).integers(0, ndofs, (nc, nd)).astype(np.int32)
+    g = torch.from_numpy(dofs).cuda()
+    pat = CsrPattern(g, ndofs)
+    emap = pat.entry_map(g) if use_map else None
+    vals = assemble_csr_from(load_program(text),
+                             {k: torch.from_numpy(v).cuda() for k, v in inputs.items()},
+                             g, pat, entry_map=emap)
+    got = pat.matrix(vals).to_dense().cpu().numpy()
+    K = np.zeros((ndofs, ndofs))
+    np.add.at(K, (dofs[:, :, None], dofs[:, None, :]), ref.reshape(nc, nd, nd))
+    assert np.abs(got - K).max() <= 1e-12 * np.abs(K).max()
+
+
+@pytest.mark.gpu
+def test_insert_csr_matches_fused_assembly(cuda):
+    """Hand C5 cell matrices inserted by sfk_csr_insert == the fused C5 CSR
+    epilogue (sfk_assemble_csr) on a lattice numbering."""
+    torch = cuda
+    from paper_1711_02473_b200 import evaluate_batched
+    from paper_1711_02473_b200.assembly import CsrPattern, assemble_csr, insert_csr, lattice_ndofs
+
+    p, dims = 2, (3, 4, 5)
+    plan = compile_kernel("laplace", "hex", p)
+    coords = torch.from_numpy(workloads.lattice_coords(*dims)).cuda()
+    g = torch.from_numpy(lattice_dof_map(*dims, p)).cuda()
+    pat = CsrPattern(g, lattice_ndofs(*dims, p))
+    fused = assemble_csr(plan, g, coords, pat)
+    A = evaluate_batched(plan, {"coords": coords})
+    ins = insert_csr(A, g, pat, entry_map=pat.entry_map(g))
+    assert torch.allclose(fused, ins, rtol=0, atol=1e-12 * fused.abs().max().item())
+
+
+def test_insert_csr_validates_arguments():
+    """CPU tier: insert_csr rejects host tensors / wrong dtypes before any
+    device work (the product path has no CPU fallback)."""
+    import torch
+
+    from paper_1711_02473_b200.assembly import insert_csr
+
+    with pytest.raises(TypeError):
+        insert_csr(torch.zeros(2, 4, dtype=torch.float64), torch.zeros(2, 2, dtype=torch.int32), None)
+    with pytest.raises(TypeError):
+        insert_csr(torch.zeros(2, 4, dtype=torch.float32), torch.zeros(2, 2, dtype=torch.int64), None)
