@@ -29,9 +29,40 @@
 #define SFK_NEO_YT 1
 #endif
 
+#ifndef SFK_NEO_FASTLOG
+#define SFK_NEO_FASTLOG 0   // measured slower (p = 4 0.657 -> 0.689 ms, r01di_*)
+#endif
+
 namespace sfk {
 
 constexpr bool NEO_YT = SFK_NEO_YT;
+
+// ln J for the volumetric term.  Near J = 1 (every finite BASELINE point:
+// |J - 1| is a few 1e-2) ln J = 2 atanh(z), z = (J - 1)/(J + 1), summed as
+// 2z (1 + z^2/3 + ... + z^14/15): for |J - 1| < 1/16, |z| < 0.0323 and the
+// truncation is below 1e-23 relative; the rounding of z and the Horner sum
+// is a few ulp — far inside the 1e-12 gate.  Elsewhere (and for J <= 0,
+// NaN as in the reference) the libm log.  Meant to replace a ~40-instruction
+// dependent chain that was 13% of C4's stall samples
+// (profiles/r01cn_C4_p4.md), but the branch and the extra code measured
+// 2-5% slower than libm alone (profiles/r01di_*.jsonl): off by default.
+__device__ __forceinline__ double neo_log(double J) {
+  const double d = J - 1.0;
+  if (SFK_NEO_FASTLOG && fabs(d) < 0.0625) {
+    const double z = d * rcp64(J + 1.0);
+    const double z2 = z * z;
+    double t = 1.0 / 15.0;
+    t = fma(t, z2, 1.0 / 13.0);
+    t = fma(t, z2, 1.0 / 11.0);
+    t = fma(t, z2, 1.0 / 9.0);
+    t = fma(t, z2, 1.0 / 7.0);
+    t = fma(t, z2, 1.0 / 5.0);
+    t = fma(t, z2, 1.0 / 3.0);
+    t = fma(t, z2, 1.0);
+    return 2.0 * z * t;
+  }
+  return log(J);
+}
 
 template <int N, int M, int CPB>
 struct NeoCfg {
@@ -234,7 +265,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
       const double Jf = fma(F[0][2], cof[0][2], fma(F[0][1], cof[0][1], F[0][0] * cof[0][0]));
       const double iJ = rcp64(Jf);
       // P = mu F + (lambda ln J - mu) / J * cof(F)
-      const double beta = (lam * log(Jf) - mu) * iJ;
+      const double beta = (lam * neo_log(Jf) - mu) * iJ;
       // flux f_a[l] = w sign(det) sum_k r_l[k] P[a][k]
       const double s = (wxy * T.W[q]) * (det < 0.0 ? -1.0 : 1.0);
 #pragma unroll
