@@ -57,9 +57,12 @@ __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, doubl
                : "d"(a), "d"(b));
 }
 
+#ifndef SFK_TC8_CPB
+#define SFK_TC8_CPB 4   // 2 cells / 4 warps per CTA at 4 CTAs/SM measured slower: 2.09 -> 2.57 ms (r01dj_*)
+#endif
 namespace tc8 {
 constexpr int N = 8, M = 8, NN = 64, N3 = 512;
-constexpr int CPB = 4;                   // cells per CTA
+constexpr int CPB = SFK_TC8_CPB;         // cells per CTA (4: 8 warps; 2: 4 warps)
 constexpr int THREADS = CPB * NN;        // 256: one thread per z-line in the pointwise pass
 constexpr int WARPS = THREADS / 32;
 constexpr int TILES = CPB * 8;           // 8-line tiles per stage (8 per cell)
@@ -86,7 +89,7 @@ __device__ __forceinline__ int yaddr(int qx, int qy, int z) { return qx * YX + q
 // x is gathered through it by the x stage, y scattered with fp64 atomics by
 // the transposed x stage.
 template <bool GS>
-__global__ void __launch_bounds__(tc8::THREADS, 2)
+__global__ void __launch_bounds__(tc8::THREADS, 8 / tc8::CPB)
 hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
                        const double* __restrict__ coords, const double* __restrict__ u,
                        double* __restrict__ A, const int* __restrict__ cmap) {
@@ -160,16 +163,16 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
     // ---- x stage (D-form): tile (c, iy), lines iz; X0 = Bx u, X1 = Dx u ----
     {
       double f[TPW][2], o[TPW][4];
-      const int iy = warp & 7;
+      // in-cell tile index of this warp's j-th tile: (warp + WARPS*j) & 7
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
         if (GS) {
-          const int* mp = smap + c * N3 + iy * 8 + gq;   // (ix, iy, iz = gq)
+          const int* mp = smap + c * N3 + ((warp + WARPS * j) & 7) * 8 + gq;   // (ix, iy, iz = gq)
           f[j][0] = c < ncb ? __ldg(u + mp[kq * NN]) : 0.0;
           f[j][1] = c < ncb ? __ldg(u + mp[(4 + kq) * NN]) : 0.0;
         } else {
-          const double* in = sU + c * UC + iy * 8 + gq;
+          const double* in = sU + c * UC + ((warp + WARPS * j) & 7) * 8 + gq;
           f[j][0] = in[kq * UPL];
           f[j][1] = in[(4 + kq) * UPL];
         }
@@ -185,7 +188,7 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
-        double* out = sX + c * XC + xaddr(gq, iy, 2 * kq);
+        double* out = sX + c * XC + xaddr(gq, ((warp + WARPS * j) & 7), 2 * kq);
         *reinterpret_cast<double2*>(out) = make_double2(o[j][0], o[j][1]);
         *reinterpret_cast<double2*>(out + XA) = make_double2(o[j][2], o[j][3]);
       }
@@ -196,15 +199,15 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
     // ---- y stage (D-form): tile (c, qx), lines iz; BB, BD <- X0, DB <- X1 --
     {
       double f[TPW][4], o[TPW][6];
-      const int qx = warp & 7;
+      // in-cell tile index of this warp's j-th tile: (warp + WARPS*j) & 7
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
         const double* x = sX + c * XC;
-        f[j][0] = x[xaddr(qx, kq, gq)];
-        f[j][1] = x[xaddr(qx, 4 + kq, gq)];
-        f[j][2] = x[XA + xaddr(qx, kq, gq)];
-        f[j][3] = x[XA + xaddr(qx, 4 + kq, gq)];
+        f[j][0] = x[xaddr(((warp + WARPS * j) & 7), kq, gq)];
+        f[j][1] = x[xaddr(((warp + WARPS * j) & 7), 4 + kq, gq)];
+        f[j][2] = x[XA + xaddr(((warp + WARPS * j) & 7), kq, gq)];
+        f[j][3] = x[XA + xaddr(((warp + WARPS * j) & 7), 4 + kq, gq)];
       }
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks)
@@ -218,7 +221,7 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
-        double* out = sY + c * YC + yaddr(qx, gq, 2 * kq);
+        double* out = sY + c * YC + yaddr(((warp + WARPS * j) & 7), gq, 2 * kq);
         *reinterpret_cast<double2*>(out) = make_double2(o[j][0], o[j][1]);           // BB
         *reinterpret_cast<double2*>(out + YA) = make_double2(o[j][2], o[j][3]);      // BD
         *reinterpret_cast<double2*>(out + 2 * YA) = make_double2(o[j][4], o[j][5]);  // DB
@@ -231,11 +234,11 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
     {
       double2 f[TPW][3];
       double o[TPW][6];
-      const int qx = warp & 7;
+      // in-cell tile index of this warp's j-th tile: (warp + WARPS*j) & 7
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
-        const double* y = sY + c * YC + yaddr(qx, gq, 2 * kq);
+        const double* y = sY + c * YC + yaddr(((warp + WARPS * j) & 7), gq, 2 * kq);
 #pragma unroll
         for (int s = 0; s < 3; ++s) f[j][s] = *reinterpret_cast<const double2*>(y + s * YA);
       }
@@ -256,7 +259,7 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
-        double* y = sY + c * YC + yaddr(qx, gq, 2 * kq);
+        double* y = sY + c * YC + yaddr(((warp + WARPS * j) & 7), gq, 2 * kq);
 #pragma unroll
         for (int s = 0; s < 3; ++s)
           *reinterpret_cast<double2*>(y + s * YA) = make_double2(o[j][2 * s], o[j][2 * s + 1]);
@@ -302,11 +305,11 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
     {
       double2 f[TPW][3];
       double o[TPW][6];
-      const int qx = warp & 7;
+      // in-cell tile index of this warp's j-th tile: (warp + WARPS*j) & 7
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
-        const double* y = sY + c * YC + yaddr(qx, gq, 2 * kq);
+        const double* y = sY + c * YC + yaddr(((warp + WARPS * j) & 7), gq, 2 * kq);
 #pragma unroll
         for (int s = 0; s < 3; ++s) f[j][s] = *reinterpret_cast<const double2*>(y + s * YA);
       }
@@ -327,7 +330,7 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
-        double* y = sY + c * YC + yaddr(qx, gq, 2 * kq);
+        double* y = sY + c * YC + yaddr(((warp + WARPS * j) & 7), gq, 2 * kq);
 #pragma unroll
         for (int s = 0; s < 3; ++s)
           *reinterpret_cast<double2*>(y + s * YA) = make_double2(o[j][2 * s], o[j][2 * s + 1]);
@@ -339,15 +342,15 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
     //      R1 = By^T Sx, R2 = Dy^T Sy + By^T Sz ---------------------------------
     {
       double f[TPW][6], o[TPW][4];
-      const int qx = warp & 7;
+      // in-cell tile index of this warp's j-th tile: (warp + WARPS*j) & 7
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
         const double* y = sY + c * YC;
 #pragma unroll
         for (int s = 0; s < 3; ++s) {
-          f[j][2 * s] = y[s * YA + yaddr(qx, kq, gq)];
-          f[j][2 * s + 1] = y[s * YA + yaddr(qx, 4 + kq, gq)];
+          f[j][2 * s] = y[s * YA + yaddr(((warp + WARPS * j) & 7), kq, gq)];
+          f[j][2 * s + 1] = y[s * YA + yaddr(((warp + WARPS * j) & 7), 4 + kq, gq)];
         }
       }
 #pragma unroll
@@ -362,7 +365,7 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
-        double* out = sX + c * XC + xaddr(qx, gq, 2 * kq);
+        double* out = sX + c * XC + xaddr(((warp + WARPS * j) & 7), gq, 2 * kq);
         *reinterpret_cast<double2*>(out) = make_double2(o[j][0], o[j][1]);
         *reinterpret_cast<double2*>(out + XA) = make_double2(o[j][2], o[j][3]);
       }
@@ -372,15 +375,15 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
     // ---- x backward (D-form): tile (c, iy), lines iz; A = Dx^T R1 + Bx^T R2 -
     {
       double f[TPW][4], o[TPW][2];
-      const int iy = warp & 7;
+      // in-cell tile index of this warp's j-th tile: (warp + WARPS*j) & 7
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
         const double* x = sX + c * XC;
-        f[j][0] = x[xaddr(kq, iy, gq)];
-        f[j][1] = x[xaddr(4 + kq, iy, gq)];
-        f[j][2] = x[XA + xaddr(kq, iy, gq)];
-        f[j][3] = x[XA + xaddr(4 + kq, iy, gq)];
+        f[j][0] = x[xaddr(kq, ((warp + WARPS * j) & 7), gq)];
+        f[j][1] = x[xaddr(4 + kq, ((warp + WARPS * j) & 7), gq)];
+        f[j][2] = x[XA + xaddr(kq, ((warp + WARPS * j) & 7), gq)];
+        f[j][3] = x[XA + xaddr(4 + kq, ((warp + WARPS * j) & 7), gq)];
       }
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks)
@@ -394,12 +397,12 @@ hex_laplace_action_tc8(const __grid_constant__ Tabs<8, 8> T, int64_t ncells,
       for (int j = 0; j < TPW; ++j) {
         const int c = (warp + WARPS * j) >> 3;
         if (GS && c < ncb) {
-          const int* mp = smap + c * N3 + gq * NN + iy * 8 + 2 * kq;
+          const int* mp = smap + c * N3 + gq * NN + ((warp + WARPS * j) & 7) * 8 + 2 * kq;
           atomicAdd(A + mp[0], o[j][0]);
           atomicAdd(A + mp[1], o[j][1]);
         } else if (c < ncb) {
           // D: ix = gq, iz = 2kq + h -> A[cell][ix*64 + iy*8 + iz]
-          double* ap = A + (cell0 + c) * N3 + gq * NN + iy * 8 + 2 * kq;
+          double* ap = A + (cell0 + c) * N3 + gq * NN + ((warp + WARPS * j) & 7) * 8 + 2 * kq;
           if ((reinterpret_cast<uintptr_t>(ap) & 15) == 0) {
             *reinterpret_cast<double2*>(ap) = make_double2(o[j][0], o[j][1]);
           } else {
