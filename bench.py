@@ -445,6 +445,8 @@ def main():
         for p in degs:
             pinned[p] = (torch.from_numpy(host_u[p]).pin_memory(),
                          torch.empty((ncells, (p + 1) ** 3), dtype=torch.float64).pin_memory())
+            if world > 1:
+                host_u[p] = None   # only rank 0 at N=1 needs it again (CPU leg): host RAM
         pc = torch.from_numpy(coords_np).pin_memory()
         for p in degs:  # warm-up
             runtime.evaluate_host_ptrs(plans[p], min(ncells, 4096), pinned[p][1].data_ptr(),
