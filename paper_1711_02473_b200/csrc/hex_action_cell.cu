@@ -1,23 +1,26 @@
 // Hex Q_p Laplace action, one thread per cell at small n — BASELINE C2 at
-// p = 2 (n = m = 3) and, measured, p = 3.
+// p = 2 (n = m = 3); also the p = 2 global operator (GS).
 //
 // Same math and reference mapping as the other C2 kernels (forms.py:186-189,
 // 235-243; passes.py:672-743 schedule; scheduling.py:617-738 emitted
 // kernel).  The line kernels (v4 at p = 2) give each lane one 1D line per
 // stage: 3 cells x 9 lines = 27 of 32 lanes busy, lines re-dealt through
 // shared memory between stages.  Here a thread owns a whole cell and runs the
-// pipeline in slices, so nothing is exchanged between threads (no barrier,
-// every lane busy, u / coords / A straight from / to HBM):
+// pipeline in slices, so nothing is exchanged between threads (no barrier in
+// the pipeline, every lane busy):
 //   (A) per iz-slice: the x contraction of the n x n (ix, iy) dofs (in
 //       registers) feeds the y contraction at once; the 3 y-outputs
 //       (BB, BD, DB) of the slice go to this thread's private shared-memory
-//       block Y[3][qx][qy][iz] (stride n^3*3 + 1 doubles per thread: odd, so
-//       the per-thread 64-bit accesses of a warp are conflict-free);
+//       block Y[3][qx][qy][iz] (3 n^3 doubles, odd stride: the per-thread
+//       64-bit accesses of a warp are conflict-free);
 //   (B) per z-line (qx, qy): z contraction, per-point geometry + Laplace
 //       flux (HexLineAdj), transposed z — written back in place;
-//   (C) per iz-slice: transposed y (registers) feeding transposed x, and the
-//       n^2 results of the slice stored to A.
-// Occupancy is bounded by the private Y block (3 n^3 doubles per thread).
+//   (C) per iz-slice: transposed y (registers) feeding transposed x.
+// The CTA's u block (contiguous in HBM) arrives through shared memory with
+// coalesced 16-byte cp.async and A leaves the same way (per-thread scattered
+// 8-byte loads / stores were 0.101 vs 0.081 ms, profiles/r01cu_*.jsonl);
+// coords are read as 16-byte vectors straight into registers.  Occupancy is
+// bounded by the per-thread shared block (4 CTAs of 64 threads per SM).
 #include <cstdint>
 #include <cstdlib>
 
