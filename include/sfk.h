@@ -91,6 +91,14 @@ int sfk_plan_create(int kind, int cell_dim, int degree, int n_dof1d,
 
 int sfk_plan_destroy(sfk_plan *plan);
 
+/* 1 when a kernel is instantiated for this (kind, cell_dim, n_dof1d, n_q1d,
+ * collocated), else 0.  Host-only, no CUDA call.  sfk_plan_create fails with
+ * SFK_EUNSUPPORTED for every combination this rejects, and compile_kernel
+ * raises Unsupported for them (the reference raises at compile time,
+ * cli.py:155-208). */
+int sfk_kernel_available(int kind, int cell_dim, int n_dof1d, int n_q1d,
+                         int collocated);
+
 /* Per-cell sizes of the plan's arguments, in doubles (for validation). */
 int sfk_plan_sizes(const sfk_plan *plan, int64_t *coords_size,
                    int64_t *w0_size, int64_t *w1_size, int64_t *a_size);
@@ -300,6 +308,17 @@ int sfk_device_info(int device, int *sm_count, int *sm_clock_khz,
  * DMMA (mma.sync m8n8k4 f64).  Runs about `seconds` in total.
  */
 int sfk_fp64_peak(double seconds, double *tflops_dfma, double *tflops_dmma);
+
+/*
+ * Tuning options (A/B runs of kernel variants; no reference counterpart —
+ * the reference has no runtime).  `name` is one of the lower-case option
+ * names of csrc/sfk_options.h ("c2_kernel", "c2_g", "host_chunk_mb", ...);
+ * 0 restores the built-in, measured-best choice.  Process-wide and
+ * thread-safe.  The library reads no environment variables for dispatch:
+ * these calls are the only way to change a kernel choice.
+ */
+int sfk_set_option(const char *name, int64_t value);
+int sfk_get_option(const char *name, int64_t *value);
 
 #ifdef __cplusplus
 }

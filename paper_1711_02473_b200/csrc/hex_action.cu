@@ -237,13 +237,9 @@ static int launch_nm(const sfk_plan* p, int64_t ncells, double* A,
                      const double* coords, const double* u, cudaStream_t s) {
   using C = HexActionCfg<N, M, CPB>;
   auto kern = hex_laplace_action_kernel<N, M, CPB>;
-  static bool configured = false;  // attribute set once per process (idempotent)
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)C::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_action)");
-    configured = true;
-  }
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)kern, C::THREADS, C::SMEM, "hex_action", &sh))
+    return rc_;
   const Tabs<N, M> T = make_tabs<N, M>(p);
   const int64_t grid = (ncells + CPB - 1) / CPB;
   kern<<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, u, A);

@@ -476,22 +476,12 @@ static int launch_v2(const sfk_plan* p, int64_t ncells, double* A, const double*
                      const double* u, cudaStream_t s, const int* cmap = nullptr) {
   using C = HexAction2Cfg<N, M, CPB, R>;
   auto kern = hex_laplace_action_v2<N, M, CPB, R, MINB, ROLL, GS>;
-  static int sms = 0, per_sm = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)C::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_action_v2)");
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-    if (per_sm < 1) return fail(SFK_ECUDA, "hex_action_v2<%d>: kernel does not fit on an SM", N);
-  }
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)kern, C::THREADS, C::SMEM, "hex_action_v2", &sh, true))
+    return rc_;
   const TabsBD<N, M> T = make_tabs_bd<N, M>(p);
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
-  const int64_t resident = (int64_t)sms * per_sm;
+  const int64_t resident = sh.resident();
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
   kern<<<grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, u, A, cmap);
   note_launch();
@@ -499,12 +489,8 @@ static int launch_v2(const sfk_plan* p, int64_t ncells, double* A, const double*
 }
 
 // Per-degree configuration (cells per CTA, lines per thread, min CTAs/SM,
-// loop rolling).  SFK_C2_R=1|2 and SFK_C2_ROLL=1|2 override the defaults
+// loop rolling).  options c2_r = 1|2 and c2_roll = 1|2 override the defaults
 // (tuning runs only).
-static int env_int(const char* name) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : 0;
-}
 
 template <int N, int CPB, int MINB1, int MINB2>
 static int pick(int r, int roll, const sfk_plan* p, int64_t ncells, double* A,
@@ -517,7 +503,7 @@ static int pick(int r, int roll, const sfk_plan* p, int64_t ncells, double* A,
 int launch_hex_action_v2(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, cudaStream_t s) {
   if (p->n != p->m) return SFK_EUNSUPPORTED;   // caller falls back to v1
-  static const int r_env = env_int("SFK_C2_R"), roll_env = env_int("SFK_C2_ROLL");
+  const int r_env = (int)option(OPT_C2_R), roll_env = (int)option(OPT_C2_ROLL);
   const int r = r_env ? r_env : 1, roll = roll_env ? roll_env : 1;
   switch (p->n) {
     case 2: return pick<2, 64, 2, 2>(r, roll, p, ncells, A, coords, w0, s);

@@ -335,22 +335,12 @@ template <class L, int MINB, bool GS = false>
 static int launch_v3(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                      const double* u, cudaStream_t s, const int* cmap = nullptr) {
   auto kern = hex_laplace_action_v3<L, MINB, GS>;
-  static int sms = 0, per_sm = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)L::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_action_v3)");
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, L::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-    if (per_sm < 1) return fail(SFK_ECUDA, "hex_action_v3<%d>: does not fit on an SM", L::N);
-  }
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)kern, L::THREADS, L::SMEM, "hex_action_v3", &sh, true))
+    return rc_;
   const Tabs<L::N, L::M> T = make_tabs<L::N, L::M>(p);
   const int64_t nbatch = (ncells + L::CPB - 1) / L::CPB;
-  const int64_t resident = (int64_t)sms * per_sm;
+  const int64_t resident = sh.resident();
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
   kern<<<grid, L::THREADS, L::SMEM, s>>>(T, ncells, coords, u, A, cmap);
   note_launch();
@@ -380,27 +370,15 @@ int launch_hex_action_v3(const sfk_plan* p, int64_t ncells, double* A, const dou
   return dispatch_v3<false>(p, ncells, A, coords, w0, s, nullptr);
 }
 
-static bool force_v3_small() {
-  static const bool v = [] {
-    const char* e = std::getenv("SFK_C2G_SMALL");   // "v3": A/B of the p = 2, 3 path
-    return e && e[0] == 'v' && e[1] == '3';
-  }();
-  return v;
-}
+static bool force_v3_small() { return option(OPT_C2G_SMALL) == 3; }   // A/B of the p = 2, 3 path
 
 // Same generation as the E-vector action per degree (sfk_api.cu c2_auto):
 // p = 1 cell kernel, p = 2, 3 v4, p = 5, 6, 8 v2, p = 7 DMMA, p = 4 v3.
-// SFK_C2G_KERNEL=v3 forces v3 (A/B runs).
+// option c2g_kernel = 3 forces v3 (A/B runs).
 int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                          double* y, const double* coords, cudaStream_t s) {
-  static const bool force_v3 = [] {
-    const char* e = std::getenv("SFK_C2G_KERNEL");
-    return e && e[0] == 'v' && e[1] == '3';
-  }();
-  static const bool force_v2 = [] {
-    const char* e = std::getenv("SFK_C2G_KERNEL");
-    return e && e[0] == 'v' && e[1] == '2';
-  }();
+  const bool force_v3 = option(OPT_C2G_KERNEL) == 3;
+  const bool force_v2 = option(OPT_C2G_KERNEL) == 2;
   if (!force_v3 && p->n == p->m) {
     if (p->n == 2 && (reinterpret_cast<uintptr_t>(cmap) & 15) == 0)   // int4 map loads
       return launch_hex_action_p1_gs(p, ncells, cmap, x, y, coords, s);

@@ -302,22 +302,12 @@ template <class L, int MINB, bool GS = false>
 static int launch_v4(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                      const double* u, cudaStream_t s, const int* cmap = nullptr) {
   auto kern = hex_laplace_action_v4<L, MINB, GS>;
-  static int sms = 0, per_sm = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)L::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_action_v4)");
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, L::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-    if (per_sm < 1) return fail(SFK_ECUDA, "hex_action_v4<%d>: does not fit on an SM", L::N);
-  }
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)kern, L::THREADS, L::SMEM, "hex_action_v4", &sh, true))
+    return rc_;
   const TabsBD<L::N, L::M> T = make_tabs_bd<L::N, L::M>(p);
   const int64_t nbatch = (ncells + L::CPB - 1) / L::CPB;
-  const int64_t resident = (int64_t)sms * per_sm;
+  const int64_t resident = sh.resident();
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
   kern<<<grid, L::THREADS, L::SMEM, s>>>(T, ncells, coords, u, A, cmap);
   note_launch();

@@ -403,29 +403,19 @@ static int launch_v5(const sfk_plan* p, int64_t ncells, double* A, const double*
                      const double* u, cudaStream_t s, const int* cmap = nullptr) {
   using C = HexAction2Cfg<N, N, CPB, 1, v5_ypad(N)>;
   auto kern = hex_laplace_action_v5<N, CPB, G, MINB, PAIRS, GS>;
-  static int sms = 0, per_sm = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)C::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_action_v5)");
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-    if (per_sm < 1) return fail(SFK_ECUDA, "hex_action_v5<%d>: kernel does not fit on an SM", N);
-  }
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)kern, C::THREADS, C::SMEM, "hex_action_v5", &sh, true))
+    return rc_;
   const TabsBD<N, N> T = make_tabs_bd<N, N>(p);
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
-  const int64_t resident = (int64_t)sms * per_sm;
+  const int64_t resident = sh.resident();
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
   kern<<<grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, u, A, cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_v5 launch");
 }
 
-// Output group size per degree: SFK_C2_G overrides (tuning runs only).
+// Output group size per degree: option c2_g overrides (tuning runs only).
 template <int N, int CPB, int G0, bool PAIRS = true>
 static int pick_v5(int g, const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                    const double* w0, cudaStream_t s) {
@@ -439,14 +429,8 @@ static int pick_v5(int g, const sfk_plan* p, int64_t ncells, double* A, const do
 int launch_hex_action_v5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, cudaStream_t s) {
   if (p->n != p->m) return SFK_EUNSUPPORTED;
-  static const int g_env = [] {
-    const char* e = getenv("SFK_C2_G");
-    return e ? atoi(e) : 0;
-  }();
-  static const int cpb6_env = [] {
-    const char* e = getenv("SFK_V5_CPB6");
-    return e ? atoi(e) : 0;
-  }();
+  const int g_env = (int)option(OPT_C2_G);
+  const int cpb6_env = (int)option(OPT_V5_CPB6);
   switch (p->n) {
     // profiles/r01bu_*.jsonl (same box, ms at 2^18 cells; G = 1 / 2 / 3):
     //   n = 5: 0.592 / 0.590 / 0.588 (v3 0.531 stays)   n = 6: 0.985 / 1.87 (spills) / 1.10
@@ -455,7 +439,7 @@ int launch_hex_action_v5(const sfk_plan* p, int64_t ncells, double* A, const dou
     case 6:
       // CPB 7 = 256 threads (register cap 128: (B, D) pairs fit) over CPB 8
       // = 288 threads (cap 96: no pairs): 0.995 -> 0.947 ms with G = 1
-      // (profiles/r01cb_*.jsonl); SFK_V5_CPB6=8 selects the latter.  6 cells
+      // (profiles/r01cb_*.jsonl); option v5_cpb6 = 8 selects the latter.  6 cells
       // per CTA at 3 CTAs/SM spill (80-register cap): 1.07 ms (r01cz_*)
       if (cpb6_env == 8) return pick_v5<6, 8, 1, false>(g_env, p, ncells, A, coords, w0, s);
       return pick_v5<6, 7, 1>(g_env, p, ncells, A, coords, w0, s);

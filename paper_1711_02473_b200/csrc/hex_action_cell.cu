@@ -262,14 +262,9 @@ static int launch_cell(const sfk_plan* p, int64_t ncells, double* A, const doubl
   constexpr size_t SMEM =
       (size_t)TH * (CellCfg<N>::YS + (SFK_CELL_STAGE || GS ? CellCfg<N>::N3 : 0)) * sizeof(double);
   auto kern = hex_laplace_action_cell<N, TH, MINB, GS>;
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_action_cell)");
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    init = true;
-  }
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)kern, TH, SMEM, "hex_action_cell", &sh, true))
+    return rc_;
   const TabsBD<N, N> T = make_tabs_bd<N, N>(p);
   const int64_t grid = (ncells + TH - 1) / TH;
   if (grid > 0) kern<<<(unsigned)grid, TH, SMEM, s>>>(T, ncells, coords, u, A, cmap);
@@ -277,22 +272,16 @@ static int launch_cell(const sfk_plan* p, int64_t ncells, double* A, const doubl
   return cuda_status(cudaGetLastError(), "hex_laplace_action_cell launch");
 }
 
-// Threads per CTA: SFK_CELL_TH overrides (tuning runs only).
+// Threads per CTA: option cell_th overrides (tuning runs only).
 int launch_hex_action_cell(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                            const double* w0, cudaStream_t s) {
   if (p->n != p->m) return SFK_EUNSUPPORTED;
-  static const int th = [] {
-    const char* e = getenv("SFK_CELL_TH");
-    return e ? atoi(e) : 0;
-  }();
-  static const int minb = [] {
-    const char* e = getenv("SFK_CELL_MINB");
-    return e ? atoi(e) : 0;
-  }();
+  const int th = (int)option(OPT_CELL_TH);
+  const int minb = (int)option(OPT_CELL_MINB);
   switch (p->n) {
     case 3:
       // 64 threads per CTA (profiles/r01cs_*.jsonl: 0.1008 ms vs 0.1071 / 0.1032
-      // at 96 / 128); SFK_CELL_MINB=5 caps registers for a 5th CTA per SM
+      // at 96 / 128); option cell_minb = 5 caps registers for a 5th CTA per SM
       if (th == 128) return launch_cell<3, 128, 1>(p, ncells, A, coords, w0, s);
       if (th == 96) return launch_cell<3, 96, 1>(p, ncells, A, coords, w0, s);
       if (minb == 5) return launch_cell<3, 64, 5>(p, ncells, A, coords, w0, s);

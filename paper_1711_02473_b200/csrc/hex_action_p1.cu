@@ -192,14 +192,10 @@ template <bool GS>
 static int launch_p1(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                      const double* w0, cudaStream_t s, const int* cmap) {
   if (p->n != 2 || p->m != 2) return SFK_EUNSUPPORTED;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(hex_laplace_action_p1<GS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)p1::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_action_p1)");
-    configured = true;
-  }
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)hex_laplace_action_p1<GS>, p1::CPB, p1::SMEM,
+                                   "hex_action_p1", &sh))
+    return rc_;
   const Tabs<2, 2> T = make_tabs<2, 2>(p);
   const unsigned grid = (unsigned)((ncells + p1::CPB - 1) / p1::CPB);
   hex_laplace_action_p1<GS><<<grid, p1::CPB, p1::SMEM, s>>>(T, ncells, coords, w0, A, cmap);

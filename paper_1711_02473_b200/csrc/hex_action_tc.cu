@@ -422,22 +422,12 @@ static int launch_tc8(const sfk_plan* p, int64_t ncells, double* A, const double
   if (p->n != 8 || p->m != 8) return SFK_EUNSUPPORTED;
   using namespace tc8;
   auto kern = hex_laplace_action_tc8<GS>;
-  static int sms = 0, per_sm = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_action_tc8)");
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "occupancy(hex_action_tc8)");
-    if (per_sm < 1) return fail(SFK_ECUDA, "hex_action_tc8 does not fit on an SM");
-  }
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)kern, THREADS, SMEM, "hex_action_tc8", &sh, true))
+    return rc_;
   const Tabs<8, 8> T = make_tabs<8, 8>(p);
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
-  const int64_t resident = (int64_t)sms * per_sm;
+  const int64_t resident = sh.resident();
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
   kern<<<grid, THREADS, SMEM, s>>>(T, ncells, coords, w0, A, cmap);
   note_launch();

@@ -406,28 +406,19 @@ static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* 
     T.Bc[N + q] = p->Bc[N + q];
   }
   int64_t grid = (ncells + CPB * G - 1) / (CPB * G);
-  cudaError_t e;
   // persistent mode: one resident wave of CTAs looping over the batches
-  auto resident = [&](auto k, size_t smem_bytes) -> int64_t {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem_bytes);
-    return (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-  };
+  LaunchShape sh;
   if (kappa) {
     auto k = colloc_kernel<N, CPB, SY, SX, CS, true, GS, WARPS>();
     const size_t sm = G * C::smem(true, WARPS);
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
-    if (C::persist(WARPS)) grid = std::min(grid, resident(k, sm));
+    if (const int rc_ = kernel_shape((const void*)k, THREADS, sm, "hex_colloc", &sh)) return rc_;
+    if (C::persist(WARPS)) grid = std::min<int64_t>(grid, sh.resident());
     if (grid > 0) k<<<(unsigned)grid, THREADS, sm, s>>>(T, ncells, coords, u, kappa, A, cmap);
   } else {
     auto k = colloc_kernel<N, CPB, SY, SX, CS, false, GS, WARPS>();
     const size_t sm = G * C::smem(false, WARPS);
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc)");
-    if (C::persist(WARPS)) grid = std::min(grid, resident(k, sm));
+    if (const int rc_ = kernel_shape((const void*)k, THREADS, sm, "hex_colloc", &sh)) return rc_;
+    if (C::persist(WARPS)) grid = std::min<int64_t>(grid, sh.resident());
     if (grid > 0) k<<<(unsigned)grid, THREADS, sm, s>>>(T, ncells, coords, u, nullptr, A, cmap);
   }
   note_launch();
@@ -452,11 +443,9 @@ static int dispatch_colloc(const sfk_plan* p, int64_t ncells, double* A, const d
                            const int* cmap) {
   if (p->n != p->m)
     return fail(SFK_EINVAL, "collocated action needs n_q1d == n_dof1d (got %d, %d)", p->n, p->m);
-  // warp-synchronous variants for n <= 5 (SFK_COLLOC_WARPS = warps per CTA)
-  static const int cw = [] {
-    const char* e = std::getenv("SFK_COLLOC_WARPS");
-    return e ? std::atoi(e) : SFK_COLLOC_WARPS_DEFAULT;
-  }();
+  // warp-synchronous variants for n <= 5 (option colloc_warps = warps per CTA)
+  const int64_t ocw = option(OPT_COLLOC_WARPS);   // 0: built-in, < 0: off
+  const int cw = ocw == 0 ? SFK_COLLOC_WARPS_DEFAULT : ocw < 0 ? 0 : (int)ocw;
   if (cw > 0) {
     switch (p->n) {
       case 2: return launch_n<2, 8, 2, 5, 12, GS, 8>(p, ncells, A, coords, w0, w1, s, cmap);

@@ -237,33 +237,24 @@ static int launch_colloc_tc(const sfk_plan* p, int64_t ncells, double* A, const 
     T.Bc[N + q] = p->Bc[N + q];
   }
   auto kern = kappa ? hex_colloc_tc_kernel<N, true> : hex_colloc_tc_kernel<N, false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)C::SMEM);
-  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_colloc_tc)");
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM);
-  if (e != cudaSuccess) return cuda_status(e, "occupancy(hex_colloc_tc)");
-  if (per_sm < 1) return fail(SFK_ECUDA, "hex_colloc_tc<%d> does not fit on an SM", N);
-  const int64_t resident = (int64_t)sms * per_sm;
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)kern, C::THREADS, C::SMEM, "hex_colloc_tc", &sh))
+    return rc_;
+  const int64_t resident = sh.resident();
   const unsigned grid = (unsigned)(ncells < resident ? ncells : resident);
   kern<<<grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, u, kappa, A);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_colloc_tc launch");
 }
 
-// DMMA path for n = 8, 12, 16 — OPT-IN (SFK_C3_TC=1).  Measured slower than
+// DMMA path for n = 8, 12, 16 — OPT-IN (option c3_tc = 1).  Measured slower than
 // the line kernel (p = 7: 1.25 vs 0.385 ms, p = 15: 5.51 vs 4.89 ms,
 // profiles/r01bn_c3_dmma.jsonl): one cell at a time per CTA with an exposed
 // per-cell u load and 1 CTA/SM by registers; kept correct (parity-tested)
 // as the starting point for a prefetching, multi-cell version.
 int launch_hex_colloc_tc(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, const double* w1, cudaStream_t s) {
-  static const bool off = [] {
-    const char* e = std::getenv("SFK_C3_TC");
-    return !(e && e[0] == '1');
-  }();
+  const bool off = option(OPT_C3_TC) != 1;
   if (off || p->n != p->m) return SFK_EUNSUPPORTED;
   switch (p->n) {
     case 8: return launch_colloc_tc<8>(p, ncells, A, coords, w0, w1, s);

@@ -362,9 +362,9 @@ static int launch_mat(const sfk_plan* p, int64_t ncells, double* A, const double
   }
   const unsigned grid = (unsigned)((ncells + CPB - 1) / CPB);
   auto kern = hex_laplace_matrix_kernel<N, M, CPB, CSR, YMAP>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)C::SMEM);
-  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_matrix)");
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)kern, C::THREADS, C::SMEM, "hex_matrix", &sh))
+    return rc_;
   kern<<<grid, C::THREADS, C::SMEM, s>>>(T, ncells, coords, A, dofs, row_ptr, col_idx, emap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_matrix_kernel launch");
@@ -377,12 +377,9 @@ int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double
   if (p->n == p->m) {
     switch (p->n) {
       case 2: {
-        // thread-per-cell kernel (hex_matrix_p1.cu); SFK_C5_P1=phase selects
+        // thread-per-cell kernel (hex_matrix_p1.cu); option c5_p1 = 1 selects
         // the CTA-phase kernel below for A/B runs
-        static const bool phase = [] {
-          const char* e = std::getenv("SFK_C5_P1");
-          return e && e[0] == 'p';
-        }();
+        const bool phase = option(OPT_C5_P1) == 1;
         if (!phase) return launch_hex_matrix_p1(p, ncells, A, coords, s);
         return launch_mat<2, 2, 16>(p, ncells, A, coords, s);
       }
@@ -390,11 +387,8 @@ int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double
       // work per cell for the padded tiles, profiles/r01bl_c5_p2_dmma.jsonl)
       case 3: return launch_mat<3, 3, 3>(p, ncells, A, coords, s);
       case 4: {
-        // DMMA kernel (hex_matrix_tc.cu); SFK_C5_P3=phase selects the FMA one
-        static const bool phase = [] {
-          const char* e = std::getenv("SFK_C5_P3");
-          return e && e[0] == 'p';
-        }();
+        // DMMA kernel (hex_matrix_tc.cu); option c5_p3 = 1 selects the FMA one
+        const bool phase = option(OPT_C5_P3) == 1;
         if (!phase) {
           const int rc = launch_hex_matrix_tc4(p, ncells, A, coords, s);
           if (rc != SFK_EUNSUPPORTED) return rc;
@@ -402,11 +396,8 @@ int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double
         return launch_mat<4, 4, 1, false, true>(p, ncells, A, coords, s);
       }
       case 5: {
-        // DMMA kernel (hex_matrix_tc.cu); SFK_C5_P4=phase selects the FMA one
-        static const bool phase = [] {
-          const char* e = std::getenv("SFK_C5_P4");
-          return e && e[0] == 'p';
-        }();
+        // DMMA kernel (hex_matrix_tc.cu); option c5_p4 = 1 selects the FMA one
+        const bool phase = option(OPT_C5_P4) == 1;
         if (!phase) {
           const int rc = launch_hex_matrix_tc5(p, ncells, A, coords, s);
           if (rc != SFK_EUNSUPPORTED) return rc;
@@ -427,11 +418,8 @@ int launch_hex_matrix_csr(const sfk_plan* p, int64_t ncells, const int32_t* dofs
     return fail(SFK_EUNSUPPORTED, "CSR assembly: hex laplace with m == n only");
   // (the DMMA kernels of hex_matrix_tc.cu have an entry-map epilogue too, but
   // their fragment-order map loads and atomics scatter: p = 3 1.74 -> 1.88 ms,
-  // p = 4 8.7 -> 10.9 ms, profiles/r01bk_csr_dmma.jsonl; SFK_CSR_DMMA=1 uses them)
-  static const bool csr_dmma = [] {
-    const char* e = std::getenv("SFK_CSR_DMMA");
-    return e && e[0] == '1';
-  }();
+  // p = 4 8.7 -> 10.9 ms, profiles/r01bk_csr_dmma.jsonl; option csr_dmma = 1 uses them)
+  const bool csr_dmma = option(OPT_CSR_DMMA) == 1;
   if (csr_dmma && emap && (p->n == 4 || p->n == 5)) {
     const int rc = p->n == 4 ? launch_hex_matrix_tc4(p, ncells, values, coords, s, emap)
                              : launch_hex_matrix_tc5(p, ncells, values, coords, s, emap);

@@ -135,19 +135,12 @@ int launch_hex_matrix_p1(const sfk_plan* p, int64_t ncells, double* A, const dou
                          cudaStream_t s) {
   if (p->n != 2 || p->m != 2) return SFK_EUNSUPPORTED;
   // register budget: MINB=2 -> no spills (254 regs unconstrained); MINB=3
-  // spills ~300 B.  SFK_C5_P1_MINB=3 selects the latter for A/B runs.
-  static const int minb = [] {
-    const char* e = std::getenv("SFK_C5_P1_MINB");
-    return (e && e[0] == '3') ? 3 : 2;
-  }();
+  // spills ~300 B.  option c5_p1_minb = 3 selects the latter for A/B runs.
+  const int minb = option(OPT_C5_P1_MINB) == 3 ? 3 : 2;
   auto kern = minb == 3 ? hex_laplace_matrix_p1<3> : hex_laplace_matrix_p1<2>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)m1::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_matrix_p1)");
-    configured = true;
-  }
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)kern, m1::CPB, m1::SMEM, "hex_matrix_p1", &sh))
+    return rc_;
   const Tabs<2, 2> T = make_tabs<2, 2>(p);
   const unsigned grid = (unsigned)((ncells + m1::CPB - 1) / m1::CPB);
   kern<<<grid, m1::CPB, m1::SMEM, s>>>(T, ncells, coords, A);

@@ -199,14 +199,9 @@ int launch_hex_matrix_tc4(const sfk_plan* p, int64_t ncells, double* A, const do
                           cudaStream_t s, const int32_t* emap) {
   if (p->n != 4 || p->m != 4 || p->collocated) return SFK_EUNSUPPORTED;
   if (!emap && (reinterpret_cast<uintptr_t>(A) & 15) != 0) return SFK_EUNSUPPORTED;   // double2 stores
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(hex_laplace_matrix_tc4,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)m4::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_matrix_tc4)");
-    configured = true;
-  }
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)hex_laplace_matrix_tc4, m4::THREADS, m4::SMEM, "hex_matrix_tc4", &sh))
+    return rc_;
   TabsMat4 T;
   for (int i = 0; i < 16; ++i) {
     T.B[i] = p->B[i];
@@ -217,17 +212,7 @@ int launch_hex_matrix_tc4(const sfk_plan* p, int64_t ncells, double* A, const do
     T.Bc[q] = p->Bc[q];
     T.Bc[4 + q] = p->Bc[4 + q];
   }
-  static int sms = 0, per_sm = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, hex_laplace_matrix_tc4, m4::THREADS, m4::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "occupancy(hex_matrix_tc4)");
-    if (per_sm < 1) per_sm = 1;
-  }
-  const int64_t resident = (int64_t)sms * per_sm;
+  const int64_t resident = sh.resident();
   const unsigned grid = (unsigned)(ncells < resident ? ncells : resident);
   hex_laplace_matrix_tc4<<<grid, m4::THREADS, m4::SMEM, s>>>(T, ncells, coords, A, emap);
   note_launch();
@@ -440,20 +425,9 @@ hex_laplace_matrix_tc5(const __grid_constant__ TabsMat5 T, int64_t ncells,
 int launch_hex_matrix_tc5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                           cudaStream_t s, const int32_t* emap) {
   if (p->n != 5 || p->m != 5 || p->collocated) return SFK_EUNSUPPORTED;
-  static int sms = 0, per_sm = 0;
-  if (!sms) {
-    cudaError_t e = cudaFuncSetAttribute(hex_laplace_matrix_tc5,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)m5::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(hex_matrix_tc5)");
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hex_laplace_matrix_tc5,
-                                                      m5::THREADS, m5::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "occupancy(hex_matrix_tc5)");
-    if (per_sm < 1) return fail(SFK_ECUDA, "hex_matrix_tc5 does not fit on an SM");
-  }
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)hex_laplace_matrix_tc5, m5::THREADS, m5::SMEM, "hex_matrix_tc5", &sh))
+    return rc_;
   TabsMat5 T;
   for (int i = 0; i < 25; ++i) {
     T.B[i] = p->B[i];
@@ -464,7 +438,7 @@ int launch_hex_matrix_tc5(const sfk_plan* p, int64_t ncells, double* A, const do
     T.Bc[q] = p->Bc[q];
     T.Bc[5 + q] = p->Bc[5 + q];
   }
-  const int64_t resident = (int64_t)sms * per_sm;
+  const int64_t resident = sh.resident();
   const unsigned grid = (unsigned)(ncells < resident ? ncells : resident);
   hex_laplace_matrix_tc5<<<grid, m5::THREADS, m5::SMEM, s>>>(T, ncells, coords, A, emap);
   note_launch();

@@ -375,19 +375,12 @@ static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double
   constexpr size_t SMEM = WARPS ? WARPS * C::SMEM : C::SMEM;
   constexpr int CPBT = WARPS ? WARPS * CPB : CPB;
   auto k = hex_neohookean_kernel<N, M, CPB, GS, WARPS>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)SMEM);
-  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(neohookean)");
-  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, SMEM);
-  if (e != cudaSuccess) return cuda_status(e, "occupancy(neohookean)");
-  if (per_sm < 1) return fail(SFK_ECUDA, "neo-Hookean kernel does not fit on an SM");
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)k, THREADS, SMEM, "hex_neohookean", &sh, true))
+    return rc_;
   const Tabs<N, M> T = make_tabs<N, M>(p);
   const int64_t nbatch = (ncells + CPBT - 1) / CPBT;
-  const int64_t resident = (int64_t)sms * per_sm;
+  const int64_t resident = sh.resident();
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
   k<<<grid, THREADS, SMEM, s>>>(T, p->params[0], p->params[1], ncells, coords, u, A, cmap);
   note_launch();
@@ -424,10 +417,8 @@ template <bool GS>
 static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                         const double* w0, cudaStream_t s, const int* cmap) {
   const int n = p->n, m = p->m;
-  static const int warps = [] {
-    const char* e = std::getenv("SFK_NEO_WARPS");
-    return e ? std::atoi(e) : SFK_NEO_WARPS_DEFAULT;
-  }();
+  const int64_t ow = option(OPT_NEO_WARPS);   // 0: built-in, < 0: off
+  const int warps = ow == 0 ? SFK_NEO_WARPS_DEFAULT : ow < 0 ? 0 : (int)ow;
   if (m == n + 1 && warps > 0 && n <= 4) {
     // warp-synchronous: 3 / 2 / 1 cells per warp at p = 1 / 2 / 3
     if (warps == 8) {

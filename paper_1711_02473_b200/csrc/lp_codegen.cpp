@@ -20,6 +20,7 @@
 #include <stdexcept>
 
 #include "lp_program.h"
+#include "sfk_options.h"
 
 namespace sfk {
 namespace lp {
@@ -631,7 +632,7 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
   auto bytes_of = [&](int nc) { return tb + peak * ncp_of(nc) * 8; };
   int nc = 0;
   long long cta_budget = 56 * 1024;  // ~4 CTAs per SM (measured best, tools/lp_sweep.sh)
-  if (const char* e = std::getenv("SFK_LP_SMEM_KB")) cta_budget = std::atoll(e) * 1024;
+  if (option(OPT_LP_SMEM_KB) > 0) cta_budget = option(OPT_LP_SMEM_KB) * 1024;
   for (int cand = 32; cand >= 1; cand /= 2)
     if (bytes_of(cand) <= cta_budget) { nc = cand; break; }
   if (!nc && bytes_of(1) <= smem_limit) nc = 1;
@@ -672,19 +673,19 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
   }
   long long tmax = 256;
   if (median > 256 && median <= 512) maxitems = median, tmax = 512;
-  if (const char* e = std::getenv("SFK_LP_MAX_THREADS")) tmax = std::atoll(e);
+  if (option(OPT_LP_MAX_THREADS) > 0) tmax = option(OPT_LP_MAX_THREADS);
   C.threads = (int)std::min<long long>(tmax, std::max<long long>(64, ((maxitems + 31) / 32) * 32));
 
   // warp mode: with at least one cell per warp, every warp owns whole cells
   // through all phases, so all dependencies stay inside a warp and the
   // barriers become __syncwarp (the CTA-wide version spent 18% of its stalls
-  // at barriers, profiles/r01av_lp_p3.md).  SFK_LP_WARP=0 disables it.
+  // at barriers, profiles/r01av_lp_p3.md).  option lp_warp = -1 disables it.
   {
     // measured (profiles/r01bc_lp_warp.jsonl): a win for matrix-shaped
     // programs (laplace hex p=2 1.04 -> 0.72 ms, curl_curl, prism matrices),
     // a loss for the actions, whose large phases want many threads per cell
     bool wm = C.cells_per_block >= 2 && !C.global_scratch && P.ret_size >= 128;
-    if (const char* e = std::getenv("SFK_LP_WARP")) wm = wm && std::atoi(e) != 0;
+    if (option(OPT_LP_WARP) < 0) wm = false;
     if (wm) {
       // largest power of two <= min(threads / 32, NC) (NC is a power of two)
       const int cap = std::max(1, std::min(C.threads / 32, C.cells_per_block));
@@ -804,7 +805,7 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
   // registers: enough CTAs for the smem budget, at most 1024 threads per SM
   const long long smem_ctas = std::max<long long>(1, (228 * 1024) / (C.smem_bytes + 1024));
   long long minb = std::max<long long>(1, std::min<long long>(smem_ctas, 1024 / T));
-  if (const char* e = std::getenv("SFK_LP_MINB")) minb = std::atoll(e);
+  if (option(OPT_LP_MINB) > 0) minb = option(OPT_LP_MINB);
   o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << minb << ") "
     << G.entry
     << "(double* __restrict__ gA";
@@ -875,7 +876,7 @@ Generated generate(const Program& P, int64_t smem_limit, bool allow_fma) {
   // fused loop groups: consecutive NEST phases with the same trip count, no
   // barrier between them and only same-item dependences share one loop over w
   bool fusion = true;
-  if (const char* e = std::getenv("SFK_LP_FUSE")) fusion = std::atoi(e) != 0;
+  if (option(OPT_LP_FUSE) < 0) fusion = false;
   ItemWindow iwin(C.slots * LN);
   long long group_trips = -1;   // trip count of the open loop group (-1: none open)
   auto close_group = [&]() {

@@ -40,7 +40,7 @@ void note_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed)
 
 // Hex Laplace action (BASELINE C2) kernel generation per degree.  The
 // default ("auto") is the fastest measured generation for each n = p+1
-// (profiles/r01*_*.json A/B runs); SFK_C2_KERNEL=v1|v2|v3|tc forces one
+// (profiles/r01*_*.json A/B runs); option c2_kernel (sfk_set_option) forces one
 // (tuning / A-B runs; a generation that has no instance for n falls back).
 //   v1: line kernel, thread per line, non-persistent       (hex_action.cu)
 //   v2: persistent, cp.async prefetch, in-place z passes    (hex_action2.cu)
@@ -48,20 +48,7 @@ void note_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed)
 //   tc: FP64 tensor-core (DMMA) stages, n = 8               (hex_action_tc.cu)
 //   cell: one thread per cell, everything in registers, n = 2 (hex_action_p1.cu)
 //   v4: v3 with whole cells per warp, no CTA barriers, n = 3..5 (hex_action4.cu)
-static int c2_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SFK_C2_KERNEL");
-    v = 0;
-    if (e && e[0] == 'v' && e[1] >= '1' && e[1] <= '3') v = e[1] - '0';
-    if (e && strcmp(e, "tc") == 0) v = 4;
-    if (e && strcmp(e, "cell") == 0) v = 5;
-    if (e && strcmp(e, "v4") == 0) v = 6;
-    if (e && strcmp(e, "v5") == 0) v = 7;
-    if (e && strcmp(e, "cellv") == 0) v = 8;
-  }
-  return v;
-}
+static int c2_variant() { return (int)option(OPT_C2_KERNEL); }
 
 static int c2_auto(int n) {
   switch (n) {
@@ -119,7 +106,7 @@ static int dispatch(const sfk_plan* p, int64_t ncells, double* A,
       return launch_hex_colloc_action(p, ncells, A, coords, w0, w1, s);
     case SFK_KIND_ACTION_MASS:
       if (p->dim == 2) return launch_quad_action(p, nullptr, ncells, A, nullptr, coords, w0, s);
-      return fail(SFK_EUNSUPPORTED, "action_mass: only the quad kernel is instantiated");
+      return launch_hex_mass(p, ncells, A, coords, w0, s);
     case SFK_KIND_LAPLACE_MATRIX:
       if (p->dim == 3) return launch_hex_matrix(p, ncells, A, coords, s);
       return fail(SFK_EUNSUPPORTED, "laplace matrix: only the hex kernel is instantiated");
@@ -179,6 +166,31 @@ static HostCtx* host_ctx(int dev) {
   return (dev >= 0 && dev < 64) ? &ctx[dev] : nullptr;
 }
 
+// The instance table of dispatch(): true when (kind, cell dim, n, m,
+// collocated) reaches a kernel.  sfk_plan_create rejects every other
+// combination, so an unsupported request fails when the plan is built (the
+// reference raises at compile time, cli.py:155-208), never at eval.
+static bool kernel_available(int kind, int dim, int n, int m, int colloc) {
+  const bool hex_line = (n == m && n >= 2 && n <= 10) || (m == n + 1 && n >= 2 && n <= 8);
+  const bool quad = dim == 2 && !colloc && n == m && n >= 2 && n <= 9;
+  const bool colloc_hex = dim == 3 && colloc && n == m && n >= 2 && n <= 17;
+  switch (kind) {
+    case SFK_KIND_ACTION_LAPLACE:
+      return dim == 3 ? (colloc ? colloc_hex : hex_line) : quad;
+    case SFK_KIND_ACTION_WEIGHTED_LAPLACE:
+      return colloc_hex;
+    case SFK_KIND_ACTION_MASS:
+      return dim == 3 ? hex_mass_supported(n, m) : quad;
+    case SFK_KIND_LAPLACE_MATRIX:
+      return dim == 3 && !colloc && n == m && n >= 2 && n <= 5;
+    case SFK_KIND_NEOHOOKEAN_RESIDUAL:
+      return dim == 3 && !colloc &&
+             ((m == n + 1 && n >= 2 && n <= 7) || (m == n && n >= 2 && n <= 4));
+    default:
+      return false;
+  }
+}
+
 static int validate(const sfk_plan* p, int64_t ncells, const double* A,
                     const double* coords, const double* w0, const double* w1) {
   if (!p) return fail(SFK_EINVAL, "plan is NULL");
@@ -213,6 +225,10 @@ int sfk_plan_create(int kind, int cell_dim, int degree, int n, int m, int colloc
   if (!B || !D || !wq || !xq || !Bc || !Dc) return fail(SFK_EINVAL, "NULL table pointer");
   if (nparams < 0 || nparams > 8 || (nparams > 0 && !params))
     return fail(SFK_EINVAL, "bad params (nparams=%d)", nparams);
+  if (!kernel_available(kind, cell_dim, n, m, collocated ? 1 : 0))
+    return fail(SFK_EUNSUPPORTED,
+                "no kernel for kind %d on a %s with %d dofs/axis, %d points/axis%s", kind,
+                cell_dim == 3 ? "hex" : "quad", n, m, collocated ? " (collocated)" : "");
   sfk_plan* p = new (std::nothrow) sfk_plan();
   if (!p) return fail(SFK_ENOMEM, "plan allocation failed");
   p->kind = kind;
@@ -258,6 +274,10 @@ int sfk_plan_create(int kind, int cell_dim, int degree, int n, int m, int colloc
   }
   *out = p;
   return SFK_OK;
+}
+
+int sfk_kernel_available(int kind, int cell_dim, int n_dof1d, int n_q1d, int collocated) {
+  return kernel_available(kind, cell_dim, n_dof1d, n_q1d, collocated ? 1 : 0) ? 1 : 0;
 }
 
 int sfk_plan_destroy(sfk_plan* plan) {
@@ -310,10 +330,7 @@ static int eval_host_impl(const sfk_plan* p, int64_t ncells, double* A, const do
     // tools/pcie_probe.py: 55 GB/s H2D, 57 GB/s D2H, 100 GB/s concurrent).
     // e2e GDoF/s by chunk size 16 / 32 / 64 / 128 / 256 MiB: 4.34 / 4.74 /
     // 4.94 / 5.09 / 4.79 (profiles/r01df_*.jsonl)
-    static const long long mb = [] {
-      const char* e = getenv("SFK_HOST_CHUNK_MB");   // A/B runs only
-      return e ? atoll(e) : 128ll;
-    }();
+    const long long mb = option(OPT_HOST_CHUNK_MB) > 0 ? option(OPT_HOST_CHUNK_MB) : 128ll;
     chunk = (int64_t)((mb << 20) / (8 * per_cell));
     if (chunk < 1024) chunk = 1024;
   }

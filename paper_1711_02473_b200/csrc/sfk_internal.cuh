@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "../../include/sfk.h"
+#include "sfk_options.h"
 
 #define SFK_MAXN 17   // dofs per axis (p <= 16)
 #define SFK_MAXM 18   // quadrature points per axis
@@ -152,6 +153,9 @@ int launch_hex_matrix_csr(const sfk_plan* p, int64_t ncells, const int32_t* dofs
 int launch_hex_neohookean(const sfk_plan* p, int64_t ncells, double* A,
                           const double* coords, const double* w0,
                           cudaStream_t s);
+int launch_hex_mass(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                    const double* w0, cudaStream_t s);
+bool hex_mass_supported(int n, int m);
 int launch_sum_squares(const double* x, int64_t n, double* out, cudaStream_t s);
 int run_fp64_peak(double seconds, double* dfma, double* dmma);
 

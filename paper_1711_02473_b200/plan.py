@@ -217,10 +217,18 @@ def compile_form(spec, cell, degree, mode="spectral", variant="equispaced",
     if kind == KIND_NEOHOOKEAN_RESIDUAL:
         params = (spec.parameters.get("mu", 1.0),
                   spec.parameters.get("lambda", 10.0))
+    n, m = len(f0.nodes), len(pts)
+    from .runtime import kernel_available
+
+    if not kernel_available(kind, d, n, m, is_colloc):
+        raise Unsupported(
+            "no B200 kernel for %s on %s at degree %d with %d quadrature points per "
+            "direction%s (kernel instances: sfk_kernel_available, csrc/sfk_api.cu)"
+            % (spec.name, cell, degree, m, ", collocated" if is_colloc else ""))
     meta = {"form": spec.name, "cell": cell, "degree": element.degree,
             "mode": mode, "variant": variant}
     return KernelPlan(spec.name, return_size, arguments, meta, kind, d,
-                      len(f0.nodes), len(pts), is_colloc, tabs[0], tabs[1],
+                      n, m, is_colloc, tabs[0], tabs[1],
                       r0.weights, pts, ctabs[0], ctabs[1], params)
 
 

@@ -17,6 +17,7 @@ CPU fallback: without a GPU or without libsfk.so every call raises.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 import threading
@@ -25,7 +26,8 @@ import numpy as np
 
 from .errors import NativeError, ShapeMismatch, UnboundVariable
 
-__all__ = ["load_library", "evaluate_batched", "evaluate_batched_pair",
+__all__ = ["load_library", "evaluate_batched", "evaluate_batched_pair", "set_option",
+           "get_option",
            "evaluate_host", "sum_squares", "launch_count", "fp64_peak",
            "device_info", "native_plan", "EXPORTED_SYMBOLS"]
 
@@ -42,7 +44,8 @@ EXPORTED_SYMBOLS = (
     "sfk_program_sizes", "sfk_program_config", "sfk_program_text", "sfk_program_eval",
     "sfk_csr_create", "sfk_csr_info", "sfk_csr_destroy", "sfk_assemble_csr",
     "sfk_csr_entry_map", "sfk_eval_global", "sfk_eval_host_async", "sfk_host_wait",
-    "sfk_csr_insert",
+    "sfk_csr_insert", "sfk_set_option", "sfk_get_option",
+    "sfk_kernel_available",
 )
 ABI_VERSION = 1
 SUM_WORKSPACE = 1024
@@ -103,6 +106,14 @@ def _declare(lib):
         lib.sfk_csr_entry_map.restype = ci
         lib.sfk_assemble_csr.argtypes = [_vp, i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         lib.sfk_assemble_csr.restype = ci
+    if hasattr(lib, "sfk_kernel_available"):
+        lib.sfk_kernel_available.argtypes = [ci] * 5
+        lib.sfk_kernel_available.restype = ci
+    if hasattr(lib, "sfk_set_option"):
+        lib.sfk_set_option.argtypes = [ctypes.c_char_p, i64]
+        lib.sfk_set_option.restype = ci
+        lib.sfk_get_option.argtypes = [ctypes.c_char_p, ctypes.POINTER(i64)]
+        lib.sfk_get_option.restype = ci
     if hasattr(lib, "sfk_csr_insert"):
         lib.sfk_csr_insert.argtypes = [i64, ci, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         lib.sfk_csr_insert.restype = ci
@@ -164,6 +175,13 @@ class _NativePlan:
             pass
 
 
+def kernel_available(kind, dim, n, m, collocated):
+    """The C library's instance table (sfk_kernel_available): is there a
+    kernel for this (kind, cell dim, dofs/axis, points/axis, collocated)?"""
+    return bool(load_library().sfk_kernel_available(int(kind), int(dim), int(n), int(m),
+                                                     int(bool(collocated))))
+
+
 def native_plan(plan):
     """The C-ABI plan handle of a KernelPlan (created once, cached)."""
     np_ = plan._native.get("handle")
@@ -222,12 +240,57 @@ def evaluate_batched(plan, inputs, out=None, stream=None):
     first = next(iter(inputs.values()), None) if inputs else None
     if first is not None and isinstance(first, np.ndarray):
         return evaluate_host(plan, inputs, out=out)
+    args, ncells, squeeze, dev, stream = _device_args(plan, inputs, stream)
+    rsize = plan.return_size
+    import torch
+
+    if out is None:
+        out = torch.empty((ncells, rsize), dtype=torch.float64, device=dev)
+    else:
+        _check_out(out, (ncells, rsize), dev, args)
+    handle = native_plan(plan)
+    with torch.cuda.device(dev):
+        _check(_LIB.sfk_eval(handle, ncells, out.data_ptr(),
+                             args["coords"].data_ptr(),
+                             args["w0"].data_ptr() if "w0" in args else None,
+                             args["w1"].data_ptr() if "w1" in args else None,
+                             stream))
+    return out.reshape(rsize) if squeeze else out
+
+
+def evaluate_batched_pair(plan0, plan1, inputs, stream=None):
+    """Two plans over the same (coords, w0) in one fused launch when the pair
+    has a fused kernel (quad mass + Laplace action, BASELINE config C1).
+    Same validation as ``evaluate_batched``."""
+    import torch
+
+    _collect(plan1, inputs, True)
+    args, ncells, _, dev, stream = _device_args(plan0, inputs, stream)
+    a0 = torch.empty((ncells, plan0.return_size), dtype=torch.float64, device=dev)
+    a1 = torch.empty((ncells, plan1.return_size), dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        _check(load_library().sfk_eval_pair(
+            native_plan(plan0), native_plan(plan1), ncells, a0.data_ptr(),
+            a1.data_ptr(), args["coords"].data_ptr(),
+            args["w0"].data_ptr() if "w0" in args else None, stream))
+    return a0, a1
+
+
+def _device_args(plan, inputs, stream):
+    """Validate device inputs (reference interpreter.py:291-299 checks, then
+    dtype / device / contiguity) and resolve the stream handle.
+
+    Non-contiguous arguments are copied on the CURRENT torch stream; when the
+    kernel runs on another ``stream`` that stream is made to wait for the
+    copies and the temporaries are recorded on it, so the caching allocator
+    cannot hand their memory out before the kernel has read it."""
     import torch
 
     args, ncells, squeeze = _collect(plan, inputs, True)
     if not torch.cuda.is_available():
         raise NativeError(-1, "evaluate_batched needs a CUDA device (no CPU fallback)")
     dev = None
+    copied = []
     for name, t in args.items():
         if not isinstance(t, torch.Tensor):
             raise TypeError("argument %s must be a torch.Tensor or numpy array" % name)
@@ -240,41 +303,39 @@ def evaluate_batched(plan, inputs, out=None, stream=None):
             raise ValueError("all arguments must be on one device")
         if not t.is_contiguous():
             args[name] = t.contiguous()
-    rsize = plan.return_size
-    if out is None:
-        out = torch.empty((ncells, rsize), dtype=torch.float64, device=dev)
-    elif tuple(out.shape) != (ncells, rsize) or not out.is_contiguous():
-        raise ShapeMismatch("out must be a contiguous (%d, %d) tensor" % (ncells, rsize))
-    handle = native_plan(plan)
+            copied.append(args[name])
+    if dev is None:
+        raise UnboundVariable("coords")
+    cur = torch.cuda.current_stream(dev)
     if stream is None:
-        stream = torch.cuda.current_stream(dev).cuda_stream
-    with torch.cuda.device(dev):
-        _check(_LIB.sfk_eval(handle, ncells, out.data_ptr(),
-                             args["coords"].data_ptr(),
-                             args["w0"].data_ptr() if "w0" in args else None,
-                             args["w1"].data_ptr() if "w1" in args else None,
-                             stream))
-    return out.reshape(rsize) if squeeze else out
+        stream = cur.cuda_stream
+    elif copied and int(stream) != cur.cuda_stream:
+        ext = torch.cuda.ExternalStream(int(stream), device=dev)
+        ext.wait_stream(cur)
+        for t in copied:
+            t.record_stream(ext)
+    return args, ncells, squeeze, dev, stream
 
 
-def evaluate_batched_pair(plan0, plan1, inputs, stream=None):
-    """Two plans over the same (coords, w0) in one fused launch when the pair
-    has a fused kernel (quad mass + Laplace action, BASELINE config C1)."""
+def _check_out(out, shape, dev, args):
     import torch
 
-    args, ncells, _ = _collect(plan0, inputs, True)
-    _collect(plan1, inputs, True)
-    dev = args["coords"].device
-    a0 = torch.empty((ncells, plan0.return_size), dtype=torch.float64, device=dev)
-    a1 = torch.empty((ncells, plan1.return_size), dtype=torch.float64, device=dev)
-    if stream is None:
-        stream = torch.cuda.current_stream(dev).cuda_stream
-    with torch.cuda.device(dev):
-        _check(load_library().sfk_eval_pair(
-            native_plan(plan0), native_plan(plan1), ncells, a0.data_ptr(),
-            a1.data_ptr(), args["coords"].contiguous().data_ptr(),
-            args["w0"].contiguous().data_ptr(), stream))
-    return a0, a1
+    if not isinstance(out, torch.Tensor) or out.dtype != torch.float64:
+        raise TypeError("out must be a float64 torch.Tensor")
+    if tuple(out.shape) != shape or not out.is_contiguous():
+        raise ShapeMismatch("out must be a contiguous (%d, %d) tensor" % shape)
+    if out.device != dev:
+        raise ValueError("out must be on %s, got %s" % (dev, out.device))
+    for name, t in args.items():
+        if out.numel() and t.numel() and _overlaps(out, t):
+            raise ValueError("out must not alias argument %s (A is overwritten)" % name)
+
+
+def _overlaps(a, b):
+    a0, b0 = a.data_ptr(), b.data_ptr()
+    a1 = a0 + a.numel() * a.element_size()
+    b1 = b0 + b.numel() * b.element_size()
+    return a0 < b1 and b0 < a1
 
 
 def evaluate_host(plan, inputs, out=None, chunk_cells=0):
@@ -331,6 +392,63 @@ def sum_squares(x, workspace=None, stream=None):
         _check(load_library().sfk_sum_squares(x.data_ptr(), x.numel(),
                                               workspace.data_ptr(), stream))
     return workspace[:2]
+
+
+# Kernel-variant names of option "c2_kernel" (sfk_options.h OPT_C2_KERNEL).
+C2_KERNELS = {"auto": 0, "v1": 1, "v2": 2, "v3": 3, "tc": 4, "cell": 5, "v4": 6, "v5": 7,
+              "cellv": 8, "eo": 9}
+
+
+def set_option(name, value):
+    """Set a process-wide tuning option of libsfk (A/B runs; 0 = built-in
+    choice).  ``c2_kernel`` also accepts a generation name (``"v5"``)."""
+    if name == "c2_kernel" and isinstance(value, str):
+        value = C2_KERNELS[value]
+    _check(load_library().sfk_set_option(name.encode(), int(value)))
+
+
+def get_option(name):
+    v = ctypes.c_int64()
+    _check(load_library().sfk_get_option(name.encode(), ctypes.byref(v)))
+    return v.value
+
+
+@contextlib.contextmanager
+def options(**values):
+    """Temporarily set tuning options (restored on exit)."""
+    old = {k: get_option(k) for k in values}
+    try:
+        for k, v in values.items():
+            set_option(k, v)
+        yield
+    finally:
+        for k, v in old.items():
+            set_option(k, v)
+
+
+def options_from_env(environ=None):
+    """Tools only: map the round-1 ``SFK_<NAME>=value`` A/B switches onto
+    set_option (the library itself reads no environment).  Returns the
+    options applied."""
+    env = os.environ if environ is None else environ
+    applied = {}
+    for key, val in env.items():
+        if not key.startswith("SFK_") or key in ("SFK_LIBRARY", "SFK_NVRTC"):
+            continue
+        name = key[4:].lower()
+        if name == "c2_kernel":
+            v = C2_KERNELS[val]
+        elif name in ("c2g_kernel", "c2g_small"):
+            v = int(val.lstrip("v"))
+        elif name in ("c5_p1", "c5_p3", "c5_p4"):
+            v = 1 if val.startswith("p") else 0
+        elif name in ("colloc_warps", "neo_warps", "lp_warp", "lp_fuse"):
+            v = int(val) if int(val) != 0 else -1
+        else:
+            v = int(val)
+        set_option(name, v)
+        applied[name] = v
+    return applied
 
 
 def launch_count():

@@ -243,6 +243,23 @@ def c5(degrees=(1, 2, 3, 4)):
     np.savez_compressed(os.path.join(HERE, "c5.npz"), **out)
 
 
+def mass_hex():
+    """Hex ``action_mass`` (registry, forms.py:173, 261-263): GL(p+1) and
+    GL(p+2) equispaced, and the GLL-collocated variant (B = Delta)."""
+    coords = _small_lattice()[:3]
+    out = {"coords": coords}
+    cases = [("gl", p, "equispaced", None) for p in range(1, 9)]
+    cases += [("glp2", p, "equispaced", p + 2) for p in (1, 2, 4)]
+    cases += [("gll", p, "spectral_gll", "collocated-gll") for p in (2, 4, 7)]
+    for tag, p, variant, quad in cases:
+        n = p + 1
+        w0 = workloads.uniform_dofs(3, n ** 3)
+        k = _request("action_mass", "hex", p, variant, quad)
+        out["w0_%s_p%d" % (tag, p)] = w0
+        out["A_%s_p%d" % (tag, p)] = _evaluate(k, coords, w0)
+    np.savez_compressed(os.path.join(HERE, "mass_hex.npz"), **out)
+
+
 def flops():
     rec = {}
     for p in range(1, 9):

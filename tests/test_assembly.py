@@ -254,34 +254,27 @@ def test_vector_dof_map_layout():
 
 @pytest.mark.gpu
 def test_csr_dmma_epilogue_opt_in(cuda):
-    """The DMMA kernels' entry-map CSR epilogue (opt-in, SFK_CSR_DMMA=1) gives
-    the same assembled matrices."""
-    import os
-    import subprocess
-    import sys
+    """The DMMA kernels' entry-map CSR epilogue (opt-in, option csr_dmma = 1)
+    gives the same assembled matrices."""
+    from paper_1711_02473_b200 import runtime
 
-    env = dict(os.environ, SFK_CSR_DMMA="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m",
-                        "gpu", "-k", "csr_assembly_matches_oracle"],
-                       env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:]
+    with runtime.options(csr_dmma=1):
+        for p in (3, 4):
+            for numbering in ("lattice", "permuted"):
+                test_csr_assembly_matches_oracle(cuda, p, numbering)
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("gen", ["v2", "v3"])
+@pytest.mark.parametrize("gen", [2, 3])
 def test_gather_scatter_alternative_generations(cuda, gen):
-    """The global operator through the older kernel generations
-    (SFK_C2G_KERNEL=v2 / v3; the default is v5 at p = 5, 6, 8) agrees with
-    the assembled oracle too."""
-    import os
-    import subprocess
-    import sys
+    """The global operator through the older kernel generations (option
+    c2g_kernel = 2 / 3; the default is v5 at p = 5, 6, 8) agrees with the
+    assembled oracle too."""
+    from paper_1711_02473_b200 import runtime
 
-    env = dict(os.environ, SFK_C2G_KERNEL=gen)
-    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m",
-                        "gpu", "-k", "gather_scatter_matches_oracle"],
-                       env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:]
+    with runtime.options(c2g_kernel=gen):
+        for p in range(1, 9):
+            test_gather_scatter_matches_oracle(cuda, p)
 
 
 # ---------------------------------------------------------------------------

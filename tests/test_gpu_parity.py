@@ -326,63 +326,43 @@ def test_non_contiguous_and_offset_inputs(cuda):
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_c2_every_kernel_generation(cuda, p):
     """Each C2 kernel generation that has an instance for n = p+1 agrees with
-    the oracle (the auto selection only changes speed, never results)."""
-    import subprocess
-    import sys
-
-    code = (
-        "import numpy as np, torch, sys; sys.path.insert(0, %r);"
-        "from paper_1711_02473_b200 import compile_kernel, evaluate_batched, workloads;"
-        "from oracle import cpu;"
-        "plan = compile_kernel('action_laplace', 'hex', %d);"
-        "inp = workloads.c2_inputs(%d, dims=(5, 5, 7));"
-        "out = evaluate_batched(plan, {k: torch.from_numpy(v).cuda() for k, v in inp.items()}).cpu().numpy();"
-        "ref = cpu.evaluate(plan, inp);"
-        "err = (np.abs(out-ref).max(axis=1)/np.abs(ref).max(axis=1)).max();"
-        "print(err); assert err < 1e-12"
-    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), p, p)
-    gens = [(g, {}) for g in ("v1", "v2", "v3", "v4", "tc", "cell", "v5", "cellv")]
-    gens += [("v5", {"SFK_C2_G": g}) for g in ("1", "2", "3")]
-    for gen, extra in gens:
-        env = dict(os.environ, SFK_C2_KERNEL=gen, **extra)
-        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
-        assert r.returncode == 0, (gen, extra, r.stdout, r.stderr[-2000:])
+    the oracle (the auto selection only changes speed, never results);
+    selected in-process through the explicit option API (sfk_set_option)."""
+    plan = compile_kernel("action_laplace", "hex", p)
+    inp = workloads.c2_inputs(p, dims=(5, 5, 7))
+    ref = cpu.evaluate(plan, inp)
+    gens = [(g, 0) for g in ("v1", "v2", "v3", "v4", "tc", "cell", "v5", "cellv", "eo")]
+    gens += [("v5", g) for g in (1, 2, 3)]
+    for gen, g in gens:
+        with runtime.options(c2_kernel=runtime.C2_KERNELS[gen], c2_g=g):
+            err = rel_err(_run(cuda, plan, inp), ref)
+        assert err < TOL, (gen, g, err)
 
 
 @pytest.mark.parametrize("mode", ["colloc_warps", "neo_cta", "colloc_tc"])
 def test_alternative_kernel_modes(cuda, mode):
     """Kernel modes that are off by default for speed (C3's warp-synchronous
-    variant, SFK_COLLOC_WARPS) or on by default (C4's, SFK_NEO_WARPS=0 turns
-    it off) agree with the oracle too."""
-    import subprocess
-    import sys
+    variant, option colloc_warps; C3's DMMA variant, c3_tc) or on by default
+    (C4's warp-synchronous variant; neo_warps = -1 turns it off) agree with
+    the oracle too."""
+    from paper_1711_02473_b200 import (REGISTRY, action_form, compile_form,
+                                       neohookean_residual_form)
 
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     if mode in ("colloc_warps", "colloc_tc"):
-        env_var, degrees = (({"SFK_COLLOC_WARPS": "8"}, (1, 2, 3, 4)) if mode == "colloc_warps"
-                            else ({"SFK_C3_TC": "1"}, (7, 11, 15)))
-        build = ("compile_form(action_form(REGISTRY['weighted_laplace']), 'hex', p, 'spectral',"
-                 " 'spectral_gll', 'collocated-gll')")
-        inputs = "workloads.c3_inputs(p, dims=(3, 5, 7))"
+        opts, degrees = (({"colloc_warps": 8}, (1, 2, 3, 4)) if mode == "colloc_warps"
+                         else ({"c3_tc": 1}, (7, 11, 15)))
+        build = lambda p: compile_form(action_form(REGISTRY["weighted_laplace"]), "hex", p,  # noqa
+                                       "spectral", "spectral_gll", "collocated-gll")
+        inputs = lambda p: workloads.c3_inputs(p, dims=(3, 5, 7))  # noqa
     else:
-        env_var, degrees = {"SFK_NEO_WARPS": "0"}, (1, 2, 3)
-        build = "compile_form(neohookean_residual_form(), 'hex', p, quadrature=p + 2)"
-        inputs = "workloads.c4_inputs(p, dims=(3, 5, 7))"
-    code = (
-        "import numpy as np, torch, sys; sys.path.insert(0, %r);"
-        "from paper_1711_02473_b200 import *; from paper_1711_02473_b200 import workloads;"
-        "from oracle import cpu;"
-        "errs = []\n"
-        "for p in %r:\n"
-        "    plan = %s; inp = %s\n"
-        "    out = evaluate_batched(plan, {k: torch.from_numpy(v).cuda() for k, v in inp.items()}).cpu().numpy()\n"
-        "    ref = cpu.evaluate(plan, inp)\n"
-        "    errs.append((np.abs(out-ref).max(axis=1)/np.abs(ref).max(axis=1)).max())\n"
-        "print(errs); assert max(errs) < 1e-12"
-    ) % (root, degrees, build, inputs)
-    env = dict(os.environ, **env_var)
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
-    assert r.returncode == 0, (mode, r.stdout, r.stderr[-2000:])
+        opts, degrees = {"neo_warps": -1}, (1, 2, 3)
+        build = lambda p: compile_form(neohookean_residual_form(), "hex", p, quadrature=p + 2)  # noqa
+        inputs = lambda p: workloads.c4_inputs(p, dims=(3, 5, 7))  # noqa
+    for p in degrees:
+        plan, inp = build(p), inputs(p)
+        with runtime.options(**opts):
+            err = rel_err(_run(cuda, plan, inp), cpu.evaluate(plan, inp))
+        assert err < TOL, (mode, p, err)
 
 
 def test_host_async_overlapping_calls(cuda):
@@ -404,3 +384,20 @@ def test_host_async_overlapping_calls(cuda):
     for p, (plan, u, a) in res.items():
         dev = evaluate_batched(plan, {"coords": coords.cuda(), "w0": u.cuda()}).cpu()
         assert torch.equal(a, dev), p
+
+
+@pytest.mark.parametrize("tag,p", [("gl", p) for p in range(1, 9)] + [("glp2", p) for p in (1, 2, 4)]
+                         + [("gll", p) for p in (2, 4, 7)])
+def test_hex_mass_action(cuda, tag, p):
+    """Hex action_mass (registry forms.py:173, 261-263): the reference's own
+    outputs (golden) and the dense numpy restatement on a ragged batch."""
+    from oracle import dense
+    from test_oracle import mass_plan
+
+    g = np.load(os.path.join(GOLDEN, "mass_hex.npz"))
+    plan = mass_plan(tag, p)
+    inp = {"coords": g["coords"], "w0": g["w0_%s_p%d" % (tag, p)]}
+    assert rel_err(_run(cuda, plan, inp), g["A_%s_p%d" % (tag, p)]) < TOL
+    coords = workloads.lattice_coords(3, 3, 5)[:37]
+    inp = {"coords": coords, "w0": workloads.uniform_dofs(37, plan.n ** 3)}
+    assert rel_err(_run(cuda, plan, inp), dense.evaluate(plan, inp)) < TOL

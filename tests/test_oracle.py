@@ -103,3 +103,25 @@ def test_properties_patch_symmetry_consistency():
     act = cpu.evaluate(compile_kernel("action_laplace", "hex", p),
                        {"coords": coords, "w0": u})
     assert rel_err(act, np.einsum("cij,cj->ci", A, u)) < 1e-13
+
+
+MASS_CASES = ([("gl", p) for p in range(1, 9)] + [("glp2", p) for p in (1, 2, 4)]
+              + [("gll", p) for p in (2, 4, 7)])
+
+
+def mass_plan(tag, p):
+    if tag == "gl":
+        return compile_kernel("action_mass", "hex", p)
+    if tag == "glp2":
+        return compile_kernel("action_mass", "hex", p, quadrature=p + 2)
+    return compile_kernel("action_mass", "hex", p, "spectral", "spectral_gll", "collocated-gll")
+
+
+@pytest.mark.parametrize("tag,p", MASS_CASES)
+def test_hex_mass_golden(tag, p):
+    """Hex action_mass: the dense numpy restatement against the reference's
+    own eval_expr outputs (tests/golden/make_golden.py mass_hex)."""
+    g = np.load(os.path.join(GOLDEN, "mass_hex.npz"))
+    plan = mass_plan(tag, p)
+    inp = {"coords": g["coords"], "w0": g["w0_%s_p%d" % (tag, p)]}
+    assert rel_err(dense.evaluate(plan, inp), g["A_%s_p%d" % (tag, p)]) < TOL

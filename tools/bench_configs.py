@@ -257,4 +257,7 @@ def main():
 
 
 if __name__ == "__main__":
+    from paper_1711_02473_b200 import runtime as _rt
+
+    print("options from env:", _rt.options_from_env(), file=sys.stderr)
     main()

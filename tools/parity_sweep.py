@@ -6,7 +6,7 @@
 Families: c2, c3, c4, c5, c1, gs (global operators), csr, lp (generated
 kernels: CTA / warp / fused modes).  Every result is compared with the CPU
 oracle (or, for the generated kernels, the reference's golden outputs bit for
-bit).  compute-sanitizer is not available on this GPU pool, so odd batch
+bit).  odd batch
 sizes (partial CTAs, tails) and every mode switch are exercised here instead.
 """
 
@@ -125,6 +125,9 @@ FAMILIES = {"c2": fam_c2, "c3": fam_c3, "c4": fam_c4, "c5": fam_c5, "c1": fam_c1
             "gs": fam_gs, "csr": fam_csr, "lp": fam_lp}
 
 if __name__ == "__main__":
+    from paper_1711_02473_b200 import runtime as _rt
+
+    print("options from env:", _rt.options_from_env(), file=sys.stderr)
     for f in sys.argv[1:] or list(FAMILIES):
         FAMILIES[f]()
     torch.cuda.synchronize()
