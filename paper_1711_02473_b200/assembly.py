@@ -113,11 +113,16 @@ class GlobalOperator:
             w1 = w1.contiguous()
         elif w1 is not None:
             raise ShapeMismatch("plan %s takes no w1" % plan.name)
+        if coords.device != cell_dofs.device:
+            raise ValueError("cell_dofs and coords must be on one device")
         self.plan = plan
         self.cell_dofs = cell_dofs.contiguous()
         self.coords = coords.contiguous()
         self.ndofs = int(ndofs)
         self.w1 = w1
+        # one-time map check: an index outside [0, ndofs) would turn into an
+        # out-of-bounds fp64 atomic in the fused scatter
+        _check_map(self.cell_dofs, self.ndofs)
 
     def apply(self, x, out=None, accumulate=False, stream=None):
         import torch
@@ -126,11 +131,22 @@ class GlobalOperator:
 
         if x.dtype != torch.float64 or not x.is_cuda or x.numel() != self.ndofs:
             raise ShapeMismatch("x must be a float64 CUDA vector of length %d" % self.ndofs)
+        if x.device != self.coords.device:
+            raise ValueError("x must be on %s" % self.coords.device)
         x = x.contiguous()
         if out is None:
             out = torch.zeros_like(x)
-        elif not accumulate:
-            out.zero_()
+        else:
+            if (not isinstance(out, torch.Tensor) or out.dtype != torch.float64
+                    or out.device != x.device or out.numel() != self.ndofs
+                    or not out.is_contiguous()):
+                raise ShapeMismatch("out must be a contiguous float64 vector of length %d on %s"
+                                    % (self.ndofs, x.device))
+            if out.data_ptr() == x.data_ptr() or _aliases(out, x):
+                raise ValueError("out must not alias x (the gather reads x while the "
+                                 "scatter writes out)")
+            if not accumulate:
+                out.zero_()
         if stream is None:
             stream = torch.cuda.current_stream(x.device).cuda_stream
         with torch.cuda.device(x.device):
@@ -141,6 +157,36 @@ class GlobalOperator:
         return out
 
     __call__ = apply
+
+
+def _aliases(a, b):
+    a0, b0 = a.data_ptr(), b.data_ptr()
+    return a0 < b0 + b.numel() * b.element_size() and b0 < a0 + a.numel() * a.element_size()
+
+
+def _check_map(cell_dofs, ndofs):
+    """0 <= cell_dofs < ndofs (one device reduction, checked once)."""
+    if cell_dofs.numel() == 0:
+        return
+    lo = int(cell_dofs.min().item())
+    hi = int(cell_dofs.max().item())
+    if lo < 0 or hi >= ndofs:
+        raise ValueError("cell_dofs entries must lie in [0, %d), got [%d, %d]" % (ndofs, lo, hi))
+
+
+def _values(values, pattern, device):
+    """The CSR value array to accumulate into: zeros, or the caller's
+    (checked: float64, contiguous, nnz entries, on the pattern's device)."""
+    import torch
+
+    if values is None:
+        return torch.zeros(pattern.nnz, dtype=torch.float64, device=device)
+    if (not isinstance(values, torch.Tensor) or values.dtype != torch.float64
+            or not values.is_contiguous() or values.device != device):
+        raise ShapeMismatch("values must be a contiguous float64 tensor on %s" % device)
+    if values.numel() != pattern.nnz:
+        raise ShapeMismatch("values must have nnz = %d entries" % pattern.nnz)
+    return values
 
 
 def cg(op, b, fixed=None, tol=1e-10, maxiter=1000):
@@ -204,6 +250,7 @@ class CsrPattern:
         if cell_dofs.dtype != torch.int32 or not cell_dofs.is_cuda or cell_dofs.dim() != 2:
             raise TypeError("cell_dofs must be a 2D int32 CUDA tensor")
         cell_dofs = cell_dofs.contiguous()
+        _check_map(cell_dofs, int(ndofs))
         self._lib = load_library()
         self._h = ctypes.c_void_p()
         if stream is None:
@@ -285,10 +332,7 @@ def assemble_csr(plan, cell_dofs, coords, pattern, values=None, entry_map=None, 
                                   or tuple(entry_map.shape) != (coords.shape[0], n3 * n3)):
         raise ShapeMismatch("entry_map must be a contiguous int32 (%d, %d) tensor"
                             % (coords.shape[0], n3 * n3))
-    if values is None:
-        values = torch.zeros(pattern.nnz, dtype=torch.float64, device=coords.device)
-    elif values.numel() != pattern.nnz:
-        raise ShapeMismatch("values must have nnz = %d entries" % pattern.nnz)
+    values = _values(values, pattern, coords.device)
     if stream is None:
         stream = torch.cuda.current_stream(coords.device).cuda_stream
     with torch.cuda.device(coords.device):
@@ -323,10 +367,7 @@ def insert_csr(cell_matrices, cell_dofs, pattern, values=None, entry_map=None, s
                                   or entry_map.numel() != ncells * nd * nd):
         raise ShapeMismatch("entry_map must be a contiguous int32 (%d, %d) tensor"
                             % (ncells, nd * nd))
-    if values is None:
-        values = torch.zeros(pattern.nnz, dtype=torch.float64, device=cell_dofs.device)
-    elif values.numel() != pattern.nnz:
-        raise ShapeMismatch("values must have nnz = %d entries" % pattern.nnz)
+    values = _values(values, pattern, cell_dofs.device)
     if stream is None:
         stream = torch.cuda.current_stream(cell_dofs.device).cuda_stream
     with torch.cuda.device(cell_dofs.device):

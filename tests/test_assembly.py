@@ -356,3 +356,36 @@ def test_insert_csr_validates_arguments():
         insert_csr(torch.zeros(2, 4, dtype=torch.float64), torch.zeros(2, 2, dtype=torch.int32), None)
     with pytest.raises(TypeError):
         insert_csr(torch.zeros(2, 4, dtype=torch.float32), torch.zeros(2, 2, dtype=torch.int64), None)
+
+
+@pytest.mark.gpu
+def test_global_operator_validates_out_and_map(cuda):
+    """GlobalOperator rejects an out that is short, float32, or aliases x, and
+    a cell->dof map with entries outside [0, ndofs) (which the fused scatter
+    would otherwise turn into out-of-bounds fp64 atomics)."""
+    torch = cuda
+    from paper_1711_02473_b200.assembly import CsrPattern, GlobalOperator
+    from paper_1711_02473_b200.errors import ShapeMismatch
+
+    p = 2
+    plan = compile_kernel("action_laplace", "hex", p)
+    dims = (2, 3, 2)
+    cmap = torch.from_numpy(lattice_dof_map(*dims, p)).cuda()
+    coords = torch.from_numpy(workloads.lattice_coords(*dims)).cuda()
+    nd = lattice_ndofs(*dims, p)
+    op = GlobalOperator(plan, cmap, coords, nd)
+    x = torch.rand(nd, dtype=torch.float64, device="cuda")
+    with pytest.raises(ShapeMismatch):
+        op.apply(x, out=torch.zeros(nd - 1, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ShapeMismatch):
+        op.apply(x, out=torch.zeros(nd, dtype=torch.float32, device="cuda"))
+    with pytest.raises(ValueError):
+        op.apply(x, out=x)
+    y = op.apply(x)
+    assert torch.isfinite(y).all()
+    bad = cmap.clone()
+    bad[0, 0] = nd
+    with pytest.raises(ValueError):
+        GlobalOperator(plan, bad, coords, nd)
+    with pytest.raises(ValueError):
+        CsrPattern(bad, nd)
