@@ -47,7 +47,12 @@ def allreduce_sums(partials, group=None):
     import torch.distributed as dist
 
     if dist.is_available() and dist.is_initialized():
-        dist.all_reduce(partials, op=dist.ReduceOp.SUM, group=group)
+        if partials.is_cuda and dist.get_backend(group) == "gloo":
+            host = partials.cpu()                # gloo reduces host tensors
+            dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+            partials.copy_(host)
+        else:
+            dist.all_reduce(partials, op=dist.ReduceOp.SUM, group=group)
     return partials
 
 

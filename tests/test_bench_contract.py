@@ -49,6 +49,38 @@ def test_cpu_baseline_leg_reports_both_builds_and_single_thread():
     degs = [1, 2]
     coords = workloads.lattice_coords(8, 8, 8)
     hu = {p: workloads.uniform_dofs(coords.shape[0], (p + 1) ** 3) for p in degs}
-    cb = bench.cpu_baseline_leg(degs, coords, hu, 256)
+    dev_out = {p: bench_ref(p, coords, hu[p]) for p in degs}
+    cb, parity = bench.cpu_baseline_leg(degs, coords, hu, 256, dev_out)
     assert cb["kind"] == "reference" and cb["value"] > 0 and cb["cpu_model"]
     assert cb["single_thread"]["value"] > 0
+    assert cb["compiled_on_this_host"]
+    # the parity check itself: the oracle port vs the reference C, first 256 cells
+    assert set(parity) == set(degs) and max(parity.values()) < 1e-12
+
+
+def bench_ref(p, coords, u):
+    from oracle import cpu
+    from paper_1711_02473_b200 import compile_kernel
+    return cpu.evaluate(compile_kernel("action_laplace", "hex", p), {"coords": coords, "w0": u})
+
+
+def test_parity_err_metric():
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    import bench
+    ref = np.array([[1.0, -2.0, 0.5], [0.0, 0.0, 1e-3]])
+    assert bench.parity_err(ref, ref) == 0.0
+    x = ref.copy()
+    x[0, 1] += 2e-12       # 1e-12 relative to the cell's max |y| = 2
+    assert abs(bench.parity_err(x, ref) - 1e-12) < 1e-15
+    x = ref.copy()
+    x[1, 0] = np.nan       # NaN where the reference is finite
+    assert bench.parity_err(x, ref) == float("inf")
+
+
+def test_gpus_flag_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4",
+                          "--impl", "reference"], capture_output=True, text=True, env=env,
+                         timeout=300, cwd=ROOT)
+    assert res.returncode != 0 and "WORLD_SIZE" in res.stderr

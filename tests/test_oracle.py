@@ -125,3 +125,41 @@ def test_hex_mass_golden(tag, p):
     plan = mass_plan(tag, p)
     inp = {"coords": g["coords"], "w0": g["w0_%s_p%d" % (tag, p)]}
     assert rel_err(dense.evaluate(plan, inp), g["A_%s_p%d" % (tag, p)]) < TOL
+
+
+def _refc_or_skip(plan):
+    from oracle import refc
+    if not refc.available(plan):
+        pytest.skip("oracle/_ref (reference emitted C) not generated")
+    return refc
+
+
+@pytest.mark.parametrize("cfg,p", [("C2", p) for p in range(1, 9)] + [("C3", p) for p in (4, 8, 12, 16)]
+                         + [("C4", p) for p in range(2, 7)] + [("C5", p) for p in range(1, 5)])
+def test_oracle_port_vs_reference_emitted_c(cfg, p):
+    """The C restatement (oracle/cpu.py) against the reference's OWN emitted
+    C (oracle/_ref, built by gen_ref.py through the reference API) on 256
+    cells of each config's generator — a larger pin than the golden cells."""
+    if cfg == "C2":
+        plan = compile_kernel("action_laplace", "hex", p)
+        inp = workloads.c2_inputs(p, dims=(4, 8, 8))
+    elif cfg == "C3":
+        plan = compile_form(action_form(REGISTRY["weighted_laplace"]), "hex", p, "spectral",
+                            "spectral_gll", "collocated-gll")
+        inp = workloads.c3_inputs(p, dims=(4, 8, 8))
+    elif cfg == "C4":
+        plan = compile_form(neohookean_residual_form(), "hex", p, quadrature=p + 2)
+        inp = workloads.c4_inputs(p, dims=(4, 8, 8))
+    else:
+        plan = compile_kernel("laplace", "hex", p)
+        inp = workloads.c5_inputs(0, 1, (2, 4, 8))
+    refc = _refc_or_skip(plan)
+    with np.errstate(invalid="ignore"):
+        ref = refc.evaluate(plan, inp)
+        out = cpu.evaluate(plan, inp)
+    assert np.array_equal(np.isnan(out), np.isnan(ref))
+    ok = ~np.isnan(ref).any(axis=1)
+    if ok.any():
+        # C4 p = 5: cells the config's draw nearly inverts amplify rounding
+        tol = 1e-12 if cfg == "C4" and p == 5 else TOL
+        assert rel_err(out[ok], ref[ok]) < tol

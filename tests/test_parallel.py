@@ -103,3 +103,77 @@ def test_nccl_checksum_single_gpu():
                      {"coords": workloads.c5_inputs(0, 1, (2, 4, 4))["coords"]})
     assert nloc == 32
     assert abs(norm - math.sqrt(np.sum(A * A))) <= 1e-12 * norm
+
+
+def _gpu_worker(rank, world, port, degree, q):
+    """One rank of a 2-process run on ONE GPU: real kernels (sfk_eval through
+    sharded_matrix_checksum), gloo all-reduce of the checksum partials.  The
+    ranks never wait on each other's kernels (only the host all-reduce)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1711_02473_b200 import parallel
+
+        norm, total, nloc = parallel.sharded_matrix_checksum(degree, dims_per_rank=(2, 3, 2))
+        q.put((rank, norm, total, nloc))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("degree", [1, 3])
+def test_two_ranks_one_gpu_real_kernels_checksum(degree):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, degree, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1:3] == res[1][1:3]              # identical on every rank
+    full = workloads.lattice_coords(2 * world, 3, 2)
+    A = cpu.evaluate(compile_kernel("laplace", "hex", degree), {"coords": full})
+    s2 = float(np.sum(A * A))
+    assert abs(res[0][1] - math.sqrt(s2)) <= 1e-12 * math.sqrt(s2)
+    assert sum(r[3] for r in res) == full.shape[0]
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_shared_device():
+    """bench.py --gpus 2 relaunches itself under torch.distributed.run (one
+    process per rank) and reports the aggregate of both ranks.  On this 1-GPU
+    box both ranks share cuda:0 over gloo (--shared-device, test only)."""
+    import json
+    import subprocess
+    import sys
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                          "--backend", "gloo", "--shared-device", "--steps", "2", "--warmup", "1",
+                          "--degrees", "1-3", "--lattice", "8,8,8", "--c5-lattice", "2,4,4",
+                          "--no-cpu"], capture_output=True, text=True, timeout=900, cwd=root)
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = [json.loads(l) for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["config"]["cells_total"] == 2 * 512
+    assert d["e2e"]["matches_device_path"] and d["gpu_launches"] > 0
+    c5 = d["c5"]["per_degree"]
+    assert [r["p"] for r in c5] == [1, 2, 3, 4]
+    # checksum of the 2-rank lattice (4, 4, 4) equals the single-process one
+    full = workloads.lattice_coords(4, 4, 4)
+    for r in c5[:2]:
+        A = cpu.evaluate(compile_kernel("laplace", "hex", r["p"]), {"coords": full})
+        ref = math.sqrt(float(np.sum(A * A)))
+        assert abs(r["frobenius"] - ref) <= 1e-12 * ref
