@@ -67,6 +67,11 @@ def parse():
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 checksum leg")
     ap.add_argument("--c5-lattice", default="16,64,64", help="C5 cells per rank, nx,ny,nz")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl")
+    ap.add_argument("--flush", choices=["clean", "dirty"], default="clean",
+                    help="L2 flush between steps: 'dirty' = write 256 MiB (the L2 then "
+                         "holds dirty lines the first kernel must write back); 'clean' = "
+                         "that write followed by a 256 MiB read, so the L2 holds only "
+                         "clean unrelated lines (ncu's cache-control state)")
     ap.add_argument("--shared-device", action="store_true",
                     help="tests only: every rank on cuda:0 (gloo), to exercise the N>1 "
                          "host path on a 1-GPU box; never a scaling number")
@@ -185,6 +190,32 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+
+
+class L2Flush:
+    """Evict the 126 MB L2 between timed steps (outside the timed events).
+    'dirty': write a 256 MiB buffer.  'clean' (default): that write, then a
+    read of a second 256 MiB buffer, which writes the dirty lines back before
+    the step, so the first kernel of the step is not charged for another
+    buffer's write-back (the state ncu's cache control gives every kernel)."""
+
+    def __init__(self, dev, mode):
+        import torch
+        self.mode = mode
+        self.wr = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        if mode == "clean":
+            self.rd = torch.zeros(32 << 20, dtype=torch.float64, device=dev)
+            self.acc = torch.empty((), dtype=torch.float64, device=dev)
+
+    def __call__(self):
+        import torch
+        self.wr.zero_()
+        if self.mode == "clean":
+            torch.sum(self.rd, dtype=torch.float64, out=self.acc)
+
+    def describe(self):
+        return ("flushed between steps (256 MiB write + 256 MiB read: no dirty lines)"
+                if self.mode == "clean" else "flushed between steps (256 MiB write)")
 
 
 def dist_env():
@@ -427,7 +458,7 @@ def c5_leg(args, world, rank, dev, stream, flush, p64, hbm):
             dist.barrier()
         torch.cuda.synchronize()
         for e0, e1 in evs:
-            flush.zero_()
+            flush()
             torch.cuda._sleep(SPIN_CYCLES)
             e0.record(stream)
             launch()
@@ -525,7 +556,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
     lib = runtime.load_library()
     handles = {p: runtime.native_plan(plans[p]) for p in degs}
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    flush = L2Flush(dev, args.flush)
 
     # FP64 peak measured live on this GPU (DFMA chains and DMMA), seconds-long
     dfma, dmma = runtime.fp64_peak(1.0)
@@ -549,7 +580,7 @@ def main():
     l0 = runtime.launch_count()
     with ClockSampler(dev.index if world == 1 else local) as clk:
         for k in range(K):
-            flush.zero_()  # L2 flush between steps (outside the timed events)
+            flush()  # L2 flush between steps (outside the timed events)
             # ~1 ms spin on the stream before the step's first event, so the
             # host has enqueued every launch before the GPU reaches them: the
             # per-degree events then time the kernels, not the Python/ctypes
@@ -628,7 +659,7 @@ def main():
                        ("lattice_per_gpu" if args.scaling == "weak" else "lattice_total"):
                            [nx, ny, nz],
                        "parallelism": "cell-range shards x%d" % world,
-                       "l2": "flushed between steps (256 MiB write)",
+                       "l2": flush.describe(),
                        "launch": "1 ms GPU spin before each step (host launch latency hidden)"},
             "per_degree": per, "roofline": roofline, "gpu_launches": int(gpu_launches),
             "clocks": clk.summary()}
