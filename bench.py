@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 checksum leg")
     ap.add_argument("--c5-lattice", default="16,64,64", help="C5 cells per rank, nx,ny,nz")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl")
+    ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
+                    help="A/B runs only: libsfk tuning option (runtime.set_option), "
+                         "recorded in config.options")
     ap.add_argument("--flush", choices=["clean", "dirty"], default="clean",
                     help="L2 flush between steps: 'dirty' = write 256 MiB (the L2 then "
                          "holds dirty lines the first kernel must write back); 'clean' = "
@@ -211,7 +214,7 @@ class L2Flush:
         import torch
         self.wr.zero_()
         if self.mode == "clean":
-            torch.sum(self.rd, dtype=torch.float64, out=self.acc)
+            torch.sum(self.rd, dim=0, out=self.acc)
 
     def describe(self):
         return ("flushed between steps (256 MiB write + 256 MiB read: no dirty lines)"
@@ -550,6 +553,11 @@ def main():
                       workloads.uniform_dofs(total_cells, (p + 1) ** 3)[c0:c0 + ncells])
                   for p in degs}
     plans = {p: compile_kernel("action_laplace", "hex", p) for p in degs}
+    opts = {}
+    for kv in args.option:
+        k, v = kv.split("=", 1)
+        runtime.set_option(k, v if k == "c2_kernel" and not v.lstrip("-").isdigit() else int(v))
+        opts[k] = v
     coords = torch.from_numpy(coords_np).to(dev)
     u = {p: torch.from_numpy(host_u[p]).to(dev) for p in degs}
     out = {p: torch.empty_like(u[p]) for p in degs}
@@ -660,6 +668,7 @@ def main():
                            [nx, ny, nz],
                        "parallelism": "cell-range shards x%d" % world,
                        "l2": flush.describe(),
+                       **({"options": opts} if opts else {}),
                        "launch": "1 ms GPU spin before each step (host launch latency hidden)"},
             "per_degree": per, "roofline": roofline, "gpu_launches": int(gpu_launches),
             "clocks": clk.summary()}

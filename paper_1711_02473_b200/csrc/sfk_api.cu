@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -55,13 +56,14 @@ static int c2_auto(int n) {
     case 2: return 5;
     case 3: return 8;   // thread-per-cell over v4: 0.1245 -> 0.1115 ms (profiles/r01cq_*.jsonl)
     case 4: return 6;
-    case 5: return 3;
-    // v5 (grouped outputs) over v2: p = 5 1.043 -> 0.985, p = 6 1.685 -> 1.621,
-    // p = 8 3.639 -> 3.513 ms (profiles/r01bu_*.jsonl)
-    case 6: return 7;
-    case 7: return 7;
+    // v6 (collocation derivative, 12 n^4 instead of 16 n^4 FMA) over v3 / v5:
+    // p = 4 0.503 -> 0.441, p = 5 0.925 -> 0.813, p = 6 1.448 -> 1.247,
+    // p = 8 3.341 -> 2.791 ms (profiles/r02c_v6.json vs r02c_clean.json)
+    case 5: return 10;
+    case 6: return 10;
+    case 7: return 10;
     case 8: return 4;
-    case 9: return 7;
+    case 9: return 10;
     default: return 1;
   }
 }
@@ -71,6 +73,10 @@ static int launch_c2(const sfk_plan* p, int64_t ncells, double* A, const double*
   int v = c2_variant();
   if (v == 0) v = c2_auto(p->n);
   int rc = SFK_EUNSUPPORTED;
+  if (v == 10) {
+    rc = launch_hex_action_v6(p, ncells, A, coords, w0, s);
+    if (rc == SFK_EUNSUPPORTED) v = c2_auto(p->n);
+  }
   if (v == 8) {
     rc = launch_hex_action_cell(p, ncells, A, coords, w0, s);
     if (rc == SFK_EUNSUPPORTED) v = 3;
@@ -170,6 +176,70 @@ static HostCtx* host_ctx(int dev) {
 // collocated) reaches a kernel.  sfk_plan_create rejects every other
 // combination, so an unsupported request fails when the plan is built (the
 // reference raises at compile time, cli.py:155-208), never at eval.
+// Collocation derivative C = B^-1 D for square tables (n == m): D = B C
+// with B[i][q] (basis i, point q).  Gaussian elimination with partial
+// pivoting in long double plus one refinement step, then rounded to double,
+// so C is (almost always) the correctly rounded product of the reference's
+// own tables.  Returns false when B is singular.
+static bool collocation_derivative(int n, const double* B, const double* D, double* C) {
+  typedef long double R;
+  R a[SFK_MAXN][SFK_MAXN], x[SFK_MAXN][SFK_MAXN], rhs[SFK_MAXN][SFK_MAXN];
+  int piv[SFK_MAXN];
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) a[i][j] = B[i * n + j];
+  for (int i = 0; i < n; ++i) piv[i] = i;
+  // LU of B (rows i), B = P^T L U
+  for (int k = 0; k < n; ++k) {
+    int best = k;
+    for (int i = k + 1; i < n; ++i)
+      if (fabsl(a[i][k]) > fabsl(a[best][k])) best = i;
+    if (a[best][k] == 0) return false;
+    if (best != k) {
+      for (int j = 0; j < n; ++j) {
+        R t = a[k][j]; a[k][j] = a[best][j]; a[best][j] = t;
+      }
+      int t = piv[k]; piv[k] = piv[best]; piv[best] = t;
+    }
+    for (int i = k + 1; i < n; ++i) {
+      a[i][k] /= a[k][k];
+      for (int j = k + 1; j < n; ++j) a[i][j] -= a[i][k] * a[k][j];
+    }
+  }
+  auto solve = [&](R (*b)[SFK_MAXN], R (*out)[SFK_MAXN]) {
+    for (int col = 0; col < n; ++col) {
+      R y[SFK_MAXN];
+      for (int i = 0; i < n; ++i) {
+        R s = b[piv[i]][col];
+        for (int j = 0; j < i; ++j) s -= a[i][j] * y[j];
+        y[i] = s;
+      }
+      for (int i = n - 1; i >= 0; --i) {
+        R s = y[i];
+        for (int j = i + 1; j < n; ++j) s -= a[i][j] * out[j][col];
+        out[i][col] = s / a[i][i];
+      }
+    }
+  };
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) rhs[i][j] = D[i * n + j];
+  solve(rhs, x);
+  for (int it = 0; it < 2; ++it) {   // refinement: r = D - B x
+    R res[SFK_MAXN][SFK_MAXN], dx[SFK_MAXN][SFK_MAXN];
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        R s = D[i * n + j];
+        for (int k = 0; k < n; ++k) s -= (R)B[i * n + k] * x[k][j];
+        res[i][j] = s;
+      }
+    solve(res, dx);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) x[i][j] += dx[i][j];
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) C[i * n + j] = (double)x[i][j];
+  return true;
+}
+
 static bool kernel_available(int kind, int dim, int n, int m, int colloc) {
   const bool hex_line = (n == m && n >= 2 && n <= 10) || (m == n + 1 && n >= 2 && n <= 8);
   const bool quad = dim == 2 && !colloc && n == m && n >= 2 && n <= 9;
@@ -245,6 +315,7 @@ int sfk_plan_create(int kind, int cell_dim, int degree, int n, int m, int colloc
   memcpy(p->Bc, Bc, sizeof(double) * 2 * m);
   memcpy(p->Dc, Dc, sizeof(double) * 2 * m);
   if (nparams) memcpy(p->params, params, sizeof(double) * nparams);
+  p->has_ct = (n == m && n <= SFK_MAXN) ? collocation_derivative(n, B, D, p->Ct) : 0;
   const int64_t nd = cell_dim == 3 ? (int64_t)n * n * n : (int64_t)n * n;
   p->coords_size = cell_dim == 3 ? 24 : 8;
   p->w0_size = 0;

@@ -23,6 +23,10 @@ struct sfk_plan {
   double Bc[2 * SFK_MAXM];         // P1 values  Bc[v*m + q]
   double Dc[2 * SFK_MAXM];         // P1 derivatives (-1, +1)
   double params[8];
+  // collocation derivative C = B^-1 D (n == m only, has_ct): C[q'*m + q],
+  // solved at plan creation in extended precision (sfk_api.cu)
+  double Ct[SFK_MAXM * SFK_MAXM];
+  int has_ct;
   int64_t coords_size, w0_size, w1_size, a_size;
 };
 
@@ -124,6 +128,8 @@ int launch_hex_action_cell_gs(const sfk_plan* p, int64_t ncells, const int* cmap
 int launch_hex_action_cell(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                            const double* w0, cudaStream_t s);
 int launch_hex_action_v5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                         const double* w0, cudaStream_t s);
+int launch_hex_action_v6(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, cudaStream_t s);
 int launch_hex_action_v4(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, cudaStream_t s);

@@ -50,7 +50,7 @@ def main():
             for _ in range(K):
                 wr.zero_()
                 if mode == "clean":
-                    torch.sum(rd, dtype=torch.float64, out=acc)
+                    torch.sum(rd, dim=0, out=acc)
                 torch.cuda._sleep(2_000_000)
                 a, b = ev(), ev()
                 a.record(s)
@@ -62,7 +62,7 @@ def main():
             res["single_%s_ms" % mode] = round(sum(ts) / K, 5)
             res["single_%s_min_ms" % mode] = round(ts[0], 5)
         wr.zero_()
-        torch.sum(rd, dtype=torch.float64, out=acc)
+        torch.sum(rd, dim=0, out=acc)
         torch.cuda._sleep(2_000_000)
         a, b = ev(), ev()
         a.record(s)
