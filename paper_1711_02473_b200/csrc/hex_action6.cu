@@ -40,10 +40,13 @@
 namespace sfk {
 
 // Tables of v6: row length LD (even, so aligned pairs of consecutive
-// entries are one LDCU.128).  B[i][q], BT[q][i], C[q'][q], CT[q][q'].
+// entries are one LDCU.128), except n = 8: with 128-bit pairs there the
+// compiler hoisted the table set into uniform registers and spilled them
+// (168 registers, or spills at the 128 cap); LD = 9 keeps 64-bit loads.
+// B[i][q], BT[q][i], C[q'][q], CT[q][q'].
 template <int N>
 struct TabsV6 {
-  static constexpr int LD = (N + 1) & ~1;
+  static constexpr int LD = N == 8 ? 9 : (N + 1) & ~1;
   alignas(16) double B[N * LD];
   alignas(16) double BT[N * LD];
   alignas(16) double C[N * LD];
@@ -81,6 +84,11 @@ __device__ __forceinline__ void v6_contract(const double* T, const double* in, d
 #pragma unroll
     for (int o = 0; o < NO; ++o) out[o] = fma(T[i * LD + o], in[i], out[o]);
 }
+
+// Scheduling fence between the independent line tasks of one stage (D, F):
+// keeps the compiler from interleaving them, which at n = 8 (every lane
+// live, stores unpredicated) raised the kernel to 168 registers.
+__device__ __forceinline__ void v6_fence() { __syncwarp(); }
 
 // Strided view of one per-cell array: element (x, y, z) at
 // c*cs + x*sx + y*sy + z.
@@ -231,6 +239,7 @@ hex_laplace_action_v6(const __grid_constant__ TabsV6<N> T, int64_t ncells,
         for (int j = 0; j < N; ++j) g[j * XZ.sx] = o[j];
       }
     }
+    v6_fence();
     {
       double in[N], o[N];
       const double* v = S1 + c * YZ.cs + ra * YZ.sx + rb;           // lane (x, z)
@@ -283,6 +292,7 @@ hex_laplace_action_v6(const __grid_constant__ TabsV6<N> T, int64_t ncells,
         for (int j = 0; j < N; ++j) g[j * XZ.sx] = o[j];
       }
     }
+    v6_fence();
     {
       double in[N], o[N];
       double* g = S3 + c * YZ.cs + ra * YZ.sx + rb;
@@ -294,6 +304,7 @@ hex_laplace_action_v6(const __grid_constant__ TabsV6<N> T, int64_t ncells,
         for (int j = 0; j < N; ++j) g[j * YZ.sy] = o[j];
       }
     }
+    v6_fence();
     {
       double in[N], o[N];
       double* g = S4 + c * YZ.cs + ra * YZ.sy + rb * YZ.sx;       // z-line (y, x)
@@ -375,18 +386,30 @@ static int launch_v6(const sfk_plan* p, int64_t ncells, double* A, const double*
   return cuda_status(cudaGetLastError(), "hex_laplace_action_v6 launch");
 }
 
+// (cells per CTA, min CTAs per SM) per n: the default, then the
+// alternatives option v6_cfg = 1..3 selects (A/B runs).
 int launch_hex_action_v6(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, cudaStream_t s) {
   if (p->n != p->m || !p->has_ct) return SFK_EUNSUPPORTED;
+  const int alt = (int)option(OPT_V6_CFG);
+#define V6_CASE(n_, c0, m0, c1, m1, c2, m2, c3, m3)                         \
+  case n_:                                                                   \
+    switch (alt) {                                                           \
+      case 1: return launch_v6<n_, c1, m1>(p, ncells, A, coords, w0, s);    \
+      case 2: return launch_v6<n_, c2, m2>(p, ncells, A, coords, w0, s);    \
+      case 3: return launch_v6<n_, c3, m3>(p, ncells, A, coords, w0, s);    \
+      default: return launch_v6<n_, c0, m0>(p, ncells, A, coords, w0, s);   \
+    }
   switch (p->n) {
-    case 4: return launch_v6<4, 8, 2>(p, ncells, A, coords, w0, s);
-    case 5: return launch_v6<5, 5, 2>(p, ncells, A, coords, w0, s);
-    case 6: return launch_v6<6, 7, 2>(p, ncells, A, coords, w0, s);
-    case 7: return launch_v6<7, 5, 2>(p, ncells, A, coords, w0, s);
-    case 8: return launch_v6<8, 4, 1>(p, ncells, A, coords, w0, s);
-    case 9: return launch_v6<9, 3, 2>(p, ncells, A, coords, w0, s);
+    V6_CASE(4, 8, 2, 16, 2, 8, 3, 4, 4)
+    V6_CASE(5, 5, 2, 10, 2, 6, 2, 7, 2)
+    V6_CASE(6, 7, 2, 8, 2, 5, 3, 3, 3)
+    V6_CASE(7, 5, 2, 4, 3, 6, 2, 3, 4)
+    V6_CASE(8, 4, 2, 3, 2, 2, 3, 5, 1)
+    V6_CASE(9, 3, 2, 2, 3, 4, 1, 2, 2)
     default: return SFK_EUNSUPPORTED;
   }
+#undef V6_CASE
 }
 
 }  // namespace sfk

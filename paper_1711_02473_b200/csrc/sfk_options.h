@@ -37,6 +37,7 @@ enum Option : int {
   OPT_LP_WARP,       // LoopProgram warp mode: -1 = off
   OPT_LP_MINB,
   OPT_LP_FUSE,       // LoopProgram loop fusion: -1 = off
+  OPT_V6_CFG,        // v6 (cells per CTA, min CTAs per SM) alternative 1..3 per n
   OPT_COUNT
 };
 
