@@ -40,13 +40,11 @@ def layouts():
 
 
 def instances():
+    """(n, cells per CTA, ZR, WS) of every launch_v6<...> instance."""
     txt = open(os.path.join(CSRC, "hex_action6.cu")).read()
     res = []
-    for m in re.finditer(r"V6_CASE\((\d+), ([\d, ]+)\)", txt):
-        n = int(m.group(1))
-        v = [int(x) for x in m.group(2).split(",")]
-        for cpb in v[0::2]:
-            res.append((n, cpb))
+    for m in re.finditer(r"launch_v6<(\d+), (\d+), (\d+)(?:, (true|false))?(?:, (true|false))?>\(p", txt):
+        res.append((int(m.group(1)), int(m.group(2)), m.group(4) == "true", m.group(5) == "true"))
     return sorted(set(res))
 
 
@@ -54,21 +52,28 @@ LAY = layouts()
 INST = instances()
 
 
-def schedule(n, cpb, zr=False):
+def schedule(n, cpb, zr=False, ws=False):
     """[(stage, [(lane, slot, addr, 'r'|'w')])] of one batch."""
     lay = LAY[n]
     nn = n * n
-    th = (cpb * nn + 31) // 32 * 32
+    cpw = 32 // nn if ws else cpb
+    th = 32 * (cpb // cpw) if ws else (cpb * nn + 31) // 32 * 32
+
+    slot_cs = max(v[2] for v in lay.values())
 
     def at(role, c, x, y, z):
         sx, sy, cs = lay[role]
+        if ws:
+            cs = slot_cs  # WS: one cell stride for every role
         return c * cs + x * sx + y * sy + z
 
     stages = defaultdict(list)
     for t in range(th):
-        on = t < cpb * nn
-        lt = t if on else 0
-        c, r = divmod(lt, nn)
+        grp, gt = (t // 32, t % 32) if ws else (0, t)
+        on = gt < cpw * nn
+        lt = gt if on else 0
+        c = grp * cpw + lt // nn
+        r = lt % nn
         ra, rb = divmod(r, n)
 
         def acc(stage, slot, addr, kind, load_guarded=False):
@@ -110,15 +115,21 @@ def schedule(n, cpb, zr=False):
     return [(s, stages[s]) for s in "ABCDEFGHI"]
 
 
-@pytest.mark.parametrize("zr", [False, True])
-@pytest.mark.parametrize("n,cpb", INST)
-def test_v6_schedule_bounds_races_coverage(n, cpb, zr):
+@pytest.mark.parametrize("n,cpb,zr,ws", INST)
+def test_v6_schedule_bounds_races_coverage(n, cpb, zr, ws):
     lay = LAY[n]
     assert set(lay) == set(ROLES)
     slot = max(v[2] for v in lay.values())
     size = cpb * slot
-    writes_per_stage = {"A": "P1", "B": "Q", "C": "V", "D": None, "G": "R", "H": "P2"}
-    for stage, accs in schedule(n, cpb, zr):
+    sched = schedule(n, cpb, zr, ws)
+    if ws:
+        # warp-synchronous: no CTA barrier at all, so no address may be
+        # touched by two warps in any stage
+        warp_of = {}
+        for stage, accs in sched:
+            for lane, sl, addr, kind in accs:
+                assert warp_of.setdefault((sl, addr), lane // 32) == lane // 32, (stage, sl, addr)
+    for stage, accs in sched:
         owner = {}
         readers = defaultdict(set)
         for lane, sl, addr, kind in accs:
@@ -148,5 +159,6 @@ def test_v6_schedule_bounds_races_coverage(n, cpb, zr):
 
 
 def test_v6_instances_cover_every_degree_dispatched():
-    ns = {n for n, _ in INST}
-    assert {4, 5, 6, 7, 8, 9} <= ns
+    ns = {i[0] for i in INST}
+    assert {3, 4, 5, 6, 7, 8, 9} <= ns
+    assert any(i[3] for i in INST) and any(i[2] for i in INST)   # WS and ZR instances modelled
