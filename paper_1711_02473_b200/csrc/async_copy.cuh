@@ -50,6 +50,7 @@ __device__ __forceinline__ int dst_shift(const void* src) {
 template <int THREADS>
 __device__ __forceinline__ void async_copy_phase(double* dst, const double* src, int n, int tid) {
   // dst and src share the 16-byte phase: one leading 8-byte copy if needed
+  if (n <= 0) return;   // (n = 0 with lead = 1 would copy src[-1])
   const int lead = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
   if (lead && tid == 0 && n > 0) cp_async8(dst, src);
   const int m = n - lead;
