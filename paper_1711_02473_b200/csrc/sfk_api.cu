@@ -55,7 +55,7 @@ static int c2_auto(int n) {
   switch (n) {
     case 2: return 5;
     case 3: return 8;   // thread-per-cell over v4: 0.1245 -> 0.1115 ms (profiles/r01cq_*.jsonl)
-    case 4: return 6;
+    case 4: return 10;  // v6 warp-synchronous over v4: 0.2088 -> 0.2034 ms (profiles/r02h_cfg3.json)
     // v6 (collocation derivative, 12 n^4 instead of 16 n^4 FMA) over v3 / v5:
     // p = 4 0.503 -> 0.441, p = 5 0.925 -> 0.813, p = 6 1.448 -> 1.247,
     // p = 8 3.341 -> 2.791 ms (profiles/r02c_v6.json vs r02c_clean.json)
