@@ -109,8 +109,6 @@ int launch_hex_action_v3(const sfk_plan* p, int64_t ncells, double* A,
                          const double* coords, const double* w0, cudaStream_t s);
 int launch_hex_action_tc(const sfk_plan* p, int64_t ncells, double* A,
                          const double* coords, const double* w0, cudaStream_t s);
-int launch_hex_action_p1c(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                          const double* w0, cudaStream_t s);
 int launch_hex_action_p1(const sfk_plan* p, int64_t ncells, double* A,
                          const double* coords, const double* w0, cudaStream_t s);
 int launch_hex_action_p1_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
