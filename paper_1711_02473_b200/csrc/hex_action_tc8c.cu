@@ -1,0 +1,459 @@
+// Hex Q_7 Laplace action on the FP64 tensor cores with the collocation-
+// derivative schedule — BASELINE C2 at p = 7 (n = m = 8).
+//
+// The operator and reference mapping of every C2 kernel (forms.py:186-189,
+// 235-243; passes.py:672-743).  Schedule of v6 (hex_action6.cu: C = B^-1 D,
+// 12 n^4 FMA per cell instead of 16 n^4), stages as batched 8x8x8 GEMMs on
+// mma.sync.m8n8k4.f64 (SASS DMMA) as in tc8 (hex_action_tc.cu): 192 DMMA
+// per cell instead of tc8's 256.  Fragment forms (lane = 4*gq + kq):
+//  * D-form (contraction along x or y; the 8 lines of a tile are the MMA n
+//    index): table fragment A[q][k] constant per lane, in[k][line] loaded as
+//    64-bit at (k = kq + 4ks, line = gq), outputs D[q = gq][line = 2kq, 2kq+1]
+//    stored as one 128-bit word;
+//  * D'-form (contraction along z; lines = MMA m index): in[line = gq][k =
+//    2kq + ks] is one 128-bit load, the output D[line = gq][q = 2kq, 2kq+1]
+//    has exactly that layout, so z stages CHAIN in registers: V = Q B_z feeds
+//    gz = V C_z without a store, and G forms t = (tx + ty) + fz C_z^T with
+//    the (tx + ty) sum as the accumulator input, then R = t B_z^T.
+//   A  x   D-form   u  -> P  = B_x u                 sU -> S1
+//   B  y   D-form   P  -> Q  = B_y P                 S1 -> S2
+//   C  z   D'-form  Q  -> V  = B_z Q -> gz = C_z V   S2 -> S1 (V), S4 (gz)
+//   D  x,y D-form   V  -> gx = C_x V, gy = C_y V     S1 -> S2, S3
+//   E  z-lines      geometry + flux in place         S2, S3, S4
+//   F  x,y D-form   tx = C_x^T fx, ty = C_y^T fy     in place S2, S3
+//   G  z   D'-form  t = tx + ty + fz C_z^T -> R = t B_z^T        -> S1
+//   H  y   D-form   S = B_y^T R                      S1 -> S2
+//   I  x   D-form   A = B_x^T S                      S2 -> HBM
+// Shared layouts are strided + XOR-swizzled per array so that every access
+// above is bank-conflict free (tools/tc8c_layout.py searched them under the
+// half-/quarter-warp bank model).
+#include "async_copy.cuh"
+#include "hex_geometry.cuh"
+
+namespace sfk {
+
+__device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+struct TabsTC8C {
+  double B[64];   // B[i*8 + q]
+  double C[64];   // C[q'*8 + q]
+  double W[8];
+  double Bc[16];
+};
+
+namespace tc8c {
+constexpr int N = 8, NN = 64, N3 = 512;
+constexpr int CPB = 4;                   // cells per CTA
+constexpr int THREADS = CPB * NN;        // 256: one thread per z-line in stage E
+constexpr int WARPS = THREADS / 32;
+constexpr int TILES = CPB * 8;           // 8-line tiles per stage
+constexpr int TPW = TILES / WARPS;       // tiles per warp and tile set
+constexpr int SLOT = 576;                // doubles per cell and slot (largest layout)
+constexpr int UC = 8 * 68;               // u per cell, ix-plane stride 68
+constexpr int CSZ = CPB * 24;
+constexpr size_t SMEM = (size_t)(4 * CPB * SLOT + CPB * UC + 2 * CSZ) * sizeof(double);
+
+__device__ __forceinline__ int b1(int v) { return ((v >> 1) & 1) << 2; }
+// element (a, b, c) = (x, y, z) of one cell's array (tools/tc8c_layout.py)
+__device__ __forceinline__ int aP(int a, int b, int c) { return a * 72 + b * 8 + (c ^ b1(b)); }
+__device__ __forceinline__ int aQR(int a, int b, int c) { return a * 64 + b * 8 + (c ^ b1(b)); }
+__device__ __forceinline__ int aV(int a, int b, int c) { return a * 68 + b * 8 + (c ^ b1(b)); }
+__device__ __forceinline__ int aGX(int a, int b, int c) {
+  return a * 72 + b * 8 + (c ^ ((((a >> 2) & 1) << 1) | b1(a)));
+}
+__device__ __forceinline__ int aGY(int a, int b, int c) { return a * 66 + b * 8 + (c ^ b1(b)); }
+__device__ __forceinline__ int aGZ(int a, int b, int c) { return a * 66 + b * 8 + c; }
+__device__ __forceinline__ int aS(int a, int b, int c) { return a * 68 + b * 8 + c; }
+__device__ __forceinline__ int aU(int a, int b, int c) { return a * 68 + b * 8 + c; }
+}  // namespace tc8c
+
+__global__ void __launch_bounds__(tc8c::THREADS, 2)
+hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
+                        const double* __restrict__ coords, const double* __restrict__ u,
+                        double* __restrict__ A) {
+  using namespace tc8c;
+  extern __shared__ __align__(16) double smem[];
+  double* S1 = smem;
+  double* S2 = S1 + CPB * SLOT;
+  double* S3 = S2 + CPB * SLOT;
+  double* S4 = S3 + CPB * SLOT;
+  double* sU = S4 + CPB * SLOT;
+  double* sCo = sU + CPB * UC;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kq = lane & 3, gq = lane >> 2;
+  const int64_t nbatch = (ncells + CPB - 1) / CPB;
+
+  // table fragments (constant per lane)
+  //  D-form fwd A[m=q][k=i] = T[i][q]: *f;  D-form bwd A[m=i][k=q] = T[i][q]: *b
+  //  D'-form fwd B[k=i][n=q] = T[i][q] (k = 2kq+ks): z*f; bwd B[k=q][n=i] = T[i][q]: z*b
+  double bf[2], bb[2], cf[2], cb[2], zbf[2], zbb[2], zcf[2], zcb[2];
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks) {
+    bf[ks] = T.B[(4 * ks + kq) * N + gq];
+    bb[ks] = T.B[gq * N + 4 * ks + kq];
+    cf[ks] = T.C[(4 * ks + kq) * N + gq];
+    cb[ks] = T.C[gq * N + 4 * ks + kq];
+    zbf[ks] = T.B[(2 * kq + ks) * N + gq];
+    zbb[ks] = T.B[gq * N + 2 * kq + ks];
+    zcf[ks] = T.C[(2 * kq + ks) * N + gq];
+    zcb[ks] = T.C[gq * N + 2 * kq + ks];
+  }
+
+  auto prefetch = [&](int64_t bt, int buf) {
+    const int64_t c0 = bt * CPB;
+    const int nc = (int)((ncells - c0) < CPB ? (ncells - c0) : CPB);
+    const double* src = u + c0 * N3;
+    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+      for (int ch = tid; ch < nc * (N3 / 2); ch += THREADS) {
+        const int c = ch >> 8, r = ch & 255;
+        cp_async16(sU + c * UC + (r >> 5) * 68 + 2 * (r & 31), src + 2 * ch);
+      }
+    } else {
+      for (int e = tid; e < nc * N3; e += THREADS) {
+        const int c = e >> 9, r = e & 511;
+        cp_async8(sU + c * UC + (r >> 6) * 68 + (r & 63), src + e);
+      }
+    }
+    async_copy<THREADS>(sCo + buf * CSZ, coords + c0 * 24, nc * 24, tid);
+    cp_async_commit();
+  };
+
+  int64_t b = blockIdx.x;
+  if (b < nbatch) prefetch(b, 0);
+  for (int it = 0; b < nbatch; b += gridDim.x, ++it) {
+    const int cur = it & 1;
+    const int64_t cell0 = b * CPB;
+    const int ncb = (int)((ncells - cell0) < CPB ? (ncells - cell0) : CPB);
+    cp_async_wait<0>();
+    __syncthreads();
+
+    // ---- A: x, D-form; tile (c, iy), lines iz: P = B_x u ------------------
+    {
+      double f[TPW][2], o[TPW][2];
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, iy = t & 7;
+        const double* in = sU + c * UC;
+        f[j][0] = in[aU(kq, iy, gq)];
+        f[j][1] = in[aU(4 + kq, iy, gq)];
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        o[j][0] = o[j][1] = 0.0;
+        dmma8(o[j][0], o[j][1], bf[0], f[j][0]);
+        dmma8(o[j][0], o[j][1], bf[1], f[j][1]);
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, iy = t & 7;
+        *reinterpret_cast<double2*>(S1 + c * SLOT + aP(gq, iy, 2 * kq)) = make_double2(o[j][0], o[j][1]);
+      }
+    }
+    __syncthreads();
+    if (b + gridDim.x < nbatch) prefetch(b + gridDim.x, cur ^ 1);
+
+    // ---- B: y, D-form; tile (c, qx), lines iz: Q = B_y P -------------------
+    {
+      double f[TPW][2], o[TPW][2];
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        const double* p = S1 + c * SLOT;
+        f[j][0] = p[aP(qx, kq, gq)];
+        f[j][1] = p[aP(qx, 4 + kq, gq)];
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        o[j][0] = o[j][1] = 0.0;
+        dmma8(o[j][0], o[j][1], bf[0], f[j][0]);
+        dmma8(o[j][0], o[j][1], bf[1], f[j][1]);
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        *reinterpret_cast<double2*>(S2 + c * SLOT + aQR(qx, gq, 2 * kq)) = make_double2(o[j][0], o[j][1]);
+      }
+    }
+    __syncthreads();
+
+    // ---- C: z, D'-form; tile (c, qx), lines qy: V = Q B_z, gz = V C_z -----
+    {
+      double2 f[TPW];
+      double v[TPW][2], g[TPW][2];
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        f[j] = *reinterpret_cast<const double2*>(S2 + c * SLOT + aQR(qx, gq, 2 * kq));
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        v[j][0] = v[j][1] = 0.0;
+        dmma8(v[j][0], v[j][1], f[j].x, zbf[0]);
+        dmma8(v[j][0], v[j][1], f[j].y, zbf[1]);
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        g[j][0] = g[j][1] = 0.0;
+        dmma8(g[j][0], g[j][1], v[j][0], zcf[0]);
+        dmma8(g[j][0], g[j][1], v[j][1], zcf[1]);
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        *reinterpret_cast<double2*>(S1 + c * SLOT + aV(qx, gq, 2 * kq)) = make_double2(v[j][0], v[j][1]);
+        *reinterpret_cast<double2*>(S4 + c * SLOT + aGZ(qx, gq, 2 * kq)) = make_double2(g[j][0], g[j][1]);
+      }
+    }
+    __syncthreads();
+
+    // ---- D: gx = C_x V (tile (c, qy), lines qz), gy = C_y V (tile (c, qx)) -
+    {
+      double f[TPW][2], o[TPW][2];
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qy = t & 7;
+        const double* v = S1 + c * SLOT;
+        f[j][0] = v[aV(kq, qy, gq)];
+        f[j][1] = v[aV(4 + kq, qy, gq)];
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        o[j][0] = o[j][1] = 0.0;
+        dmma8(o[j][0], o[j][1], cf[0], f[j][0]);
+        dmma8(o[j][0], o[j][1], cf[1], f[j][1]);
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qy = t & 7;
+        *reinterpret_cast<double2*>(S2 + c * SLOT + aGX(gq, qy, 2 * kq)) = make_double2(o[j][0], o[j][1]);
+      }
+    }
+    {
+      double f[TPW][2], o[TPW][2];
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        const double* v = S1 + c * SLOT;
+        f[j][0] = v[aV(qx, kq, gq)];
+        f[j][1] = v[aV(qx, 4 + kq, gq)];
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        o[j][0] = o[j][1] = 0.0;
+        dmma8(o[j][0], o[j][1], cf[0], f[j][0]);
+        dmma8(o[j][0], o[j][1], cf[1], f[j][1]);
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        *reinterpret_cast<double2*>(S3 + c * SLOT + aGY(qx, gq, 2 * kq)) = make_double2(o[j][0], o[j][1]);
+      }
+    }
+    __syncthreads();
+
+    // ---- E: z-line (c, qx, qy): geometry + flux, two points per step -------
+    {
+      const int c = tid >> 6, r = tid & 63;
+      const int qx = r & 7, qy = r >> 3;
+      double* gxc = S2 + c * SLOT;
+      double* gyc = S3 + c * SLOT;
+      double* gzc = S4 + c * SLOT;
+      HexLineGeom geo;
+      geo.setup(sCo + cur * CSZ + c * 24, T.Bc[qx], T.Bc[N + qx], T.Bc[qy], T.Bc[N + qy]);
+      const double wxy = T.W[qx] * T.W[qy];
+#pragma unroll 1
+      for (int q = 0; q < N; q += 2) {
+        double2* px = reinterpret_cast<double2*>(gxc + aGX(qx, qy, q));
+        double2* py = reinterpret_cast<double2*>(gyc + aGY(qx, qy, q));
+        double2* pz = reinterpret_cast<double2*>(gzc + aGZ(qx, qy, q));
+        double2 gx = *px, gy = *py, gz = *pz;
+        {
+          double r0[3], r1[3], r2[3];
+          const double det = geo.adj(T.Bc[q], T.Bc[N + q], r0, r1, r2);
+          const double s = (wxy * T.W[q]) * rcp64(fabs(det));
+          laplace_flux(r0, r1, r2, s, gx.x, gy.x, gz.x);
+        }
+        {
+          double r0[3], r1[3], r2[3];
+          const double det = geo.adj(T.Bc[q + 1], T.Bc[N + q + 1], r0, r1, r2);
+          const double s = (wxy * T.W[q + 1]) * rcp64(fabs(det));
+          laplace_flux(r0, r1, r2, s, gx.y, gy.y, gz.y);
+        }
+        *px = gx;
+        *py = gy;
+        *pz = gz;
+      }
+    }
+    __syncthreads();
+
+    // ---- F: tx = C_x^T fx (tile (c, qy)), ty = C_y^T fy (tile (c, qx)), in
+    //      place: every warp loads its tiles, then stores them ---------------
+    {
+      double f[TPW][2], o[TPW][2];
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qy = t & 7;
+        const double* g = S2 + c * SLOT;
+        f[j][0] = g[aGX(kq, qy, gq)];
+        f[j][1] = g[aGX(4 + kq, qy, gq)];
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        o[j][0] = o[j][1] = 0.0;
+        dmma8(o[j][0], o[j][1], cb[0], f[j][0]);
+        dmma8(o[j][0], o[j][1], cb[1], f[j][1]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qy = t & 7;
+        *reinterpret_cast<double2*>(S2 + c * SLOT + aGX(gq, qy, 2 * kq)) = make_double2(o[j][0], o[j][1]);
+      }
+    }
+    {
+      double f[TPW][2], o[TPW][2];
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        const double* g = S3 + c * SLOT;
+        f[j][0] = g[aGY(qx, kq, gq)];
+        f[j][1] = g[aGY(qx, 4 + kq, gq)];
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        o[j][0] = o[j][1] = 0.0;
+        dmma8(o[j][0], o[j][1], cb[0], f[j][0]);
+        dmma8(o[j][0], o[j][1], cb[1], f[j][1]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        *reinterpret_cast<double2*>(S3 + c * SLOT + aGY(qx, gq, 2 * kq)) = make_double2(o[j][0], o[j][1]);
+      }
+    }
+    __syncthreads();
+
+    // ---- G: z, D'-form; tile (c, qx), lines qy:
+    //      t = (tx + ty) + fz C_z^T, R = t B_z^T ------------------------------
+    {
+      double2 fz[TPW];
+      double tt[TPW][2], rr[TPW][2];
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        const double2 tx = *reinterpret_cast<const double2*>(S2 + c * SLOT + aGX(qx, gq, 2 * kq));
+        const double2 ty = *reinterpret_cast<const double2*>(S3 + c * SLOT + aGY(qx, gq, 2 * kq));
+        fz[j] = *reinterpret_cast<const double2*>(S4 + c * SLOT + aGZ(qx, gq, 2 * kq));
+        tt[j][0] = tx.x + ty.x;
+        tt[j][1] = tx.y + ty.y;
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        dmma8(tt[j][0], tt[j][1], fz[j].x, zcb[0]);
+        dmma8(tt[j][0], tt[j][1], fz[j].y, zcb[1]);
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        rr[j][0] = rr[j][1] = 0.0;
+        dmma8(rr[j][0], rr[j][1], tt[j][0], zbb[0]);
+        dmma8(rr[j][0], rr[j][1], tt[j][1], zbb[1]);
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        *reinterpret_cast<double2*>(S1 + c * SLOT + aQR(qx, gq, 2 * kq)) = make_double2(rr[j][0], rr[j][1]);
+      }
+    }
+    __syncthreads();
+
+    // ---- H: y, D-form bwd; tile (c, qx), lines iz: S = B_y^T R -------------
+    {
+      double f[TPW][2], o[TPW][2];
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        const double* rp = S1 + c * SLOT;
+        f[j][0] = rp[aQR(qx, kq, gq)];
+        f[j][1] = rp[aQR(qx, 4 + kq, gq)];
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        o[j][0] = o[j][1] = 0.0;
+        dmma8(o[j][0], o[j][1], bb[0], f[j][0]);
+        dmma8(o[j][0], o[j][1], bb[1], f[j][1]);
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        *reinterpret_cast<double2*>(S2 + c * SLOT + aS(qx, gq, 2 * kq)) = make_double2(o[j][0], o[j][1]);
+      }
+    }
+    __syncthreads();
+
+    // ---- I: x, D-form bwd; tile (c, iy), lines iz: A = B_x^T S -------------
+    {
+      double f[TPW][2], o[TPW][2];
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, iy = t & 7;
+        const double* sp = S2 + c * SLOT;
+        f[j][0] = sp[aS(kq, iy, gq)];
+        f[j][1] = sp[aS(4 + kq, iy, gq)];
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        o[j][0] = o[j][1] = 0.0;
+        dmma8(o[j][0], o[j][1], bb[0], f[j][0]);
+        dmma8(o[j][0], o[j][1], bb[1], f[j][1]);
+      }
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int t = warp + WARPS * j, c = t >> 3, iy = t & 7;
+        if (c < ncb) {
+          // D: ix = gq, iz = 2kq + h -> A[cell][ix*64 + iy*8 + iz]
+          double* ap = A + (cell0 + c) * N3 + gq * NN + iy * 8 + 2 * kq;
+          if ((reinterpret_cast<uintptr_t>(ap) & 15) == 0) {
+            *reinterpret_cast<double2*>(ap) = make_double2(o[j][0], o[j][1]);
+          } else {
+            ap[0] = o[j][0];
+            ap[1] = o[j][1];
+          }
+        }
+      }
+    }
+    // the next batch's stage A writes S1 only after the barrier at the top
+  }
+}
+
+int launch_hex_action_tc8c(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                           const double* w0, cudaStream_t s) {
+  if (p->n != 8 || p->m != 8 || !p->has_ct) return SFK_EUNSUPPORTED;
+  using namespace tc8c;
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)hex_laplace_action_tc8c, THREADS, SMEM,
+                                   "hex_action_tc8c", &sh, true))
+    return rc_;
+  TabsTC8C T;
+  for (int i = 0; i < 64; ++i) {
+    T.B[i] = p->B[i];
+    T.C[i] = p->Ct[i];
+  }
+  for (int q = 0; q < 8; ++q) {
+    T.W[q] = p->wq[q];
+    T.Bc[q] = p->Bc[q];
+    T.Bc[8 + q] = p->Bc[8 + q];
+  }
+  const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  const int64_t resident = sh.resident();
+  const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
+  hex_laplace_action_tc8c<<<grid, THREADS, SMEM, s>>>(T, ncells, coords, w0, A);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "hex_laplace_action_tc8c launch");
+}
+
+}  // namespace sfk
