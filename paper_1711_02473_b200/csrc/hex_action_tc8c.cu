@@ -33,7 +33,9 @@
 namespace sfk {
 
 __device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  // not volatile: a pure function of its operands, so the compiler may
+  // interleave independent tiles' MMAs with loads
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
@@ -45,13 +47,17 @@ struct TabsTC8C {
   double Bc[16];
 };
 
+// One warp per cell: the warp runs all 8 tiles of every stage of its cell
+// and two z-lines per lane in stage E, so every exchange is a __syncwarp and
+// the CTA never synchronises (the first, CTA-wide version — 4 tiles of mixed
+// cells per warp, 9 CTA barriers per batch — measured 2.46 ms, barrier and
+// shared-load latency bound).
 namespace tc8c {
 constexpr int N = 8, NN = 64, N3 = 512;
-constexpr int CPB = 4;                   // cells per CTA
-constexpr int THREADS = CPB * NN;        // 256: one thread per z-line in stage E
-constexpr int WARPS = THREADS / 32;
-constexpr int TILES = CPB * 8;           // 8-line tiles per stage
-constexpr int TPW = TILES / WARPS;       // tiles per warp and tile set
+constexpr int WARPS = 4;
+constexpr int CPB = WARPS;               // cells per CTA (one per warp)
+constexpr int THREADS = 32 * WARPS;
+constexpr int TPW = 8;                   // tiles per warp and stage
 constexpr int SLOT = 576;                // doubles per cell and slot (largest layout)
 constexpr int UC = 8 * 68;               // u per cell, ix-plane stride 68
 constexpr int CSZ = CPB * 24;
@@ -103,22 +109,23 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
     zcb[ks] = T.C[gq * N + 2 * kq + ks];
   }
 
+  // each warp stages its own cell: u (ix-planes at stride 68) and coords
   auto prefetch = [&](int64_t bt, int buf) {
-    const int64_t c0 = bt * CPB;
-    const int nc = (int)((ncells - c0) < CPB ? (ncells - c0) : CPB);
-    const double* src = u + c0 * N3;
-    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-      for (int ch = tid; ch < nc * (N3 / 2); ch += THREADS) {
-        const int c = ch >> 8, r = ch & 255;
-        cp_async16(sU + c * UC + (r >> 5) * 68 + 2 * (r & 31), src + 2 * ch);
+    const int64_t cg = bt * CPB + warp;
+    if (cg < ncells) {
+      const double* src = u + cg * N3;
+      double* du = sU + warp * UC;
+      if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int r = lane + 32 * k;   // 16-byte chunk of the cell
+          cp_async16(du + (r >> 5) * 68 + 2 * (r & 31), src + 2 * r);
+        }
+      } else {
+        for (int e = lane; e < N3; e += 32) cp_async8(du + (e >> 6) * 68 + (e & 63), src + e);
       }
-    } else {
-      for (int e = tid; e < nc * N3; e += THREADS) {
-        const int c = e >> 9, r = e & 511;
-        cp_async8(sU + c * UC + (r >> 6) * 68 + (r & 63), src + e);
-      }
+      if (lane < 24) cp_async8(sCo + buf * CSZ + warp * 24 + lane, coords + cg * 24 + lane);
     }
-    async_copy<THREADS>(sCo + buf * CSZ, coords + c0 * 24, nc * 24, tid);
     cp_async_commit();
   };
 
@@ -129,14 +136,15 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
     const int64_t cell0 = b * CPB;
     const int ncb = (int)((ncells - cell0) < CPB ? (ncells - cell0) : CPB);
     cp_async_wait<0>();
-    __syncthreads();
+    __syncwarp();
+    const int c = warp;
 
     // ---- A: x, D-form; tile (c, iy), lines iz: P = B_x u ------------------
     {
       double f[TPW][2], o[TPW][2];
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, iy = t & 7;
+        const int t = j, iy = t & 7;
         const double* in = sU + c * UC;
         f[j][0] = in[aU(kq, iy, gq)];
         f[j][1] = in[aU(4 + kq, iy, gq)];
@@ -149,11 +157,11 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       }
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, iy = t & 7;
+        const int t = j, iy = t & 7;
         *reinterpret_cast<double2*>(S1 + c * SLOT + aP(gq, iy, 2 * kq)) = make_double2(o[j][0], o[j][1]);
       }
     }
-    __syncthreads();
+    __syncwarp();
     if (b + gridDim.x < nbatch) prefetch(b + gridDim.x, cur ^ 1);
 
     // ---- B: y, D-form; tile (c, qx), lines iz: Q = B_y P -------------------
@@ -161,7 +169,7 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       double f[TPW][2], o[TPW][2];
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        const int t = j, qx = t & 7;
         const double* p = S1 + c * SLOT;
         f[j][0] = p[aP(qx, kq, gq)];
         f[j][1] = p[aP(qx, 4 + kq, gq)];
@@ -174,11 +182,11 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       }
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        const int t = j, qx = t & 7;
         *reinterpret_cast<double2*>(S2 + c * SLOT + aQR(qx, gq, 2 * kq)) = make_double2(o[j][0], o[j][1]);
       }
     }
-    __syncthreads();
+    __syncwarp();
 
     // ---- C: z, D'-form; tile (c, qx), lines qy: V = Q B_z, gz = V C_z -----
     {
@@ -186,7 +194,7 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       double v[TPW][2], g[TPW][2];
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        const int t = j, qx = t & 7;
         f[j] = *reinterpret_cast<const double2*>(S2 + c * SLOT + aQR(qx, gq, 2 * kq));
       }
 #pragma unroll
@@ -203,61 +211,51 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       }
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        const int t = j, qx = t & 7;
         *reinterpret_cast<double2*>(S1 + c * SLOT + aV(qx, gq, 2 * kq)) = make_double2(v[j][0], v[j][1]);
         *reinterpret_cast<double2*>(S4 + c * SLOT + aGZ(qx, gq, 2 * kq)) = make_double2(g[j][0], g[j][1]);
       }
     }
-    __syncthreads();
+    __syncwarp();
 
     // ---- D: gx = C_x V (tile (c, qy), lines qz), gy = C_y V (tile (c, qx)) -
+    //      both tile sets' loads first, then their MMAs (2 TPW chains)
     {
-      double f[TPW][2], o[TPW][2];
+      double f[2][TPW][2], o[2][TPW][2];
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qy = t & 7;
+        const int t = j, tt = t & 7;
         const double* v = S1 + c * SLOT;
-        f[j][0] = v[aV(kq, qy, gq)];
-        f[j][1] = v[aV(4 + kq, qy, gq)];
+        f[0][j][0] = v[aV(kq, tt, gq)];
+        f[0][j][1] = v[aV(4 + kq, tt, gq)];
+        f[1][j][0] = v[aV(tt, kq, gq)];
+        f[1][j][1] = v[aV(tt, 4 + kq, gq)];
       }
 #pragma unroll
-      for (int j = 0; j < TPW; ++j) {
-        o[j][0] = o[j][1] = 0.0;
-        dmma8(o[j][0], o[j][1], cf[0], f[j][0]);
-        dmma8(o[j][0], o[j][1], cf[1], f[j][1]);
-      }
+      for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+        for (int j = 0; j < TPW; ++j) {
+          o[s2][j][0] = o[s2][j][1] = 0.0;
+          dmma8(o[s2][j][0], o[s2][j][1], cf[0], f[s2][j][0]);
+        }
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+        for (int j = 0; j < TPW; ++j) dmma8(o[s2][j][0], o[s2][j][1], cf[1], f[s2][j][1]);
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qy = t & 7;
-        *reinterpret_cast<double2*>(S2 + c * SLOT + aGX(gq, qy, 2 * kq)) = make_double2(o[j][0], o[j][1]);
+        const int t = j, tt = t & 7;
+        *reinterpret_cast<double2*>(S2 + c * SLOT + aGX(gq, tt, 2 * kq)) = make_double2(o[0][j][0], o[0][j][1]);
+        *reinterpret_cast<double2*>(S3 + c * SLOT + aGY(tt, gq, 2 * kq)) = make_double2(o[1][j][0], o[1][j][1]);
       }
     }
-    {
-      double f[TPW][2], o[TPW][2];
-#pragma unroll
-      for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
-        const double* v = S1 + c * SLOT;
-        f[j][0] = v[aV(qx, kq, gq)];
-        f[j][1] = v[aV(qx, 4 + kq, gq)];
-      }
-#pragma unroll
-      for (int j = 0; j < TPW; ++j) {
-        o[j][0] = o[j][1] = 0.0;
-        dmma8(o[j][0], o[j][1], cf[0], f[j][0]);
-        dmma8(o[j][0], o[j][1], cf[1], f[j][1]);
-      }
-#pragma unroll
-      for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
-        *reinterpret_cast<double2*>(S3 + c * SLOT + aGY(qx, gq, 2 * kq)) = make_double2(o[j][0], o[j][1]);
-      }
-    }
-    __syncthreads();
+    __syncwarp();
 
-    // ---- E: z-line (c, qx, qy): geometry + flux, two points per step -------
-    {
-      const int c = tid >> 6, r = tid & 63;
+    // ---- E: z-lines (qx, qy) = (r & 7, r >> 3), r = lane and lane + 32:
+    //      geometry + flux, two points per step ----------------------------
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int r = lane + 32 * h;
       const int qx = r & 7, qy = r >> 3;
       double* gxc = S2 + c * SLOT;
       double* gyc = S3 + c * SLOT;
@@ -288,55 +286,42 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
         *pz = gz;
       }
     }
-    __syncthreads();
+    __syncwarp();
 
     // ---- F: tx = C_x^T fx (tile (c, qy)), ty = C_y^T fy (tile (c, qx)), in
-    //      place: every warp loads its tiles, then stores them ---------------
+    //      place: every warp loads its tiles of both sets, then stores them ---
     {
-      double f[TPW][2], o[TPW][2];
+      double f[2][TPW][2], o[2][TPW][2];
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qy = t & 7;
-        const double* g = S2 + c * SLOT;
-        f[j][0] = g[aGX(kq, qy, gq)];
-        f[j][1] = g[aGX(4 + kq, qy, gq)];
+        const int t = j, tt = t & 7;
+        const double* gx = S2 + c * SLOT;
+        const double* gy = S3 + c * SLOT;
+        f[0][j][0] = gx[aGX(kq, tt, gq)];
+        f[0][j][1] = gx[aGX(4 + kq, tt, gq)];
+        f[1][j][0] = gy[aGY(tt, kq, gq)];
+        f[1][j][1] = gy[aGY(tt, 4 + kq, gq)];
       }
 #pragma unroll
-      for (int j = 0; j < TPW; ++j) {
-        o[j][0] = o[j][1] = 0.0;
-        dmma8(o[j][0], o[j][1], cb[0], f[j][0]);
-        dmma8(o[j][0], o[j][1], cb[1], f[j][1]);
-      }
+      for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+        for (int j = 0; j < TPW; ++j) {
+          o[s2][j][0] = o[s2][j][1] = 0.0;
+          dmma8(o[s2][j][0], o[s2][j][1], cb[0], f[s2][j][0]);
+        }
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+        for (int j = 0; j < TPW; ++j) dmma8(o[s2][j][0], o[s2][j][1], cb[1], f[s2][j][1]);
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qy = t & 7;
-        *reinterpret_cast<double2*>(S2 + c * SLOT + aGX(gq, qy, 2 * kq)) = make_double2(o[j][0], o[j][1]);
+        const int t = j, tt = t & 7;
+        *reinterpret_cast<double2*>(S2 + c * SLOT + aGX(gq, tt, 2 * kq)) = make_double2(o[0][j][0], o[0][j][1]);
+        *reinterpret_cast<double2*>(S3 + c * SLOT + aGY(tt, gq, 2 * kq)) = make_double2(o[1][j][0], o[1][j][1]);
       }
     }
-    {
-      double f[TPW][2], o[TPW][2];
-#pragma unroll
-      for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
-        const double* g = S3 + c * SLOT;
-        f[j][0] = g[aGY(qx, kq, gq)];
-        f[j][1] = g[aGY(qx, 4 + kq, gq)];
-      }
-#pragma unroll
-      for (int j = 0; j < TPW; ++j) {
-        o[j][0] = o[j][1] = 0.0;
-        dmma8(o[j][0], o[j][1], cb[0], f[j][0]);
-        dmma8(o[j][0], o[j][1], cb[1], f[j][1]);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
-        *reinterpret_cast<double2*>(S3 + c * SLOT + aGY(qx, gq, 2 * kq)) = make_double2(o[j][0], o[j][1]);
-      }
-    }
-    __syncthreads();
+    __syncwarp();
 
     // ---- G: z, D'-form; tile (c, qx), lines qy:
     //      t = (tx + ty) + fz C_z^T, R = t B_z^T ------------------------------
@@ -345,7 +330,7 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       double tt[TPW][2], rr[TPW][2];
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        const int t = j, qx = t & 7;
         const double2 tx = *reinterpret_cast<const double2*>(S2 + c * SLOT + aGX(qx, gq, 2 * kq));
         const double2 ty = *reinterpret_cast<const double2*>(S3 + c * SLOT + aGY(qx, gq, 2 * kq));
         fz[j] = *reinterpret_cast<const double2*>(S4 + c * SLOT + aGZ(qx, gq, 2 * kq));
@@ -365,18 +350,18 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       }
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        const int t = j, qx = t & 7;
         *reinterpret_cast<double2*>(S1 + c * SLOT + aQR(qx, gq, 2 * kq)) = make_double2(rr[j][0], rr[j][1]);
       }
     }
-    __syncthreads();
+    __syncwarp();
 
     // ---- H: y, D-form bwd; tile (c, qx), lines iz: S = B_y^T R -------------
     {
       double f[TPW][2], o[TPW][2];
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        const int t = j, qx = t & 7;
         const double* rp = S1 + c * SLOT;
         f[j][0] = rp[aQR(qx, kq, gq)];
         f[j][1] = rp[aQR(qx, 4 + kq, gq)];
@@ -389,18 +374,18 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       }
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, qx = t & 7;
+        const int t = j, qx = t & 7;
         *reinterpret_cast<double2*>(S2 + c * SLOT + aS(qx, gq, 2 * kq)) = make_double2(o[j][0], o[j][1]);
       }
     }
-    __syncthreads();
+    __syncwarp();
 
     // ---- I: x, D-form bwd; tile (c, iy), lines iz: A = B_x^T S -------------
     {
       double f[TPW][2], o[TPW][2];
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, iy = t & 7;
+        const int t = j, iy = t & 7;
         const double* sp = S2 + c * SLOT;
         f[j][0] = sp[aS(kq, iy, gq)];
         f[j][1] = sp[aS(4 + kq, iy, gq)];
@@ -413,8 +398,8 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       }
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        const int t = warp + WARPS * j, c = t >> 3, iy = t & 7;
-        if (c < ncb) {
+        const int t = j, iy = t & 7;
+        if (c < ncb) {   // (warp-uniform)
           // D: ix = gq, iz = 2kq + h -> A[cell][ix*64 + iy*8 + iz]
           double* ap = A + (cell0 + c) * N3 + gq * NN + iy * 8 + 2 * kq;
           if ((reinterpret_cast<uintptr_t>(ap) & 15) == 0) {
@@ -426,7 +411,8 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
         }
       }
     }
-    // the next batch's stage A writes S1 only after the barrier at the top
+    // the next batch's stage A writes S1 after this warp's own stage I (same
+    // warp: program order + the __syncwarp at the top)
   }
 }
 
