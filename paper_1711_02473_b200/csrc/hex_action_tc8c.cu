@@ -61,7 +61,11 @@ constexpr int TPW = 8;                   // tiles per warp and stage
 constexpr int SLOT = 576;                // doubles per cell and slot (largest layout)
 constexpr int UC = 8 * 68;               // u per cell, ix-plane stride 68
 constexpr int CSZ = CPB * 24;
-constexpr size_t SMEM = (size_t)(4 * CPB * SLOT + CPB * UC + 2 * CSZ) * sizeof(double);
+// AU: u staged in slot S4 (gz / fz, dead from G to the next C) instead of
+// its own buffer — the next batch's u is then fetched after stage G.
+constexpr size_t smem_bytes(bool au) {
+  return (size_t)(4 * CPB * SLOT + (au ? 0 : CPB * UC) + 2 * CSZ) * sizeof(double);
+}
 
 __device__ __forceinline__ int b1(int v) { return ((v >> 1) & 1) << 2; }
 // element (a, b, c) = (x, y, z) of one cell's array (tools/tc8c_layout.py)
@@ -77,7 +81,8 @@ __device__ __forceinline__ int aS(int a, int b, int c) { return a * 68 + b * 8 +
 __device__ __forceinline__ int aU(int a, int b, int c) { return a * 68 + b * 8 + c; }
 }  // namespace tc8c
 
-__global__ void __launch_bounds__(tc8c::THREADS, 2)
+template <int MINB, bool AU>
+__global__ void __launch_bounds__(tc8c::THREADS, MINB)
 hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
                         const double* __restrict__ coords, const double* __restrict__ u,
                         double* __restrict__ A) {
@@ -87,8 +92,10 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
   double* S2 = S1 + CPB * SLOT;
   double* S3 = S2 + CPB * SLOT;
   double* S4 = S3 + CPB * SLOT;
-  double* sU = S4 + CPB * SLOT;
-  double* sCo = sU + CPB * UC;
+  static_assert(UC <= SLOT, "u fits a slot");
+  double* sU = AU ? S4 : S4 + CPB * SLOT;              // u of cell c at sU + c * (AU ? SLOT : UC)
+  double* sCo = S4 + CPB * SLOT + (AU ? 0 : CPB * UC);
+  constexpr int US = AU ? SLOT : UC;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kq = lane & 3, gq = lane >> 2;
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
@@ -114,7 +121,7 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
     const int64_t cg = bt * CPB + warp;
     if (cg < ncells) {
       const double* src = u + cg * N3;
-      double* du = sU + warp * UC;
+      double* du = sU + warp * US;
       if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -145,7 +152,7 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int t = j, iy = t & 7;
-        const double* in = sU + c * UC;
+        const double* in = sU + c * US;
         f[j][0] = in[aU(kq, iy, gq)];
         f[j][1] = in[aU(4 + kq, iy, gq)];
       }
@@ -162,7 +169,7 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       }
     }
     __syncwarp();
-    if (b + gridDim.x < nbatch) prefetch(b + gridDim.x, cur ^ 1);
+    if (!AU && b + gridDim.x < nbatch) prefetch(b + gridDim.x, cur ^ 1);
 
     // ---- B: y, D-form; tile (c, qx), lines iz: Q = B_y P -------------------
     {
@@ -356,6 +363,8 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
     }
     __syncwarp();
 
+    if (AU && b + gridDim.x < nbatch) prefetch(b + gridDim.x, cur ^ 1);   // S4 is free now
+
     // ---- H: y, D-form bwd; tile (c, qx), lines iz: S = B_y^T R -------------
     {
       double f[TPW][2], o[TPW][2];
@@ -420,9 +429,14 @@ int launch_hex_action_tc8c(const sfk_plan* p, int64_t ncells, double* A, const d
                            const double* w0, cudaStream_t s) {
   if (p->n != 8 || p->m != 8 || !p->has_ct) return SFK_EUNSUPPORTED;
   using namespace tc8c;
+  const int alt = (int)option(OPT_V6_CFG);
+  const bool au = alt == 1 || alt == 3;
+  const int minb = alt >= 2 ? 3 : 2;
+  auto kern = minb == 3 ? (au ? hex_laplace_action_tc8c<3, true> : hex_laplace_action_tc8c<3, false>)
+                        : (au ? hex_laplace_action_tc8c<2, true> : hex_laplace_action_tc8c<2, false>);
+  const size_t smem = smem_bytes(au);
   LaunchShape sh;
-  if (const int rc_ = kernel_shape((const void*)hex_laplace_action_tc8c, THREADS, SMEM,
-                                   "hex_action_tc8c", &sh, true))
+  if (const int rc_ = kernel_shape((const void*)kern, THREADS, smem, "hex_action_tc8c", &sh, true))
     return rc_;
   TabsTC8C T;
   for (int i = 0; i < 64; ++i) {
@@ -437,7 +451,7 @@ int launch_hex_action_tc8c(const sfk_plan* p, int64_t ncells, double* A, const d
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
   const int64_t resident = sh.resident();
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
-  hex_laplace_action_tc8c<<<grid, THREADS, SMEM, s>>>(T, ncells, coords, w0, A);
+  kern<<<grid, THREADS, smem, s>>>(T, ncells, coords, w0, A);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_tc8c launch");
 }
