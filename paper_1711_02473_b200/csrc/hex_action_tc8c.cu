@@ -429,9 +429,11 @@ int launch_hex_action_tc8c(const sfk_plan* p, int64_t ncells, double* A, const d
                            const double* w0, cudaStream_t s) {
   if (p->n != 8 || p->m != 8 || !p->has_ct) return SFK_EUNSUPPORTED;
   using namespace tc8c;
+  // default: u staged in S4 and 3 CTAs per SM (1.659 -> 1.633 ms,
+  // profiles/r02n_cfg*.json); option v6_cfg = 1 / 2 / 4 selects the others
   const int alt = (int)option(OPT_V6_CFG);
-  const bool au = alt == 1 || alt == 3;
-  const int minb = alt >= 2 ? 3 : 2;
+  const bool au = alt == 0 || alt == 1;
+  const int minb = (alt == 0 || alt == 2) ? 3 : 2;
   auto kern = minb == 3 ? (au ? hex_laplace_action_tc8c<3, true> : hex_laplace_action_tc8c<3, false>)
                         : (au ? hex_laplace_action_tc8c<2, true> : hex_laplace_action_tc8c<2, false>);
   const size_t smem = smem_bytes(au);

@@ -53,6 +53,23 @@ struct HexLineGeom {
     }
   }
 
+    // Same from the cell's 36 edge differences precomputed once per cell by
+  // hex_cell_edges (every line of the cell shares them): identical roundings.
+  __device__ __forceinline__ void setup_edges(const double* E, double bx0, double bx1,
+                                              double by0, double by1) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+      for (int cz = 0; cz < 2; ++cz) {
+        const double* e = E + 4 * (3 * cz + k);
+        al0[cz][k] = fma(e[1], by1, e[0] * by0);
+        al1[cz][k] = fma(e[3], bx1, e[2] * bx0);
+      }
+      const double* f = E + 24 + 4 * k;
+      c2[k] = fma(fma(f[3], by1, f[2] * by0), bx1, fma(f[1], by1, f[0] * by0) * bx0);
+    }
+  }
+
   // Adjugate rows and determinant at the point with P1 z-values (b0, b1).
   __device__ __forceinline__ double adj(double b0, double b1, double r0[3],
                                         double r1[3], double r2[3]) const {
@@ -93,6 +110,15 @@ struct HexLineAdj {
                                         double by1) {
     HexLineGeom g;
     g.setup(X, bx0, bx1, by0, by1);
+    from_geom(g);
+  }
+  __device__ __forceinline__ void setup_edges(const double* E, double bx0, double bx1,
+                                              double by0, double by1) {
+    HexLineGeom g;
+    g.setup_edges(E, bx0, bx1, by0, by1);
+    from_geom(g);
+  }
+  __device__ __forceinline__ void from_geom(const HexLineGeom& g) {
     double A[3], dA[3], B[3], dB[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -126,6 +152,26 @@ struct HexLineAdj {
     return fma(c2[2], r2[2], fma(c2[1], r2[1], c2[0] * r2[0]));
   }
 };
+
+// The 36 edge differences of a cell's vertices that HexLineGeom::setup forms
+// (X: 24 coords, v = 4a+2b+c, component inner), in setup_edges' order:
+//   E[4*(3*cz+k) + 0..3] = x-edges (b = 0, 1) and y-edges (a = 0, 1) at z = cz
+//   E[24 + 4*k + 0..3]   = z-edges (a, b) = (0,0), (0,1), (1,0), (1,1)
+// Entry e of the 36 (callers spread e over threads).
+__device__ __forceinline__ double hex_cell_edge(const double* X, int e) {
+  if (e < 24) {
+    const int g = e >> 2, w = e & 3, cz = g / 3, k = g - 3 * cz;
+    switch (w) {
+      case 0: return X[3 * (4 + cz) + k] - X[3 * cz + k];        // e00
+      case 1: return X[3 * (6 + cz) + k] - X[3 * (2 + cz) + k];  // e01
+      case 2: return X[3 * (2 + cz) + k] - X[3 * cz + k];        // e10
+      default: return X[3 * (6 + cz) + k] - X[3 * (4 + cz) + k]; // e11
+    }
+  }
+  const int k = (e - 24) >> 2, w = (e - 24) & 3;   // f00, f01, f10, f11
+  const int v0 = 2 * w;                             // (a, b) = (w >> 1, w & 1), c = 0
+  return X[3 * (v0 + 1) + k] - X[3 * v0 + k];
+}
 
 // f = s * R R^T g  (R rows r0, r1, r2).  In place on (g0, g1, g2).
 __device__ __forceinline__ void laplace_flux(const double r0[3], const double r1[3],

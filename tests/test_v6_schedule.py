@@ -43,8 +43,10 @@ def instances():
     """(n, cells per CTA, ZR, WS) of every launch_v6<...> instance."""
     txt = open(os.path.join(CSRC, "hex_action6.cu")).read()
     res = []
-    for m in re.finditer(r"launch_v6<(\d+), (\d+), (\d+)(?:, (true|false))?(?:, (true|false))?>\(p", txt):
-        res.append((int(m.group(1)), int(m.group(2)), m.group(4) == "true", m.group(5) == "true"))
+    for m in re.finditer(r"launch_v6<(\d+), (\d+), (\d+)(?:, (true|false))?(?:, (true|false))?"
+                         r"(?:, (true|false))?>\(p", txt):
+        res.append((int(m.group(1)), int(m.group(2)), m.group(4) == "true", m.group(5) == "true",
+                    m.group(6) == "true"))
     return sorted(set(res))
 
 
@@ -52,7 +54,7 @@ LAY = layouts()
 INST = instances()
 
 
-def schedule(n, cpb, zr=False, ws=False):
+def schedule(n, cpb, zr=False, ws=False, eg=False):
     """[(stage, [(lane, slot, addr, 'r'|'w')])] of one batch."""
     lay = LAY[n]
     nn = n * n
@@ -83,6 +85,11 @@ def schedule(n, cpb, zr=False, ws=False):
                 return
             stages[stage].append((t, slot, addr, kind))
 
+        if eg:   # per-cell edge differences: written in A, read by every z-line in E
+            for e in range(r, 36, nn):
+                acc("A", "GE", c * 36 + e, "w")
+            for e in range(36):
+                acc("E", "GE", c * 36 + e, "r")
         for e in range(n):
             acc("A", "S1", at("P1", c, e, ra, rb), "w")
             acc("B", "S1", at("P1", c, ra, e, rb), "r")
@@ -115,13 +122,13 @@ def schedule(n, cpb, zr=False, ws=False):
     return [(s, stages[s]) for s in "ABCDEFGHI"]
 
 
-@pytest.mark.parametrize("n,cpb,zr,ws", INST)
-def test_v6_schedule_bounds_races_coverage(n, cpb, zr, ws):
+@pytest.mark.parametrize("n,cpb,zr,ws,eg", INST)
+def test_v6_schedule_bounds_races_coverage(n, cpb, zr, ws, eg):
     lay = LAY[n]
     assert set(lay) == set(ROLES)
     slot = max(v[2] for v in lay.values())
     size = cpb * slot
-    sched = schedule(n, cpb, zr, ws)
+    sched = schedule(n, cpb, zr, ws, eg)
     if ws:
         # warp-synchronous: no CTA barrier at all, so no address may be
         # touched by two warps in any stage
@@ -133,7 +140,7 @@ def test_v6_schedule_bounds_races_coverage(n, cpb, zr, ws):
         owner = {}
         readers = defaultdict(set)
         for lane, sl, addr, kind in accs:
-            assert 0 <= addr < size, (stage, sl, addr, size)
+            assert 0 <= addr < (cpb * 36 if sl == "GE" else size), (stage, sl, addr, size)
             key = (sl, addr)
             if kind == "w":
                 assert owner.get(key, lane) == lane, ("two writers", stage, key)
@@ -154,11 +161,12 @@ def test_v6_schedule_bounds_races_coverage(n, cpb, zr, ws):
             if a[3] == "w":
                 distinct[a[1]].add(a[2])
         for sl in per_slot:
-            assert per_slot[sl] == len(distinct[sl]) == cpb * n ** 3, (stage, sl, per_slot[sl])
+            full = cpb * 36 if sl == "GE" else cpb * n ** 3
+            assert per_slot[sl] == len(distinct[sl]) == full, (stage, sl, per_slot[sl])
         assert nw > 0 or stage == "I"
 
 
 def test_v6_instances_cover_every_degree_dispatched():
     ns = {i[0] for i in INST}
     assert {3, 4, 5, 6, 7, 8, 9} <= ns
-    assert any(i[3] for i in INST) and any(i[2] for i in INST)   # WS and ZR instances modelled
+    assert any(i[3] for i in INST) and any(i[2] for i in INST) and any(i[4] for i in INST)
