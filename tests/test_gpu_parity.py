@@ -308,6 +308,44 @@ def test_host_path_thread_safe(cuda):
         assert np.array_equal(r, expect)
 
 
+def test_device_path_concurrent_first_use(cuda):
+    """Four host threads create fresh plans and launch on their own streams
+    at once, so the per-device launch-shape setup (kernel_shape: the >48 KB
+    shared-memory opt-in and the occupancy query, cached under a mutex) runs
+    concurrently on first use of each kernel; every result must equal the
+    single-threaded one bit for bit (launch state thread safety,
+    SPEC.md:580 reentrant kernels)."""
+    import threading
+
+    torch = cuda
+    degrees = (2, 4, 6, 7, 8, 3, 5, 1)
+    ins = {p: _dev(torch, workloads.c2_inputs(p, dims=(5, 6, 7))) for p in degrees}
+    res = {}
+    errs = []
+
+    def work(k):
+        try:
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                for p in degrees[k::4] + degrees[(k + 1) % 4::4]:
+                    plan = compile_kernel("action_laplace", "hex", p)
+                    out = evaluate_batched(plan, ins[p])
+                    stream.synchronize()
+                    res[(k, p)] = out
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for (k, p), out in res.items():
+        ref = evaluate_batched(compile_kernel("action_laplace", "hex", p), ins[p])
+        assert torch.equal(out, ref), (k, p)
+
+
 def test_non_contiguous_and_offset_inputs(cuda):
     torch = cuda
     plan = compile_kernel("action_laplace", "hex", 4)
