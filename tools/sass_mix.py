@@ -29,13 +29,15 @@ LIB = os.path.join(ROOT, "paper_1711_02473_b200", "libsfk.so")
 KERNELS = [
     ("C2 p=1 cell", r"hex_laplace_action_p1ILb0E"),
     ("C2 p=2 cellv", r"hex_laplace_action_cellILi3ELi64ELi1ELb0E"),
-    ("C2 p=3 v4", r"hex_laplace_action_v4INS_10Act4LayoutILi4E.*Lb0EE"),
-    ("C2 p=4 v6", r"hex_laplace_action_v6ILi5ELi5ELi2E"),
-    ("C2 p=5 v6", r"hex_laplace_action_v6ILi6ELi7ELi2E"),
-    ("C2 p=6 v6", r"hex_laplace_action_v6ILi7ELi5ELi2E"),
-    ("C2 p=7 tc (DMMA)", r"hex_laplace_action_tc.*Lb0E"),
-    ("C2 p=8 v6", r"hex_laplace_action_v6ILi9ELi3ELi2E"),
-    ("C3 colloc", r"hex_colloc_action_kernelILi9E"),
+    ("C2 p=3 v6 (warp-sync)", r"hex_laplace_action_v6ILi4ELi8ELi4ELb0ELb1ELb0E"),
+    ("C2 p=4 v6 (ZR)", r"hex_laplace_action_v6ILi5ELi5ELi4ELb1ELb0ELb0E"),
+    ("C2 p=5 v6 (ZR)", r"hex_laplace_action_v6ILi6ELi7ELi2ELb1ELb0ELb0E"),
+    ("C2 p=6 v6 (ZR)", r"hex_laplace_action_v6ILi7ELi5ELi2ELb1ELb0ELb0E"),
+    ("C2 p=7 tc8c (DMMA)", r"hex_laplace_action_tc8cILi3ELb1E"),
+    ("C2 p=8 v6 (EG)", r"hex_laplace_action_v6ILi9ELi3ELi2ELb0ELb0ELb1E"),
+    ("C2 p=7 tc8 (round 1, DMMA)", r"hex_laplace_action_tc8ILb0E"),
+    ("C2 p=8 v5 (round 1)", r"hex_laplace_action_v5ILi9ELi3ELi2ELi2ELb1ELb0E"),
+    ("C3 colloc p=8", r"hex_colloc_action_kernelILi9E"),
     ("C4 neo-Hookean p=4", r"hex_neohookean_kernelILi5ELi6E"),
     ("C5 p=3 tc4 (DMMA)", r"hex_laplace_matrix_tc4"),
     ("C5 p=4 tc5 (DMMA)", r"hex_laplace_matrix_tc5"),
@@ -87,7 +89,7 @@ def main():
         if not hits:
             rows.append((label, "(not found)", None))
             continue
-        name, body = hits[0]
+        name, body = hits[0]   # first instance matching (the dispatched one above)
         rows.append((label, name, mix(body)))
     lines = ["# Static SASS instruction mix (libsfk.so, sm_100a)", "",
              "`python tools/sass_mix.py` — counts per kernel function (fully unrolled "
