@@ -70,6 +70,25 @@ struct HexLineGeom {
     }
   }
 
+  // Same from the cell's per-line-family table (hex_cell_lg): al0 depends on
+  // qy only, al1 on qx only, c2 = g1 bx1 + g0 bx0 with g depending on qy
+  // only — identical operations and roundings, 6 FP64 ops instead of 78.
+  __device__ __forceinline__ void setup_lg(const double* LG, int n, int qx, int qy, double bx0,
+                                           double bx1) {
+    const double* a0 = LG + 6 * qy;
+    const double* a1 = LG + 6 * n + 6 * qx;
+    const double* g = LG + 12 * n + 6 * qy;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+      for (int cz = 0; cz < 2; ++cz) {
+        al0[cz][k] = a0[3 * cz + k];
+        al1[cz][k] = a1[3 * cz + k];
+      }
+      c2[k] = fma(g[3 + k], bx1, g[k] * bx0);
+    }
+  }
+
   // Adjugate rows and determinant at the point with P1 z-values (b0, b1).
   __device__ __forceinline__ double adj(double b0, double b1, double r0[3],
                                         double r1[3], double r2[3]) const {
@@ -116,6 +135,12 @@ struct HexLineAdj {
                                               double by0, double by1) {
     HexLineGeom g;
     g.setup_edges(E, bx0, bx1, by0, by1);
+    from_geom(g);
+  }
+  __device__ __forceinline__ void setup_lg(const double* LG, int n, int qx, int qy, double bx0,
+                                           double bx1) {
+    HexLineGeom g;
+    g.setup_lg(LG, n, qx, qy, bx0, bx1);
     from_geom(g);
   }
   __device__ __forceinline__ void from_geom(const HexLineGeom& g) {
@@ -171,6 +196,31 @@ __device__ __forceinline__ double hex_cell_edge(const double* X, int e) {
   const int k = (e - 24) >> 2, w = (e - 24) & 3;   // f00, f01, f10, f11
   const int v0 = 2 * w;                             // (a, b) = (w >> 1, w & 1), c = 0
   return X[3 * (v0 + 1) + k] - X[3 * v0 + k];
+}
+
+// Per-cell line-geometry table (18 n doubles), entry e:
+//   [0, 6n)    al0[qy][cz][k]  = e01 by1(qy) + e00 by0(qy)   (x-edges, b = 0 / 1)
+//   [6n, 12n)  al1[qx][cz][k]  = e11 bx1(qx) + e10 bx0(qx)   (y-edges, a = 0 / 1)
+//   [12n, 18n) g[qy][w][k]     w = 0: f01 by1 + f00 by0, w = 1: f11 by1 + f10 by0
+// with exactly HexLineGeom::setup's operations; Bc[q], Bc[n + q] = P1 values.
+__device__ __forceinline__ double hex_cell_lg(const double* X, const double* Bc, int n, int e) {
+  const int part = e / (6 * n), r = e - part * 6 * n;
+  const int q = r / 6, j = r - 6 * q, hi = j / 3, k = j - 3 * hi;   // hi = cz or w
+  const double b0 = Bc[q], b1 = Bc[n + q];
+  if (part == 0) {
+    const double e00 = X[3 * (4 + hi) + k] - X[3 * hi + k];
+    const double e01 = X[3 * (6 + hi) + k] - X[3 * (2 + hi) + k];
+    return fma(e01, b1, e00 * b0);
+  }
+  if (part == 1) {
+    const double e10 = X[3 * (2 + hi) + k] - X[3 * hi + k];
+    const double e11 = X[3 * (6 + hi) + k] - X[3 * (4 + hi) + k];
+    return fma(e11, b1, e10 * b0);
+  }
+  // w = hi: (a = hi) z-edges (hi, 0) and (hi, 1)
+  const double fl = X[3 * (4 * hi + 1) + k] - X[3 * (4 * hi) + k];       // f(a,0)
+  const double fh = X[3 * (4 * hi + 3) + k] - X[3 * (4 * hi + 2) + k];   // f(a,1)
+  return fma(fh, b1, fl * b0);
 }
 
 // f = s * R R^T g  (R rows r0, r1, r2).  In place on (g0, g1, g2).

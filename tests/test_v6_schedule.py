@@ -85,11 +85,12 @@ def schedule(n, cpb, zr=False, ws=False, eg=False):
                 return
             stages[stage].append((t, slot, addr, kind))
 
-        if eg:   # per-cell edge differences: written in A, read by every z-line in E
-            for e in range(r, 36, nn):
-                acc("A", "GE", c * 36 + e, "w")
-            for e in range(36):
-                acc("E", "GE", c * 36 + e, "r")
+        if eg:   # per-cell line-geometry table: written in A, read in E
+            for e in range(r, 18 * n, nn):
+                acc("A", "GE", c * 18 * n + e, "w")
+            for e in list(range(6 * ra, 6 * ra + 6)) + list(range(6 * n + 6 * rb, 6 * n + 6 * rb + 6)) \
+                    + list(range(12 * n + 6 * ra, 12 * n + 6 * ra + 6)):
+                acc("E", "GE", c * 18 * n + e, "r")
         for e in range(n):
             acc("A", "S1", at("P1", c, e, ra, rb), "w")
             acc("B", "S1", at("P1", c, ra, e, rb), "r")
@@ -140,7 +141,7 @@ def test_v6_schedule_bounds_races_coverage(n, cpb, zr, ws, eg):
         owner = {}
         readers = defaultdict(set)
         for lane, sl, addr, kind in accs:
-            assert 0 <= addr < (cpb * 36 if sl == "GE" else size), (stage, sl, addr, size)
+            assert 0 <= addr < (cpb * 18 * n if sl == "GE" else size), (stage, sl, addr, size)
             key = (sl, addr)
             if kind == "w":
                 assert owner.get(key, lane) == lane, ("two writers", stage, key)
@@ -161,7 +162,7 @@ def test_v6_schedule_bounds_races_coverage(n, cpb, zr, ws, eg):
             if a[3] == "w":
                 distinct[a[1]].add(a[2])
         for sl in per_slot:
-            full = cpb * 36 if sl == "GE" else cpb * n ** 3
+            full = cpb * 18 * n if sl == "GE" else cpb * n ** 3
             assert per_slot[sl] == len(distinct[sl]) == full, (stage, sl, per_slot[sl])
         assert nw > 0 or stage == "I"
 
