@@ -54,10 +54,16 @@ def main():
     ap.add_argument("--cells", type=int, default=1 << 16)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--fma", action="store_true")
+    ap.add_argument("--big", action="store_true",
+                    help="the p = 5..8 hex Laplace matrices of programs_big.npz (cells capped "
+                         "so the output stays under 2 GB)")
     ap.add_argument("keys", nargs="*")
     a = ap.parse_args()
-    idx = {m["key"]: m for m in json.load(open(os.path.join(GOLDEN, "programs.json")))}
-    z = np.load(os.path.join(GOLDEN, "programs.npz"))
+    stem = "programs_big" if a.big else "programs"
+    idx = {m["key"]: m for m in json.load(open(os.path.join(GOLDEN, stem + ".json")))}
+    z = np.load(os.path.join(GOLDEN, stem + ".npz"))
+    if a.big and not a.keys:
+        a.keys = list(idx)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     p64 = max(runtime.fp64_peak(0.5))
     for key in a.keys or DEFAULT:
@@ -65,6 +71,8 @@ def main():
         text = bytes(z[key + "__json"]).decode()
         plan = load_program(text, fma=a.fma)
         cells = a.cells
+        if a.big:
+            cells = min(cells, max(1, (2 << 30) // (8 * m["return"][1])))
         ins = {}
         for name, size in m["arguments"]:
             v = z["%s__%s" % (key, name)]
@@ -82,7 +90,7 @@ def main():
                "hbm_gbs": round(nbytes * cells / ms * 1e-6, 1), "p64_tflops": round(p64, 2),
                "bound": "fp64" if fl / (p64 * 1e12) >= nbytes / (HBM_GBS * 1e9) else "hbm",
                "roofline_frac": round(t_roof / ms, 4), "config": plan.config}
-        if key in HAND and not key.endswith("colloc"):
+        if key in HAND and not key.endswith("colloc") and not a.big:
             hp = compile_kernel(*HAND[key])
             hms = timeit(lambda: evaluate_batched(hp, ins, out=out), a.reps, flush)
             rec["hand_ms"] = round(hms, 5)
