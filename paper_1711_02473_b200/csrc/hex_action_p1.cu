@@ -30,10 +30,7 @@ constexpr size_t SMEM = (size_t)CPB * (CS + US) * sizeof(double);
 // GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
 // item 1): u = x gathered through cmap[c][0..7], A = y scatter-added with
 // fp64 atomics.
-// BK: every thread moves its own cell's coords (192 B) and u (64 B) with two
-// bulk copies (cp.async.bulk, SASS UBLKCP) completing on one CTA mbarrier,
-// instead of 16 cooperative 16-byte cp.async per thread.
-template <bool GS, bool BK = false>
+template <bool GS>
 __global__ void __launch_bounds__(p1::CPB, SFK_P1_MINB)
 hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
@@ -52,17 +49,7 @@ hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
     const double* ug = u + cell0 * 8;
     const bool al = ((reinterpret_cast<uintptr_t>(cg) |
                       (GS ? 0 : reinterpret_cast<uintptr_t>(ug))) & 15) == 0;
-    if (BK && !GS && al) {
-      __shared__ uint64_t bar;
-      if (tid == 0) mbar_init(&bar, 1);
-      __syncthreads();
-      if (tid < ncb) {
-        bulk_g2s(sC + tid * CS, cg + tid * 24, 192u, &bar);
-        bulk_g2s(sU + tid * US, ug + tid * 8, 64u, &bar);
-      }
-      if (tid == 0) mbar_arrive_expect_tx(&bar, (unsigned)ncb * 256u);
-      mbar_wait(&bar, 0);
-    } else if (al) {
+    if (al) {
       for (int ch = tid; ch < ncb * 12; ch += CPB) {
         const int c = ch / 12, k = ch - c * 12;
         cp_async16(sC + c * CS + 2 * k, cg + 2 * ch);
@@ -201,24 +188,23 @@ hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
   }
 }
 
-template <bool GS, bool BK = false>
+template <bool GS>
 static int launch_p1(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                      const double* w0, cudaStream_t s, const int* cmap) {
   if (p->n != 2 || p->m != 2) return SFK_EUNSUPPORTED;
   LaunchShape sh;
-  if (const int rc_ = kernel_shape((const void*)hex_laplace_action_p1<GS, BK>, p1::CPB, p1::SMEM,
+  if (const int rc_ = kernel_shape((const void*)hex_laplace_action_p1<GS>, p1::CPB, p1::SMEM,
                                    "hex_action_p1", &sh))
     return rc_;
   const Tabs<2, 2> T = make_tabs<2, 2>(p);
   const unsigned grid = (unsigned)((ncells + p1::CPB - 1) / p1::CPB);
-  hex_laplace_action_p1<GS, BK><<<grid, p1::CPB, p1::SMEM, s>>>(T, ncells, coords, w0, A, cmap);
+  hex_laplace_action_p1<GS><<<grid, p1::CPB, p1::SMEM, s>>>(T, ncells, coords, w0, A, cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_p1 launch");
 }
 
 int launch_hex_action_p1(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, cudaStream_t s) {
-  if (option(OPT_V6_CFG) == 8) return launch_p1<false, true>(p, ncells, A, coords, w0, s, nullptr);
   return launch_p1<false>(p, ncells, A, coords, w0, s, nullptr);
 }
 

@@ -64,7 +64,7 @@ constexpr int CSZ = CPB * 24;
 // AU: u staged in slot S4 (gz / fz, dead from G to the next C) instead of
 // its own buffer — the next batch's u is then fetched after stage G.
 constexpr size_t smem_bytes(bool au) {
-  return (size_t)(4 * CPB * SLOT + (au ? 0 : CPB * UC) + 2 * CSZ + CPB) * sizeof(double);
+  return (size_t)(4 * CPB * SLOT + (au ? 0 : CPB * UC) + 2 * CSZ) * sizeof(double);
 }
 
 __device__ __forceinline__ int b1(int v) { return ((v >> 1) & 1) << 2; }
@@ -81,9 +81,7 @@ __device__ __forceinline__ int aS(int a, int b, int c) { return a * 68 + b * 8 +
 __device__ __forceinline__ int aU(int a, int b, int c) { return a * 68 + b * 8 + c; }
 }  // namespace tc8c
 
-// BK: each warp's u planes (8 x 512 B into the stride-68 layout) and
-// coordinates arrive as bulk copies on a per-warp mbarrier (UBLKCP).
-template <int MINB, bool AU, bool BK = false>
+template <int MINB, bool AU>
 __global__ void __launch_bounds__(tc8c::THREADS, MINB)
 hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
                         const double* __restrict__ coords, const double* __restrict__ u,
@@ -97,7 +95,6 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
   static_assert(UC <= SLOT, "u fits a slot");
   double* sU = AU ? S4 : S4 + CPB * SLOT;              // u of cell c at sU + c * (AU ? SLOT : UC)
   double* sCo = S4 + CPB * SLOT + (AU ? 0 : CPB * UC);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sCo + 2 * CSZ);   // [CPB] (BK)
   constexpr int US = AU ? SLOT : UC;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kq = lane & 3, gq = lane >> 2;
@@ -120,19 +117,8 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
   }
 
   // each warp stages its own cell: u (ix-planes at stride 68) and coords
-  const bool bk = BK && (reinterpret_cast<uintptr_t>(u) & 15) == 0 &&
-                  (reinterpret_cast<uintptr_t>(coords) & 15) == 0;
   auto prefetch = [&](int64_t bt, int buf) {
     const int64_t cg = bt * CPB + warp;
-    if (bk) {
-      if (cg < ncells) {
-        fence_proxy_async_smem();   // the slot's earlier generic reads come first
-        if (lane < 8) bulk_g2s(sU + warp * US + lane * 68, u + cg * N3 + lane * 64, 512u, &bars[warp]);
-        if (lane == 8) bulk_g2s(sCo + buf * CSZ + warp * 24, coords + cg * 24, 192u, &bars[warp]);
-      }
-      if (lane == 0) mbar_arrive_expect_tx(&bars[warp], cg < ncells ? 8u * 512u + 192u : 0u);
-      return;
-    }
     if (cg < ncells) {
       const double* src = u + cg * N3;
       double* du = sU + warp * US;
@@ -150,10 +136,6 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
     cp_async_commit();
   };
 
-  if (bk) {
-    if (lane == 0) mbar_init(&bars[warp], 1);
-    __syncwarp();
-  }
   int64_t b = blockIdx.x;
   if (b < nbatch) prefetch(b, 0);
   for (int it = 0; b < nbatch; b += gridDim.x, ++it) {
@@ -161,7 +143,6 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
     const int64_t cell0 = b * CPB;
     const int ncb = (int)((ncells - cell0) < CPB ? (ncells - cell0) : CPB);
     cp_async_wait<0>();
-    if (bk) mbar_wait(&bars[warp], (unsigned)(it & 1));
     __syncwarp();
     const int c = warp;
 
@@ -451,10 +432,9 @@ int launch_hex_action_tc8c(const sfk_plan* p, int64_t ncells, double* A, const d
   // default: u staged in S4 and 3 CTAs per SM (1.659 -> 1.633 ms,
   // profiles/r02n_cfg*.json); option v6_cfg = 1 / 2 / 4 selects the others
   const int alt = (int)option(OPT_V6_CFG);
-  const bool au = alt == 0 || alt == 1 || alt == 8;
-  const int minb = (alt == 0 || alt == 2 || alt == 8) ? 3 : 2;
-  auto kern = alt == 8 ? hex_laplace_action_tc8c<3, true, true>
-            : minb == 3 ? (au ? hex_laplace_action_tc8c<3, true> : hex_laplace_action_tc8c<3, false>)
+  const bool au = alt == 0 || alt == 1;
+  const int minb = (alt == 0 || alt == 2) ? 3 : 2;
+  auto kern = minb == 3 ? (au ? hex_laplace_action_tc8c<3, true> : hex_laplace_action_tc8c<3, false>)
                         : (au ? hex_laplace_action_tc8c<2, true> : hex_laplace_action_tc8c<2, false>);
   const size_t smem = smem_bytes(au);
   LaunchShape sh;
