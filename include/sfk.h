@@ -148,6 +148,29 @@ int sfk_eval_host_async(const sfk_plan *plan, int64_t ncells, double *A,
 int sfk_host_wait(void);
 
 /*
+ * Device-resident meshes.  The reference's caller loop passes the same
+ * coordinates to every kernel it runs on a mesh (scheduling.py:731-735 takes
+ * `coords` per call); with several operators, degrees or iterations over one
+ * mesh the host path would re-send them on every call.  A mesh holds them on
+ * the current device: upload once (sfk_mesh_upload: asynchronous, on the
+ * host path's first staging stream; every later sfk_eval_host_mesh call on
+ * the device is ordered after it), then evaluate with host w0 / w1 / A only.
+ *   coords_size: 24 (hex) or 8 (quad) doubles per cell.
+ */
+typedef struct sfk_mesh sfk_mesh;
+int sfk_mesh_create(int64_t ncells, int coords_size, sfk_mesh **out);
+int sfk_mesh_upload(sfk_mesh *mesh, const double *coords_host);
+/* device pointer of the mesh coordinates ([ncells][coords_size]) for sfk_eval */
+const double *sfk_mesh_coords(const sfk_mesh *mesh);
+int sfk_mesh_destroy(sfk_mesh *mesh);
+/* cells [first_cell, first_cell + ncells) of the mesh; A, w0, w1 are HOST
+ * arrays for those cells.  wait = 0: asynchronous like sfk_eval_host_async
+ * (complete after sfk_host_wait); wait != 0: synchronous like sfk_eval_host. */
+int sfk_eval_host_mesh(const sfk_plan *plan, const sfk_mesh *mesh, int64_t first_cell,
+                       int64_t ncells, double *A, const double *w0, const double *w1,
+                       int64_t chunk_cells, int wait);
+
+/*
  * Global (assembled) operator application, matrix-free:
  *     y += sum_c P_c^T A_c P_c x
  * P_c gathers the cell's local dofs from the global vector x through

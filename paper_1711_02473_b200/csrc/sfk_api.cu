@@ -73,10 +73,6 @@ static int launch_c2(const sfk_plan* p, int64_t ncells, double* A, const double*
   int v = c2_variant();
   if (v == 0) v = c2_auto(p->n);
   int rc = SFK_EUNSUPPORTED;
-  if (v == 12) {
-    rc = launch_hex_action_v6r(p, ncells, A, coords, w0, s);
-    if (rc == SFK_EUNSUPPORTED) v = c2_auto(p->n);
-  }
   if (v == 11) {
     rc = launch_hex_action_tc8c(p, ncells, A, coords, w0, s);
     if (rc == SFK_EUNSUPPORTED) v = c2_auto(p->n);
@@ -144,6 +140,7 @@ struct HostCtx {
   std::mutex mu;
   bool init = false;
   cudaStream_t stream[NS] = {};
+  cudaEvent_t done[NS] = {};   // scratch events (mesh upload fences)
   double* buf[NS] = {};
   size_t cap = 0;
   int reserve(size_t bytes) {
@@ -151,6 +148,9 @@ struct HostCtx {
       for (int i = 0; i < NS; ++i) {
         int rc = cuda_status(cudaStreamCreateWithFlags(&stream[i], cudaStreamNonBlocking),
                              "cudaStreamCreate(eval_host)");
+        if (rc == SFK_OK)
+          rc = cuda_status(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming),
+                           "cudaEventCreate(eval_host)");
         if (rc != SFK_OK) return rc;
       }
       init = true;
@@ -398,11 +398,15 @@ int sfk_eval_pair(const sfk_plan* p0, const sfk_plan* p1, int64_t ncells, double
   return dispatch(p1, ncells, A1, coords, w0, nullptr, s);
 }
 
+struct sfk_mesh_impl;
 static int eval_host_impl(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                          const double* w0, const double* w1, int64_t chunk, bool wait) {
-  int st = validate(p, ncells, A, coords, w0, w1);
+                          const double* w0, const double* w1, int64_t chunk, bool wait,
+                          const double* dcoords = nullptr, cudaEvent_t ready = nullptr) {
+  // dcoords: device-resident coordinates (sfk_mesh), no coords H2D; `ready`
+  // orders every staging stream after the mesh upload
+  int st = validate(p, ncells, A, dcoords ? dcoords : coords, w0, w1);
   if (st != SFK_OK || ncells == 0) return st;
-  const int64_t per_cell = p->coords_size + p->w0_size + p->w1_size + p->a_size;
+  const int64_t per_cell = (dcoords ? 0 : p->coords_size) + p->w0_size + p->w1_size + p->a_size;
   if (chunk <= 0) {
     // ~128 MiB of traffic per chunk: H2D of chunk k+1, the kernel of chunk k
     // and the D2H of chunk k-1 overlap (separate copy engines per direction;
@@ -429,12 +433,18 @@ static int eval_host_impl(const sfk_plan* p, int64_t ncells, double* A, const do
     const int i = (int)(k % HostCtx::NS);
     cudaStream_t s = ctx->stream[i];
     double* dc = ctx->buf[i];
-    double* dw0 = dc + chunk * p->coords_size;
+    double* dw0 = dc + (dcoords ? 0 : chunk * p->coords_size);
     double* dw1 = dw0 + chunk * p->w0_size;
     double* dA = dw1 + chunk * p->w1_size;
-    rc = cuda_status(cudaMemcpyAsync(dc, coords + c0 * p->coords_size,
-                                     nc * p->coords_size * sizeof(double),
-                                     cudaMemcpyHostToDevice, s), "H2D coords");
+    if (dcoords) {
+      dc = const_cast<double*>(dcoords) + c0 * p->coords_size;
+      if (ready && k < HostCtx::NS)
+        rc = cuda_status(cudaStreamWaitEvent(s, ready, 0), "cudaStreamWaitEvent(mesh)");
+    } else {
+      rc = cuda_status(cudaMemcpyAsync(dc, coords + c0 * p->coords_size,
+                                       nc * p->coords_size * sizeof(double),
+                                       cudaMemcpyHostToDevice, s), "H2D coords");
+    }
     if (rc == SFK_OK && p->w0_size)
       rc = cuda_status(cudaMemcpyAsync(dw0, w0 + c0 * p->w0_size, nc * p->w0_size * sizeof(double),
                                        cudaMemcpyHostToDevice, s), "H2D w0");
@@ -478,6 +488,103 @@ int sfk_host_wait(void) {
     if (rc == SFK_OK) rc = cuda_status(e, "cudaStreamSynchronize(host_wait)");
   }
   return rc;
+}
+
+// ---- device-resident meshes ------------------------------------------------
+struct sfk_mesh {
+  int dev = 0;
+  int64_t ncells = 0;
+  int coords_size = 0;
+  double* d = nullptr;
+  cudaEvent_t ready = nullptr;
+};
+
+int sfk_mesh_create(int64_t ncells, int coords_size, sfk_mesh** out) {
+  if (!out) return fail(SFK_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (ncells < 0) return fail(SFK_EINVAL, "ncells < 0");
+  if (coords_size != 24 && coords_size != 8)
+    return fail(SFK_EINVAL, "coords_size must be 24 (hex) or 8 (quad), got %d", coords_size);
+  sfk_mesh* m = new (std::nothrow) sfk_mesh();
+  if (!m) return fail(SFK_ENOMEM, "mesh allocation failed");
+  int rc = cuda_status(cudaGetDevice(&m->dev), "cudaGetDevice");
+  if (rc == SFK_OK && ncells > 0)
+    rc = cuda_status(cudaMalloc(&m->d, (size_t)ncells * coords_size * sizeof(double)),
+                     "cudaMalloc(mesh)");
+  if (rc == SFK_OK)
+    rc = cuda_status(cudaEventCreateWithFlags(&m->ready, cudaEventDisableTiming),
+                     "cudaEventCreate(mesh)");
+  if (rc != SFK_OK) {
+    if (m->d) cudaFree(m->d);
+    delete m;
+    return rc;
+  }
+  m->ncells = ncells;
+  m->coords_size = coords_size;
+  *out = m;
+  return SFK_OK;
+}
+
+int sfk_mesh_destroy(sfk_mesh* m) {
+  if (!m) return SFK_OK;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(m->dev);
+  cudaEventSynchronize(m->ready);
+  if (m->d) cudaFree(m->d);
+  cudaEventDestroy(m->ready);
+  cudaSetDevice(cur);
+  delete m;
+  return SFK_OK;
+}
+
+const double* sfk_mesh_coords(const sfk_mesh* m) { return m ? m->d : nullptr; }
+
+int sfk_mesh_upload(sfk_mesh* m, const double* coords) {
+  if (!m) return fail(SFK_EINVAL, "mesh is NULL");
+  if (m->ncells == 0) return SFK_OK;
+  if (!coords) return fail(SFK_EINVAL, "coords is NULL");
+  int dev = 0;
+  int rc = cuda_status(cudaGetDevice(&dev), "cudaGetDevice");
+  if (rc != SFK_OK) return rc;
+  if (dev != m->dev) return fail(SFK_EINVAL, "mesh lives on device %d, current is %d", m->dev, dev);
+  HostCtx* ctx = host_ctx(dev);
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  rc = ctx->reserve(0);   // streams exist
+  if (rc != SFK_OK) return rc;
+  cudaStream_t s = ctx->stream[0];
+  // earlier evaluations on the other staging streams may still read the
+  // mesh: order the overwrite after them
+  for (int i = 1; i < HostCtx::NS && rc == SFK_OK; ++i) {
+    cudaEvent_t e = ctx->done[i];
+    rc = cuda_status(cudaEventRecord(e, ctx->stream[i]), "cudaEventRecord(mesh fence)");
+    if (rc == SFK_OK) rc = cuda_status(cudaStreamWaitEvent(s, e, 0), "cudaStreamWaitEvent(mesh fence)");
+  }
+  if (rc != SFK_OK) return rc;
+  rc = cuda_status(cudaMemcpyAsync(m->d, coords, (size_t)m->ncells * m->coords_size * sizeof(double),
+                                   cudaMemcpyHostToDevice, s), "H2D mesh");
+  if (rc == SFK_OK) rc = cuda_status(cudaEventRecord(m->ready, s), "cudaEventRecord(mesh)");
+  return rc;
+}
+
+int sfk_eval_host_mesh(const sfk_plan* p, const sfk_mesh* m, int64_t first_cell, int64_t ncells,
+                       double* A, const double* w0, const double* w1, int64_t chunk_cells,
+                       int wait) {
+  if (!m) return fail(SFK_EINVAL, "mesh is NULL");
+  if (!p) return fail(SFK_EINVAL, "plan is NULL");
+  if (p->coords_size != m->coords_size)
+    return fail(SFK_EINVAL, "plan takes %lld coordinates per cell, the mesh holds %d",
+                (long long)p->coords_size, m->coords_size);
+  if (first_cell < 0 || ncells < 0 || first_cell + ncells > m->ncells)
+    return fail(SFK_EINVAL, "cells [%lld, %lld) outside the mesh (%lld cells)",
+                (long long)first_cell, (long long)(first_cell + ncells), (long long)m->ncells);
+  int dev = 0;
+  int rc = cuda_status(cudaGetDevice(&dev), "cudaGetDevice");
+  if (rc != SFK_OK) return rc;
+  if (dev != m->dev) return fail(SFK_EINVAL, "mesh lives on device %d, current is %d", m->dev, dev);
+  if (ncells == 0) return SFK_OK;
+  return eval_host_impl(p, ncells, A, nullptr, w0, w1, chunk_cells, wait != 0,
+                        m->d + first_cell * m->coords_size, m->ready);
 }
 
 int sfk_eval_gather_scatter(const sfk_plan* p, int64_t ncells, const int32_t* cell_dofs,

@@ -29,7 +29,7 @@ from .errors import NativeError, ShapeMismatch, UnboundVariable
 __all__ = ["load_library", "evaluate_batched", "evaluate_batched_pair", "set_option",
            "get_option",
            "evaluate_host", "sum_squares", "launch_count", "fp64_peak",
-           "device_info", "native_plan", "EXPORTED_SYMBOLS"]
+           "device_info", "native_plan", "EXPORTED_SYMBOLS", "Mesh"]
 
 _LIB = None
 _LOCK = threading.Lock()
@@ -45,7 +45,8 @@ EXPORTED_SYMBOLS = (
     "sfk_csr_create", "sfk_csr_info", "sfk_csr_destroy", "sfk_assemble_csr",
     "sfk_csr_entry_map", "sfk_eval_global", "sfk_eval_host_async", "sfk_host_wait",
     "sfk_csr_insert", "sfk_set_option", "sfk_get_option",
-    "sfk_kernel_available",
+    "sfk_kernel_available", "sfk_mesh_create", "sfk_mesh_upload", "sfk_mesh_coords",
+    "sfk_mesh_destroy", "sfk_eval_host_mesh",
 )
 ABI_VERSION = 1
 SUM_WORKSPACE = 1024
@@ -117,6 +118,17 @@ def _declare(lib):
     if hasattr(lib, "sfk_csr_insert"):
         lib.sfk_csr_insert.argtypes = [i64, ci, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         lib.sfk_csr_insert.restype = ci
+    if hasattr(lib, "sfk_mesh_create"):
+        lib.sfk_mesh_create.argtypes = [i64, ci, ctypes.POINTER(_vp)]
+        lib.sfk_mesh_create.restype = ci
+        lib.sfk_mesh_upload.argtypes = [_vp, _vp]
+        lib.sfk_mesh_upload.restype = ci
+        lib.sfk_mesh_coords.argtypes = [_vp]
+        lib.sfk_mesh_coords.restype = _vp
+        lib.sfk_mesh_destroy.argtypes = [_vp]
+        lib.sfk_mesh_destroy.restype = ci
+        lib.sfk_eval_host_mesh.argtypes = [_vp, _vp, i64, i64, _vp, _vp, _vp, i64, ci]
+        lib.sfk_eval_host_mesh.restype = ci
 
 
 def load_library(build_if_missing=True):
@@ -376,6 +388,44 @@ def host_wait():
     _check(load_library().sfk_host_wait())
 
 
+class Mesh:
+    """Device-resident cell coordinates (sfk_mesh, include/sfk.h): upload once,
+    then evaluate host-side w0 / w1 -> A on any number of plans without
+    re-sending the coordinates (the reference's emitted kernels take
+    ``coords`` on every call, scheduling.py:731-735)."""
+
+    def __init__(self, ncells, coords_size=24):
+        import ctypes
+
+        lib = load_library()
+        h = ctypes.c_void_p()
+        _check(lib.sfk_mesh_create(int(ncells), int(coords_size), ctypes.byref(h)))
+        self._h, self._lib = h, lib
+        self.ncells, self.coords_size = int(ncells), int(coords_size)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.sfk_mesh_destroy(h)
+            self._h = None
+
+    def upload(self, coords_ptr):
+        """Asynchronous H2D of the coordinates (host pointer, ideally pinned);
+        later evaluate_host calls are ordered after it."""
+        _check(self._lib.sfk_mesh_upload(self._h, coords_ptr))
+
+    def device_coords(self):
+        """Device address of the [ncells][coords_size] coordinates."""
+        return self._lib.sfk_mesh_coords(self._h)
+
+    def evaluate_host_ptrs(self, plan, a_ptr, w0_ptr, w1_ptr=None, first_cell=0, ncells=None,
+                           chunk_cells=0, wait=True):
+        n = self.ncells - first_cell if ncells is None else ncells
+        _check(self._lib.sfk_eval_host_mesh(native_plan(plan), self._h, int(first_cell), int(n),
+                                            a_ptr, w0_ptr, w1_ptr, int(chunk_cells),
+                                            1 if wait else 0))
+
+
 def sum_squares(x, workspace=None, stream=None):
     """(sum x^2, sum x) of a CUDA float64 tensor, as a 2-element CUDA tensor
     (device-side, stream-ordered; no host sync)."""
@@ -396,7 +446,7 @@ def sum_squares(x, workspace=None, stream=None):
 
 # Kernel-variant names of option "c2_kernel" (sfk_options.h OPT_C2_KERNEL).
 C2_KERNELS = {"auto": 0, "v1": 1, "v2": 2, "v3": 3, "tc": 4, "cell": 5, "v4": 6, "v5": 7,
-              "cellv": 8, "v6": 10, "tc8c": 11, "v6r": 12}
+              "cellv": 8, "v6": 10, "tc8c": 11}
 
 
 def set_option(name, value):
