@@ -47,6 +47,8 @@ def main():
     lib = runtime.load_library()
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_rd = torch.zeros(32 << 20, dtype=torch.float64, device=dev)
+    flush_acc = torch.empty((), dtype=torch.float64, device=dev)
     dfma, dmma = runtime.fp64_peak(0.5)
     p64 = max(dfma, dmma)
     peaks = {}
@@ -61,7 +63,8 @@ def main():
         torch.cuda.synchronize()
         ts = []
         for _ in range(args.reps):
-            flush.zero_()
+            flush.zero_()   # write + read: a clean L2 (bench.py --flush clean)
+            torch.sum(flush_rd, dim=0, out=flush_acc)
             torch.cuda._sleep(2_000_000)   # host launch latency off the timed events
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
