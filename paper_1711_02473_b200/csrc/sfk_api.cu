@@ -73,10 +73,6 @@ static int launch_c2(const sfk_plan* p, int64_t ncells, double* A, const double*
   int v = c2_variant();
   if (v == 0) v = c2_auto(p->n);
   int rc = SFK_EUNSUPPORTED;
-  if (v == 12) {
-    rc = launch_hex_action_tc9c(p, ncells, A, coords, w0, s);
-    if (rc == SFK_EUNSUPPORTED) v = c2_auto(p->n);
-  }
   if (v == 11) {
     rc = launch_hex_action_tc8c(p, ncells, A, coords, w0, s);
     if (rc == SFK_EUNSUPPORTED) v = c2_auto(p->n);

@@ -129,8 +129,6 @@ int launch_hex_action_cell(const sfk_plan* p, int64_t ncells, double* A, const d
                            const double* w0, cudaStream_t s);
 int launch_hex_action_v5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, cudaStream_t s);
-int launch_hex_action_tc9c(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                           const double* w0, cudaStream_t s);
 int launch_hex_action_tc8c(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                            const double* w0, cudaStream_t s);
 int launch_hex_action_v6(const sfk_plan* p, int64_t ncells, double* A, const double* coords,

@@ -14,7 +14,7 @@
 namespace sfk {
 
 enum Option : int {
-  OPT_C2_KERNEL,     // C2 generation: 1 v1, 2 v2, 3 v3, 4 tc, 5 cell(p1), 6 v4, 7 v5, 8 cellv, 10 v6, 11 tc8c, 12 tc9c
+  OPT_C2_KERNEL,     // C2 generation: 1 v1, 2 v2, 3 v3, 4 tc, 5 cell(p1), 6 v4, 7 v5, 8 cellv, 10 v6, 11 tc8c
   OPT_C2_G,          // v5 output group size
   OPT_V5_CPB6,       // v5 cells per CTA at n = 6 (8 = the pair-free 288-thread variant)
   OPT_C2_R,          // v2 lines per thread

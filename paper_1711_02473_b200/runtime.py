@@ -446,7 +446,7 @@ def sum_squares(x, workspace=None, stream=None):
 
 # Kernel-variant names of option "c2_kernel" (sfk_options.h OPT_C2_KERNEL).
 C2_KERNELS = {"auto": 0, "v1": 1, "v2": 2, "v3": 3, "tc": 4, "cell": 5, "v4": 6, "v5": 7,
-              "cellv": 8, "v6": 10, "tc8c": 11, "tc9c": 12}
+              "cellv": 8, "v6": 10, "tc8c": 11}
 
 
 def set_option(name, value):

@@ -408,7 +408,7 @@ def test_c2_every_kernel_generation(cuda, p):
     plan = compile_kernel("action_laplace", "hex", p)
     inp = workloads.c2_inputs(p, dims=(5, 5, 7))
     ref = cpu.evaluate(plan, inp)
-    gens = [(g, 0) for g in ("v1", "v2", "v3", "v4", "tc", "cell", "v5", "cellv", "v6", "tc8c", "tc9c")]
+    gens = [(g, 0) for g in ("v1", "v2", "v3", "v4", "tc", "cell", "v5", "cellv", "v6", "tc8c")]
     gens += [("v5", g) for g in (1, 2, 3)]
     for gen, g in gens:
         with runtime.options(c2_kernel=runtime.C2_KERNELS[gen], c2_g=g):

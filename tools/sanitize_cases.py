@@ -53,7 +53,7 @@ def c1():
 
 
 def c2():
-    gens = ["v1", "v2", "v3", "v4", "tc", "cell", "v5", "cellv", "v6", "tc8c", "tc9c"]
+    gens = ["v1", "v2", "v3", "v4", "tc", "cell", "v5", "cellv", "v6", "tc8c"]
     for p in range(1, 9):
         pl = compile_kernel("action_laplace", "hex", p)
         inp = workloads.c2_inputs(p, dims=(3, 3, 5))
