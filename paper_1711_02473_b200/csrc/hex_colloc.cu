@@ -109,6 +109,22 @@ __host__ __device__ constexpr int colloc_minb(int n) {
 // WARPS > 0: warp-synchronous mode for n <= 5 — each warp owns CPB whole
 // cells (CPB * n^2 <= 32 lines) in its own shared-memory slice and the
 // phases sync with __syncwarp instead of CTA barriers.
+struct C3Arr {
+  int sx, sy, cs;
+};
+// Per-n strides of the GX (x- and z-line accesses) and GY (y- and z-line)
+// arrays, from tools/c3_layout.py (half-warp bank model of hex_colloc.cu's
+// lane mapping): modelled wavefronts at n = 6 / 7 / 9 / 11 (GX + GY)
+// 252 / 218 / 188 / 188 -> 180 / 136 / 132 / 158.  Other n keep U's layout.
+__host__ __device__ constexpr C3Arr c3_gx(int n, int sx, int sy, int cs) {
+  return n == 7 ? C3Arr{49, 7, 343} : n == 9 ? C3Arr{81, 9, 729}
+       : n == 11 ? C3Arr{121, 11, 1331} : C3Arr{sx, sy, cs};
+}
+__host__ __device__ constexpr C3Arr c3_gy(int n, int sx, int sy, int cs) {
+  return n == 6 ? C3Arr{6, 41, 244} : n == 7 ? C3Arr{7, 49, 353} : n == 9 ? C3Arr{9, 81, 737}
+       : C3Arr{sx, sy, cs};
+}
+
 template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS = false, int WARPS = 0>
 __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
                                             const double* __restrict__ coords,
@@ -118,6 +134,13 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
                                             const int* __restrict__ cmap) {
   using C = CollocCfg<N, CPB, SY, SX, CS>;
   constexpr int NN = C::NN, N3 = C::N3;
+  // GX / GY get their own strides (x/z- and y/z-accessed arrays, chosen by
+  // tools/c3_layout.py's bank model); U keeps (SX, SY, CS)
+  constexpr int GXX = c3_gx(N, SX, SY, CS).sx, GXY = c3_gx(N, SX, SY, CS).sy,
+                GXC = c3_gx(N, SX, SY, CS).cs;
+  constexpr int GYX = c3_gy(N, SX, SY, CS).sx, GYY = c3_gy(N, SX, SY, CS).sy,
+                GYC = c3_gy(N, SX, SY, CS).cs;
+  static_assert(GXC <= CS && GYC <= CS, "GX / GY must fit the CS-strided buffers");
   constexpr bool SPLITZ = colloc_splitz(N);
   constexpr bool PERSIST = C::persist(WARPS);
   constexpr bool KG = WEIGHTED && colloc_kg(N) && !PERSIST;
@@ -188,7 +211,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
         double g = T.D[q] * ul[0];
   #pragma unroll
         for (int i = 1; i < N; ++i) g = fma(T.D[i * N + q], ul[i], g);
-        sGX[cb + q * SX + a * SY + b] = g;
+        sGX[c * GXC + q * GXX + a * GXY + b] = g;
       }
   #pragma unroll
       for (int i = 0; i < N; ++i) ul[i] = sU[cb + a * SX + i * SY + b];
@@ -197,7 +220,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
         double g = T.D[q] * ul[0];
   #pragma unroll
         for (int i = 1; i < N; ++i) g = fma(T.D[i * N + q], ul[i], g);
-        sGY[cb + a * SX + q * SY + b] = g;
+        sGY[c * GYC + a * GYX + q * GYY + b] = g;
       }
     }
     if (WEIGHTED && !PERSIST) cp_async_wait<0>();   // kappa copies of this thread landed
@@ -212,6 +235,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
     // in the same order per output (bit-identical to the fused loop).
     if (SPLITZ && act) {
       const int base = cb + a * SX + b * SY;
+      const int bx = c * GXC + a * GXX + b * GXY, by = c * GYC + a * GYX + b * GYY;
       {
         double ul[N];
   #pragma unroll
@@ -231,14 +255,14 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
         const double* kp = KG ? kappa + (cell0 + c) * N3 + a * NN + b * N : sK + base;
   #pragma unroll 1
         for (int q = 0; q < N; ++q) {
-          double gx = sGX[base + q], gy = sGY[base + q], gz = sU[base + q];
+          double gx = sGX[bx + q], gy = sGY[by + q], gz = sU[base + q];
           double r0[3], r1[3], r2[3];
           const double det = geo.adj(T.Bc[N + q], r0, r1, r2);
           double s = (wxy * T.W[q]) * rcp64(fabs(det));
           if (WEIGHTED) s *= KG ? __ldg(kp + q) : kp[q];
           laplace_flux(r0, r1, r2, s, gx, gy, gz);
-          sGX[base + q] = gx;
-          sGY[base + q] = gy;
+          sGX[bx + q] = gx;
+          sGY[by + q] = gy;
           sU[base + q] = gz;
         }
       }
@@ -257,6 +281,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
     }
     if (!SPLITZ && act) {
       const int base = cb + a * SX + b * SY;
+      const int bx = c * GXC + a * GXX + b * GXY, by = c * GYC + a * GYX + b * GYY;
       double ul[N], az[N];
   #pragma unroll
       for (int i = 0; i < N; ++i) {
@@ -276,7 +301,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
         double gz = T.D[q] * ul[0];
   #pragma unroll
         for (int i = 1; i < N; ++i) gz = fma(T.D[i * N + q], ul[i], gz);
-        double gx = sGX[base + q], gy = sGY[base + q];
+        double gx = sGX[bx + q], gy = sGY[by + q];
         double r0[3], r1[3], r2[3];
         double det;
         if constexpr (N == 15 || N == 16) det = geo.adj(T.Bc[q], T.Bc[N + q], r0, r1, r2);
@@ -284,8 +309,8 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
         double s = (wxy * T.W[q]) * rcp64(fabs(det));
         if (WEIGHTED) s *= KG ? __ldg(kp + q) : kp[q];
         laplace_flux(r0, r1, r2, s, gx, gy, gz);
-        sGX[base + q] = gx;
-        sGY[base + q] = gy;
+        sGX[bx + q] = gx;
+        sGY[by + q] = gy;
   #pragma unroll
         for (int i = 0; i < N; ++i) az[i] = fma(T.D[i * N + q], gz, az[i]);
       }
@@ -298,7 +323,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
     if (act) {
       double fl[N];
   #pragma unroll
-      for (int q = 0; q < N; ++q) fl[q] = sGX[cb + q * SX + a * SY + b];
+      for (int q = 0; q < N; ++q) fl[q] = sGX[c * GXC + q * GXX + a * GXY + b];
   #pragma unroll
       for (int i = 0; i < N; ++i) {
         double s = T.D[i * N] * fl[0];
@@ -313,7 +338,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
     if (act) {
       double fl[N];
   #pragma unroll
-      for (int q = 0; q < N; ++q) fl[q] = sGY[cb + a * SX + q * SY + b];
+      for (int q = 0; q < N; ++q) fl[q] = sGY[c * GYC + a * GYX + q * GYY + b];
   #pragma unroll
       for (int i = 0; i < N; ++i) {
         double s = T.D[i * N] * fl[0];
