@@ -64,16 +64,25 @@ __device__ __forceinline__ double neo_log(double J) {
   return log(J);
 }
 
+// X-array q-stride and per-cell Y padding from tools/c4_layout.py's bank
+// model (x-line writes / y-line reads of X: n = 4..7 modelled wavefronts
+// 40 / 40 / 50 / 30 -> 24 / 30 / 34 / 16 with PX 17 / 25 / 37 / 49 ->
+// 20 / 37 / 38 / 55; Y cell pad 8 at n = 4, 6: 84 -> 62, 102 -> 90).
+__host__ __device__ constexpr int neo_px(int n) {
+  return n == 4 ? 20 : n == 5 ? 37 : n == 6 ? 38 : n == 7 ? 55 : (n * n) | 1;
+}
+__host__ __device__ constexpr int neo_ypad(int n) { return (n == 4 || n == 6) ? 8 : 0; }
+
 template <int N, int M, int CPB>
 struct NeoCfg {
   static constexpr int NN = N * N, MN = M * N, MM = M * M;
   static constexpr int THREADS = round_up(CPB * MM, 32);
-  static constexpr int PX = NN | 1;
+  static constexpr int PX = neo_px(N);
   static constexpr int LZ = M | 1;             // z-line stride (>= m, odd)
   static constexpr int XA = M * PX;            // one X/R array per cell
   static constexpr int XSZ = 2 * XA;
   static constexpr int YA = MM * LZ;           // one Y array per cell
-  static constexpr int YSZ = 9 * YA;
+  static constexpr int YSZ = 9 * YA + neo_ypad(N);
   static constexpr int USZ = round_up(CPB * 3 * N * N * N + 1, 2);   // u of one batch
   static constexpr int CSZ = CPB * 24;
   static constexpr size_t SMEM =
