@@ -113,16 +113,16 @@ struct C3Arr {
   int sx, sy, cs;
 };
 // Per-n strides of the GX (x- and z-line accesses) and GY (y- and z-line)
-// arrays, from tools/c3_layout.py (half-warp bank model of hex_colloc.cu's
-// lane mapping): modelled wavefronts at n = 6 / 7 / 9 / 11 (GX + GY)
-// 252 / 218 / 188 / 188 -> 180 / 136 / 132 / 158.  Other n keep U's layout.
+// arrays (tools/c3_layout.py's half-warp bank model of this lane mapping).
+// Measured same-box A/B against U's layout for both (profiles/r02aa_c3*):
+// n = 6 GY 2.2% faster (kept); n = 7, 9, 11 within +-1% (the bank model's
+// 20-30% fewer wavefronts do not show: C3 is not shared-memory bound), kept
+// on U's layout.
 __host__ __device__ constexpr C3Arr c3_gx(int n, int sx, int sy, int cs) {
-  return n == 7 ? C3Arr{49, 7, 343} : n == 9 ? C3Arr{81, 9, 729}
-       : n == 11 ? C3Arr{121, 11, 1331} : C3Arr{sx, sy, cs};
+  return (void)n, C3Arr{sx, sy, cs};
 }
 __host__ __device__ constexpr C3Arr c3_gy(int n, int sx, int sy, int cs) {
-  return n == 6 ? C3Arr{6, 41, 244} : n == 7 ? C3Arr{7, 49, 353} : n == 9 ? C3Arr{9, 81, 737}
-       : C3Arr{sx, sy, cs};
+  return n == 6 ? C3Arr{6, 41, 244} : C3Arr{sx, sy, cs};
 }
 
 template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS = false, int WARPS = 0>
