@@ -379,6 +379,14 @@ int launch_hex_action_gs(const sfk_plan* p, int64_t ncells, const int* cmap, con
                          double* y, const double* coords, cudaStream_t s) {
   const bool force_v3 = option(OPT_C2G_KERNEL) == 3;
   const bool force_v2 = option(OPT_C2G_KERNEL) == 2;
+  // round 2: the collocation-derivative kernels with fused gather / scatter
+  // (v6 at n = 4..7, 9; tc8c at n = 8) unless option c2g_kernel picks a
+  // round-1 generation (1 = round 1 selection below)
+  if (option(OPT_C2G_KERNEL) == 0 && p->n == p->m) {
+    int rc = p->n == 8 ? launch_hex_action_tc8c_gs(p, ncells, cmap, x, y, coords, s)
+                       : launch_hex_action_v6_gs(p, ncells, cmap, x, y, coords, s);
+    if (rc != SFK_EUNSUPPORTED) return rc;
+  }
   if (!force_v3 && p->n == p->m) {
     if (p->n == 2 && (reinterpret_cast<uintptr_t>(cmap) & 15) == 0)   // int4 map loads
       return launch_hex_action_p1_gs(p, ncells, cmap, x, y, coords, s);

@@ -81,11 +81,15 @@ __device__ __forceinline__ int aS(int a, int b, int c) { return a * 68 + b * 8 +
 __device__ __forceinline__ int aU(int a, int b, int c) { return a * 68 + b * 8 + c; }
 }  // namespace tc8c
 
-template <int MINB, bool AU>
+// GS: global operator y += sum_c P_c^T A_c P_c x: the cell's dof map
+// (int32) is double-buffered in the u staging area (so not with AU), x is
+// gathered through it in stage A and y scatter-added in stage I.
+template <int MINB, bool AU, bool GS = false>
 __global__ void __launch_bounds__(tc8c::THREADS, MINB)
 hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
                         const double* __restrict__ coords, const double* __restrict__ u,
-                        double* __restrict__ A) {
+                        double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
+  static_assert(!(GS && AU), "GS keeps the map through stage I: own staging area");
   using namespace tc8c;
   extern __shared__ __align__(16) double smem[];
   double* S1 = smem;
@@ -119,7 +123,12 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
   // each warp stages its own cell: u (ix-planes at stride 68) and coords
   auto prefetch = [&](int64_t bt, int buf) {
     const int64_t cg = bt * CPB + warp;
-    if (cg < ncells) {
+    if (GS && cg < ncells) {
+      int* m = reinterpret_cast<int*>(sU + warp * US) + buf * N3;
+#pragma unroll
+      for (int k = 0; k < N3 / 32; ++k) cp_async4(m + lane + 32 * k, cmap + cg * N3 + lane + 32 * k);
+      if (lane < 24) cp_async8(sCo + buf * CSZ + warp * 24 + lane, coords + cg * 24 + lane);
+    } else if (cg < ncells) {
       const double* src = u + cg * N3;
       double* du = sU + warp * US;
       if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
@@ -145,6 +154,7 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
     cp_async_wait<0>();
     __syncwarp();
     const int c = warp;
+    const int* smap = reinterpret_cast<const int*>(sU + warp * US) + cur * N3;   // GS
 
     // ---- A: x, D-form; tile (c, iy), lines iz: P = B_x u ------------------
     {
@@ -153,8 +163,13 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       for (int j = 0; j < TPW; ++j) {
         const int t = j, iy = t & 7;
         const double* in = sU + c * US;
-        f[j][0] = in[aU(kq, iy, gq)];
-        f[j][1] = in[aU(4 + kq, iy, gq)];
+        if (GS) {   // dof (ix, iy, iz) = ix*64 + iy*8 + iz, gathered through the map
+          f[j][0] = c < ncb ? __ldg(u + smap[kq * NN + iy * 8 + gq]) : 0.0;
+          f[j][1] = c < ncb ? __ldg(u + smap[(4 + kq) * NN + iy * 8 + gq]) : 0.0;
+        } else {
+          f[j][0] = in[aU(kq, iy, gq)];
+          f[j][1] = in[aU(4 + kq, iy, gq)];
+        }
       }
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
@@ -408,7 +423,10 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int t = j, iy = t & 7;
-        if (c < ncb) {   // (warp-uniform)
+        if (GS && c < ncb) {
+          atomicAdd(A + smap[gq * NN + iy * 8 + 2 * kq], o[j][0]);
+          atomicAdd(A + smap[gq * NN + iy * 8 + 2 * kq + 1], o[j][1]);
+        } else if (c < ncb) {   // (warp-uniform)
           // D: ix = gq, iz = 2kq + h -> A[cell][ix*64 + iy*8 + iz]
           double* ap = A + (cell0 + c) * N3 + gq * NN + iy * 8 + 2 * kq;
           if ((reinterpret_cast<uintptr_t>(ap) & 15) == 0) {
@@ -453,9 +471,38 @@ int launch_hex_action_tc8c(const sfk_plan* p, int64_t ncells, double* A, const d
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
   const int64_t resident = sh.resident();
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
-  kern<<<grid, THREADS, smem, s>>>(T, ncells, coords, w0, A);
+  kern<<<grid, THREADS, smem, s>>>(T, ncells, coords, w0, A, nullptr);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_tc8c launch");
+}
+
+// Global operator (fused gather / scatter) at n = 8: the map needs its own
+// staging area, so 2 CTAs per SM (non-AU layout).
+int launch_hex_action_tc8c_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                              double* y, const double* coords, cudaStream_t s) {
+  if (p->n != 8 || p->m != 8 || !p->has_ct) return SFK_EUNSUPPORTED;
+  using namespace tc8c;
+  auto kern = hex_laplace_action_tc8c<2, false, true>;
+  const size_t smem = smem_bytes(false);
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)kern, THREADS, smem, "hex_action_tc8c_gs", &sh, true))
+    return rc_;
+  TabsTC8C T;
+  for (int i = 0; i < 64; ++i) {
+    T.B[i] = p->B[i];
+    T.C[i] = p->Ct[i];
+  }
+  for (int q = 0; q < 8; ++q) {
+    T.W[q] = p->wq[q];
+    T.Bc[q] = p->Bc[q];
+    T.Bc[8 + q] = p->Bc[8 + q];
+  }
+  const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  const int64_t resident = sh.resident();
+  const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
+  kern<<<grid, THREADS, smem, s>>>(T, ncells, coords, x, y, cmap);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "hex_laplace_action_tc8c_gs launch");
 }
 
 }  // namespace sfk

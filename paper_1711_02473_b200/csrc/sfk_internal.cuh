@@ -129,6 +129,10 @@ int launch_hex_action_cell(const sfk_plan* p, int64_t ncells, double* A, const d
                            const double* w0, cudaStream_t s);
 int launch_hex_action_v5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, cudaStream_t s);
+int launch_hex_action_v6_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                            double* y, const double* coords, cudaStream_t s);
+int launch_hex_action_tc8c_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                              double* y, const double* coords, cudaStream_t s);
 int launch_hex_action_tc8c(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                            const double* w0, cudaStream_t s);
 int launch_hex_action_v6(const sfk_plan* p, int64_t ncells, double* A, const double* coords,

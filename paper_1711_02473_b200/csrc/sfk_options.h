@@ -20,7 +20,7 @@ enum Option : int {
   OPT_C2_R,          // v2 lines per thread
   OPT_C2_ROLL,       // v2 pointwise loop rolling
   OPT_C2G_SMALL,     // 3: global operator at p = 2, 3 through v3
-  OPT_C2G_KERNEL,    // 2 / 3: global operator forced through v2 / v3
+  OPT_C2G_KERNEL,    // global operator: 0 v6 / tc8c, 1 round-1 selection, 2 / 3 forced v2 / v3
   OPT_CELL_TH,       // cellv threads per CTA
   OPT_CELL_MINB,     // cellv min CTAs per SM
   OPT_COLLOC_WARPS,  // C3 warp-synchronous variant: warps per CTA, -1 = off

@@ -265,10 +265,11 @@ def test_csr_dmma_epilogue_opt_in(cuda):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("gen", [2, 3])
+@pytest.mark.parametrize("gen", [1, 2, 3])
 def test_gather_scatter_alternative_generations(cuda, gen):
     """The global operator through the older kernel generations (option
-    c2g_kernel = 2 / 3; the default is v5 at p = 5, 6, 8) agrees with the
+    c2g_kernel = 1: the round-1 selection, 2 / 3: forced v2 / v3; the
+    default is the collocation-derivative v6 / tc8c) agrees with the
     assembled oracle too."""
     from paper_1711_02473_b200 import runtime
 
