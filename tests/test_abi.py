@@ -59,3 +59,18 @@ def test_error_paths_without_gpu():
     assert lib.sfk_eval(h, 0, None, None, None, None, None) == 0
     with pytest.raises(NativeError):
         runtime._check(1)
+
+
+def test_mesh_error_paths_without_gpu():
+    """sfk_mesh_* validate before touching the device (include/sfk.h)."""
+    lib = runtime.load_library()
+    out = ctypes.c_void_p()
+    assert lib.sfk_mesh_create(10, 7, ctypes.byref(out)) == 1          # coords_size 24 or 8
+    assert lib.sfk_mesh_create(-1, 24, ctypes.byref(out)) == 1
+    assert lib.sfk_mesh_create(10, 24, None) == 1
+    assert lib.sfk_mesh_upload(None, None) == 1
+    assert lib.sfk_mesh_coords(None) is None
+    assert lib.sfk_mesh_destroy(None) == 0
+    plan = compile_kernel("action_laplace", "hex", 2)
+    h = runtime.native_plan(plan)
+    assert lib.sfk_eval_host_mesh(h, None, 0, 1, None, None, None, 0, 1) == 1
