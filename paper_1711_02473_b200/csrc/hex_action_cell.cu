@@ -33,6 +33,12 @@
 
 namespace sfk {
 
+// TabsBD plus the collocation derivative C = B^-1 D (CD variant)
+template <int N>
+struct TabsCell : TabsBD<N, N> {
+  double C[N * N];   // C[q'*N + q]
+};
+
 template <int N>
 struct CellCfg {
   static constexpr int N3 = N * N * N;
@@ -43,9 +49,13 @@ struct CellCfg {
 // item 1): `u` is x, `A` is y; the CTA's block of the cell -> dof map
 // (int32, contiguous) is staged in the u area, each thread gathers its
 // cell's x values through it and scatter-adds its results with fp64 atomics.
-template <int N, int TH, int MINB, bool GS = false>
+// CD: the collocation-derivative form of phases (A) and (C) (v6's schedule
+// inside the slice loops): per slice Bx, By, then C_x, C_y on the interpolated
+// slice (108 instead of 135 FMA per slice and direction); phase (B) is
+// unchanged (gz = D_z BB etc., since C_y B_y = D_y).
+template <int N, int TH, int MINB, bool GS = false, bool CD = false>
 __global__ void __launch_bounds__(TH, MINB)
-hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
+hex_laplace_action_cell(const __grid_constant__ TabsCell<N> T, int64_t ncells,
                         const double* __restrict__ coords, const double* __restrict__ u,
                         double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
   constexpr bool PAIRS = true;
@@ -88,7 +98,44 @@ hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
 
     // (A) forward x + y, one iz-slice at a time
 #pragma unroll
-    for (int iz = 0; iz < N; ++iz) {
+    for (int iz = 0; CD && iz < N; ++iz) {
+      double x0[M][N], q[M][M];   // Bx u [qx][iy];  By Bx u [qx][qy]
+#pragma unroll
+      for (int qx = 0; qx < M; ++qx)
+#pragma unroll
+        for (int iy = 0; iy < N; ++iy) {
+          double b = TBP(qx) * ua[iy * N + iz];
+#pragma unroll
+          for (int ix = 1; ix < N; ++ix) b = fma(TBP(ix * M + qx), ua[(ix * N + iy) * N + iz], b);
+          x0[qx][iy] = b;
+        }
+#pragma unroll
+      for (int qx = 0; qx < M; ++qx)
+#pragma unroll
+        for (int qy = 0; qy < M; ++qy) {
+          double b = TBP(qy) * x0[qx][0];
+#pragma unroll
+          for (int iy = 1; iy < N; ++iy) b = fma(TBP(iy * M + qy), x0[qx][iy], b);
+          q[qx][qy] = b;
+        }
+#pragma unroll
+      for (int qx = 0; qx < M; ++qx)
+#pragma unroll
+        for (int qy = 0; qy < M; ++qy) {
+          double gy = T.C[qy] * q[qx][0], gx = T.C[qx] * q[0][qy];
+#pragma unroll
+          for (int k = 1; k < M; ++k) {
+            gy = fma(T.C[k * M + qy], q[qx][k], gy);
+            gx = fma(T.C[k * M + qx], q[k][qy], gx);
+          }
+          const int o = (qx * M + qy) * N + iz;
+          Y[o] = q[qx][qy];      // BB
+          Y[S1 + o] = gy;        // BD = D_y B_x u
+          Y[2 * S1 + o] = gx;    // DB = B_y D_x u
+        }
+    }
+#pragma unroll
+    for (int iz = 0; !CD && iz < N; ++iz) {
       double ux[N][N];   // [ix][iy]
 #pragma unroll
       for (int ix = 0; ix < N; ++ix)
@@ -179,7 +226,53 @@ hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
     // (C) transposed y + x, one iz-slice at a time
     double* ac = A + cell * N3;
 #pragma unroll 1
-    for (int iz = 0; iz < N; ++iz) {
+    for (int iz = 0; CD && iz < N; ++iz) {
+      // t = C_x^T Sx + C_y^T Sy + Sz on the slice, then B_y^T, B_x^T
+      double sx[M][M], sy[M][M], t[M][M], r[M][N];
+#pragma unroll
+      for (int qx = 0; qx < M; ++qx)
+#pragma unroll
+        for (int qy = 0; qy < M; ++qy) {
+          const int o = (qx * M + qy) * N + iz;
+          t[qx][qy] = Y[o];
+          sy[qx][qy] = Y[S1 + o];
+          sx[qx][qy] = Y[2 * S1 + o];
+        }
+#pragma unroll
+      for (int qx = 0; qx < M; ++qx)
+#pragma unroll
+        for (int qy = 0; qy < M; ++qy) {
+          double v = t[qx][qy];
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            v = fma(T.C[qx * M + k], sx[k][qy], v);
+            v = fma(T.C[qy * M + k], sy[qx][k], v);
+          }
+          t[qx][qy] = v;
+        }
+#pragma unroll
+      for (int qx = 0; qx < M; ++qx)
+#pragma unroll
+        for (int iy = 0; iy < N; ++iy) {
+          double a = TBP(iy * M) * t[qx][0];
+#pragma unroll
+          for (int qy = 1; qy < M; ++qy) a = fma(TBP(iy * M + qy), t[qx][qy], a);
+          r[qx][iy] = a;
+        }
+#pragma unroll
+      for (int ix = 0; ix < N; ++ix)
+#pragma unroll
+        for (int iy = 0; iy < N; ++iy) {
+          double a = TBP(ix * M) * r[0][iy];
+#pragma unroll
+          for (int qx = 1; qx < M; ++qx) a = fma(TBP(ix * M + qx), r[qx][iy], a);
+          if (GS) atomicAdd(A + sMap[threadIdx.x * N3 + (ix * N + iy) * N + iz], a);
+          else if (STAGE) sU[threadIdx.x * N3 + (ix * N + iy) * N + iz] = a;
+          else ac[(ix * N + iy) * N + iz] = a;
+        }
+    }
+#pragma unroll 1
+    for (int iz = 0; !CD && iz < N; ++iz) {
       double r1[M][N], r2[M][N];   // [qx][iy]: By^T Sx, Dy^T Sy + By^T Sz
 #pragma unroll
       for (int qx = 0; qx < M; ++qx) {
@@ -256,16 +349,19 @@ hex_laplace_action_cell(const __grid_constant__ TabsBD<N, N> T, int64_t ncells,
   }
 }
 
-template <int N, int TH, int MINB, bool GS = false>
+template <int N, int TH, int MINB, bool GS = false, bool CD = false>
 static int launch_cell(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                        const double* u, cudaStream_t s, const int* cmap = nullptr) {
   constexpr size_t SMEM =
       (size_t)TH * (CellCfg<N>::YS + (SFK_CELL_STAGE || GS ? CellCfg<N>::N3 : 0)) * sizeof(double);
-  auto kern = hex_laplace_action_cell<N, TH, MINB, GS>;
+  if (CD && !p->has_ct) return SFK_EUNSUPPORTED;
+  auto kern = hex_laplace_action_cell<N, TH, MINB, GS, CD>;
   LaunchShape sh;
   if (const int rc_ = kernel_shape((const void*)kern, TH, SMEM, "hex_action_cell", &sh, true))
     return rc_;
-  const TabsBD<N, N> T = make_tabs_bd<N, N>(p);
+  TabsCell<N> T;
+  static_cast<TabsBD<N, N>&>(T) = make_tabs_bd<N, N>(p);
+  for (int k = 0; k < N * N; ++k) T.C[k] = p->has_ct ? p->Ct[k] : 0.0;
   const int64_t grid = (ncells + TH - 1) / TH;
   if (grid > 0) kern<<<(unsigned)grid, TH, SMEM, s>>>(T, ncells, coords, u, A, cmap);
   note_launch();
@@ -285,6 +381,8 @@ int launch_hex_action_cell(const sfk_plan* p, int64_t ncells, double* A, const d
       if (th == 128) return launch_cell<3, 128, 1>(p, ncells, A, coords, w0, s);
       if (th == 96) return launch_cell<3, 96, 1>(p, ncells, A, coords, w0, s);
       if (minb == 5) return launch_cell<3, 64, 5>(p, ncells, A, coords, w0, s);
+      if (option(OPT_V6_CFG) == 6) return launch_cell<3, 64, 1, false, true>(p, ncells, A, coords, w0, s);
+      if (option(OPT_V6_CFG) == 7) return launch_cell<3, 64, 5, false, true>(p, ncells, A, coords, w0, s);
       return launch_cell<3, 64, 1>(p, ncells, A, coords, w0, s);
     case 4:
       if (th == 64) return launch_cell<4, 64, 1>(p, ncells, A, coords, w0, s);
