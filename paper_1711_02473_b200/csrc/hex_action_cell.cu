@@ -381,9 +381,10 @@ int launch_hex_action_cell(const sfk_plan* p, int64_t ncells, double* A, const d
       if (th == 128) return launch_cell<3, 128, 1>(p, ncells, A, coords, w0, s);
       if (th == 96) return launch_cell<3, 96, 1>(p, ncells, A, coords, w0, s);
       if (minb == 5) return launch_cell<3, 64, 5>(p, ncells, A, coords, w0, s);
-      if (option(OPT_V6_CFG) == 6) return launch_cell<3, 64, 1, false, true>(p, ncells, A, coords, w0, s);
-      if (option(OPT_V6_CFG) == 7) return launch_cell<3, 64, 5, false, true>(p, ncells, A, coords, w0, s);
-      return launch_cell<3, 64, 1>(p, ncells, A, coords, w0, s);
+      // collocation-derivative slices (CD): 0.0760 -> 0.0740 ms
+      // (profiles/r02ae_cfg*.json); option v6_cfg = 6 selects the round-1 form
+      if (option(OPT_V6_CFG) == 6) return launch_cell<3, 64, 1>(p, ncells, A, coords, w0, s);
+      return launch_cell<3, 64, 1, false, true>(p, ncells, A, coords, w0, s);
     case 4:
       if (th == 64) return launch_cell<4, 64, 1>(p, ncells, A, coords, w0, s);
       return launch_cell<4, 32, 1>(p, ncells, A, coords, w0, s);
