@@ -20,11 +20,6 @@
 
 namespace sfk {
 
-// Tabs<2, 2> plus the collocation derivative C = B^-1 D (CD variant)
-struct TabsP1 : Tabs<2, 2> {
-  double C[4];   // C[q'*2 + q]
-};
-
 namespace p1 {
 constexpr int CPB = 128;             // cells (= threads) per CTA
 constexpr int CS = 26;               // padded coords stride (24 used)
@@ -35,12 +30,9 @@ constexpr size_t SMEM = (size_t)CPB * (CS + US) * sizeof(double);
 // GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
 // item 1): u = x gathered through cmap[c][0..7], A = y scatter-added with
 // fp64 atomics.
-// CD: the collocation-derivative schedule (V = B x B x B u, g = C_a V,
-// t = sum C_a^T f_a, A = B^T x B^T x B^T t): 96 + 96 instead of 128 + 128
-// contraction FP64 ops per cell.
-template <bool GS, bool CD = false>
+template <bool GS>
 __global__ void __launch_bounds__(p1::CPB, SFK_P1_MINB)
-hex_laplace_action_p1(const __grid_constant__ TabsP1 T, int64_t ncells,
+hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
                       double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
   using namespace p1;
@@ -101,84 +93,6 @@ hex_laplace_action_p1(const __grid_constant__ TabsP1 T, int64_t ncells,
       uu[2 * k + 1] = v.y;
     }
   }
-  double a[8];
-  if (CD) {
-    // V at the 8 points: x, y, z interpolation ([qx][..][..] index 4x + 2y + z)
-    double vx[8], vy[8], V[8];
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) vx[4 * q + r] = fma(T.B[2 + q], uu[4 + r], T.B[q] * uu[r]);
-#pragma unroll
-    for (int qx = 0; qx < 2; ++qx)
-#pragma unroll
-      for (int qy = 0; qy < 2; ++qy)
-#pragma unroll
-        for (int iz = 0; iz < 2; ++iz)
-          vy[4 * qx + 2 * qy + iz] = fma(T.B[2 + qy], vx[4 * qx + 2 + iz], T.B[qy] * vx[4 * qx + iz]);
-#pragma unroll
-    for (int l = 0; l < 8; l += 2)
-#pragma unroll
-      for (int qz = 0; qz < 2; ++qz) V[l + qz] = fma(T.B[2 + qz], vy[l + 1], T.B[qz] * vy[l]);
-    double gx[8], gy[8], gz[8];
-#pragma unroll
-    for (int qx = 0; qx < 2; ++qx)
-#pragma unroll
-      for (int qy = 0; qy < 2; ++qy)
-#pragma unroll
-        for (int qz = 0; qz < 2; ++qz) {
-          const int k = 4 * qx + 2 * qy + qz;
-          gx[k] = fma(T.C[2 + qx], V[4 + 2 * qy + qz], T.C[qx] * V[2 * qy + qz]);
-          gy[k] = fma(T.C[2 + qy], V[4 * qx + 2 + qz], T.C[qy] * V[4 * qx + qz]);
-          gz[k] = fma(T.C[2 + qz], V[4 * qx + 2 * qy + 1], T.C[qz] * V[4 * qx + 2 * qy]);
-        }
-#pragma unroll
-    for (int qx = 0; qx < 2; ++qx)
-#pragma unroll
-      for (int qy = 0; qy < 2; ++qy) {
-        HexLineGeom geo;
-        geo.setup(X, T.Bc[qx], T.Bc[2 + qx], T.Bc[qy], T.Bc[2 + qy]);
-        const double wxy = T.W[qx] * T.W[qy];
-        const int l = 4 * qx + 2 * qy;
-#pragma unroll
-        for (int qz = 0; qz < 2; ++qz) {
-          double r0[3], r1[3], r2[3];
-          const double det = geo.adj(T.Bc[qz], T.Bc[2 + qz], r0, r1, r2);
-          const double s = (wxy * T.W[qz]) * rcp64(fabs(det));
-          laplace_flux(r0, r1, r2, s, gx[l + qz], gy[l + qz], gz[l + qz]);
-        }
-      }
-    // t = C_x^T f_x + C_y^T f_y + C_z^T f_z   (C^T f)[q'] = sum_q C[q'][q] f[q]
-    double t[8];
-#pragma unroll
-    for (int qx = 0; qx < 2; ++qx)
-#pragma unroll
-      for (int qy = 0; qy < 2; ++qy)
-#pragma unroll
-        for (int qz = 0; qz < 2; ++qz) {
-          const int k = 4 * qx + 2 * qy + qz;
-          double v = fma(T.C[2 * qx + 1], gx[4 + 2 * qy + qz], T.C[2 * qx] * gx[2 * qy + qz]);
-          v = fma(T.C[2 * qy + 1], gy[4 * qx + 2 + qz], fma(T.C[2 * qy], gy[4 * qx + qz], v));
-          t[k] = fma(T.C[2 * qz + 1], gz[4 * qx + 2 * qy + 1], fma(T.C[2 * qz], gz[4 * qx + 2 * qy], v));
-        }
-    // B_z^T, B_y^T, B_x^T
-    double sz[8], sy[8];
-#pragma unroll
-    for (int l = 0; l < 8; l += 2)
-#pragma unroll
-      for (int iz = 0; iz < 2; ++iz) sz[l + iz] = fma(T.B[2 * iz + 1], t[l + 1], T.B[2 * iz] * t[l]);
-#pragma unroll
-    for (int qx = 0; qx < 2; ++qx)
-#pragma unroll
-      for (int iy = 0; iy < 2; ++iy)
-#pragma unroll
-        for (int iz = 0; iz < 2; ++iz)
-          sy[4 * qx + 2 * iy + iz] = fma(T.B[2 * iy + 1], sz[4 * qx + 2 + iz], T.B[2 * iy] * sz[4 * qx + iz]);
-#pragma unroll
-    for (int ix = 0; ix < 2; ++ix)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) a[4 * ix + r] = fma(T.B[2 * ix + 1], sy[4 + r], T.B[2 * ix] * sy[r]);
-  } else {
   // dof / point index (x, y, z) -> 4x + 2y + z;  tables T.B[i*2+q], T.D[i*2+q]
   // forward: g_x = Dx By Bz u, g_y = Bx Dy Bz u, g_z = Bx By Dz u at 8 points
   double bx[8], dx[8];   // [qx][iy][iz]
@@ -248,6 +162,7 @@ hex_laplace_action_p1(const __grid_constant__ TabsP1 T, int64_t ncells,
         r2[o] = fma(T.B[2 * iy + 1], sz[a1], fma(T.B[2 * iy], sz[a0], r2[o]));
       }
   // transposed x: A = Dx^T r1 + Bx^T r2
+  double a[8];
 #pragma unroll
   for (int ix = 0; ix < 2; ++ix)
 #pragma unroll
@@ -258,7 +173,6 @@ hex_laplace_action_p1(const __grid_constant__ TabsP1 T, int64_t ncells,
       v = fma(T.B[2 * ix + 1], r2[4 + r], v);
       a[4 * ix + r] = v;
     }
-  }
   if (GS) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) atomicAdd(A + gm[k], a[k]);
@@ -274,27 +188,23 @@ hex_laplace_action_p1(const __grid_constant__ TabsP1 T, int64_t ncells,
   }
 }
 
-template <bool GS, bool CD = false>
+template <bool GS>
 static int launch_p1(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                      const double* w0, cudaStream_t s, const int* cmap) {
   if (p->n != 2 || p->m != 2) return SFK_EUNSUPPORTED;
   LaunchShape sh;
-  if (CD && !p->has_ct) return SFK_EUNSUPPORTED;
-  if (const int rc_ = kernel_shape((const void*)hex_laplace_action_p1<GS, CD>, p1::CPB, p1::SMEM,
+  if (const int rc_ = kernel_shape((const void*)hex_laplace_action_p1<GS>, p1::CPB, p1::SMEM,
                                    "hex_action_p1", &sh))
     return rc_;
-  TabsP1 T;
-  static_cast<Tabs<2, 2>&>(T) = make_tabs<2, 2>(p);
-  for (int k = 0; k < 4; ++k) T.C[k] = p->has_ct ? p->Ct[k] : 0.0;
+  const Tabs<2, 2> T = make_tabs<2, 2>(p);
   const unsigned grid = (unsigned)((ncells + p1::CPB - 1) / p1::CPB);
-  hex_laplace_action_p1<GS, CD><<<grid, p1::CPB, p1::SMEM, s>>>(T, ncells, coords, w0, A, cmap);
+  hex_laplace_action_p1<GS><<<grid, p1::CPB, p1::SMEM, s>>>(T, ncells, coords, w0, A, cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_p1 launch");
 }
 
 int launch_hex_action_p1(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, cudaStream_t s) {
-  if (option(OPT_V6_CFG) == 6) return launch_p1<false, true>(p, ncells, A, coords, w0, s, nullptr);
   return launch_p1<false>(p, ncells, A, coords, w0, s, nullptr);
 }
 
