@@ -223,29 +223,6 @@ __device__ __forceinline__ double hex_cell_lg(const double* X, const double* Bc,
   return fma(fh, b1, fl * b0);
 }
 
-// Row `row` (0..17) of the same table — part = row / 6, (hi, k) = divmod(row
-// % 6, 3) — for every q: the two edge differences once, then n products.
-// Identical operations to hex_cell_lg, without per-entry index arithmetic.
-template <int N>
-__device__ __forceinline__ void hex_cell_lg_row(const double* X, const double* Bc, int row,
-                                                double* LG) {
-  const int part = row / 6, j = row - 6 * part, hi = j / 3, k = j - 3 * hi;
-  double lo, up;
-  if (part == 0) {
-    lo = X[3 * (4 + hi) + k] - X[3 * hi + k];                 // e00 (cz = hi)
-    up = X[3 * (6 + hi) + k] - X[3 * (2 + hi) + k];           // e01
-  } else if (part == 1) {
-    lo = X[3 * (2 + hi) + k] - X[3 * hi + k];                 // e10
-    up = X[3 * (6 + hi) + k] - X[3 * (4 + hi) + k];           // e11
-  } else {
-    lo = X[3 * (4 * hi + 1) + k] - X[3 * (4 * hi) + k];       // f(a = hi, 0)
-    up = X[3 * (4 * hi + 3) + k] - X[3 * (4 * hi + 2) + k];   // f(a = hi, 1)
-  }
-  double* o = LG + part * 6 * N + j;
-#pragma unroll
-  for (int q = 0; q < N; ++q) o[6 * q] = fma(up, Bc[N + q], lo * Bc[q]);
-}
-
 // f = s * R R^T g  (R rows r0, r1, r2).  In place on (g0, g1, g2).
 __device__ __forceinline__ void laplace_flux(const double r0[3], const double r1[3],
                                              const double r2[3], double s,

@@ -86,10 +86,8 @@ def schedule(n, cpb, zr=False, ws=False, eg=False):
             stages[stage].append((t, slot, addr, kind))
 
         if eg:   # per-cell line-geometry table: written in A, read in E
-            for row in range(r, 18, nn):           # hex_cell_lg_row: one row, every q
-                part, j = divmod(row, 6)
-                for q in range(n):
-                    acc("A", "GE", c * 18 * n + part * 6 * n + 6 * q + j, "w")
+            for e in range(r, 18 * n, nn):
+                acc("A", "GE", c * 18 * n + e, "w")
             for e in list(range(6 * ra, 6 * ra + 6)) + list(range(6 * n + 6 * rb, 6 * n + 6 * rb + 6)) \
                     + list(range(12 * n + 6 * ra, 12 * n + 6 * ra + 6)):
                 acc("E", "GE", c * 18 * n + e, "r")
