@@ -53,13 +53,17 @@ struct CellCfg {
 // inside the slice loops): per slice Bx, By, then C_x, C_y on the interpolated
 // slice (108 instead of 135 FMA per slice and direction); phase (B) is
 // unchanged (gz = D_z BB etc., since C_y B_y = D_y).
-template <int N, int TH, int MINB, bool GS = false, bool CD = false>
+// LG: phase (B) runs qy-outer and forms the line-geometry parts that depend
+// on one of qx, qy only once per cell instead of once per line (STAGE only:
+// the qx parts live in the thread's sU row, free between (A) and (C)).
+template <int N, int TH, int MINB, bool GS = false, bool CD = false, bool LG = false>
 __global__ void __launch_bounds__(TH, MINB)
 hex_laplace_action_cell(const __grid_constant__ TabsCell<N> T, int64_t ncells,
                         const double* __restrict__ coords, const double* __restrict__ u,
                         double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
   constexpr bool PAIRS = true;
   constexpr bool STAGE = SFK_CELL_STAGE || GS;
+  constexpr bool LGS = LG && STAGE && !GS;
   constexpr int M = N, N3 = CellCfg<N>::N3, YS = CellCfg<N>::YS;
   constexpr int S1 = N3;                           // slot stride in Y
   extern __shared__ double smem[];
@@ -174,10 +178,8 @@ hex_laplace_action_cell(const __grid_constant__ TabsCell<N> T, int64_t ncells,
     }
 
     // (B) z-lines: gradients, pointwise flux, transposed z, in place
-#pragma unroll 1
-    for (int l = 0; l < M * M; ++l) {
-      const int qx = l / M, qy = l - qx * M;
-      double* yl = Y + l * N;
+    auto z_line = [&](int qx, int qy, const HexLineAdj& geo) {
+      double* yl = Y + (qx * M + qy) * N;
       double bb[N], bd[N], db[N];
 #pragma unroll
       for (int i = 0; i < N; ++i) {
@@ -198,8 +200,6 @@ hex_laplace_action_cell(const __grid_constant__ TabsCell<N> T, int64_t ncells,
           gx[q] = fma(TBP(i * M + q), db[i], gx[q]);
         }
       }
-      HexLineAdj geo;
-      geo.setup(X, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
       const double wxy = T.W[qx] * T.W[qy];
 #pragma unroll
       for (int q = 0; q < M; ++q) {
@@ -220,6 +220,60 @@ hex_laplace_action_cell(const __grid_constant__ TabsCell<N> T, int64_t ncells,
         yl[i] = sz;
         yl[S1 + i] = sy;
         yl[2 * S1 + i] = sx;
+      }
+    };
+    if (LGS) {
+      // line geometry shared between lines: col1's polynomial (B, dB) per qx
+      // in this thread's free sU row, col0's (A, dA) and col2's partial sums
+      // per qy in registers — the operations of HexLineAdj::setup, formed 3
+      // instead of 9 times (bit-identical)
+      double* lgx = sU + threadIdx.x * N3;
+#pragma unroll
+      for (int qx = 0; qx < M; ++qx) {
+        const double bx0 = T.Bc[qx], bx1 = T.Bc[M + qx];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double a0 = fma(X[3 * 6 + k] - X[3 * 4 + k], bx1, (X[3 * 2 + k] - X[k]) * bx0);
+          const double a1 = fma(X[3 * 7 + k] - X[3 * 5 + k], bx1, (X[3 * 3 + k] - X[3 + k]) * bx0);
+          lgx[6 * qx + k] = a0;
+          lgx[6 * qx + 3 + k] = a1 - a0;
+        }
+      }
+#pragma unroll 1
+      for (int qy = 0; qy < M; ++qy) {
+        const double by0 = T.Bc[qy], by1 = T.Bc[M + qy];
+        double Ay[3], dAy[3], g0[3], g1[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double a0 = fma(X[3 * 6 + k] - X[3 * 2 + k], by1, (X[3 * 4 + k] - X[k]) * by0);
+          const double a1 = fma(X[3 * 7 + k] - X[3 * 3 + k], by1, (X[3 * 5 + k] - X[3 + k]) * by0);
+          Ay[k] = a0;
+          dAy[k] = a1 - a0;
+          g0[k] = fma(X[3 * 3 + k] - X[3 * 2 + k], by1, (X[3 * 1 + k] - X[k]) * by0);
+          g1[k] = fma(X[3 * 7 + k] - X[3 * 6 + k], by1, (X[3 * 5 + k] - X[3 * 4 + k]) * by0);
+        }
+#pragma unroll 1
+        for (int qx = 0; qx < M; ++qx) {
+          const double bx0 = T.Bc[qx], bx1 = T.Bc[M + qx];
+          double Bx[3], dBx[3], cc[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            Bx[k] = lgx[6 * qx + k];
+            dBx[k] = lgx[6 * qx + 3 + k];
+            cc[k] = fma(g1[k], bx1, g0[k] * bx0);
+          }
+          HexLineAdj geo;
+          geo.from_parts(Ay, dAy, Bx, dBx, cc);
+          z_line(qx, qy, geo);
+        }
+      }
+    } else {
+#pragma unroll 1
+      for (int l = 0; l < M * M; ++l) {
+        const int qx = l / M, qy = l - qx * M;
+        HexLineAdj geo;
+        geo.setup(X, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
+        z_line(qx, qy, geo);
       }
     }
 
@@ -349,13 +403,13 @@ hex_laplace_action_cell(const __grid_constant__ TabsCell<N> T, int64_t ncells,
   }
 }
 
-template <int N, int TH, int MINB, bool GS = false, bool CD = false>
+template <int N, int TH, int MINB, bool GS = false, bool CD = false, bool LG = false>
 static int launch_cell(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                        const double* u, cudaStream_t s, const int* cmap = nullptr) {
   constexpr size_t SMEM =
       (size_t)TH * (CellCfg<N>::YS + (SFK_CELL_STAGE || GS ? CellCfg<N>::N3 : 0)) * sizeof(double);
   if (CD && !p->has_ct) return SFK_EUNSUPPORTED;
-  auto kern = hex_laplace_action_cell<N, TH, MINB, GS, CD>;
+  auto kern = hex_laplace_action_cell<N, TH, MINB, GS, CD, LG>;
   LaunchShape sh;
   if (const int rc_ = kernel_shape((const void*)kern, TH, SMEM, "hex_action_cell", &sh, true))
     return rc_;
@@ -384,7 +438,10 @@ int launch_hex_action_cell(const sfk_plan* p, int64_t ncells, double* A, const d
       // collocation-derivative slices (CD): 0.0760 -> 0.0740 ms
       // (profiles/r02ae_cfg*.json); option v6_cfg = 6 selects the round-1 form
       if (option(OPT_V6_CFG) == 6) return launch_cell<3, 64, 1>(p, ncells, A, coords, w0, s);
-      return launch_cell<3, 64, 1, false, true>(p, ncells, A, coords, w0, s);
+      // line geometry shared between the cell's z-lines (LG): 0.0740 -> 0.0723 ms,
+      // bit-identical (profiles/r02am_p2_lgs*.json*); option v6_cfg = 7 drops it
+      if (option(OPT_V6_CFG) == 7) return launch_cell<3, 64, 1, false, true>(p, ncells, A, coords, w0, s);
+      return launch_cell<3, 64, 1, false, true, true>(p, ncells, A, coords, w0, s);
     case 4:
       if (th == 64) return launch_cell<4, 64, 1>(p, ncells, A, coords, w0, s);
       return launch_cell<4, 32, 1>(p, ncells, A, coords, w0, s);

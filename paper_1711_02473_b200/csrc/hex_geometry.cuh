@@ -151,8 +151,17 @@ struct HexLineAdj {
       dA[k] = g.al0[1][k] - g.al0[0][k];
       B[k] = g.al1[0][k];
       dB[k] = g.al1[1][k] - g.al1[0][k];
-      c2[k] = g.c2[k];
     }
+    from_parts(A, dA, B, dB, g.c2);
+  }
+  // From the line's column polynomials: col0 = A + t dA (A, dA depend on qy
+  // only), col1 = B + t dB (qx only), col2 = cc — callers that share A, dA
+  // (or B, dB) between the lines of a cell form them once (identical roundings).
+  __device__ __forceinline__ void from_parts(const double A[3], const double dA[3],
+                                             const double B[3], const double dB[3],
+                                             const double cc[3]) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) c2[k] = cc[k];
     HexLineGeom::cross(B, c2, P0);
     HexLineGeom::cross(dB, c2, Q0);
     HexLineGeom::cross(c2, A, P1);
