@@ -125,7 +125,8 @@ __host__ __device__ constexpr C3Arr c3_gy(int n, int sx, int sy, int cs) {
   return n == 6 ? C3Arr{6, 41, 244} : C3Arr{sx, sy, cs};
 }
 
-template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS = false, int WARPS = 0>
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS = false, int WARPS = 0,
+          bool C3_CONTIG = true>
 __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
                                             const double* __restrict__ coords,
                                             const double* __restrict__ u,
@@ -144,6 +145,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
   constexpr bool SPLITZ = colloc_splitz(N);
   constexpr bool PERSIST = C::persist(WARPS);
   constexpr bool KG = WEIGHTED && colloc_kg(N) && !PERSIST;
+  constexpr bool CONTIG = SY == N && SX == NN && CS == N3 && C3_CONTIG;
   extern __shared__ double smem[];
   constexpr int TH = WARPS ? 32 : C::THREADS;
   static_assert(!WARPS || CPB * NN <= 32, "warp mode needs CPB * n^2 <= 32");
@@ -173,20 +175,30 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
       for (int i = tid; i < CPB * 24; i += TH)
         sC[i] = i < ncb * 24 ? __ldg(coords + cell0 * 24 + i) : 0.0;
     }
-    // consecutive threads copy consecutive doubles (coalesced global reads)
+    // consecutive threads copy consecutive doubles (coalesced global reads);
+    // unpadded layouts (CONTIG) are the global order itself: 16-byte copies
+    // without the per-element (c, x, y, z) decomposition
     const double* ug = u + cell0 * N3;
-    for (int i = tid; i < ncb * N3; i += TH) {
-      const int c = i / N3, r = i - c * N3;
-      const int x = r / NN, yz = r - x * NN, y = yz / N, z = yz - y * N;
-      cp_async8(sU + c * CS + x * SX + y * SY + z, GS ? u + __ldg(cmap + cell0 * N3 + i) : ug + i);
+    if (CONTIG && !GS) {
+      async_copy<TH>(sU, ug, ncb * N3, tid);
+    } else {
+      for (int i = tid; i < ncb * N3; i += TH) {
+        const int c = i / N3, r = i - c * N3;
+        const int x = r / NN, yz = r - x * NN, y = yz / N, z = yz - y * N;
+        cp_async8(sU + c * CS + x * SX + y * SY + z, GS ? u + __ldg(cmap + cell0 * N3 + i) : ug + i);
+      }
     }
     cp_async_commit();
     if (WEIGHTED && !KG) {
       const double* kg = kappa + cell0 * N3;
-      for (int i = tid; i < ncb * N3; i += TH) {
-        const int c = i / N3, r = i - c * N3;
-        const int x = r / NN, yz = r - x * NN, y = yz / N, z = yz - y * N;
-        cp_async8(sK + c * CS + x * SX + y * SY + z, kg + i);
+      if (CONTIG) {
+        async_copy<TH>(sK, kg, ncb * N3, tid);
+      } else {
+        for (int i = tid; i < ncb * N3; i += TH) {
+          const int c = i / N3, r = i - c * N3;
+          const int x = r / NN, yz = r - x * NN, y = yz / N, z = yz - y * N;
+          cp_async8(sK + c * CS + x * SX + y * SY + z, kg + i);
+        }
       }
       cp_async_commit();
     }
@@ -353,6 +365,16 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
       // coalesced write-back: consecutive threads take consecutive elements of
       // the batch; the (c, x, y, z) decomposition is incremental per thread
       double* ag = A + cell0 * N3;
+      if (CONTIG && !GS) {
+        const int n = ncb * N3;
+        if (((reinterpret_cast<uintptr_t>(ag) | reinterpret_cast<uintptr_t>(sU)) & 15) == 0) {
+          for (int i = tid; i < n / 2; i += TH)
+            reinterpret_cast<double2*>(ag)[i] = reinterpret_cast<const double2*>(sU)[i];
+          if ((n & 1) && tid == 0) ag[n - 1] = sU[n - 1];
+        } else {
+          for (int i = tid; i < n; i += TH) ag[i] = sU[i];
+        }
+      } else
       for (int i = tid; i < ncb * N3; i += TH) {
         const int cc = i / N3, rr = i - cc * N3;
         const int x = rr / NN, yz = rr - x * NN, y = yz / N, z = yz - y * N;
@@ -390,36 +412,40 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
   (void)ngroups;
 }
 
-template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, int MINB, bool GS, int WARPS>
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, int MINB, bool GS, int WARPS,
+          int VAR>
 __global__ void __launch_bounds__(WARPS ? 32 * WARPS : CollocCfg<N, CPB, SY, SX, CS>::THREADS, MINB)
 hex_colloc_action_kernel(const __grid_constant__ TabsD<N> T, int64_t ncells,
                          const double* __restrict__ coords, const double* __restrict__ u,
                          const double* __restrict__ kappa, double* __restrict__ A,
                          const int* __restrict__ cmap) {
-  colloc_body<N, CPB, SY, SX, CS, WEIGHTED, GS, WARPS>(T, ncells, coords, u, kappa, A, cmap);
+  colloc_body<N, CPB, SY, SX, CS, WEIGHTED, GS, WARPS, (VAR & 1) == 0>(T, ncells, coords, u, kappa,
+                                                                      A, cmap);
 }
 
-template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS, int WARPS>
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS, int WARPS, int VAR>
 __global__ void __launch_bounds__(WARPS ? 32 * WARPS : CollocCfg<N, CPB, SY, SX, CS>::THREADS)
 hex_colloc_action_kernel_free(const __grid_constant__ TabsD<N> T, int64_t ncells,
                               const double* __restrict__ coords, const double* __restrict__ u,
                               const double* __restrict__ kappa, double* __restrict__ A,
                               const int* __restrict__ cmap) {
-  colloc_body<N, CPB, SY, SX, CS, WEIGHTED, GS, WARPS>(T, ncells, coords, u, kappa, A, cmap);
+  colloc_body<N, CPB, SY, SX, CS, WEIGHTED, GS, WARPS, (VAR & 1) == 0>(T, ncells, coords, u, kappa,
+                                                                      A, cmap);
 }
 
-template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS, int WARPS = 0>
+template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS, int WARPS, int VAR>
 static auto colloc_kernel() {
   constexpr int mb = colloc_minb(N);
   if constexpr (mb == 0)
-    return hex_colloc_action_kernel_free<N, CPB, SY, SX, CS, WEIGHTED, GS, WARPS>;
-  else return hex_colloc_action_kernel<N, CPB, SY, SX, CS, WEIGHTED, mb, GS, WARPS>;
+    return hex_colloc_action_kernel_free<N, CPB, SY, SX, CS, WEIGHTED, GS, WARPS, VAR>;
+  else return hex_colloc_action_kernel<N, CPB, SY, SX, CS, WEIGHTED, mb, GS, WARPS, VAR>;
 }
 
-template <int N, int CPB, int SY, int SX, int CS, bool GS = false, int WARPS = 0>
-static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
-                    const double* u, const double* kappa, cudaStream_t s,
-                    const int* cmap = nullptr) {
+// VAR bit 0 (option c3_cfg = 1, A/B only): the per-element staging copies
+// even where the shared layout is unpadded
+template <int N, int CPB, int SY, int SX, int CS, bool GS, int WARPS, int VAR>
+static int launch_nv(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                     const double* u, const double* kappa, cudaStream_t s, const int* cmap) {
   using C = CollocCfg<N, CPB, SY, SX, CS>;
   constexpr int G = WARPS ? WARPS : 1;                 // cell groups per CTA
   constexpr int THREADS = WARPS ? 32 * WARPS : C::THREADS;
@@ -434,13 +460,13 @@ static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* 
   // persistent mode: one resident wave of CTAs looping over the batches
   LaunchShape sh;
   if (kappa) {
-    auto k = colloc_kernel<N, CPB, SY, SX, CS, true, GS, WARPS>();
+    auto k = colloc_kernel<N, CPB, SY, SX, CS, true, GS, WARPS, VAR>();
     const size_t sm = G * C::smem(true, WARPS);
     if (const int rc_ = kernel_shape((const void*)k, THREADS, sm, "hex_colloc", &sh)) return rc_;
     if (C::persist(WARPS)) grid = std::min<int64_t>(grid, sh.resident());
     if (grid > 0) k<<<(unsigned)grid, THREADS, sm, s>>>(T, ncells, coords, u, kappa, A, cmap);
   } else {
-    auto k = colloc_kernel<N, CPB, SY, SX, CS, false, GS, WARPS>();
+    auto k = colloc_kernel<N, CPB, SY, SX, CS, false, GS, WARPS, VAR>();
     const size_t sm = G * C::smem(false, WARPS);
     if (const int rc_ = kernel_shape((const void*)k, THREADS, sm, "hex_colloc", &sh)) return rc_;
     if (C::persist(WARPS)) grid = std::min<int64_t>(grid, sh.resident());
@@ -448,6 +474,20 @@ static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* 
   }
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_colloc_action_kernel launch");
+}
+
+template <int N, int CPB, int SY, int SX, int CS, bool GS = false, int WARPS = 0>
+static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                    const double* u, const double* kappa, cudaStream_t s,
+                    const int* cmap = nullptr) {
+  // unpadded layouts at n = 3, 5, 13 stage with 16-byte copies: p = 4
+  // 0.1157 -> 0.1147, p = 12 1.928 -> 1.894 ms; at n = 15, 17 they measured
+  // 0.3-0.8% slower and keep the per-element copies (profiles/r02ap_c3_*)
+  if constexpr (SY == N && SX == N * N && CS == N * N * N && !GS) {
+    if (N >= 15 || option(OPT_C3_CFG) == 1)
+      return launch_nv<N, CPB, SY, SX, CS, GS, WARPS, 1>(p, ncells, A, coords, u, kappa, s, cmap);
+  }
+  return launch_nv<N, CPB, SY, SX, CS, GS, WARPS, 0>(p, ncells, A, coords, u, kappa, s, cmap);
 }
 
 #ifndef SFK_COLLOC_WARPS_DEFAULT

@@ -97,7 +97,7 @@ struct NeoCfg {
 // cells (every stage has <= 32 lines for them) with its own shared-memory
 // slice and prefetch, and the stages sync with __syncwarp instead of CTA
 // barriers (the CTA version runs ~13 barriers per batch).
-template <int N, int M, int CPB, bool GS = false, int WARPS = 0>
+template <int N, int M, int CPB, bool GS = false, int WARPS = 0, int VAR = 0>
 __global__ void __launch_bounds__(WARPS ? 32 * WARPS : NeoCfg<N, M, CPB>::THREADS)
 hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double lam,
                       int64_t ncells, const double* __restrict__ coords,
@@ -246,8 +246,15 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
     HexLineAdj geo;
     geo.setup(sC + c * 24, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
     const double wxy = T.W[qx] * T.W[qy];
-#pragma unroll 1
-    for (int q = 0; q < M; ++q) {
+    // g[3a + l]: reference derivative l (0 x, 1 y, 2 z) of component a at q
+    auto load_point = [&](int q, double g[9]) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int l = 0; l < 3; ++l) g[3 * a + l] = line[(3 * a + 2 - l) * YA + q];
+    };
+    // flux at point q from its gradients g (overwritten with the 9 fluxes)
+    auto point_flux = [&](int q, double g[9]) {
       double rr[3][3];
       const double det = geo.adj(T.Bc[M + q], rr[0], rr[1], rr[2]);
       const double idet = rcp64(det);
@@ -255,9 +262,9 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
       double F[3][3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        const double g0 = line[(3 * a + 2) * YA + q];  // d_x
-        const double g1 = line[(3 * a + 1) * YA + q];  // d_y
-        const double g2 = line[(3 * a + 0) * YA + q];  // d_z
+        const double g0 = g[3 * a];      // d_x
+        const double g1 = g[3 * a + 1];  // d_y
+        const double g2 = g[3 * a + 2];  // d_z
 #pragma unroll
         for (int k = 0; k < 3; ++k)
           F[a][k] = fma(fma(g2, rr[2][k], fma(g1, rr[1][k], g0 * rr[0][k])), idet,
@@ -283,10 +290,42 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
 #pragma unroll
         for (int k = 0; k < 3; ++k) P[k] = fma(mu, F[a][k], beta * cof[a][k]);
 #pragma unroll
-        for (int l = 0; l < 3; ++l) {
-          const double f = s * fma(rr[l][2], P[2], fma(rr[l][1], P[1], rr[l][0] * P[0]));
-          line[(3 * a + 2 - l) * YA + q] = f;   // slot 2 = x, 1 = y, 0 = z
-        }
+        for (int l = 0; l < 3; ++l)
+          g[3 * a + l] = s * fma(rr[l][2], P[2], fma(rr[l][1], P[1], rr[l][0] * P[0]));
+      }
+    };
+    auto store_point = [&](int q, const double g[9]) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int l = 0; l < 3; ++l) line[(3 * a + 2 - l) * YA + q] = g[3 * a + l];   // slot 2 = x
+    };
+    if (VAR & 1) {
+      // two points per iteration: two independent dependency chains
+      // (adjugate -> F -> cof -> J -> log -> P -> flux) in flight per thread
+#pragma unroll 1
+      for (int q = 0; q + 1 < M; q += 2) {
+        double g0[9], g1[9];
+        load_point(q, g0);
+        load_point(q + 1, g1);
+        point_flux(q, g0);
+        point_flux(q + 1, g1);
+        store_point(q, g0);
+        store_point(q + 1, g1);
+      }
+      if (M & 1) {
+        double g0[9];
+        load_point(M - 1, g0);
+        point_flux(M - 1, g0);
+        store_point(M - 1, g0);
+      }
+    } else {
+#pragma unroll 1
+      for (int q = 0; q < M; ++q) {
+        double g0[9];
+        load_point(q, g0);
+        point_flux(q, g0);
+        store_point(q, g0);
       }
     }
     // (3) transposed z, in place: slot 2 <- Bz^T f_x, 1 <- Bz^T f_y, 0 <- Dz^T f_z
@@ -376,14 +415,14 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
   }  // persistent batch loop
 }
 
-template <int N, int M, int CPB, bool GS = false, int WARPS = 0>
+template <int N, int M, int CPB, bool GS = false, int WARPS = 0, int VAR = 0>
 static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                       const double* u, cudaStream_t s, const int* cmap = nullptr) {
   using C = NeoCfg<N, M, CPB>;
   constexpr int THREADS = WARPS ? 32 * WARPS : C::THREADS;
   constexpr size_t SMEM = WARPS ? WARPS * C::SMEM : C::SMEM;
   constexpr int CPBT = WARPS ? WARPS * CPB : CPB;
-  auto k = hex_neohookean_kernel<N, M, CPB, GS, WARPS>;
+  auto k = hex_neohookean_kernel<N, M, CPB, GS, WARPS, VAR>;
   LaunchShape sh;
   if (const int rc_ = kernel_shape((const void*)k, THREADS, SMEM, "hex_neohookean", &sh, true))
     return rc_;
@@ -428,16 +467,31 @@ static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const doub
   const int n = p->n, m = p->m;
   const int64_t ow = option(OPT_NEO_WARPS);   // 0: built-in, < 0: off
   const int warps = ow == 0 ? SFK_NEO_WARPS_DEFAULT : ow < 0 ? 0 : (int)ow;
+  const int var = (int)option(OPT_NEO_CFG);   // 1: two points per pointwise iteration everywhere
   if (m == n + 1 && warps > 0 && n <= 4) {
     // warp-synchronous: 3 / 2 / 1 cells per warp at p = 1 / 2 / 3
     if (warps == 8) {
       if (n == 2) return launch_neo<2, 3, 3, GS, 8>(p, ncells, A, coords, w0, s, cmap);
       if (n == 3) return launch_neo<3, 4, 2, GS, 8>(p, ncells, A, coords, w0, s, cmap);
       if (n == 4) return launch_neo<4, 5, 1, GS, 8>(p, ncells, A, coords, w0, s, cmap);
+    } else if (var == 1) {
+      if (n == 2) return launch_neo<2, 3, 3, GS, 4, 1>(p, ncells, A, coords, w0, s, cmap);
+      if (n == 3) return launch_neo<3, 4, 2, GS, 4, 1>(p, ncells, A, coords, w0, s, cmap);
+      if (n == 4) return launch_neo<4, 5, 1, GS, 4, 1>(p, ncells, A, coords, w0, s, cmap);
     } else {
       if (n == 2) return launch_neo<2, 3, 3, GS, 4>(p, ncells, A, coords, w0, s, cmap);
       if (n == 3) return launch_neo<3, 4, 2, GS, 4>(p, ncells, A, coords, w0, s, cmap);
       if (n == 4) return launch_neo<4, 5, 1, GS, 4>(p, ncells, A, coords, w0, s, cmap);
+    }
+  }
+  // two points per pointwise iteration: p = 6 1.831 -> 1.772 ms, neutral at
+  // p = 2..5 (profiles/r02ao_c4_*); option neo_cfg = 2 turns it off at p = 6
+  if (m == n + 1 && (var == 1 || (n == 7 && var != 2))) {
+    switch (n) {
+      case 5: return launch_neo<5, 6, SFK_NEO_CPB_P4, GS, 0, 1>(p, ncells, A, coords, w0, s, cmap);
+      case 6: return launch_neo<6, 7, SFK_NEO_CPB_P5, GS, 0, 1>(p, ncells, A, coords, w0, s, cmap);
+      case 7: return launch_neo<7, 8, SFK_NEO_CPB_P6, GS, 0, 1>(p, ncells, A, coords, w0, s, cmap);
+      default: break;
     }
   }
   if (m == n + 1) {

@@ -20,7 +20,8 @@ static const char* const kNames[OPT_COUNT] = {
     "c2g_small",     "c2g_kernel",  "cell_th",   "cell_minb",    "colloc_warps",
     "c3_tc",         "c5_p1",       "c5_p3",     "c5_p4",        "csr_dmma",
     "c5_p1_minb",    "neo_warps",   "host_chunk_mb", "lp_smem_kb", "lp_max_threads",
-    "lp_warp",       "lp_minb",     "lp_fuse",   "v6_cfg",
+    "lp_warp",       "lp_minb",     "lp_fuse",   "v6_cfg",       "neo_cfg",
+    "c3_cfg",
 };
 
 static std::atomic<int64_t> g_opt[OPT_COUNT];

@@ -38,6 +38,8 @@ enum Option : int {
   OPT_LP_MINB,
   OPT_LP_FUSE,       // LoopProgram loop fusion: -1 = off
   OPT_V6_CFG,        // v6 (cells per CTA, min CTAs per SM) alternative 1..3 per n
+  OPT_NEO_CFG,       // C4 variant: 1 two points per pointwise iteration at every p, 2 at none
+  OPT_C3_CFG,        // C3 variant: 1 per-element staging copies everywhere
   OPT_COUNT
 };
 
