@@ -29,7 +29,8 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("configs", nargs="*", default=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("configs", nargs="*", default=["C1", "C2", "C3", "C4", "C5"],
+                    help="C4 also prints C4F lines (the finite displacement draw)")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cpu-cells", type=int, default=4096)
     ap.add_argument("--no-cpu", action="store_true")
@@ -243,6 +244,17 @@ def main():
                 d = dev_inputs(inp)
                 out = torch.empty_like(d["w0"])
                 report("C4", plan, inp, 3 * (p + 1) ** 3, sfk(plan, d, out))
+                del d, out
+                # C4F: the same batch with the finite draw (amplitude 0.03 h / p^2,
+                # tests/test_fullsize_parity.py): BASELINE's draw inverts cells at
+                # p >= 5 (all of them at p = 6), whose NaN results take log's
+                # special-case path — this line times every point on the finite path
+                amp = 0.03 / p ** 2
+                inp = dict(inp, w0=workloads.uniform_dofs(inp["coords"].shape[0], 3 * (p + 1) ** 3,
+                                                          -amp, amp, seed=99, scale=workloads.H))
+                d = dev_inputs(inp)
+                out = torch.empty_like(d["w0"])
+                report("C4F", plan, inp, 3 * (p + 1) ** 3, sfk(plan, d, out))
                 del d, out
         elif cfg == "C5":
             for p in range(1, 5):
