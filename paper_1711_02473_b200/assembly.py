@@ -313,7 +313,9 @@ class CsrPattern:
 def assemble_csr(plan, cell_dofs, coords, pattern, values=None, entry_map=None, stream=None):
     """Assembled stiffness matrix values (length pattern.nnz, float64 CUDA):
     values += sum_c P_c^T A_c P_c with A_c the hex ``laplace`` cell matrix of
-    ``plan`` (C5 kernel, p <= 4).  ``values`` is zeroed unless given."""
+    ``plan`` (C5 kernels: p <= 4 fused with a binary search or the entry map,
+    p = 5..8 the DMMA kernel of hex_matrix_tcn.cu, which inserts through the
+    entry map — built here when not given).  ``values`` is zeroed unless given."""
     import torch
 
     from .runtime import _check, load_library, native_plan
@@ -332,6 +334,8 @@ def assemble_csr(plan, cell_dofs, coords, pattern, values=None, entry_map=None, 
                                   or tuple(entry_map.shape) != (coords.shape[0], n3 * n3)):
         raise ShapeMismatch("entry_map must be a contiguous int32 (%d, %d) tensor"
                             % (coords.shape[0], n3 * n3))
+    if entry_map is None and n3 > 125:
+        entry_map = pattern.entry_map(cell_dofs)
     values = _values(values, pattern, coords.device)
     if stream is None:
         stream = torch.cuda.current_stream(coords.device).cuda_stream

@@ -404,11 +404,15 @@ int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double
         }
         return launch_mat<5, 5, 1>(p, ncells, A, coords, s);
       }
-      default: break;
+      default:
+        // p = 5..8: chunked DMMA kernel (hex_matrix_tcn.cu)
+        if (hex_matrix_tcn_supported(p->n, p->m))
+          return launch_hex_matrix_tcn(p, ncells, A, coords, s);
+        break;
     }
   }
   return fail(SFK_EUNSUPPORTED,
-              "hex laplace matrix: no kernel for n=%d, m=%d (n==m in 2..5, p<=4)", p->n, p->m);
+              "hex laplace matrix: no kernel for n=%d, m=%d (n==m in 2..9, p<=8)", p->n, p->m);
 }
 
 int launch_hex_matrix_csr(const sfk_plan* p, int64_t ncells, const int32_t* dofs,
@@ -438,9 +442,17 @@ int launch_hex_matrix_csr(const sfk_plan* p, int64_t ncells, const int32_t* dofs
     case 5:
       return launch_mat<5, 5, 1, true>(p, ncells, values, coords, s, dofs, row_ptr, col_idx,
                                         emap);
-    default: break;
+    default:
+      // p = 5..8: the chunked DMMA kernel with its entry-map epilogue
+      if (hex_matrix_tcn_supported(p->n, p->m)) {
+        if (!emap)
+          return fail(SFK_EUNSUPPORTED,
+                      "CSR assembly at p >= 5 needs the entry map (sfk_csr_entry_map)");
+        return launch_hex_matrix_tcn(p, ncells, values, coords, s, emap);
+      }
+      break;
   }
-  return fail(SFK_EUNSUPPORTED, "CSR assembly: no kernel for n=%d (p<=4)", p->n);
+  return fail(SFK_EUNSUPPORTED, "CSR assembly: no kernel for n=%d (p<=8)", p->n);
 }
 
 }  // namespace sfk

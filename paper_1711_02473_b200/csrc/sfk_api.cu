@@ -260,7 +260,7 @@ static bool kernel_available(int kind, int dim, int n, int m, int colloc) {
     case SFK_KIND_ACTION_MASS:
       return dim == 3 ? hex_mass_supported(n, m) : quad;
     case SFK_KIND_LAPLACE_MATRIX:
-      return dim == 3 && !colloc && n == m && n >= 2 && n <= 5;
+      return dim == 3 && !colloc && n == m && n >= 2 && n <= 9;
     case SFK_KIND_NEOHOOKEAN_RESIDUAL:
       return dim == 3 && !colloc &&
              ((m == n + 1 && n >= 2 && n <= 7) || (m == n && n >= 2 && n <= 4));

@@ -157,6 +157,9 @@ int launch_hex_matrix_tc4(const sfk_plan* p, int64_t ncells, double* A, const do
                           cudaStream_t s, const int32_t* emap = nullptr);
 int launch_hex_matrix_tc5(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                           cudaStream_t s, const int32_t* emap = nullptr);
+int launch_hex_matrix_tcn(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                          cudaStream_t s, const int32_t* emap = nullptr);
+bool hex_matrix_tcn_supported(int n, int m);
 int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A,
                       const double* coords, cudaStream_t s);
 int launch_hex_matrix_csr(const sfk_plan* p, int64_t ncells, const int32_t* dofs,

@@ -40,6 +40,7 @@ enum Option : int {
   OPT_V6_CFG,        // v6 (cells per CTA, min CTAs per SM) alternative 1..3 per n
   OPT_NEO_CFG,       // C4 variant: 1 two points per pointwise iteration at every p, 2 at none
   OPT_C3_CFG,        // C3 variant: 1 per-element staging copies everywhere
+  OPT_C5_HI_CFG,     // C5 p = 5..8 DMMA kernel: (iy block, warps per row tile) alternative 1, 2
   OPT_COUNT
 };
 

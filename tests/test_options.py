@@ -53,7 +53,7 @@ def test_library_reads_no_dispatch_environment():
     ("action_mass", "hex", 3, {"quadrature": 5}),
     ("action_mass", "hex", 6, {"variant": "spectral_gll", "quadrature": "collocated-gll"}),
     ("action_laplace", "hex", 9, {}), ("action_laplace", "quad", 8, {}),
-    ("laplace", "hex", 4, {}),
+    ("laplace", "hex", 4, {}), ("laplace", "hex", 5, {}), ("laplace", "hex", 8, {}),
     ("action_laplace", "hex", 16, {"variant": "spectral_gll", "quadrature": "collocated-gll"}),
 ])
 def test_supported_requests_compile(form, cell, p, kw):
@@ -64,7 +64,7 @@ def test_supported_requests_compile(form, cell, p, kw):
 @pytest.mark.parametrize("form,cell,p,kw", [
     ("action_laplace", "quad", 9, {}),        # quad kernel stops at n = 9
     ("action_mass", "quad", 12, {}),
-    ("laplace", "hex", 5, {}),                # local matrices: p <= 4
+    ("laplace", "hex", 9, {}),                # local matrices: p <= 8
     ("laplace", "hex", 2, {"quadrature": 4}),  # matrices need m == n
     ("action_laplace", "hex", 10, {}),        # n = 11 > the line-kernel table
     ("action_laplace", "hex", 2, {"quadrature": 7}),
@@ -83,9 +83,10 @@ def test_plan_create_rejects_what_the_table_rejects():
     z = np.zeros(18 * 18)
     ptr = z.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
     out = ctypes.c_void_p()
-    # hex laplace matrix at n = 6 (p = 5): no kernel -> SFK_EUNSUPPORTED at create
-    assert lib.sfk_kernel_available(4, 3, 6, 6, 0) == 0
-    rc = lib.sfk_plan_create(4, 3, 5, 6, 6, 0, ptr, ptr, ptr, ptr, ptr, ptr, None, 0,
+    # hex laplace matrix at n = 10 (p = 9): no kernel -> SFK_EUNSUPPORTED at create
+    assert lib.sfk_kernel_available(4, 3, 10, 10, 0) == 0
+    assert lib.sfk_kernel_available(4, 3, 9, 9, 0) == 1
+    rc = lib.sfk_plan_create(4, 3, 9, 10, 10, 0, ptr, ptr, ptr, ptr, ptr, ptr, None, 0,
                              ctypes.byref(out))
     assert rc == 2 and not out.value
     assert lib.sfk_kernel_available(3, 3, 4, 4, 0) == 1   # hex action_mass

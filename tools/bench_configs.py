@@ -268,6 +268,25 @@ def main():
                                   device=dev)
                 report("C5", plan, inp, nd, sfk(plan, d, out))
                 del d, out
+        elif cfg == "C5H":
+            # C5 beyond the BASELINE degrees: p = 5..8 on
+            # the chunked DMMA kernel; (p+1)^6 doubles per cell, so the batch
+            # shrinks with p to keep A at 6-9 GB (2^14 .. 2^11 cells)
+            for p in range(5, 9):
+                if args.p and p not in args.p:
+                    continue
+                plan = compile_kernel("laplace", "hex", p)
+                nx = {5: 4, 6: 2, 7: 1, 8: 1}[p]
+                inp = {"coords": workloads.lattice_coords(nx, 64, 64 if p <= 7 else 32)}
+                d = dev_inputs(inp)
+                nd = (p + 1) ** 3
+                out = torch.empty((d["coords"].shape[0], nd * nd), dtype=torch.float64,
+                                  device=dev)
+                cc = args.cpu_cells
+                args.cpu_cells = min(cc, 64)
+                report("C5H", plan, inp, nd, sfk(plan, d, out))
+                args.cpu_cells = cc
+                del d, out
         torch.cuda.empty_cache()
 
 
