@@ -21,21 +21,21 @@
 namespace sfk {
 
 namespace p1 {
-constexpr int CPB = 128;             // cells (= threads) per CTA
 constexpr int CS = 26;               // padded coords stride (24 used)
 constexpr int US = 10;               // padded u stride (8 used)
-constexpr size_t SMEM = (size_t)CPB * (CS + US) * sizeof(double);
+constexpr size_t smem(int cpb) { return (size_t)cpb * (CS + US) * sizeof(double); }
 }  // namespace p1
 
 // GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
 // item 1): u = x gathered through cmap[c][0..7], A = y scatter-added with
 // fp64 atomics.
-template <bool GS>
-__global__ void __launch_bounds__(p1::CPB, SFK_P1_MINB)
+template <bool GS, int CPB = 128, int MINB = SFK_P1_MINB>
+__global__ void __launch_bounds__(CPB, MINB)
 hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
                       double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
-  using namespace p1;
+  using p1::CS;
+  using p1::US;
   extern __shared__ __align__(16) double smem[];
   double* sC = smem;
   double* sU = smem + CPB * CS;
@@ -188,19 +188,32 @@ hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
   }
 }
 
+template <bool GS, int CPB, int MINB>
+static int launch_p1_cfg(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                         const double* w0, cudaStream_t s, const int* cmap) {
+  auto kern = hex_laplace_action_p1<GS, CPB, MINB>;
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)kern, CPB, p1::smem(CPB), "hex_action_p1", &sh))
+    return rc_;
+  const Tabs<2, 2> T = make_tabs<2, 2>(p);
+  const unsigned grid = (unsigned)((ncells + CPB - 1) / CPB);
+  kern<<<grid, CPB, p1::smem(CPB), s>>>(T, ncells, coords, w0, A, cmap);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "hex_laplace_action_p1 launch");
+}
+
+// (cells per CTA, min CTAs per SM): option p1_cfg = 1..3 selects the
+// alternatives (A/B runs)
 template <bool GS>
 static int launch_p1(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                      const double* w0, cudaStream_t s, const int* cmap) {
   if (p->n != 2 || p->m != 2) return SFK_EUNSUPPORTED;
-  LaunchShape sh;
-  if (const int rc_ = kernel_shape((const void*)hex_laplace_action_p1<GS>, p1::CPB, p1::SMEM,
-                                   "hex_action_p1", &sh))
-    return rc_;
-  const Tabs<2, 2> T = make_tabs<2, 2>(p);
-  const unsigned grid = (unsigned)((ncells + p1::CPB - 1) / p1::CPB);
-  hex_laplace_action_p1<GS><<<grid, p1::CPB, p1::SMEM, s>>>(T, ncells, coords, w0, A, cmap);
-  note_launch();
-  return cuda_status(cudaGetLastError(), "hex_laplace_action_p1 launch");
+  switch ((int)option(OPT_P1_CFG)) {
+    case 1: return launch_p1_cfg<GS, 64, 6>(p, ncells, A, coords, w0, s, cmap);
+    case 2: return launch_p1_cfg<GS, 32, 12>(p, ncells, A, coords, w0, s, cmap);
+    case 3: return launch_p1_cfg<GS, 96, 4>(p, ncells, A, coords, w0, s, cmap);
+    default: return launch_p1_cfg<GS, 128, SFK_P1_MINB>(p, ncells, A, coords, w0, s, cmap);
+  }
 }
 
 int launch_hex_action_p1(const sfk_plan* p, int64_t ncells, double* A, const double* coords,

@@ -387,7 +387,10 @@ int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double
       // work per cell for the padded tiles, profiles/r01bl_c5_p2_dmma.jsonl)
       case 3: return launch_mat<3, 3, 3>(p, ncells, A, coords, s);
       case 4: {
-        // DMMA kernel (hex_matrix_tc.cu); option c5_p3 = 1 selects the FMA one
+        // DMMA kernel (hex_matrix_tc.cu); option c5_p3 = 1 selects the FMA one,
+        // c5_hi_cfg = 3, 4 the chunked DMMA kernel of hex_matrix_tcn.cu (slower
+        // here: 0.98 vs 1.08 / 1.18 ms, profiles/r02bc_c5.jsonl)
+        if (option(OPT_C5_HI_CFG) >= 3) return launch_hex_matrix_tcn(p, ncells, A, coords, s);
         const bool phase = option(OPT_C5_P3) == 1;
         if (!phase) {
           const int rc = launch_hex_matrix_tc4(p, ncells, A, coords, s);
@@ -396,13 +399,17 @@ int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double
         return launch_mat<4, 4, 1, false, true>(p, ncells, A, coords, s);
       }
       case 5: {
-        // DMMA kernel (hex_matrix_tc.cu); option c5_p4 = 1 selects the FMA one
-        const bool phase = option(OPT_C5_P4) == 1;
-        if (!phase) {
+        // chunked DMMA kernel (hex_matrix_tcn.cu): 5.01 -> 4.41 ms against
+        // tc5 (profiles/r02bc_c5.jsonl); option c5_p4 = 1 selects the FMA
+        // kernel, c5_p4 = 2 tc5 (hex_matrix_tc.cu)
+        const int64_t v = option(OPT_C5_P4);
+        if (v == 1) return launch_mat<5, 5, 1>(p, ncells, A, coords, s);
+        if (v == 2) {
           const int rc = launch_hex_matrix_tc5(p, ncells, A, coords, s);
           if (rc != SFK_EUNSUPPORTED) return rc;
+          return launch_mat<5, 5, 1>(p, ncells, A, coords, s);
         }
-        return launch_mat<5, 5, 1>(p, ncells, A, coords, s);
+        return launch_hex_matrix_tcn(p, ncells, A, coords, s);
       }
       default:
         // p = 5..8: chunked DMMA kernel (hex_matrix_tcn.cu)

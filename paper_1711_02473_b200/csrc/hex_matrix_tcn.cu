@@ -340,6 +340,14 @@ int launch_hex_matrix_tcn(const sfk_plan* p, int64_t ncells, double* A, const do
   // option c5_hi_cfg = 1, 2 selects the alternatives for A/B runs
   const int cfg = (int)option(OPT_C5_HI_CFG);
   switch (p->n) {
+    // n = 4: A/B against tc4 (option c5_hi_cfg = 3, 4); n = 5: the default
+    // (4.41 ms at 2^16 cells against 5.01 for tc5 and 6.51 for <5, 5, 2>)
+    case 4:
+      if (cfg == 4) return launch_tcn<4, 4, 2>(p, ncells, A, coords, s, emap);
+      return launch_tcn<4, 4, 1>(p, ncells, A, coords, s, emap);
+    case 5:
+      if (cfg == 4) return launch_tcn<5, 5, 2>(p, ncells, A, coords, s, emap);
+      return launch_tcn<5, 5, 1>(p, ncells, A, coords, s, emap);
     case 6:   // 3.48 ms (2^14 cells) vs 3.89 <6,6,2>, 4.62 <6,3,2>
       if (cfg == 1) return launch_tcn<6, 3, 2>(p, ncells, A, coords, s, emap);
       if (cfg == 2) return launch_tcn<6, 6, 2>(p, ncells, A, coords, s, emap);

@@ -21,7 +21,7 @@ static const char* const kNames[OPT_COUNT] = {
     "c3_tc",         "c5_p1",       "c5_p3",     "c5_p4",        "csr_dmma",
     "c5_p1_minb",    "neo_warps",   "host_chunk_mb", "lp_smem_kb", "lp_max_threads",
     "lp_warp",       "lp_minb",     "lp_fuse",   "v6_cfg",       "neo_cfg",
-    "c3_cfg",        "c5_hi_cfg",
+    "c3_cfg",        "c5_hi_cfg",   "p1_cfg",
 };
 
 static std::atomic<int64_t> g_opt[OPT_COUNT];

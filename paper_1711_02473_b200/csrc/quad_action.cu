@@ -212,10 +212,18 @@ int launch_quad_action(const sfk_plan* p0, const sfk_plan* p1, int64_t ncells, d
       case 7: return launch_quad_nm<7, 7>(pm, pl, ncells, Am, Al, coords, u, s);
       case 8: return launch_quad_nm<8, 8>(pm, pl, ncells, Am, Al, coords, u, s);
       case 9: return launch_quad_nm<9, 9>(pm, pl, ncells, Am, Al, coords, u, s);
+      case 10: return launch_quad_nm<10, 10>(pm, pl, ncells, Am, Al, coords, u, s);
+      case 11: return launch_quad_nm<11, 11>(pm, pl, ncells, Am, Al, coords, u, s);
+      case 12: return launch_quad_nm<12, 12>(pm, pl, ncells, Am, Al, coords, u, s);
+      case 13: return launch_quad_nm<13, 13>(pm, pl, ncells, Am, Al, coords, u, s);
+      case 14: return launch_quad_nm<14, 14>(pm, pl, ncells, Am, Al, coords, u, s);
+      case 15: return launch_quad_nm<15, 15>(pm, pl, ncells, Am, Al, coords, u, s);
+      case 16: return launch_quad_nm<16, 16>(pm, pl, ncells, Am, Al, coords, u, s);
+      case 17: return launch_quad_nm<17, 17>(pm, pl, ncells, Am, Al, coords, u, s);
       default: break;
     }
   }
-  return fail(SFK_EUNSUPPORTED, "quad actions: no kernel for n=%d, m=%d (n==m in 2..9)", n, m);
+  return fail(SFK_EUNSUPPORTED, "quad actions: no kernel for n=%d, m=%d (n==m in 2..17)", n, m);
 }
 
 }  // namespace sfk

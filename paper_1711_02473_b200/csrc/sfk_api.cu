@@ -250,7 +250,7 @@ static bool collocation_derivative(int n, const double* B, const double* D, doub
 
 static bool kernel_available(int kind, int dim, int n, int m, int colloc) {
   const bool hex_line = (n == m && n >= 2 && n <= 10) || (m == n + 1 && n >= 2 && n <= 8);
-  const bool quad = dim == 2 && !colloc && n == m && n >= 2 && n <= 9;
+  const bool quad = dim == 2 && !colloc && n == m && n >= 2 && n <= 17;
   const bool colloc_hex = dim == 3 && colloc && n == m && n >= 2 && n <= 17;
   switch (kind) {
     case SFK_KIND_ACTION_LAPLACE:

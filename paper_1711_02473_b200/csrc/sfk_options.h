@@ -27,7 +27,7 @@ enum Option : int {
   OPT_C3_TC,         // 1: C3 DMMA variant
   OPT_C5_P1,         // 1: C5 p = 1 through the CTA-phase kernel
   OPT_C5_P3,         // 1: C5 p = 3 through the FMA phase kernel
-  OPT_C5_P4,         // 1: C5 p = 4 through the FMA phase kernel
+  OPT_C5_P4,         // 1: C5 p = 4 through the FMA phase kernel, 2: through tc5
   OPT_CSR_DMMA,      // 1: CSR epilogue on the DMMA matrix kernels
   OPT_C5_P1_MINB,    // 3: C5 p = 1 kernel with min 3 CTAs per SM
   OPT_NEO_WARPS,     // C4 warp-synchronous variant: warps per CTA, -1 = off
@@ -40,7 +40,8 @@ enum Option : int {
   OPT_V6_CFG,        // v6 (cells per CTA, min CTAs per SM) alternative 1..3 per n
   OPT_NEO_CFG,       // C4 variant: 1 two points per pointwise iteration at every p, 2 at none
   OPT_C3_CFG,        // C3 variant: 1 per-element staging copies everywhere
-  OPT_C5_HI_CFG,     // C5 p = 5..8 DMMA kernel: (iy block, warps per row tile) alternative 1, 2
+  OPT_C5_HI_CFG,
+  OPT_P1_CFG,        // C2 p = 1 kernel: (cells per CTA, min CTAs per SM) alternative 1..3     // C5 p = 5..8 DMMA kernel: (iy block, warps per row tile) alternative 1, 2
   OPT_COUNT
 };
 

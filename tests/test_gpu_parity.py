@@ -186,7 +186,7 @@ def test_c1_golden_and_fused_pair(cuda):
     assert rel_err(am.cpu().numpy(), _run(torch, pm, full)) < 1e-14
 
 
-@pytest.mark.parametrize("p", range(1, 9))
+@pytest.mark.parametrize("p", range(1, 17))
 def test_quad_actions_vs_oracle(cuda, p):
     nc = 45
     inp = {"coords": workloads.quad_coords(nc), "w0": workloads.uniform_dofs(nc, (p + 1) ** 2)}
@@ -216,6 +216,22 @@ def test_c5_golden_and_properties(cuda, p):
     u = workloads.uniform_dofs(coords.shape[0], nd)
     act = _run(cuda, compile_kernel("action_laplace", "hex", p), {"coords": coords, "w0": u})
     assert rel_err(np.einsum("cij,cj->ci", M, u), act) < 1e-12
+
+
+@pytest.mark.parametrize("p,opts", [
+    (3, {"c5_p3": 1}), (3, {"c5_hi_cfg": 3}), (3, {"c5_hi_cfg": 4}),
+    (4, {"c5_p4": 1}), (4, {"c5_p4": 2}), (4, {"c5_hi_cfg": 4}),
+])
+def test_c5_kernel_variants_vs_oracle(cuda, p, opts):
+    """Every selectable C5 kernel at p = 3, 4 (FMA phases, tc4 / tc5, the
+    chunked DMMA kernel) on a batch larger than the resident grid."""
+    from paper_1711_02473_b200 import runtime
+
+    plan = compile_kernel("laplace", "hex", p)
+    coords = workloads.lattice_coords(6, 8, 8)[:379]
+    with runtime.options(**opts):
+        A = _run(cuda, plan, {"coords": coords})
+    assert rel_err(A, cpu.evaluate(plan, {"coords": coords})) < TOL
 
 
 def test_c5_reference_cell_analytic(cuda):

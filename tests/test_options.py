@@ -53,6 +53,7 @@ def test_library_reads_no_dispatch_environment():
     ("action_mass", "hex", 3, {"quadrature": 5}),
     ("action_mass", "hex", 6, {"variant": "spectral_gll", "quadrature": "collocated-gll"}),
     ("action_laplace", "hex", 9, {}), ("action_laplace", "quad", 8, {}),
+    ("action_laplace", "quad", 16, {}), ("action_mass", "quad", 12, {}),
     ("laplace", "hex", 4, {}), ("laplace", "hex", 5, {}), ("laplace", "hex", 8, {}),
     ("action_laplace", "hex", 16, {"variant": "spectral_gll", "quadrature": "collocated-gll"}),
 ])
@@ -62,8 +63,8 @@ def test_supported_requests_compile(form, cell, p, kw):
 
 
 @pytest.mark.parametrize("form,cell,p,kw", [
-    ("action_laplace", "quad", 9, {}),        # quad kernel stops at n = 9
-    ("action_mass", "quad", 12, {}),
+    ("action_laplace", "quad", 17, {}),       # quad kernel stops at n = 17 (p = 16)
+    ("action_mass", "quad", 3, {"quadrature": 5}),   # quad: m == n only
     ("laplace", "hex", 9, {}),                # local matrices: p <= 8
     ("laplace", "hex", 2, {"quadrature": 4}),  # matrices need m == n
     ("action_laplace", "hex", 10, {}),        # n = 11 > the line-kernel table
