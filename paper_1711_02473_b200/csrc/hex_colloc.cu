@@ -32,6 +32,40 @@
 
 namespace sfk {
 
+// Probe builds (tools/c3_sweep.py): -DSFK_C3_ONLY_N=n compiles the dispatch of
+// that n alone (no global-operator / warp-mode / DMMA variants) into a small
+// library exporting sfk_c3_probe_eval, with SFK_C3P_{PERSIST,KG,SPLITZ,MINB,
+// GEOM} (>= 0) overriding the per-n policies below and SFK_C3P_{CPB,SY,SX,CS}
+// the launch shape and shared-memory strides.  Product builds leave all of
+// them undefined.
+#ifndef SFK_C3_ONLY_N
+#define SFK_C3_ONLY_N 0
+#endif
+#ifndef SFK_C3P_PERSIST
+#define SFK_C3P_PERSIST -1
+#endif
+#ifndef SFK_C3P_KG
+#define SFK_C3P_KG -1
+#endif
+#ifndef SFK_C3P_SPLITZ
+#define SFK_C3P_SPLITZ -1
+#endif
+#ifndef SFK_C3P_MINB
+#define SFK_C3P_MINB -1
+#endif
+#ifndef SFK_C3P_GEOM
+#define SFK_C3P_GEOM -1
+#endif
+#ifndef SFK_C3_PROBE_ENTRY
+#define SFK_C3_PROBE_ENTRY sfk_c3_probe_eval
+#endif
+#if SFK_C3_ONLY_N
+namespace {   // every variant object of a probe library keeps its own instances
+#endif
+__host__ __device__ constexpr int c3p(int n, int probe, int dflt) {
+  return (SFK_C3_ONLY_N != 0 && n == SFK_C3_ONLY_N && probe >= 0) ? probe : dflt;
+}
+
 template <int N>
 struct TabsD {
   double D[N * N];
@@ -40,25 +74,27 @@ struct TabsD {
 };
 
 // Persistent CTAs with the next batch's u / kappa / coords prefetched by
-// cp.async while the current batch computes (one-shot CTAs load, then
-// compute: their load latency showed as 16% long-scoreboard stalls at p = 4,
-// profiles/r01cj_C3_p4.md).  Measured per n (profiles/r01ck_*.jsonl): only
-// n = 5 gains (p = 4 0.1167 -> 0.1127 ms); at n = 6..11 the doubled u /
-// kappa buffers cost occupancy and registers (p = 6..10 up to 44% slower).
-// SFK_COLLOC_PERSIST=n0 (A/B builds) makes every n <= n0 persistent.
+// cp.async while the current batch computes.  Round 1 kept it at n = 5 only
+// (p = 4 0.1167 -> 0.1127 ms; at n = 6..11 the doubled u / kappa buffers cost
+// occupancy, profiles/r01ck_*.jsonl); the round-2 sweep (tools/kernel_sweep.py,
+// profiles/r02cb_c3_sweep.jsonl) found one-shot CTAs with the split z phase at
+// 80 registers faster there too (0.1127 -> 0.1045 ms), so no n uses it by
+// default.  SFK_COLLOC_PERSIST=n0 (A/B builds) makes every n <= n0 persistent.
 #ifdef SFK_COLLOC_PERSIST
 __host__ __device__ constexpr bool colloc_persist(int n) { return n <= SFK_COLLOC_PERSIST; }
 #else
-__host__ __device__ constexpr bool colloc_persist(int n) { return n == 5; }
+__host__ __device__ constexpr bool colloc_persist(int n) { return c3p(n, SFK_C3P_PERSIST, false); }
 #endif
 
 // KG: kappa read from global memory (through L1/L2) in the pointwise phase
 // instead of being staged in shared memory — drops one of the four N^3
-// arrays, so n = 16 (139 -> 104 KB per CTA) fits two CTAs per SM.
+// arrays: n = 16 (139 -> 104 KB per CTA) fits two CTAs per SM; the round-2
+// sweep adds n = 7 (+5%), 10 (5 one-cell CTAs per SM, +17%) and 14 (3 CTAs
+// per SM with the unpadded layout, +18%).
 #ifdef SFK_COLLOC_KG
 __host__ __device__ constexpr bool colloc_kg(int n) { return n >= SFK_COLLOC_KG; }
 #else
-__host__ __device__ constexpr bool colloc_kg(int n) { return n == 16; }
+__host__ __device__ constexpr bool colloc_kg(int n) { return c3p(n, SFK_C3P_KG, n == 7 || n == 10 || n == 14 || n == 16); }
 #endif
 
 template <int N, int CPB, int SY, int SX, int CS>
@@ -69,7 +105,7 @@ struct CollocCfg {
   static constexpr bool persist(int warps) { return warps == 0 && colloc_persist(N); }
   static constexpr size_t smem(bool weighted, int warps = 0) {
     return persist(warps)
-               ? (size_t)((weighted ? 6 : 4) * CPB * CS + 2 * CPB * 24) * sizeof(double)
+               ? (size_t)((weighted && !colloc_kg(N) ? 6 : 4) * CPB * CS + 2 * CPB * 24) * sizeof(double)
                : (size_t)((weighted && !colloc_kg(N) ? 4 : 3) * CPB * CS + CPB * 24) * sizeof(double);
   }
 };
@@ -85,13 +121,16 @@ struct CollocCfg {
 // Phase 3 as three register-light passes (SPLITZ) at n = 12..15, with its
 // own register policy (same-box A/B over fused/split x min-blocks 0-3,
 // profiles/r01cf_*.jsonl: p = 11 1.969 -> 1.664 ms, p = 12 2.118 -> 1.918,
-// p = 13 3.803 -> 3.085, p = 14 3.652 -> 3.355; the other n keep the fused
-// loop).  SFK_COLLOC_SPLITZ=n0 (A/B builds) splits every n >= n0.
+// p = 13 3.803 -> 3.085, p = 14 3.652 -> 3.355).  The round-2 sweep
+// (profiles/r02cb_c3_sweep.jsonl) adds n = 5, 6 (80 registers, 3+ CTAs per
+// SM: p = 4 0.1127 -> 0.1045, p = 5 0.1987 -> 0.1679 ms) and n = 11 (p = 10
+// 1.118 -> 1.015); the other n keep the fused loop.
+// SFK_COLLOC_SPLITZ=n0 (A/B builds) splits every n >= n0.
 __host__ __device__ constexpr bool colloc_splitz(int n) {
 #ifdef SFK_COLLOC_SPLITZ
   return n >= SFK_COLLOC_SPLITZ;
 #else
-  return n >= 12 && n <= 15;
+  return c3p(n, SFK_C3P_SPLITZ, n == 5 || n == 6 || (n >= 11 && n <= 15));
 #endif
 }
 
@@ -99,8 +138,16 @@ __host__ __device__ constexpr int colloc_minb(int n) {
 #ifdef SFK_COLLOC_MINB
   if (SFK_COLLOC_MINB >= 0) return SFK_COLLOC_MINB;   // A/B builds (tools/build_variant.py)
 #endif
-  if (colloc_splitz(n)) return n <= 13 ? 3 : n == 14 ? 0 : 2;
-  return (n <= 7 || (n >= 9 && n <= 13) || n == 16) ? 2 : (n == 8 || n == 15) ? 0 : 1;
+  if (SFK_C3_ONLY_N != 0 && n == SFK_C3_ONLY_N && SFK_C3P_MINB >= 0) return SFK_C3P_MINB;
+  // round-2 sweep of (cells per CTA, strides, persist, kg, splitz, min-blocks)
+  // per n (tools/kernel_sweep.py, profiles/r02cb_c3_sweep.jsonl)
+  switch (n) {
+    case 5: case 6: case 13: case 14: return 3;
+    case 7: case 8: return 0;
+    case 10: case 11: case 12: return 4;
+    case 17: return 1;
+    default: return 2;   // n <= 4, 9, 15, 16
+  }
 }
 
 // GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
@@ -122,7 +169,7 @@ __host__ __device__ constexpr C3Arr c3_gx(int n, int sx, int sy, int cs) {
   return (void)n, C3Arr{sx, sy, cs};
 }
 __host__ __device__ constexpr C3Arr c3_gy(int n, int sx, int sy, int cs) {
-  return n == 6 ? C3Arr{6, 41, 244} : C3Arr{sx, sy, cs};
+  return (n == 6 && cs >= 244) ? C3Arr{6, 41, 244} : C3Arr{sx, sy, cs};
 }
 
 template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS = false, int WARPS = 0,
@@ -144,7 +191,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
   static_assert(GXC <= CS && GYC <= CS, "GX / GY must fit the CS-strided buffers");
   constexpr bool SPLITZ = colloc_splitz(N);
   constexpr bool PERSIST = C::persist(WARPS);
-  constexpr bool KG = WEIGHTED && colloc_kg(N) && !PERSIST;
+  constexpr bool KG = WEIGHTED && colloc_kg(N);
   constexpr bool CONTIG = SY == N && SX == NN && CS == N3 && C3_CONTIG;
   extern __shared__ double smem[];
   constexpr int TH = WARPS ? 32 : C::THREADS;
@@ -264,7 +311,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
         HexLineAdj geo;
         geo.setup(sC + c * 24, T.Bc[a], T.Bc[N + a], T.Bc[b], T.Bc[N + b]);
         const double wxy = T.W[a] * T.W[b];
-        const double* kp = KG ? kappa + (cell0 + c) * N3 + a * NN + b * N : sK + base;
+        const double* kp = KG ? kappa + (cell0 + (c < ncb ? c : 0)) * N3 + a * NN + b * N : sK + base;
   #pragma unroll 1
         for (int q = 0; q < N; ++q) {
           double gx = sGX[bx + q], gy = sGY[by + q], gz = sU[base + q];
@@ -303,11 +350,12 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
       // precomputed adjugate polynomials (hex_geometry.cuh) except at n = 15, 16,
       // where their 9 extra registers per thread cost more than they save
       // (same-box A/B, profiles/r01ai_*)
-      using Geo = typename std::conditional<(N == 15 || N == 16), HexLineGeom, HexLineAdj>::type;
+      constexpr bool GEOM = c3p(N, SFK_C3P_GEOM, N == 15 || N == 16);
+      using Geo = typename std::conditional<GEOM, HexLineGeom, HexLineAdj>::type;
       Geo geo;
       geo.setup(sC + c * 24, T.Bc[a], T.Bc[N + a], T.Bc[b], T.Bc[N + b]);
       const double wxy = T.W[a] * T.W[b];
-      const double* kp = KG ? kappa + (cell0 + c) * N3 + a * NN + b * N : sK + base;
+      const double* kp = KG ? kappa + (cell0 + (c < ncb ? c : 0)) * N3 + a * NN + b * N : sK + base;
   #pragma unroll
       for (int q = 0; q < N; ++q) {
         double gz = T.D[q] * ul[0];
@@ -316,7 +364,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
         double gx = sGX[bx + q], gy = sGY[by + q];
         double r0[3], r1[3], r2[3];
         double det;
-        if constexpr (N == 15 || N == 16) det = geo.adj(T.Bc[q], T.Bc[N + q], r0, r1, r2);
+        if constexpr (GEOM) det = geo.adj(T.Bc[q], T.Bc[N + q], r0, r1, r2);
         else det = geo.adj(T.Bc[N + q], r0, r1, r2);
         double s = (wxy * T.W[q]) * rcp64(fabs(det));
         if (WEIGHTED) s *= KG ? __ldg(kp + q) : kp[q];
@@ -466,11 +514,15 @@ static int launch_nv(const sfk_plan* p, int64_t ncells, double* A, const double*
     if (C::persist(WARPS)) grid = std::min<int64_t>(grid, sh.resident());
     if (grid > 0) k<<<(unsigned)grid, THREADS, sm, s>>>(T, ncells, coords, u, kappa, A, cmap);
   } else {
+#if SFK_C3_ONLY_N
+    return fail(SFK_EUNSUPPORTED, "probe build: weighted form only");
+#else
     auto k = colloc_kernel<N, CPB, SY, SX, CS, false, GS, WARPS, VAR>();
     const size_t sm = G * C::smem(false, WARPS);
     if (const int rc_ = kernel_shape((const void*)k, THREADS, sm, "hex_colloc", &sh)) return rc_;
     if (C::persist(WARPS)) grid = std::min<int64_t>(grid, sh.resident());
     if (grid > 0) k<<<(unsigned)grid, THREADS, sm, s>>>(T, ncells, coords, u, nullptr, A, cmap);
+#endif
   }
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_colloc_action_kernel launch");
@@ -496,7 +548,7 @@ static int launch_n(const sfk_plan* p, int64_t ncells, double* A, const double* 
 
 // cells per CTA at n = 10, 12 (overridable for A/B builds)
 #ifndef SFK_COLLOC_CPB10
-#define SFK_COLLOC_CPB10 2
+#define SFK_COLLOC_CPB10 1
 #endif
 #ifndef SFK_COLLOC_CPB12
 #define SFK_COLLOC_CPB12 1
@@ -508,6 +560,12 @@ static int dispatch_colloc(const sfk_plan* p, int64_t ncells, double* A, const d
                            const int* cmap) {
   if (p->n != p->m)
     return fail(SFK_EINVAL, "collocated action needs n_q1d == n_dof1d (got %d, %d)", p->n, p->m);
+#if SFK_C3_ONLY_N
+  if (p->n != SFK_C3_ONLY_N)
+    return fail(SFK_EUNSUPPORTED, "probe build: n=%d only (got %d)", SFK_C3_ONLY_N, p->n);
+  return launch_n<SFK_C3_ONLY_N, SFK_C3P_CPB, SFK_C3P_SY, SFK_C3P_SX, SFK_C3P_CS, GS>(
+      p, ncells, A, coords, w0, w1, s, cmap);
+#else
   // warp-synchronous variants for n <= 5 (option colloc_warps = warps per CTA)
   const int64_t ocw = option(OPT_COLLOC_WARPS);   // 0: built-in, < 0: off
   const int cw = ocw == 0 ? SFK_COLLOC_WARPS_DEFAULT : ocw < 0 ? 0 : (int)ocw;
@@ -520,29 +578,45 @@ static int dispatch_colloc(const sfk_plan* p, int64_t ncells, double* A, const d
       default: break;
     }
   }
-  // (N, cells/CTA, SY, SX, CS) from tools/smem_pads.py
+  // (N, cells/CTA, SY, SX, CS): strides from tools/smem_pads.py; the round-2
+  // sweep moved n = 6, 9, 10, 11, 12, 14 to the unpadded layout (smaller CTAs,
+  // 16-byte staging: more CTAs per SM beat the conflict-free strides) and
+  // n = 10, 11 to one cell per CTA (profiles/r02cb_c3_sweep.jsonl)
   switch (p->n) {
     case 2: return launch_n<2, 16, 2, 5, 12, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 3: return launch_n<3, 16, 3, 9, 27, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 4: return launch_n<4, 8, 4, 19, 76, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 5: return launch_n<5, 10, 5, 25, 125, GS>(p, ncells, A, coords, w0, w1, s, cmap);
-    case 6: return launch_n<6, 8, 6, 39, 244, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 6: return launch_n<6, 7, 6, 36, 216, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 7: return launch_n<7, 5, 7, 52, 369, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 8: return launch_n<8, 4, 9, 72, 576, GS>(p, ncells, A, coords, w0, w1, s, cmap);
-    case 9: return launch_n<9, 3, 9, 89, 801, GS>(p, ncells, A, coords, w0, w1, s, cmap);
-    case 10: return launch_n<10, SFK_COLLOC_CPB10, 11, 110, 1100, GS>(p, ncells, A, coords, w0, w1, s, cmap);
-    case 11: return launch_n<11, 2, 11, 123, 1353, GS>(p, ncells, A, coords, w0, w1, s, cmap);
-    case 12: return launch_n<12, SFK_COLLOC_CPB12, 13, 156, 1872, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 9: return launch_n<9, 3, 9, 81, 729, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 10: return launch_n<10, SFK_COLLOC_CPB10, 10, 100, 1000, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 11: return launch_n<11, 1, 11, 121, 1331, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 12: return launch_n<12, SFK_COLLOC_CPB12, 12, 144, 1728, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 13: return launch_n<13, 1, 13, 169, 2197, GS>(p, ncells, A, coords, w0, w1, s, cmap);
-    case 14: return launch_n<14, 1, 17, 238, 3332, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 14: return launch_n<14, 1, 14, 196, 2744, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 15: return launch_n<15, 1, 15, 225, 3375, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 16: return launch_n<16, 1, 17, 272, 4352, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 17: return launch_n<17, 1, 17, 289, 4913, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     default:
       return fail(SFK_EUNSUPPORTED, "collocated hex action: n=%d outside [2,17]", p->n);
   }
+#endif
 }
 
+#if SFK_C3_ONLY_N
+}  // anonymous namespace
+}  // namespace sfk
+// the probe object's only entry point: p is a plan made by the product
+// library (a plain host struct), all buffers device pointers as in sfk_eval
+extern "C" int SFK_C3_PROBE_ENTRY(const sfk_plan* p, int64_t ncells, double* A,
+                                 const double* coords, const double* w0, const double* w1,
+                                 void* stream) {
+  return sfk::dispatch_colloc<false>(p, ncells, A, coords, w0, w1, (cudaStream_t)stream, nullptr);
+}
+namespace sfk {
+#else
 int launch_hex_colloc_action(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                              const double* w0, const double* w1, cudaStream_t s) {
   // n = 8, 12, 16: DMMA kernel (hex_colloc_tc.cu)
@@ -555,5 +629,6 @@ int launch_hex_colloc_gs(const sfk_plan* p, int64_t ncells, const int* cmap, con
                          double* y, const double* coords, const double* kappa, cudaStream_t s) {
   return dispatch_colloc<true>(p, ncells, y, coords, x, kappa, s, cmap);
 }
+#endif
 
 }  // namespace sfk

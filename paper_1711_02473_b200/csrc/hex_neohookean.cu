@@ -24,45 +24,28 @@
 
 #include "async_copy.cuh"
 #include "hex_geometry.cuh"
+#include "hex_neohookean_point.cuh"
+
+// component loops: rolled (one copy of each stage's code) or unrolled x3 —
+// rolled, ptxas hoists the stages' table constants out of the loop into vector
+// registers and moves them back to uniform registers at every use (R2UR: 15%
+// of the executed instructions at p = 4, profiles/r02ce_C4_p4_opmix.txt)
+#ifndef SFK_NEO_UNROLLA
+#define SFK_NEO_UNROLLA 0
+#endif
+#if SFK_NEO_UNROLLA
+#define NEO_PRAGMA_A _Pragma("unroll")
+#else
+#define NEO_PRAGMA_A _Pragma("unroll 1")
+#endif
 
 #ifndef SFK_NEO_YT
 #define SFK_NEO_YT 1
 #endif
 
-#ifndef SFK_NEO_FASTLOG
-#define SFK_NEO_FASTLOG 0   // measured slower (p = 4 0.657 -> 0.689 ms, r01di_*)
-#endif
-
 namespace sfk {
 
 constexpr bool NEO_YT = SFK_NEO_YT;
-
-// ln J for the volumetric term.  Near J = 1 (every finite BASELINE point:
-// |J - 1| is a few 1e-2) ln J = 2 atanh(z), z = (J - 1)/(J + 1), summed as
-// 2z (1 + z^2/3 + ... + z^14/15): for |J - 1| < 1/16, |z| < 0.0323 and the
-// truncation is below 1e-23 relative; the rounding of z and the Horner sum
-// is a few ulp — far inside the 1e-12 gate.  Elsewhere (and for J <= 0,
-// NaN as in the reference) the libm log.  Meant to replace a ~40-instruction
-// dependent chain that was 13% of C4's stall samples
-// (profiles/r01cn_C4_p4.md), but the branch and the extra code measured
-// 2-5% slower than libm alone (profiles/r01di_*.jsonl): off by default.
-__device__ __forceinline__ double neo_log(double J) {
-  const double d = J - 1.0;
-  if (SFK_NEO_FASTLOG && fabs(d) < 0.0625) {
-    const double z = d * rcp64(J + 1.0);
-    const double z2 = z * z;
-    double t = 1.0 / 15.0;
-    t = fma(t, z2, 1.0 / 13.0);
-    t = fma(t, z2, 1.0 / 11.0);
-    t = fma(t, z2, 1.0 / 9.0);
-    t = fma(t, z2, 1.0 / 7.0);
-    t = fma(t, z2, 1.0 / 5.0);
-    t = fma(t, z2, 1.0 / 3.0);
-    t = fma(t, z2, 1.0);
-    return 2.0 * z * t;
-  }
-  return log(J);
-}
 
 // X-array q-stride and per-cell Y padding from tools/c4_layout.py's bank
 // model (x-line writes / y-line reads of X: n = 4..7 modelled wavefronts
@@ -160,7 +143,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
   const double* su = sU + (GS ? 0 : dst_shift(u + cell0 * (3 * N3)));
 
   // ---------------- forward x / y stages, per component -------------------
-#pragma unroll 1
+NEO_PRAGMA_A
   for (int a = 0; a < 3; ++a) {
     if (tid < CPB * NN) {
       const int c = tid / NN, r = tid - c * NN;
@@ -218,7 +201,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
     const int qx = NYT ? r1 : r0, qy = NYT ? r0 : r1;
     double* line = sY + c * C::YSZ + r * LZ;   // component a, slot k: line[(3a+k)*YA + .]
     // (1) reference gradients, in place: slots (0,1,2) <- (d_z, d_y, d_x)
-#pragma unroll 1
+NEO_PRAGMA_A
     for (int a = 0; a < 3; ++a) {
       double bb[N], bd[N], db[N];
       double* l0 = line + 3 * a * YA;
@@ -255,44 +238,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
     };
     // flux at point q from its gradients g (overwritten with the 9 fluxes)
     auto point_flux = [&](int q, double g[9]) {
-      double rr[3][3];
-      const double det = geo.adj(T.Bc[M + q], rr[0], rr[1], rr[2]);
-      const double idet = rcp64(det);
-      // grad u_a [k] = (1/det) sum_l r_l[k] d_l u_a ;  F = I + grad u
-      double F[3][3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const double g0 = g[3 * a];      // d_x
-        const double g1 = g[3 * a + 1];  // d_y
-        const double g2 = g[3 * a + 2];  // d_z
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-          F[a][k] = fma(fma(g2, rr[2][k], fma(g1, rr[1][k], g0 * rr[0][k])), idet,
-                        a == k ? 1.0 : 0.0);
-      }
-      double cof[3][3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const int a1 = (a + 1) % 3, a2 = (a + 2) % 3, k1 = (k + 1) % 3, k2 = (k + 2) % 3;
-          cof[a][k] = fma(F[a1][k1], F[a2][k2], -(F[a1][k2] * F[a2][k1]));
-        }
-      const double Jf = fma(F[0][2], cof[0][2], fma(F[0][1], cof[0][1], F[0][0] * cof[0][0]));
-      const double iJ = rcp64(Jf);
-      // P = mu F + (lambda ln J - mu) / J * cof(F)
-      const double beta = (lam * neo_log(Jf) - mu) * iJ;
-      // flux f_a[l] = w sign(det) sum_k r_l[k] P[a][k]
-      const double s = (wxy * T.W[q]) * (det < 0.0 ? -1.0 : 1.0);
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        double P[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) P[k] = fma(mu, F[a][k], beta * cof[a][k]);
-#pragma unroll
-        for (int l = 0; l < 3; ++l)
-          g[3 * a + l] = s * fma(rr[l][2], P[2], fma(rr[l][1], P[1], rr[l][0] * P[0]));
-      }
+      neo_point_flux(geo, T.Bc[M + q], wxy * T.W[q], mu, lam, g);
     };
     auto store_point = [&](int q, const double g[9]) {
 #pragma unroll
@@ -329,7 +275,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
       }
     }
     // (3) transposed z, in place: slot 2 <- Bz^T f_x, 1 <- Bz^T f_y, 0 <- Dz^T f_z
-#pragma unroll 1
+NEO_PRAGMA_A
     for (int a = 0; a < 3; ++a) {
       double fz[M], fy[M], fx[M];
       double* l0 = line + 3 * a * YA;
@@ -357,7 +303,7 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
   sync();
 
   // ---------------- transposed y / x stages, per component ---------------
-#pragma unroll 1
+NEO_PRAGMA_A
   for (int a = 0; a < 3; ++a) {
     if (tid < CPB * MN) {
       const int c = tid / MN, r = tid - c * MN;
@@ -468,6 +414,13 @@ static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const doub
   const int64_t ow = option(OPT_NEO_WARPS);   // 0: built-in, < 0: off
   const int warps = ow == 0 ? SFK_NEO_WARPS_DEFAULT : ow < 0 ? 0 : (int)ow;
   const int var = (int)option(OPT_NEO_CFG);   // 1: two points per pointwise iteration everywhere
+  // component-parallel kernel (hex_neohookean3.cu): option neo_cfg = 3 wherever
+  // it is instantiated, 4 nowhere
+  if (m == n + 1 && var == 3) {
+    const int rc = GS ? launch_hex_neohookean3_gs(p, ncells, cmap, w0, A, coords, s)
+                      : launch_hex_neohookean3(p, ncells, A, coords, w0, s);
+    if (rc != SFK_EUNSUPPORTED) return rc;
+  }
   if (m == n + 1 && warps > 0 && n <= 4) {
     // warp-synchronous: 3 / 2 / 1 cells per warp at p = 1 / 2 / 3
     if (warps == 8) {

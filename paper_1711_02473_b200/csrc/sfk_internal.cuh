@@ -119,6 +119,11 @@ int launch_hex_action_tc_gs(const sfk_plan* p, int64_t ncells, const int* cmap, 
                             double* y, const double* coords, cudaStream_t s);
 int launch_hex_neohookean_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                              double* y, const double* coords, cudaStream_t s);
+// component-parallel C4 kernel (hex_neohookean3.cu); SFK_EUNSUPPORTED where not instantiated
+int launch_hex_neohookean3(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                           const double* w0, cudaStream_t s);
+int launch_hex_neohookean3_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
+                              double* y, const double* coords, cudaStream_t s);
 int launch_hex_colloc_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                          double* y, const double* coords, const double* kappa, cudaStream_t s);
 int launch_hex_action_v5_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,

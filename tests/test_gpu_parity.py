@@ -284,6 +284,32 @@ def test_c4_vs_oracle(cuda, p):
     assert rel_err(_run(cuda, plan, small), ref) < TOL
 
 
+@pytest.mark.parametrize("p", range(2, 7))
+def test_c4_component_parallel_kernel(cuda, p):
+    """hex_neohookean3.cu (three thread groups, one per displacement
+    component; option neo_cfg = 3 forces it, 4 forces the line kernel): same
+    operation order as the line kernel, so bit-identical on finite cells, on a
+    ragged batch count (cells not a multiple of any CTA batch) and with
+    inverted cells (NaN as in the reference); parity with the oracle."""
+    plan = compile_form(neohookean_residual_form(), "hex", p, quadrature=p + 2)
+    inp = workloads.c4_inputs(p, dims=(3, 5, 7))
+    inp = {k: v[:101] for k, v in inp.items()}
+    with runtime.options(neo_cfg=4):
+        line = _run(cuda, plan, inp)
+    with runtime.options(neo_cfg=3):
+        comp = _run(cuda, plan, inp)
+    assert np.array_equal(np.isnan(comp), np.isnan(line))
+    assert np.array_equal(np.nan_to_num(comp), np.nan_to_num(line))
+    amp = 0.03 / p ** 2
+    small = {"coords": inp["coords"],
+             "w0": workloads.uniform_dofs(inp["coords"].shape[0], inp["w0"].shape[1],
+                                          -amp, amp, seed=11, scale=workloads.H)}
+    ref = cpu.evaluate(plan, small)
+    assert not np.isnan(ref).any()
+    with runtime.options(neo_cfg=3):
+        assert rel_err(_run(cuda, plan, small), ref) < TOL
+
+
 # ---------------------------------------------------------------------------
 # determinism, streams, threads, layouts
 

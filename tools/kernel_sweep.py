@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Auto-tuning sweeps of per-n launch policies:
+
+  c3  GLL-collocated weighted Laplace (csrc/hex_colloc.cu): persistent
+      prefetch, kappa from global memory, split z phase, min-blocks (register
+      cap), geometry form, cells per CTA, shared-memory strides
+  c4  neo-Hookean residual, component-parallel kernel
+      (csrc/hex_neohookean3.cu): cells per CTA, min-blocks, X / Y strides
+
+    python tools/kernel_sweep.py build FAMILY N [N ...]     # here (nvcc only)
+    python tools/kernel_sweep.py run FAMILY [N ...]         # on the GPU box
+
+`build` compiles the family's source once per variant with -DSFK_<F>_ONLY_N=n
+(-DSFK_<F>P_* = the variant, -DSFK_<F>_PROBE_ENTRY = its entry point) and
+links all variants of one n into paper_1711_02473_b200/probe/<f>_n<n>.so plus
+a manifest.  `run` times every variant on the BASELINE batch of that degree
+(same timing as tools/bench_configs.py), checks it against the product
+library's output, and prints one JSON line per variant.
+"""
+import concurrent.futures as cf
+import ctypes
+import itertools
+import json
+import os
+import re
+import statistics
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+PROBE = os.path.join(ROOT, "paper_1711_02473_b200", "probe")
+
+# the product dispatch table (hex_colloc.cu dispatch_colloc): n -> (CPB, SY, SX, CS)
+TABLE = {5: (10, 5, 25, 125), 6: (8, 6, 39, 244), 7: (5, 7, 52, 369), 8: (4, 9, 72, 576),
+         9: (3, 9, 89, 801), 10: (2, 11, 110, 1100), 11: (2, 11, 123, 1353),
+         12: (1, 13, 156, 1872), 13: (1, 13, 169, 2197), 14: (1, 17, 238, 3332),
+         15: (1, 15, 225, 3375), 16: (1, 17, 272, 4352), 17: (1, 17, 289, 4913)}
+SMEM_MAX = 227 * 1024
+
+
+def default_policy(n):
+    splitz = 12 <= n <= 15
+    if splitz:
+        minb = 3 if n <= 13 else 0 if n == 14 else 2
+    else:
+        minb = 2 if (n <= 7 or 9 <= n <= 13 or n == 16) else 0 if n in (8, 15) else 1
+    return dict(persist=int(n == 5), kg=int(n == 16), splitz=int(splitz), minb=minb,
+                geom=int(n in (15, 16)))
+
+
+def smem_bytes(n, cpb, cs, persist, kg):
+    arrays = (4 if kg else 6) if persist else (3 if kg else 4)
+    return 8 * (arrays * cpb * cs + (2 if persist else 1) * cpb * 24)
+
+
+def c3_variants(n):
+    cpb0, sy0, sx0, cs0 = TABLE[n]
+    strides = {(sy0, sx0, cs0), (n, n * n, n ** 3)}
+    so = n | 1
+    strides.add((so, so * n, so * n * n))
+    cpbs = sorted({max(1, cpb0 - 1), cpb0, cpb0 + 1, cpb0 * 2 if n <= 7 else cpb0})
+    out = []
+    for cpb, (sy, sx, cs), persist, kg, splitz in itertools.product(
+            cpbs, sorted(strides), (0, 1), (0, 1), (0, 1)):
+        threads = -(-cpb * n * n // 32) * 32
+        if threads > 1024:
+            continue
+        sm = smem_bytes(n, cpb, cs, persist, kg)
+        if sm > SMEM_MAX:
+            continue
+        by_smem = min(8, (228 * 1024) // (sm + 1024))
+        for minb in (0, 1, 2, 3, 4, 5):
+            if minb > by_smem or (minb and 65536 // (minb * threads) < 72):
+                continue
+            if minb == 1 and by_smem > 2:
+                continue
+            for geom in ((0, 1) if n >= 13 else (0,)):
+                out.append(dict(n=n, cpb=cpb, sy=sy, sx=sx, cs=cs, persist=persist, kg=kg,
+                                splitz=splitz, minb=minb, geom=geom, threads=threads, smem=sm))
+    return out
+
+
+def c3_defines(v, entry):
+    return ["-DSFK_C3_ONLY_N=%d" % v["n"], "-DSFK_C3P_CPB=%d" % v["cpb"],
+            "-DSFK_C3P_SY=%d" % v["sy"], "-DSFK_C3P_SX=%d" % v["sx"], "-DSFK_C3P_CS=%d" % v["cs"],
+            "-DSFK_C3P_PERSIST=%d" % v["persist"], "-DSFK_C3P_KG=%d" % v["kg"],
+            "-DSFK_C3P_SPLITZ=%d" % v["splitz"], "-DSFK_C3P_MINB=%d" % v["minb"],
+            "-DSFK_C3P_GEOM=%d" % v["geom"], "-DSFK_C3_PROBE_ENTRY=%s" % entry]
+
+
+def neo_px(n):
+    return {4: 20, 5: 37, 6: 38, 7: 55}.get(n, (n * n) | 1)
+
+
+def c4_variants(n):
+    m = n + 1
+    out = []
+    pxs = sorted({neo_px(n), (n * n) | 1})
+    for cpb, px, lz, ypad, nyt in itertools.product((1, 2, 3, 4), pxs, sorted({m | 1, m}), (0, 8),
+                                                    (0, 1)):
+        threads = -(-3 * cpb * m * m // 32) * 32
+        if threads > 1024:
+            continue
+        rup2 = lambda x: (x + 1) // 2 * 2
+        sm = 8 * (rup2(cpb * (6 * m * px + 9 * m * m * lz + ypad)) + rup2(cpb * 3 * n ** 3 + 1)
+                  + 2 * cpb * 24)
+        if sm > SMEM_MAX:
+            continue
+        by_smem = min(8, (228 * 1024) // (sm + 1024))
+        if cpb > 1 and 3 * cpb * m * m > 400:
+            continue
+        for minb in (0, 1, 2, 3, 4, 5, 6):
+            if minb > by_smem or (minb and 65536 // (minb * threads) < 80):
+                continue
+            out.append(dict(n=n, cpb=cpb, px=px, lz=lz, ypad=ypad, nyt=nyt, minb=minb,
+                            threads=threads, smem=sm))
+    return out
+
+
+def c4_defines(v, entry):
+    return ["-DSFK_C4_ONLY_N=%d" % v["n"], "-DSFK_C4P_CPB=%d" % v["cpb"],
+            "-DSFK_C4P_PX=%d" % v["px"], "-DSFK_C4P_LZ=%d" % v["lz"],
+            "-DSFK_C4P_YPAD=%d" % v["ypad"], "-DSFK_C4P_NYT=%d" % v["nyt"],
+            "-DSFK_C4P_MINB=%d" % v["minb"], "-DSFK_C4_PROBE_ENTRY=%s" % entry]
+
+
+# v6 product defaults (hex_action6.cu launch_hex_action_v6): n -> EO (parity-gated, fixed)
+V6_EO = {4: 0, 5: 1, 6: 1, 7: 0, 8: 0, 9: 0}
+
+
+def c2_variants(n):
+    out = []
+    nn = n * n
+    cpbs = {4: (2, 4, 6, 8, 12, 16), 5: (2, 3, 4, 5, 6, 8, 10), 6: (3, 4, 5, 6, 7, 8),
+            7: (2, 3, 4, 5, 6), 8: (2, 3, 4, 5), 9: (1, 2, 3, 4)}[n]
+    for cpb, ws, zr, eg, bk in itertools.product(cpbs, (0, 1), (0, 1), (0, 1), (0, 1)):
+        if ws and (nn > 32 or cpb % (32 // nn)):
+            continue
+        threads = 32 * (cpb // (32 // nn)) if ws else -(-cpb * nn // 32) * 32
+        if threads > 1024:
+            continue
+        for minb in (0, 1, 2, 3, 4, 5, 6, 8):
+            if minb and 65536 // (minb * threads) < 80:
+                continue
+            out.append(dict(n=n, cpb=cpb, ws=ws, zr=zr, eg=eg, bk=bk, eo=V6_EO[n], minb=minb,
+                            threads=threads, smem=0))
+    return out
+
+
+def c2_defines(v, entry):
+    return ["-DSFK_V6_ONLY_N=%d" % v["n"], "-DSFK_V6P_CPB=%d" % v["cpb"],
+            "-DSFK_V6P_MINB=%d" % v["minb"], "-DSFK_V6P_ZR=%d" % v["zr"],
+            "-DSFK_V6P_WS=%d" % v["ws"], "-DSFK_V6P_EG=%d" % v["eg"], "-DSFK_V6P_BK=%d" % v["bk"],
+            "-DSFK_V6P_EO=%d" % v["eo"], "-DSFK_V6_PROBE_ENTRY=%s" % entry]
+
+
+FAMILIES = {
+    "c3": dict(src="hex_colloc.cu", variants=c3_variants, defines=c3_defines,
+               keys=("cpb", "sy", "sx", "cs", "persist", "kg", "splitz", "minb", "geom")),
+    "c2": dict(src="hex_action6.cu", variants=c2_variants, defines=c2_defines,
+               keys=("cpb", "ws", "zr", "eg", "bk", "eo", "minb")),
+    "c4": dict(src="hex_neohookean3.cu", variants=c4_variants, defines=c4_defines,
+               keys=("cpb", "px", "lz", "ypad", "nyt", "minb")),
+}
+
+
+def _compile(job):
+    from paper_1711_02473_b200 import _build as B
+    fam, v, entry, obj = job
+    F = FAMILIES[fam]
+    src = os.path.join(B.CSRC, F["src"])
+    flags = [f for f in B.NVCC_FLAGS if f != "-lineinfo"]
+    r = subprocess.run([B.nvcc()] + flags + F["defines"](v, entry)
+                       + ["-Xptxas", "-v", "-c", src, "-o", obj], capture_output=True, text=True)
+    if r.returncode != 0:
+        return dict(v, entry=entry, error=r.stderr[-400:])
+    regs = [int(x) for x in re.findall(r"Used (\d+) registers", r.stderr)]
+    spills = [int(x) for x in re.findall(r"(\d+) bytes spill stores", r.stderr)]
+    return dict(v, entry=entry, regs=max(regs or [0]), spill=max(spills or [0]))
+
+
+def build(fam, ns):
+    from paper_1711_02473_b200 import _build as B
+    B.build_native()
+    os.makedirs(PROBE, exist_ok=True)
+    tmp = os.path.join(B.BUILD, fam + "probe")
+    os.makedirs(tmp, exist_ok=True)
+    sup = os.path.join(tmp, "probe_support.o")
+    subprocess.run([B.nvcc()] + B.NVCC_FLAGS + ["-c", os.path.join(ROOT, "tools", "probe_support.cu"),
+                                                "-o", sup], check=True)
+    for n in ns:
+        vs = FAMILIES[fam]["variants"](n)
+        jobs = [(fam, v, "sfk_%s_probe_%d" % (fam, i), os.path.join(tmp, "n%d_%d.o" % (n, i)))
+                for i, v in enumerate(vs)]
+        mpath = os.path.join(PROBE, "%s_n%d.json" % (fam, n))
+        if os.environ.get("SWEEP_RELINK") and os.path.exists(mpath):
+            res = json.load(open(mpath))
+        else:
+            with cf.ProcessPoolExecutor(max_workers=os.cpu_count()) as ex:
+                res = list(ex.map(_compile, jobs))
+        good = [r for r in res if "error" not in r and r["spill"] <= 64]
+        bad = [r for r in res if "error" in r]
+        if bad:
+            print("n=%d: %d variants failed to compile, e.g. %s" % (n, len(bad), bad[0]["error"]))
+        objs = [os.path.join(tmp, "n%d_%d.o" % (n, int(r["entry"].rsplit("_", 1)[1]))) for r in good]
+        out = os.path.join(PROBE, "%s_n%d.so" % (fam, n))
+        subprocess.run([B.nvcc()] + B.ARCH + ["-shared", "-o", out] + objs
+                       + [os.path.join(B.BUILD, "util.o"), os.path.join(B.BUILD, "options.o"), sup,
+                          "-cudart", "static", "-ldl"], check=True)
+        with open(mpath, "w") as f:
+            json.dump(good, f)
+        print("%s n=%d: %d variants (%d dropped for spills) -> %s (%.1f MB)"
+              % (fam, n, len(good), len(res) - len(good) - len(bad), out,
+                 os.path.getsize(out) / 1e6), flush=True)
+
+
+def run(fam, ns):
+    import numpy as np
+    import torch
+    from paper_1711_02473_b200 import runtime, workloads
+    from paper_1711_02473_b200.forms import REGISTRY, action_form, neohookean_residual_form
+    from paper_1711_02473_b200.plan import compile_form
+
+    dev = torch.device("cuda", 0)
+    lib = runtime.load_library()
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_rd = flush.view(torch.float64).view(8, -1)
+    flush_acc = torch.empty(flush_rd.shape[1], dtype=torch.float64, device=dev)
+    reps = int(os.environ.get("SWEEP_REPS", "5"))
+
+    def time_launch(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            torch.sum(flush_rd, dim=0, out=flush_acc)
+            torch.cuda._sleep(2_000_000)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        return statistics.median(ts)
+
+    if not ns:
+        ns = sorted(int(f[len(fam) + 2:-5]) for f in os.listdir(PROBE)
+                    if f.endswith(".json") and f.startswith(fam + "_n"))
+    vp, dp, i64 = ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64
+    for n in ns:
+        p = n - 1
+        man = json.load(open(os.path.join(PROBE, "%s_n%d.json" % (fam, n))))
+        plib = ctypes.CDLL(os.path.join(PROBE, "%s_n%d.so" % (fam, n)))
+        if fam == "c3":
+            plan = compile_form(action_form(REGISTRY["weighted_laplace"]), "hex", p,
+                                "spectral", "spectral_gll", "collocated-gll")
+            inp = workloads.c3_inputs(p)
+        elif fam == "c2":
+            from paper_1711_02473_b200 import compile_kernel
+            plan = compile_kernel("action_laplace", "hex", p)
+            inp = workloads.c2_inputs(p)
+        else:
+            plan = compile_form(neohookean_residual_form(), "hex", p, quadrature=p + 2)
+            inp = workloads.c4_inputs(p)
+        d = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in inp.items()}
+        C = d["coords"].shape[0]
+        ref = torch.empty_like(d["w0"])
+        out = torch.empty_like(d["w0"])
+        h = runtime.native_plan(plan)
+        w1 = d["w1"].data_ptr() if "w1" in d else None
+        args = lambda o: (h, C, o.data_ptr(), d["coords"].data_ptr(), d["w0"].data_ptr(),
+                          w1, stream.cuda_stream)
+        pargs = (lambda o: args(o)) if fam == "c3" else (lambda o: args(o)[:5] + args(o)[6:])
+        base = lambda: runtime._check(lib.sfk_eval(*args(ref)))
+        t0 = time_launch(base)
+        scale = torch.nan_to_num(ref, nan=0.0).abs().amax(dim=1).clamp_min(1e-300)
+        print(json.dumps({"n": n, "p": p, "variant": "product", "ms": round(t0 * 1e3, 5)}),
+              flush=True)
+        for v in man:
+            fn = getattr(plib, v["entry"])
+            fn.restype = ctypes.c_int
+            fn.argtypes = [vp, i64, dp, dp, dp, dp, vp] if fam == "c3" else [vp, i64, dp, dp, dp, vp]
+            out.fill_(float("nan"))
+            call = lambda: fn(*pargs(out))
+            rc = call()
+            torch.cuda.synchronize()
+            rec = {k: v[k] for k in ("n",) + FAMILIES[fam]["keys"]
+                   + ("threads", "smem", "regs", "spill")}
+            if rc != 0:
+                rec["rc"] = rc
+                print(json.dumps(rec), flush=True)
+                continue
+            # NaN cells of the reference (C4's inverted cells) must be NaN here too
+            both = torch.isnan(out) == torch.isnan(ref)
+            diff = torch.nan_to_num(out - ref, nan=0.0).abs().amax(dim=1)
+            err = float((diff / scale).max()) if bool(both.all()) else float("inf")
+            rec["err_vs_product"] = err
+            if not (err <= 1e-13):
+                rec["ms"] = None
+            else:
+                rec["ms"] = round(time_launch(call) * 1e3, 5)
+            print(json.dumps(rec), flush=True)
+        # the product kernel again, to bracket drift over the sweep
+        print(json.dumps({"n": n, "p": p, "variant": "product",
+                          "ms": round(time_launch(base) * 1e3, 5)}), flush=True)
+        del d, ref, out
+
+
+if __name__ == "__main__":
+    mode, fam, ns = sys.argv[1], sys.argv[2], [int(x) for x in sys.argv[3:]]
+    if mode == "build":
+        build(fam, ns)
+    elif mode == "count":
+        for n in ns:
+            print(n, len(FAMILIES[fam]["variants"](n)))
+    else:
+        run(fam, ns)
