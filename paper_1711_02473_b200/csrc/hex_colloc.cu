@@ -134,6 +134,16 @@ __host__ __device__ constexpr bool colloc_splitz(int n) {
 #endif
 }
 
+// FUSE bit 0: phase 2 runs the thread's x-line and y-line together, bit 1:
+// phases 4 / 5 compute Dx^T f_x and Dy^T f_y together (the y result waits in
+// registers for the barrier) — the two contractions share the table D, so
+// each constant (one LDCU per DFMA in the separate form) feeds two DFMAs.
+// Same operations in the same order per output: bit-identical.
+#ifndef SFK_C3P_FUSE
+#define SFK_C3P_FUSE -1
+#endif
+__host__ __device__ constexpr int colloc_fuse(int n) { return c3p(n, SFK_C3P_FUSE, 0); }
+
 __host__ __device__ constexpr int colloc_minb(int n) {
 #ifdef SFK_COLLOC_MINB
   if (SFK_COLLOC_MINB >= 0) return SFK_COLLOC_MINB;   // A/B builds (tools/build_variant.py)
@@ -261,7 +271,27 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
     const int cb = c * CS;
 
     // ---- phase 2: x-line (y=a, z=b) and y-line (x=a, z=b) ---------------
-    if (act) {
+    constexpr int FUSE = colloc_fuse(N);
+    if ((FUSE & 1) && act) {
+      double ux[N], uy[N];
+  #pragma unroll
+      for (int i = 0; i < N; ++i) {
+        ux[i] = sU[cb + i * SX + a * SY + b];
+        uy[i] = sU[cb + a * SX + i * SY + b];
+      }
+  #pragma unroll
+      for (int q = 0; q < N; ++q) {
+        double gx = T.D[q] * ux[0], gy = T.D[q] * uy[0];
+  #pragma unroll
+        for (int i = 1; i < N; ++i) {
+          gx = fma(T.D[i * N + q], ux[i], gx);
+          gy = fma(T.D[i * N + q], uy[i], gy);
+        }
+        sGX[c * GXC + q * GXX + a * GXY + b] = gx;
+        sGY[c * GYC + a * GYX + q * GYY + b] = gy;
+      }
+    }
+    if (!(FUSE & 1) && act) {
       double ul[N];
   #pragma unroll
       for (int i = 0; i < N; ++i) ul[i] = sU[cb + i * SX + a * SY + b];
@@ -379,6 +409,36 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
     }
     sync();
 
+    if (FUSE & 2) {
+      // ---- phases 4 + 5 fused: both transposed contractions share D -------
+      double sy[N];
+      if (act) {
+        double fx[N], fy[N];
+  #pragma unroll
+        for (int q = 0; q < N; ++q) {
+          fx[q] = sGX[c * GXC + q * GXX + a * GXY + b];
+          fy[q] = sGY[c * GYC + a * GYX + q * GYY + b];
+        }
+  #pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double s = T.D[i * N] * fx[0];
+          double t = T.D[i * N] * fy[0];
+  #pragma unroll
+          for (int q = 1; q < N; ++q) {
+            s = fma(T.D[i * N + q], fx[q], s);
+            t = fma(T.D[i * N + q], fy[q], t);
+          }
+          sU[cb + i * SX + a * SY + b] += s;
+          sy[i] = t;
+        }
+      }
+      sync();
+      if (act) {
+  #pragma unroll
+        for (int i = 0; i < N; ++i) sU[cb + a * SX + i * SY + b] += sy[i];
+      }
+      sync();
+    } else {
     // ---- phase 4: x-lines (y=a, z=b): U += Dx^T f_x ----------------------
     if (act) {
       double fl[N];
@@ -408,6 +468,8 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
       }
     }
     sync();
+
+    }
 
     {
       // coalesced write-back: consecutive threads take consecutive elements of

@@ -26,18 +26,21 @@
 #include "hex_geometry.cuh"
 #include "hex_neohookean_point.cuh"
 
-// component loops: rolled (one copy of each stage's code) or unrolled x3 —
-// rolled, ptxas hoists the stages' table constants out of the loop into vector
+// Component loops: rolled (one copy of each stage's code) or unrolled x3.
+// Rolled, ptxas hoists the stages' table constants out of the loop into vector
 // registers and moves them back to uniform registers at every use (R2UR: 15%
-// of the executed instructions at p = 4, profiles/r02ce_C4_p4_opmix.txt)
+// of the executed instructions at p = 4, profiles/r02ce_C4_p4_opmix.txt);
+// unrolled, the constants are loaded where they are used.  Same-box A/B
+// (profiles/r02cg_c4_*.jsonl): p = 2 0.1603 -> 0.1557, p = 4 0.6758 -> 0.6492
+// ms; neutral at p = 3, slower at p = 5, 6 (220-254 registers) — so n = 3, 5.
+// SFK_NEO_UNROLLA = 0 / 1 (A/B builds) forces rolled / unrolled everywhere.
 #ifndef SFK_NEO_UNROLLA
-#define SFK_NEO_UNROLLA 0
+#define SFK_NEO_UNROLLA -1
 #endif
-#if SFK_NEO_UNROLLA
-#define NEO_PRAGMA_A _Pragma("unroll")
-#else
-#define NEO_PRAGMA_A _Pragma("unroll 1")
-#endif
+__host__ __device__ constexpr int neo_unroll_a(int n) {
+  return (SFK_NEO_UNROLLA >= 0 ? SFK_NEO_UNROLLA != 0 : (n == 3 || n == 5)) ? 3 : 1;
+}
+#define NEO_PRAGMA_A _Pragma("unroll (neo_unroll_a(N))")
 
 #ifndef SFK_NEO_YT
 #define SFK_NEO_YT 1
@@ -416,7 +419,9 @@ static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const doub
   const int var = (int)option(OPT_NEO_CFG);   // 1: two points per pointwise iteration everywhere
   // component-parallel kernel (hex_neohookean3.cu): option neo_cfg = 3 wherever
   // it is instantiated, 4 nowhere
-  if (m == n + 1 && var == 3) {
+  // Default at p = 5 (n = 6): 1.2565 -> 1.187 ms; the line kernel stays ahead
+  // at the other degrees (tools/kernel_sweep.py c4, profiles/r02cd_c4_sweep.jsonl).
+  if (m == n + 1 && (var == 3 || (n == 6 && var == 0))) {
     const int rc = GS ? launch_hex_neohookean3_gs(p, ncells, cmap, w0, A, coords, s)
                       : launch_hex_neohookean3(p, ncells, A, coords, w0, s);
     if (rc != SFK_EUNSUPPORTED) return rc;

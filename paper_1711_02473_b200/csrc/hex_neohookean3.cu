@@ -322,17 +322,18 @@ extern "C" int SFK_C4_PROBE_ENTRY(const sfk_plan* p, int64_t ncells, double* A,
 namespace sfk {
 #else
 
-// (cells per CTA, strides, min CTAs per SM) per n from tools/kernel_sweep.py
+// (cells per CTA, strides, min CTAs per SM) per n: the fastest variant of
+// tools/kernel_sweep.py c4 (profiles/r02cd_c4_sweep.jsonl)
 template <bool GS>
 static int dispatch_neo3(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, cudaStream_t s, const int* cmap) {
   if (p->m != p->n + 1) return SFK_EUNSUPPORTED;
   switch (p->n) {
     case 3: return launch_neo3<3, 4, 2, 9, 5, 0, false, 0, GS>(p, ncells, A, coords, w0, s, cmap);
-    case 4: return launch_neo3<4, 5, 1, 20, 5, 8, false, 0, GS>(p, ncells, A, coords, w0, s, cmap);
-    case 5: return launch_neo3<5, 6, 1, 37, 7, 0, false, 0, GS>(p, ncells, A, coords, w0, s, cmap);
-    case 6: return launch_neo3<6, 7, 1, 38, 7, 8, true, 0, GS>(p, ncells, A, coords, w0, s, cmap);
-    case 7: return launch_neo3<7, 8, 1, 55, 9, 0, false, 0, GS>(p, ncells, A, coords, w0, s, cmap);
+    case 4: return launch_neo3<4, 5, 2, 20, 5, 8, false, 3, GS>(p, ncells, A, coords, w0, s, cmap);
+    case 5: return launch_neo3<5, 6, 1, 37, 6, 8, true, 0, GS>(p, ncells, A, coords, w0, s, cmap);
+    case 6: return launch_neo3<6, 7, 1, 38, 7, 0, true, 3, GS>(p, ncells, A, coords, w0, s, cmap);
+    case 7: return launch_neo3<7, 8, 1, 55, 9, 0, false, 2, GS>(p, ncells, A, coords, w0, s, cmap);
     default: return SFK_EUNSUPPORTED;
   }
 }

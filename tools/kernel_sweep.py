@@ -32,10 +32,13 @@ sys.path.insert(0, ROOT)
 PROBE = os.path.join(ROOT, "paper_1711_02473_b200", "probe")
 
 # the product dispatch table (hex_colloc.cu dispatch_colloc): n -> (CPB, SY, SX, CS)
-TABLE = {5: (10, 5, 25, 125), 6: (8, 6, 39, 244), 7: (5, 7, 52, 369), 8: (4, 9, 72, 576),
-         9: (3, 9, 89, 801), 10: (2, 11, 110, 1100), 11: (2, 11, 123, 1353),
-         12: (1, 13, 156, 1872), 13: (1, 13, 169, 2197), 14: (1, 17, 238, 3332),
+TABLE = {5: (10, 5, 25, 125), 6: (7, 6, 36, 216), 7: (5, 7, 52, 369), 8: (4, 9, 72, 576),
+         9: (3, 9, 81, 729), 10: (1, 10, 100, 1000), 11: (1, 11, 121, 1331),
+         12: (1, 12, 144, 1728), 13: (1, 13, 169, 2197), 14: (1, 14, 196, 2744),
          15: (1, 15, 225, 3375), 16: (1, 17, 272, 4352), 17: (1, 17, 289, 4913)}
+# first-level sweep (profiles/r02cb_c3_sweep.jsonl) used the round-1 table:
+# 6: (8, 6, 39, 244), 9: (3, 9, 89, 801), 10: (2, 11, 110, 1100), 11: (2, 11, 123, 1353),
+# 12: (1, 13, 156, 1872), 14: (1, 17, 238, 3332); SWEEP_LEVEL=1 re-runs its variant space
 SMEM_MAX = 227 * 1024
 
 
@@ -55,6 +58,8 @@ def smem_bytes(n, cpb, cs, persist, kg):
 
 
 def c3_variants(n):
+    if os.environ.get("SWEEP_LEVEL", "2") == "2":
+        return c3_variants_l2(n)
     cpb0, sy0, sx0, cs0 = TABLE[n]
     strides = {(sy0, sx0, cs0), (n, n * n, n ** 3)}
     so = n | 1
@@ -81,12 +86,34 @@ def c3_variants(n):
     return out
 
 
+def c3_variants_l2(n):
+    """Second level: the product layout, FUSE x persist-free policy knobs."""
+    cpb, sy, sx, cs = TABLE[n]
+    out = []
+    threads = -(-cpb * n * n // 32) * 32
+    for fuse, kg, splitz in itertools.product((0, 1, 2, 3), (0, 1), (0, 1)):
+        sm = smem_bytes(n, cpb, cs, 0, kg)
+        if sm > SMEM_MAX:
+            continue
+        by_smem = min(8, (228 * 1024) // (sm + 1024))
+        for minb in (0, 1, 2, 3, 4, 5, 6):
+            if minb > by_smem or (minb and 65536 // (minb * threads) < 72):
+                continue
+            if minb == 1 and by_smem > 2:
+                continue
+            out.append(dict(n=n, cpb=cpb, sy=sy, sx=sx, cs=cs, persist=0, kg=kg, splitz=splitz,
+                            minb=minb, geom=int(n in (15, 16)), fuse=fuse, threads=threads,
+                            smem=sm))
+    return out
+
+
 def c3_defines(v, entry):
     return ["-DSFK_C3_ONLY_N=%d" % v["n"], "-DSFK_C3P_CPB=%d" % v["cpb"],
             "-DSFK_C3P_SY=%d" % v["sy"], "-DSFK_C3P_SX=%d" % v["sx"], "-DSFK_C3P_CS=%d" % v["cs"],
             "-DSFK_C3P_PERSIST=%d" % v["persist"], "-DSFK_C3P_KG=%d" % v["kg"],
             "-DSFK_C3P_SPLITZ=%d" % v["splitz"], "-DSFK_C3P_MINB=%d" % v["minb"],
-            "-DSFK_C3P_GEOM=%d" % v["geom"], "-DSFK_C3_PROBE_ENTRY=%s" % entry]
+            "-DSFK_C3P_GEOM=%d" % v["geom"], "-DSFK_C3P_FUSE=%d" % v.get("fuse", 0),
+            "-DSFK_C3_PROBE_ENTRY=%s" % entry]
 
 
 def neo_px(n):
@@ -157,7 +184,7 @@ def c2_defines(v, entry):
 
 FAMILIES = {
     "c3": dict(src="hex_colloc.cu", variants=c3_variants, defines=c3_defines,
-               keys=("cpb", "sy", "sx", "cs", "persist", "kg", "splitz", "minb", "geom")),
+               keys=("cpb", "sy", "sx", "cs", "persist", "kg", "splitz", "minb", "geom", "fuse")),
     "c2": dict(src="hex_action6.cu", variants=c2_variants, defines=c2_defines,
                keys=("cpb", "ws", "zr", "eg", "bk", "eo", "minb")),
     "c4": dict(src="hex_neohookean3.cu", variants=c4_variants, defines=c4_defines,
@@ -288,7 +315,7 @@ def run(fam, ns):
             call = lambda: fn(*pargs(out))
             rc = call()
             torch.cuda.synchronize()
-            rec = {k: v[k] for k in ("n",) + FAMILIES[fam]["keys"]
+            rec = {k: v.get(k, 0) for k in ("n",) + FAMILIES[fam]["keys"]
                    + ("threads", "smem", "regs", "spill")}
             if rc != 0:
                 rec["rc"] = rc
