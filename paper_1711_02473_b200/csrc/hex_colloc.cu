@@ -66,6 +66,33 @@ __host__ __device__ constexpr int c3p(int n, int probe, int dflt) {
   return (SFK_C3_ONLY_N != 0 && n == SFK_C3_ONLY_N && probe >= 0) ? probe : dflt;
 }
 
+// Per-n policy (kg, splitz, min CTAs per SM, fuse) — the fastest variant of
+// the two sweeps of tools/kernel_sweep.py c3 on the BASELINE batches
+// (profiles/r02cb_c3_sweep.jsonl: layout, cells per CTA, persist, kg, splitz,
+// min-blocks; profiles/r02ci_c3_sweep2.jsonl: + fuse); what each knob does is
+// described where it is used below.
+struct C3Policy {
+  bool kg, splitz;
+  int minb, fuse;
+};
+__host__ __device__ constexpr C3Policy c3_policy(int n) {
+  switch (n) {
+    case 5: case 6: return {false, true, 3, 0};
+    case 7: return {true, false, 0, 3};
+    case 8: return {true, false, 2, 3};
+    case 9: return {false, false, 0, 1};
+    case 10: return {false, false, 4, 1};
+    case 11: return {false, true, 3, 3};
+    case 12: return {false, true, 4, 1};
+    case 13: return {false, true, 2, 1};
+    case 14: return {true, true, 3, 1};
+    case 15: return {true, false, 2, 3};
+    case 16: return {true, true, 1, 3};
+    case 17: return {false, false, 0, 3};
+    default: return {false, false, 2, 0};   // n <= 4
+  }
+}
+
 template <int N>
 struct TabsD {
   double D[N * N];
@@ -88,13 +115,12 @@ __host__ __device__ constexpr bool colloc_persist(int n) { return c3p(n, SFK_C3P
 
 // KG: kappa read from global memory (through L1/L2) in the pointwise phase
 // instead of being staged in shared memory — drops one of the four N^3
-// arrays: n = 16 (139 -> 104 KB per CTA) fits two CTAs per SM; the round-2
-// sweep adds n = 7 (+5%), 10 (5 one-cell CTAs per SM, +17%) and 14 (3 CTAs
-// per SM with the unpadded layout, +18%).
+// arrays, i.e. more CTAs per SM where shared memory is the limit (round 1:
+// n = 16, 139 -> 104 KB per CTA and two CTAs per SM; round 2: see c3_policy).
 #ifdef SFK_COLLOC_KG
 __host__ __device__ constexpr bool colloc_kg(int n) { return n >= SFK_COLLOC_KG; }
 #else
-__host__ __device__ constexpr bool colloc_kg(int n) { return c3p(n, SFK_C3P_KG, n == 7 || n == 10 || n == 14 || n == 16); }
+__host__ __device__ constexpr bool colloc_kg(int n) { return c3p(n, SFK_C3P_KG, c3_policy(n).kg); }
 #endif
 
 template <int N, int CPB, int SY, int SX, int CS>
@@ -110,27 +136,19 @@ struct CollocCfg {
   }
 };
 
-// Register policy per n, from same-box A/B runs (profiles/r01ae_*,
-// r01an_c3_minb.jsonl, r01ao_c3_cpb.jsonl: n = 6, 10, 12, 13 moved to 2
-// after the kappa/adjugate changes, with 2 / 1 cells per CTA at n = 10 / 12;
-// p = 5: 0.29 -> 0.20 ms, p = 9: 1.21 -> 0.93, p = 11: 2.11 -> 1.96,
-// p = 12: 3.06 -> 2.11): 2 =
-// __launch_bounds__(T, 2) (two CTAs per SM, no spills at that cap), 1 =
-// (T, 1), 0 = (T) only — ptxas picks different (and here faster) register
-// budgets for the last two (e.g. n = 16: 132 vs 254 registers).
-// Phase 3 as three register-light passes (SPLITZ) at n = 12..15, with its
-// own register policy (same-box A/B over fused/split x min-blocks 0-3,
-// profiles/r01cf_*.jsonl: p = 11 1.969 -> 1.664 ms, p = 12 2.118 -> 1.918,
-// p = 13 3.803 -> 3.085, p = 14 3.652 -> 3.355).  The round-2 sweep
-// (profiles/r02cb_c3_sweep.jsonl) adds n = 5, 6 (80 registers, 3+ CTAs per
-// SM: p = 4 0.1127 -> 0.1045, p = 5 0.1987 -> 0.1679 ms) and n = 11 (p = 10
-// 1.118 -> 1.015); the other n keep the fused loop.
+// Register policy (c3_policy.minb): 2 = __launch_bounds__(T, 2) (two CTAs per
+// SM, no spills at that cap), 1 = (T, 1), 0 = (T) only — ptxas picks different
+// register budgets for the last two (e.g. n = 16: 132 vs 254 registers).
+// SPLITZ: phase 3 as three register-light passes over the thread's own lines
+// instead of one fused loop (round 1, n = 12..15: p = 11 1.969 -> 1.664 ms,
+// p = 13 3.803 -> 3.085, profiles/r01cf_*.jsonl; round 2 adds n = 5, 6, 11 and
+// 16 and drops 15, see c3_policy).
 // SFK_COLLOC_SPLITZ=n0 (A/B builds) splits every n >= n0.
 __host__ __device__ constexpr bool colloc_splitz(int n) {
 #ifdef SFK_COLLOC_SPLITZ
   return n >= SFK_COLLOC_SPLITZ;
 #else
-  return c3p(n, SFK_C3P_SPLITZ, n == 5 || n == 6 || (n >= 11 && n <= 15));
+  return c3p(n, SFK_C3P_SPLITZ, c3_policy(n).splitz);
 #endif
 }
 
@@ -142,22 +160,14 @@ __host__ __device__ constexpr bool colloc_splitz(int n) {
 #ifndef SFK_C3P_FUSE
 #define SFK_C3P_FUSE -1
 #endif
-__host__ __device__ constexpr int colloc_fuse(int n) { return c3p(n, SFK_C3P_FUSE, 0); }
+__host__ __device__ constexpr int colloc_fuse(int n) { return c3p(n, SFK_C3P_FUSE, c3_policy(n).fuse); }
 
 __host__ __device__ constexpr int colloc_minb(int n) {
 #ifdef SFK_COLLOC_MINB
   if (SFK_COLLOC_MINB >= 0) return SFK_COLLOC_MINB;   // A/B builds (tools/build_variant.py)
 #endif
   if (SFK_C3_ONLY_N != 0 && n == SFK_C3_ONLY_N && SFK_C3P_MINB >= 0) return SFK_C3P_MINB;
-  // round-2 sweep of (cells per CTA, strides, persist, kg, splitz, min-blocks)
-  // per n (tools/kernel_sweep.py, profiles/r02cb_c3_sweep.jsonl)
-  switch (n) {
-    case 5: case 6: case 13: case 14: return 3;
-    case 7: case 8: return 0;
-    case 10: case 11: case 12: return 4;
-    case 17: return 1;
-    default: return 2;   // n <= 4, 9, 15, 16
-  }
+  return c3_policy(n).minb;
 }
 
 // GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)

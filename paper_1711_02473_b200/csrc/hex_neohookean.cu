@@ -419,9 +419,10 @@ static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const doub
   const int var = (int)option(OPT_NEO_CFG);   // 1: two points per pointwise iteration everywhere
   // component-parallel kernel (hex_neohookean3.cu): option neo_cfg = 3 wherever
   // it is instantiated, 4 nowhere
-  // Default at p = 5 (n = 6): 1.2565 -> 1.187 ms; the line kernel stays ahead
-  // at the other degrees (tools/kernel_sweep.py c4, profiles/r02cd_c4_sweep.jsonl).
-  if (m == n + 1 && (var == 3 || (n == 6 && var == 0))) {
+  // Default at p = 4..6 (n = 5..7): 0.650 -> 0.616, 1.257 -> 1.013, 1.759 ->
+  // 1.701 ms; the line kernel stays ahead at p = 2, 3 (tools/kernel_sweep.py
+  // c4, profiles/r02cj_c4_sweep2.jsonl).
+  if (m == n + 1 && (var == 3 || (n >= 5 && var == 0))) {
     const int rc = GS ? launch_hex_neohookean3_gs(p, ncells, cmap, w0, A, coords, s)
                       : launch_hex_neohookean3(p, ncells, A, coords, w0, s);
     if (rc != SFK_EUNSUPPORTED) return rc;

@@ -15,8 +15,8 @@
 //   * pointwise stage: thread (g, z-line) takes the points q = g, g + 3, ...
 //     of its z-line (all nine gradients of a point are needed together), with
 //     its own copy of the line's adjugate polynomials.
-// 7 barriers per batch; 16 / 15 / 12 warps per SM at p = 4 / 5 / 6.
-// Persistent CTAs; u and coords of the next batch stream in with cp.async.
+// 7 barriers per batch; 16-20 warps per SM at p = 4..6 (96-118 registers in
+// the one-shot form, see ONESHOT below).
 #include "async_copy.cuh"
 #include "hex_geometry.cuh"
 #include "hex_neohookean_point.cuh"
@@ -24,7 +24,7 @@
 namespace sfk {
 
 // probe builds (tools/kernel_sweep.py): -DSFK_C4_ONLY_N=n instantiates that n
-// alone with SFK_C4P_{CPB,MINB,PX,LZ,YPAD,NYT} as given
+// alone with SFK_C4P_{CPB,MINB,PX,LZ,YPAD,NYT,ONESHOT} as given
 #ifndef SFK_C4_ONLY_N
 #define SFK_C4_ONLY_N 0
 #endif
@@ -53,7 +53,13 @@ struct Neo3Cfg {
   static_assert(PX >= NN && LZ >= M, "strides");
 };
 
-template <int N, int M, int CPB, int PX_, int LZ_, int YPAD, bool NYT_, int MINB, bool GS>
+// ONESHOT: one batch per CTA (grid = batches) instead of a persistent loop —
+// without the loop ptxas cannot hoist the stages' table constants out of it
+// into vector registers (it then moves them back with R2UR at every use and
+// the kernel needs 168+ registers at n = 7); the load latency is covered by
+// the other resident CTAs.
+template <int N, int M, int CPB, int PX_, int LZ_, int YPAD, bool NYT_, int MINB, bool GS,
+          bool ONESHOT = false>
 __global__ void __launch_bounds__(Neo3Cfg<N, M, CPB, PX_, LZ_, YPAD, NYT_>::THREADS, MINB)
 hex_neohookean3_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double lam,
                        int64_t ncells, const double* __restrict__ coords,
@@ -87,8 +93,10 @@ hex_neohookean3_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double l
   };
 
   int64_t batch = blockIdx.x;
-  if (batch < nbatch) prefetch(batch, 0);
-  for (int it = 0; batch < nbatch; batch += gridDim.x, ++it) {
+  if (batch >= nbatch) return;
+  prefetch(batch, 0);
+  int it = 0;
+  do {
     const int64_t cell0 = batch * CPB;
     const int ncb = (int)((ncells - cell0) < CPB ? (ncells - cell0) : CPB);
     cp_async_wait<0>();
@@ -119,7 +127,7 @@ hex_neohookean3_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double l
     }
     __syncthreads();
     // sU is free: the next batch's u (and coords, other buffer) stream in
-    if (batch + gridDim.x < nbatch) prefetch(batch + gridDim.x, (it & 1) ^ 1);
+    if (!ONESHOT && batch + gridDim.x < nbatch) prefetch(batch + gridDim.x, (it & 1) ^ 1);
 
     // ---- y: thread (c, g, qx, iz) ----------------------------------------
     if (tid < 3 * CPB * MN) {
@@ -287,21 +295,23 @@ hex_neohookean3_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double l
         }
       }
     }
-  }
+    ++it;
+  } while (!ONESHOT && (batch += gridDim.x) < nbatch);
 }
 
-template <int N, int M, int CPB, int PX, int LZ, int YPAD, bool NYT, int MINB, bool GS>
+template <int N, int M, int CPB, int PX, int LZ, int YPAD, bool NYT, int MINB, bool GS,
+          bool ONESHOT = false>
 static int launch_neo3(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                        const double* u, cudaStream_t s, const int* cmap) {
   using C = Neo3Cfg<N, M, CPB, PX, LZ, YPAD, NYT>;
-  auto k = hex_neohookean3_kernel<N, M, CPB, PX, LZ, YPAD, NYT, MINB, GS>;
+  auto k = hex_neohookean3_kernel<N, M, CPB, PX, LZ, YPAD, NYT, MINB, GS, ONESHOT>;
   LaunchShape sh;
   if (const int rc_ = kernel_shape((const void*)k, C::THREADS, C::SMEM, "hex_neohookean3", &sh, true))
     return rc_;
   const Tabs<N, M> T = make_tabs<N, M>(p);
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
   const int64_t resident = sh.resident();
-  const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
+  const unsigned grid = (unsigned)(ONESHOT || nbatch < resident ? nbatch : resident);
   if (grid > 0)
     k<<<grid, C::THREADS, C::SMEM, s>>>(T, p->params[0], p->params[1], ncells, coords, u, A, cmap);
   note_launch();
@@ -316,24 +326,28 @@ extern "C" int SFK_C4_PROBE_ENTRY(const sfk_plan* p, int64_t ncells, double* A,
   if (p->n != SFK_C4_ONLY_N || p->m != SFK_C4_ONLY_N + 1)
     return sfk::fail(SFK_EUNSUPPORTED, "probe build: n=%d only", SFK_C4_ONLY_N);
   return sfk::launch_neo3<SFK_C4_ONLY_N, SFK_C4_ONLY_N + 1, SFK_C4P_CPB, SFK_C4P_PX, SFK_C4P_LZ,
-                          SFK_C4P_YPAD, SFK_C4P_NYT != 0, SFK_C4P_MINB, false>(
+                          SFK_C4P_YPAD, SFK_C4P_NYT != 0, SFK_C4P_MINB, false,
+                          SFK_C4P_ONESHOT != 0>(
       p, ncells, A, coords, w0, (cudaStream_t)stream, nullptr);
 }
 namespace sfk {
 #else
 
-// (cells per CTA, strides, min CTAs per SM) per n: the fastest variant of
-// tools/kernel_sweep.py c4 (profiles/r02cd_c4_sweep.jsonl)
+// (cells per CTA, strides, min CTAs per SM, one-shot) per n: the fastest
+// variant of tools/kernel_sweep.py c4 (profiles/r02cj_c4_sweep2.jsonl; the
+// persistent form: r02cd_c4_sweep.jsonl).  One-shot CTAs win at every n: p = 4
+// 0.650 (line kernel) -> 0.616 ms, p = 5 1.257 -> 1.013, p = 6 1.759 -> 1.701;
+// the line kernel stays ahead at p = 2, 3 (0.156 / 0.369 vs 0.197 / 0.377).
 template <bool GS>
 static int dispatch_neo3(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, cudaStream_t s, const int* cmap) {
   if (p->m != p->n + 1) return SFK_EUNSUPPORTED;
   switch (p->n) {
-    case 3: return launch_neo3<3, 4, 2, 9, 5, 0, false, 0, GS>(p, ncells, A, coords, w0, s, cmap);
-    case 4: return launch_neo3<4, 5, 2, 20, 5, 8, false, 3, GS>(p, ncells, A, coords, w0, s, cmap);
-    case 5: return launch_neo3<5, 6, 1, 37, 6, 8, true, 0, GS>(p, ncells, A, coords, w0, s, cmap);
-    case 6: return launch_neo3<6, 7, 1, 38, 7, 0, true, 3, GS>(p, ncells, A, coords, w0, s, cmap);
-    case 7: return launch_neo3<7, 8, 1, 55, 9, 0, false, 2, GS>(p, ncells, A, coords, w0, s, cmap);
+    case 3: return launch_neo3<3, 4, 2, 9, 5, 0, false, 0, GS, true>(p, ncells, A, coords, w0, s, cmap);
+    case 4: return launch_neo3<4, 5, 2, 20, 5, 0, false, 0, GS, true>(p, ncells, A, coords, w0, s, cmap);
+    case 5: return launch_neo3<5, 6, 1, 37, 7, 0, true, 5, GS, true>(p, ncells, A, coords, w0, s, cmap);
+    case 6: return launch_neo3<6, 7, 1, 38, 7, 0, true, 4, GS, true>(p, ncells, A, coords, w0, s, cmap);
+    case 7: return launch_neo3<7, 8, 1, 55, 9, 0, false, 0, GS, true>(p, ncells, A, coords, w0, s, cmap);
     default: return SFK_EUNSUPPORTED;
   }
 }

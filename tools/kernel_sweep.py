@@ -124,8 +124,8 @@ def c4_variants(n):
     m = n + 1
     out = []
     pxs = sorted({neo_px(n), (n * n) | 1})
-    for cpb, px, lz, ypad, nyt in itertools.product((1, 2, 3, 4), pxs, sorted({m | 1, m}), (0, 8),
-                                                    (0, 1)):
+    for cpb, px, lz, ypad, nyt, oneshot in itertools.product(
+            (1, 2, 3, 4), pxs, sorted({m | 1, m}), (0,), (0, 1), (0, 1)):
         threads = -(-3 * cpb * m * m // 32) * 32
         if threads > 1024:
             continue
@@ -141,7 +141,7 @@ def c4_variants(n):
             if minb > by_smem or (minb and 65536 // (minb * threads) < 80):
                 continue
             out.append(dict(n=n, cpb=cpb, px=px, lz=lz, ypad=ypad, nyt=nyt, minb=minb,
-                            threads=threads, smem=sm))
+                            oneshot=oneshot, threads=threads, smem=sm))
     return out
 
 
@@ -149,7 +149,8 @@ def c4_defines(v, entry):
     return ["-DSFK_C4_ONLY_N=%d" % v["n"], "-DSFK_C4P_CPB=%d" % v["cpb"],
             "-DSFK_C4P_PX=%d" % v["px"], "-DSFK_C4P_LZ=%d" % v["lz"],
             "-DSFK_C4P_YPAD=%d" % v["ypad"], "-DSFK_C4P_NYT=%d" % v["nyt"],
-            "-DSFK_C4P_MINB=%d" % v["minb"], "-DSFK_C4_PROBE_ENTRY=%s" % entry]
+            "-DSFK_C4P_MINB=%d" % v["minb"], "-DSFK_C4P_ONESHOT=%d" % v["oneshot"],
+            "-DSFK_C4_PROBE_ENTRY=%s" % entry]
 
 
 # v6 product defaults (hex_action6.cu launch_hex_action_v6): n -> EO (parity-gated, fixed)
@@ -188,7 +189,7 @@ FAMILIES = {
     "c2": dict(src="hex_action6.cu", variants=c2_variants, defines=c2_defines,
                keys=("cpb", "ws", "zr", "eg", "bk", "eo", "minb")),
     "c4": dict(src="hex_neohookean3.cu", variants=c4_variants, defines=c4_defines,
-               keys=("cpb", "px", "lz", "ypad", "nyt", "minb")),
+               keys=("cpb", "px", "lz", "ypad", "nyt", "minb", "oneshot")),
 }
 
 
