@@ -134,9 +134,14 @@ hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double la
     async_copy<TH>(sCo + buf * C::CSZ, coords + c0 * 24, nc * 24, tid);
     cp_async_commit();
   };
+  // VAR bit 1: one batch per CTA (grid = batches) instead of the persistent
+  // loop (cf. hex_neohookean3.cu ONESHOT)
+  constexpr bool OS = (VAR & 2) != 0;
   int64_t batch = blockIdx.x;
-  if (batch < nbatch) prefetch(batch, 0);
-  for (int it = 0; batch < nbatch; batch += gridDim.x, ++it) {
+  if (batch >= nbatch) return;
+  prefetch(batch, 0);
+  int it = 0;
+  do {
   const int64_t cell0 = batch * (CPB * GROUPS) + grp * CPB;
   const int ncb = (int)((ncells - cell0) < CPB ? ((ncells - cell0) > 0 ? ncells - cell0 : 0)
                                                 : CPB);
@@ -168,7 +173,7 @@ NEO_PRAGMA_A
       }
     }
     sync();
-    if (a == 2 && batch + gridDim.x < nbatch) prefetch(batch + gridDim.x, (it & 1) ^ 1);
+    if (!OS && a == 2 && batch + gridDim.x < nbatch) prefetch(batch + gridDim.x, (it & 1) ^ 1);
     if (tid < CPB * MN) {
       const int c = tid / MN, r = tid - c * MN;
       const int qx = r / N, iz = r - qx * N;
@@ -361,7 +366,8 @@ NEO_PRAGMA_A
     }
     sync();
   }
-  }  // persistent batch loop
+  ++it;
+  } while (!OS && (batch += gridDim.x) < nbatch);   // persistent batch loop
 }
 
 template <int N, int M, int CPB, bool GS = false, int WARPS = 0, int VAR = 0>
@@ -378,8 +384,9 @@ static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double
   const Tabs<N, M> T = make_tabs<N, M>(p);
   const int64_t nbatch = (ncells + CPBT - 1) / CPBT;
   const int64_t resident = sh.resident();
-  const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
-  k<<<grid, THREADS, SMEM, s>>>(T, p->params[0], p->params[1], ncells, coords, u, A, cmap);
+  const unsigned grid = (unsigned)((VAR & 2) || nbatch < resident ? nbatch : resident);
+  if (grid > 0)
+    k<<<grid, THREADS, SMEM, s>>>(T, p->params[0], p->params[1], ncells, coords, u, A, cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_neohookean_kernel launch");
 }
@@ -433,14 +440,20 @@ static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const doub
       if (n == 2) return launch_neo<2, 3, 3, GS, 8>(p, ncells, A, coords, w0, s, cmap);
       if (n == 3) return launch_neo<3, 4, 2, GS, 8>(p, ncells, A, coords, w0, s, cmap);
       if (n == 4) return launch_neo<4, 5, 1, GS, 8>(p, ncells, A, coords, w0, s, cmap);
+    } else if (var == 5) {   // persistent CTAs (the default until r02cl)
+      if (n == 2) return launch_neo<2, 3, 3, GS, 4>(p, ncells, A, coords, w0, s, cmap);
+      if (n == 3) return launch_neo<3, 4, 2, GS, 4>(p, ncells, A, coords, w0, s, cmap);
+      if (n == 4) return launch_neo<4, 5, 1, GS, 4>(p, ncells, A, coords, w0, s, cmap);
     } else if (var == 1) {
       if (n == 2) return launch_neo<2, 3, 3, GS, 4, 1>(p, ncells, A, coords, w0, s, cmap);
       if (n == 3) return launch_neo<3, 4, 2, GS, 4, 1>(p, ncells, A, coords, w0, s, cmap);
       if (n == 4) return launch_neo<4, 5, 1, GS, 4, 1>(p, ncells, A, coords, w0, s, cmap);
     } else {
-      if (n == 2) return launch_neo<2, 3, 3, GS, 4>(p, ncells, A, coords, w0, s, cmap);
-      if (n == 3) return launch_neo<3, 4, 2, GS, 4>(p, ncells, A, coords, w0, s, cmap);
-      if (n == 4) return launch_neo<4, 5, 1, GS, 4>(p, ncells, A, coords, w0, s, cmap);
+      // one-shot CTAs (VAR bit 1): p = 2 0.1566 -> 0.1464, p = 3 0.3738 ->
+      // 0.3359 ms (profiles/r02cl_c4_*.jsonl)
+      if (n == 2) return launch_neo<2, 3, 3, GS, 4, 2>(p, ncells, A, coords, w0, s, cmap);
+      if (n == 3) return launch_neo<3, 4, 2, GS, 4, 2>(p, ncells, A, coords, w0, s, cmap);
+      if (n == 4) return launch_neo<4, 5, 1, GS, 4, 2>(p, ncells, A, coords, w0, s, cmap);
     }
   }
   // two points per pointwise iteration: p = 6 1.831 -> 1.772 ms, neutral at

@@ -44,7 +44,7 @@ def instances():
     txt = open(os.path.join(CSRC, "hex_action6.cu")).read()
     res = []
     for m in re.finditer(r"launch_v6<(\d+), (\d+), (\d+)(?:, (true|false))?(?:, (true|false))?"
-                         r"(?:, (true|false))?(?:, (?:true|false))?>\(p", txt):
+                         r"(?:, (true|false))?(?:, (?:true|false))*>\(p", txt):
         res.append((int(m.group(1)), int(m.group(2)), m.group(4) == "true", m.group(5) == "true",
                     m.group(6) == "true"))
     return sorted(set(res))

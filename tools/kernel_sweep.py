@@ -157,12 +157,27 @@ def c4_defines(v, entry):
 V6_EO = {4: 0, 5: 1, 6: 1, 7: 0, 8: 0, 9: 0}
 
 
+# v6 product defaults (cpb, minb, zr, ws, eg, bk) per n
+V6_DEFAULT = {4: (16, 2, 1, 1, 0, 0), 5: (5, 4, 1, 0, 0, 0), 6: (7, 2, 1, 0, 0, 0),
+              7: (5, 2, 1, 0, 0, 0), 8: (4, 2, 0, 0, 0, 0), 9: (3, 2, 0, 0, 1, 1)}
+
+
 def c2_variants(n):
+    """Level 2 (default): one-shot CTAs (os) x cells per CTA x min-blocks x zr / eg around
+    the product default; SWEEP_LEVEL=1: the full persistent-kernel space of
+    profiles/r02cg_c2_sweep.jsonl."""
     out = []
     nn = n * n
     cpbs = {4: (2, 4, 6, 8, 12, 16), 5: (2, 3, 4, 5, 6, 8, 10), 6: (3, 4, 5, 6, 7, 8),
             7: (2, 3, 4, 5, 6), 8: (2, 3, 4, 5), 9: (1, 2, 3, 4)}[n]
-    for cpb, ws, zr, eg, bk in itertools.product(cpbs, (0, 1), (0, 1), (0, 1), (0, 1)):
+    if os.environ.get("SWEEP_LEVEL", "2") == "2":
+        cpb0, minb0, zr0, ws0, eg0, bk0 = V6_DEFAULT[n]
+        space = itertools.product(cpbs, (ws0,), (0, 1), sorted({0, eg0}), (0,), (0, 1))
+    elif os.environ.get("SWEEP_LEVEL") == "3":   # one-shot x bulk staging x eg x zr
+        space = itertools.product(cpbs, (V6_DEFAULT[n][3],), (0, 1), (0, 1), (0, 1), (1,))
+    else:
+        space = itertools.product(cpbs, (0, 1), (0, 1), (0, 1), (0, 1), (0,))
+    for cpb, ws, zr, eg, bk, os_ in space:
         if ws and (nn > 32 or cpb % (32 // nn)):
             continue
         threads = 32 * (cpb // (32 // nn)) if ws else -(-cpb * nn // 32) * 32
@@ -172,7 +187,7 @@ def c2_variants(n):
             if minb and 65536 // (minb * threads) < 80:
                 continue
             out.append(dict(n=n, cpb=cpb, ws=ws, zr=zr, eg=eg, bk=bk, eo=V6_EO[n], minb=minb,
-                            threads=threads, smem=0))
+                            os=os_, threads=threads, smem=0))
     return out
 
 
@@ -180,14 +195,15 @@ def c2_defines(v, entry):
     return ["-DSFK_V6_ONLY_N=%d" % v["n"], "-DSFK_V6P_CPB=%d" % v["cpb"],
             "-DSFK_V6P_MINB=%d" % v["minb"], "-DSFK_V6P_ZR=%d" % v["zr"],
             "-DSFK_V6P_WS=%d" % v["ws"], "-DSFK_V6P_EG=%d" % v["eg"], "-DSFK_V6P_BK=%d" % v["bk"],
-            "-DSFK_V6P_EO=%d" % v["eo"], "-DSFK_V6_PROBE_ENTRY=%s" % entry]
+            "-DSFK_V6P_EO=%d" % v["eo"], "-DSFK_V6P_OS=%d" % v.get("os", 0),
+            "-DSFK_V6_PROBE_ENTRY=%s" % entry]
 
 
 FAMILIES = {
     "c3": dict(src="hex_colloc.cu", variants=c3_variants, defines=c3_defines,
                keys=("cpb", "sy", "sx", "cs", "persist", "kg", "splitz", "minb", "geom", "fuse")),
     "c2": dict(src="hex_action6.cu", variants=c2_variants, defines=c2_defines,
-               keys=("cpb", "ws", "zr", "eg", "bk", "eo", "minb")),
+               keys=("cpb", "ws", "zr", "eg", "bk", "eo", "minb", "os")),
     "c4": dict(src="hex_neohookean3.cu", variants=c4_variants, defines=c4_defines,
                keys=("cpb", "px", "lz", "ypad", "nyt", "minb", "oneshot")),
 }
