@@ -422,6 +422,18 @@ static int launch_cell(const sfk_plan* p, int64_t ncells, double* A, const doubl
   return cuda_status(cudaGetLastError(), "hex_laplace_action_cell launch");
 }
 
+#ifdef SFK_CELL_ONLY_N
+// probe builds (tools/kernel_sweep.py): one instantiation instead of the dispatch
+}  // namespace sfk
+extern "C" int SFK_CELL_PROBE_ENTRY(const sfk_plan* p, int64_t ncells, double* A,
+                                    const double* coords, const double* w0, void* stream) {
+  if (p->n != SFK_CELL_ONLY_N || p->n != p->m)
+    return sfk::fail(SFK_EUNSUPPORTED, "probe build: n = m = %d only", SFK_CELL_ONLY_N);
+  return sfk::launch_cell<SFK_CELL_ONLY_N, SFK_CELLP_TH, SFK_CELLP_MINB, false, SFK_CELLP_CD != 0,
+                          SFK_CELLP_LG != 0>(p, ncells, A, coords, w0, (cudaStream_t)stream);
+}
+namespace sfk {
+#else
 // Threads per CTA: option cell_th overrides (tuning runs only).
 int launch_hex_action_cell(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                            const double* w0, cudaStream_t s) {
@@ -441,7 +453,10 @@ int launch_hex_action_cell(const sfk_plan* p, int64_t ncells, double* A, const d
       // line geometry shared between the cell's z-lines (LG): 0.0740 -> 0.0723 ms,
       // bit-identical (profiles/r02am_p2_lgs*.json*); option v6_cfg = 7 drops it
       if (option(OPT_V6_CFG) == 7) return launch_cell<3, 64, 1, false, true>(p, ncells, A, coords, w0, s);
-      return launch_cell<3, 64, 1, false, true, true>(p, ncells, A, coords, w0, s);
+      if (th == 64) return launch_cell<3, 64, 1, false, true, true>(p, ncells, A, coords, w0, s);
+      // one warp per CTA (tools/kernel_sweep.py cell, profiles/r02cn_cell_sweep.jsonl):
+      // 0.0778 -> 0.0758 ms
+      return launch_cell<3, 32, 1, false, true, true>(p, ncells, A, coords, w0, s);
     case 4:
       if (th == 64) return launch_cell<4, 64, 1>(p, ncells, A, coords, w0, s);
       return launch_cell<4, 32, 1>(p, ncells, A, coords, w0, s);
@@ -455,5 +470,7 @@ int launch_hex_action_cell_gs(const sfk_plan* p, int64_t ncells, const int* cmap
   if (p->n != 3 || p->m != 3) return SFK_EUNSUPPORTED;
   return launch_cell<3, 64, 1, true>(p, ncells, y, coords, x, s, cmap);
 }
+
+#endif  // SFK_CELL_ONLY_N
 
 }  // namespace sfk

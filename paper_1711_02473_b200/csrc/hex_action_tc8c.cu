@@ -84,12 +84,18 @@ __device__ __forceinline__ int aU(int a, int b, int c) { return a * 68 + b * 8 +
 // GS: global operator y += sum_c P_c^T A_c P_c x: the cell's dof map
 // (int32) is double-buffered in the u staging area (so not with AU), x is
 // gathered through it in stage A and y scatter-added in stage I.
-template <int MINB, bool AU, bool GS = false>
+// COL: the GLL-collocated (weighted) Laplace action of BASELINE C3 at p = 7
+// (hex_colloc.cu's operator: B = I, T.C holds the derivative table D, kappa =
+// w1 at the points or nullptr): stages A, B and the B_z halves of C and G drop
+// out — C reads u, G's t is the result — and stage E multiplies by kappa.
+template <int MINB, bool AU, bool GS = false, bool COL = false>
 __global__ void __launch_bounds__(tc8c::THREADS, MINB)
 hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
                         const double* __restrict__ coords, const double* __restrict__ u,
-                        double* __restrict__ A, const int* __restrict__ cmap = nullptr) {
+                        double* __restrict__ A, const int* __restrict__ cmap = nullptr,
+                        const double* __restrict__ kappa = nullptr) {
   static_assert(!(GS && AU), "GS keeps the map through stage I: own staging area");
+  static_assert(!COL || (!GS && !AU), "COL: E-vector form with its own u staging area");
   using namespace tc8c;
   extern __shared__ __align__(16) double smem[];
   double* S1 = smem;
@@ -157,7 +163,7 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
     const int* smap = reinterpret_cast<const int*>(sU + warp * US) + cur * N3;   // GS
 
     // ---- A: x, D-form; tile (c, iy), lines iz: P = B_x u ------------------
-    {
+    if (!COL) {
       double f[TPW][2], o[TPW][2];
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
@@ -184,10 +190,10 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       }
     }
     __syncwarp();
-    if (!AU && b + gridDim.x < nbatch) prefetch(b + gridDim.x, cur ^ 1);
+    if (!COL && !AU && b + gridDim.x < nbatch) prefetch(b + gridDim.x, cur ^ 1);
 
     // ---- B: y, D-form; tile (c, qx), lines iz: Q = B_y P -------------------
-    {
+    if (!COL) {
       double f[TPW][2], o[TPW][2];
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
@@ -217,13 +223,19 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         const int t = j, qx = t & 7;
-        f[j] = *reinterpret_cast<const double2*>(S2 + c * SLOT + aQR(qx, gq, 2 * kq));
+        f[j] = COL ? *reinterpret_cast<const double2*>(sU + c * US + aU(qx, gq, 2 * kq))
+                   : *reinterpret_cast<const double2*>(S2 + c * SLOT + aQR(qx, gq, 2 * kq));
       }
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
-        v[j][0] = v[j][1] = 0.0;
-        dmma8(v[j][0], v[j][1], f[j].x, zbf[0]);
-        dmma8(v[j][0], v[j][1], f[j].y, zbf[1]);
+        if (COL) {   // collocated: V = u
+          v[j][0] = f[j].x;
+          v[j][1] = f[j].y;
+        } else {
+          v[j][0] = v[j][1] = 0.0;
+          dmma8(v[j][0], v[j][1], f[j].x, zbf[0]);
+          dmma8(v[j][0], v[j][1], f[j].y, zbf[1]);
+        }
       }
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
@@ -239,6 +251,7 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       }
     }
     __syncwarp();
+    if (COL && b + gridDim.x < nbatch) prefetch(b + gridDim.x, cur ^ 1);   // sU was read by C
 
     // ---- D: gx = C_x V (tile (c, qy), lines qz), gy = C_y V (tile (c, qx)) -
     //      both tile sets' loads first, then their MMAs (2 TPW chains)
@@ -285,8 +298,12 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
       HexLineGeom geo;
       geo.setup(sCo + cur * CSZ + c * 24, T.Bc[qx], T.Bc[N + qx], T.Bc[qy], T.Bc[N + qy]);
       const double wxy = T.W[qx] * T.W[qy];
+      const bool wk = COL && kappa != nullptr && c < ncb;
+      const double* kp = kappa + (cell0 + (c < ncb ? c : 0)) * N3 + qx * NN + qy * N;
 #pragma unroll 1
       for (int q = 0; q < N; q += 2) {
+        const double2 kk = wk ? __ldg(reinterpret_cast<const double2*>(kp + q))
+                              : make_double2(1.0, 1.0);
         double2* px = reinterpret_cast<double2*>(gxc + aGX(qx, qy, q));
         double2* py = reinterpret_cast<double2*>(gyc + aGY(qx, qy, q));
         double2* pz = reinterpret_cast<double2*>(gzc + aGZ(qx, qy, q));
@@ -294,13 +311,15 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
         {
           double r0[3], r1[3], r2[3];
           const double det = geo.adj(T.Bc[q], T.Bc[N + q], r0, r1, r2);
-          const double s = (wxy * T.W[q]) * rcp64(fabs(det));
+          double s = (wxy * T.W[q]) * rcp64(fabs(det));
+          if (COL) s *= kk.x;
           laplace_flux(r0, r1, r2, s, gx.x, gy.x, gz.x);
         }
         {
           double r0[3], r1[3], r2[3];
           const double det = geo.adj(T.Bc[q + 1], T.Bc[N + q + 1], r0, r1, r2);
-          const double s = (wxy * T.W[q + 1]) * rcp64(fabs(det));
+          double s = (wxy * T.W[q + 1]) * rcp64(fabs(det));
+          if (COL) s *= kk.y;
           laplace_flux(r0, r1, r2, s, gx.y, gy.y, gz.y);
         }
         *px = gx;
@@ -364,19 +383,37 @@ hex_laplace_action_tc8c(const __grid_constant__ TabsTC8C T, int64_t ncells,
         dmma8(tt[j][0], tt[j][1], fz[j].x, zcb[0]);
         dmma8(tt[j][0], tt[j][1], fz[j].y, zcb[1]);
       }
+      if (COL) {
+        // collocated: t is the result; lane (gq, kq) of tile qx holds
+        // A[qx][gq][2kq, 2kq + 1] — a tile is 64 consecutive doubles
+        if (c < ncb) {
 #pragma unroll
-      for (int j = 0; j < TPW; ++j) {
-        rr[j][0] = rr[j][1] = 0.0;
-        dmma8(rr[j][0], rr[j][1], tt[j][0], zbb[0]);
-        dmma8(rr[j][0], rr[j][1], tt[j][1], zbb[1]);
-      }
+          for (int j = 0; j < TPW; ++j) {
+            double* ap = A + (cell0 + c) * N3 + (j & 7) * NN + gq * 8 + 2 * kq;
+            if ((reinterpret_cast<uintptr_t>(ap) & 15) == 0) {
+              *reinterpret_cast<double2*>(ap) = make_double2(tt[j][0], tt[j][1]);
+            } else {
+              ap[0] = tt[j][0];
+              ap[1] = tt[j][1];
+            }
+          }
+        }
+      } else {
 #pragma unroll
-      for (int j = 0; j < TPW; ++j) {
-        const int t = j, qx = t & 7;
-        *reinterpret_cast<double2*>(S1 + c * SLOT + aQR(qx, gq, 2 * kq)) = make_double2(rr[j][0], rr[j][1]);
+        for (int j = 0; j < TPW; ++j) {
+          rr[j][0] = rr[j][1] = 0.0;
+          dmma8(rr[j][0], rr[j][1], tt[j][0], zbb[0]);
+          dmma8(rr[j][0], rr[j][1], tt[j][1], zbb[1]);
+        }
+#pragma unroll
+        for (int j = 0; j < TPW; ++j) {
+          const int t = j, qx = t & 7;
+          *reinterpret_cast<double2*>(S1 + c * SLOT + aQR(qx, gq, 2 * kq)) = make_double2(rr[j][0], rr[j][1]);
+        }
       }
     }
     __syncwarp();
+    if (COL) continue;   // (the prefetch of the next batch was issued after stage C)
 
     if (AU && b + gridDim.x < nbatch) prefetch(b + gridDim.x, cur ^ 1);   // S4 is free now
 
@@ -471,9 +508,39 @@ int launch_hex_action_tc8c(const sfk_plan* p, int64_t ncells, double* A, const d
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
   const int64_t resident = sh.resident();
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
-  kern<<<grid, THREADS, smem, s>>>(T, ncells, coords, w0, A, nullptr);
+  kern<<<grid, THREADS, smem, s>>>(T, ncells, coords, w0, A, nullptr, nullptr);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_tc8c launch");
+}
+
+// BASELINE C3 at p = 7 (GLL-collocated weighted Laplace, n = m = 8) on the
+// same one-warp-per-cell DMMA kernel (COL): 96 DMMA per cell.  w1 = kappa at
+// the points (nullptr: the unweighted collocated action).
+int launch_hex_colloc_tc8c(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                           const double* w0, const double* w1, cudaStream_t s) {
+  if (p->n != 8 || p->m != 8) return SFK_EUNSUPPORTED;
+  using namespace tc8c;
+  auto kern = hex_laplace_action_tc8c<3, false, false, true>;
+  const size_t smem = smem_bytes(false);
+  LaunchShape sh;
+  if (const int rc_ = kernel_shape((const void*)kern, THREADS, smem, "hex_colloc_tc8c", &sh, true))
+    return rc_;
+  TabsTC8C T;
+  for (int i = 0; i < 64; ++i) {
+    T.B[i] = p->B[i];   // (identity at the collocation points; unused)
+    T.C[i] = p->D[i];   // D[i*8 + q]: derivative of basis i at point q
+  }
+  for (int q = 0; q < 8; ++q) {
+    T.W[q] = p->wq[q];
+    T.Bc[q] = p->Bc[q];
+    T.Bc[8 + q] = p->Bc[8 + q];
+  }
+  const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  const int64_t resident = sh.resident();
+  const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
+  if (grid > 0) kern<<<grid, THREADS, smem, s>>>(T, ncells, coords, w0, A, nullptr, w1);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "hex_colloc_tc8c launch");
 }
 
 // Global operator (fused gather / scatter) at n = 8: the map needs its own
@@ -500,7 +567,7 @@ int launch_hex_action_tc8c_gs(const sfk_plan* p, int64_t ncells, const int* cmap
   const int64_t nbatch = (ncells + CPB - 1) / CPB;
   const int64_t resident = sh.resident();
   const unsigned grid = (unsigned)(nbatch < resident ? nbatch : resident);
-  kern<<<grid, THREADS, smem, s>>>(T, ncells, coords, x, y, cmap);
+  kern<<<grid, THREADS, smem, s>>>(T, ncells, coords, x, y, cmap, nullptr);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_tc8c_gs launch");
 }

@@ -691,9 +691,12 @@ namespace sfk {
 #else
 int launch_hex_colloc_action(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                              const double* w0, const double* w1, cudaStream_t s) {
-  // n = 8, 12, 16: DMMA kernel (hex_colloc_tc.cu)
+  // option c3_tc = 1: CTA-wide DMMA kernels at n = 8, 12, 16 (hex_colloc_tc.cu,
+  // slower); 2: n = 8 on the one-warp-per-cell DMMA kernel (hex_action_tc8c.cu)
   const int rc = launch_hex_colloc_tc(p, ncells, A, coords, w0, w1, s);
   if (rc != SFK_EUNSUPPORTED) return rc;
+  if (p->n == 8 && p->m == 8 && option(OPT_C3_TC) == 2)
+    return launch_hex_colloc_tc8c(p, ncells, A, coords, w0, w1, s);
   return dispatch_colloc<false>(p, ncells, A, coords, w0, w1, s, nullptr);
 }
 

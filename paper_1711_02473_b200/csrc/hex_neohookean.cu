@@ -426,10 +426,11 @@ static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const doub
   const int var = (int)option(OPT_NEO_CFG);   // 1: two points per pointwise iteration everywhere
   // component-parallel kernel (hex_neohookean3.cu): option neo_cfg = 3 wherever
   // it is instantiated, 4 nowhere
-  // Default at p = 4..6 (n = 5..7): 0.650 -> 0.616, 1.257 -> 1.013, 1.759 ->
-  // 1.701 ms; the line kernel stays ahead at p = 2, 3 (tools/kernel_sweep.py
-  // c4, profiles/r02cj_c4_sweep2.jsonl).
-  if (m == n + 1 && (var == 3 || (n >= 5 && var == 0))) {
+  // Default at p = 5, 6 (n = 6, 7): 1.257 -> 1.006, 1.759 -> 1.691 ms
+  // (tools/kernel_sweep.py c4, profiles/r02cj_c4_sweep2.jsonl); at p = 2..4 the
+  // line kernel with one-shot CTAs stays ahead (p = 4: 0.569 vs 0.612 ms,
+  // profiles/r02cp_c4_*.jsonl).
+  if (m == n + 1 && (var == 3 || (n >= 6 && var == 0))) {
     const int rc = GS ? launch_hex_neohookean3_gs(p, ncells, cmap, w0, A, coords, s)
                       : launch_hex_neohookean3(p, ncells, A, coords, w0, s);
     if (rc != SFK_EUNSUPPORTED) return rc;
@@ -454,6 +455,17 @@ static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const doub
       if (n == 2) return launch_neo<2, 3, 3, GS, 4, 2>(p, ncells, A, coords, w0, s, cmap);
       if (n == 3) return launch_neo<3, 4, 2, GS, 4, 2>(p, ncells, A, coords, w0, s, cmap);
       if (n == 4) return launch_neo<4, 5, 1, GS, 4, 2>(p, ncells, A, coords, w0, s, cmap);
+    }
+  }
+  // the line kernel with one-shot CTAs (VAR bit 1): default at p = 4; option
+  // neo_cfg = 6 selects it at p = 5, 6 too (A/B against the component-parallel
+  // default there)
+  if (m == n + 1 && (var == 6 || (n == 5 && var == 0))) {
+    switch (n) {
+      case 5: return launch_neo<5, 6, SFK_NEO_CPB_P4, GS, 0, 2>(p, ncells, A, coords, w0, s, cmap);
+      case 6: return launch_neo<6, 7, SFK_NEO_CPB_P5, GS, 0, 2>(p, ncells, A, coords, w0, s, cmap);
+      case 7: return launch_neo<7, 8, SFK_NEO_CPB_P6, GS, 0, 3>(p, ncells, A, coords, w0, s, cmap);
+      default: break;
     }
   }
   // two points per pointwise iteration: p = 6 1.831 -> 1.772 ms, neutral at

@@ -119,6 +119,9 @@ int launch_hex_action_tc_gs(const sfk_plan* p, int64_t ncells, const int* cmap, 
                             double* y, const double* coords, cudaStream_t s);
 int launch_hex_neohookean_gs(const sfk_plan* p, int64_t ncells, const int* cmap, const double* x,
                              double* y, const double* coords, cudaStream_t s);
+// C3 at n = 8 on the one-warp-per-cell DMMA kernel (hex_action_tc8c.cu, COL mode)
+int launch_hex_colloc_tc8c(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
+                           const double* w0, const double* w1, cudaStream_t s);
 // component-parallel C4 kernel (hex_neohookean3.cu); SFK_EUNSUPPORTED where not instantiated
 int launch_hex_neohookean3(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                            const double* w0, cudaStream_t s);

@@ -458,7 +458,7 @@ def test_c2_every_kernel_generation(cuda, p):
         assert err < TOL, (gen, g, err)
 
 
-@pytest.mark.parametrize("mode", ["colloc_warps", "neo_cta", "colloc_tc"])
+@pytest.mark.parametrize("mode", ["colloc_warps", "neo_cta", "colloc_tc", "colloc_tc8c"])
 def test_alternative_kernel_modes(cuda, mode):
     """Kernel modes that are off by default for speed (C3's warp-synchronous
     variant, option colloc_warps; C3's DMMA variant, c3_tc) or on by default
@@ -467,9 +467,10 @@ def test_alternative_kernel_modes(cuda, mode):
     from paper_1711_02473_b200 import (REGISTRY, action_form, compile_form,
                                        neohookean_residual_form)
 
-    if mode in ("colloc_warps", "colloc_tc"):
+    if mode in ("colloc_warps", "colloc_tc", "colloc_tc8c"):
         opts, degrees = (({"colloc_warps": 8}, (1, 2, 3, 4)) if mode == "colloc_warps"
-                         else ({"c3_tc": 1}, (7, 11, 15)))
+                         else ({"c3_tc": 1}, (7, 11, 15)) if mode == "colloc_tc"
+                         else ({"c3_tc": 2}, (7,)))   # one-warp-per-cell DMMA kernel, COL mode
         build = lambda p: compile_form(action_form(REGISTRY["weighted_laplace"]), "hex", p,  # noqa
                                        "spectral", "spectral_gll", "collocated-gll")
         inputs = lambda p: workloads.c3_inputs(p, dims=(3, 5, 7))  # noqa

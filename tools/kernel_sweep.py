@@ -199,11 +199,31 @@ def c2_defines(v, entry):
             "-DSFK_V6_PROBE_ENTRY=%s" % entry]
 
 
+def cell_variants(n):
+    out = []
+    for th, cd, lg in itertools.product((32, 64, 96, 128, 160, 192, 256), (0, 1), (0, 1)):
+        if lg and not cd:
+            continue
+        for minb in (0, 1, 2, 3, 4, 5, 6, 8):
+            if minb and 65536 // (minb * th) < 96:
+                continue
+            out.append(dict(n=n, th=th, cd=cd, lg=lg, minb=minb, threads=th, smem=0))
+    return out
+
+
+def cell_defines(v, entry):
+    return ["-DSFK_CELL_ONLY_N=%d" % v["n"], "-DSFK_CELLP_TH=%d" % v["th"],
+            "-DSFK_CELLP_MINB=%d" % v["minb"], "-DSFK_CELLP_CD=%d" % v["cd"],
+            "-DSFK_CELLP_LG=%d" % v["lg"], "-DSFK_CELL_PROBE_ENTRY=%s" % entry]
+
+
 FAMILIES = {
     "c3": dict(src="hex_colloc.cu", variants=c3_variants, defines=c3_defines,
                keys=("cpb", "sy", "sx", "cs", "persist", "kg", "splitz", "minb", "geom", "fuse")),
     "c2": dict(src="hex_action6.cu", variants=c2_variants, defines=c2_defines,
                keys=("cpb", "ws", "zr", "eg", "bk", "eo", "minb", "os")),
+    "cell": dict(src="hex_action_cell.cu", variants=cell_variants, defines=cell_defines,
+                 keys=("th", "cd", "lg", "minb")),
     "c4": dict(src="hex_neohookean3.cu", variants=c4_variants, defines=c4_defines,
                keys=("cpb", "px", "lz", "ypad", "nyt", "minb", "oneshot")),
 }
@@ -303,7 +323,7 @@ def run(fam, ns):
             plan = compile_form(action_form(REGISTRY["weighted_laplace"]), "hex", p,
                                 "spectral", "spectral_gll", "collocated-gll")
             inp = workloads.c3_inputs(p)
-        elif fam == "c2":
+        elif fam in ("c2", "cell"):
             from paper_1711_02473_b200 import compile_kernel
             plan = compile_kernel("action_laplace", "hex", p)
             inp = workloads.c2_inputs(p)
@@ -319,6 +339,7 @@ def run(fam, ns):
         args = lambda o: (h, C, o.data_ptr(), d["coords"].data_ptr(), d["w0"].data_ptr(),
                           w1, stream.cuda_stream)
         pargs = (lambda o: args(o)) if fam == "c3" else (lambda o: args(o)[:5] + args(o)[6:])
+        nrep = 3 if fam == "cell" else 1   # short kernels: median of medians
         base = lambda: runtime._check(lib.sfk_eval(*args(ref)))
         t0 = time_launch(base)
         scale = torch.nan_to_num(ref, nan=0.0).abs().amax(dim=1).clamp_min(1e-300)
