@@ -370,6 +370,19 @@ static int launch_mat(const sfk_plan* p, int64_t ncells, double* A, const double
   return cuda_status(cudaGetLastError(), "hex_laplace_matrix_kernel launch");
 }
 
+#ifdef SFK_MAT_ONLY_N
+// probe builds (tools/kernel_sweep.py c5): one instantiation of the FMA kernel
+}  // namespace sfk
+extern "C" int SFK_MAT_PROBE_ENTRY(const sfk_plan* p, int64_t ncells, double* A,
+                                   const double* coords, const double* w0, void* stream) {
+  (void)w0;
+  if (p->n != SFK_MAT_ONLY_N || p->m != SFK_MAT_ONLY_N)
+    return sfk::fail(SFK_EUNSUPPORTED, "probe build: n = m = %d only", SFK_MAT_ONLY_N);
+  return sfk::launch_mat<SFK_MAT_ONLY_N, SFK_MAT_ONLY_N, SFK_MATP_CPB>(p, ncells, A, coords,
+                                                                      (cudaStream_t)stream);
+}
+namespace sfk {
+#else
 int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                       cudaStream_t s) {
   if (p->collocated)
@@ -461,5 +474,7 @@ int launch_hex_matrix_csr(const sfk_plan* p, int64_t ncells, const int32_t* dofs
   }
   return fail(SFK_EUNSUPPORTED, "CSR assembly: no kernel for n=%d (p<=8)", p->n);
 }
+
+#endif  // SFK_MAT_ONLY_N
 
 }  // namespace sfk

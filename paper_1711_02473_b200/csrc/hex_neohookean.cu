@@ -83,8 +83,8 @@ struct NeoCfg {
 // cells (every stage has <= 32 lines for them) with its own shared-memory
 // slice and prefetch, and the stages sync with __syncwarp instead of CTA
 // barriers (the CTA version runs ~13 barriers per batch).
-template <int N, int M, int CPB, bool GS = false, int WARPS = 0, int VAR = 0>
-__global__ void __launch_bounds__(WARPS ? 32 * WARPS : NeoCfg<N, M, CPB>::THREADS)
+template <int N, int M, int CPB, bool GS = false, int WARPS = 0, int VAR = 0, int MINB = 0>
+__global__ void __launch_bounds__(WARPS ? 32 * WARPS : NeoCfg<N, M, CPB>::THREADS, MINB)
 hex_neohookean_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double lam,
                       int64_t ncells, const double* __restrict__ coords,
                       const double* __restrict__ u, double* __restrict__ A,
@@ -370,14 +370,14 @@ NEO_PRAGMA_A
   } while (!OS && (batch += gridDim.x) < nbatch);   // persistent batch loop
 }
 
-template <int N, int M, int CPB, bool GS = false, int WARPS = 0, int VAR = 0>
+template <int N, int M, int CPB, bool GS = false, int WARPS = 0, int VAR = 0, int MINB = 0>
 static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                       const double* u, cudaStream_t s, const int* cmap = nullptr) {
   using C = NeoCfg<N, M, CPB>;
   constexpr int THREADS = WARPS ? 32 * WARPS : C::THREADS;
   constexpr size_t SMEM = WARPS ? WARPS * C::SMEM : C::SMEM;
   constexpr int CPBT = WARPS ? WARPS * CPB : CPB;
-  auto k = hex_neohookean_kernel<N, M, CPB, GS, WARPS, VAR>;
+  auto k = hex_neohookean_kernel<N, M, CPB, GS, WARPS, VAR, MINB>;
   LaunchShape sh;
   if (const int rc_ = kernel_shape((const void*)k, THREADS, SMEM, "hex_neohookean", &sh, true))
     return rc_;
@@ -417,6 +417,19 @@ static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double
 #define SFK_NEO_CPB_P6 1
 #endif
 
+#ifdef SFK_C4L_ONLY_N
+// probe builds (tools/kernel_sweep.py c4l): one instantiation of the line kernel
+}  // namespace sfk
+extern "C" int SFK_C4L_PROBE_ENTRY(const sfk_plan* p, int64_t ncells, double* A,
+                                   const double* coords, const double* w0, void* stream) {
+  if (p->n != SFK_C4L_ONLY_N || p->m != SFK_C4L_ONLY_N + 1)
+    return sfk::fail(SFK_EUNSUPPORTED, "probe build: n=%d only", SFK_C4L_ONLY_N);
+  return sfk::launch_neo<SFK_C4L_ONLY_N, SFK_C4L_ONLY_N + 1, SFK_C4LP_CPB, false, SFK_C4LP_WARPS,
+                         SFK_C4LP_VAR, SFK_C4LP_MINB>(p, ncells, A, coords, w0,
+                                                      (cudaStream_t)stream, nullptr);
+}
+namespace sfk {
+#else
 template <bool GS>
 static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                         const double* w0, cudaStream_t s, const int* cmap) {
@@ -452,9 +465,13 @@ static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const doub
     } else {
       // one-shot CTAs (VAR bit 1): p = 2 0.1566 -> 0.1464, p = 3 0.3738 ->
       // 0.3359 ms (profiles/r02cl_c4_*.jsonl)
+      // sweep of (warps, cells, two-point, min-blocks) on the one-shot kernel
+      // (tools/kernel_sweep.py c4l, profiles/r02cq_c4l_sweep.jsonl): p = 2 two
+      // warps per CTA 0.1464 -> 0.1392 ms; p = 3 CTA mode, 6 cells per 160-thread
+      // CTA at 3 CTAs per SM 0.3338 -> 0.2870 ms
       if (n == 2) return launch_neo<2, 3, 3, GS, 4, 2>(p, ncells, A, coords, w0, s, cmap);
-      if (n == 3) return launch_neo<3, 4, 2, GS, 4, 2>(p, ncells, A, coords, w0, s, cmap);
-      if (n == 4) return launch_neo<4, 5, 1, GS, 4, 2>(p, ncells, A, coords, w0, s, cmap);
+      if (n == 3) return launch_neo<3, 4, 2, GS, 2, 2>(p, ncells, A, coords, w0, s, cmap);
+      if (n == 4) return launch_neo<4, 5, 6, GS, 0, 2, 3>(p, ncells, A, coords, w0, s, cmap);
     }
   }
   // the line kernel with one-shot CTAs (VAR bit 1): default at p = 4; option
@@ -510,5 +527,7 @@ int launch_hex_neohookean_gs(const sfk_plan* p, int64_t ncells, const int* cmap,
                              double* y, const double* coords, cudaStream_t s) {
   return dispatch_neo<true>(p, ncells, y, coords, x, s, cmap);
 }
+
+#endif  // SFK_C4L_ONLY_N
 
 }  // namespace sfk

@@ -217,6 +217,52 @@ def cell_defines(v, entry):
             "-DSFK_CELLP_LG=%d" % v["lg"], "-DSFK_CELL_PROBE_ENTRY=%s" % entry]
 
 
+def c4l_variants(n):
+    """C4 line kernel (hex_neohookean.cu), one-shot CTAs."""
+    m = n + 1
+    out = []
+    for warps, cpb, var, unroll in itertools.product((0, 2, 4, 8), (1, 2, 3, 4, 6, 8), (2, 3),
+                                                     (0, 1)):
+        if warps and cpb * m * m > 32:
+            continue
+        threads = 32 * warps if warps else -(-cpb * m * m // 32) * 32
+        if threads > 512 or (not warps and cpb * m * m > 300):
+            continue
+        for minb in (0, 2, 3, 4, 5, 6, 8):
+            if minb and 65536 // (minb * threads) < 88:
+                continue
+            out.append(dict(n=n, warps=warps, cpb=cpb, var=var, unroll=unroll, minb=minb,
+                            threads=threads, smem=0))
+    return out
+
+
+def c4l_defines(v, entry):
+    return ["-DSFK_C4L_ONLY_N=%d" % v["n"], "-DSFK_C4LP_CPB=%d" % v["cpb"],
+            "-DSFK_C4LP_WARPS=%d" % v["warps"], "-DSFK_C4LP_VAR=%d" % v["var"],
+            "-DSFK_C4LP_MINB=%d" % v["minb"], "-DSFK_NEO_UNROLLA=%d" % v["unroll"],
+            "-DSFK_C4L_PROBE_ENTRY=%s" % entry]
+
+
+def c5_variants(n):
+    """C5 FMA matrix kernel (hex_matrix.cu) at n = 3."""
+    out = []
+    for cpb, zb, yb in itertools.product((1, 2, 3, 4, 5, 6, 8), (0, 1), (0, 1)):
+        threads = -(-cpb * n ** 4 // 32) * 32
+        if threads > 1024:
+            continue
+        for minb in (0, 1, 2, 3, 4, 5, 6, 8):
+            if minb and 65536 // (minb * threads) < 64:
+                continue
+            out.append(dict(n=n, cpb=cpb, zb=zb, yb=yb, minb=minb, threads=threads, smem=0))
+    return out
+
+
+def c5_defines(v, entry):
+    return ["-DSFK_MAT_ONLY_N=%d" % v["n"], "-DSFK_MATP_CPB=%d" % v["cpb"],
+            "-DSFK_MAT_ZB=%d" % v["zb"], "-DSFK_MAT_YB=%d" % v["yb"],
+            "-DSFK_MAT_MINB3=%d" % v["minb"], "-DSFK_MAT_PROBE_ENTRY=%s" % entry]
+
+
 FAMILIES = {
     "c3": dict(src="hex_colloc.cu", variants=c3_variants, defines=c3_defines,
                keys=("cpb", "sy", "sx", "cs", "persist", "kg", "splitz", "minb", "geom", "fuse")),
@@ -224,6 +270,10 @@ FAMILIES = {
                keys=("cpb", "ws", "zr", "eg", "bk", "eo", "minb", "os")),
     "cell": dict(src="hex_action_cell.cu", variants=cell_variants, defines=cell_defines,
                  keys=("th", "cd", "lg", "minb")),
+    "c4l": dict(src="hex_neohookean.cu", variants=c4l_variants, defines=c4l_defines,
+                keys=("warps", "cpb", "var", "unroll", "minb")),
+    "c5": dict(src="hex_matrix.cu", variants=c5_variants, defines=c5_defines,
+               keys=("cpb", "zb", "yb", "minb")),
     "c4": dict(src="hex_neohookean3.cu", variants=c4_variants, defines=c4_defines,
                keys=("cpb", "px", "lz", "ypad", "nyt", "minb", "oneshot")),
 }
@@ -323,6 +373,10 @@ def run(fam, ns):
             plan = compile_form(action_form(REGISTRY["weighted_laplace"]), "hex", p,
                                 "spectral", "spectral_gll", "collocated-gll")
             inp = workloads.c3_inputs(p)
+        elif fam == "c5":
+            from paper_1711_02473_b200 import compile_kernel
+            plan = compile_kernel("laplace", "hex", p)
+            inp = workloads.c5_inputs()
         elif fam in ("c2", "cell"):
             from paper_1711_02473_b200 import compile_kernel
             plan = compile_kernel("action_laplace", "hex", p)
@@ -332,12 +386,15 @@ def run(fam, ns):
             inp = workloads.c4_inputs(p)
         d = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in inp.items()}
         C = d["coords"].shape[0]
-        ref = torch.empty_like(d["w0"])
-        out = torch.empty_like(d["w0"])
+        if "w0" in d:
+            ref = torch.empty_like(d["w0"])
+        else:   # matrix kernels: no coefficient, (cells, n^6) output
+            ref = torch.empty((C, plan.return_size), dtype=torch.float64, device=dev)
+        out = torch.empty_like(ref)
         h = runtime.native_plan(plan)
         w1 = d["w1"].data_ptr() if "w1" in d else None
-        args = lambda o: (h, C, o.data_ptr(), d["coords"].data_ptr(), d["w0"].data_ptr(),
-                          w1, stream.cuda_stream)
+        w0 = d["w0"].data_ptr() if "w0" in d else None
+        args = lambda o: (h, C, o.data_ptr(), d["coords"].data_ptr(), w0, w1, stream.cuda_stream)
         pargs = (lambda o: args(o)) if fam == "c3" else (lambda o: args(o)[:5] + args(o)[6:])
         nrep = 3 if fam == "cell" else 1   # short kernels: median of medians
         base = lambda: runtime._check(lib.sfk_eval(*args(ref)))
