@@ -37,10 +37,14 @@
 #define SFK_MAT_YB 1   // all-jy Y phase at n <= 3 (A/B builds: 0)
 #endif
 #ifndef SFK_MAT_MINB3
-#define SFK_MAT_MINB3 0   // min CTAs/SM of the n = 3 kernel (A/B builds)
+#define SFK_MAT_MINB3 6   // min CTAs/SM of the n = 3 kernel (one-cell CTAs; A/B builds)
 #endif
 
 namespace sfk {
+
+#ifdef SFK_MAT_ONLY_N
+namespace {   // probe objects differ in macros, not template arguments: keep instances apart
+#endif
 
 template <int N, int M>
 struct TabsMat {
@@ -88,7 +92,7 @@ __device__ __forceinline__ int64_t csr_find(const int32_t* __restrict__ col_idx,
 //              matrix (values A, pattern row_ptr / col_idx from sfk_csr_create)
 //              through cell_dofs — the local matrix never reaches HBM.
 template <int N, int M, int CPB, bool CSR, bool YMAP = false>
-__global__ void __launch_bounds__(MatCfg<N, M, CPB>::THREADS, N == 3 ? SFK_MAT_MINB3 : 0)
+__global__ void __launch_bounds__(MatCfg<N, M, CPB>::THREADS, (N == 3 && CPB == 1) ? SFK_MAT_MINB3 : 0)
 hex_laplace_matrix_kernel(const __grid_constant__ TabsMat<N, M> T, int64_t ncells,
                           const double* __restrict__ coords, double* __restrict__ A,
                           const int32_t* __restrict__ dofs, const int64_t* __restrict__ row_ptr,
@@ -372,6 +376,7 @@ static int launch_mat(const sfk_plan* p, int64_t ncells, double* A, const double
 
 #ifdef SFK_MAT_ONLY_N
 // probe builds (tools/kernel_sweep.py c5): one instantiation of the FMA kernel
+}  // anonymous namespace
 }  // namespace sfk
 extern "C" int SFK_MAT_PROBE_ENTRY(const sfk_plan* p, int64_t ncells, double* A,
                                    const double* coords, const double* w0, void* stream) {
@@ -398,7 +403,9 @@ int launch_hex_matrix(const sfk_plan* p, int64_t ncells, double* A, const double
       }
       // (a DMMA version at n = 3 measured slower, 0.54 vs 0.37 ms: too little
       // work per cell for the padded tiles, profiles/r01bl_c5_p2_dmma.jsonl)
-      case 3: return launch_mat<3, 3, 3>(p, ncells, A, coords, s);
+      // one cell per 96-thread CTA at 6 CTAs per SM (tools/kernel_sweep.py c5,
+      // profiles/r02cs_c5_sweep.jsonl: 0.2908 -> 0.2499 ms; 3 cells per CTA before)
+      case 3: return launch_mat<3, 3, 1>(p, ncells, A, coords, s);
       case 4: {
         // DMMA kernel (hex_matrix_tc.cu); option c5_p3 = 1 selects the FMA one,
         // c5_hi_cfg = 3, 4 the chunked DMMA kernel of hex_matrix_tcn.cu (slower

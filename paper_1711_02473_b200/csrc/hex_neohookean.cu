@@ -32,13 +32,14 @@
 // of the executed instructions at p = 4, profiles/r02ce_C4_p4_opmix.txt);
 // unrolled, the constants are loaded where they are used.  Same-box A/B
 // (profiles/r02cg_c4_*.jsonl): p = 2 0.1603 -> 0.1557, p = 4 0.6758 -> 0.6492
-// ms; neutral at p = 3, slower at p = 5, 6 (220-254 registers) — so n = 3, 5.
+// ms; slower at p = 5, 6 (220-254 registers); p = 3 on the one-shot 6-cell CTAs
+// 0.2970 -> 0.2867 ms (profiles/r02ct_c4l_sweep2.jsonl) — so n = 3, 4, 5.
 // SFK_NEO_UNROLLA = 0 / 1 (A/B builds) forces rolled / unrolled everywhere.
 #ifndef SFK_NEO_UNROLLA
 #define SFK_NEO_UNROLLA -1
 #endif
 __host__ __device__ constexpr int neo_unroll_a(int n) {
-  return (SFK_NEO_UNROLLA >= 0 ? SFK_NEO_UNROLLA != 0 : (n == 3 || n == 5)) ? 3 : 1;
+  return (SFK_NEO_UNROLLA >= 0 ? SFK_NEO_UNROLLA != 0 : (n >= 3 && n <= 5)) ? 3 : 1;
 }
 #define NEO_PRAGMA_A _Pragma("unroll (neo_unroll_a(N))")
 
@@ -47,6 +48,10 @@ __host__ __device__ constexpr int neo_unroll_a(int n) {
 #endif
 
 namespace sfk {
+
+#ifdef SFK_C4L_ONLY_N
+namespace {   // probe objects differ in macros (SFK_NEO_UNROLLA): keep their instances apart
+#endif
 
 constexpr bool NEO_YT = SFK_NEO_YT;
 
@@ -419,6 +424,7 @@ static int launch_neo(const sfk_plan* p, int64_t ncells, double* A, const double
 
 #ifdef SFK_C4L_ONLY_N
 // probe builds (tools/kernel_sweep.py c4l): one instantiation of the line kernel
+}  // anonymous namespace
 }  // namespace sfk
 extern "C" int SFK_C4L_PROBE_ENTRY(const sfk_plan* p, int64_t ncells, double* A,
                                    const double* coords, const double* w0, void* stream) {

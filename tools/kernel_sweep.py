@@ -261,6 +261,8 @@ def c5_defines(v, entry):
     return ["-DSFK_MAT_ONLY_N=%d" % v["n"], "-DSFK_MATP_CPB=%d" % v["cpb"],
             "-DSFK_MAT_ZB=%d" % v["zb"], "-DSFK_MAT_YB=%d" % v["yb"],
             "-DSFK_MAT_MINB3=%d" % v["minb"], "-DSFK_MAT_PROBE_ENTRY=%s" % entry]
+    # (the kernel applies SFK_MAT_MINB3 at one cell per CTA only; the sweep of
+    # profiles/r02cs_c5_sweep.jsonl ran with it applied at every CPB)
 
 
 FAMILIES = {
