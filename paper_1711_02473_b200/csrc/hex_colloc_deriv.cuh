@@ -91,6 +91,26 @@ __device__ __forceinline__ void v6_contract(const double* T, const double* in, d
     for (int o = 0; o < NO; ++o) out[o] = fma(T[i * LD + o], in[i], out[o]);
 }
 
+// Two lines through the same table in one pass: every table entry (one LDCU
+// per use on sm_100a, DFMA takes no constant-bank operand) feeds two DFMAs.
+// Per output the operations and their order are those of v6_contract.
+template <int NI, int NO, int LD>
+__device__ __forceinline__ void v6_contract2(const double* T, const double* in1, const double* in2,
+                                             double* out1, double* out2) {
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+    out1[o] = T[o] * in1[0];
+    out2[o] = T[o] * in2[0];
+  }
+#pragma unroll
+  for (int i = 1; i < NI; ++i)
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      out1[o] = fma(T[i * LD + o], in1[i], out1[o]);
+      out2[o] = fma(T[i * LD + o], in2[i], out2[o]);
+    }
+}
+
 // out[o] = sum_i T[i][o] in[i] in even-odd form (EOTab), S = +1 / -1.
 template <int N, int S>
 __device__ __forceinline__ void v6_contract_eo(const EOTab<N>& E, const double* in, double* out) {

@@ -173,6 +173,9 @@ def c2_variants(n):
     if os.environ.get("SWEEP_LEVEL", "2") == "2":
         cpb0, minb0, zr0, ws0, eg0, bk0 = V6_DEFAULT[n]
         space = itertools.product(cpbs, (ws0,), (0, 1), sorted({0, eg0}), (0,), (0, 1))
+    elif os.environ.get("SWEEP_LEVEL") == "4":   # one-shot, fused D / F contractions (eo off)
+        space = ((cpb, V6_DEFAULT[n][3], zr, 0, bk, 1) for cpb in cpbs for zr in (0, 1)
+                 for bk in (0, 1))
     elif os.environ.get("SWEEP_LEVEL") == "3":   # one-shot x bulk staging x eg x zr
         space = itertools.product(cpbs, (V6_DEFAULT[n][3],), (0, 1), (0, 1), (0, 1), (1,))
     else:
@@ -186,6 +189,11 @@ def c2_variants(n):
         for minb in (0, 1, 2, 3, 4, 5, 6, 8):
             if minb and 65536 // (minb * threads) < 80:
                 continue
+            if os.environ.get("SWEEP_LEVEL") == "4":
+                for fdf, eo in ((1, 0), (0, 0), (0, V6_EO[n])):
+                    out.append(dict(n=n, cpb=cpb, ws=ws, zr=zr, eg=eg, bk=bk, eo=eo, minb=minb,
+                                    os=os_, fdf=fdf, threads=threads, smem=0))
+                continue
             out.append(dict(n=n, cpb=cpb, ws=ws, zr=zr, eg=eg, bk=bk, eo=V6_EO[n], minb=minb,
                             os=os_, threads=threads, smem=0))
     return out
@@ -196,6 +204,7 @@ def c2_defines(v, entry):
             "-DSFK_V6P_MINB=%d" % v["minb"], "-DSFK_V6P_ZR=%d" % v["zr"],
             "-DSFK_V6P_WS=%d" % v["ws"], "-DSFK_V6P_EG=%d" % v["eg"], "-DSFK_V6P_BK=%d" % v["bk"],
             "-DSFK_V6P_EO=%d" % v["eo"], "-DSFK_V6P_OS=%d" % v.get("os", 0),
+            "-DSFK_V6P_FDF=%d" % v.get("fdf", 0),
             "-DSFK_V6_PROBE_ENTRY=%s" % entry]
 
 
@@ -269,7 +278,7 @@ FAMILIES = {
     "c3": dict(src="hex_colloc.cu", variants=c3_variants, defines=c3_defines,
                keys=("cpb", "sy", "sx", "cs", "persist", "kg", "splitz", "minb", "geom", "fuse")),
     "c2": dict(src="hex_action6.cu", variants=c2_variants, defines=c2_defines,
-               keys=("cpb", "ws", "zr", "eg", "bk", "eo", "minb", "os")),
+               keys=("cpb", "ws", "zr", "eg", "bk", "eo", "minb", "os", "fdf")),
     "cell": dict(src="hex_action_cell.cu", variants=cell_variants, defines=cell_defines,
                  keys=("th", "cd", "lg", "minb")),
     "c4l": dict(src="hex_neohookean.cu", variants=c4l_variants, defines=c4l_defines,
