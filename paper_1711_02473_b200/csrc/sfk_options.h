@@ -24,7 +24,7 @@ enum Option : int {
   OPT_CELL_TH,       // cellv threads per CTA
   OPT_CELL_MINB,     // cellv min CTAs per SM
   OPT_COLLOC_WARPS,  // C3 warp-synchronous variant: warps per CTA, -1 = off
-  OPT_C3_TC,         // 1: C3 DMMA variant
+  OPT_C3_TC,         // 1: C3 CTA-wide DMMA variants (n = 8, 12, 16), 2: n = 8 on the one-warp-per-cell DMMA kernel
   OPT_C5_P1,         // 1: C5 p = 1 through the CTA-phase kernel
   OPT_C5_P3,         // 1: C5 p = 3 through the FMA phase kernel
   OPT_C5_P4,         // 1: C5 p = 4 through the FMA phase kernel, 2: through tc5
@@ -37,8 +37,8 @@ enum Option : int {
   OPT_LP_WARP,       // LoopProgram warp mode: -1 = off
   OPT_LP_MINB,
   OPT_LP_FUSE,       // LoopProgram loop fusion: -1 = off
-  OPT_V6_CFG,        // v6 (cells per CTA, min CTAs per SM) alternative 1..3 per n
-  OPT_NEO_CFG,       // C4 variant: 1 two points per pointwise iteration at every p, 2 at none
+  OPT_V6_CFG,        // v6 launch-shape / schedule alternatives per n (1..9: A/B history; 10, 11, 12: the persistent and earlier one-shot defaults)
+  OPT_NEO_CFG,       // C4 variant: 1 two points per pointwise iteration at every p, 2 at none, 3 component-parallel kernel everywhere, 4 line kernel everywhere, 5 persistent warp-mode line kernel (p <= 3), 6 one-shot line kernel at p = 4..6
   OPT_C3_CFG,        // C3 variant: 1 per-element staging copies everywhere
   OPT_C5_HI_CFG,
   OPT_P1_CFG,        // C2 p = 1 kernel: (cells per CTA, min CTAs per SM) alternative 1..3     // C5 p = 5..8 DMMA kernel: (iy block, warps per row tile) alternative 1, 2

@@ -220,7 +220,7 @@ def test_global_collocated_matches_oracle(cuda, p, weighted):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("p", [2, 3, 4, 6])
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 6])
 def test_global_neohookean_residual_matches_oracle(cuda, p):
     """Assembled nonlinear residual r(x) = sum_c P_c^T r_c(P_c x)."""
     torch = cuda
