@@ -29,7 +29,12 @@ constexpr size_t smem(int cpb) { return (size_t)cpb * (CS + US) * sizeof(double)
 // GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
 // item 1): u = x gathered through cmap[c][0..7], A = y scatter-added with
 // fp64 atomics.
-template <bool GS, int CPB = 128, int MINB = SFK_P1_MINB>
+// PERSIST: a resident grid of CTAs loops over the batches with two staging
+// buffers — the next batch's coords / u stream in (cp.async) behind the
+// current batch's arithmetic (the one-shot form waits for its loads with
+// nothing else to do: 22% long-scoreboard stalls at 12 warps per SM,
+// profiles/r02cm_p1.md).  The tables are 2 x 2: nothing for ptxas to hoist.
+template <bool GS, int CPB = 128, int MINB = SFK_P1_MINB, bool PERSIST = false>
 __global__ void __launch_bounds__(CPB, MINB)
 hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
                       const double* __restrict__ coords, const double* __restrict__ u,
@@ -37,12 +42,14 @@ hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
   using p1::CS;
   using p1::US;
   extern __shared__ __align__(16) double smem[];
-  double* sC = smem;
-  double* sU = smem + CPB * CS;
+  constexpr int BUF = CPB * (CS + US);   // doubles per staging buffer
   const int tid = threadIdx.x;
-  const int64_t cell0 = (int64_t)blockIdx.x * CPB;
-  const int ncb = (int)((ncells - cell0) < CPB ? (ncells - cell0) : CPB);
-  {
+  const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  auto stage = [&](int64_t bt, int buf) {
+    double* sC = smem + buf * BUF;
+    double* sU = sC + CPB * CS;
+    const int64_t cell0 = bt * CPB;
+    const int ncb = (int)((ncells - cell0) < CPB ? (ncells - cell0) : CPB);
     // 16-byte chunks: coords 12 per cell, u 4 per cell (both 16B-aligned
     // per cell when the bases are; otherwise fall back to 8-byte copies)
     const double* cg = coords + cell0 * 24;
@@ -65,11 +72,21 @@ hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
         for (int e = tid; e < ncb * 8; e += CPB) cp_async8(sU + (e >> 3) * US + (e & 7), ug + e);
     }
     cp_async_commit();
-    cp_async_wait<0>();
-  }
-  __syncthreads();
-  if (tid >= ncb) return;
-
+  };
+  int64_t bt = blockIdx.x;
+  if (bt >= nbatch) return;
+  stage(bt, 0);
+  int it = 0;
+  do {
+  const int cur = PERSIST ? (it & 1) : 0;
+  const double* sC = smem + cur * BUF;
+  const double* sU = sC + CPB * CS;
+  const int64_t cell0 = bt * CPB;
+  const int ncb = (int)((ncells - cell0) < CPB ? (ncells - cell0) : CPB);
+  cp_async_wait<0>();
+  __syncthreads();   // this batch landed; everybody is done reading the other buffer
+  if (PERSIST && bt + gridDim.x < nbatch) stage(bt + gridDim.x, cur ^ 1);
+  if (tid < ncb) {
   double X[24], uu[8];
   int gm[8];
 #pragma unroll
@@ -176,28 +193,34 @@ hex_laplace_action_p1(const __grid_constant__ Tabs<2, 2> T, int64_t ncells,
   if (GS) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) atomicAdd(A + gm[k], a[k]);
-    return;
-  }
-  double* ap = A + (cell0 + tid) * 8;
-  if ((reinterpret_cast<uintptr_t>(ap) & 15) == 0) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) reinterpret_cast<double2*>(ap)[k] = make_double2(a[2 * k], a[2 * k + 1]);
   } else {
+    double* ap = A + (cell0 + tid) * 8;
+    if ((reinterpret_cast<uintptr_t>(ap) & 15) == 0) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) ap[k] = a[k];
+      for (int k = 0; k < 4; ++k) reinterpret_cast<double2*>(ap)[k] = make_double2(a[2 * k], a[2 * k + 1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ap[k] = a[k];
+    }
   }
+  }   // tid < ncb
+  ++it;
+  } while (PERSIST && (bt += gridDim.x) < nbatch);
 }
 
-template <bool GS, int CPB, int MINB>
+template <bool GS, int CPB, int MINB, bool PERSIST = false>
 static int launch_p1_cfg(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                          const double* w0, cudaStream_t s, const int* cmap) {
-  auto kern = hex_laplace_action_p1<GS, CPB, MINB>;
+  auto kern = hex_laplace_action_p1<GS, CPB, MINB, PERSIST>;
+  const size_t smem = (PERSIST ? 2 : 1) * p1::smem(CPB);
   LaunchShape sh;
-  if (const int rc_ = kernel_shape((const void*)kern, CPB, p1::smem(CPB), "hex_action_p1", &sh))
+  if (const int rc_ = kernel_shape((const void*)kern, CPB, smem, "hex_action_p1", &sh, PERSIST))
     return rc_;
   const Tabs<2, 2> T = make_tabs<2, 2>(p);
-  const unsigned grid = (unsigned)((ncells + CPB - 1) / CPB);
-  kern<<<grid, CPB, p1::smem(CPB), s>>>(T, ncells, coords, w0, A, cmap);
+  const int64_t nbatch = (ncells + CPB - 1) / CPB;
+  const unsigned grid =
+      (unsigned)(PERSIST && nbatch > sh.resident() ? sh.resident() : nbatch);
+  if (grid > 0) kern<<<grid, CPB, smem, s>>>(T, ncells, coords, w0, A, cmap);
   note_launch();
   return cuda_status(cudaGetLastError(), "hex_laplace_action_p1 launch");
 }
@@ -212,6 +235,13 @@ static int launch_p1(const sfk_plan* p, int64_t ncells, double* A, const double*
     case 1: return launch_p1_cfg<GS, 64, 6>(p, ncells, A, coords, w0, s, cmap);
     case 2: return launch_p1_cfg<GS, 32, 12>(p, ncells, A, coords, w0, s, cmap);
     case 3: return launch_p1_cfg<GS, 96, 4>(p, ncells, A, coords, w0, s, cmap);
+    // persistent, double-buffered staging (A/B): measured slower, 0.0287 vs
+    // 0.0246 ms (profiles/r02cy_p1.txt) — the resident grid's 444 CTAs x 168
+    // registers leave no room for the extra waves that hide the tail
+    case 4: return launch_p1_cfg<GS, 128, SFK_P1_MINB, true>(p, ncells, A, coords, w0, s, cmap);
+    case 5: return launch_p1_cfg<GS, 64, 6, true>(p, ncells, A, coords, w0, s, cmap);
+    case 6: return launch_p1_cfg<GS, 96, 4, true>(p, ncells, A, coords, w0, s, cmap);
+    case 7: return launch_p1_cfg<GS, 32, 12, true>(p, ncells, A, coords, w0, s, cmap);
     default: return launch_p1_cfg<GS, 128, SFK_P1_MINB>(p, ncells, A, coords, w0, s, cmap);
   }
 }

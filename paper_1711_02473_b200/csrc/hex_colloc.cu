@@ -83,7 +83,7 @@ __host__ __device__ constexpr C3Policy c3_policy(int n) {
     case 9: return {false, false, 0, 1};
     case 10: return {false, false, 4, 1};
     case 11: return {false, true, 3, 3};
-    case 12: return {false, true, 4, 1};
+    case 12: return {true, true, 3, 3};   // third sweep (r02cy_c3_sweep3): with the padded layout
     case 13: return {false, true, 2, 1};
     case 14: return {true, true, 3, 1};
     case 15: return {true, false, 2, 3};
@@ -651,7 +651,7 @@ static int dispatch_colloc(const sfk_plan* p, int64_t ncells, double* A, const d
     }
   }
   // (N, cells/CTA, SY, SX, CS): strides from tools/smem_pads.py; the round-2
-  // sweep moved n = 6, 9, 10, 11, 12, 14 to the unpadded layout (smaller CTAs,
+  // sweep moved n = 6, 9, 10, 11, 14 to the unpadded layout (smaller CTAs,
   // 16-byte staging: more CTAs per SM beat the conflict-free strides) and
   // n = 10, 11 to one cell per CTA (profiles/r02cb_c3_sweep.jsonl)
   switch (p->n) {
@@ -665,7 +665,7 @@ static int dispatch_colloc(const sfk_plan* p, int64_t ncells, double* A, const d
     case 9: return launch_n<9, 3, 9, 81, 729, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 10: return launch_n<10, SFK_COLLOC_CPB10, 10, 100, 1000, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 11: return launch_n<11, 1, 11, 121, 1331, GS>(p, ncells, A, coords, w0, w1, s, cmap);
-    case 12: return launch_n<12, SFK_COLLOC_CPB12, 12, 144, 1728, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 12: return launch_n<12, SFK_COLLOC_CPB12, 13, 156, 1872, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 13: return launch_n<13, 1, 13, 169, 2197, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 14: return launch_n<14, 1, 14, 196, 2744, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 15: return launch_n<15, 1, 15, 225, 3375, GS>(p, ncells, A, coords, w0, w1, s, cmap);

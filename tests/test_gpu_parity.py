@@ -310,6 +310,36 @@ def test_c4_component_parallel_kernel(cuda, p):
         assert rel_err(_run(cuda, plan, small), ref) < TOL
 
 
+@pytest.mark.parametrize("cfg", range(1, 8))
+def test_c2_p1_kernel_variants(cuda, cfg):
+    """The thread-per-cell p = 1 kernel's launch shapes (option p1_cfg = 1..3)
+    and its persistent double-buffered forms (4..7: a resident grid looping
+    over the batches, more batches than CTAs, ragged last batch) give the
+    default kernel's result bit for bit, E-vector and global operator."""
+    torch = cuda
+    from paper_1711_02473_b200.assembly import GlobalOperator, lattice_dof_map, lattice_ndofs
+
+    plan = compile_kernel("action_laplace", "hex", 1)
+    dims = (48, 50, 53)                      # 127200 cells: > resident CTAs x 128
+    inp = workloads.c2_inputs(1, dims=dims)
+    inp = {k: v[:-37] for k, v in inp.items()}   # ragged
+    ref = _run(cuda, plan, inp)
+    with runtime.options(p1_cfg=cfg):
+        out = _run(cuda, plan, inp)
+    assert np.array_equal(out, ref)
+    # global operator (atomics: compare to rounding)
+    gd = (9, 10, 11)
+    coords = torch.from_numpy(workloads.lattice_coords(*gd)).cuda()
+    gmap = torch.from_numpy(lattice_dof_map(*gd, 1)).cuda()
+    nd = lattice_ndofs(*gd, 1)
+    x = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, nd)).cuda()
+    op = GlobalOperator(plan, gmap, coords, nd)
+    y0 = op.apply(x).cpu().numpy()
+    with runtime.options(p1_cfg=cfg):
+        y1 = op.apply(x).cpu().numpy()
+    assert np.abs(y1 - y0).max() <= 1e-13 * np.abs(y0).max()
+
+
 # ---------------------------------------------------------------------------
 # determinism, streams, threads, layouts
 

@@ -34,12 +34,14 @@ PROBE = os.path.join(ROOT, "paper_1711_02473_b200", "probe")
 # the product dispatch table (hex_colloc.cu dispatch_colloc): n -> (CPB, SY, SX, CS)
 TABLE = {5: (10, 5, 25, 125), 6: (7, 6, 36, 216), 7: (5, 7, 52, 369), 8: (4, 9, 72, 576),
          9: (3, 9, 81, 729), 10: (1, 10, 100, 1000), 11: (1, 11, 121, 1331),
-         12: (1, 12, 144, 1728), 13: (1, 13, 169, 2197), 14: (1, 14, 196, 2744),
+         12: (1, 13, 156, 1872), 13: (1, 13, 169, 2197), 14: (1, 14, 196, 2744),
          15: (1, 15, 225, 3375), 16: (1, 17, 272, 4352), 17: (1, 17, 289, 4913)}
 # first-level sweep (profiles/r02cb_c3_sweep.jsonl) used the round-1 table:
 # 6: (8, 6, 39, 244), 9: (3, 9, 89, 801), 10: (2, 11, 110, 1100), 11: (2, 11, 123, 1353),
 # 12: (1, 13, 156, 1872), 14: (1, 17, 238, 3332); SWEEP_LEVEL=1 re-runs its variant space
 SMEM_MAX = 227 * 1024
+# product fuse policy per n (hex_colloc.cu c3_policy)
+C3_FUSE = {7: 3, 8: 3, 9: 1, 10: 1, 11: 3, 12: 3, 13: 1, 14: 1, 15: 3, 16: 3, 17: 3}
 
 
 def default_policy(n):
@@ -81,8 +83,10 @@ def c3_variants(n):
             if minb == 1 and by_smem > 2:
                 continue
             for geom in ((0, 1) if n >= 13 else (0,)):
-                out.append(dict(n=n, cpb=cpb, sy=sy, sx=sx, cs=cs, persist=persist, kg=kg,
-                                splitz=splitz, minb=minb, geom=geom, threads=threads, smem=sm))
+                for fuse in sorted({C3_FUSE.get(n, 0), 3}) if os.environ.get("SWEEP_FUSE") else (0,):
+                    out.append(dict(n=n, cpb=cpb, sy=sy, sx=sx, cs=cs, persist=persist, kg=kg,
+                                    splitz=splitz, minb=minb, geom=geom, fuse=fuse,
+                                    threads=threads, smem=sm))
     return out
 
 
@@ -135,7 +139,7 @@ def c4_variants(n):
         if sm > SMEM_MAX:
             continue
         by_smem = min(8, (228 * 1024) // (sm + 1024))
-        if cpb > 1 and 3 * cpb * m * m > 400:
+        if cpb > 1 and 3 * cpb * m * m > 600:
             continue
         for minb in (0, 1, 2, 3, 4, 5, 6):
             if minb > by_smem or (minb and 65536 // (minb * threads) < 80):
