@@ -331,13 +331,28 @@ static int launch_tcn(const sfk_plan* p, int64_t ncells, double* A, const double
   return cuda_status(cudaGetLastError(), "hex_laplace_matrix_tcn launch");
 }
 
+#ifdef SFK_TCN_ONLY_N
+// probe builds (tools/kernel_sweep.py c5h): one instantiation
+}  // namespace sfk
+extern "C" int SFK_TCN_PROBE_ENTRY(const sfk_plan* p, int64_t ncells, double* A,
+                                   const double* coords, const double* w0, void* stream) {
+  (void)w0;
+  if (p->n != SFK_TCN_ONLY_N || p->m != SFK_TCN_ONLY_N)
+    return sfk::fail(SFK_EUNSUPPORTED, "probe build: n = m = %d only", SFK_TCN_ONLY_N);
+  return sfk::launch_tcn<SFK_TCN_ONLY_N, SFK_TCNP_IB, SFK_TCNP_WX>(p, ncells, A, coords,
+                                                                    (cudaStream_t)stream, nullptr);
+}
+namespace sfk {
+#else
 bool hex_matrix_tcn_supported(int n, int m) { return n == m && n >= 6 && n <= 9; }
 
 int launch_hex_matrix_tcn(const sfk_plan* p, int64_t ncells, double* A, const double* coords,
                           cudaStream_t s, const int32_t* emap) {
   if (p->collocated || p->n != p->m) return SFK_EUNSUPPORTED;
-  // (iy block, warps per x-stage row tile), measured per n (profiles/r02bb_c5h*);
-  // option c5_hi_cfg = 1, 2 selects the alternatives for A/B runs
+  // (iy block, warps per x-stage row tile) per n: the fastest of all
+  // combinations that fit (tools/kernel_sweep.py c5h, profiles/r02cz_c5h_sweep.jsonl:
+  // p = 5 / 6 / 7 / 8 3.48 / 4.59 / 3.87 / 6.15 -> 3.24 / 4.34 / 3.72 / 5.46 ms);
+  // option c5_hi_cfg = 1, 2 selects earlier alternatives, 5 the r02bb defaults
   const int cfg = (int)option(OPT_C5_HI_CFG);
   switch (p->n) {
     // n = 4: A/B against tc4 (option c5_hi_cfg = 3, 4); n = 5: the default
@@ -351,20 +366,26 @@ int launch_hex_matrix_tcn(const sfk_plan* p, int64_t ncells, double* A, const do
     case 6:   // 3.48 ms (2^14 cells) vs 3.89 <6,6,2>, 4.62 <6,3,2>
       if (cfg == 1) return launch_tcn<6, 3, 2>(p, ncells, A, coords, s, emap);
       if (cfg == 2) return launch_tcn<6, 6, 2>(p, ncells, A, coords, s, emap);
-      return launch_tcn<6, 6, 1>(p, ncells, A, coords, s, emap);
+      if (cfg == 5) return launch_tcn<6, 6, 1>(p, ncells, A, coords, s, emap);
+      return launch_tcn<6, 2, 1>(p, ncells, A, coords, s, emap);
     case 7:   // 4.59 ms (2^13 cells) vs 5.54 <7,1,2>, 5.93 <7,7,1>
       if (cfg == 1) return launch_tcn<7, 1, 2>(p, ncells, A, coords, s, emap);
       if (cfg == 2) return launch_tcn<7, 7, 1>(p, ncells, A, coords, s, emap);
-      return launch_tcn<7, 4, 2>(p, ncells, A, coords, s, emap);
+      if (cfg == 5) return launch_tcn<7, 4, 2>(p, ncells, A, coords, s, emap);
+      return launch_tcn<7, 7, 3>(p, ncells, A, coords, s, emap);
     case 8:   // 3.88 ms (2^12 cells) vs 3.98 <8,2,2>, 4.12 <8,4,1>
       if (cfg == 1) return launch_tcn<8, 2, 2>(p, ncells, A, coords, s, emap);
       if (cfg == 2) return launch_tcn<8, 4, 1>(p, ncells, A, coords, s, emap);
-      return launch_tcn<8, 1, 2>(p, ncells, A, coords, s, emap);
+      if (cfg == 5) return launch_tcn<8, 1, 2>(p, ncells, A, coords, s, emap);
+      return launch_tcn<8, 4, 2>(p, ncells, A, coords, s, emap);
     case 9:   // 6.17 ms (2^11 cells), <9,1,2> the same (and spills)
       if (cfg == 1) return launch_tcn<9, 1, 2>(p, ncells, A, coords, s, emap);
-      return launch_tcn<9, 1, 1>(p, ncells, A, coords, s, emap);
+      if (cfg == 5) return launch_tcn<9, 1, 1>(p, ncells, A, coords, s, emap);
+      return launch_tcn<9, 2, 1>(p, ncells, A, coords, s, emap);
     default: return SFK_EUNSUPPORTED;
   }
 }
+
+#endif  // SFK_TCN_ONLY_N
 
 }  // namespace sfk

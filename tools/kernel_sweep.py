@@ -278,6 +278,23 @@ def c5_defines(v, entry):
     # profiles/r02cs_c5_sweep.jsonl ran with it applied at every CPB)
 
 
+def c5h_variants(n):
+    """C5 chunked DMMA kernel (hex_matrix_tcn.cu): iy block x warps per row tile."""
+    out = []
+    rt = (n * n + 7) // 8
+    for ib, wx in itertools.product(range(1, n + 1), (1, 2, 3, 4)):
+        threads = 32 * rt * wx
+        if threads > 1024:
+            continue
+        out.append(dict(n=n, ib=ib, wx=wx, threads=threads, smem=0))
+    return out
+
+
+def c5h_defines(v, entry):
+    return ["-DSFK_TCN_ONLY_N=%d" % v["n"], "-DSFK_TCNP_IB=%d" % v["ib"],
+            "-DSFK_TCNP_WX=%d" % v["wx"], "-DSFK_TCN_PROBE_ENTRY=%s" % entry]
+
+
 FAMILIES = {
     "c3": dict(src="hex_colloc.cu", variants=c3_variants, defines=c3_defines,
                keys=("cpb", "sy", "sx", "cs", "persist", "kg", "splitz", "minb", "geom", "fuse")),
@@ -289,6 +306,8 @@ FAMILIES = {
                 keys=("warps", "cpb", "var", "unroll", "minb")),
     "c5": dict(src="hex_matrix.cu", variants=c5_variants, defines=c5_defines,
                keys=("cpb", "zb", "yb", "minb")),
+    "c5h": dict(src="hex_matrix_tcn.cu", variants=c5h_variants, defines=c5h_defines,
+                keys=("ib", "wx")),
     "c4": dict(src="hex_neohookean3.cu", variants=c4_variants, defines=c4_defines,
                keys=("cpb", "px", "lz", "ypad", "nyt", "minb", "oneshot")),
 }
@@ -388,6 +407,14 @@ def run(fam, ns):
             plan = compile_form(action_form(REGISTRY["weighted_laplace"]), "hex", p,
                                 "spectral", "spectral_gll", "collocated-gll")
             inp = workloads.c3_inputs(p)
+        elif fam == "c5h":
+            from paper_1711_02473_b200 import compile_kernel
+            plan = compile_kernel("laplace", "hex", p)
+            if p <= 4:
+                inp = workloads.c5_inputs()
+            else:   # the C5H batches of tools/bench_configs.py
+                nx = {5: 4, 6: 2, 7: 1, 8: 1}[p]
+                inp = {"coords": workloads.lattice_coords(nx, 64, 64 if p <= 7 else 32)}
         elif fam == "c5":
             from paper_1711_02473_b200 import compile_kernel
             plan = compile_kernel("laplace", "hex", p)
