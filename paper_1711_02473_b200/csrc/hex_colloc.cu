@@ -162,6 +162,14 @@ __host__ __device__ constexpr bool colloc_splitz(int n) {
 #endif
 __host__ __device__ constexpr int colloc_fuse(int n) { return c3p(n, SFK_C3P_FUSE, c3_policy(n).fuse); }
 
+// UQ: unroll factor of the split z phase's pointwise loop (1 = rolled; 2+:
+// that many points' dependency chains in flight per thread, more registers)
+#ifndef SFK_C3P_UQ
+#define SFK_C3P_UQ -1
+#endif
+// (sweep: n = 16 4.046 -> 3.799 ms at 2; neutral or slower elsewhere, profiles/r02db_c3_uq.jsonl)
+__host__ __device__ constexpr int colloc_uq(int n) { return c3p(n, SFK_C3P_UQ, n == 16 ? 2 : 1); }
+
 __host__ __device__ constexpr int colloc_minb(int n) {
 #ifdef SFK_COLLOC_MINB
   if (SFK_COLLOC_MINB >= 0) return SFK_COLLOC_MINB;   // A/B builds (tools/build_variant.py)
@@ -352,7 +360,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
         geo.setup(sC + c * 24, T.Bc[a], T.Bc[N + a], T.Bc[b], T.Bc[N + b]);
         const double wxy = T.W[a] * T.W[b];
         const double* kp = KG ? kappa + (cell0 + (c < ncb ? c : 0)) * N3 + a * NN + b * N : sK + base;
-  #pragma unroll 1
+  #pragma unroll (colloc_uq(N))
         for (int q = 0; q < N; ++q) {
           double gx = sGX[bx + q], gy = sGY[by + q], gz = sU[base + q];
           double r0[3], r1[3], r2[3];

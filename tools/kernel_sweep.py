@@ -62,6 +62,8 @@ def smem_bytes(n, cpb, cs, persist, kg):
 def c3_variants(n):
     if os.environ.get("SWEEP_LEVEL", "2") == "2":
         return c3_variants_l2(n)
+    if os.environ.get("SWEEP_LEVEL") == "uq":
+        return c3_variants_uq(n)
     cpb0, sy0, sx0, cs0 = TABLE[n]
     strides = {(sy0, sx0, cs0), (n, n * n, n ** 3)}
     so = n | 1
@@ -87,6 +89,28 @@ def c3_variants(n):
                     out.append(dict(n=n, cpb=cpb, sy=sy, sx=sx, cs=cs, persist=persist, kg=kg,
                                     splitz=splitz, minb=minb, geom=geom, fuse=fuse,
                                     threads=threads, smem=sm))
+    return out
+
+
+def c3_variants_uq(n):
+    """Split-z kernels: pointwise-loop unroll factor x min-blocks on the product policy."""
+    cpb, sy, sx, cs = TABLE[n]
+    pol = {5: (0, 1, 0), 6: (0, 1, 0), 11: (0, 1, 3), 12: (1, 1, 3), 13: (0, 1, 1), 14: (1, 1, 1),
+           16: (1, 1, 3)}.get(n)
+    if pol is None:
+        return []
+    kg, splitz, fuse = pol
+    threads = -(-cpb * n * n // 32) * 32
+    sm = smem_bytes(n, cpb, cs, 0, kg)
+    by_smem = min(8, (228 * 1024) // (sm + 1024))
+    out = []
+    for uq in (1, 2, 3, 4):
+        for minb in (0, 1, 2, 3, 4, 5, 6):
+            if minb > by_smem or (minb and 65536 // (minb * threads) < 72):
+                continue
+            out.append(dict(n=n, cpb=cpb, sy=sy, sx=sx, cs=cs, persist=0, kg=kg, splitz=splitz,
+                            minb=minb, geom=int(n in (15, 16)), fuse=fuse, uq=uq,
+                            threads=threads, smem=sm))
     return out
 
 
@@ -117,6 +141,7 @@ def c3_defines(v, entry):
             "-DSFK_C3P_PERSIST=%d" % v["persist"], "-DSFK_C3P_KG=%d" % v["kg"],
             "-DSFK_C3P_SPLITZ=%d" % v["splitz"], "-DSFK_C3P_MINB=%d" % v["minb"],
             "-DSFK_C3P_GEOM=%d" % v["geom"], "-DSFK_C3P_FUSE=%d" % v.get("fuse", 0),
+            "-DSFK_C3P_UQ=%d" % v.get("uq", -1),
             "-DSFK_C3_PROBE_ENTRY=%s" % entry]
 
 
@@ -297,7 +322,7 @@ def c5h_defines(v, entry):
 
 FAMILIES = {
     "c3": dict(src="hex_colloc.cu", variants=c3_variants, defines=c3_defines,
-               keys=("cpb", "sy", "sx", "cs", "persist", "kg", "splitz", "minb", "geom", "fuse")),
+               keys=("cpb", "sy", "sx", "cs", "persist", "kg", "splitz", "minb", "geom", "fuse", "uq")),
     "c2": dict(src="hex_action6.cu", variants=c2_variants, defines=c2_defines,
                keys=("cpb", "ws", "zr", "eg", "bk", "eo", "minb", "os", "fdf")),
     "cell": dict(src="hex_action_cell.cu", variants=cell_variants, defines=cell_defines,
