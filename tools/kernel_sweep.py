@@ -183,11 +183,11 @@ def c4_defines(v, entry):
 
 
 # v6 product defaults (hex_action6.cu launch_hex_action_v6): n -> EO (parity-gated, fixed)
-V6_EO = {4: 0, 5: 1, 6: 1, 7: 0, 8: 0, 9: 0}
+V6_EO = {3: 0, 4: 0, 5: 1, 6: 1, 7: 0, 8: 0, 9: 0}
 
 
 # v6 product defaults (cpb, minb, zr, ws, eg, bk) per n
-V6_DEFAULT = {4: (16, 2, 1, 1, 0, 0), 5: (5, 4, 1, 0, 0, 0), 6: (7, 2, 1, 0, 0, 0),
+V6_DEFAULT = {3: (12, 4, 0, 1, 0, 0), 4: (16, 2, 1, 1, 0, 0), 5: (5, 4, 1, 0, 0, 0), 6: (7, 2, 1, 0, 0, 0),
               7: (5, 2, 1, 0, 0, 0), 8: (4, 2, 0, 0, 0, 0), 9: (3, 2, 0, 0, 1, 1)}
 
 
@@ -197,7 +197,7 @@ def c2_variants(n):
     profiles/r02cg_c2_sweep.jsonl."""
     out = []
     nn = n * n
-    cpbs = {4: (2, 4, 6, 8, 12, 16), 5: (2, 3, 4, 5, 6, 8, 10), 6: (3, 4, 5, 6, 7, 8),
+    cpbs = {3: (3, 6, 12, 24), 4: (2, 4, 6, 8, 12, 16), 5: (2, 3, 4, 5, 6, 8, 10), 6: (3, 4, 5, 6, 7, 8),
             7: (2, 3, 4, 5, 6), 8: (2, 3, 4, 5), 9: (1, 2, 3, 4)}[n]
     if os.environ.get("SWEEP_LEVEL", "2") == "2":
         cpb0, minb0, zr0, ws0, eg0, bk0 = V6_DEFAULT[n]
