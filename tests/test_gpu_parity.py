@@ -340,6 +340,32 @@ def test_c2_p1_kernel_variants(cuda, cfg):
     assert np.abs(y1 - y0).max() <= 1e-13 * np.abs(y0).max()
 
 
+@pytest.mark.parametrize("family,p", [("c3", 4), ("c3", 7), ("c3", 10), ("c3", 11), ("c3", 15),
+                                      ("c3", 16), ("c4", 2), ("c4", 3), ("c4", 4), ("c4", 5),
+                                      ("c4", 6)])
+def test_c3_c4_bitwise_reproducible(cuda, family, p):
+    """The swept C3 / C4 kernels (fused x/y contractions, in-place z phases,
+    the component-parallel kernel's three-way split of a z-line's points) are
+    race-free as far as repetition can tell: five runs on a batch that fills
+    the GPU several times over give identical bits."""
+    torch = cuda
+    if family == "c3":
+        plan = compile_form(action_form(REGISTRY["weighted_laplace"]), "hex", p,
+                            "spectral", "spectral_gll", "collocated-gll")
+        inp = workloads.c3_inputs(p, dims=(8, 16, 16) if p <= 11 else (4, 8, 16))
+    else:
+        plan = compile_form(neohookean_residual_form(), "hex", p, quadrature=p + 2)
+        inp = workloads.c4_inputs(p, dims=(8, 16, 16))
+    d = _dev(torch, inp)
+    ref = evaluate_batched(plan, d)
+    torch.cuda.synchronize()
+    for _ in range(4):
+        out = evaluate_batched(plan, d)
+        torch.cuda.synchronize()
+        assert torch.equal(torch.nan_to_num(out), torch.nan_to_num(ref))
+        assert torch.equal(torch.isnan(out), torch.isnan(ref))
+
+
 # ---------------------------------------------------------------------------
 # determinism, streams, threads, layouts
 
