@@ -225,6 +225,17 @@ static int launch_p1_cfg(const sfk_plan* p, int64_t ncells, double* A, const dou
   return cuda_status(cudaGetLastError(), "hex_laplace_action_p1 launch");
 }
 
+#ifdef SFK_P1_ONLY
+// probe builds (tools/kernel_sweep.py p1): one instantiation
+}  // namespace sfk
+extern "C" int SFK_P1_PROBE_ENTRY(const sfk_plan* p, int64_t ncells, double* A,
+                                  const double* coords, const double* w0, void* stream) {
+  if (p->n != 2 || p->m != 2) return sfk::fail(SFK_EUNSUPPORTED, "probe build: n = m = 2 only");
+  return sfk::launch_p1_cfg<false, SFK_P1P_CPB, SFK_P1P_MINB, SFK_P1P_PERSIST != 0>(
+      p, ncells, A, coords, w0, (cudaStream_t)stream, nullptr);
+}
+namespace sfk {
+#else
 // (cells per CTA, min CTAs per SM): option p1_cfg = 1..3 selects the
 // alternatives (A/B runs)
 template <bool GS>
@@ -255,5 +266,7 @@ int launch_hex_action_p1_gs(const sfk_plan* p, int64_t ncells, const int* cmap, 
                             double* y, const double* coords, cudaStream_t s) {
   return launch_p1<true>(p, ncells, y, coords, x, s, cmap);
 }
+
+#endif  // SFK_P1_ONLY
 
 }  // namespace sfk

@@ -320,6 +320,23 @@ def c5h_defines(v, entry):
             "-DSFK_TCNP_WX=%d" % v["wx"], "-DSFK_TCN_PROBE_ENTRY=%s" % entry]
 
 
+def p1_variants(n):
+    """C2 p = 1 thread-per-cell kernel (hex_action_p1.cu): cells per CTA x min-blocks."""
+    out = []
+    for cpb, persist in itertools.product((32, 64, 96, 128, 160, 192, 256), (0, 1)):
+        for minb in (0, 1, 2, 3, 4, 5, 6, 8, 10, 12):
+            if minb and 65536 // (minb * cpb) < 128:
+                continue
+            sm = (2 if persist else 1) * cpb * 36 * 8
+            out.append(dict(n=n, cpb=cpb, minb=minb, persist=persist, threads=cpb, smem=sm))
+    return out
+
+
+def p1_defines(v, entry):
+    return ["-DSFK_P1_ONLY=1", "-DSFK_P1P_CPB=%d" % v["cpb"], "-DSFK_P1P_MINB=%d" % v["minb"],
+            "-DSFK_P1P_PERSIST=%d" % v["persist"], "-DSFK_P1_PROBE_ENTRY=%s" % entry]
+
+
 FAMILIES = {
     "c3": dict(src="hex_colloc.cu", variants=c3_variants, defines=c3_defines,
                keys=("cpb", "sy", "sx", "cs", "persist", "kg", "splitz", "minb", "geom", "fuse", "uq")),
@@ -333,6 +350,8 @@ FAMILIES = {
                keys=("cpb", "zb", "yb", "minb")),
     "c5h": dict(src="hex_matrix_tcn.cu", variants=c5h_variants, defines=c5h_defines,
                 keys=("ib", "wx")),
+    "p1": dict(src="hex_action_p1.cu", variants=p1_variants, defines=p1_defines,
+               keys=("cpb", "minb", "persist")),
     "c4": dict(src="hex_neohookean3.cu", variants=c4_variants, defines=c4_defines,
                keys=("cpb", "px", "lz", "ypad", "nyt", "minb", "oneshot")),
 }
@@ -444,7 +463,7 @@ def run(fam, ns):
             from paper_1711_02473_b200 import compile_kernel
             plan = compile_kernel("laplace", "hex", p)
             inp = workloads.c5_inputs()
-        elif fam in ("c2", "cell"):
+        elif fam in ("c2", "cell", "p1"):
             from paper_1711_02473_b200 import compile_kernel
             plan = compile_kernel("action_laplace", "hex", p)
             inp = workloads.c2_inputs(p)
