@@ -449,7 +449,9 @@ static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const doub
   // (tools/kernel_sweep.py c4, profiles/r02cj_c4_sweep2.jsonl); at p = 2..4 the
   // line kernel with one-shot CTAs stays ahead (p = 4: 0.569 vs 0.612 ms,
   // profiles/r02cp_c4_*.jsonl).
-  if (m == n + 1 && (var == 3 || (n >= 6 && var == 0))) {
+  // (global operator: p = 5 only — with the atomic scatter the persistent line
+  // kernel is ahead at p = 6, 1.93 vs 2.17 ms, profiles/r02dj_c4g_*.jsonl)
+  if (m == n + 1 && (var == 3 || (var == 0 && (GS ? n == 6 : n >= 6)))) {
     const int rc = GS ? launch_hex_neohookean3_gs(p, ncells, cmap, w0, A, coords, s)
                       : launch_hex_neohookean3(p, ncells, A, coords, w0, s);
     if (rc != SFK_EUNSUPPORTED) return rc;
