@@ -442,15 +442,22 @@ static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const doub
   const int n = p->n, m = p->m;
   const int64_t ow = option(OPT_NEO_WARPS);   // 0: built-in, < 0: off
   const int warps = ow == 0 ? SFK_NEO_WARPS_DEFAULT : ow < 0 ? 0 : (int)ow;
-  const int var = (int)option(OPT_NEO_CFG);   // 1: two points per pointwise iteration everywhere
-  // component-parallel kernel (hex_neohookean3.cu): option neo_cfg = 3 wherever
-  // it is instantiated, 4 nowhere
-  // Default at p = 5, 6 (n = 6, 7): 1.257 -> 1.006, 1.759 -> 1.691 ms
-  // (tools/kernel_sweep.py c4, profiles/r02cj_c4_sweep2.jsonl); at p = 2..4 the
-  // line kernel with one-shot CTAs stays ahead (p = 4: 0.569 vs 0.612 ms,
-  // profiles/r02cp_c4_*.jsonl).
-  // (global operator: p = 5 only — with the atomic scatter the persistent line
-  // kernel is ahead at p = 6, 1.93 vs 2.17 ms, profiles/r02dj_c4g_*.jsonl)
+  const int var = (int)option(OPT_NEO_CFG);
+  // Defaults per degree (m = n + 1), each the fastest of its sweep or A/B run
+  // (tools/kernel_sweep.py c4 / c4l; profiles named in brackets):
+  //   p = 1     warp-synchronous line kernel, one-shot CTAs
+  //   p = 2     the same, two warps per CTA                      [r02cq]
+  //   p = 3     CTA-mode line kernel, 6 cells per 160-thread CTA,
+  //             one-shot, 3 CTAs per SM, component loops unrolled [r02cq, r02ct]
+  //   p = 4     CTA-mode line kernel, 3 cells per CTA, one-shot   [r02cp]
+  //   p = 5, 6  component-parallel kernel (hex_neohookean3.cu),
+  //             one-shot: 1.257 -> 1.006, 1.759 -> 1.691 ms       [r02cj]
+  //             (global operator at p = 6: persistent two-point line
+  //             kernel, 1.93 vs 2.17 ms with the atomic scatter)  [r02dj]
+  // option neo_cfg: 1 two points per pointwise iteration everywhere, 2 nowhere,
+  // 3 the component-parallel kernel wherever it is instantiated, 4 the line
+  // kernel everywhere, 5 persistent warp-mode kernels at p <= 3, 6 the one-shot
+  // line kernel at p = 4..6.
   if (m == n + 1 && (var == 3 || (var == 0 && (GS ? n == 6 : n >= 6)))) {
     const int rc = GS ? launch_hex_neohookean3_gs(p, ncells, cmap, w0, A, coords, s)
                       : launch_hex_neohookean3(p, ncells, A, coords, w0, s);
@@ -472,11 +479,9 @@ static int dispatch_neo(const sfk_plan* p, int64_t ncells, double* A, const doub
       if (n == 4) return launch_neo<4, 5, 1, GS, 4, 1>(p, ncells, A, coords, w0, s, cmap);
     } else {
       // one-shot CTAs (VAR bit 1): p = 2 0.1566 -> 0.1464, p = 3 0.3738 ->
-      // 0.3359 ms (profiles/r02cl_c4_*.jsonl)
-      // sweep of (warps, cells, two-point, min-blocks) on the one-shot kernel
-      // (tools/kernel_sweep.py c4l, profiles/r02cq_c4l_sweep.jsonl): p = 2 two
-      // warps per CTA 0.1464 -> 0.1392 ms; p = 3 CTA mode, 6 cells per 160-thread
-      // CTA at 3 CTAs per SM 0.3338 -> 0.2870 ms
+      // 0.3359 ms (profiles/r02cl_c4_*.jsonl); then the shapes of the c4l sweep
+      // (profiles/r02cq_c4l_sweep.jsonl): p = 2 0.1464 -> 0.1392, p = 3 0.3338
+      // -> 0.2870 ms
       if (n == 2) return launch_neo<2, 3, 3, GS, 4, 2>(p, ncells, A, coords, w0, s, cmap);
       if (n == 3) return launch_neo<3, 4, 2, GS, 2, 2>(p, ncells, A, coords, w0, s, cmap);
       if (n == 4) return launch_neo<4, 5, 6, GS, 0, 2, 3>(p, ncells, A, coords, w0, s, cmap);
