@@ -37,8 +37,12 @@ int fail(int status, const char* fmt, ...);
 int cuda_status(cudaError_t err, const char* what);
 void note_launch(int64_t k = 1);
 
-// Tables in the form kernels consume them (kernel parameter => constant bank;
-// compile-time indices become c[0x0][...] operands of DFMA, no loads).
+// Tables in the form kernels consume them (kernel parameter => constant
+// bank).  On sm_100a DFMA takes no constant-bank operand: an entry with a
+// compile-time index reaches it through a uniform register (LDCU, then
+// DFMA R, R, UR, R) — one extra instruction per use unless the entry feeds
+// several DFMAs, and a reason to keep such kernels free of loops ptxas could
+// hoist the loads out of.
 template <int N, int M>
 struct Tabs {
   double B[N * M];
