@@ -77,9 +77,11 @@ struct C3Policy {
 };
 __host__ __device__ constexpr C3Policy c3_policy(int n) {
   switch (n) {
-    case 5: case 6: return {false, true, 3, 0};
+    // n = 5, 6, 8: small CTAs from the wide cells-per-CTA sweep (r02dm_c3_cpb.jsonl)
+    case 5: return {false, false, 0, 0};
+    case 6: return {false, false, 4, 0};
     case 7: return {true, false, 0, 3};
-    case 8: return {true, false, 2, 3};
+    case 8: return {true, false, 8, 3};
     case 9: return {false, false, 0, 1};
     case 10: return {false, false, 4, 1};
     case 11: return {false, true, 3, 3};
@@ -104,9 +106,8 @@ struct TabsD {
 // cp.async while the current batch computes.  Round 1 kept it at n = 5 only
 // (p = 4 0.1167 -> 0.1127 ms; at n = 6..11 the doubled u / kappa buffers cost
 // occupancy, profiles/r01ck_*.jsonl); the round-2 sweep (tools/kernel_sweep.py,
-// profiles/r02cb_c3_sweep.jsonl) found one-shot CTAs with the split z phase at
-// 80 registers faster there too (0.1127 -> 0.1045 ms), so no n uses it by
-// default.  SFK_COLLOC_PERSIST=n0 (A/B builds) makes every n <= n0 persistent.
+// profiles/r02cb_c3_sweep.jsonl, r02dm_c3_cpb.jsonl) found small one-shot CTAs
+// faster there too (0.1127 -> 0.0983 ms), so no n uses it by default.  SFK_COLLOC_PERSIST=n0 (A/B builds) makes every n <= n0 persistent.
 #ifdef SFK_COLLOC_PERSIST
 __host__ __device__ constexpr bool colloc_persist(int n) { return n <= SFK_COLLOC_PERSIST; }
 #else
@@ -141,8 +142,8 @@ struct CollocCfg {
 // register budgets for the last two (e.g. n = 16: 132 vs 254 registers).
 // SPLITZ: phase 3 as three register-light passes over the thread's own lines
 // instead of one fused loop (round 1, n = 12..15: p = 11 1.969 -> 1.664 ms,
-// p = 13 3.803 -> 3.085, profiles/r01cf_*.jsonl; round 2 adds n = 5, 6, 11 and
-// 16 and drops 15, see c3_policy).
+// p = 13 3.803 -> 3.085, profiles/r01cf_*.jsonl; round 2 adds n = 11 and 16
+// and drops 15, see c3_policy).
 // SFK_COLLOC_SPLITZ=n0 (A/B builds) splits every n >= n0.
 __host__ __device__ constexpr bool colloc_splitz(int n) {
 #ifdef SFK_COLLOC_SPLITZ
@@ -661,15 +662,18 @@ static int dispatch_colloc(const sfk_plan* p, int64_t ncells, double* A, const d
   // (N, cells/CTA, SY, SX, CS): strides from tools/smem_pads.py; the round-2
   // sweep moved n = 6, 9, 10, 11, 14 to the unpadded layout (smaller CTAs,
   // 16-byte staging: more CTAs per SM beat the conflict-free strides) and
-  // n = 10, 11 to one cell per CTA (profiles/r02cb_c3_sweep.jsonl)
+  // n = 10, 11 to one cell per CTA (profiles/r02cb_c3_sweep.jsonl); a wider
+  // cells-per-CTA sweep at n = 5..9 (r02dm_c3_cpb.jsonl) then moved n = 5, 6, 8
+  // to 128- / 128- / 64-thread CTAs (p = 4, 5, 7: 0.1045 / 0.1685 / 0.3686 ->
+  // 0.0983 / 0.1577 / 0.3338 ms)
   switch (p->n) {
     case 2: return launch_n<2, 16, 2, 5, 12, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 3: return launch_n<3, 16, 3, 9, 27, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 4: return launch_n<4, 8, 4, 19, 76, GS>(p, ncells, A, coords, w0, w1, s, cmap);
-    case 5: return launch_n<5, 10, 5, 25, 125, GS>(p, ncells, A, coords, w0, w1, s, cmap);
-    case 6: return launch_n<6, 7, 6, 36, 216, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 5: return launch_n<5, 5, 5, 25, 125, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 6: return launch_n<6, 3, 6, 36, 216, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 7: return launch_n<7, 5, 7, 52, 369, GS>(p, ncells, A, coords, w0, w1, s, cmap);
-    case 8: return launch_n<8, 4, 9, 72, 576, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 8: return launch_n<8, 1, 9, 72, 576, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 9: return launch_n<9, 3, 9, 81, 729, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 10: return launch_n<10, SFK_COLLOC_CPB10, 10, 100, 1000, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 11: return launch_n<11, 1, 11, 121, 1331, GS>(p, ncells, A, coords, w0, w1, s, cmap);

@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 PROBE = os.path.join(ROOT, "paper_1711_02473_b200", "probe")
 
 # the product dispatch table (hex_colloc.cu dispatch_colloc): n -> (CPB, SY, SX, CS)
-TABLE = {5: (10, 5, 25, 125), 6: (7, 6, 36, 216), 7: (5, 7, 52, 369), 8: (4, 9, 72, 576),
+TABLE = {5: (5, 5, 25, 125), 6: (3, 6, 36, 216), 7: (5, 7, 52, 369), 8: (1, 9, 72, 576),
          9: (3, 9, 81, 729), 10: (1, 10, 100, 1000), 11: (1, 11, 121, 1331),
          12: (1, 13, 156, 1872), 13: (1, 13, 169, 2197), 14: (1, 14, 196, 2744),
          15: (1, 15, 225, 3375), 16: (1, 17, 272, 4352), 17: (1, 17, 289, 4913)}
@@ -64,6 +64,8 @@ def c3_variants(n):
         return c3_variants_l2(n)
     if os.environ.get("SWEEP_LEVEL") == "uq":
         return c3_variants_uq(n)
+    if os.environ.get("SWEEP_LEVEL") == "cpb":
+        return c3_variants_cpb(n)
     cpb0, sy0, sx0, cs0 = TABLE[n]
     strides = {(sy0, sx0, cs0), (n, n * n, n ** 3)}
     so = n | 1
@@ -111,6 +113,27 @@ def c3_variants_uq(n):
             out.append(dict(n=n, cpb=cpb, sy=sy, sx=sx, cs=cs, persist=0, kg=kg, splitz=splitz,
                             minb=minb, geom=int(n in (15, 16)), fuse=fuse, uq=uq,
                             threads=threads, smem=sm))
+    return out
+
+
+def c3_variants_cpb(n):
+    """Wide cells-per-CTA range (1..12) on the product layout and fuse policy."""
+    _c, sy, sx, cs = TABLE[n]
+    fuse = C3_FUSE.get(n, 0)
+    out = []
+    for cpb, kg, splitz in itertools.product(range(1, 13), (0, 1), (0, 1)):
+        threads = -(-cpb * n * n // 32) * 32
+        if threads > 1024:
+            continue
+        sm = smem_bytes(n, cpb, cs, 0, kg)
+        if sm > SMEM_MAX:
+            continue
+        by_smem = min(16, (228 * 1024) // (sm + 1024))
+        for minb in (0, 2, 3, 4, 6, 8):
+            if minb > by_smem or (minb and 65536 // (minb * threads) < 72):
+                continue
+            out.append(dict(n=n, cpb=cpb, sy=sy, sx=sx, cs=cs, persist=0, kg=kg, splitz=splitz,
+                            minb=minb, geom=0, fuse=fuse, threads=threads, smem=sm))
     return out
 
 
