@@ -360,6 +360,29 @@ def p1_defines(v, entry):
             "-DSFK_P1P_PERSIST=%d" % v["persist"], "-DSFK_P1_PROBE_ENTRY=%s" % entry]
 
 
+def c2g_variants(n):
+    """Global operator (fused gather / scatter) on v6: one-shot, no bulk staging."""
+    out = []
+    nn = n * n
+    cpbs = {4: (2, 4, 6, 8, 12, 16), 5: (2, 3, 4, 5, 6, 8, 10), 6: (3, 4, 5, 6, 7, 8),
+            7: (2, 3, 4, 5, 6), 9: (1, 2, 3, 4)}[n]
+    ws0 = V6_DEFAULT[n][3]
+    for cpb, zr, os_ in itertools.product(cpbs, (0, 1), (0, 1)):
+        if ws0 and (nn > 32 or cpb % (32 // nn)):
+            continue
+        threads = 32 * (cpb // (32 // nn)) if ws0 else -(-cpb * nn // 32) * 32
+        for minb in (0, 1, 2, 3, 4, 5, 6, 8):
+            if minb and 65536 // (minb * threads) < 80:
+                continue
+            out.append(dict(n=n, cpb=cpb, ws=ws0, zr=zr, eg=0, bk=0, eo=V6_EO[n], minb=minb,
+                            os=os_, fdf=0, threads=threads, smem=0))
+    return out
+
+
+def c2g_defines(v, entry):
+    return c2_defines(v, entry) + ["-DSFK_V6P_GS=1"]
+
+
 FAMILIES = {
     "c3": dict(src="hex_colloc.cu", variants=c3_variants, defines=c3_defines,
                keys=("cpb", "sy", "sx", "cs", "persist", "kg", "splitz", "minb", "geom", "fuse", "uq")),
@@ -375,6 +398,8 @@ FAMILIES = {
                 keys=("ib", "wx")),
     "p1": dict(src="hex_action_p1.cu", variants=p1_variants, defines=p1_defines,
                keys=("cpb", "minb", "persist")),
+    "c2g": dict(src="hex_action6.cu", variants=c2g_variants, defines=c2g_defines,
+                keys=("cpb", "ws", "zr", "eo", "minb", "os")),
     "c4": dict(src="hex_neohookean3.cu", variants=c4_variants, defines=c4_defines,
                keys=("cpb", "px", "lz", "ypad", "nyt", "minb", "oneshot")),
 }
@@ -430,6 +455,50 @@ def build(fam, ns):
                  os.path.getsize(out) / 1e6), flush=True)
 
 
+def run_c2g(n, man, plib, lib, runtime, workloads, torch, dev, stream, time_launch):
+    """Global operator variants on the (64, 64, 64) lattice's continuous Q_p space."""
+    from paper_1711_02473_b200 import compile_kernel
+    from paper_1711_02473_b200.assembly import GlobalOperator, lattice_dof_map, lattice_ndofs
+
+    p = n - 1
+    dims = (64, 64, 64)
+    plan = compile_kernel("action_laplace", "hex", p)
+    coords = torch.from_numpy(workloads.lattice_coords(*dims)).to(dev)
+    gmap = torch.from_numpy(lattice_dof_map(*dims, p)).to(dev)
+    nd = lattice_ndofs(*dims, p)
+    C = coords.shape[0]
+    x = torch.rand(nd, dtype=torch.float64, device=dev)
+    op = GlobalOperator(plan, gmap, coords, nd)
+    ref = op.apply(x)
+    y = torch.zeros_like(x)
+    t0 = time_launch(lambda: op.apply(x, out=y, accumulate=True))
+    print(json.dumps({"n": n, "p": p, "variant": "product", "ms": round(t0 * 1e3, 5)}), flush=True)
+    h = runtime.native_plan(plan)
+    scale = float(ref.abs().max())
+    vp, i64 = ctypes.c_void_p, ctypes.c_int64
+    for v in man:
+        fn = getattr(plib, v["entry"])
+        fn.restype = ctypes.c_int
+        fn.argtypes = [vp, i64, vp, vp, vp, vp, vp]
+        y.zero_()
+        call = lambda: fn(h, C, y.data_ptr(), coords.data_ptr(), x.data_ptr(), gmap.data_ptr(),
+                          stream.cuda_stream)
+        rc = call()
+        torch.cuda.synchronize()
+        rec = {k: v.get(k, 0) for k in ("n",) + FAMILIES["c2g"]["keys"] + ("threads", "regs", "spill")}
+        if rc != 0:
+            rec["rc"] = rc
+            print(json.dumps(rec), flush=True)
+            continue
+        err = float((y - ref).abs().max()) / scale
+        rec["err_vs_product"] = err
+        rec["ms"] = round(time_launch(call) * 1e3, 5) if err <= 1e-13 else None
+        print(json.dumps(rec), flush=True)
+    print(json.dumps({"n": n, "p": p, "variant": "product",
+                      "ms": round(time_launch(lambda: op.apply(x, out=y, accumulate=True)) * 1e3, 5)}),
+          flush=True)
+
+
 def run(fam, ns):
     import numpy as np
     import torch
@@ -470,6 +539,9 @@ def run(fam, ns):
         p = n - 1
         man = json.load(open(os.path.join(PROBE, "%s_n%d.json" % (fam, n))))
         plib = ctypes.CDLL(os.path.join(PROBE, "%s_n%d.so" % (fam, n)))
+        if fam == "c2g":
+            run_c2g(n, man, plib, lib, runtime, workloads, torch, dev, stream, time_launch)
+            continue
         if fam == "c3":
             plan = compile_form(action_form(REGISTRY["weighted_laplace"]), "hex", p,
                                 "spectral", "spectral_gll", "collocated-gll")
