@@ -28,6 +28,9 @@ namespace sfk {
 #ifndef SFK_C4_ONLY_N
 #define SFK_C4_ONLY_N 0
 #endif
+#ifndef SFK_C4P_PQ
+#define SFK_C4P_PQ 1
+#endif
 #ifndef SFK_C4_PROBE_ENTRY
 #define SFK_C4_PROBE_ENTRY sfk_c4_probe_eval
 #endif
@@ -197,7 +200,10 @@ hex_neohookean3_kernel(const __grid_constant__ Tabs<N, M> T, double mu, double l
       HexLineAdj geo;
       geo.setup(sC + zc * 24, T.Bc[qx], T.Bc[M + qx], T.Bc[qy], T.Bc[M + qy]);
       const double wxy = T.W[qx] * T.W[qy];
-#pragma unroll 1
+      // (SFK_C4P_PQ > 1, probe builds: that many of the thread's points in flight —
+      // measured slower, 128+ registers: profiles/r02ds_c4_pq.jsonl)
+      constexpr int PQ = SFK_C4P_PQ;
+#pragma unroll (PQ)
       for (int q = zg; q < M; q += 3) {
         double gq[9];
 #pragma unroll

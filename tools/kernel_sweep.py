@@ -173,6 +173,8 @@ def neo_px(n):
 
 
 def c4_variants(n):
+    if os.environ.get("SWEEP_LEVEL") == "pq":
+        return c4_variants_pq(n)
     m = n + 1
     out = []
     pxs = sorted({neo_px(n), (n * n) | 1})
@@ -197,11 +199,28 @@ def c4_variants(n):
     return out
 
 
+def c4_variants_pq(n):
+    """Product shapes x pointwise-loop unroll factor x min-blocks (one-shot)."""
+    base = {5: (1, 37, 7, 1), 6: (1, 38, 7, 1), 7: (1, 55, 9, 0)}[n]
+    cpb, px, lz, nyt = base
+    m = n + 1
+    threads = -(-3 * cpb * m * m // 32) * 32
+    out = []
+    for pq in (1, 2, 3):
+        for minb in (0, 2, 3, 4, 5, 6):
+            if minb and 65536 // (minb * threads) < 80:
+                continue
+            out.append(dict(n=n, cpb=cpb, px=px, lz=lz, ypad=0, nyt=nyt, minb=minb, oneshot=1,
+                            pq=pq, threads=threads, smem=0))
+    return out
+
+
 def c4_defines(v, entry):
     return ["-DSFK_C4_ONLY_N=%d" % v["n"], "-DSFK_C4P_CPB=%d" % v["cpb"],
             "-DSFK_C4P_PX=%d" % v["px"], "-DSFK_C4P_LZ=%d" % v["lz"],
             "-DSFK_C4P_YPAD=%d" % v["ypad"], "-DSFK_C4P_NYT=%d" % v["nyt"],
             "-DSFK_C4P_MINB=%d" % v["minb"], "-DSFK_C4P_ONESHOT=%d" % v["oneshot"],
+            "-DSFK_C4P_PQ=%d" % v.get("pq", 1),
             "-DSFK_C4_PROBE_ENTRY=%s" % entry]
 
 
@@ -401,7 +420,7 @@ FAMILIES = {
     "c2g": dict(src="hex_action6.cu", variants=c2g_variants, defines=c2g_defines,
                 keys=("cpb", "ws", "zr", "eo", "minb", "os")),
     "c4": dict(src="hex_neohookean3.cu", variants=c4_variants, defines=c4_defines,
-               keys=("cpb", "px", "lz", "ypad", "nyt", "minb", "oneshot")),
+               keys=("cpb", "px", "lz", "ypad", "nyt", "minb", "oneshot", "pq")),
 }
 
 
