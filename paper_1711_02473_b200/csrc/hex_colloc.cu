@@ -694,11 +694,24 @@ static int dispatch_colloc(const sfk_plan* p, int64_t ncells, double* A, const d
 }  // namespace sfk
 // the probe object's only entry point: p is a plan made by the product
 // library (a plain host struct), all buffers device pointers as in sfk_eval
+#ifndef SFK_C3P_GS
+#define SFK_C3P_GS 0
+#endif
+#if SFK_C3P_GS
+// global-operator form: w0 = x (global vector), A = y (accumulated), cmap =
+// the cell -> global dof map
+extern "C" int SFK_C3_PROBE_ENTRY(const sfk_plan* p, int64_t ncells, double* A,
+                                 const double* coords, const double* w0, const double* w1,
+                                 const int* cmap, void* stream) {
+  return sfk::dispatch_colloc<true>(p, ncells, A, coords, w0, w1, (cudaStream_t)stream, cmap);
+}
+#else
 extern "C" int SFK_C3_PROBE_ENTRY(const sfk_plan* p, int64_t ncells, double* A,
                                  const double* coords, const double* w0, const double* w1,
                                  void* stream) {
   return sfk::dispatch_colloc<false>(p, ncells, A, coords, w0, w1, (cudaStream_t)stream, nullptr);
 }
+#endif
 namespace sfk {
 #else
 int launch_hex_colloc_action(const sfk_plan* p, int64_t ncells, double* A, const double* coords,

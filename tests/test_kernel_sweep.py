@@ -20,7 +20,7 @@ def _load():
 
 
 KS = _load()
-REPRESENTATIVE = {"c3": 9, "c2": 5, "cell": 3, "c4": 6, "c4l": 4, "c5": 3, "c5h": 6, "p1": 2, "c2g": 5}
+REPRESENTATIVE = {"c3": 9, "c2": 5, "cell": 3, "c4": 6, "c4l": 4, "c5": 3, "c5h": 6, "p1": 2, "c2g": 5, "c3g": 9}
 
 
 @pytest.mark.parametrize("fam", sorted(REPRESENTATIVE))

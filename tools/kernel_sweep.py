@@ -402,6 +402,39 @@ def c2g_defines(v, entry):
     return c2_defines(v, entry) + ["-DSFK_V6P_GS=1"]
 
 
+# product policy per n (hex_colloc.cu c3_policy): (kg, splitz, minb, fuse)
+C3_POLICY = {5: (0, 0, 0, 0), 6: (0, 0, 4, 0), 7: (1, 0, 0, 3), 8: (1, 0, 8, 3), 9: (0, 0, 0, 1),
+             10: (0, 0, 4, 1), 11: (0, 1, 3, 3), 12: (1, 1, 3, 3), 13: (0, 1, 2, 1),
+             14: (1, 1, 3, 1), 15: (1, 0, 2, 3), 16: (1, 1, 1, 3), 17: (0, 0, 0, 3)}
+
+
+def c3g_variants(n):
+    """Global-operator form of the C3 kernel: cells per CTA x kg x splitz x min-blocks x fuse
+    on the product layout."""
+    cpb0, sy, sx, cs = TABLE[n]
+    out = []
+    for cpb, kg, splitz, fuse in itertools.product(sorted({1, max(1, cpb0 - 1), cpb0, cpb0 + 1,
+                                                           2 * cpb0}), (0, 1), (0, 1), (0, 3)):
+        threads = -(-cpb * n * n // 32) * 32
+        if threads > 1024:
+            continue
+        sm = smem_bytes(n, cpb, cs, 0, kg)
+        if sm > SMEM_MAX:
+            continue
+        by_smem = min(16, (228 * 1024) // (sm + 1024))
+        for minb in (0, 2, 3, 4, 6, 8):
+            if minb > by_smem or (minb and 65536 // (minb * threads) < 72):
+                continue
+            out.append(dict(n=n, cpb=cpb, sy=sy, sx=sx, cs=cs, persist=0, kg=kg, splitz=splitz,
+                            minb=minb, geom=int(n in (15, 16)), fuse=fuse, threads=threads,
+                            smem=sm))
+    return out
+
+
+def c3g_defines(v, entry):
+    return c3_defines(v, entry) + ["-DSFK_C3P_GS=1"]
+
+
 FAMILIES = {
     "c3": dict(src="hex_colloc.cu", variants=c3_variants, defines=c3_defines,
                keys=("cpb", "sy", "sx", "cs", "persist", "kg", "splitz", "minb", "geom", "fuse", "uq")),
@@ -419,6 +452,8 @@ FAMILIES = {
                keys=("cpb", "minb", "persist")),
     "c2g": dict(src="hex_action6.cu", variants=c2g_variants, defines=c2g_defines,
                 keys=("cpb", "ws", "zr", "eo", "minb", "os")),
+    "c3g": dict(src="hex_colloc.cu", variants=c3g_variants, defines=c3g_defines,
+                keys=("cpb", "kg", "splitz", "minb", "fuse")),
     "c4": dict(src="hex_neohookean3.cu", variants=c4_variants, defines=c4_defines,
                keys=("cpb", "px", "lz", "ypad", "nyt", "minb", "oneshot", "pq")),
 }
@@ -474,20 +509,28 @@ def build(fam, ns):
                  os.path.getsize(out) / 1e6), flush=True)
 
 
-def run_c2g(n, man, plib, lib, runtime, workloads, torch, dev, stream, time_launch):
-    """Global operator variants on the (64, 64, 64) lattice's continuous Q_p space."""
-    from paper_1711_02473_b200 import compile_kernel
+def run_c2g(fam, n, man, plib, lib, runtime, workloads, torch, dev, stream, time_launch):
+    """Global operator variants on the config's lattice and its continuous Q_p space
+    (c2g: (64, 64, 64), Laplace action; c3g: (16, 64, 64), collocated weighted Laplace)."""
+    from paper_1711_02473_b200 import REGISTRY, action_form, compile_form, compile_kernel
     from paper_1711_02473_b200.assembly import GlobalOperator, lattice_dof_map, lattice_ndofs
 
     p = n - 1
-    dims = (64, 64, 64)
-    plan = compile_kernel("action_laplace", "hex", p)
+    if fam == "c2g":
+        dims = (64, 64, 64)
+        plan = compile_kernel("action_laplace", "hex", p)
+        w1 = None
+    else:
+        dims = (16, 64, 64)
+        plan = compile_form(action_form(REGISTRY["weighted_laplace"]), "hex", p,
+                            "spectral", "spectral_gll", "collocated-gll")
+        w1 = torch.from_numpy(workloads.c3_inputs(p, dims)["w1"]).to(dev)
     coords = torch.from_numpy(workloads.lattice_coords(*dims)).to(dev)
     gmap = torch.from_numpy(lattice_dof_map(*dims, p)).to(dev)
     nd = lattice_ndofs(*dims, p)
     C = coords.shape[0]
     x = torch.rand(nd, dtype=torch.float64, device=dev)
-    op = GlobalOperator(plan, gmap, coords, nd)
+    op = GlobalOperator(plan, gmap, coords, nd, w1=w1)
     ref = op.apply(x)
     y = torch.zeros_like(x)
     t0 = time_launch(lambda: op.apply(x, out=y, accumulate=True))
@@ -498,13 +541,18 @@ def run_c2g(n, man, plib, lib, runtime, workloads, torch, dev, stream, time_laun
     for v in man:
         fn = getattr(plib, v["entry"])
         fn.restype = ctypes.c_int
-        fn.argtypes = [vp, i64, vp, vp, vp, vp, vp]
         y.zero_()
-        call = lambda: fn(h, C, y.data_ptr(), coords.data_ptr(), x.data_ptr(), gmap.data_ptr(),
-                          stream.cuda_stream)
+        if fam == "c2g":
+            fn.argtypes = [vp, i64, vp, vp, vp, vp, vp]
+            call = lambda: fn(h, C, y.data_ptr(), coords.data_ptr(), x.data_ptr(),
+                              gmap.data_ptr(), stream.cuda_stream)
+        else:
+            fn.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp]
+            call = lambda: fn(h, C, y.data_ptr(), coords.data_ptr(), x.data_ptr(), w1.data_ptr(),
+                              gmap.data_ptr(), stream.cuda_stream)
         rc = call()
         torch.cuda.synchronize()
-        rec = {k: v.get(k, 0) for k in ("n",) + FAMILIES["c2g"]["keys"] + ("threads", "regs", "spill")}
+        rec = {k: v.get(k, 0) for k in ("n",) + FAMILIES[fam]["keys"] + ("threads", "regs", "spill")}
         if rc != 0:
             rec["rc"] = rc
             print(json.dumps(rec), flush=True)
@@ -558,8 +606,8 @@ def run(fam, ns):
         p = n - 1
         man = json.load(open(os.path.join(PROBE, "%s_n%d.json" % (fam, n))))
         plib = ctypes.CDLL(os.path.join(PROBE, "%s_n%d.so" % (fam, n)))
-        if fam == "c2g":
-            run_c2g(n, man, plib, lib, runtime, workloads, torch, dev, stream, time_launch)
+        if fam in ("c2g", "c3g"):
+            run_c2g(fam, n, man, plib, lib, runtime, workloads, torch, dev, stream, time_launch)
             continue
         if fam == "c3":
             plan = compile_form(action_form(REGISTRY["weighted_laplace"]), "hex", p,
