@@ -75,7 +75,18 @@ struct C3Policy {
   bool kg, splitz;
   int minb, fuse;
 };
-__host__ __device__ constexpr C3Policy c3_policy(int n) {
+__host__ __device__ constexpr C3Policy c3_policy(int n, bool gs = false) {
+  // the global-operator form (gather through the dof map, atomic scatter) has
+  // its own optimum at four n (tools/kernel_sweep.py c3g,
+  // profiles/r02du_c3g_sweep.jsonl: 6-13% over the E-vector form's policy)
+  if (gs) {
+    switch (n) {
+      case 7: case 8: return {false, false, 8, 3};
+      case 12: return {true, true, 4, 0};
+      case 14: return {false, true, 2, 3};
+      default: break;
+    }
+  }
   switch (n) {
     // n = 5, 6, 8: small CTAs from the wide cells-per-CTA sweep (r02dm_c3_cpb.jsonl)
     case 5: return {false, false, 0, 0};
@@ -119,9 +130,11 @@ __host__ __device__ constexpr bool colloc_persist(int n) { return c3p(n, SFK_C3P
 // arrays, i.e. more CTAs per SM where shared memory is the limit (round 1:
 // n = 16, 139 -> 104 KB per CTA and two CTAs per SM; round 2: see c3_policy).
 #ifdef SFK_COLLOC_KG
-__host__ __device__ constexpr bool colloc_kg(int n) { return n >= SFK_COLLOC_KG; }
+__host__ __device__ constexpr bool colloc_kg(int n, bool = false) { return n >= SFK_COLLOC_KG; }
 #else
-__host__ __device__ constexpr bool colloc_kg(int n) { return c3p(n, SFK_C3P_KG, c3_policy(n).kg); }
+__host__ __device__ constexpr bool colloc_kg(int n, bool gs = false) {
+  return c3p(n, SFK_C3P_KG, c3_policy(n, gs).kg);
+}
 #endif
 
 template <int N, int CPB, int SY, int SX, int CS>
@@ -130,10 +143,10 @@ struct CollocCfg {
   static constexpr int N3 = N * N * N;
   static constexpr int THREADS = round_up(CPB * NN, 32);
   static constexpr bool persist(int warps) { return warps == 0 && colloc_persist(N); }
-  static constexpr size_t smem(bool weighted, int warps = 0) {
+  static constexpr size_t smem(bool weighted, int warps = 0, bool gs = false) {
     return persist(warps)
-               ? (size_t)((weighted && !colloc_kg(N) ? 6 : 4) * CPB * CS + 2 * CPB * 24) * sizeof(double)
-               : (size_t)((weighted && !colloc_kg(N) ? 4 : 3) * CPB * CS + CPB * 24) * sizeof(double);
+               ? (size_t)((weighted && !colloc_kg(N, gs) ? 6 : 4) * CPB * CS + 2 * CPB * 24) * sizeof(double)
+               : (size_t)((weighted && !colloc_kg(N, gs) ? 4 : 3) * CPB * CS + CPB * 24) * sizeof(double);
   }
 };
 
@@ -145,11 +158,11 @@ struct CollocCfg {
 // p = 13 3.803 -> 3.085, profiles/r01cf_*.jsonl; round 2 adds n = 11 and 16
 // and drops 15, see c3_policy).
 // SFK_COLLOC_SPLITZ=n0 (A/B builds) splits every n >= n0.
-__host__ __device__ constexpr bool colloc_splitz(int n) {
+__host__ __device__ constexpr bool colloc_splitz(int n, bool gs = false) {
 #ifdef SFK_COLLOC_SPLITZ
   return n >= SFK_COLLOC_SPLITZ;
 #else
-  return c3p(n, SFK_C3P_SPLITZ, c3_policy(n).splitz);
+  return c3p(n, SFK_C3P_SPLITZ, c3_policy(n, gs).splitz);
 #endif
 }
 
@@ -161,7 +174,9 @@ __host__ __device__ constexpr bool colloc_splitz(int n) {
 #ifndef SFK_C3P_FUSE
 #define SFK_C3P_FUSE -1
 #endif
-__host__ __device__ constexpr int colloc_fuse(int n) { return c3p(n, SFK_C3P_FUSE, c3_policy(n).fuse); }
+__host__ __device__ constexpr int colloc_fuse(int n, bool gs = false) {
+  return c3p(n, SFK_C3P_FUSE, c3_policy(n, gs).fuse);
+}
 
 // UQ: unroll factor of the split z phase's pointwise loop (1 = rolled; 2+:
 // that many points' dependency chains in flight per thread, more registers)
@@ -171,12 +186,12 @@ __host__ __device__ constexpr int colloc_fuse(int n) { return c3p(n, SFK_C3P_FUS
 // (sweep: n = 16 4.046 -> 3.799 ms at 2; neutral or slower elsewhere, profiles/r02db_c3_uq.jsonl)
 __host__ __device__ constexpr int colloc_uq(int n) { return c3p(n, SFK_C3P_UQ, n == 16 ? 2 : 1); }
 
-__host__ __device__ constexpr int colloc_minb(int n) {
+__host__ __device__ constexpr int colloc_minb(int n, bool gs = false) {
 #ifdef SFK_COLLOC_MINB
   if (SFK_COLLOC_MINB >= 0) return SFK_COLLOC_MINB;   // A/B builds (tools/build_variant.py)
 #endif
   if (SFK_C3_ONLY_N != 0 && n == SFK_C3_ONLY_N && SFK_C3P_MINB >= 0) return SFK_C3P_MINB;
-  return c3_policy(n).minb;
+  return c3_policy(n, gs).minb;
 }
 
 // GS = true: global operator y += sum_c P_c^T A_c P_c x (SURVEY.md §8(f)
@@ -218,9 +233,9 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
   constexpr int GYX = c3_gy(N, SX, SY, CS).sx, GYY = c3_gy(N, SX, SY, CS).sy,
                 GYC = c3_gy(N, SX, SY, CS).cs;
   static_assert(GXC <= CS && GYC <= CS, "GX / GY must fit the CS-strided buffers");
-  constexpr bool SPLITZ = colloc_splitz(N);
+  constexpr bool SPLITZ = colloc_splitz(N, GS);
   constexpr bool PERSIST = C::persist(WARPS);
-  constexpr bool KG = WEIGHTED && colloc_kg(N);
+  constexpr bool KG = WEIGHTED && colloc_kg(N, GS);
   constexpr bool CONTIG = SY == N && SX == NN && CS == N3 && C3_CONTIG;
   extern __shared__ double smem[];
   constexpr int TH = WARPS ? 32 : C::THREADS;
@@ -229,7 +244,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
   // one-shot:   [U][GX][GY][coords][K]
   // persistent: [U0][U1][GX][GY][coords0][coords1][K0][K1] (u, coords, kappa
   //             of the next batch stream in while the current one computes)
-  double* base = smem + (size_t)grp * (C::smem(WEIGHTED, WARPS) / sizeof(double));
+  double* base = smem + (size_t)grp * (C::smem(WEIGHTED, WARPS, GS) / sizeof(double));
   double* sGX = base + (PERSIST ? 2 : 1) * CPB * CS;
   double* sGY = sGX + CPB * CS;
   double* sC0 = sGY + CPB * CS;
@@ -290,7 +305,7 @@ __device__ __forceinline__ void colloc_body(const TabsD<N>& T, int64_t ncells,
     const int cb = c * CS;
 
     // ---- phase 2: x-line (y=a, z=b) and y-line (x=a, z=b) ---------------
-    constexpr int FUSE = colloc_fuse(N);
+    constexpr int FUSE = colloc_fuse(N, GS);
     if ((FUSE & 1) && act) {
       double ux[N], uy[N];
   #pragma unroll
@@ -564,7 +579,7 @@ hex_colloc_action_kernel_free(const __grid_constant__ TabsD<N> T, int64_t ncells
 
 template <int N, int CPB, int SY, int SX, int CS, bool WEIGHTED, bool GS, int WARPS, int VAR>
 static auto colloc_kernel() {
-  constexpr int mb = colloc_minb(N);
+  constexpr int mb = colloc_minb(N, GS);
   if constexpr (mb == 0)
     return hex_colloc_action_kernel_free<N, CPB, SY, SX, CS, WEIGHTED, GS, WARPS, VAR>;
   else return hex_colloc_action_kernel<N, CPB, SY, SX, CS, WEIGHTED, mb, GS, WARPS, VAR>;
@@ -590,7 +605,7 @@ static int launch_nv(const sfk_plan* p, int64_t ncells, double* A, const double*
   LaunchShape sh;
   if (kappa) {
     auto k = colloc_kernel<N, CPB, SY, SX, CS, true, GS, WARPS, VAR>();
-    const size_t sm = G * C::smem(true, WARPS);
+    const size_t sm = G * C::smem(true, WARPS, GS);
     if (const int rc_ = kernel_shape((const void*)k, THREADS, sm, "hex_colloc", &sh)) return rc_;
     if (C::persist(WARPS)) grid = std::min<int64_t>(grid, sh.resident());
     if (grid > 0) k<<<(unsigned)grid, THREADS, sm, s>>>(T, ncells, coords, u, kappa, A, cmap);
@@ -599,7 +614,7 @@ static int launch_nv(const sfk_plan* p, int64_t ncells, double* A, const double*
     return fail(SFK_EUNSUPPORTED, "probe build: weighted form only");
 #else
     auto k = colloc_kernel<N, CPB, SY, SX, CS, false, GS, WARPS, VAR>();
-    const size_t sm = G * C::smem(false, WARPS);
+    const size_t sm = G * C::smem(false, WARPS, GS);
     if (const int rc_ = kernel_shape((const void*)k, THREADS, sm, "hex_colloc", &sh)) return rc_;
     if (C::persist(WARPS)) grid = std::min<int64_t>(grid, sh.resident());
     if (grid > 0) k<<<(unsigned)grid, THREADS, sm, s>>>(T, ncells, coords, u, nullptr, A, cmap);
@@ -672,7 +687,7 @@ static int dispatch_colloc(const sfk_plan* p, int64_t ncells, double* A, const d
     case 4: return launch_n<4, 8, 4, 19, 76, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 5: return launch_n<5, 5, 5, 25, 125, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 6: return launch_n<6, 3, 6, 36, 216, GS>(p, ncells, A, coords, w0, w1, s, cmap);
-    case 7: return launch_n<7, 5, 7, 52, 369, GS>(p, ncells, A, coords, w0, w1, s, cmap);
+    case 7: return launch_n<7, GS ? 1 : 5, 7, 52, 369, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 8: return launch_n<8, 1, 9, 72, 576, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 9: return launch_n<9, 3, 9, 81, 729, GS>(p, ncells, A, coords, w0, w1, s, cmap);
     case 10: return launch_n<10, SFK_COLLOC_CPB10, 10, 100, 1000, GS>(p, ncells, A, coords, w0, w1, s, cmap);
